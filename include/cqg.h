@@ -1,0 +1,167 @@
+/*
+ * cqg.h -- C-ABI of the B200-native colour-quantiser hot path (libcqg.so).
+ *
+ * The reference (arXiv 1101.0395 artifact, /root/reference/proj) exposes its
+ * hot path only as the C++ library API in proj/include/quant/*.hpp (no FFI,
+ * plugin or operator registry: SURVEY.md §8(b)). Each entry point below
+ * replaces one of those functions for the count-weighted ("unique" sampling)
+ * path and keeps its argument meaning and error behaviour:
+ *
+ *   cqg_histogram      quant::build_histogram   include/quant/histogram.hpp:57
+ *                                               (src/histogram.cpp:69-104)
+ *   cqg_init_maximin   quant::init_maximin      include/quant/init.hpp:40
+ *                                               (src/init.cpp:37-52,127-138)
+ *   cqg_init_kmeanspp  quant::init_kmeanspp     include/quant/init.hpp:60
+ *                                               (src/init.cpp:295-314)
+ *   cqg_lloyd          quant::wsm               include/quant/kmeans.hpp:128-129
+ *                                               (src/kmeans.cpp:173-277)
+ *   cqg_map            quant::map_pixels        include/quant/metrics.hpp:28
+ *                                               (src/metrics.cpp:15-55)
+ *   cqg_quantize       quant::run_quantize      include/quant/pipeline.hpp:53
+ *                                               (src/pipeline.cpp:81-164), for
+ *                                               methods wsm-mmx / wsm-kpp and
+ *                                               caller-supplied initial centres
+ *
+ * Plain pointers and sizes only. Every pointer argument may be host memory
+ * (pageable or pinned) or device memory of the context's device; the library
+ * detects which (cudaPointerGetAttributes) and copies only what is needed.
+ * All work is ordered on the context's stream; every call returns after its
+ * results are visible at the output pointers.
+ *
+ * Errors: every function returns CQG_OK (0) or a CQG_E_* code; the message is
+ * available from cqg_last_error() (thread-local). CQG_E_INVALID corresponds to
+ * the reference's std::invalid_argument sites and carries the same message text
+ * (e.g. "clustering: k (9) exceeds number of points (4)", kmeans.cpp:178-181);
+ * CQG_E_RUNTIME corresponds to std::runtime_error (kmeans.cpp:159).
+ *
+ * Colours are packed 0x00RRGGBB in uint32; images are interleaved 8-bit RGB,
+ * row-major, 3 bytes per pixel (quant::RawImage, image.hpp:13-24).
+ * Centres / palettes are K x 3 doubles (r, g, b) as quant::ColorPoint.
+ */
+#ifndef CQG_H
+#define CQG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CQG_OK 0
+#define CQG_E_INVALID 1 /* std::invalid_argument in the reference */
+#define CQG_E_RUNTIME 2 /* std::runtime_error in the reference */
+#define CQG_E_CUDA 3    /* CUDA failure (no device, launch error, ...) */
+#define CQG_E_NOMEM 4   /* device or pinned allocation failed */
+
+#define CQG_INIT_MAXIMIN 0  /* "mmx" (init.cpp:127) */
+#define CQG_INIT_KMEANSPP 1 /* "kpp" (init.cpp:295) */
+#define CQG_INIT_GIVEN 2    /* caller supplies K initial centres */
+
+typedef struct cqg_ctx cqg_ctx;
+
+/* quant::Termination (kmeans.hpp:17-21) + ClusterOptions::record_history (:28-35).
+ * fixed_iterations <= 0 means "not set" (std::optional empty). */
+typedef struct {
+    double epsilon;
+    int max_iterations;
+    int fixed_iterations;
+    int record_history;
+} cqg_term;
+
+/* Scalar fields of quant::ClusterState (kmeans.hpp:42-56). */
+typedef struct {
+    int iterations;
+    int repair_count;
+    uint64_t ndc_total;
+    uint64_t n_points;
+    uint64_t flagged_total; /* points replayed in exact FP64 (diagnostic) */
+} cqg_lloyd_stats;
+
+typedef struct {
+    int init_kind; /* CQG_INIT_* */
+    int k;
+    uint64_t seed;
+    cqg_term term;
+    int index_bytes; /* 4: uint32 per pixel (MappingResult::indices layout); 1: uint8 (K <= 256) */
+} cqg_quantize_cfg;
+
+typedef struct {
+    uint64_t n_unique;   /* substrate_points (pipeline.cpp:117) */
+    cqg_lloyd_stats lloyd;
+    double mean_sq_dist; /* QuantReport::mse (pipeline.cpp:155) */
+    double ms_histogram, ms_init, ms_lloyd, ms_map; /* device time per stage (CUDA events) */
+} cqg_quantize_stats;
+
+/* ---- context ------------------------------------------------------------ */
+cqg_ctx *cqg_create(int device);
+void cqg_destroy(cqg_ctx *ctx);
+const char *cqg_last_error(void);
+/* Use an existing cudaStream_t (NULL = the context's own stream). */
+int cqg_set_stream(cqg_ctx *ctx, void *cuda_stream);
+/* Number of library kernels launched by this context so far (bench evidence). */
+uint64_t cqg_launch_count(const cqg_ctx *ctx);
+const char *cqg_version(void);
+
+/* ---- kernel-level profiling (bench evidence) -------------------------------
+ * When enabled, the library brackets its hot kernels with CUDA events on the
+ * launching stream and accumulates per category: device milliseconds, launch
+ * count and algorithmic work units (distances for the sweeps, bytes for the
+ * byte-bound kernels). */
+#define CQG_PROF_SWEEP 0     /* Lloyd sweep (units: unique colours x K) */
+#define CQG_PROF_MAPSWEEP 1  /* mapping sweep per distinct colour (units: N' x K) */
+#define CQG_PROF_HIST 2      /* histogram stage (units: 3P + 8N' bytes) */
+#define CQG_PROF_PIXEL 3     /* pixel mapping kernel (units: bytes moved) */
+#define CQG_PROF_INIT 4      /* initialiser kernel (units: N' x (K-1) distance updates) */
+#define CQG_PROF_REPLAY 5    /* exact FP64 replays (units: queued points) */
+#define CQG_PROF_N 8
+typedef struct {
+    double ms[CQG_PROF_N];
+    double units[CQG_PROF_N];
+    uint64_t launches[CQG_PROF_N];
+} cqg_profile;
+int cqg_set_profiling(cqg_ctx *ctx, int on);
+int cqg_read_profile(cqg_ctx *ctx, cqg_profile *out, int reset);
+
+/* ---- stage 1: unique colours in first-occurrence order -------------------
+ * rgb: P*3 bytes. colors/counts/first: capacity min(P, 2^24) each; `first`
+ * (pixel index of first sight) may be NULL. *n_unique receives N'. Weights are
+ * counts[i] * (1.0 / P) exactly as histogram.cpp:99-102. */
+int cqg_histogram(cqg_ctx *ctx, const uint8_t *rgb, uint64_t P, uint32_t *colors,
+                  uint32_t *counts, uint32_t *first, uint64_t *n_unique);
+
+/* ---- initialisers (bit-exact with init.cpp for the same histogram) ------- */
+int cqg_init_maximin(cqg_ctx *ctx, const uint32_t *colors, const uint32_t *counts, uint64_t n,
+                     uint64_t P, int k, uint64_t seed, int weighted_first, double *centers);
+int cqg_init_kmeanspp(cqg_ctx *ctx, const uint32_t *colors, const uint32_t *counts, uint64_t n,
+                      uint64_t P, int k, uint64_t seed, double *centers);
+
+/* ---- stages 2+3: weighted sort-means over the count-weighted histogram ----
+ * Weights are counts[i]/P (P = source pixel count). init: k x 3. Outputs:
+ * centers (k x 3), labels (n, post-repair memberships), sse_trace (capacity
+ * fixed_iterations or max_iterations), stats. hist_labels (iters x n) and
+ * hist_centers (iters x k x 3) are filled when term->record_history != 0 and
+ * the pointers are non-NULL (ClusterState::history, pre-repair snapshots). */
+int cqg_lloyd(cqg_ctx *ctx, const uint32_t *colors, const uint32_t *counts, uint64_t n,
+              uint64_t P, const double *init, int k, const cqg_term *term, double *centers,
+              uint32_t *labels, double *sse_trace, cqg_lloyd_stats *stats,
+              uint32_t *hist_labels, double *hist_centers);
+
+/* ---- stage 4: exact lowest-index nearest palette entry per pixel + MSE ----
+ * indices: P entries of index_bytes (4 = uint32 as MappingResult::indices,
+ * 1 = uint8, requires k <= 256); may be NULL. quantized: P*3 bytes (palette
+ * rendered with channel_to_u8, color.hpp:63-72); may be NULL. */
+int cqg_map(cqg_ctx *ctx, const uint8_t *rgb, uint64_t P, const double *palette, int k,
+            void *indices, int index_bytes, uint8_t *quantized, double *mean_sq_dist);
+
+/* ---- whole hot path: histogram -> init -> wsm -> map --------------------
+ * init: required for CQG_INIT_GIVEN (k x 3), ignored otherwise. palette: k x 3.
+ * labels (capacity min(P,2^24)), sse_trace, indices, quantized may be NULL. */
+int cqg_quantize(cqg_ctx *ctx, const uint8_t *rgb, uint64_t P, const cqg_quantize_cfg *cfg,
+                 const double *init, double *palette, uint32_t *labels, double *sse_trace,
+                 void *indices, uint8_t *quantized, cqg_quantize_stats *stats);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CQG_H */

@@ -1,0 +1,456 @@
+// api.cu -- the extern "C" boundary of libcqg.so (declared in include/cqg.h).
+//
+// Validation mirrors the reference's exception sites and messages so the C++
+// wrapper (quant:: API) can rethrow the same exception type and text:
+//   histogram.cpp:70, init.cpp:15-19, kmeans.cpp:175-188 and :275,
+//   metrics.cpp:16-17, pipeline.cpp:82-83.
+#include <chrono>
+#include <cstring>
+#include <string>
+
+#include "cqg_internal.cuh"
+
+namespace {
+thread_local std::string g_last_error;
+
+template <class F>
+int guarded(F &&f) {
+    try {
+        f();
+        return CQG_OK;
+    } catch (const cqg::Error &e) {
+        g_last_error = e.msg;
+        return e.code;
+    } catch (const std::exception &e) {
+        g_last_error = e.what();
+        return CQG_E_RUNTIME;
+    }
+}
+
+void use_device(cqg_ctx *ctx) {
+    if (!ctx) cqg::fail(CQG_E_INVALID, "null cqg context");
+    CQG_CUDA(cudaSetDevice(ctx->device));
+}
+
+void validate_k_init(int k, uint64_t n) {
+    if (k < 1) cqg::fail(CQG_E_INVALID, "initialization: k must be at least 1");
+    if ((uint64_t)k > n)
+        cqg::fail(CQG_E_INVALID, "initialization: k (" + std::to_string(k) + ") exceeds distinct colors (" +
+                                     std::to_string(n) + ")");
+}
+
+void validate_run(uint64_t n, int k, const cqg_term &t) {
+    if (k <= 0) cqg::fail(CQG_E_INVALID, "clustering: no initial centers");
+    if (n == 0) cqg::fail(CQG_E_INVALID, "clustering: no points");
+    if ((uint64_t)k > n)
+        cqg::fail(CQG_E_INVALID, "clustering: k (" + std::to_string(k) + ") exceeds number of points (" +
+                                     std::to_string(n) + ")");
+    if (t.epsilon < 0.0) cqg::fail(CQG_E_INVALID, "clustering: negative epsilon");
+    if (t.max_iterations <= 0) cqg::fail(CQG_E_INVALID, "clustering: max_iterations < 1");
+    if (k > 4096) cqg::fail(CQG_E_INVALID, "clustering: k > 4096 is not supported by the device engine");
+}
+
+void validate_pixels(uint64_t P, const char *who) {
+    if (P >= (1ull << 32)) cqg::fail(CQG_E_INVALID, std::string(who) + ": more than 2^32-1 pixels");
+}
+
+struct Timer {
+    cqg_ctx *ctx;
+    bool on;
+    cudaEvent_t a, b;
+    Timer(cqg_ctx *c, bool enable) : ctx(c), on(enable) {
+        if (on) {
+            cudaEventCreate(&a);
+            cudaEventCreate(&b);
+            cudaEventRecord(a, ctx->stream);
+        }
+    }
+    double lap() {
+        if (!on) return 0.0;
+        cudaEventRecord(b, ctx->stream);
+        cudaEventSynchronize(b);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, a, b);
+        std::swap(a, b);
+        return ms;
+    }
+    ~Timer() {
+        if (on) {
+            cudaEventDestroy(a);
+            cudaEventDestroy(b);
+        }
+    }
+};
+
+} // namespace
+
+namespace cqg {
+
+bool is_device_ptr(const void *p) {
+    if (!p) return false;
+    cudaPointerAttributes attr{};
+    if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
+}
+
+void launched(cqg_ctx *ctx, int n) { ctx->launches += (unsigned long long)n; }
+
+static int take_event(cqg_ctx *ctx) {
+    if (ctx->ev_used == ctx->ev_pool.size()) {
+        cudaEvent_t e;
+        CQG_CUDA(cudaEventCreate(&e));
+        ctx->ev_pool.push_back(e);
+    }
+    return (int)ctx->ev_used++;
+}
+
+int prof_begin(cqg_ctx *ctx) {
+    if (!ctx->prof_on) return -1;
+    const int e = take_event(ctx);
+    CQG_CUDA(cudaEventRecord(ctx->ev_pool[e], ctx->stream));
+    return e;
+}
+
+void prof_end(cqg_ctx *ctx, int cat, int begin, double units) {
+    if (!ctx->prof_on || begin < 0) return;
+    const int e = take_event(ctx);
+    CQG_CUDA(cudaEventRecord(ctx->ev_pool[e], ctx->stream));
+    ctx->prof_recs.push_back({cat, begin, e, units});
+}
+
+static void prof_drain(cqg_ctx *ctx) {
+    if (ctx->prof_recs.empty()) {
+        ctx->ev_used = 0;
+        return;
+    }
+    CQG_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (const auto &r : ctx->prof_recs) {
+        float ms = 0.f;
+        CQG_CUDA(cudaEventElapsedTime(&ms, ctx->ev_pool[r.e0], ctx->ev_pool[r.e1]));
+        ctx->prof_ms[r.cat] += ms;
+        ctx->prof_units[r.cat] += r.units;
+        ctx->prof_launches[r.cat] += 1;
+    }
+    ctx->prof_recs.clear();
+    ctx->ev_used = 0;
+}
+
+const void *stage_in(cqg_ctx *ctx, const void *user, size_t bytes, DevBuf &buf) {
+    if (is_device_ptr(user)) return user;
+    void *d = buf.ensure(bytes);
+    CQG_CUDA(cudaMemcpyAsync(d, user, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    return d;
+}
+
+void copy_out(cqg_ctx *ctx, void *user, const void *dev, size_t bytes) {
+    if (!user || bytes == 0 || user == dev) return;
+    CQG_CUDA(cudaMemcpyAsync(user, dev, bytes, cudaMemcpyDefault, ctx->stream));
+}
+
+uint64_t read_scalar_u32(cqg_ctx *ctx, const uint32_t *dev) {
+    uint32_t *h = static_cast<uint32_t *>(ctx->pinned.ensure(4096));
+    CQG_CUDA(cudaMemcpyAsync(h, dev, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    CQG_CUDA(cudaStreamSynchronize(ctx->stream));
+    return *h;
+}
+
+// pick the caller's buffer when it is device memory, else a context buffer
+template <class T>
+T *out_buf(void *user, DevBuf &buf, size_t count) {
+    if (user && is_device_ptr(user)) return static_cast<T *>(user);
+    return static_cast<T *>(buf.ensure(count * sizeof(T)));
+}
+
+// histogram into device buffers; returns N'
+static uint64_t histogram_into(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P, uint32_t *colors_d,
+                               uint32_t *counts_d, uint32_t *first_d) {
+    uint32_t *n_dev = static_cast<uint32_t *>(ctx->scal.ensure(256)) + 32;
+    histogram_dev(ctx, rgb_d, P, colors_d, counts_d, first_d, n_dev);
+    return read_scalar_u32(ctx, n_dev);
+}
+
+} // namespace cqg
+
+using namespace cqg;
+
+extern "C" {
+
+const char *cqg_version(void) { return "cqg 0.1 (sm_100a)"; }
+
+const char *cqg_last_error(void) { return g_last_error.c_str(); }
+
+cqg_ctx *cqg_create(int device) {
+    cqg_ctx *ctx = nullptr;
+    const int rc = guarded([&] {
+        int count = 0;
+        CQG_CUDA(cudaGetDeviceCount(&count));
+        if (device < 0 || device >= count) fail(CQG_E_INVALID, "cqg_create: no CUDA device " + std::to_string(device));
+        CQG_CUDA(cudaSetDevice(device));
+        cudaDeviceProp prop{};
+        CQG_CUDA(cudaGetDeviceProperties(&prop, device));
+        if (prop.major < 10)
+            fail(CQG_E_CUDA, std::string("cqg_create: device ") + prop.name + " is not sm_100 (Blackwell)");
+        ctx = new cqg_ctx();
+        ctx->device = device;
+        ctx->num_sms = prop.multiProcessorCount;
+        CQG_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+        ctx->own_stream = true;
+    });
+    if (rc != CQG_OK) {
+        delete ctx;
+        return nullptr;
+    }
+    return ctx;
+}
+
+void cqg_destroy(cqg_ctx *ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    DevBuf *bufs[] = {&ctx->tab, &ctx->list, &ctx->bitmap, &ctx->wordpref, &ctx->scal, &ctx->img,
+                      &ctx->colors, &ctx->counts, &ctx->first, &ctx->labels, &ctx->cen, &ctx->fcen,
+                      &ctx->dtab, &ctx->dsorted, &ctx->order, &ctx->mom, &ctx->queue, &ctx->ndc,
+                      &ctx->status, &ctx->sizes, &ctx->red, &ctx->hist_labels, &ctx->hist_centers,
+                      &ctx->sse, &ctx->lut, &ctx->idx_out, &ctx->q_out, &ctx->mom_map, &ctx->mind2,
+                      &ctx->initpart, &ctx->initsel, &ctx->unit_draws};
+    for (DevBuf *b : bufs) b->release();
+    ctx->pinned.release();
+    for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
+    if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+int cqg_set_stream(cqg_ctx *ctx, void *stream) {
+    return guarded([&] {
+        use_device(ctx);
+        if (!stream) {
+            if (!ctx->own_stream) {
+                CQG_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+                ctx->own_stream = true;
+            }
+            return;
+        }
+        if (ctx->own_stream) {
+            cudaStreamSynchronize(ctx->stream);
+            cudaStreamDestroy(ctx->stream);
+        }
+        ctx->stream = static_cast<cudaStream_t>(stream);
+        ctx->own_stream = false;
+    });
+}
+
+uint64_t cqg_launch_count(const cqg_ctx *ctx) { return ctx ? ctx->launches : 0; }
+
+int cqg_set_profiling(cqg_ctx *ctx, int on) {
+    return guarded([&] {
+        use_device(ctx);
+        prof_drain(ctx);
+        ctx->prof_on = on != 0;
+    });
+}
+
+int cqg_read_profile(cqg_ctx *ctx, cqg_profile *out, int reset) {
+    return guarded([&] {
+        use_device(ctx);
+        prof_drain(ctx);
+        if (out) {
+            for (int i = 0; i < CQG_PROF_N; ++i) {
+                out->ms[i] = ctx->prof_ms[i];
+                out->units[i] = ctx->prof_units[i];
+                out->launches[i] = ctx->prof_launches[i];
+            }
+        }
+        if (reset) {
+            for (int i = 0; i < CQG_PROF_N; ++i) {
+                ctx->prof_ms[i] = 0;
+                ctx->prof_units[i] = 0;
+                ctx->prof_launches[i] = 0;
+            }
+        }
+    });
+}
+
+int cqg_histogram(cqg_ctx *ctx, const uint8_t *rgb, uint64_t P, uint32_t *colors, uint32_t *counts,
+                  uint32_t *first, uint64_t *n_unique) {
+    return guarded([&] {
+        use_device(ctx);
+        if (P == 0 || !rgb) fail(CQG_E_INVALID, "build_histogram: no pixels");
+        validate_pixels(P, "build_histogram");
+        const uint64_t cap = P < (1ull << 24) ? P : (1ull << 24);
+        const uint8_t *rgb_d = static_cast<const uint8_t *>(stage_in(ctx, rgb, P * 3, ctx->img));
+        uint32_t *col_d = out_buf<uint32_t>(colors, ctx->colors, cap);
+        uint32_t *cnt_d = out_buf<uint32_t>(counts, ctx->counts, cap);
+        uint32_t *fst_d = first ? out_buf<uint32_t>(first, ctx->first, cap) : nullptr;
+        const uint64_t n = histogram_into(ctx, rgb_d, P, col_d, cnt_d, fst_d);
+        copy_out(ctx, colors, col_d, n * 4);
+        copy_out(ctx, counts, cnt_d, n * 4);
+        if (first) copy_out(ctx, first, fst_d, n * 4);
+        CQG_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (n_unique) *n_unique = n;
+    });
+}
+
+static void init_common(cqg_ctx *ctx, int kind, const uint32_t *colors, const uint32_t *counts, uint64_t n,
+                        uint64_t P, int k, uint64_t seed, int weighted_first, double *centers) {
+    use_device(ctx);
+    validate_k_init(k, n);
+    if (P == 0) fail(CQG_E_INVALID, "initialization: zero source pixel count");
+    const uint32_t *col_d = static_cast<const uint32_t *>(stage_in(ctx, colors, n * 4, ctx->colors));
+    const uint32_t *cnt_d = static_cast<const uint32_t *>(stage_in(ctx, counts, n * 4, ctx->counts));
+    double *cen_d = out_buf<double>(centers, ctx->cen, 3 * (size_t)k);
+    if (kind == CQG_INIT_MAXIMIN) init_maximin_dev(ctx, col_d, cnt_d, n, P, k, seed, weighted_first, cen_d);
+    else init_kmeanspp_dev(ctx, col_d, cnt_d, n, P, k, seed, cen_d);
+    copy_out(ctx, centers, cen_d, 24 * (size_t)k);
+    CQG_CUDA(cudaStreamSynchronize(ctx->stream));
+    CQG_CUDA(cudaGetLastError());
+}
+
+int cqg_init_maximin(cqg_ctx *ctx, const uint32_t *colors, const uint32_t *counts, uint64_t n, uint64_t P,
+                     int k, uint64_t seed, int weighted_first, double *centers) {
+    return guarded([&] { init_common(ctx, CQG_INIT_MAXIMIN, colors, counts, n, P, k, seed, weighted_first, centers); });
+}
+
+int cqg_init_kmeanspp(cqg_ctx *ctx, const uint32_t *colors, const uint32_t *counts, uint64_t n, uint64_t P,
+                      int k, uint64_t seed, double *centers) {
+    return guarded([&] { init_common(ctx, CQG_INIT_KMEANSPP, colors, counts, n, P, k, seed, 1, centers); });
+}
+
+int cqg_lloyd(cqg_ctx *ctx, const uint32_t *colors, const uint32_t *counts, uint64_t n, uint64_t P,
+              const double *init, int k, const cqg_term *term, double *centers, uint32_t *labels,
+              double *sse_trace, cqg_lloyd_stats *stats, uint32_t *hist_labels, double *hist_centers) {
+    return guarded([&] {
+        use_device(ctx);
+        if (!term) fail(CQG_E_INVALID, "clustering: null termination");
+        validate_run(n, k, *term);
+        if (!init || !centers || !sse_trace) fail(CQG_E_INVALID, "cqg_lloyd: null output");
+        if (P == 0) fail(CQG_E_INVALID, "wsm: weights must be positive");
+        if (!is_device_ptr(counts)) {
+            uint64_t tot = 0;
+            for (uint64_t i = 0; i < n; ++i) {
+                if (counts[i] == 0) fail(CQG_E_INVALID, "wsm: weights must be positive");
+                tot += counts[i];
+            }
+            if (tot > P) fail(CQG_E_INVALID, "cqg_lloyd: counts exceed the source pixel count");
+        }
+        const uint32_t *col_d = static_cast<const uint32_t *>(stage_in(ctx, colors, n * 4, ctx->colors));
+        const uint32_t *cnt_d = static_cast<const uint32_t *>(stage_in(ctx, counts, n * 4, ctx->counts));
+        const double *init_d = static_cast<const double *>(stage_in(ctx, init, 24 * (size_t)k, ctx->initsel));
+        uint32_t *lab_d = out_buf<uint32_t>(labels, ctx->labels, n);
+        double *cen_d = out_buf<double>(centers, ctx->cen, 3 * (size_t)k);
+        if (cen_d == init_d) fail(CQG_E_INVALID, "cqg_lloyd: centers must not alias init");
+        LloydOut o = lloyd_dev(ctx, col_d, cnt_d, n, P, init_d, k, *term, lab_d, cen_d, sse_trace,
+                               hist_labels, hist_centers);
+        copy_out(ctx, centers, cen_d, 24 * (size_t)k);
+        copy_out(ctx, labels, lab_d, 4 * n);
+        CQG_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (stats) {
+            stats->iterations = o.iterations;
+            stats->repair_count = o.repairs;
+            stats->ndc_total = o.ndc;
+            stats->n_points = n;
+            stats->flagged_total = o.flagged;
+        }
+    });
+}
+
+int cqg_map(cqg_ctx *ctx, const uint8_t *rgb, uint64_t P, const double *palette, int k, void *indices,
+            int index_bytes, uint8_t *quantized, double *mean_sq_dist) {
+    return guarded([&] {
+        use_device(ctx);
+        if (k < 1 || !palette) fail(CQG_E_INVALID, "map_pixels: empty palette");
+        if (P == 0 || !rgb) fail(CQG_E_INVALID, "map_pixels: empty image");
+        validate_pixels(P, "map_pixels");
+        if (k > 4096) fail(CQG_E_INVALID, "map_pixels: palettes above 4096 entries are not supported");
+        if (index_bytes != 1 && index_bytes != 4) fail(CQG_E_INVALID, "map_pixels: index_bytes must be 1 or 4");
+        if (index_bytes == 1 && k > 256) fail(CQG_E_INVALID, "map_pixels: 8-bit indices need k <= 256");
+        const uint64_t cap = P < (1ull << 24) ? P : (1ull << 24);
+        const uint8_t *rgb_d = static_cast<const uint8_t *>(stage_in(ctx, rgb, P * 3, ctx->img));
+        const double *pal_d = static_cast<const double *>(stage_in(ctx, palette, 24 * (size_t)k, ctx->initsel));
+        uint32_t *col_d = static_cast<uint32_t *>(ctx->colors.ensure(cap * 4));
+        uint32_t *cnt_d = static_cast<uint32_t *>(ctx->counts.ensure(cap * 4));
+        const uint64_t n = histogram_into(ctx, rgb_d, P, col_d, cnt_d, nullptr);
+        void *idx_d = indices ? out_buf<uint8_t>(indices, ctx->idx_out, P * (size_t)index_bytes) : nullptr;
+        uint8_t *q_d = quantized ? out_buf<uint8_t>(quantized, ctx->q_out, P * 3) : nullptr;
+        const double mse = map_dev(ctx, rgb_d, P, col_d, cnt_d, n, pal_d, k, idx_d, index_bytes, q_d);
+        copy_out(ctx, indices, idx_d, P * (size_t)index_bytes);
+        copy_out(ctx, quantized, q_d, P * 3);
+        CQG_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (mean_sq_dist) *mean_sq_dist = mse;
+    });
+}
+
+int cqg_quantize(cqg_ctx *ctx, const uint8_t *rgb, uint64_t P, const cqg_quantize_cfg *cfg, const double *init,
+                 double *palette, uint32_t *labels, double *sse_trace, void *indices, uint8_t *quantized,
+                 cqg_quantize_stats *stats) {
+    return guarded([&] {
+        use_device(ctx);
+        if (P == 0 || !rgb) fail(CQG_E_INVALID, "run_quantize: empty image");
+        if (!cfg) fail(CQG_E_INVALID, "run_quantize: null config");
+        const int k = cfg->k;
+        if (k < 1) fail(CQG_E_INVALID, "run_quantize: k must be at least 1");
+        validate_pixels(P, "run_quantize");
+        if (!palette) fail(CQG_E_INVALID, "run_quantize: null palette output");
+        const int ib = cfg->index_bytes == 1 ? 1 : 4;
+        if (ib == 1 && k > 256) fail(CQG_E_INVALID, "map_pixels: 8-bit indices need k <= 256");
+        Timer tm(ctx, stats != nullptr);
+        const uint64_t cap = P < (1ull << 24) ? P : (1ull << 24);
+        const uint8_t *rgb_d = static_cast<const uint8_t *>(stage_in(ctx, rgb, P * 3, ctx->img));
+        uint32_t *col_d = static_cast<uint32_t *>(ctx->colors.ensure(cap * 4));
+        uint32_t *cnt_d = static_cast<uint32_t *>(ctx->counts.ensure(cap * 4));
+        const uint64_t n = histogram_into(ctx, rgb_d, P, col_d, cnt_d, nullptr);
+        const double t_hist = tm.lap();
+
+        double *init_d = static_cast<double *>(ctx->initsel.ensure(24 * (size_t)k + 64));
+        if (cfg->init_kind == CQG_INIT_GIVEN) {
+            if (!init) fail(CQG_E_INVALID, "run_quantize: initial centres required");
+            CQG_CUDA(cudaMemcpyAsync(init_d, init, 24 * (size_t)k, cudaMemcpyDefault, ctx->stream));
+        } else {
+            validate_k_init(k, n);
+            double *tmp = static_cast<double *>(ctx->hist_centers.ensure(24 * (size_t)k));
+            if (cfg->init_kind == CQG_INIT_MAXIMIN) init_maximin_dev(ctx, col_d, cnt_d, n, P, k, cfg->seed, 1, tmp);
+            else if (cfg->init_kind == CQG_INIT_KMEANSPP) init_kmeanspp_dev(ctx, col_d, cnt_d, n, P, k, cfg->seed, tmp);
+            else fail(CQG_E_INVALID, "run_quantize: unknown initializer kind");
+            CQG_CUDA(cudaMemcpyAsync(init_d, tmp, 24 * (size_t)k, cudaMemcpyDeviceToDevice, ctx->stream));
+        }
+        const double t_init = tm.lap();
+
+        cqg_term term = cfg->term;
+        term.record_history = 0;
+        validate_run(n, k, term);
+        uint32_t *lab_d = static_cast<uint32_t *>(ctx->labels.ensure(cap * 4));
+        double *cen_d = static_cast<double *>(ctx->cen.ensure(24 * (size_t)k));
+        const int limit = term.fixed_iterations > 0 ? term.fixed_iterations : term.max_iterations;
+        double *sse_h = static_cast<double *>(ctx->pinned.ensure(4096 + 8 * (size_t)limit)) + 512;
+        LloydOut o = lloyd_dev(ctx, col_d, cnt_d, n, P, init_d, k, term, lab_d, cen_d, sse_h, nullptr, nullptr);
+        if (sse_trace) std::memcpy(sse_trace, sse_h, 8 * (size_t)o.iterations);
+        const double t_lloyd = tm.lap();
+
+        void *idx_d = indices ? out_buf<uint8_t>(indices, ctx->idx_out, P * (size_t)ib) : nullptr;
+        uint8_t *q_d = quantized ? out_buf<uint8_t>(quantized, ctx->q_out, P * 3) : nullptr;
+        const double mse = map_dev(ctx, rgb_d, P, col_d, cnt_d, n, cen_d, k, idx_d, ib, q_d);
+        copy_out(ctx, palette, cen_d, 24 * (size_t)k);
+        copy_out(ctx, labels, lab_d, 4 * n);
+        copy_out(ctx, indices, idx_d, P * (size_t)ib);
+        copy_out(ctx, quantized, q_d, P * 3);
+        CQG_CUDA(cudaStreamSynchronize(ctx->stream));
+        const double t_map = tm.lap();
+        if (stats) {
+            stats->n_unique = n;
+            stats->lloyd.iterations = o.iterations;
+            stats->lloyd.repair_count = o.repairs;
+            stats->lloyd.ndc_total = o.ndc;
+            stats->lloyd.n_points = n;
+            stats->lloyd.flagged_total = o.flagged;
+            stats->mean_sq_dist = mse;
+            stats->ms_histogram = t_hist;
+            stats->ms_init = t_init;
+            stats->ms_lloyd = t_lloyd;
+            stats->ms_map = t_map;
+        }
+    });
+}
+
+} // extern "C"

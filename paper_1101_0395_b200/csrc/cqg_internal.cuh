@@ -1,0 +1,219 @@
+// cqg_internal.cuh -- shared context, buffers, error plumbing and exact-FP64
+// device helpers for libcqg.so (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "cqg.h"
+
+namespace cqg {
+
+// ---------------------------------------------------------------------------
+// errors: thrown inside the library, converted to CQG_E_* at the C boundary
+
+struct Error {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] inline void fail(int code, const std::string &msg) { throw Error{code, msg}; }
+
+#define CQG_CUDA(call)                                                                    \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess)                                                            \
+            ::cqg::fail(CQG_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// grow-only device buffers owned by a context
+
+struct DevBuf {
+    void *p = nullptr;
+    size_t cap = 0;
+    void *ensure(size_t bytes) {
+        if (bytes <= cap && p) return p;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        size_t want = bytes < 256 ? 256 : bytes;
+        if (cudaMalloc(&p, want) != cudaSuccess) {
+            cudaGetLastError();
+            fail(CQG_E_NOMEM, "device allocation of " + std::to_string(want) + " bytes failed");
+        }
+        cap = want;
+        return p;
+    }
+    template <class T>
+    T *as() const { return static_cast<T *>(p); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+struct HostBuf {
+    void *p = nullptr;
+    size_t cap = 0;
+    void *ensure(size_t bytes) {
+        if (bytes <= cap && p) return p;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+        size_t want = bytes < 256 ? 256 : bytes;
+        if (cudaMallocHost(&p, want) != cudaSuccess) {
+            cudaGetLastError();
+            fail(CQG_E_NOMEM, "pinned allocation failed");
+        }
+        cap = want;
+        return p;
+    }
+    template <class T>
+    T *as() const { return static_cast<T *>(p); }
+    void release() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+// Per-iteration device status written by the finalize kernel and read back by
+// the host loop (one small D2H per Lloyd iteration).
+struct IterStatus {
+    int32_t state;      // 0 continue, 1 done, 2 empty cluster -> repair needed
+    int32_t iteration;
+    uint32_t n_flagged; // FP64 replays this iteration
+    uint32_t pad;
+    double sse;
+};
+
+// Moments of one cluster over the count-weighted substrate: n = sum count,
+// s = sum count*x (per channel), q = sum count*|x|^2. Exact integers.
+struct Moments {
+    unsigned long long n;
+    long long s[3];
+    unsigned long long q;
+};
+
+} // namespace cqg
+
+struct cqg_ctx {
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    unsigned long long launches = 0;
+
+    // stage 1 scratch
+    cqg::DevBuf tab;       // 2^24 x uint2 {count, ~first_index}; kept all-zero between calls
+    cqg::DevBuf list;      // unique colours in arrival order
+    cqg::DevBuf bitmap;    // P bits: first-occurrence marks
+    cqg::DevBuf wordpref;  // per-bitmap-block exclusive prefix
+    cqg::DevBuf scal;      // small device scalars (counters)
+    // input / substrate staging
+    cqg::DevBuf img;       // image bytes when the caller passes host memory
+    cqg::DevBuf colors, counts, first;
+    // Lloyd state
+    cqg::DevBuf labels, cen, fcen, dtab, dsorted, order, mom, queue, ndc, status, sizes, red;
+    cqg::DevBuf hist_labels, hist_centers, sse;
+    // mapping
+    cqg::DevBuf lut, idx_out, q_out, mom_map;
+    // init
+    cqg::DevBuf mind2, initpart, initsel, unit_draws;
+    cqg::HostBuf pinned;   // status readback and small results
+
+    // kernel-level profiling (cqg_set_profiling)
+    bool prof_on = false;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    struct ProfRec {
+        int cat;
+        int e0, e1;
+        double units;
+    };
+    std::vector<ProfRec> prof_recs;
+    double prof_ms[CQG_PROF_N] = {};
+    double prof_units[CQG_PROF_N] = {};
+    unsigned long long prof_launches[CQG_PROF_N] = {};
+};
+
+namespace cqg {
+
+// ---------------------------------------------------------------------------
+// exact FP64 helpers: no FMA contraction, so results equal the reference's
+// dist2 (color.hpp:47-59: ((dr*dr)+(dg*dg))+(db*db)) bit for bit.
+
+__device__ __forceinline__ double d2_exact(double xr, double xg, double xb, double cr, double cg,
+                                           double cb) {
+    const double dr = __dsub_rn(xr, cr), dg = __dsub_rn(xg, cg), db = __dsub_rn(xb, cb);
+    return __dadd_rn(__dadd_rn(__dmul_rn(dr, dr), __dmul_rn(dg, dg)), __dmul_rn(db, db));
+}
+
+// correctly rounded unsigned 128-bit -> double (same contract as the oracle)
+__device__ __forceinline__ double u128_to_double(unsigned __int128 x) {
+    const unsigned long long hi = (unsigned long long)(x >> 64);
+    if (hi == 0) return __ull2double_rn((unsigned long long)x);
+    const int s = 64 - __clzll((long long)hi);
+    unsigned long long v = (unsigned long long)(x >> s);
+    const unsigned __int128 lostmask = (((unsigned __int128)1) << s) - 1;
+    if ((x & lostmask) != 0) v |= 1ULL;
+    return scalbn(__ull2double_rn(v), s);
+}
+
+// (n*Q - |S|^2) / n for one cluster, exact numerator (cluster_sse_exact in the oracle)
+__device__ __forceinline__ double cluster_sse_exact(unsigned long long n, const long long *s,
+                                                    unsigned long long q) {
+    const unsigned __int128 nq = (unsigned __int128)n * q;
+    const unsigned __int128 ss = (unsigned __int128)((__int128)s[0] * s[0]) +
+                                 (unsigned __int128)((__int128)s[1] * s[1]) +
+                                 (unsigned __int128)((__int128)s[2] * s[2]);
+    return __ddiv_rn(u128_to_double(nq - ss), __ull2double_rn(n));
+}
+
+__host__ __device__ __forceinline__ unsigned ceil_div(unsigned long long a, unsigned long long b) {
+    return (unsigned)((a + b - 1) / b);
+}
+
+// host-side helpers implemented in api.cu
+bool is_device_ptr(const void *p);
+// profiling: prof_begin records a start event (returns -1 when profiling is off)
+int prof_begin(cqg_ctx *ctx);
+void prof_end(cqg_ctx *ctx, int cat, int begin, double units);
+void launched(cqg_ctx *ctx, int n = 1);
+// copy `bytes` from user pointer (host or device) into a device buffer and
+// return a device pointer that holds the data (the user pointer itself when
+// it is already device memory).
+const void *stage_in(cqg_ctx *ctx, const void *user, size_t bytes, DevBuf &buf);
+void copy_out(cqg_ctx *ctx, void *user, const void *dev, size_t bytes);
+
+// stage implementations (device pointers only; n_dev is a device scalar)
+void histogram_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P, uint32_t *colors_d,
+                   uint32_t *counts_d, uint32_t *first_d, uint32_t *n_dev);
+uint64_t read_scalar_u32(cqg_ctx *ctx, const uint32_t *dev);
+
+struct LloydOut {
+    int iterations = 0;
+    int repairs = 0;
+    unsigned long long ndc = 0;
+    unsigned long long flagged = 0;
+};
+LloydOut lloyd_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *counts_d, uint64_t n,
+                   uint64_t P, const double *init_d, int k, const cqg_term &term, uint32_t *labels_d,
+                   double *centers_d, double *sse_host, uint32_t *hist_labels_user,
+                   double *hist_centers_user);
+
+double map_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P, const uint32_t *colors_d,
+               const uint32_t *counts_d, uint64_t n, const double *pal_d, int k, void *indices_d,
+               int index_bytes, uint8_t *quant_d);
+
+void init_maximin_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *counts_d, uint64_t n,
+                      uint64_t P, int k, uint64_t seed, int weighted_first, double *centers_d);
+void init_kmeanspp_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *counts_d,
+                       uint64_t n, uint64_t P, int k, uint64_t seed, double *centers_d);
+
+} // namespace cqg

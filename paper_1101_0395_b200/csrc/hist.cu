@@ -1,0 +1,239 @@
+// hist.cu -- stage 1: distinct colours in first-occurrence order.
+//
+// Replaces quant::build_histogram (reference src/histogram.cpp:69-104). The
+// reference dedups through a seeded chained hash and appends colours on first
+// sight, so its output order is "by first pixel index". Here:
+//
+//   A  hist_count   per pixel (16 pixels / thread, 3 x 128-bit loads):
+//                   atomicAdd(tab[c].count) with return -> the lane that sees 0
+//                   appends c to an (unordered) list (warp-aggregated append);
+//                   atomicMax(tab[c].neg_first, ~p) keeps the minimum index.
+//   B  hist_mark    per listed colour: set bit first(c) in a P-bit bitmap.
+//   C  scan         popcount prefix over the bitmap words (2 small kernels).
+//   D  hist_emit    per listed colour: rank = prefix(first(c)) -> write
+//                   (colour, count, first) at that rank, i.e. in first-occurrence
+//                   order; reset tab[c] to zero so the 2^24 table stays clean
+//                   without a 128 MiB memset per call.
+//
+// The table (2^24 x {count, ~first}) is 128 MiB and lives in the context; it
+// is zero between calls. HBM bound: 3P bytes read + 8N' written + atomics.
+#include "cqg_internal.cuh"
+
+namespace cqg {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWordsPerThread = 16;                         // scan granularity
+constexpr int kWordsPerBlock = kThreads * kWordsPerThread;  // 4096 words = 131072 pixels
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+__device__ __forceinline__ uint4 ld_stream(const uint4 *p) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+    return v;
+}
+
+// Count one pixel; returns true if this lane saw the colour first.
+__device__ __forceinline__ bool count_pixel(uint2 *tab, uint32_t c, uint32_t p) {
+    const uint32_t old = atomicAdd(&tab[c].x, 1u);
+    atomicMax(&tab[c].y, ~p);
+    return old == 0;
+}
+
+__device__ __forceinline__ void append(bool isnew, uint32_t c, uint32_t *list, uint32_t *list_n) {
+    const uint32_t active = __activemask();
+    const uint32_t m = __ballot_sync(active, isnew);
+    if (m == 0) return;
+    const int leader = __ffs(m) - 1;
+    uint32_t base = 0;
+    if ((int)(threadIdx.x & 31) == leader) base = atomicAdd(list_n, (uint32_t)__popc(m));
+    base = __shfl_sync(active, base, leader);
+    if (isnew) list[base + __popc(m & lanemask_lt())] = c;
+}
+
+__global__ void __launch_bounds__(kThreads) hist_count(const uint8_t *__restrict__ rgb, uint64_t P,
+                                                      uint2 *__restrict__ tab,
+                                                      uint32_t *__restrict__ list,
+                                                      uint32_t *__restrict__ list_n, int aligned) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t groups = aligned ? P / 16 : 0;
+    for (uint64_t g = tid; g < groups; g += stride) {
+        const uint4 *src = reinterpret_cast<const uint4 *>(rgb + g * 48);
+        const uint4 a = ld_stream(src), b = ld_stream(src + 1), d = ld_stream(src + 2);
+        const uint32_t w[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, d.x, d.y, d.z, d.w};
+        uint32_t col[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            // bytes 3j, 3j+1, 3j+2 of the 48-byte group (little endian)
+            const int o = 3 * j;
+            const uint32_t b0 = (w[o >> 2] >> (8 * (o & 3))) & 255u;
+            const uint32_t b1 = (w[(o + 1) >> 2] >> (8 * ((o + 1) & 3))) & 255u;
+            const uint32_t b2 = (w[(o + 2) >> 2] >> (8 * ((o + 2) & 3))) & 255u;
+            col[j] = (b0 << 16) | (b1 << 8) | b2;
+        }
+        bool isnew[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) isnew[j] = count_pixel(tab, col[j], (uint32_t)(g * 16 + j));
+#pragma unroll
+        for (int j = 0; j < 16; ++j) append(isnew[j], col[j], list, list_n);
+    }
+    // tail (or everything when the input is not 16-byte aligned)
+    for (uint64_t p = groups * 16 + tid; p < P; p += stride) {
+        const uint32_t c = ((uint32_t)rgb[3 * p] << 16) | ((uint32_t)rgb[3 * p + 1] << 8) | rgb[3 * p + 2];
+        const bool isnew = count_pixel(tab, c, (uint32_t)p);
+        append(isnew, c, list, list_n);
+    }
+}
+
+__global__ void hist_mark(const uint32_t *__restrict__ list, const uint32_t *__restrict__ list_n,
+                          const uint2 *__restrict__ tab, uint32_t *__restrict__ bitmap) {
+    const uint32_t n = *list_n;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t f = ~tab[list[i]].y;
+        atomicOr(&bitmap[f >> 5], 1u << (f & 31));
+    }
+}
+
+// block sums of popcounts over kWordsPerBlock words
+__global__ void __launch_bounds__(kThreads) scan_blocksum(const uint32_t *__restrict__ bitmap,
+                                                          uint64_t words, uint32_t *__restrict__ bsum) {
+    __shared__ uint32_t red[kThreads / 32];
+    const uint64_t base = (uint64_t)blockIdx.x * kWordsPerBlock + (uint64_t)threadIdx.x * kWordsPerThread;
+    uint32_t s = 0;
+#pragma unroll
+    for (int i = 0; i < kWordsPerThread; ++i)
+        if (base + i < words) s += __popc(bitmap[base + i]);
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t t = 0;
+        for (int i = 0; i < kThreads / 32; ++i) t += red[i];
+        bsum[blockIdx.x] = t;
+    }
+}
+
+// exclusive scan of the block sums (one block, sequential chunks)
+__global__ void scan_blocks(uint32_t *__restrict__ bsum, uint32_t nblocks) {
+    __shared__ uint32_t carry;
+    __shared__ uint32_t tmp[1024];
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (uint32_t base = 0; base < nblocks; base += 1024) {
+        const uint32_t i = base + threadIdx.x;
+        const uint32_t v = i < nblocks ? bsum[i] : 0;
+        tmp[threadIdx.x] = v;
+        __syncthreads();
+        for (int off = 1; off < 1024; off <<= 1) {
+            const uint32_t add = threadIdx.x >= (unsigned)off ? tmp[threadIdx.x - off] : 0;
+            __syncthreads();
+            tmp[threadIdx.x] += add;
+            __syncthreads();
+        }
+        if (i < nblocks) bsum[i] = carry + tmp[threadIdx.x] - v;
+        __syncthreads();
+        if (threadIdx.x == 1023) carry += tmp[1023];
+        __syncthreads();
+    }
+}
+
+// per-word exclusive prefix (global)
+__global__ void __launch_bounds__(kThreads) scan_words(const uint32_t *__restrict__ bitmap, uint64_t words,
+                                                       const uint32_t *__restrict__ bsum,
+                                                       uint32_t *__restrict__ wpref) {
+    __shared__ uint32_t wsum[kThreads / 32];
+    const uint64_t base = (uint64_t)blockIdx.x * kWordsPerBlock + (uint64_t)threadIdx.x * kWordsPerThread;
+    uint32_t pc[kWordsPerThread];
+    uint32_t s = 0;
+#pragma unroll
+    for (int i = 0; i < kWordsPerThread; ++i) {
+        pc[i] = (base + i < words) ? __popc(bitmap[base + i]) : 0;
+        s += pc[i];
+    }
+    // exclusive scan of s across the block
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t incl = s;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    if (lane == 31) wsum[wid] = incl;
+    __syncthreads();
+    uint32_t woff = 0;
+    for (int i = 0; i < wid; ++i) woff += wsum[i];
+    uint32_t run = bsum[blockIdx.x] + woff + incl - s;
+#pragma unroll
+    for (int i = 0; i < kWordsPerThread; ++i) {
+        if (base + i < words) wpref[base + i] = run;
+        run += pc[i];
+    }
+}
+
+__global__ void hist_emit(const uint32_t *__restrict__ list, const uint32_t *__restrict__ list_n,
+                          uint2 *__restrict__ tab, const uint32_t *__restrict__ bitmap,
+                          const uint32_t *__restrict__ wpref, uint32_t *__restrict__ colors,
+                          uint32_t *__restrict__ counts, uint32_t *__restrict__ first) {
+    const uint32_t n = *list_n;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t c = list[i];
+        const uint2 t = tab[c];
+        const uint32_t f = ~t.y;
+        const uint32_t w = f >> 5;
+        const uint32_t rank = wpref[w] + __popc(bitmap[w] & ((1u << (f & 31)) - 1u));
+        colors[rank] = c;
+        counts[rank] = t.x;
+        if (first) first[rank] = f;
+        tab[c] = make_uint2(0u, 0u);
+    }
+}
+
+} // namespace
+
+void histogram_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P, uint32_t *colors_d,
+                   uint32_t *counts_d, uint32_t *first_d, uint32_t *n_dev) {
+    cudaStream_t s = ctx->stream;
+    if (ctx->tab.cap < (sizeof(uint2) << 24)) {
+        ctx->tab.ensure(sizeof(uint2) << 24);
+        CQG_CUDA(cudaMemsetAsync(ctx->tab.p, 0, sizeof(uint2) << 24, s));
+    }
+    const uint64_t cap = P < (1ull << 24) ? P : (1ull << 24);
+    uint32_t *list = static_cast<uint32_t *>(ctx->list.ensure(cap * 4));
+    const uint64_t words = (P + 31) / 32;
+    const uint32_t nblk = ceil_div(words, kWordsPerBlock);
+    uint32_t *bitmap = static_cast<uint32_t *>(ctx->bitmap.ensure(words * 4 + 16));
+    uint32_t *wpref = static_cast<uint32_t *>(ctx->wordpref.ensure(words * 4 + 16 + (size_t)nblk * 4));
+    uint32_t *bsum = wpref + words + 4;
+
+    const int pb = prof_begin(ctx);
+    CQG_CUDA(cudaMemsetAsync(n_dev, 0, 4, s));
+    CQG_CUDA(cudaMemsetAsync(bitmap, 0, words * 4, s));
+
+    const int aligned = (reinterpret_cast<uintptr_t>(rgb_d) & 15) == 0;
+    const uint64_t work = aligned ? (P / 16 > 0 ? P / 16 : P) : P;
+    unsigned grid = ceil_div(work, kThreads);
+    const unsigned gmax = (unsigned)ctx->num_sms * 8;
+    if (grid > gmax) grid = gmax;
+    if (grid == 0) grid = 1;
+    hist_count<<<grid, kThreads, 0, s>>>(rgb_d, P, ctx->tab.as<uint2>(), list, n_dev, aligned);
+    unsigned lgrid = ceil_div(cap, kThreads);
+    if (lgrid > gmax) lgrid = gmax;
+    hist_mark<<<lgrid, kThreads, 0, s>>>(list, n_dev, ctx->tab.as<uint2>(), bitmap);
+    scan_blocksum<<<nblk, kThreads, 0, s>>>(bitmap, words, bsum);
+    scan_blocks<<<1, 1024, 0, s>>>(bsum, nblk);
+    scan_words<<<nblk, kThreads, 0, s>>>(bitmap, words, bsum, wpref);
+    hist_emit<<<lgrid, kThreads, 0, s>>>(list, n_dev, ctx->tab.as<uint2>(), bitmap, wpref, colors_d,
+                                         counts_d, first_d);
+    prof_end(ctx, CQG_PROF_HIST, pb, 3.0 * (double)P); // + 8 N' added by the caller
+    CQG_CUDA(cudaGetLastError());
+    launched(ctx, 6);
+}
+
+} // namespace cqg

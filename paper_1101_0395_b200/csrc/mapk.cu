@@ -1,0 +1,225 @@
+// mapk.cu -- stage 4: pixel -> palette mapping and MSE.
+//
+// Replaces quant::map_pixels (reference src/metrics.cpp:15-55). The reference
+// resolves each distinct colour once through nearest_pruned_lowest_index
+// (kmeans.cpp:81-105), whose result is the exact lowest-index FP64 argmin
+// (kmeans.hpp:88-96), caches it in a hash map and accumulates
+// dist2(centre, pixel) sequentially. Here:
+//   sweep<MAP> + replay<MAP>  lowest-index argmin per distinct colour (same
+//                             FP32 sweep + exact FP64 replay as Lloyd) written
+//                             to a 2^24-entry LUT, plus exact per-cluster
+//                             pixel moments (count-weighted);
+//   mse_kernel                mean_sq_dist = sum_k [(nQ-|S|^2)/n + n|c-S/n|^2] / P
+//                             from those moments (deterministic, ~1e-14 of the
+//                             reference's sequential FP64 sum);
+//   pixel_kernel              per pixel: LUT gather -> index (u8 or u32) and the
+//                             palette colour rendered by channel_to_u8
+//                             (color.hpp:63-72); 16 pixels / thread, 128-bit
+//                             loads and stores. HBM bound: 3P in, (1|4)P + 3P out.
+#include "sweep.cuh"
+
+namespace cqg {
+namespace {
+
+__global__ void mse_kernel(const Moments *mom, const double *pal, int K, uint64_t P, double *out) {
+    extern __shared__ double s_t[];
+    for (int k = threadIdx.x; k < K; k += blockDim.x) {
+        const Moments m = mom[k];
+        double t = 0.0;
+        if (m.n != 0) {
+            const double nd = __ull2double_rn(m.n);
+            const double a = cluster_sse_exact(m.n, m.s, m.q);
+            const double dr = __dsub_rn(pal[3 * k], __ddiv_rn(__ll2double_rn(m.s[0]), nd));
+            const double dg = __dsub_rn(pal[3 * k + 1], __ddiv_rn(__ll2double_rn(m.s[1]), nd));
+            const double db = __dsub_rn(pal[3 * k + 2], __ddiv_rn(__ll2double_rn(m.s[2]), nd));
+            const double e = __dadd_rn(__dadd_rn(__dmul_rn(dr, dr), __dmul_rn(dg, dg)), __dmul_rn(db, db));
+            t = __dadd_rn(a, __dmul_rn(nd, e));
+        }
+        s_t[k] = t;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double tot = 0.0;
+        for (int k = 0; k < K; ++k)
+            if (mom[k].n != 0) tot = __dadd_rn(tot, s_t[k]);
+        *out = __ddiv_rn(tot, __ull2double_rn(P));
+    }
+}
+
+__device__ __forceinline__ uint8_t channel_to_u8(double v) {
+    double r = floor(__dadd_rn(v, 0.5));
+    if (r < 0.0) r = 0.0;
+    if (r > 255.0) r = 255.0;
+    return (uint8_t)r;
+}
+
+__device__ __forceinline__ uint4 ld_stream4(const uint4 *p) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+    return v;
+}
+
+__device__ __forceinline__ void st_stream4(uint4 *p, uint4 v) {
+    asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+                 "r"(v.w));
+}
+
+// IB = index bytes (1 or 4); LUT8 = LUT element is uint8 (K <= 256)
+template <int IB, bool LUT8>
+__global__ void __launch_bounds__(256) pixel_kernel(const uint8_t *__restrict__ rgb, uint64_t P,
+                                                   const void *__restrict__ lut_v,
+                                                   const double *__restrict__ pal, int K,
+                                                   void *__restrict__ idx_out,
+                                                   uint8_t *__restrict__ q_out, int vec) {
+    extern __shared__ uint32_t s_pal8[]; // packed 0x00BBGGRR little-endian bytes r,g,b
+    for (int k = threadIdx.x; k < K; k += blockDim.x)
+        s_pal8[k] = (uint32_t)channel_to_u8(pal[3 * k]) | ((uint32_t)channel_to_u8(pal[3 * k + 1]) << 8) |
+                    ((uint32_t)channel_to_u8(pal[3 * k + 2]) << 16);
+    __syncthreads();
+    const uint8_t *lut8 = static_cast<const uint8_t *>(lut_v);
+    const uint32_t *lut32 = static_cast<const uint32_t *>(lut_v);
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t groups = vec ? P / 16 : 0;
+    for (uint64_t g = tid; g < groups; g += stride) {
+        const uint4 *src = reinterpret_cast<const uint4 *>(rgb + g * 48);
+        const uint4 a = ld_stream4(src), b = ld_stream4(src + 1), d = ld_stream4(src + 2);
+        const uint32_t w[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, d.x, d.y, d.z, d.w};
+        uint32_t idx[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const int o = 3 * j;
+            const uint32_t b0 = (w[o >> 2] >> (8 * (o & 3))) & 255u;
+            const uint32_t b1 = (w[(o + 1) >> 2] >> (8 * ((o + 1) & 3))) & 255u;
+            const uint32_t b2 = (w[(o + 2) >> 2] >> (8 * ((o + 2) & 3))) & 255u;
+            const uint32_t c = (b0 << 16) | (b1 << 8) | b2;
+            idx[j] = LUT8 ? (uint32_t)__ldg(lut8 + c) : __ldg(lut32 + c);
+        }
+        // quantized RGB: 16 pixels = 48 bytes = 12 words
+        uint32_t qw[12];
+#pragma unroll
+        for (int i = 0; i < 12; ++i) qw[i] = 0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const uint32_t p8 = s_pal8[idx[j]];
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) {
+                const int o = 3 * j + ch;
+                qw[o >> 2] |= ((p8 >> (8 * ch)) & 255u) << (8 * (o & 3));
+            }
+        }
+        uint4 *dst = reinterpret_cast<uint4 *>(q_out + g * 48);
+        if (q_out) {
+            st_stream4(dst, make_uint4(qw[0], qw[1], qw[2], qw[3]));
+            st_stream4(dst + 1, make_uint4(qw[4], qw[5], qw[6], qw[7]));
+            st_stream4(dst + 2, make_uint4(qw[8], qw[9], qw[10], qw[11]));
+        }
+        if (idx_out) {
+            if (IB == 1) {
+                uint32_t iw[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    iw[i] = idx[4 * i] | (idx[4 * i + 1] << 8) | (idx[4 * i + 2] << 16) | (idx[4 * i + 3] << 24);
+                st_stream4(reinterpret_cast<uint4 *>(static_cast<uint8_t *>(idx_out) + g * 16),
+                           make_uint4(iw[0], iw[1], iw[2], iw[3]));
+            } else {
+                uint4 *o4 = reinterpret_cast<uint4 *>(static_cast<uint32_t *>(idx_out) + g * 16);
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    st_stream4(o4 + i, make_uint4(idx[4 * i], idx[4 * i + 1], idx[4 * i + 2], idx[4 * i + 3]));
+            }
+        }
+    }
+    for (uint64_t p = groups * 16 + tid; p < P; p += stride) {
+        const uint32_t c = ((uint32_t)rgb[3 * p] << 16) | ((uint32_t)rgb[3 * p + 1] << 8) | rgb[3 * p + 2];
+        const uint32_t id = LUT8 ? (uint32_t)lut8[c] : lut32[c];
+        const uint32_t p8 = s_pal8[id];
+        if (q_out) {
+            q_out[3 * p] = (uint8_t)(p8 & 255u);
+            q_out[3 * p + 1] = (uint8_t)((p8 >> 8) & 255u);
+            q_out[3 * p + 2] = (uint8_t)((p8 >> 16) & 255u);
+        }
+        if (idx_out) {
+            if (IB == 1) static_cast<uint8_t *>(idx_out)[p] = (uint8_t)id;
+            else static_cast<uint32_t *>(idx_out)[p] = id;
+        }
+    }
+}
+
+} // namespace
+
+double map_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P, const uint32_t *colors_d,
+               const uint32_t *counts_d, uint64_t n, const double *pal_d, int K, void *indices_d,
+               int index_bytes, uint8_t *quant_d) {
+    cudaStream_t s = ctx->stream;
+    const int Kp = (K + 3) & ~3;
+    const bool lut8 = K <= 256;
+    float *fc = static_cast<float *>(ctx->fcen.ensure(sizeof(float) * (4 * (size_t)Kp + 8)));
+    float *tau = fc + 4 * Kp;
+    void *lut = ctx->lut.ensure(lut8 ? (1u << 24) : (sizeof(uint32_t) << 24));
+    Moments *mom = static_cast<Moments *>(ctx->mom_map.ensure(sizeof(Moments) * (size_t)K + 64));
+    double *mse_d = reinterpret_cast<double *>(mom + K);
+    uint32_t *queue = static_cast<uint32_t *>(ctx->queue.ensure(sizeof(uint32_t) * (n + 1)));
+    uint32_t *qn = static_cast<uint32_t *>(ctx->scal.ensure(256));
+
+    CQG_CUDA(cudaMemsetAsync(mom, 0, sizeof(Moments) * (size_t)K, s));
+    CQG_CUDA(cudaMemsetAsync(qn, 0, 4, s));
+    fc_kernel<<<1, 256, 0, s>>>(pal_d, K, Kp, fc, tau);
+    launched(ctx);
+
+    SweepArgs a{};
+    a.colors = colors_d;
+    a.counts = counts_d;
+    a.n = n;
+    a.lut8 = lut8 ? static_cast<uint8_t *>(lut) : nullptr;
+    a.lut32 = lut8 ? nullptr : static_cast<uint32_t *>(lut);
+    a.fc = fc;
+    a.cen = pal_d;
+    a.tau = tau;
+    a.queue = queue;
+    a.qn = qn;
+    a.mom = mom;
+    a.K = K;
+    a.Kp = Kp;
+    launch_sweep(ctx, MODE_MAP, a);
+
+    if ((size_t)K * 8 > 48 * 1024)
+        CQG_CUDA(cudaFuncSetAttribute(mse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, K * 8));
+    mse_kernel<<<1, 256, (size_t)K * 8, s>>>(mom, pal_d, K, P, mse_d);
+    launched(ctx);
+
+    if (indices_d || quant_d) {
+        const int vec = ((reinterpret_cast<uintptr_t>(rgb_d) | reinterpret_cast<uintptr_t>(indices_d) |
+                          reinterpret_cast<uintptr_t>(quant_d)) & 15) == 0;
+        uint64_t work = vec ? P / 16 + 1 : P;
+        uint64_t grid = (work + 255) / 256;
+        const uint64_t gmax = (uint64_t)ctx->num_sms * 8;
+        if (grid > gmax) grid = gmax;
+        const size_t smem = (size_t)K * 4;
+        if (smem > 48 * 1024) {
+            CQG_CUDA(cudaFuncSetAttribute(pixel_kernel<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        }
+        const int pp = prof_begin(ctx);
+        if (index_bytes == 1) {
+            if (lut8) pixel_kernel<1, true><<<(unsigned)grid, 256, smem, s>>>(rgb_d, P, lut, pal_d, K, indices_d, quant_d, vec);
+            else fail(CQG_E_INVALID, "map_pixels: 8-bit indices need k <= 256");
+        } else {
+            if (lut8) pixel_kernel<4, true><<<(unsigned)grid, 256, smem, s>>>(rgb_d, P, lut, pal_d, K, indices_d, quant_d, vec);
+            else pixel_kernel<4, false><<<(unsigned)grid, 256, smem, s>>>(rgb_d, P, lut, pal_d, K, indices_d, quant_d, vec);
+        }
+        prof_end(ctx, CQG_PROF_PIXEL, pp,
+                 (double)P * (3.0 + (indices_d ? (double)index_bytes : 0.0) + (quant_d ? 3.0 : 0.0)));
+        launched(ctx);
+    }
+    CQG_CUDA(cudaGetLastError());
+    double mse = 0.0;
+    double *hm = static_cast<double *>(ctx->pinned.ensure(4096));
+    CQG_CUDA(cudaMemcpyAsync(hm, mse_d, 8, cudaMemcpyDeviceToHost, s));
+    CQG_CUDA(cudaStreamSynchronize(s));
+    mse = *hm;
+    return mse;
+}
+
+} // namespace cqg

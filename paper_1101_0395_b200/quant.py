@@ -1,0 +1,509 @@
+"""Python mirror of the reference quantiser API for the hot path.
+
+Same names, argument meaning and error behaviour as the reference's C++ API in
+proj/include/quant/*.hpp (cited per function); everything is computed by
+libcqg.so through the C-ABI (cabi.py). std::invalid_argument maps to
+``ValueError`` (cabi.InvalidArgument), std::runtime_error to ``RuntimeError``.
+
+Images are numpy uint8 arrays of shape (H, W, 3) (quant::RawImage,
+image.hpp:13-24) or flat P*3 byte arrays; palettes / centres are (K, 3) float64
+(quant::ColorPoint, color.hpp:21-45).
+"""
+from __future__ import annotations
+
+import json
+import math
+import time
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import cabi
+
+# ---------------------------------------------------------------------------
+# colour helpers (color.hpp:47-72)
+
+
+def channel_to_u8(v: np.ndarray | float) -> np.ndarray:
+    """Round half up, clamp to [0, 255] (color.hpp:63-68)."""
+    r = np.floor(np.asarray(v, np.float64) + 0.5)
+    return np.clip(r, 0.0, 255.0).astype(np.uint8)
+
+
+def pack_colors(rgb: np.ndarray) -> np.ndarray:
+    rgb = np.asarray(rgb, np.uint8).reshape(-1, 3).astype(np.uint32)
+    return (rgb[:, 0] << 16) | (rgb[:, 1] << 8) | rgb[:, 2]
+
+
+def unpack_colors(c: np.ndarray) -> np.ndarray:
+    c = np.asarray(c, np.uint32)
+    return np.stack([(c >> 16) & 255, (c >> 8) & 255, c & 255], axis=1).astype(np.float64)
+
+
+def _pixels(image) -> tuple[np.ndarray, int, int]:
+    if isinstance(image, RawImage):
+        arr = image.pixels
+    else:
+        arr = image
+    if hasattr(arr, "data_ptr") and not isinstance(arr, np.ndarray):  # device tensor
+        shape = tuple(arr.shape)
+        if len(shape) == 3:
+            return arr, shape[1], shape[0]
+        return arr, arr.numel() // 3, 1
+    arr = np.ascontiguousarray(arr, np.uint8)
+    if arr.ndim == 3:
+        return arr, arr.shape[1], arr.shape[0]
+    return arr.reshape(-1), arr.size // 3, 1
+
+
+@dataclass
+class RawImage:
+    """quant::RawImage (image.hpp:13-24): interleaved 8-bit RGB, row-major."""
+    width: int
+    height: int
+    pixels: np.ndarray  # (H, W, 3) uint8
+
+    def pixel_count(self) -> int:
+        return self.width * self.height
+
+
+# ---------------------------------------------------------------------------
+# stage 1 (histogram.hpp:19-60)
+
+SAMPLING_TOKENS = {"none": "None", "2to1": "TwoToOne", "unique": "Unique", "both": "TwoToOneUnique"}
+
+
+def parse_sampling_mode(token: str) -> str:
+    """histogram.cpp:19-26."""
+    if token not in SAMPLING_TOKENS:
+        raise ValueError(f"unknown sampling mode '{token}' (expected none|2to1|unique|both)")
+    return token
+
+
+@dataclass
+class WeightedHistogram:
+    """quant::WeightedHistogram (histogram.hpp:43-51), first-occurrence order."""
+    colors: np.ndarray                  # (N', 3) float64
+    weights: np.ndarray                 # (N',) float64 = counts * (1/P)
+    counts: np.ndarray                  # (N',) uint32
+    source_pixel_count: int
+    packed: np.ndarray = field(repr=False, default=None)  # (N',) uint32 0x00RRGGBB
+    first: np.ndarray = field(repr=False, default=None)   # first pixel index per colour
+
+    def size(self) -> int:
+        return int(self.counts.size)
+
+
+def build_histogram(pixels, seed: int = 1, ctx: Optional[cabi.Context] = None) -> WeightedHistogram:
+    """quant::build_histogram (histogram.hpp:57, histogram.cpp:69-104) on the device.
+
+    ``seed`` only seeds the reference's hash coefficients; the output does not
+    depend on it (the device dedups through a direct 2^24 table)."""
+    ctx = ctx or cabi.default_context()
+    arr, w, h = _pixels(pixels)
+    P = w * h
+    if P == 0:
+        raise ValueError("build_histogram: no pixels")
+    cap = min(P, 1 << 24)
+    colors = np.empty(cap, np.uint32)
+    counts = np.empty(cap, np.uint32)
+    first = np.empty(cap, np.uint32)
+    n = ctx.histogram_raw(arr, P, colors, counts, first)
+    colors, counts, first = colors[:n].copy(), counts[:n].copy(), first[:n].copy()
+    inv = 1.0 / float(P)
+    weights = counts.astype(np.float64) * inv
+    return WeightedHistogram(unpack_colors(colors), weights, counts, P, colors, first)
+
+
+# ---------------------------------------------------------------------------
+# stages 2+3 (kmeans.hpp:17-129)
+
+
+@dataclass
+class Termination:
+    """quant::Termination (kmeans.hpp:17-21)."""
+    epsilon: float = 1e-3
+    max_iterations: int = 100
+    fixed_iterations: Optional[int] = None
+
+
+@dataclass
+class ClusterOptions:
+    """quant::ClusterOptions (kmeans.hpp:28-35)."""
+    term: Termination = field(default_factory=Termination)
+    record_history: bool = False
+
+
+@dataclass
+class IterationSnapshot:
+    centers: np.ndarray
+    memberships: np.ndarray
+
+
+@dataclass
+class ClusterState:
+    """quant::ClusterState (kmeans.hpp:42-56)."""
+    centers: np.ndarray = None
+    memberships: np.ndarray = None
+    sse_trace: np.ndarray = None
+    iterations: int = 0
+    ndc_total: int = 0
+    repair_count: int = 0
+    history: list = field(default_factory=list)
+    flagged_total: int = 0  # device diagnostic: points replayed in exact FP64
+
+    def ndc_per_point_iter(self, point_count: int) -> float:
+        if point_count == 0 or self.iterations == 0:
+            return 0.0
+        return float(self.ndc_total) / (float(point_count) * float(self.iterations))
+
+
+def check_convergence(sse_prev: float, sse_cur: float, epsilon: float) -> bool:
+    """kmeans.cpp:9-12."""
+    if sse_cur == 0.0:
+        return True
+    return (sse_prev - sse_cur) / sse_cur <= epsilon
+
+
+def _term_struct(term: Termination, record_history: bool) -> cabi.Term:
+    if term.fixed_iterations is not None and term.fixed_iterations <= 0:
+        raise ValueError("clustering: fixed_iterations < 1")  # kmeans.cpp:187-188
+    return cabi.Term(float(term.epsilon), int(term.max_iterations),
+                     int(term.fixed_iterations or 0), 1 if record_history else 0)
+
+
+def wsm_hist(hist: WeightedHistogram, init, options: ClusterOptions = None,
+             ctx: Optional[cabi.Context] = None) -> ClusterState:
+    """quant::wsm (kmeans.hpp:128-129, kmeans.cpp:271-277) over a histogram's
+    count-weighted colours (weights = counts / source_pixel_count)."""
+    return wsm_counts(hist.packed if hist.packed is not None else pack_colors(hist.colors),
+                      hist.counts, hist.source_pixel_count, init, options, ctx)
+
+
+def wsm_counts(colors_packed, counts, P: int, init, options: ClusterOptions = None,
+               ctx: Optional[cabi.Context] = None) -> ClusterState:
+    """Weighted sort-means on packed colours with integer counts (weights = counts/P)."""
+    options = options or ClusterOptions()
+    term = _term_struct(options.term, options.record_history)
+    ctx = ctx or cabi.default_context()
+    colors_packed = np.ascontiguousarray(colors_packed, np.uint32)
+    counts = np.ascontiguousarray(counts, np.uint32)
+    init = np.ascontiguousarray(np.asarray(init, np.float64).reshape(-1, 3))
+    n, k = colors_packed.size, init.shape[0]
+    limit = term.fixed_iterations if term.fixed_iterations > 0 else max(term.max_iterations, 1)
+    centers = np.empty((max(k, 1), 3), np.float64)
+    labels = np.empty(max(n, 1), np.uint32)
+    sse = np.zeros(limit, np.float64)
+    hl = np.empty((limit, n), np.uint32) if options.record_history else None
+    hc = np.empty((limit, max(k, 1), 3), np.float64) if options.record_history else None
+    st = ctx.lloyd_raw(colors_packed, counts, n, P, init if k else np.zeros((1, 3)), k, term,
+                       centers, labels, sse, hl, hc)
+    it = st.iterations
+    hist = []
+    if options.record_history:
+        hist = [IterationSnapshot(hc[i].copy(), hl[i].copy()) for i in range(it)]
+    return ClusterState(centers[:k].copy(), labels[:n].copy(), sse[:it].copy(), it,
+                        int(st.ndc_total), int(st.repair_count), hist, int(st.flagged_total))
+
+
+def wsm(points, weights, init, options: ClusterOptions = None,
+        ctx: Optional[cabi.Context] = None) -> ClusterState:
+    """quant::wsm(points, weights, init, options) for count-weighted substrates.
+
+    The device engine keeps exact integer moments, so the weights must be
+    count / P for integer counts and the points must lie on the 8-bit grid
+    (every substrate run_quantize builds). Other inputs raise ValueError."""
+    pts = np.asarray(points, np.float64).reshape(-1, 3)
+    w = np.asarray(weights, np.float64).reshape(-1)
+    init = np.asarray(init, np.float64).reshape(-1, 3)
+    n, k = pts.shape[0], init.shape[0]
+    if k == 0:
+        raise ValueError("clustering: no initial centers")
+    if n == 0:
+        raise ValueError("clustering: no points")
+    if k > n:
+        raise ValueError(f"clustering: k ({k}) exceeds number of points ({n})")
+    if w.size != n:
+        raise ValueError("clustering: weights/points size mismatch")
+    if not np.all(w > 0.0):
+        raise ValueError("wsm: weights must be positive")
+    if np.any(pts != np.round(pts)) or pts.min() < 0 or pts.max() > 255:
+        raise ValueError("wsm: device engine needs points on the 8-bit colour grid")
+    # recover integer counts: w_i = c_i * (1/P) exactly (histogram.cpp:99-102)
+    wmin = float(w.min())
+    counts, P = None, None
+    for cmin in range(1, 257):
+        cand_p = int(round(cmin / wmin))
+        if cand_p <= 0:
+            continue
+        c = np.round(w * cand_p)
+        if int(c.sum()) == cand_p and np.array_equal(c * (1.0 / float(cand_p)), w):
+            counts, P = c, cand_p
+            break
+    if P is None:
+        raise ValueError("wsm: device engine needs weights of the form count/P")
+    packed = pack_colors(pts.astype(np.uint8))
+    return wsm_counts(packed, np.asarray(counts, np.uint32), P, init, options, ctx)
+
+
+# ---------------------------------------------------------------------------
+# init (init.hpp:17-72)
+
+
+@dataclass
+class SeedConfig:
+    """quant::SeedConfig (init.hpp:17-27), the fields the device initialisers use."""
+    k: int = 8
+    seed: int = 1
+    maximin_weighted_first: bool = True
+
+
+def init_maximin(hist: WeightedHistogram, cfg: SeedConfig,
+                 ctx: Optional[cabi.Context] = None) -> np.ndarray:
+    """quant::init_maximin (init.hpp:40, init.cpp:127-138)."""
+    return _init(cabi.INIT_MAXIMIN, hist, cfg, ctx)
+
+
+def init_kmeanspp(hist: WeightedHistogram, cfg: SeedConfig,
+                  ctx: Optional[cabi.Context] = None) -> np.ndarray:
+    """quant::init_kmeanspp (init.hpp:60, init.cpp:295-314)."""
+    return _init(cabi.INIT_KMEANSPP, hist, cfg, ctx)
+
+
+def _init(kind, hist, cfg, ctx):
+    ctx = ctx or cabi.default_context()
+    k = int(cfg.k)
+    out = np.empty((max(k, 1), 3), np.float64)
+    packed = hist.packed if hist.packed is not None else pack_colors(hist.colors)
+    ctx.init_raw(kind, np.ascontiguousarray(packed, np.uint32),
+                 np.ascontiguousarray(hist.counts, np.uint32), hist.size(),
+                 hist.source_pixel_count, k, int(cfg.seed), out, cfg.maximin_weighted_first)
+    return out[:k].copy()
+
+
+# ---------------------------------------------------------------------------
+# stage 4 (metrics.hpp:14-57)
+
+
+@dataclass
+class MappingResult:
+    """quant::MappingResult (metrics.hpp:14-22)."""
+    indices: np.ndarray     # (P,) uint32 (or uint8 when requested)
+    quantized: np.ndarray   # (H, W, 3) uint8
+    mean_sq_dist: float
+    ndc: int = 0
+
+
+def map_pixels(image, palette, index_bytes: int = 4,
+               ctx: Optional[cabi.Context] = None) -> MappingResult:
+    """quant::map_pixels (metrics.hpp:28, metrics.cpp:15-55)."""
+    ctx = ctx or cabi.default_context()
+    pal = np.ascontiguousarray(np.asarray(palette, np.float64).reshape(-1, 3))
+    arr, w, h = _pixels(image)
+    P = w * h
+    k = pal.shape[0]
+    if k == 0:
+        raise ValueError("map_pixels: empty palette")
+    if P == 0:
+        raise ValueError("map_pixels: empty image")
+    idx = np.empty(P, np.uint8 if index_bytes == 1 else np.uint32)
+    q = np.empty((h, w, 3) if h > 1 or isinstance(image, RawImage) else (P, 3), np.uint8)
+    mse = ctx.map_raw(arr, P, pal, k, idx, index_bytes, q)
+    return MappingResult(idx, q, mse, 0)
+
+
+def mse(a, b) -> float:
+    """metrics.cpp:57-69 (host helper, integer exact)."""
+    a = np.asarray(a, np.int64)
+    b = np.asarray(b, np.int64)
+    if a.shape != b.shape:
+        raise ValueError("mse: image dimensions differ")
+    if a.size == 0:
+        raise ValueError("mse: empty images")
+    return float(((a - b) ** 2).sum()) / float(a.size // 3)
+
+
+def psnr_from_mse(mse_value: float) -> float:
+    """metrics.cpp:71-75."""
+    if mse_value < 0.0:
+        raise ValueError("psnr_from_mse: negative mse")
+    if mse_value == 0.0:
+        return math.inf
+    return 20.0 * math.log10(255.0 / math.sqrt(mse_value))
+
+
+@dataclass
+class QuantReport:
+    """quant::QuantReport (metrics.hpp:37-57) with the frozen CSV/JSON formats
+    of metrics.cpp:96-150."""
+    image: str = ""
+    method: str = ""
+    k_requested: int = 0
+    k_actual: int = 0
+    run: int = 0
+    seed: int = 0
+    sampling: str = "unique"
+    mse: float = 0.0
+    psnr: float = 0.0
+    iterations: int = 0
+    ndc_per_point_iter: float = 0.0
+    time_ms: float = 0.0
+    flags: list = field(default_factory=list)
+
+    @staticmethod
+    def csv_header() -> str:
+        return ("image,method,k,run,seed,sampling,mse,psnr,iterations,ndc_per_point_iter,"
+                "time_ms,actual_k,flags")
+
+    def csv_row(self) -> str:
+        def f(spec, v):
+            return spec % v
+        mse_s = "nan" if math.isnan(self.mse) else f("%.6f", self.mse)
+        if math.isinf(self.psnr):
+            psnr_s = "inf"
+        elif math.isnan(self.psnr):
+            psnr_s = "nan"
+        else:
+            psnr_s = f("%.4f", self.psnr)
+        return ",".join([self.image, self.method, str(self.k_requested), str(self.run),
+                         str(self.seed), self.sampling, mse_s, psnr_s, str(self.iterations),
+                         f("%.4f", self.ndc_per_point_iter), f("%.3f", self.time_ms),
+                         str(self.k_actual), ";".join(self.flags)])
+
+    def to_json(self) -> str:
+        return json.dumps({
+            "image": self.image, "method": self.method, "k": self.k_requested,
+            "actual_k": self.k_actual, "run": self.run, "seed": self.seed,
+            "sampling": self.sampling, "mse": self.mse,
+            "psnr": "inf" if math.isinf(self.psnr) else self.psnr,
+            "iterations": self.iterations, "ndc_per_point_iter": self.ndc_per_point_iter,
+            "time_ms": self.time_ms, "flags": list(self.flags)}, indent=2)
+
+
+# ---------------------------------------------------------------------------
+# pipeline (pipeline.hpp:19-53)
+
+PRECLUSTER_TOKENS = ["mc", "ott", "oct", "wan", "wu", "bs"]
+INIT_TOKENS = ["fgy", "lbg", "mmx", "den", "var", "sff", "kpp"]
+DEVICE_INITS = {"mmx": cabi.INIT_MAXIMIN, "kpp": cabi.INIT_KMEANSPP}
+
+
+@dataclass
+class MethodSpec:
+    """quant::MethodSpec (pipeline.hpp:19-24)."""
+    refine: bool = False
+    base: str = ""
+
+    def token(self) -> str:
+        return "wsm-" + self.base if self.refine else self.base
+
+
+def parse_method(method: str, init: str = "") -> MethodSpec:
+    """pipeline.cpp:20-45 (token grammar and messages)."""
+    spec = MethodSpec()
+    if method == "wsm":
+        spec.refine, spec.base = True, (init or "fgy")
+    elif method.startswith("wsm-"):
+        if init:
+            raise ValueError(f"method '{method}' already names its initializer; drop --init")
+        spec.refine, spec.base = True, method[4:]
+    else:
+        if init:
+            raise ValueError(f"--init only applies to wsm methods, not '{method}'")
+        spec.refine, spec.base = False, method
+    if spec.refine:
+        if spec.base not in INIT_TOKENS and spec.base not in PRECLUSTER_TOKENS:
+            raise ValueError(f"unknown initializer '{spec.base}' "
+                             "(expected fgy|lbg|mmx|den|var|sff|kpp|mc|ott|oct|wan|wu|bs)")
+    elif spec.base not in PRECLUSTER_TOKENS:
+        raise ValueError(f"unknown method '{method}' (expected mc|ott|oct|wan|wu|bs, wsm, or wsm-<init>)")
+    return spec
+
+
+def all_method_tokens() -> list[str]:
+    """pipeline.cpp:47-52."""
+    return PRECLUSTER_TOKENS + ["wsm-" + t for t in INIT_TOKENS] + ["wsm-" + t for t in PRECLUSTER_TOKENS]
+
+
+@dataclass
+class QuantizeConfig:
+    """quant::QuantizeConfig (pipeline.hpp:33-40). ``init_centers`` is this
+    build's hook for initialisers that are outside the device path (e.g. a
+    preclusterer palette for wsm-wu): when given, it seeds the device engine."""
+    method: MethodSpec = field(default_factory=lambda: parse_method("wsm-mmx"))
+    k: int = 8
+    sampling: str = "unique"
+    seed: int = 1
+    term: Termination = field(default_factory=Termination)
+    record_history: bool = False
+    init_centers: Optional[np.ndarray] = None
+    index_bytes: int = 4
+
+
+@dataclass
+class QuantizeResult:
+    """quant::QuantizeResult (pipeline.hpp:42-48)."""
+    palette: np.ndarray
+    mapping: MappingResult
+    state: ClusterState
+    report: QuantReport
+    substrate_points: int = 0
+    stage_ms: dict = field(default_factory=dict)
+
+
+def run_quantize(image, config: QuantizeConfig, ctx: Optional[cabi.Context] = None) -> QuantizeResult:
+    """quant::run_quantize (pipeline.hpp:53, pipeline.cpp:81-164) for the
+    device path: sampling 'unique', refined methods wsm-mmx / wsm-kpp, or any
+    wsm-<x> whose initial centres are supplied in ``config.init_centers``."""
+    ctx = ctx or cabi.default_context()
+    arr, w, h = _pixels(image)
+    P = w * h
+    if P == 0:
+        raise ValueError("run_quantize: empty image")
+    if config.k < 1:
+        raise ValueError("run_quantize: k must be at least 1")
+    if config.sampling != "unique":
+        raise ValueError("run_quantize: the device path implements sampling 'unique' only")
+    if not config.method.refine:
+        raise ValueError("run_quantize: standalone preclusterers are outside the device path")
+    k = int(config.k)
+    if config.init_centers is not None:
+        kind = cabi.INIT_GIVEN
+        init = np.ascontiguousarray(np.asarray(config.init_centers, np.float64).reshape(-1, 3))
+        if init.shape[0] != k:
+            raise ValueError("run_quantize: init_centers must have k rows")
+    elif config.method.base in DEVICE_INITS:
+        kind = DEVICE_INITS[config.method.base]
+        init = None
+    else:
+        raise ValueError(f"run_quantize: initializer '{config.method.base}' is outside the device "
+                         "path; pass config.init_centers")
+    term = _term_struct(config.term, False)
+    cfg = cabi.QuantizeCfg(kind, k, int(config.seed), term, int(config.index_bytes))
+    limit = term.fixed_iterations if term.fixed_iterations > 0 else term.max_iterations
+    palette = np.empty((k, 3), np.float64)
+    cap = min(P, 1 << 24)
+    labels = np.empty(cap, np.uint32)
+    sse = np.zeros(limit, np.float64)
+    idx = np.empty(P, np.uint8 if config.index_bytes == 1 else np.uint32)
+    q = np.empty((h, w, 3), np.uint8)
+    t0 = time.perf_counter()
+    st = ctx.quantize_raw(arr, P, cfg, init, palette, labels, sse, idx, q)
+    t1 = time.perf_counter()
+    n = int(st.n_unique)
+    it = st.lloyd.iterations
+    state = ClusterState(palette.copy(), labels[:n].copy(), sse[:it].copy(), it,
+                         int(st.lloyd.ndc_total), int(st.lloyd.repair_count), [],
+                         int(st.lloyd.flagged_total))
+    mapping = MappingResult(idx, q, float(st.mean_sq_dist), 0)
+    rep = QuantReport(method=config.method.token(), k_requested=k, k_actual=k,
+                      seed=int(config.seed), sampling=config.sampling, mse=mapping.mean_sq_dist,
+                      psnr=psnr_from_mse(mapping.mean_sq_dist), iterations=it,
+                      ndc_per_point_iter=state.ndc_per_point_iter(n),
+                      time_ms=(t1 - t0) * 1e3)
+    if state.repair_count > 0:
+        rep.flags.append(f"repairs:{state.repair_count}")
+    return QuantizeResult(palette, mapping, state, rep, n,
+                          dict(histogram=st.ms_histogram, init=st.ms_init, lloyd=st.ms_lloyd,
+                               map=st.ms_map))
