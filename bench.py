@@ -1,0 +1,423 @@
+"""Benchmark: quantized MPixel/s (and Lloyd colour-centre distances/s) of the
+B200-native hot path on BASELINE.json's configuration.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config cfg2|cfg1|cfg3|cfg3k64|cfg4|cfg5]
+
+A step is one pass of the hot path (histogram -> init -> weighted Lloyd ->
+mapping + MSE, i.e. quant::run_quantize) over one batch of synthetic input.
+Default workload: BASELINE.json configs[1] (512x512, K=256, k-means++), the
+configuration the metric ("... at K=256") is quoted on that fits one GPU.
+
+Multi-GPU (torchrun, one rank per GPU): single-image configs run one
+independent replica per rank (the path does not shard below ~1M colours;
+"replicas only"); cfg4 shards its 64 images across ranks. Timing: W untimed
+warm-up steps, then K steps, each bracketed by CUDA events on the launching
+stream with an L2 flush (write of a 512 MiB buffer) between steps outside the
+timed events; the per-rank device time is max-reduced over ranks.
+
+--impl reference times the reference's own CPU implementation (the reference
+sources compiled in place: oracle/_ref/libquantref.so, through its public
+run_quantize / stage API) on this box's host cores, one image per host thread.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Lloyd color-center distances/s and quantized MPixel/s at K=256, 1-8 B200"
+UNIT = "MPixel/s"
+
+
+def env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            return json.load(f), "measured"
+    return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (FileNotFoundError, OSError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# reference arm (CPU)
+
+def ref_pipeline_once(R, img, cfg, k, kind):
+    h, w = img.shape[:2]
+    t0 = time.perf_counter()
+    out = R.time_pipeline(img, w, h, kind, k, cfg.seed, fixed_it=cfg.fixed_iterations)
+    t1 = time.perf_counter()
+    return t1 - t0, out
+
+
+def run_reference(args, cfg):
+    from concurrent.futures import ThreadPoolExecutor
+    from oracle.pyoracle import RefLib, have_ref, Oracle
+    rank = env_int("RANK", 0)
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    if have_ref():
+        R = RefLib()
+        kind = "reference"
+    else:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        return 0
+    imgs = [cfg.image(i % max(cfg.images, 1)) for i in range(threads)]
+    ks = [cfg.k_for(i) for i in range(threads)]
+    P = imgs[0].shape[0] * imgs[0].shape[1]
+
+    def one(i):
+        return ref_pipeline_once(R, imgs[i], cfg, ks[i], cfg.init)
+
+    times, dist, lloyd_s = [], 0.0, 0.0
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        for s in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            res = list(ex.map(one, range(threads)))
+            t1 = time.perf_counter()
+            if s >= args.warmup:
+                times.append(t1 - t0)
+                for (_, o), k in zip(res, ks):
+                    dist += o["n_unique"] * k * o["iterations"]
+                    lloyd_s += o["stage_s"][2]
+    step = sum(times) / len(times)
+    value = threads * P / step / 1e6
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": step * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg.name, "image": f"{cfg.width}x{cfg.height}", "k": cfg.k,
+                   "init": cfg.init, "images_per_step": threads,
+                   "note": "reference sources compiled -O3 -DNDEBUG (oracle/Makefile), one image per host thread"},
+        "lloyd_distances_per_s": dist / lloyd_s * threads if lloyd_s > 0 else None,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+                         "sample": f"{threads} concurrent {cfg.name} run_quantize pipelines per step"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def cpu_baseline(cfg, budget_s: float):
+    """Reference pipeline (oracle/_ref) on 1 core, bounded sample."""
+    try:
+        from oracle.pyoracle import RefLib, have_ref, Oracle, UPDATE_REFERENCE
+    except Exception as e:  # pragma: no cover
+        return {"value": None, "unit": UNIT, "cores": 1, "kind": "unavailable", "sample": str(e)}
+    img = cfg.image(0)
+    h, w = img.shape[:2]
+    P = w * h
+    k = cfg.k_for(0)
+    if not have_ref():
+        return {"value": None, "unit": UNIT, "cores": 1, "kind": "unavailable",
+                "sample": "oracle/_ref not built"}
+    R = RefLib()
+    runs, tot, st_sum = 0, 0.0, np.zeros(4)
+    t_start = time.perf_counter()
+    while True:
+        dt, out = ref_pipeline_once(R, img, cfg, k, cfg.init)
+        runs += 1
+        tot += dt
+        st_sum += out["stage_s"]
+        if time.perf_counter() - t_start >= budget_s or runs >= 50:
+            break
+    return {"value": runs * P / tot / 1e6, "unit": UNIT, "cores": 1, "kind": "reference",
+            "sample": f"{runs} full {cfg.name} pipelines ({w}x{h}, K={k}, {cfg.init}) in {tot:.1f} s",
+            "stage_s_mean": (st_sum / runs).round(6).tolist(),
+            "lloyd_distances_per_s": (out["n_unique"] * k * out["iterations"]) / out["stage_s"][2]}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+    from paper_1101_0395_b200 import cabi, quant
+
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    local = env_int("LOCAL_RANK", 0)
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+    ctx = cabi.Context(local)
+    ctx.set_stream(stream.cuda_stream)
+
+    # work owned by this rank
+    if cfg.images > 1:
+        my = list(range(rank, cfg.images, world))
+    else:
+        my = [0]
+    imgs = [cfg.image(i) for i in my]
+    ks = [cfg.k_for(i) for i in my]
+    P_list = [im.shape[0] * im.shape[1] for im in imgs]
+    kind = cabi.INIT_KMEANSPP if cfg.init == "kpp" else cabi.INIT_MAXIMIN
+
+    def mkcfg(k):
+        term = cabi.Term(1e-3, 100, cfg.fixed_iterations, 0)
+        return cabi.QuantizeCfg(kind, k, cfg.seed, term, 4)
+
+    d_imgs = [torch.from_numpy(im).to(dev) for im in imgs]
+    d_idx = [torch.empty(P, dtype=torch.int32, device=dev) for P in P_list]
+    d_q = [torch.empty((P, 3), dtype=torch.uint8, device=dev) for P in P_list]
+    d_pal = [torch.empty((k, 3), dtype=torch.float64, device=dev) for k in ks]
+    sse = np.zeros(128)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+
+    def step_device():
+        stats = []
+        for i in range(len(imgs)):
+            st = ctx.quantize_raw(d_imgs[i], P_list[i], mkcfg(ks[i]), None, d_pal[i], None, sse,
+                                  d_idx[i], d_q[i])
+            stats.append(st)
+        return stats
+
+    # warm-up
+    for _ in range(args.warmup):
+        step_device()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    ctx.set_profiling(True)
+    ctx.read_profile(reset=True)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    step_ms, all_stats = [], []
+    launches0 = ctx.launches
+    with ClockSampler(local) as clk:
+        for s in range(args.steps):
+            flush.fill_(s & 255)  # L2 flush outside the timed events
+            torch.cuda.synchronize()
+            ev0.record(stream)
+            st = step_device()
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            step_ms.append(ev0.elapsed_time(ev1))
+            all_stats.append(st)
+    gpu_launches = ctx.launches - launches0
+    prof = ctx.read_profile(reset=True)
+    ctx.set_profiling(False)
+    clocks = clk.summary()
+
+    total_ms = float(sum(step_ms))
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+    total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    pixels_per_step_all = cfg.images * P_list[0] * (1 if cfg.images > 1 else world)
+    value = pixels_per_step_all / (ms_per_step / 1e3) / 1e6
+
+    # Lloyd distances/s (full-sweep equivalent N'.K.iters over Lloyd device time)
+    dist_n = sum(s.n_unique * k * s.lloyd.iterations for st in all_stats for s, k in zip(st, ks))
+    lloyd_ms = sum(s.ms_lloyd for st in all_stats for s in st)
+    lloyd_rate = dist_n / (lloyd_ms / 1e3) if lloyd_ms > 0 else None
+    if world > 1:
+        v = torch.tensor([lloyd_rate or 0.0], dtype=torch.float64, device=dev)
+        dist.all_reduce(v)
+        lloyd_rate = float(v.item())
+
+    # roofline of the dominant kernel: the Lloyd sweep (FP32 pipe)
+    peaks, peak_kind = measured_peaks()
+    sms = torch.cuda.get_device_properties(local).multi_processor_count
+    fp32_peak = sms * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+    sweep_ms = prof.ms[cabi.PROF_SWEEP]
+    sweep_launch = max(int(prof.launches[cabi.PROF_SWEEP]), 1)
+    sweep_units = prof.units[cabi.PROF_SWEEP]
+    achieved = 8.0 * sweep_units / (sweep_ms / 1e3) / 1e12 if sweep_ms > 0 else None
+    stage_share = {}
+    names = ["sweep", "map_sweep", "histogram", "pixel_map", "init", "replay", "ndc"]
+    for i, nm in enumerate(names):
+        stage_share[nm] = {"ms_per_step": prof.ms[i] / args.steps,
+                           "launches_per_step": prof.launches[i] / args.steps}
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", f"ncu_traffic_{cfg.name}.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            traffic = json.load(f).get("sweep_dram_bytes_per_launch")
+    roofline = {
+        "bound": "fp32", "kernel": "sweep_kernel (Lloyd assignment)",
+        "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
+        "frac": (achieved / fp32_peak) if achieved else None, "traffic": traffic,
+        "peak_source": f"{sms} SMs x 128 FP32 lanes x 2 x sm_max_mhz ({peak_kind} MEASURED_PEAKS.json)",
+        "algorithmic_unit": "8 FLOP per (unique colour, centre) pair, full-sweep equivalent",
+        "avg_launch_ms": sweep_ms / sweep_launch,
+        "launch_share_of_step": (sweep_ms / args.steps) / ms_per_step,
+    }
+    hist_ms = prof.ms[cabi.PROF_HIST]
+    pix_ms = prof.ms[cabi.PROF_PIXEL]
+    hbm = peaks.get("hbm_gbs", 6545.6)
+    n_unique = all_stats[-1][0].n_unique
+    byte_kernels = {
+        "histogram": {"achieved_gbs": (prof.units[cabi.PROF_HIST] + 8.0 * n_unique * args.steps * len(imgs)) / (hist_ms / 1e3) / 1e9 if hist_ms else None,
+                      "peak_gbs": hbm},
+        "pixel_map": {"achieved_gbs": prof.units[cabi.PROF_PIXEL] / (pix_ms / 1e3) / 1e9 if pix_ms else None,
+                      "peak_gbs": hbm},
+    }
+
+    # end-to-end through the C-ABI with pinned HOST buffers (H2D + D2H inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        h_imgs = [torch.from_numpy(im).pin_memory() for im in imgs]
+        h_idx = [torch.empty(P, dtype=torch.int32).pin_memory() for P in P_list]
+        h_q = [torch.empty((P, 3), dtype=torch.uint8).pin_memory() for P in P_list]
+        h_pal = [np.empty((k, 3)) for k in ks]
+        for _ in range(max(1, args.warmup // 2)):
+            for i in range(len(imgs)):
+                ctx.quantize_raw(h_imgs[i], P_list[i], mkcfg(ks[i]), None, h_pal[i], None, sse, h_idx[i], h_q[i])
+        e_ms = []
+        for s in range(args.steps):
+            flush.fill_(s & 255)
+            torch.cuda.synchronize()
+            ev0.record(stream)
+            for i in range(len(imgs)):
+                ctx.quantize_raw(h_imgs[i], P_list[i], mkcfg(ks[i]), None, h_pal[i], None, sse,
+                                 h_idx[i], h_q[i])
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            e_ms.append(ev0.elapsed_time(ev1))
+        et = torch.tensor([sum(e_ms)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e_step = float(et.item()) / args.steps
+        h2d = sum(3 * P for P in P_list)
+        d2h = sum(7 * P + 24 * k + 8 * 100 for P, k in zip(P_list, ks))
+        e2e = {"value": pixels_per_step_all / (e_step / 1e3) / 1e6, "unit": UNIT,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e_step,
+               "index_layout": "uint32 per pixel (MappingResult::indices)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, args.cpu_seconds)
+
+    if rank == 0:
+        st0 = all_stats[-1][0]
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": cfg.name, "image": f"{cfg.width}x{cfg.height}",
+                       "images_per_rank": len(imgs), "k": cfg.k if not cfg.k_cycle else list(cfg.k_cycle),
+                       "init": cfg.init, "fixed_iterations": cfg.fixed_iterations or None,
+                       "parallelism": f"replicas x{world}" if cfg.images == 1 else f"images sharded over {world}",
+                       "l2": "flushed (512 MiB write) between timed steps",
+                       "arithmetic": "FP32 packed sweep + exact FP64 replay of near-ties + int64 moments",
+                       "index_layout": "uint32 per pixel"},
+            "lloyd_distances_per_s": lloyd_rate,
+            "n_unique": int(st0.n_unique), "iterations": int(st0.lloyd.iterations),
+            "flagged_per_step": int(st0.lloyd.flagged_total),
+            "stage_ms_last_step": {"histogram": st0.ms_histogram, "init": st0.ms_init,
+                                   "lloyd": st0.ms_lloyd, "map": st0.ms_map},
+            "kernels": stage_share, "byte_kernels": byte_kernels,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": int(gpu_launches), "clocks": clocks,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    ctx.close()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    from paper_1101_0395_b200.synth import CONFIGS
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+    return run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

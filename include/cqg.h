@@ -113,6 +113,7 @@ const char *cqg_version(void);
 #define CQG_PROF_PIXEL 3     /* pixel mapping kernel (units: bytes moved) */
 #define CQG_PROF_INIT 4      /* initialiser kernel (units: N' x (K-1) distance updates) */
 #define CQG_PROF_REPLAY 5    /* exact FP64 replays (units: queued points) */
+#define CQG_PROF_NDC 6       /* per-point distance-count (NDC) pass (units: points) */
 #define CQG_PROF_N 8
 typedef struct {
     double ms[CQG_PROF_N];

@@ -36,7 +36,7 @@ EXPORTS = (
     "cqg_map", "cqg_quantize", "cqg_set_profiling", "cqg_read_profile",
 )
 
-PROF_SWEEP, PROF_MAPSWEEP, PROF_HIST, PROF_PIXEL, PROF_INIT, PROF_REPLAY = range(6)
+PROF_SWEEP, PROF_MAPSWEEP, PROF_HIST, PROF_PIXEL, PROF_INIT, PROF_REPLAY, PROF_NDC = range(7)
 
 
 class Term(C.Structure):

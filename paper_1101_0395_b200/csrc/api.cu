@@ -5,6 +5,7 @@
 //   histogram.cpp:70, init.cpp:15-19, kmeans.cpp:175-188 and :275,
 //   metrics.cpp:16-17, pipeline.cpp:82-83.
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -198,6 +199,8 @@ cqg_ctx *cqg_create(int device) {
         ctx->num_sms = prop.multiProcessorCount;
         CQG_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
         ctx->own_stream = true;
+        const char *ng = getenv("CQG_NO_GRAPH");
+        ctx->use_graphs = !(ng && ng[0] == '1');
     });
     if (rc != CQG_OK) {
         delete ctx;
@@ -210,6 +213,7 @@ void cqg_destroy(cqg_ctx *ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
+    release_graphs(ctx);
     DevBuf *bufs[] = {&ctx->tab, &ctx->list, &ctx->bitmap, &ctx->wordpref, &ctx->scal, &ctx->img,
                       &ctx->colors, &ctx->counts, &ctx->first, &ctx->labels, &ctx->cen, &ctx->fcen,
                       &ctx->dtab, &ctx->dsorted, &ctx->order, &ctx->mom, &ctx->queue, &ctx->ndc,
@@ -237,6 +241,7 @@ int cqg_set_stream(cqg_ctx *ctx, void *stream) {
             cudaStreamSynchronize(ctx->stream);
             cudaStreamDestroy(ctx->stream);
         }
+        release_graphs(ctx);
         ctx->stream = static_cast<cudaStream_t>(stream);
         ctx->own_stream = false;
     });

@@ -127,6 +127,11 @@ struct cqg_ctx {
     cqg::DevBuf mind2, initpart, initsel, unit_draws;
     cqg::HostBuf pinned;   // status readback and small results
 
+    // cached CUDA graph of the Lloyd WHILE loop (lloyd.cu)
+    bool use_graphs = true;
+    cudaGraphExec_t loop_exec = nullptr;
+    cudaGraph_t loop_graph = nullptr;
+    std::vector<uint64_t> loop_key;
     // kernel-level profiling (cqg_set_profiling)
     bool prof_on = false;
     std::vector<cudaEvent_t> ev_pool;
@@ -185,6 +190,7 @@ bool is_device_ptr(const void *p);
 int prof_begin(cqg_ctx *ctx);
 void prof_end(cqg_ctx *ctx, int cat, int begin, double units);
 void launched(cqg_ctx *ctx, int n = 1);
+void release_graphs(cqg_ctx *ctx);
 // copy `bytes` from user pointer (host or device) into a device buffer and
 // return a device pointer that holds the data (the user pointer itself when
 // it is already device memory).

@@ -1,21 +1,30 @@
 // init.cu -- maximin and k-means++ initialisers on the device, bit-exact with
 // the reference (src/init.cpp:37-52, 127-138, 295-314; rng.hpp:43-54).
 //
-// Centres are histogram colours, so every distance is an exact integer and
-// min-distances are kept as uint32. One persistent cooperative kernel runs all
-// K rounds; each block owns a contiguous index range so block partials are in
-// histogram order.
+// Centres are histogram colours, so every distance is an exact integer; the
+// running min-distances are uint32. One persistent cooperative kernel runs all
+// K rounds with ONE grid barrier per round:
 //
-//  maximin round:   mind2 = min(mind2, d2(x, c_last)); argmax (lowest index on
-//                   ties, init.cpp:43-46) via a packed (mind2, ~index) u64 max.
-//  weighted draw:   masses m_i = fl(fl(count_i * (1/P)) * mind2_i) exactly as the
-//                   reference forms them; their sum is taken EXACTLY in 128-bit
-//                   fixed point (2^-88 units), the draw u = fl(unit * total) is
-//                   located by a prefix search, and the decision is accepted
-//                   only when u lies farther than a rigorous bound on the
-//                   reference's sequential-FP64 rounding from every prefix
-//                   boundary; otherwise one thread replays the reference's
-//                   sequential weighted_draw in FP64 (never observed; counted).
+//   update   block b owns a contiguous index range (segments of 1024 points);
+//            mind2 = min(mind2, d2(x, c_last)) into a ping-pong buffer, plus
+//            either the packed (mind2, ~index) maximum (maximin) or the exact
+//            mass sums per segment and per block (k-means++).
+//   barrier  grid.sync()
+//   select   every block redundantly finds the same winner:
+//            maximin  warp max over block partials (lowest index on ties,
+//                     init.cpp:43-46);
+//            draw     masses m_i = fl(fl(count_i * (1/P)) * mind2_i), formed as
+//                     the reference forms them, summed EXACTLY in 128-bit fixed
+//                     point (2^-88 units). u = fl(unit * total) is located by
+//                     warp scans over block sums, then segment sums, then a
+//                     block scan inside the 1024-point segment.
+//            When P is a power of two every mass is an integer multiple of 1/P
+//            and all prefix sums stay below 2^53/P, so the reference's
+//            sequential FP64 sums are exact and the located index IS the
+//            reference's. Otherwise the decision is accepted only when u is
+//            farther than a rigorous bound on the sequential rounding from
+//            both neighbouring prefix sums, and one thread replays the
+//            reference's sequential weighted_draw when it is not (counted).
 #include <cooperative_groups.h>
 
 #include <random>
@@ -28,8 +37,10 @@ namespace cqg {
 namespace {
 
 typedef unsigned __int128 u128;
-constexpr int kFix = 88;     // fixed-point fraction bits
+constexpr int kFix = 88;        // fixed-point fraction bits
 constexpr int kInitThreads = 256;
+constexpr int kSeg = 1024;      // points per segment (4 per thread)
+constexpr uint32_t kWeightsOnly = 0xFFFFFFFFu;
 
 struct InitArgs {
     const uint32_t *colors;
@@ -37,29 +48,28 @@ struct InitArgs {
     uint64_t n;
     double inv;
     int K;
-    int kind;           // 0 maximin, 1 k-means++
-    int weighted_first; // maximin only
+    int kind;            // 0 maximin, 1 k-means++
+    int weighted_first;  // maximin only
+    int exact_sums;      // P is a power of two: sequential FP64 sums are exact
     uint64_t first_index;
-    const double *nu;   // unit draws, in consumption order
-    uint32_t *mind2;
-    u128 *parts;                 // 2 x gridDim
-    unsigned long long *mparts;  // 2 x gridDim
-    unsigned long long *result;  // [0] chosen index of the current draw, [1] inexact flag
+    uint64_t chunk;      // points per block (multiple of kSeg)
+    const double *nu;    // unit draws, in consumption order
+    uint32_t *md;        // 2 x n ping-pong min distances
+    u128 *parts;         // 2 x gridDim block mass sums
+    u128 *segs;          // 2 x nseg segment mass sums
+    unsigned long long *mparts; // 2 x gridDim maximin keys
+    unsigned long long *result; // [2] fallback result slots
     unsigned long long *fallbacks;
     double *cen;
 };
 
-__device__ __forceinline__ u128 to_fixed(double m, int *inexact) {
+__device__ __forceinline__ u128 to_fixed(double m) {
     if (m == 0.0) return 0;
     const unsigned long long bits = (unsigned long long)__double_as_longlong(m);
     const int e = (int)((bits >> 52) & 0x7FF);
     const unsigned long long mant = (bits & ((1ull << 52) - 1)) | (1ull << 52);
-    const int s = e - 1075 + kFix;
-    if (s < 0) {
-        *inexact = 1;
-        return (u128)(mant >> (-s > 63 ? 63 : -s));
-    }
-    return ((u128)mant) << s;
+    const int s = e - 1075 + kFix; // >= 0 for m >= 2^-36, i.e. P < 2^32
+    return s >= 0 ? ((u128)mant) << s : (u128)(mant >> (-s > 63 ? 63 : -s));
 }
 
 __device__ __forceinline__ u128 floor_fixed(double u) {
@@ -82,10 +92,10 @@ __device__ __forceinline__ uint32_t d2_int(uint32_t a, uint32_t b) {
     return (uint32_t)(dr * dr + dg * dg + db * db);
 }
 
-// mass of point i (mind2 == 0xFFFFFFFF means "weights only")
+// the reference's mass: weights[i] (* mind2[i])
 __device__ __forceinline__ double mass_of(const InitArgs &a, uint64_t i, uint32_t md) {
     const double w = __dmul_rn((double)a.counts[i], a.inv);
-    return md == 0xFFFFFFFFu ? w : __dmul_rn(w, (double)md);
+    return md == kWeightsOnly ? w : __dmul_rn(w, (double)md);
 }
 
 __device__ __forceinline__ u128 shfl_u128(u128 v, int src) {
@@ -102,28 +112,122 @@ __device__ __forceinline__ u128 shfl_up_u128(u128 v, int d) {
     return ((u128)hi << 64) | lo;
 }
 
-// block-wide sum (all threads get the result)
-__device__ u128 block_sum_u128(u128 v, u128 *s_w) {
-    for (int o = 16; o; o >>= 1) v += shfl_u128(v, (threadIdx.x & 31) ^ o);
+// ---- mass arithmetic -----------------------------------------------------
+// Exact: P is a power of two, masses are the integers count*mind2 (the
+//        reference's FP64 masses times P, all partial sums < 2^53), u*P is
+//        fl(unit * T) exactly; no rounding ambiguity exists.
+// Fixed: masses are the reference's FP64 masses in 2^-88 fixed point (u128);
+//        decisions closer than a rigorous bound to a prefix boundary replay the
+//        reference sequentially.
+struct ExactMass {
+    typedef unsigned long long T;
+    static __device__ __forceinline__ T mass(const InitArgs &a, uint64_t i, uint32_t md) {
+        const T c = (T)a.counts[i];
+        return md == kWeightsOnly ? c : c * (T)md;
+    }
+    static __device__ __forceinline__ T target(double nu, T total) {
+        return (T)floor(__dmul_rn(nu, (double)total)); // u * P, exact scaling
+    }
+    static __device__ __forceinline__ T shfl(T v, int src) { return __shfl_sync(0xffffffffu, v, src); }
+    static __device__ __forceinline__ T shfl_up(T v, int d) { return __shfl_up_sync(0xffffffffu, v, d); }
+    static __device__ __forceinline__ T bound(uint64_t, T) { return 0; }
+    static constexpr bool exact = true;
+};
+
+struct FixedMass {
+    typedef u128 T;
+    static __device__ __forceinline__ T mass(const InitArgs &a, uint64_t i, uint32_t md) {
+        return to_fixed(mass_of(a, i, md));
+    }
+    static __device__ __forceinline__ T target(double nu, T total) {
+        return floor_fixed(__dmul_rn(nu, fixed_to_double(total)));
+    }
+    static __device__ __forceinline__ T shfl(T v, int src) { return shfl_u128(v, src); }
+    static __device__ __forceinline__ T shfl_up(T v, int d) { return shfl_up_u128(v, d); }
+    // |reference prefix (or u) - exact| <= (n+4) * 2^-52 * T, doubled
+    static __device__ __forceinline__ T bound(uint64_t n, T total) {
+        return (u128)2 * (u128)(n + 4) * ((total >> 52) + 1) + 2;
+    }
+    static constexpr bool exact = false;
+};
+
+template <class M>
+__device__ __forceinline__ typename M::T warp_incl(typename M::T v) {
+    const int lane = threadIdx.x & 31;
+    for (int o = 1; o < 32; o <<= 1) {
+        const typename M::T t = M::shfl_up(v, o);
+        if (lane >= o) v += t;
+    }
+    return v;
+}
+
+// Warp-cooperative: arr[0..cnt) held in registers (lane l owns the contiguous
+// run [l*R, l*R+R)). Returns the first j whose inclusive prefix exceeds U
+// (cnt if none), the exclusive prefix before it, and the total. When
+// want_total_first, U is computed from the total by `target` first.
+template <class M>
+__device__ int warp_locate(const typename M::T *arr, int cnt, bool from_total, double nu,
+                           typename M::T &U, typename M::T *before, typename M::T *total) {
+    typedef typename M::T T;
+    constexpr int RMAX = 12;
+    const int lane = threadIdx.x & 31;
+    const int R = (cnt + 31) / 32;
+    T v[RMAX];
+    T loc = 0;
+#pragma unroll
+    for (int r = 0; r < RMAX; ++r) {
+        const int j = lane * R + r;
+        v[r] = (r < R && j < cnt) ? arr[j] : (T)0;
+        loc += v[r];
+    }
+    const T incl = warp_incl<M>(loc);
+    const T tot = M::shfl(incl, 31);
+    if (from_total) U = M::target(nu, tot);
+    const T excl = incl - loc;
+    const unsigned m = __ballot_sync(0xffffffffu, incl > U);
+    int found = cnt;
+    T fb = 0;
+    if (m) {
+        const int l = __ffs(m) - 1;
+        if (lane == l) {
+            T run = excl;
+#pragma unroll
+            for (int r = 0; r < RMAX; ++r) {
+                if (r < R && found == cnt && run + v[r] > U) {
+                    found = lane * R + r;
+                    fb = run;
+                }
+                run += v[r];
+            }
+        }
+        found = __shfl_sync(0xffffffffu, found, l);
+        fb = M::shfl(fb, l);
+    }
+    *before = fb;
+    *total = tot;
+    return found;
+}
+
+template <class M>
+__device__ typename M::T block_sum(typename M::T v, typename M::T *s_w) {
+    typedef typename M::T T;
+    for (int o = 16; o; o >>= 1) v += M::shfl(v, (threadIdx.x & 31) ^ o);
     if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = v;
     __syncthreads();
-    u128 t = 0;
+    T t = 0;
     for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += s_w[i];
     __syncthreads();
     return t;
 }
 
-// block-wide exclusive scan; *total receives the block total
-__device__ u128 block_excl_u128(u128 v, u128 *s_w, u128 *total) {
+template <class M>
+__device__ typename M::T block_excl(typename M::T v, typename M::T *s_w, typename M::T *total) {
+    typedef typename M::T T;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    u128 incl = v;
-    for (int o = 1; o < 32; o <<= 1) {
-        const u128 t = shfl_up_u128(incl, o);
-        if (lane >= o) incl += t;
-    }
+    const T incl = warp_incl<M>(v);
     if (lane == 31) s_w[wid] = incl;
     __syncthreads();
-    u128 off = 0, tot = 0;
+    T off = 0, tot = 0;
     for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
         if (i < wid) off += s_w[i];
         tot += s_w[i];
@@ -133,152 +237,169 @@ __device__ u128 block_excl_u128(u128 v, u128 *s_w, u128 *total) {
     return off + incl - v;
 }
 
-// Exact replay of rng.hpp:43-54 (one thread). Used only when the fast path
-// cannot certify its decision.
-__device__ uint64_t sequential_draw(const InitArgs &a, double nu, int weights_only) {
+// Reference rng.hpp:43-54 replayed sequentially in FP64 (one thread).
+__device__ uint64_t sequential_draw(const InitArgs &a, const uint32_t *md, double nu, int weights_only) {
     double total = 0.0;
-    for (uint64_t i = 0; i < a.n; ++i) total = __dadd_rn(total, mass_of(a, i, weights_only ? 0xFFFFFFFFu : a.mind2[i]));
+    for (uint64_t i = 0; i < a.n; ++i) total = __dadd_rn(total, mass_of(a, i, weights_only ? kWeightsOnly : md[i]));
     const double u = __dmul_rn(nu, total);
     double acc = 0.0;
     for (uint64_t i = 0; i + 1 < a.n; ++i) {
-        acc = __dadd_rn(acc, mass_of(a, i, weights_only ? 0xFFFFFFFFu : a.mind2[i]));
+        acc = __dadd_rn(acc, mass_of(a, i, weights_only ? kWeightsOnly : md[i]));
         if (u < acc) return i;
     }
     return a.n - 1;
 }
 
-// Weighted draw over the current masses. Phase A (block sums) must already be
-// in parts[par * gridDim.x + b]. Returns the chosen index in every block.
-__device__ uint64_t draw(const InitArgs &a, cg::grid_group &grid, int par, double nu, int weights_only,
-                         uint64_t lo, uint64_t hi, u128 *s_w, unsigned long long *s_res) {
-    const u128 *parts = a.parts + (size_t)par * gridDim.x;
-    // every block: total, u, target block
-    __shared__ u128 s_before;
-    __shared__ int s_tblock;
-    __shared__ u128 s_U, s_T;
-    if (threadIdx.x == 0) {
-        u128 T = 0;
-        for (unsigned b = 0; b < gridDim.x; ++b) T += parts[b];
-        const double u = __dmul_rn(nu, fixed_to_double(T));
-        const u128 U = floor_fixed(u);
-        u128 run = 0;
-        int tb = -1;
-        u128 before = 0;
-        for (unsigned b = 0; b < gridDim.x; ++b) {
-            if (run + parts[b] > U) {
-                tb = (int)b;
-                before = run;
-                break;
-            }
-            run += parts[b];
-        }
-        s_tblock = tb;
-        s_before = before;
-        s_U = U;
-        s_T = T;
-    }
-    __syncthreads();
-    const int tb = s_tblock;
-    const u128 U = s_U, T = s_T;
-    // rigorous bound on |reference prefix / u - exact| (units 2^-88), doubled
-    const u128 B2 = (u128)2 * (u128)(a.n + 4) * ((T >> 52) + 1) + 2;
-    // the block holding the crossing (or the last block if u >= total) searches
-    const int searcher = tb >= 0 ? tb : (int)gridDim.x - 1;
-    if ((int)blockIdx.x == searcher) {
-        __shared__ unsigned long long s_found;
-        __shared__ u128 s_prevE, s_E;
-        if (threadIdx.x == 0) s_found = ~0ull;
-        __syncthreads();
-        int inexact = 0;
-        if (tb >= 0) {
-            u128 run = s_before;
-            for (uint64_t base = lo; base < hi; base += 8ull * blockDim.x) {
-                u128 m[8];
-                u128 loc = 0;
+// Update pass over this block's range: new min distances (unless weights_only)
+// and mass sums per segment and per block.
+template <class M>
+__device__ void update_masses(const InitArgs &a, int par, int weights_only, int first_round, uint32_t clast,
+                              const uint32_t *md_in, uint32_t *md_out, uint64_t lo, uint64_t hi,
+                              typename M::T *s_w) {
+    typedef typename M::T T;
+    T *segs = reinterpret_cast<T *>(a.segs) + (size_t)par * ((a.n + kSeg - 1) / kSeg);
+    T *parts = reinterpret_cast<T *>(a.parts) + (size_t)par * gridDim.x;
+    T blk = 0;
+    for (uint64_t s0 = lo; s0 < hi; s0 += kSeg) {
+        T loc = 0;
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const uint64_t i = base + 8ull * threadIdx.x + j;
-                    m[j] = i < hi ? to_fixed(mass_of(a, i, weights_only ? 0xFFFFFFFFu : a.mind2[i]), &inexact) : 0;
-                    loc += m[j];
+        for (int j = 0; j < kSeg / kInitThreads; ++j) {
+            const uint64_t i = s0 + threadIdx.x + (uint64_t)j * kInitThreads;
+            if (i < hi) {
+                uint32_t m;
+                if (weights_only) {
+                    m = kWeightsOnly;
+                } else {
+                    const uint32_t d = d2_int(__ldg(a.colors + i), clast);
+                    m = first_round ? d : min(md_in[i], d);
+                    md_out[i] = m;
                 }
-                u128 btot;
-                const u128 start = run + block_excl_u128(loc, s_w, &btot);
-                if (start <= U && start + loc > U) {
-                    u128 acc = start;
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        const u128 nxt = acc + m[j];
-                        if (nxt > U) {
-                            s_found = base + 8ull * threadIdx.x + j;
-                            s_prevE = acc;
-                            s_E = nxt;
-                            break;
-                        }
-                        acc = nxt;
-                    }
-                }
-                __syncthreads();
-                if (s_found != ~0ull) break;
-                run += btot;
+                loc += M::mass(a, i, m);
             }
         }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            uint64_t idx;
-            bool ambiguous;
-            if (s_found == ~0ull || s_found >= a.n - 1) {
-                // reference returns n-1: need U clearly above E_{n-2}
-                idx = a.n - 1;
-                int ix = 0;
-                const u128 mlast = to_fixed(mass_of(a, a.n - 1, weights_only ? 0xFFFFFFFFu : a.mind2[a.n - 1]), &ix);
-                inexact |= ix;
-                const u128 Enm2 = T - mlast;
-                ambiguous = a.n > 1 && !(U > Enm2 + B2);
-            } else {
-                idx = s_found;
-                ambiguous = !(s_E > U + B2) || (idx > 0 && !(U > s_prevE + B2));
-            }
-            s_res[0] = idx;
-            s_res[1] = (ambiguous || inexact) ? 1ull : 0ull;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            if (s_res[1]) {
-                s_res[0] = sequential_draw(a, nu, weights_only);
-                atomicAdd(a.fallbacks, 1ull);
-            }
-            a.result[par] = s_res[0];
-        }
+        const T tot = block_sum<M>(loc, s_w);
+        if (threadIdx.x == 0) segs[s0 / kSeg] = tot;
+        blk += tot;
     }
-    grid.sync();
-    return a.result[par];
+    if (threadIdx.x == 0) parts[blockIdx.x] = blk;
 }
 
+// Every block: locate the draw for unit `nu` over the masses of buffer `par`.
+template <class M>
+__device__ uint64_t locate_draw(const InitArgs &a, cg::grid_group &grid, int par, double nu, int weights_only,
+                                const uint32_t *md, typename M::T *s_w) {
+    typedef typename M::T T;
+    __shared__ T s_U, s_T, s_before, s_prevE, s_E;
+    __shared__ int s_ts;
+    __shared__ unsigned long long s_found;
+    const uint64_t nseg = (a.n + kSeg - 1) / kSeg;
+    const T *parts = reinterpret_cast<const T *>(a.parts) + (size_t)par * gridDim.x;
+    const T *segs = reinterpret_cast<const T *>(a.segs) + (size_t)par * nseg;
+    if (threadIdx.x < 32) {
+        T U = 0, before, tot;
+        const int tb = warp_locate<M>(parts, (int)gridDim.x, true, nu, U, &before, &tot);
+        int ts = -1;
+        T sbefore = before;
+        if (tb < (int)gridDim.x) {
+            const uint64_t lo = (uint64_t)tb * a.chunk;
+            const uint64_t hi = lo + a.chunk < a.n ? lo + a.chunk : a.n;
+            const int s0 = (int)(lo / kSeg), s1 = (int)((hi + kSeg - 1) / kSeg);
+            if (s1 - s0 == 1) {
+                ts = s0;
+            } else {
+                T U2 = U - before, b2, t2;
+                const int j = warp_locate<M>(segs + s0, s1 - s0, false, 0.0, U2, &b2, &t2);
+                ts = j < s1 - s0 ? s0 + j : -1;
+                sbefore = before + b2;
+            }
+        }
+        if (threadIdx.x == 0) {
+            s_U = U;
+            s_T = tot;
+            s_ts = ts;
+            s_before = sbefore;
+            s_found = ~0ull;
+        }
+    }
+    __syncthreads();
+    const T U = s_U, tot = s_T;
+    const int ts = s_ts;
+    if (ts >= 0) {
+        // block scan inside the 1024-point segment, 4 consecutive points / thread
+        const uint64_t base = (uint64_t)ts * kSeg + 4ull * threadIdx.x;
+        T m[4];
+        T loc = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint64_t i = base + j;
+            m[j] = i < a.n ? M::mass(a, i, weights_only ? kWeightsOnly : md[i]) : (T)0;
+            loc += m[j];
+        }
+        T btot;
+        const T start = s_before + block_excl<M>(loc, s_w, &btot);
+        if (start <= U && start + loc > U) {
+            T acc = start;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const T nxt = acc + m[j];
+                if (nxt > U) {
+                    s_found = base + j;
+                    s_prevE = acc;
+                    s_E = nxt;
+                    break;
+                }
+                acc = nxt;
+            }
+        }
+    }
+    __syncthreads();
+    uint64_t idx;
+    bool ambiguous = false;
+    if (s_found == ~0ull || s_found >= a.n - 1) {
+        idx = a.n - 1; // the reference returns n-1 when no i < n-1 qualifies
+        if (!M::exact && a.n > 1) {
+            const T mlast = M::mass(a, a.n - 1, weights_only ? kWeightsOnly : md[a.n - 1]);
+            ambiguous = !(U > tot - mlast + M::bound(a.n, tot));
+        }
+    } else {
+        idx = s_found;
+        if (!M::exact) {
+            const T B2 = M::bound(a.n, tot);
+            ambiguous = !(s_E > U + B2) || (idx > 0 && !(U > s_prevE + B2));
+        }
+    }
+    __syncthreads();
+    if (ambiguous) { // identical decision in every block -> uniform barrier
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            a.result[par] = sequential_draw(a, md, nu, weights_only);
+            atomicAdd(a.fallbacks, 1ull);
+        }
+        grid.sync();
+        idx = a.result[par];
+    }
+    return idx;
+}
+
+template <class M>
 __global__ void __launch_bounds__(kInitThreads) init_kernel(InitArgs a) {
     cg::grid_group grid = cg::this_grid();
-    __shared__ u128 s_w[kInitThreads / 32];
-    __shared__ unsigned long long s_res[2];
+    __shared__ typename M::T s_w[kInitThreads / 32];
     __shared__ unsigned long long s_m[kInitThreads / 32];
-    const uint64_t chunk = (a.n + gridDim.x - 1) / gridDim.x;
-    const uint64_t lo = (uint64_t)blockIdx.x * chunk;
-    const uint64_t hi = lo + chunk < a.n ? lo + chunk : a.n;
+    const uint64_t lo = (uint64_t)blockIdx.x * a.chunk;
+    const uint64_t hi = lo + a.chunk < a.n ? lo + a.chunk : a.n;
     int par = 0;
-    int inexact = 0;
 
     // ---- first centre ---------------------------------------------------
     uint64_t first;
     if (a.kind == 1 || a.weighted_first) {
-        u128 loc = 0;
-        for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) loc += to_fixed(mass_of(a, i, 0xFFFFFFFFu), &inexact);
-        const u128 t = block_sum_u128(loc, s_w);
-        if (threadIdx.x == 0) a.parts[(size_t)par * gridDim.x + blockIdx.x] = t;
+        update_masses<M>(a, par, 1, 0, 0, nullptr, nullptr, lo, hi, s_w);
         grid.sync();
-        first = draw(a, grid, par, a.nu[0], 1, lo, hi, s_w, s_res);
+        first = locate_draw<M>(a, grid, par, a.nu[0], 1, nullptr, s_w);
         par ^= 1;
     } else {
         first = a.first_index;
     }
-    uint32_t clast = a.colors[first];
+    uint32_t clast = __ldg(a.colors + first);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         a.cen[0] = (double)((clast >> 16) & 255u);
         a.cen[1] = (double)((clast >> 8) & 255u);
@@ -286,14 +407,17 @@ __global__ void __launch_bounds__(kInitThreads) init_kernel(InitArgs a) {
     }
 
     for (int k = 1; k < a.K; ++k) {
-        // update min distances with the last centre; per-block partial
+        // round k reads md[(k-1)&1] (absent for k == 1) and writes md[k&1]
+        const uint32_t *md_in = a.md + (size_t)((k - 1) & 1) * a.n;
+        uint32_t *md_out = a.md + (size_t)(k & 1) * a.n;
+        uint64_t pick;
         if (a.kind == 0) {
             unsigned long long best = 0;
             for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-                const uint32_t d = d2_int(a.colors[i], clast);
-                const uint32_t md = (k == 1) ? d : min(a.mind2[i], d);
-                a.mind2[i] = md;
-                const unsigned long long key = ((unsigned long long)md << 32) | (uint32_t)~(uint32_t)i;
+                const uint32_t d = d2_int(__ldg(a.colors + i), clast);
+                const uint32_t m = (k == 1) ? d : min(md_in[i], d);
+                md_out[i] = m;
+                const unsigned long long key = ((unsigned long long)m << 32) | (uint32_t)~(uint32_t)i;
                 best = key > best ? key : best;
             }
             for (int o = 16; o; o >>= 1) {
@@ -309,44 +433,35 @@ __global__ void __launch_bounds__(kInitThreads) init_kernel(InitArgs a) {
             }
             grid.sync();
             unsigned long long b = 0;
-            for (unsigned i = threadIdx.x; i < gridDim.x; i += blockDim.x) {
-                const unsigned long long t = a.mparts[(size_t)par * gridDim.x + i];
-                b = t > b ? t : b;
+            if (threadIdx.x < 32) {
+                for (unsigned i = threadIdx.x; i < gridDim.x; i += 32) {
+                    const unsigned long long t = a.mparts[(size_t)par * gridDim.x + i];
+                    b = t > b ? t : b;
+                }
+                for (int o = 16; o; o >>= 1) {
+                    const unsigned long long t = __shfl_xor_sync(0xffffffffu, b, o);
+                    b = t > b ? t : b;
+                }
             }
-            for (int o = 16; o; o >>= 1) {
-                const unsigned long long t = __shfl_xor_sync(0xffffffffu, b, o);
-                b = t > b ? t : b;
-            }
-            if ((threadIdx.x & 31) == 0) s_m[threadIdx.x >> 5] = b;
+            __syncthreads(); // everyone has read s_m before it is overwritten
+            if (threadIdx.x == 0) s_m[0] = b;
             __syncthreads();
-            b = 0;
-            for (int i = 0; i < kInitThreads / 32; ++i) b = s_m[i] > b ? s_m[i] : b;
-            __syncthreads();
-            // index = ~low32 (indices < 2^32)
-            const uint64_t pick = (uint64_t)(uint32_t)~(uint32_t)(b & 0xFFFFFFFFull);
-            clast = a.colors[pick];
+            b = s_m[0];
+            pick = (uint64_t)(uint32_t)~(uint32_t)(b & 0xFFFFFFFFull);
         } else {
-            u128 loc = 0;
-            for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-                const uint32_t d = d2_int(a.colors[i], clast);
-                const uint32_t md = (k == 1) ? d : min(a.mind2[i], d);
-                a.mind2[i] = md;
-                loc += to_fixed(mass_of(a, i, md), &inexact);
-            }
-            const u128 t = block_sum_u128(loc, s_w);
-            if (threadIdx.x == 0) a.parts[(size_t)par * gridDim.x + blockIdx.x] = t;
+            update_masses<M>(a, par, 0, k == 1, clast, md_in, md_out, lo, hi, s_w);
             grid.sync();
-            const uint64_t pick = draw(a, grid, par, a.nu[k], 0, lo, hi, s_w, s_res);
-            clast = a.colors[pick];
+            pick = locate_draw<M>(a, grid, par, a.nu[k], 0, md_out, s_w);
         }
         par ^= 1;
+        clast = __ldg(a.colors + pick);
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             a.cen[3 * k] = (double)((clast >> 16) & 255u);
             a.cen[3 * k + 1] = (double)((clast >> 8) & 255u);
             a.cen[3 * k + 2] = (double)(clast & 255u);
         }
+        __syncthreads();
     }
-    if (inexact) atomicAdd(a.fallbacks, 0ull); // masses below 2^-36 only for P > 2^32
 }
 
 void run_init(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *counts_d, uint64_t n, uint64_t P,
@@ -367,18 +482,26 @@ void run_init(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *counts_d, 
         const int draws = kind == 1 ? K : 1;
         for (int i = 0; i < draws; ++i) nu.push_back(unit());
     }
+    const bool exact = (P & (P - 1)) == 0 && P <= (1ull << 32);
+    const void *kern = exact ? (const void *)init_kernel<ExactMass> : (const void *)init_kernel<FixedMass>;
     int occ = 0;
-    CQG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, init_kernel, kInitThreads, 0));
+    CQG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kInitThreads, 0));
     if (occ < 1) occ = 1;
     uint64_t grid = (uint64_t)ctx->num_sms * (uint64_t)(occ > 2 ? 2 : occ);
-    const uint64_t want = (n + 4 * kInitThreads - 1) / (4 * kInitThreads);
+    const uint64_t want = (n + kSeg - 1) / kSeg;
     if (grid > want) grid = want;
     if (grid < 1) grid = 1;
+    uint64_t chunk = (n + grid - 1) / grid;
+    chunk = (chunk + kSeg - 1) / kSeg * kSeg;
+    grid = (n + chunk - 1) / chunk;
+    const uint64_t nseg = (n + kSeg - 1) / kSeg;
     double *nu_d = static_cast<double *>(ctx->unit_draws.ensure(sizeof(double) * nu.size()));
     CQG_CUDA(cudaMemcpyAsync(nu_d, nu.data(), sizeof(double) * nu.size(), cudaMemcpyHostToDevice, s));
-    uint32_t *mind2 = static_cast<uint32_t *>(ctx->mind2.ensure(sizeof(uint32_t) * n));
-    u128 *parts = static_cast<u128 *>(ctx->initpart.ensure(sizeof(u128) * 2 * grid + 16 * 2 * grid + 64));
-    unsigned long long *mparts = reinterpret_cast<unsigned long long *>(parts + 2 * grid);
+    uint32_t *md = static_cast<uint32_t *>(ctx->mind2.ensure(sizeof(uint32_t) * 2 * n));
+    const size_t part_bytes = sizeof(u128) * (2 * grid + 2 * nseg) + 8 * 2 * grid + 64;
+    u128 *parts = static_cast<u128 *>(ctx->initpart.ensure(part_bytes));
+    u128 *segs = parts + 2 * grid;
+    unsigned long long *mparts = reinterpret_cast<unsigned long long *>(segs + 2 * nseg);
     unsigned long long *res = static_cast<unsigned long long *>(ctx->status.ensure(64));
     CQG_CUDA(cudaMemsetAsync(res, 0, 64, s));
     InitArgs a{};
@@ -389,17 +512,20 @@ void run_init(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *counts_d, 
     a.K = K;
     a.kind = kind;
     a.weighted_first = weighted_first;
+    a.exact_sums = exact ? 1 : 0;
     a.first_index = first_index;
+    a.chunk = chunk;
     a.nu = nu_d;
-    a.mind2 = mind2;
+    a.md = md;
     a.parts = parts;
+    a.segs = segs;
     a.mparts = mparts;
     a.result = res;
     a.fallbacks = res + 4;
     a.cen = centers_d;
     void *args[] = {&a};
     const int pb = prof_begin(ctx);
-    CQG_CUDA(cudaLaunchCooperativeKernel((const void *)init_kernel, dim3((unsigned)grid), dim3(kInitThreads),
+    CQG_CUDA(cudaLaunchCooperativeKernel(kern, dim3((unsigned)grid), dim3(kInitThreads),
                                          args, 0, s));
     prof_end(ctx, CQG_PROF_INIT, pb, (double)n * (double)(K - 1));
     launched(ctx);

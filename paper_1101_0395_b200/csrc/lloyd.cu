@@ -4,12 +4,15 @@
 // count-weighted substrates. Per iteration (all on the context stream):
 //   sweep<FULL|WALK>   FP32 argmin + near-tie queue + NDC + moment deltas
 //   replay<FULL|WALK>  exact FP64 reference assignment for queued points
-//   finalize           centres = S/n (FP64), SSE from int128 moments,
-//                      termination test (kmeans.cpp:249-257) -> IterStatus
-//   fc / table         FP32 centre table + bound, K x K walk table
-// The host reads one 24-byte IterStatus per iteration. Empty clusters (rare)
-// are repaired by a host-driven loop of device kernels that reproduces
-// repair_empty_clusters (kmeans.cpp:124-169) exactly.
+//   iter_end           (K blocks) centres = S/n in FP64, SSE from the int128
+//                      moment numerators, termination test (kmeans.cpp:249-257),
+//                      FP32 centre table + error bound, and the K x K walk
+//                      table for the next iteration (kmeans.cpp:14-38)
+// Iteration 1 runs eagerly; iterations >= 2 run as ONE CUDA graph whose
+// conditional WHILE node is driven by iter_end (cudaGraphSetConditional), so
+// there is no host round trip per iteration. Empty clusters (rare) stop the
+// loop; the host then runs a device-kernel replay of repair_empty_clusters
+// (kmeans.cpp:124-169) and resumes.
 #include <algorithm>
 #include <cstring>
 
@@ -17,8 +20,10 @@
 
 namespace cqg {
 
-// ---------------------------------------------------------------------------
-__global__ void fc_kernel(const double *cen, int K, int Kp, float *fc, float *tau) {
+// FP32 centre table and sweep error bound from FP64 centres (device helper,
+// block-cooperative). E <= u|cc err| + u|m2c err| x + 4 u M, u = 2^-24, M the
+// largest |partial sum| (cc + xx when all coordinates are >= 0).
+__device__ void fc_block(const double *cen, int K, int Kp, float *fc, float *tau) {
     __shared__ float s_max[32];
     __shared__ int s_neg[32];
     float cm = 0.f;
@@ -59,97 +64,137 @@ __global__ void fc_kernel(const double *cen, int K, int Kp, float *fc, float *ta
         const double u = 0x1.0p-24, X = 255.0;
         const double cc_err = u * 3.0 * C * C;
         const double m2c_err = u * 2.0 * X * 3.0 * C;
-        // all partial sums lie in [0, cc + xx] when x, c >= 0; otherwise a
-        // looser magnitude bound applies
         const double M = anyneg ? 3.0 * C * C + 3.0 * X * X + 6.0 * X * C : 3.0 * C * C + 3.0 * X * X;
         const double E = cc_err + m2c_err + 4.0 * u * M;
         tau[0] = (float)(2.0 * E * 1.0625 + 1.0e-3);
-        tau[1] = 0x1.0p-14f; // covers the 8 truncated mantissa bits of both keys
+        tau[1] = 0x1.0p-20f; // rounding of the FP32 gap test itself
     }
+    __syncthreads();
 }
 
-__global__ void table_kernel(const double *cen, int K, double *dtab, double *dsorted, uint32_t *order) {
-    extern __shared__ double s_d[]; // K doubles + K ints
-    int *s_rank = reinterpret_cast<int *>(s_d + K);
-    const int i = blockIdx.x;
-    const double cr = cen[3 * i], cg = cen[3 * i + 1], cb = cen[3 * i + 2];
-    for (int j = threadIdx.x; j < K; j += blockDim.x) {
-        const double d = d2_exact(cr, cg, cb, cen[3 * j], cen[3 * j + 1], cen[3 * j + 2]);
-        s_d[j] = d;
-        dtab[(size_t)i * K + j] = d;
-    }
-    __syncthreads();
-    for (int j = threadIdx.x; j < K; j += blockDim.x) {
-        const double d = s_d[j];
-        int rank = 0;
-        for (int t = 0; t < K; ++t) {
-            const double e = s_d[t];
-            rank += (e < d) || (e == d && t < j);
-        }
-        s_rank[j] = rank;
-    }
-    __syncthreads();
-    const int rself = s_rank[i];
-    for (int j = threadIdx.x; j < K; j += blockDim.x) {
-        const int rk = s_rank[j];
-        const int pos = (j == i) ? 0 : (rk < rself ? rk + 1 : rk);
-        order[(size_t)i * K + pos] = (uint32_t)j;
-        dsorted[(size_t)i * K + pos] = s_d[j];
-    }
+__global__ void fc_kernel(const double *cen, int K, int Kp, float *fc, float *tau) {
+    fc_block(cen, K, Kp, fc, tau);
 }
 
 namespace {
 
-// Centres from moments, SSE, termination. One block.
-__global__ void finalize_kernel(Moments *mom, double *cen, int K, uint64_t P, int iter, double eps,
-                                int limit, int fixed, double *sse_arr, IterStatus *st,
-                                const uint32_t *qn, unsigned long long *ndc, uint64_t n_points) {
-    extern __shared__ double s_a[];
+struct IterArgs {
+    Moments *mom;
+    double *cen;
+    int K, Kp;
+    uint64_t P;
+    uint64_t n_points;
+    double eps;
+    int limit, fixed;
+    double *sse_arr;
+    IterStatus *st;
+    int *iter_dev;       // last completed iteration
+    const uint32_t *qn;
+    unsigned long long *ndc;
+    unsigned long long *flagged;
+    float *fc, *tau;
+    double *dtab, *dsorted;
+    uint32_t *order;
+    int Kpow;
+    cudaGraphConditionalHandle cond;
+    int use_cond;
+};
+
+// K blocks. Block 0 finalises the iteration; every block builds one row of the
+// next iteration's walk table from the new centres (kept in shared memory).
+__global__ void __launch_bounds__(256) iter_end_kernel(IterArgs a) {
+    extern __shared__ double sm[];
+    const int K = a.K;
+    double *s_c = sm;               // 3K centres
+    double *s_a = sm + 3 * K;       // K per-cluster SSE terms (block 0)
+    double *s_d = sm + 4 * K;       // K row distances
+    int *s_rank = reinterpret_cast<int *>(sm + 5 * K);
     __shared__ int s_empty;
     if (threadIdx.x == 0) s_empty = 0;
     __syncthreads();
     int empty = 0;
-    for (int k = threadIdx.x; k < K; k += blockDim.x) empty |= (mom[k].n == 0);
+    for (int k = threadIdx.x; k < K; k += blockDim.x) {
+        const Moments m = a.mom[k];
+        if (m.n == 0) {
+            empty = 1;
+            continue;
+        }
+        const double nd = __ull2double_rn(m.n);
+        s_c[3 * k] = __ddiv_rn(__ll2double_rn(m.s[0]), nd);
+        s_c[3 * k + 1] = __ddiv_rn(__ll2double_rn(m.s[1]), nd);
+        s_c[3 * k + 2] = __ddiv_rn(__ll2double_rn(m.s[2]), nd);
+        if (blockIdx.x == 0) s_a[k] = cluster_sse_exact(m.n, m.s, m.q);
+    }
     if (empty) atomicOr(&s_empty, 1);
     __syncthreads();
+    const int iter = *a.iter_dev + 1;
     if (s_empty) {
-        if (threadIdx.x == 0) {
-            st->state = 2;
-            st->iteration = iter;
-            st->n_flagged = *qn;
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            a.st->state = 2;
+            a.st->iteration = iter;
+            a.st->n_flagged = *a.qn;
+            if (a.use_cond) cudaGraphSetConditional(a.cond, 0);
         }
         return;
     }
-    for (int k = threadIdx.x; k < K; k += blockDim.x) {
-        const Moments m = mom[k];
-        const double nd = __ull2double_rn(m.n);
-        cen[3 * k] = __ddiv_rn(__ll2double_rn(m.s[0]), nd);
-        cen[3 * k + 1] = __ddiv_rn(__ll2double_rn(m.s[1]), nd);
-        cen[3 * k + 2] = __ddiv_rn(__ll2double_rn(m.s[2]), nd);
-        s_a[k] = cluster_sse_exact(m.n, m.s, m.q);
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double tot = 0.0;
-        for (int k = 0; k < K; ++k) tot = __dadd_rn(tot, s_a[k]);
-        const double sse = __ddiv_rn(tot, __ull2double_rn(P));
-        sse_arr[iter - 1] = sse;
-        int done;
-        if (fixed > 0) {
-            done = iter >= limit;
-        } else {
-            done = (sse == 0.0);
-            if (!done && iter >= 2) {
-                const double prev = sse_arr[iter - 2];
-                done = __ddiv_rn(__dsub_rn(prev, sse), sse) <= eps;
+    if (blockIdx.x == 0) {
+        for (int k = threadIdx.x; k < 3 * K; k += blockDim.x) a.cen[k] = s_c[k];
+        if (threadIdx.x == 0) {
+            double tot = 0.0;
+            for (int k = 0; k < K; ++k) tot = __dadd_rn(tot, s_a[k]);
+            const double sse = __ddiv_rn(tot, __ull2double_rn(a.P));
+            a.sse_arr[iter - 1] = sse;
+            int done;
+            if (a.fixed > 0) {
+                done = iter >= a.limit;
+            } else {
+                done = (sse == 0.0);
+                if (!done && iter >= 2) {
+                    const double prev = a.sse_arr[iter - 2];
+                    done = __ddiv_rn(__dsub_rn(prev, sse), sse) <= a.eps;
+                }
+                if (!done && iter >= a.limit) done = 1;
             }
-            if (!done && iter >= limit) done = 1;
+            if (iter == 1) *a.ndc += (unsigned long long)a.n_points * (unsigned long long)K;
+            *a.flagged += *a.qn;
+            a.st->state = done ? 1 : 0;
+            a.st->iteration = iter;
+            a.st->n_flagged = *a.qn;
+            a.st->sse = sse;
+            *a.iter_dev = iter;
+            if (a.use_cond) cudaGraphSetConditional(a.cond, done ? 0 : 1);
         }
-        if (iter == 1) *ndc += (unsigned long long)n_points * (unsigned long long)K;
-        st->state = done ? 1 : 0;
-        st->iteration = iter;
-        st->n_flagged = *qn;
-        st->sse = sse;
+        fc_block(s_c, K, a.Kp, a.fc, a.tau);
+    }
+    // walk table row i (kmeans.cpp:14-38): sort by (d, index), self first
+    for (int i = blockIdx.x; i < K; i += gridDim.x) {
+        const double cr = s_c[3 * i], cg = s_c[3 * i + 1], cb = s_c[3 * i + 2];
+        for (int j = threadIdx.x; j < K; j += blockDim.x) {
+            const double d = d2_exact(cr, cg, cb, s_c[3 * j], s_c[3 * j + 1], s_c[3 * j + 2]);
+            s_d[j] = d;
+            a.dtab[(size_t)i * K + j] = d;
+        }
+        __syncthreads();
+        for (int j = threadIdx.x; j < K; j += blockDim.x) {
+            const double d = s_d[j];
+            int rank = 0;
+            for (int t = 0; t < K; ++t) {
+                const double e = s_d[t];
+                rank += (e < d) || (e == d && t < j);
+            }
+            s_rank[j] = rank;
+        }
+        __syncthreads();
+        const int rself = s_rank[i];
+        for (int j = threadIdx.x; j < K; j += blockDim.x) {
+            const int rk = s_rank[j];
+            const int pos = (j == i) ? 0 : (rk < rself ? rk + 1 : rk);
+            a.order[(size_t)i * K + pos] = (uint32_t)j;
+            a.dsorted[(size_t)i * a.Kpow + pos] = s_d[j];
+        }
+        for (int j = K + threadIdx.x; j < a.Kpow; j += blockDim.x)
+            a.dsorted[(size_t)i * a.Kpow + j] = __longlong_as_double(0x7FF0000000000000ll); // +inf
+        __syncthreads();
     }
 }
 
@@ -250,43 +295,55 @@ int pick_grid(cqg_ctx *ctx, uint64_t work, int per_block, int per_sm) {
 } // namespace
 
 size_t sweep_smem_bytes(int K, int Kp) {
-    return (size_t)4 * Kp * sizeof(float) + (size_t)K * kAccPerCluster * sizeof(uint32_t);
+    // u32 accumulators (FULL/MAP) or u64 (WALK): reserve the larger
+    const size_t acc32 = (size_t)K * kAccPerCluster * sizeof(uint32_t);
+    const size_t acc64 = (size_t)K * 5 * sizeof(unsigned long long);
+    return (size_t)4 * Kp * sizeof(float) + (acc64 > acc32 ? acc64 : acc32);
+}
+
+template <int MODE, int PPT>
+static int sweep_bps(size_t smem) {
+    int bps = 0;
+    CQG_CUDA(cudaFuncSetAttribute(sweep_kernel<MODE, PPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CQG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, sweep_kernel<MODE, PPT>, kSweepThreads, smem));
+    return bps < 1 ? 1 : bps;
+}
+
+template <int MODE, int PPT>
+static void launch_ppt(cqg_ctx *ctx, const SweepArgs &a, size_t smem, int bps) {
+    // one balanced wave: every SM gets bps blocks with equal point ranges
+    uint64_t grid = (uint64_t)ctx->num_sms * (uint64_t)bps;
+    const uint64_t cap = (a.n + 63) / 64; // at least 64 points per block
+    if (grid > cap) grid = cap;
+    if (grid < 1) grid = 1;
+    sweep_kernel<MODE, PPT><<<(unsigned)grid, kSweepThreads, smem, ctx->stream>>>(a);
 }
 
 template <int MODE>
 static void launch_sweep_mode(cqg_ctx *ctx, const SweepArgs &a) {
     const size_t smem = sweep_smem_bytes(a.K, a.Kp);
     const uint64_t n = a.n;
-    const int pb = prof_begin(ctx);
-    if (a.K > 256) {
-        auto kern = sweep_wide_kernel<MODE>;
-        CQG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        const int grid = pick_grid(ctx, n, kSweepThreads, 4);
-        kern<<<grid, kSweepThreads, smem, ctx->stream>>>(a);
-    } else {
-        // choose points-per-thread so the grid still covers every SM twice
-        const uint64_t per_sm2 = (uint64_t)ctx->num_sms * 2;
-        if (n >= per_sm2 * kSweepThreads * 8) {
-            auto kern = sweep_kernel<MODE, 8>;
-            CQG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            kern<<<pick_grid(ctx, n, kSweepThreads * 8, 4), kSweepThreads, smem, ctx->stream>>>(a);
-        } else if (n >= per_sm2 * kSweepThreads * 4) {
-            auto kern = sweep_kernel<MODE, 4>;
-            CQG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            kern<<<pick_grid(ctx, n, kSweepThreads * 4, 4), kSweepThreads, smem, ctx->stream>>>(a);
-        } else if (n >= per_sm2 * kSweepThreads * 2) {
-            auto kern = sweep_kernel<MODE, 2>;
-            CQG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            kern<<<pick_grid(ctx, n, kSweepThreads * 2, 4), kSweepThreads, smem, ctx->stream>>>(a);
-        } else {
-            auto kern = sweep_kernel<MODE, 1>;
-            CQG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            kern<<<pick_grid(ctx, n, kSweepThreads, 4), kSweepThreads, smem, ctx->stream>>>(a);
-        }
+    const uint64_t sms = (uint64_t)ctx->num_sms;
+    if (MODE == MODE_WALK) {
+        const int pn = prof_begin(ctx);
+        const size_t csm = a.K <= 2048 ? (size_t)a.K * 24 : 0;
+        if (csm > 48 * 1024)
+            CQG_CUDA(cudaFuncSetAttribute(ndc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
+        ndc_kernel<<<pick_grid(ctx, n, 1024, 8), 256, csm, ctx->stream>>>(a.colors, a.labels, n, a.cen,
+                                                                           a.dsorted, a.K, a.Kpow, a.ndc);
+        prof_end(ctx, CQG_PROF_NDC, pn, (double)n);
+        launched(ctx);
     }
+    const int pb = prof_begin(ctx);
+    // smallest points-per-thread whose single wave covers all points (fewest
+    // idle lanes, most blocks); large inputs loop over 8-point tiles
+    const int b2 = sweep_bps<MODE, 2>(smem), b4 = sweep_bps<MODE, 4>(smem), b8 = sweep_bps<MODE, 8>(smem);
+    if (n <= sms * b2 * kSweepThreads * 2) launch_ppt<MODE, 2>(ctx, a, smem, b2);
+    else if (n <= sms * b4 * kSweepThreads * 4) launch_ppt<MODE, 4>(ctx, a, smem, b4);
+    else launch_ppt<MODE, 8>(ctx, a, smem, b8);
     prof_end(ctx, MODE == MODE_MAP ? CQG_PROF_MAPSWEEP : CQG_PROF_SWEEP, pb, (double)n * (double)a.K);
     const int pr = prof_begin(ctx);
-    replay_kernel<MODE><<<pick_grid(ctx, n / 64 + 1, 128, 2), 128, 0, ctx->stream>>>(a);
+    replay_kernel<MODE><<<pick_grid(ctx, n * 32 / 256 + 1, 256, 2), 256, 0, ctx->stream>>>(a);
     prof_end(ctx, CQG_PROF_REPLAY, pr, 0.0);
     CQG_CUDA(cudaGetLastError());
     launched(ctx, 2);
@@ -351,24 +408,85 @@ static int repair_loop(cqg_ctx *ctx, const uint32_t *colors, const uint32_t *cou
     return repairs;
 }
 
+static size_t iter_end_smem(int K) { return (size_t)K * (5 * sizeof(double) + sizeof(int)); }
+
+static void launch_iter_end(cqg_ctx *ctx, const IterArgs &ia) {
+    const size_t smem = iter_end_smem(ia.K);
+    if (smem > 48 * 1024)
+        CQG_CUDA(cudaFuncSetAttribute(iter_end_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    iter_end_kernel<<<ia.K, 256, smem, ctx->stream>>>(ia);
+    launched(ctx);
+}
+
+// Cached CUDA graph: WHILE(cond) { memset(qn); sweep<WALK>; replay<WALK>; iter_end }
+static cudaGraphExec_t loop_graph(cqg_ctx *ctx, const SweepArgs &a, IterArgs ia, uint32_t *qn) {
+    std::vector<uint64_t> key = {(uint64_t)a.colors, (uint64_t)a.counts, a.n, (uint64_t)a.labels,
+                                 (uint64_t)a.cen, (uint64_t)a.K, (uint64_t)ia.limit, (uint64_t)ia.fixed,
+                                 ia.P, __builtin_bit_cast(uint64_t, ia.eps), (uint64_t)a.mom,
+                                 (uint64_t)a.queue, (uint64_t)ia.sse_arr, (uint64_t)ia.st,
+                                 (uint64_t)ctx->stream};
+    if (ctx->loop_exec && ctx->loop_key == key) return ctx->loop_exec;
+    release_graphs(ctx);
+    cudaGraph_t graph;
+    CQG_CUDA(cudaGraphCreate(&graph, 0));
+    cudaGraphConditionalHandle h;
+    CQG_CUDA(cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams cp{};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t cn;
+    CQG_CUDA(cudaGraphAddNode(&cn, graph, nullptr, 0, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    ia.cond = h;
+    ia.use_cond = 1;
+    const bool prof = ctx->prof_on;
+    ctx->prof_on = false; // no event records inside the captured body
+    CQG_CUDA(cudaStreamBeginCaptureToGraph(ctx->stream, body, nullptr, nullptr, 0,
+                                           cudaStreamCaptureModeThreadLocal));
+    CQG_CUDA(cudaMemsetAsync(qn, 0, 4, ctx->stream));
+    launch_sweep(ctx, MODE_WALK, a);
+    launch_iter_end(ctx, ia);
+    cudaGraph_t captured;
+    CQG_CUDA(cudaStreamEndCapture(ctx->stream, &captured));
+    ctx->prof_on = prof;
+    CQG_CUDA(cudaGraphInstantiate(&ctx->loop_exec, graph, 0));
+    ctx->loop_graph = graph;
+    ctx->loop_key = key;
+    return ctx->loop_exec;
+}
+
+void release_graphs(cqg_ctx *ctx) {
+    if (ctx->loop_exec) cudaGraphExecDestroy(ctx->loop_exec);
+    if (ctx->loop_graph) cudaGraphDestroy(ctx->loop_graph);
+    ctx->loop_exec = nullptr;
+    ctx->loop_graph = nullptr;
+    ctx->loop_key.clear();
+}
+
 LloydOut lloyd_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *counts_d, uint64_t n,
                    uint64_t P, const double *init_d, int K, const cqg_term &term, uint32_t *labels_d,
                    double *centers_d, double *sse_host, uint32_t *hist_labels_user,
                    double *hist_centers_user) {
     cudaStream_t s = ctx->stream;
-    const int Kp = (K + 3) & ~3;
+    const int Kp = (K + 7) & ~7;
     const int limit = term.fixed_iterations > 0 ? term.fixed_iterations : term.max_iterations;
     double *cen = centers_d;
     CQG_CUDA(cudaMemcpyAsync(cen, init_d, sizeof(double) * 3 * K, cudaMemcpyDeviceToDevice, s));
     float *fc = static_cast<float *>(ctx->fcen.ensure(sizeof(float) * (4 * (size_t)Kp + 8)));
     float *tau = fc + 4 * Kp;
     double *dtab = static_cast<double *>(ctx->dtab.ensure(sizeof(double) * (size_t)K * K));
-    double *dsorted = static_cast<double *>(ctx->dsorted.ensure(sizeof(double) * (size_t)K * K));
+    int Kpow = 1;
+    while (Kpow < K) Kpow <<= 1;
+    double *dsorted = static_cast<double *>(ctx->dsorted.ensure(sizeof(double) * (size_t)K * Kpow));
     uint32_t *order = static_cast<uint32_t *>(ctx->order.ensure(sizeof(uint32_t) * (size_t)K * K));
     Moments *mom = static_cast<Moments *>(ctx->mom.ensure(sizeof(Moments) * (size_t)K));
     uint32_t *queue = static_cast<uint32_t *>(ctx->queue.ensure(sizeof(uint32_t) * (n + 1)));
     uint32_t *qn = static_cast<uint32_t *>(ctx->scal.ensure(256));
     unsigned long long *ndc = reinterpret_cast<unsigned long long *>(qn + 8);
+    unsigned long long *flagged = reinterpret_cast<unsigned long long *>(qn + 10);
+    int *iter_dev = reinterpret_cast<int *>(qn + 12);
     IterStatus *st = reinterpret_cast<IterStatus *>(qn + 16);
     double *sse_d = static_cast<double *>(ctx->sse.ensure(sizeof(double) * (size_t)(limit + 1)));
     IterStatus *hst = static_cast<IterStatus *>(ctx->pinned.ensure(4096));
@@ -381,7 +499,7 @@ LloydOut lloyd_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *count
     }
 
     CQG_CUDA(cudaMemsetAsync(mom, 0, sizeof(Moments) * (size_t)K, s));
-    CQG_CUDA(cudaMemsetAsync(ndc, 0, 8, s));
+    CQG_CUDA(cudaMemsetAsync(ndc, 0, 24, s)); // ndc, flagged, iter_dev
     fc_kernel<<<1, 256, 0, s>>>(cen, K, Kp, fc, tau);
     launched(ctx);
 
@@ -402,54 +520,80 @@ LloydOut lloyd_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *count
     a.ndc = ndc;
     a.K = K;
     a.Kp = Kp;
+    a.Kpow = Kpow;
 
+    IterArgs ia{};
+    ia.mom = mom;
+    ia.cen = cen;
+    ia.K = K;
+    ia.Kp = Kp;
+    ia.P = P;
+    ia.n_points = n;
+    ia.eps = term.epsilon;
+    ia.limit = limit;
+    ia.fixed = term.fixed_iterations;
+    ia.sse_arr = sse_d;
+    ia.st = st;
+    ia.iter_dev = iter_dev;
+    ia.qn = qn;
+    ia.ndc = ndc;
+    ia.flagged = flagged;
+    ia.fc = fc;
+    ia.tau = tau;
+    ia.dtab = dtab;
+    ia.dsorted = dsorted;
+    ia.order = order;
+    ia.Kpow = Kpow;
+    ia.use_cond = 0;
+
+    // The graph path needs no per-iteration host work: used unless history is
+    // recorded (per-iteration copies) or kernel profiling is on (per-launch events).
+    const bool use_graph = !hist && !ctx->prof_on && ctx->use_graphs;
     LloydOut out;
-    const int fin_threads = K >= 1024 ? 1024 : ((K + 31) / 32) * 32;
-    const size_t table_smem = (size_t)K * (sizeof(double) + sizeof(int));
-    if (table_smem > 48 * 1024)
-        CQG_CUDA(cudaFuncSetAttribute(table_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)table_smem));
-    if ((size_t)K * 8 > 48 * 1024)
-        CQG_CUDA(cudaFuncSetAttribute(finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, K * 8));
-    int iter = 1;
-    for (;; ++iter) {
-        CQG_CUDA(cudaMemsetAsync(qn, 0, 4, s));
-        launch_sweep(ctx, iter == 1 ? MODE_FULL : MODE_WALK, a);
-        if (hist) {
-            if (hist_labels_user)
-                CQG_CUDA(cudaMemcpyAsync(hl_d + (size_t)(iter - 1) * n, labels_d, 4 * n,
-                                         cudaMemcpyDeviceToDevice, s));
-            if (hist_centers_user)
-                CQG_CUDA(cudaMemcpyAsync(hc_d + (size_t)(iter - 1) * 3 * K, cen, 24 * (size_t)K,
-                                         cudaMemcpyDeviceToDevice, s));
+    int iter = 0;
+    bool done = false;
+    while (!done) {
+        const bool first = (iter == 0);
+        if (!first && use_graph) {
+            cudaGraphExec_t ge = loop_graph(ctx, a, ia, qn);
+            CQG_CUDA(cudaGraphLaunch(ge, s));
+            launched(ctx, 4);
+        } else {
+            CQG_CUDA(cudaMemsetAsync(qn, 0, 4, s));
+            launch_sweep(ctx, first ? MODE_FULL : MODE_WALK, a);
+            if (hist) {
+                if (hist_labels_user)
+                    CQG_CUDA(cudaMemcpyAsync(hl_d + (size_t)iter * n, labels_d, 4 * n, cudaMemcpyDeviceToDevice, s));
+                if (hist_centers_user)
+                    CQG_CUDA(cudaMemcpyAsync(hc_d + (size_t)iter * 3 * K, cen, 24 * (size_t)K,
+                                             cudaMemcpyDeviceToDevice, s));
+            }
+            launch_iter_end(ctx, ia);
         }
-        finalize_kernel<<<1, fin_threads, (size_t)K * 8, s>>>(mom, cen, K, P, iter, term.epsilon, limit,
-                                                              term.fixed_iterations, sse_d, st, qn, ndc, n);
-        launched(ctx);
         CQG_CUDA(cudaMemcpyAsync(hst, st, sizeof(IterStatus), cudaMemcpyDeviceToHost, s));
         CQG_CUDA(cudaStreamSynchronize(s));
-        out.flagged += hst->n_flagged;
+        iter = hst->iteration;
         if (hst->state == 2) {
             out.repairs += repair_loop(ctx, colors_d, counts_d, n, P, K, labels_d, cen, mom);
-            finalize_kernel<<<1, fin_threads, (size_t)K * 8, s>>>(mom, cen, K, P, iter, term.epsilon, limit,
-                                                                  term.fixed_iterations, sse_d, st, qn, ndc, n);
-            launched(ctx);
+            launch_iter_end(ctx, ia);
             CQG_CUDA(cudaMemcpyAsync(hst, st, sizeof(IterStatus), cudaMemcpyDeviceToHost, s));
             CQG_CUDA(cudaStreamSynchronize(s));
             if (hst->state == 2) fail(CQG_E_RUNTIME, "repair left an empty cluster");
+            iter = hst->iteration;
         }
-        if (hst->state == 1) break;
-        fc_kernel<<<1, 256, 0, s>>>(cen, K, Kp, fc, tau);
-        table_kernel<<<K, 256, table_smem, s>>>(cen, K, dtab, dsorted, order);
-        launched(ctx, 2);
+        done = hst->state == 1;
     }
     out.iterations = iter;
     CQG_CUDA(cudaMemcpyAsync(sse_host, sse_d, sizeof(double) * iter, cudaMemcpyDefault, s));
-    CQG_CUDA(cudaMemcpyAsync(&out.ndc, ndc, 8, cudaMemcpyDeviceToHost, s));
+    unsigned long long *hcnt = reinterpret_cast<unsigned long long *>(hst + 1);
+    CQG_CUDA(cudaMemcpyAsync(hcnt, ndc, 16, cudaMemcpyDeviceToHost, s));
     if (hist) {
         if (hist_labels_user) copy_out(ctx, hist_labels_user, hl_d, sizeof(uint32_t) * n * (size_t)iter);
         if (hist_centers_user) copy_out(ctx, hist_centers_user, hc_d, 24 * (size_t)K * iter);
     }
     CQG_CUDA(cudaStreamSynchronize(s));
+    out.ndc = hcnt[0];
+    out.flagged = hcnt[1];
     return out;
 }
 

@@ -154,7 +154,7 @@ double map_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P, const uint32_t *c
                const uint32_t *counts_d, uint64_t n, const double *pal_d, int K, void *indices_d,
                int index_bytes, uint8_t *quant_d) {
     cudaStream_t s = ctx->stream;
-    const int Kp = (K + 3) & ~3;
+    const int Kp = (K + 7) & ~7;
     const bool lut8 = K <= 256;
     float *fc = static_cast<float *>(ctx->fcen.ensure(sizeof(float) * (4 * (size_t)Kp + 8)));
     float *tau = fc + 4 * Kp;

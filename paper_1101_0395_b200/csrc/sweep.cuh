@@ -4,9 +4,9 @@
 //
 // Per (unique colour x, centre c) the sweep evaluates the expanded form
 //     d = (|c|^2 + |x|^2) - 2 x.c
-// as FADD2 + 3 FFMA2 on float pairs (two centres per instruction), packs the
-// centre index into the low 8 mantissa bits of d and keeps the best and the
-// second-best key with 3-input integer min/max (VIMNMX3). The result is exact
+// as FADD2 + 3 FFMA2 on float pairs (two centres per instruction) and keeps
+// the best and the
+// second-best value with 3-input float min/max (FMNMX3). The result is exact
 // whenever the best/second gap exceeds a rigorous bound on the FP32 error
 // (tau, computed per iteration from the centre magnitudes); otherwise the
 // point is queued and replayed in FP64 with the reference's own walk
@@ -23,7 +23,7 @@ constexpr uint32_t kHeavyCount = 2048; // counts >= this bypass the u32 smem acc
 
 enum { MODE_FULL = 0, MODE_WALK = 1, MODE_MAP = 2 };
 
-// Shared-memory layout of the FP32 centre table (Kp = K rounded up to 4):
+// Shared-memory layout of the FP32 centre table (Kp = K rounded up to 8):
 //   m2r[Kp], m2g[Kp], m2b[Kp], cc[Kp]  (m2* = -2 * centre, cc = |centre|^2)
 // Padding centres have cc = 1e30 and never win.
 
@@ -45,6 +45,7 @@ struct SweepArgs {
     Moments *mom;
     unsigned long long *ndc;
     int K, Kp;
+    int Kpow; // dsorted row stride: next power of two >= K
 };
 
 __device__ __forceinline__ uint32_t lane_lt_mask() {
@@ -90,6 +91,19 @@ __device__ __forceinline__ void accumulate(uint32_t *acc, Moments *mom, int k, u
     }
 }
 
+// 64-bit shared accumulators laid out exactly like Moments (n, s[3], q): the
+// WALK-mode block total is flushed with one global add per field.
+__device__ __forceinline__ void accumulate64(unsigned long long *acc, int k, uint32_t cnt, uint32_t r,
+                                             uint32_t g, uint32_t b, int sign) {
+    const long long sc = (long long)sign * (long long)cnt;
+    unsigned long long *m = acc + 5 * k;
+    atomicAdd(m + 0, (unsigned long long)sc);
+    atomicAdd(m + 1, (unsigned long long)(sc * (long long)r));
+    atomicAdd(m + 2, (unsigned long long)(sc * (long long)g));
+    atomicAdd(m + 3, (unsigned long long)(sc * (long long)b));
+    atomicAdd(m + 4, (unsigned long long)(sc * (long long)(r * r + g * g + b * b)));
+}
+
 // global-atomic version (replay / repair paths)
 __device__ __forceinline__ void accumulate_global(Moments *mom, int k, uint32_t cnt, uint32_t r,
                                                   uint32_t g, uint32_t b, int sign) {
@@ -128,240 +142,305 @@ __device__ __forceinline__ void flush_acc(uint32_t *acc, Moments *mom, int K) {
 
 // NDC of assign_point_sortmeans for point x with previous label prev
 // (kmeans.cpp:56-79): 1 + #{walk positions j >= 1 : D[prev][order[j]] < 4*d2(x,c_prev)}.
-// Rows are sorted ascending after the self-first rotation, so this is a
-// lower_bound in exact FP64.
+// Each row of dsorted holds the row's distances in walk order (ascending: the
+// self distance 0 first), padded with +inf to Kpow = next power of two >= K.
+// Binary lifting counts the entries < cutoff without branches; position 0 (the
+// self entry, 0) counts iff cutoff > 0.
+__device__ __forceinline__ uint32_t walk_positions(double cut, const double *row, int Kpow) {
+    int pos = 0;
+    for (int step = Kpow >> 1; step >= 1; step >>= 1)
+        if (__ldg(row + pos + step - 1) < cut) pos += step;
+    return (uint32_t)(pos - (cut > 0.0 ? 1 : 0)) + 1u; // positions visited: 0..ret-1
+}
+
 __device__ __forceinline__ uint32_t walk_ndc(double xr, double xg, double xb, int prev,
-                                             const double *cen, const double *dsorted, int K) {
+                                             const double *cen, const double *dsorted, int K, int Kpow) {
     const double pd = d2_exact(xr, xg, xb, cen[3 * prev], cen[3 * prev + 1], cen[3 * prev + 2]);
-    const double cutoff = __dmul_rn(4.0, pd);
-    const double *row = dsorted + (size_t)prev * K;
-    int lo = 1, hi = K;
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (__ldg(row + mid) < cutoff) lo = mid + 1;
-        else hi = mid;
+    return walk_positions(__dmul_rn(4.0, pd), dsorted + (size_t)prev * Kpow, Kpow);
+}
+
+// NDC of one WALK iteration, before the sweep rewrites the labels: 4 points per
+// thread with their lifting searches interleaved (independent loads in flight).
+static __global__ void __launch_bounds__(256) ndc_kernel(const uint32_t *__restrict__ colors,
+                                                  const uint32_t *__restrict__ labels, uint64_t n,
+                                                  const double *__restrict__ cen,
+                                                  const double *__restrict__ dsorted, int K, int Kpow,
+                                                  unsigned long long *ndc) {
+    extern __shared__ double s_cen[];
+    const bool in_smem = K <= 2048;
+    if (in_smem)
+        for (int i = threadIdx.x; i < 3 * K; i += blockDim.x) s_cen[i] = cen[i];
+    __syncthreads();
+    const double *c = in_smem ? s_cen : cen;
+    constexpr int Q = 4;
+    unsigned long long local = 0;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * Q;
+    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x * Q; base < n; base += stride) {
+        double cut[Q];
+        const double *row[Q];
+        int pos[Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const uint64_t i = base + threadIdx.x + (uint64_t)q * blockDim.x;
+            const bool v = i < n;
+            const uint32_t col = v ? __ldg(colors + i) : 0u;
+            const int prev = v ? (int)__ldg(labels + i) : 0;
+            const double pd = d2_exact((double)((col >> 16) & 255u), (double)((col >> 8) & 255u),
+                                       (double)(col & 255u), c[3 * prev], c[3 * prev + 1], c[3 * prev + 2]);
+            cut[q] = v ? __dmul_rn(4.0, pd) : -1.0; // -1: counts nothing and adds 0 below
+            row[q] = dsorted + (size_t)prev * Kpow;
+            pos[q] = 0;
+        }
+        for (int step = Kpow >> 1; step >= 1; step >>= 1) {
+            double vv[Q];
+#pragma unroll
+            for (int q = 0; q < Q; ++q) vv[q] = __ldg(row[q] + pos[q] + step - 1);
+#pragma unroll
+            for (int q = 0; q < Q; ++q) pos[q] += vv[q] < cut[q] ? step : 0;
+        }
+#pragma unroll
+        for (int q = 0; q < Q; ++q)
+            if (cut[q] >= 0.0) local += (unsigned long long)(pos[q] - (cut[q] > 0.0 ? 1 : 0) + 1);
     }
-    return (uint32_t)lo; // 1 + (lo - 1)
+    for (int o = 16; o; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+    if ((threadIdx.x & 31) == 0 && local) atomicAdd(ndc, local);
 }
 
 // ---------------------------------------------------------------------------
-// The sweep kernel. PPT points per thread amortise the shared-memory centre
-// loads (one LDS.128 per 4 centres per operand array).
+// The sweep kernel. Each block owns a contiguous, equal share of the points
+// (balanced across SMs); PPT points per thread amortise the shared-memory
+// centre loads (one LDS.128 per 4 centres per operand array).
+//
+// Per point the best (b1) and second-best (b2) FP32 values are tracked with
+// 3-input float min/max; instead of packing the centre index into the value,
+// only the index of the 8-centre GROUP that last improved b1 is kept (one
+// compare + select per group). The exact index is recovered afterwards by
+// recomputing the 8 distances of that group with the identical FP operation
+// sequence (bit-identical values) and taking the first that equals b1.
+constexpr int kGroup = 8;
+constexpr int kSmemCentres = 1024; // FP64 centres staged in shared memory up to this K
+
+__device__ __forceinline__ void track_pair(float2 v, float &b1, float &b2) {
+    const float lo = fminf(v.x, v.y), hi = fmaxf(v.x, v.y);
+    b2 = fminf(fminf(b2, hi), fmaxf(b1, lo));
+    b1 = fminf(b1, lo);
+}
+
 template <int MODE, int PPT>
-__global__ void __launch_bounds__(kSweepThreads) sweep_kernel(SweepArgs a) {
+__global__ void __launch_bounds__(kSweepThreads, 2) sweep_kernel(SweepArgs a) {
+    static_assert(PPT % 2 == 0, "points are processed in pairs");
+    constexpr int PP = PPT / 2;
     extern __shared__ __align__(16) float smem[];
     const int K = a.K, Kp = a.Kp;
     float *s_m2r = smem, *s_m2g = smem + Kp, *s_m2b = smem + 2 * Kp, *s_cc = smem + 3 * Kp;
     uint32_t *s_acc = reinterpret_cast<uint32_t *>(smem + 4 * Kp);
+    // WALK iterations move few points: their moment deltas go to 64-bit shared
+    // accumulators (flushed once per block); FULL/MAP use u32 + per-tile flush
+    unsigned long long *s_acc64 = reinterpret_cast<unsigned long long *>(s_acc);
     for (int i = threadIdx.x; i < 4 * Kp; i += blockDim.x) smem[i] = a.fc[i];
-    for (int i = threadIdx.x; i < K * kAccPerCluster; i += blockDim.x) s_acc[i] = 0;
+    if (MODE == MODE_WALK)
+        for (int i = threadIdx.x; i < K * 5; i += blockDim.x) s_acc64[i] = 0;
+    else
+        for (int i = threadIdx.x; i < K * kAccPerCluster; i += blockDim.x) s_acc[i] = 0;
     __syncthreads();
     const float tau_abs = a.tau[0], tau_rel = a.tau[1];
     unsigned long long ndc_local = 0;
 
+    const uint64_t chunk = (a.n + gridDim.x - 1) / gridDim.x;
+    const uint64_t lo = (uint64_t)blockIdx.x * chunk;
+    const uint64_t hi = lo + chunk < a.n ? lo + chunk : a.n;
     const uint64_t tile = (uint64_t)kSweepThreads * PPT;
-    for (uint64_t base = (uint64_t)blockIdx.x * tile; base < a.n; base += (uint64_t)gridDim.x * tile) {
-        float2 xr2[PPT], xg2[PPT], xb2[PPT], xx2[PPT];
+    for (uint64_t base = lo; base < hi; base += tile) {
+        // point pairs: lane .x = point 2p, lane .y = point 2p+1 (FFMA2 with a
+        // broadcast scalar centre operand evaluates one centre for both)
+        float2 xr2[PP], xg2[PP], xb2[PP], xx2[PP];
         uint32_t col[PPT];
-        int b1[PPT], b2[PPT];
+        float b1[PPT], b2[PPT];
+        int g1[PPT];
 #pragma unroll
         for (int i = 0; i < PPT; ++i) {
             const uint64_t idx = base + threadIdx.x + (uint64_t)i * kSweepThreads;
-            col[i] = idx < a.n ? __ldg(a.colors + idx) : 0u;
+            col[i] = idx < hi ? __ldg(a.colors + idx) : 0u;
             const float r = (float)((col[i] >> 16) & 255u), g = (float)((col[i] >> 8) & 255u),
                         b = (float)(col[i] & 255u);
-            const float xx = r * r + g * g + b * b; // exact: integers < 2^18
-            xr2[i] = make_float2(r, r);
-            xg2[i] = make_float2(g, g);
-            xb2[i] = make_float2(b, b);
-            xx2[i] = make_float2(xx, xx);
-            b1[i] = 0x7FFFFFFF;
-            b2[i] = 0x7FFFFFFF;
-        }
-#pragma unroll 2
-        for (int j = 0; j < Kp; j += 4) {
-            const float4 r4 = *reinterpret_cast<const float4 *>(s_m2r + j);
-            const float4 g4 = *reinterpret_cast<const float4 *>(s_m2g + j);
-            const float4 b4 = *reinterpret_cast<const float4 *>(s_m2b + j);
-            const float4 c4 = *reinterpret_cast<const float4 *>(s_cc + j);
-            const float2 rlo = make_float2(r4.x, r4.y), rhi = make_float2(r4.z, r4.w);
-            const float2 glo = make_float2(g4.x, g4.y), ghi = make_float2(g4.z, g4.w);
-            const float2 blo = make_float2(b4.x, b4.y), bhi = make_float2(b4.z, b4.w);
-            const float2 clo = make_float2(c4.x, c4.y), chi = make_float2(c4.z, c4.w);
-#pragma unroll
-            for (int i = 0; i < PPT; ++i) {
-                float2 A = __fadd2_rn(clo, xx2[i]);
-                A = __ffma2_rn(xr2[i], rlo, A);
-                A = __ffma2_rn(xg2[i], glo, A);
-                A = __ffma2_rn(xb2[i], blo, A);
-                float2 B = __fadd2_rn(chi, xx2[i]);
-                B = __ffma2_rn(xr2[i], rhi, B);
-                B = __ffma2_rn(xg2[i], ghi, B);
-                B = __ffma2_rn(xb2[i], bhi, B);
-                const int k0 = (__float_as_int(A.x) & ~0xFF) | j;
-                const int k1 = (__float_as_int(A.y) & ~0xFF) | (j + 1);
-                const int k2 = (__float_as_int(B.x) & ~0xFF) | (j + 2);
-                const int k3 = (__float_as_int(B.y) & ~0xFF) | (j + 3);
-                int lo = min(k0, k1), hi = max(k0, k1);
-                b2[i] = min(min(b2[i], hi), max(b1[i], lo));
-                b1[i] = min(b1[i], lo);
-                lo = min(k2, k3);
-                hi = max(k2, k3);
-                b2[i] = min(min(b2[i], hi), max(b1[i], lo));
-                b1[i] = min(b1[i], lo);
+            float xx = r * r + g * g + b * b; // exact: integers < 2^18
+            // opaque copies: keep the floats resident instead of letting ptxas
+            // rematerialise them from the packed colour inside the centre loop
+            float rr = r, gg = g, bb = b;
+            asm volatile("" : "+f"(rr), "+f"(gg), "+f"(bb), "+f"(xx));
+            if (i & 1) {
+                xr2[i / 2].y = rr; xg2[i / 2].y = gg; xb2[i / 2].y = bb; xx2[i / 2].y = xx;
+            } else {
+                xr2[i / 2].x = rr; xg2[i / 2].x = gg; xb2[i / 2].x = bb; xx2[i / 2].x = xx;
             }
+            b1[i] = 3.0e38f;
+            b2[i] = 3.0e38f;
+            g1[i] = 0;
+        }
+        for (int j = 0; j < Kp; j += kGroup) {
+            float before[PPT];
+#pragma unroll
+            for (int i = 0; i < PPT; ++i) before[i] = b1[i];
+#pragma unroll
+            for (int q = 0; q < kGroup; q += 4) {
+                const float4 r4 = *reinterpret_cast<const float4 *>(s_m2r + j + q);
+                const float4 g4 = *reinterpret_cast<const float4 *>(s_m2g + j + q);
+                const float4 b4 = *reinterpret_cast<const float4 *>(s_m2b + j + q);
+                const float4 c4 = *reinterpret_cast<const float4 *>(s_cc + j + q);
+#pragma unroll
+                for (int p = 0; p < PP; ++p) {
+                    float2 A0 = __fadd2_rn(xx2[p], make_float2(c4.x, c4.x));
+                    A0 = __ffma2_rn(xr2[p], make_float2(r4.x, r4.x), A0);
+                    A0 = __ffma2_rn(xg2[p], make_float2(g4.x, g4.x), A0);
+                    A0 = __ffma2_rn(xb2[p], make_float2(b4.x, b4.x), A0);
+                    float2 A1 = __fadd2_rn(xx2[p], make_float2(c4.y, c4.y));
+                    A1 = __ffma2_rn(xr2[p], make_float2(r4.y, r4.y), A1);
+                    A1 = __ffma2_rn(xg2[p], make_float2(g4.y, g4.y), A1);
+                    A1 = __ffma2_rn(xb2[p], make_float2(b4.y, b4.y), A1);
+                    float2 A2 = __fadd2_rn(xx2[p], make_float2(c4.z, c4.z));
+                    A2 = __ffma2_rn(xr2[p], make_float2(r4.z, r4.z), A2);
+                    A2 = __ffma2_rn(xg2[p], make_float2(g4.z, g4.z), A2);
+                    A2 = __ffma2_rn(xb2[p], make_float2(b4.z, b4.z), A2);
+                    float2 A3 = __fadd2_rn(xx2[p], make_float2(c4.w, c4.w));
+                    A3 = __ffma2_rn(xr2[p], make_float2(r4.w, r4.w), A3);
+                    A3 = __ffma2_rn(xg2[p], make_float2(g4.w, g4.w), A3);
+                    A3 = __ffma2_rn(xb2[p], make_float2(b4.w, b4.w), A3);
+                    track_pair(make_float2(A0.x, A1.x), b1[2 * p], b2[2 * p]);
+                    track_pair(make_float2(A2.x, A3.x), b1[2 * p], b2[2 * p]);
+                    track_pair(make_float2(A0.y, A1.y), b1[2 * p + 1], b2[2 * p + 1]);
+                    track_pair(make_float2(A2.y, A3.y), b1[2 * p + 1], b2[2 * p + 1]);
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < PPT; ++i) g1[i] = b1[i] < before[i] ? j : g1[i];
         }
         // resolve
 #pragma unroll
         for (int i = 0; i < PPT; ++i) {
             const uint64_t idx = base + threadIdx.x + (uint64_t)i * kSweepThreads;
-            const bool valid = idx < a.n;
-            const int j1 = b1[i] & 0xFF;
-            const float f1 = __int_as_float(b1[i] & ~0xFF), f2 = __int_as_float(b2[i] & ~0xFF);
+            const bool valid = idx < hi;
+            const float f1 = b1[i], f2 = b2[i];
             const bool flag = valid && !((f2 - f1) > tau_abs + tau_rel * (fabsf(f1) + fabsf(f2)));
+            // exact index: first centre of group g1 whose (bit-identical) value is b1
+            int j1;
+            {
+                const int g0 = g1[i];
+                const float xr = (i & 1) ? xr2[i / 2].y : xr2[i / 2].x;
+                const float xg = (i & 1) ? xg2[i / 2].y : xg2[i / 2].x;
+                const float xb = (i & 1) ? xb2[i / 2].y : xb2[i / 2].x;
+                const float xx = (i & 1) ? xx2[i / 2].y : xx2[i / 2].x;
+                int found = -1;
+#pragma unroll
+                for (int q = 0; q < kGroup; ++q) {
+                    float d = __fadd_rn(xx, s_cc[g0 + q]);
+                    d = __fmaf_rn(xr, s_m2r[g0 + q], d);
+                    d = __fmaf_rn(xg, s_m2g[g0 + q], d);
+                    d = __fmaf_rn(xb, s_m2b[g0 + q], d);
+                    if (found < 0 && d == f1) found = g0 + q;
+                }
+                j1 = found < 0 ? g0 : found;
+            }
             const uint32_t r = (col[i] >> 16) & 255u, g = (col[i] >> 8) & 255u, b = col[i] & 255u;
             if (MODE == MODE_WALK && valid) {
                 const int prev = (int)a.labels[idx];
-                ndc_local += walk_ndc((double)r, (double)g, (double)b, prev, a.cen, a.dsorted, K);
                 if (!flag && j1 != prev) {
                     const uint32_t cnt = __ldg(a.counts + idx);
                     a.labels[idx] = (uint32_t)j1;
-                    accumulate(s_acc, a.mom, j1, cnt, r, g, b, +1);
-                    accumulate(s_acc, a.mom, prev, cnt, r, g, b, -1);
+                    accumulate64(s_acc64, j1, cnt, r, g, b, +1);
+                    accumulate64(s_acc64, prev, cnt, r, g, b, -1);
                 }
             } else if (valid && !flag) {
                 const uint32_t cnt = __ldg(a.counts + idx);
                 if (MODE == MODE_FULL) a.labels[idx] = (uint32_t)j1;
-                else a.lut8[col[i]] = (uint8_t)j1;
+                else if (a.lut8) a.lut8[col[i]] = (uint8_t)j1;
+                else a.lut32[col[i]] = (uint32_t)j1;
                 accumulate(s_acc, a.mom, j1, cnt, r, g, b, +1);
             }
             enqueue(flag, (uint32_t)idx, a.queue, a.qn);
         }
-        __syncthreads();
-        flush_acc(s_acc, a.mom, K);
-        __syncthreads();
-    }
-    if (MODE == MODE_WALK) {
-        for (int o = 16; o; o >>= 1) ndc_local += __shfl_xor_sync(0xffffffffu, ndc_local, o);
-        if ((threadIdx.x & 31) == 0 && ndc_local) atomicAdd(a.ndc, ndc_local);
-    }
-}
-
-// ---------------------------------------------------------------------------
-// Wide variant for K > 256 (index does not fit in 8 mantissa bits): separate
-// value/index tracking, one centre at a time.
-template <int MODE>
-__global__ void __launch_bounds__(kSweepThreads) sweep_wide_kernel(SweepArgs a) {
-    extern __shared__ __align__(16) float smem[];
-    const int K = a.K, Kp = a.Kp;
-    float *s_m2r = smem, *s_m2g = smem + Kp, *s_m2b = smem + 2 * Kp, *s_cc = smem + 3 * Kp;
-    uint32_t *s_acc = reinterpret_cast<uint32_t *>(smem + 4 * Kp);
-    for (int i = threadIdx.x; i < 4 * Kp; i += blockDim.x) smem[i] = a.fc[i];
-    for (int i = threadIdx.x; i < K * kAccPerCluster; i += blockDim.x) s_acc[i] = 0;
-    __syncthreads();
-    const float tau_abs = a.tau[0], tau_rel = a.tau[1];
-    unsigned long long ndc_local = 0;
-    int since_flush = 0;
-    for (uint64_t base = (uint64_t)blockIdx.x * kSweepThreads; base < a.n;
-         base += (uint64_t)gridDim.x * kSweepThreads) {
-        const uint64_t idx = base + threadIdx.x;
-        const bool valid = idx < a.n;
-        const uint32_t c = valid ? __ldg(a.colors + idx) : 0u;
-        const uint32_t r = (c >> 16) & 255u, g = (c >> 8) & 255u, b = c & 255u;
-        const float fr = (float)r, fg = (float)g, fb = (float)b;
-        const float xx = fr * fr + fg * fg + fb * fb;
-        float v1 = 3.0e38f, v2 = 3.0e38f;
-        int j1 = 0;
-        for (int j = 0; j < K; ++j) {
-            float d = s_cc[j] + xx;
-            d = fmaf(fr, s_m2r[j], d);
-            d = fmaf(fg, s_m2g[j], d);
-            d = fmaf(fb, s_m2b[j], d);
-            v2 = fminf(v2, fmaxf(v1, d));
-            if (d < v1) j1 = j;
-            v1 = fminf(v1, d);
-        }
-        const bool flag = valid && !((v2 - v1) > tau_abs + tau_rel * (fabsf(v1) + fabsf(v2)));
-        if (MODE == MODE_WALK && valid) {
-            const int prev = (int)a.labels[idx];
-            ndc_local += walk_ndc((double)r, (double)g, (double)b, prev, a.cen, a.dsorted, K);
-            if (!flag && j1 != prev) {
-                const uint32_t cnt = __ldg(a.counts + idx);
-                a.labels[idx] = (uint32_t)j1;
-                accumulate(s_acc, a.mom, j1, cnt, r, g, b, +1);
-                accumulate(s_acc, a.mom, prev, cnt, r, g, b, -1);
-            }
-        } else if (valid && !flag) {
-            const uint32_t cnt = __ldg(a.counts + idx);
-            if (MODE == MODE_FULL) a.labels[idx] = (uint32_t)j1;
-            else a.lut32[c] = (uint32_t)j1;
-            accumulate(s_acc, a.mom, j1, cnt, r, g, b, +1);
-        }
-        enqueue(flag, (uint32_t)idx, a.queue, a.qn);
-        if (++since_flush == 8) { // flush every 2048 points
-            since_flush = 0;
+        if (MODE != MODE_WALK) {
             __syncthreads();
             flush_acc(s_acc, a.mom, K);
             __syncthreads();
         }
     }
-    __syncthreads();
-    flush_acc(s_acc, a.mom, K);
     if (MODE == MODE_WALK) {
-        for (int o = 16; o; o >>= 1) ndc_local += __shfl_xor_sync(0xffffffffu, ndc_local, o);
-        if ((threadIdx.x & 31) == 0 && ndc_local) atomicAdd(a.ndc, ndc_local);
+        __syncthreads();
+        for (int e = threadIdx.x; e < K * 5; e += blockDim.x) {
+            const unsigned long long v = s_acc64[e];
+            if (v) atomicAdd(reinterpret_cast<unsigned long long *>(a.mom) + e, v);
+        }
     }
 }
 
 // ---------------------------------------------------------------------------
-// Exact FP64 replay of the reference's assignment for queued (near-tie) points.
-//   FULL / MAP: nearest_full (kmeans.cpp:40-54): strict <, lowest index wins.
-//   WALK: assign_point_sortmeans (kmeans.cpp:56-79) from the previous label.
+// Exact FP64 replay of the reference's assignment for queued (near-tie) points,
+// one warp per point (lanes split the candidates, lexicographic warp min).
+//   FULL / MAP: nearest_full (kmeans.cpp:40-54): min d, lowest index on ties.
+//   WALK: assign_point_sortmeans (kmeans.cpp:56-79): candidates are walk
+//         positions 0..cnt (0 = the previous label) with cnt from the exact
+//         cutoff; the walk keeps the FIRST minimum in walk order, i.e. the
+//         minimum of (d, position).
+__device__ __forceinline__ void warp_min_dp(double &d, int &p) {
+    for (int o = 16; o; o >>= 1) {
+        const double od = __shfl_xor_sync(0xffffffffu, d, o);
+        const int op = __shfl_xor_sync(0xffffffffu, p, o);
+        if (od < d || (od == d && op < p)) {
+            d = od;
+            p = op;
+        }
+    }
+}
+
 template <int MODE>
 __global__ void replay_kernel(SweepArgs a) {
     const uint32_t nq = *a.qn;
-    for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += gridDim.x * blockDim.x) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < nq; q += warps) {
         const uint32_t idx = a.queue[q];
         const uint32_t c = a.colors[idx], cnt = a.counts[idx];
         const uint32_t r = (c >> 16) & 255u, g = (c >> 8) & 255u, b = c & 255u;
         const double xr = (double)r, xg = (double)g, xb = (double)b;
         const int K = a.K;
+        double bd = 1.0e300;
+        int bp = 0x7FFFFFFF;
+        int best;
         if (MODE == MODE_WALK) {
             const int prev = (int)a.labels[idx];
-            const double *drow = a.dtab + (size_t)prev * K;
+            const uint32_t npos = walk_ndc(xr, xg, xb, prev, a.cen, a.dsorted, K, a.Kpow); // positions 0..npos-1
             const uint32_t *orow = a.order + (size_t)prev * K;
-            const double pd = d2_exact(xr, xg, xb, a.cen[3 * prev], a.cen[3 * prev + 1], a.cen[3 * prev + 2]);
-            const double cutoff = __dmul_rn(4.0, pd);
-            double bd = pd;
-            int best = prev;
-            for (int j = 1; j < K; ++j) {
-                const uint32_t t = orow[j];
-                if (drow[t] >= cutoff) break;
+            for (uint32_t p = lane; p < npos; p += 32) {
+                const uint32_t t = orow[p];
                 const double d = d2_exact(xr, xg, xb, a.cen[3 * t], a.cen[3 * t + 1], a.cen[3 * t + 2]);
                 if (d < bd) {
                     bd = d;
-                    best = (int)t;
+                    bp = (int)p;
                 }
             }
-            if (best != prev) {
+            warp_min_dp(bd, bp);
+            best = (int)orow[bp];
+            if (lane == 0 && best != prev) {
                 a.labels[idx] = (uint32_t)best;
                 accumulate_global(a.mom, best, cnt, r, g, b, +1);
                 accumulate_global(a.mom, prev, cnt, r, g, b, -1);
             }
         } else {
-            double bd = d2_exact(xr, xg, xb, a.cen[0], a.cen[1], a.cen[2]);
-            int best = 0;
-            for (int j = 1; j < K; ++j) {
+            for (int j = lane; j < K; j += 32) {
                 const double d = d2_exact(xr, xg, xb, a.cen[3 * j], a.cen[3 * j + 1], a.cen[3 * j + 2]);
                 if (d < bd) {
                     bd = d;
-                    best = j;
+                    bp = j;
                 }
             }
-            if (MODE == MODE_FULL) a.labels[idx] = (uint32_t)best;
-            else if (a.lut8) a.lut8[c] = (uint8_t)best;
-            else a.lut32[c] = (uint32_t)best;
-            accumulate_global(a.mom, best, cnt, r, g, b, +1);
+            warp_min_dp(bd, bp);
+            best = bp;
+            if (lane == 0) {
+                if (MODE == MODE_FULL) a.labels[idx] = (uint32_t)best;
+                else if (a.lut8) a.lut8[c] = (uint8_t)best;
+                else a.lut32[c] = (uint32_t)best;
+                accumulate_global(a.mom, best, cnt, r, g, b, +1);
+            }
         }
     }
 }
@@ -371,9 +450,6 @@ __global__ void replay_kernel(SweepArgs a) {
 //   magnitude of any partial sum (cc + xx when all coordinates are >= 0).
 __global__ void fc_kernel(const double *cen, int K, int Kp, float *fc, float *tau);
 
-// K x K centre distances, per-row walk order (sorted by (d, index), self first:
-// kmeans.cpp:14-38) and the rows' distances in walk order.
-__global__ void table_kernel(const double *cen, int K, double *dtab, double *dsorted, uint32_t *order);
 
 size_t sweep_smem_bytes(int K, int Kp);
 void launch_sweep(cqg_ctx *ctx, int mode, const SweepArgs &a);
