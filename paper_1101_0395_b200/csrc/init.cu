@@ -93,9 +93,12 @@ __device__ __forceinline__ uint32_t d2_int(uint32_t a, uint32_t b) {
 }
 
 // the reference's mass: weights[i] (* mind2[i])
-__device__ __forceinline__ double mass_of(const InitArgs &a, uint64_t i, uint32_t md) {
-    const double w = __dmul_rn((double)a.counts[i], a.inv);
+__device__ __forceinline__ double mass_c(uint32_t cnt, double inv, uint32_t md) {
+    const double w = __dmul_rn((double)cnt, inv);
     return md == kWeightsOnly ? w : __dmul_rn(w, (double)md);
+}
+__device__ __forceinline__ double mass_of(const InitArgs &a, uint64_t i, uint32_t md) {
+    return mass_c(a.counts[i], a.inv, md);
 }
 
 __device__ __forceinline__ u128 shfl_u128(u128 v, int src) {
@@ -122,8 +125,10 @@ __device__ __forceinline__ u128 shfl_up_u128(u128 v, int d) {
 struct ExactMass {
     typedef unsigned long long T;
     static __device__ __forceinline__ T mass(const InitArgs &a, uint64_t i, uint32_t md) {
-        const T c = (T)a.counts[i];
-        return md == kWeightsOnly ? c : c * (T)md;
+        return mass_c(a, a.counts[i], md);
+    }
+    static __device__ __forceinline__ T mass_c(const InitArgs &, uint32_t cnt, uint32_t md) {
+        return md == kWeightsOnly ? (T)cnt : (T)cnt * (T)md;
     }
     static __device__ __forceinline__ T target(double nu, T total) {
         return (T)floor(__dmul_rn(nu, (double)total)); // u * P, exact scaling
@@ -138,6 +143,9 @@ struct FixedMass {
     typedef u128 T;
     static __device__ __forceinline__ T mass(const InitArgs &a, uint64_t i, uint32_t md) {
         return to_fixed(mass_of(a, i, md));
+    }
+    static __device__ __forceinline__ T mass_c(const InitArgs &a, uint32_t cnt, uint32_t md) {
+        return to_fixed(cqg::mass_c(cnt, a.inv, md));
     }
     static __device__ __forceinline__ T target(double nu, T total) {
         return floor_fixed(__dmul_rn(nu, fixed_to_double(total)));
@@ -251,7 +259,9 @@ __device__ uint64_t sequential_draw(const InitArgs &a, const uint32_t *md, doubl
 }
 
 // Update pass over this block's range: new min distances (unless weights_only)
-// and mass sums per segment and per block.
+// and mass sums per segment and per block. One warp per 1024-point segment,
+// 8 points per lane loaded before use (memory-level parallelism), no block
+// barrier until the block total.
 template <class M>
 __device__ void update_masses(const InitArgs &a, int par, int weights_only, int first_round, uint32_t clast,
                               const uint32_t *md_in, uint32_t *md_out, uint64_t lo, uint64_t hi,
@@ -259,29 +269,81 @@ __device__ void update_masses(const InitArgs &a, int par, int weights_only, int 
     typedef typename M::T T;
     T *segs = reinterpret_cast<T *>(a.segs) + (size_t)par * ((a.n + kSeg - 1) / kSeg);
     T *parts = reinterpret_cast<T *>(a.parts) + (size_t)par * gridDim.x;
-    T blk = 0;
-    for (uint64_t s0 = lo; s0 < hi; s0 += kSeg) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if (hi <= lo + kSeg) {
+        // a single segment (small inputs): all warps share it, 4 points per lane
         T loc = 0;
+        uint32_t col[4], cnt[4], mi[4];
 #pragma unroll
-        for (int j = 0; j < kSeg / kInitThreads; ++j) {
-            const uint64_t i = s0 + threadIdx.x + (uint64_t)j * kInitThreads;
+        for (int u = 0; u < 4; ++u) {
+            const uint64_t i = lo + (uint64_t)u * blockDim.x + threadIdx.x;
+            const bool v = i < hi;
+            cnt[u] = v ? __ldg(a.counts + i) : 0u;
+            col[u] = (v && !weights_only) ? __ldg(a.colors + i) : 0u;
+            mi[u] = (v && !weights_only && !first_round) ? md_in[i] : 0xFFFFFFFFu;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint64_t i = lo + (uint64_t)u * blockDim.x + threadIdx.x;
             if (i < hi) {
-                uint32_t m;
-                if (weights_only) {
-                    m = kWeightsOnly;
-                } else {
-                    const uint32_t d = d2_int(__ldg(a.colors + i), clast);
-                    m = first_round ? d : min(md_in[i], d);
+                uint32_t m = kWeightsOnly;
+                if (!weights_only) {
+                    m = min(mi[u], d2_int(col[u], clast));
                     md_out[i] = m;
                 }
-                loc += M::mass(a, i, m);
+                loc += M::mass_c(a, cnt[u], m);
             }
         }
-        const T tot = block_sum<M>(loc, s_w);
-        if (threadIdx.x == 0) segs[s0 / kSeg] = tot;
-        blk += tot;
+        for (int o = 16; o; o >>= 1) loc += M::shfl(loc, lane ^ o);
+        if (lane == 0) s_w[warp] = loc;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            T t = 0;
+            for (int w = 0; w < nw; ++w) t += s_w[w];
+            if (lo < hi) segs[lo / kSeg] = t;
+            parts[blockIdx.x] = t;
+        }
+        __syncthreads();
+        return;
     }
-    if (threadIdx.x == 0) parts[blockIdx.x] = blk;
+    T wsum = 0;
+    for (uint64_t s0 = lo + (uint64_t)warp * kSeg; s0 < hi; s0 += (uint64_t)nw * kSeg) {
+        T loc = 0;
+        for (int b = 0; b < kSeg; b += 32 * 8) {
+            uint32_t col[8], cnt[8], mi[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint64_t i = s0 + b + u * 32 + lane;
+                const bool v = i < hi;
+                cnt[u] = v ? __ldg(a.counts + i) : 0u;
+                col[u] = (v && !weights_only) ? __ldg(a.colors + i) : 0u;
+                mi[u] = (v && !weights_only && !first_round) ? md_in[i] : 0xFFFFFFFFu;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint64_t i = s0 + b + u * 32 + lane;
+                if (i < hi) {
+                    uint32_t m = kWeightsOnly;
+                    if (!weights_only) {
+                        m = min(mi[u], d2_int(col[u], clast));
+                        md_out[i] = m;
+                    }
+                    loc += M::mass_c(a, cnt[u], m);
+                }
+            }
+        }
+        for (int o = 16; o; o >>= 1) loc += M::shfl(loc, lane ^ o);
+        if (lane == 0) segs[s0 / kSeg] = loc;
+        wsum += loc;
+    }
+    if (lane == 0) s_w[warp] = wsum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        T t = 0;
+        for (int w = 0; w < nw; ++w) t += s_w[w];
+        parts[blockIdx.x] = t;
+    }
+    __syncthreads();
 }
 
 // Every block: locate the draw for unit `nu` over the masses of buffer `par`.
@@ -413,12 +475,24 @@ __global__ void __launch_bounds__(kInitThreads) init_kernel(InitArgs a) {
         uint64_t pick;
         if (a.kind == 0) {
             unsigned long long best = 0;
-            for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-                const uint32_t d = d2_int(__ldg(a.colors + i), clast);
-                const uint32_t m = (k == 1) ? d : min(md_in[i], d);
-                md_out[i] = m;
-                const unsigned long long key = ((unsigned long long)m << 32) | (uint32_t)~(uint32_t)i;
-                best = key > best ? key : best;
+            for (uint64_t i0 = lo + threadIdx.x; i0 < hi; i0 += 8ull * blockDim.x) {
+                uint32_t col[8], mi[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const uint64_t i = i0 + (uint64_t)u * blockDim.x;
+                    col[u] = i < hi ? __ldg(a.colors + i) : 0u;
+                    mi[u] = (i < hi && k > 1) ? md_in[i] : 0xFFFFFFFFu;
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const uint64_t i = i0 + (uint64_t)u * blockDim.x;
+                    if (i < hi) {
+                        const uint32_t m = min(mi[u], d2_int(col[u], clast));
+                        md_out[i] = m;
+                        const unsigned long long key = ((unsigned long long)m << 32) | (uint32_t)~(uint32_t)i;
+                        best = key > best ? key : best;
+                    }
+                }
             }
             for (int o = 16; o; o >>= 1) {
                 const unsigned long long t = __shfl_xor_sync(0xffffffffu, best, o);

@@ -102,7 +102,7 @@ struct IterArgs {
 
 // K blocks. Block 0 finalises the iteration; every block builds one row of the
 // next iteration's walk table from the new centres (kept in shared memory).
-__global__ void __launch_bounds__(256) iter_end_kernel(IterArgs a) {
+__global__ void __launch_bounds__(1024) iter_end_kernel(IterArgs a) {
     extern __shared__ double sm[];
     const int K = a.K;
     double *s_c = sm;               // 3K centres
@@ -175,14 +175,22 @@ __global__ void __launch_bounds__(256) iter_end_kernel(IterArgs a) {
             a.dtab[(size_t)i * K + j] = d;
         }
         __syncthreads();
-        for (int j = threadIdx.x; j < K; j += blockDim.x) {
-            const double d = s_d[j];
+        // rank of (d_j, j) by (distance, index): 4 threads per element, each
+        // counting a quarter of the row, combined by shuffles
+        for (int e = threadIdx.x; e < 4 * ((K + 7) & ~7); e += blockDim.x) {
+            const int j = e >> 2, part = e & 3;
             int rank = 0;
-            for (int t = 0; t < K; ++t) {
-                const double e = s_d[t];
-                rank += (e < d) || (e == d && t < j);
+            if (j < K) {
+                const double d = s_d[j];
+                const int t0 = part * ((K + 3) / 4), t1 = min(K, t0 + (K + 3) / 4);
+                for (int t = t0; t < t1; ++t) {
+                    const double v = s_d[t];
+                    rank += (v < d) || (v == d && t < j);
+                }
             }
-            s_rank[j] = rank;
+            rank += __shfl_xor_sync(0xffffffffu, rank, 1);
+            rank += __shfl_xor_sync(0xffffffffu, rank, 2);
+            if (part == 0 && j < K) s_rank[j] = rank;
         }
         __syncthreads();
         const int rself = s_rank[i];
@@ -327,10 +335,16 @@ static void launch_sweep_mode(cqg_ctx *ctx, const SweepArgs &a) {
     if (MODE == MODE_WALK) {
         const int pn = prof_begin(ctx);
         const size_t csm = a.K <= 2048 ? (size_t)a.K * 24 : 0;
-        if (csm > 48 * 1024)
-            CQG_CUDA(cudaFuncSetAttribute(ndc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
-        ndc_kernel<<<pick_grid(ctx, n, 1024, 8), 256, csm, ctx->stream>>>(a.colors, a.labels, n, a.cen,
-                                                                           a.dsorted, a.K, a.Kpow, a.ndc);
+        if (csm > 48 * 1024) {
+            CQG_CUDA(cudaFuncSetAttribute(ndc_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
+            CQG_CUDA(cudaFuncSetAttribute(ndc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
+        }
+        if (n >= (uint64_t)ctx->num_sms * 4 * 256 * 8)
+            ndc_kernel<8><<<pick_grid(ctx, n, 2048, 4), 256, csm, ctx->stream>>>(a.colors, a.labels, n, a.cen,
+                                                                              a.dsorted, a.K, a.Kpow, a.ndc);
+        else
+            ndc_kernel<2><<<pick_grid(ctx, n, 512, 8), 256, csm, ctx->stream>>>(a.colors, a.labels, n, a.cen,
+                                                                             a.dsorted, a.K, a.Kpow, a.ndc);
         prof_end(ctx, CQG_PROF_NDC, pn, (double)n);
         launched(ctx);
     }
@@ -414,7 +428,7 @@ static void launch_iter_end(cqg_ctx *ctx, const IterArgs &ia) {
     const size_t smem = iter_end_smem(ia.K);
     if (smem > 48 * 1024)
         CQG_CUDA(cudaFuncSetAttribute(iter_end_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    iter_end_kernel<<<ia.K, 256, smem, ctx->stream>>>(ia);
+    iter_end_kernel<<<ia.K, ia.K >= 256 ? 1024 : 256, smem, ctx->stream>>>(ia);
     launched(ctx);
 }
 

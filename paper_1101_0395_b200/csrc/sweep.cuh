@@ -150,7 +150,26 @@ __device__ __forceinline__ uint32_t walk_positions(double cut, const double *row
     int pos = 0;
     for (int step = Kpow >> 1; step >= 1; step >>= 1)
         if (__ldg(row + pos + step - 1) < cut) pos += step;
+    if (pos == Kpow - 1 && __ldg(row + Kpow - 1) < cut) pos = Kpow; // whole row below
     return (uint32_t)(pos - (cut > 0.0 ? 1 : 0)) + 1u; // positions visited: 0..ret-1
+}
+
+// Warp-cooperative version (all 32 lanes, same row/cutoff): a 32-ary search,
+// two dependent loads for Kpow <= 1024.
+__device__ __forceinline__ uint32_t walk_positions_warp(double cut, const double *row, int Kpow) {
+    const int lane = threadIdx.x & 31;
+    int base = 0, span = Kpow;
+    while (span > 1) {
+        const int S = span >= 32 ? span / 32 : 1; // stride between probes
+        const int probes = span >= 32 ? 32 : span;
+        const int p = base + (lane + 1) * S - 1;
+        const bool lt = lane < probes && __ldg(row + p) < cut;
+        const int c = __popc(__ballot_sync(0xffffffffu, lt));
+        base += c * S;
+        span = S;
+        if (c == probes) break; // everything probed is below the cutoff
+    }
+    return (uint32_t)(base - (cut > 0.0 ? 1 : 0)) + 1u;
 }
 
 __device__ __forceinline__ uint32_t walk_ndc(double xr, double xg, double xb, int prev,
@@ -161,7 +180,8 @@ __device__ __forceinline__ uint32_t walk_ndc(double xr, double xg, double xb, in
 
 // NDC of one WALK iteration, before the sweep rewrites the labels: 4 points per
 // thread with their lifting searches interleaved (independent loads in flight).
-static __global__ void __launch_bounds__(256) ndc_kernel(const uint32_t *__restrict__ colors,
+template <int Q>
+static __global__ void __launch_bounds__(256, 4) ndc_kernel(const uint32_t *__restrict__ colors,
                                                   const uint32_t *__restrict__ labels, uint64_t n,
                                                   const double *__restrict__ cen,
                                                   const double *__restrict__ dsorted, int K, int Kpow,
@@ -172,7 +192,6 @@ static __global__ void __launch_bounds__(256) ndc_kernel(const uint32_t *__restr
         for (int i = threadIdx.x; i < 3 * K; i += blockDim.x) s_cen[i] = cen[i];
     __syncthreads();
     const double *c = in_smem ? s_cen : cen;
-    constexpr int Q = 4;
     unsigned long long local = 0;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * Q;
     for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x * Q; base < n; base += stride) {
@@ -199,8 +218,11 @@ static __global__ void __launch_bounds__(256) ndc_kernel(const uint32_t *__restr
             for (int q = 0; q < Q; ++q) pos[q] += vv[q] < cut[q] ? step : 0;
         }
 #pragma unroll
-        for (int q = 0; q < Q; ++q)
+        for (int q = 0; q < Q; ++q) {
+            // lifting reaches at most Kpow-1: the whole row may lie below the cutoff
+            if (pos[q] == Kpow - 1 && cut[q] >= 0.0 && __ldg(row[q] + Kpow - 1) < cut[q]) pos[q] = Kpow;
             if (cut[q] >= 0.0) local += (unsigned long long)(pos[q] - (cut[q] > 0.0 ? 1 : 0) + 1);
+        }
     }
     for (int o = 16; o; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
     if ((threadIdx.x & 31) == 0 && local) atomicAdd(ndc, local);
@@ -408,7 +430,9 @@ __global__ void replay_kernel(SweepArgs a) {
         int best;
         if (MODE == MODE_WALK) {
             const int prev = (int)a.labels[idx];
-            const uint32_t npos = walk_ndc(xr, xg, xb, prev, a.cen, a.dsorted, K, a.Kpow); // positions 0..npos-1
+            const double pd = d2_exact(xr, xg, xb, a.cen[3 * prev], a.cen[3 * prev + 1], a.cen[3 * prev + 2]);
+            const uint32_t npos = walk_positions_warp(__dmul_rn(4.0, pd), a.dsorted + (size_t)prev * a.Kpow,
+                                                      a.Kpow); // positions 0..npos-1
             const uint32_t *orow = a.order + (size_t)prev * K;
             for (uint32_t p = lane; p < npos; p += 32) {
                 const uint32_t t = orow[p];
