@@ -71,7 +71,35 @@ def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False) 
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError("link failed: " + " ".join(cmd) + "\n" + r.stdout + r.stderr)
+    build_host(force)
     return LIB
+
+
+HOST_LIB = os.path.join(PKG, "libquant_b200.so")
+CPP_TEST_SRC = os.path.join(ROOT, "tests", "cpp", "test_dropin.cpp")
+CPP_TEST_BIN = os.path.join(ROOT, "tests", "cpp", "test_dropin")
+
+
+def build_host(force: bool = False) -> str:
+    """libquant_b200.so: the reference's quant:: C++ API over libcqg.so, plus
+    the C++ drop-in test binary."""
+    cxx = shutil.which("g++") or "g++"
+    inc = ["-I" + os.path.join(ROOT, "include")]
+    src = os.path.join(PKG, "host", "quant_b200.cpp")
+    hdrs = [os.path.join(ROOT, "include", "quant", "quant.hpp"), os.path.join(ROOT, "include", "cqg.h")]
+    if force or _newer([src, LIB, *hdrs], HOST_LIB):
+        cmd = [cxx, "-std=c++20", "-O2", "-fPIC", "-shared", *inc, src, "-o", HOST_LIB, "-L" + PKG, "-l:libcqg.so",
+               "-Wl,-rpath,$ORIGIN"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError("host library build failed:\n" + r.stdout + r.stderr)
+    if force or _newer([CPP_TEST_SRC, HOST_LIB, *hdrs], CPP_TEST_BIN):
+        cmd = [cxx, "-std=c++20", "-O2", *inc, CPP_TEST_SRC, "-o", CPP_TEST_BIN, "-L" + PKG, "-l:libquant_b200.so",
+               "-l:libcqg.so", "-Wl,-rpath," + PKG]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError("C++ test build failed:\n" + r.stdout + r.stderr)
+    return HOST_LIB
 
 
 if __name__ == "__main__":

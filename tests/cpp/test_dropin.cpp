@@ -1,0 +1,218 @@
+// test_dropin.cpp -- the reference's own style of checks (its doctest suites,
+// proj/tests/test_*.cpp) run against libquant_b200.so through the C++ quant::
+// API. Built by __graft_entry__.build() into tests/cpp/test_dropin; run by
+// tests/test_gpu_cpp.py on a GPU box. Prints one line per case, exit 0 = pass.
+//
+//   argv[1] = tests/golden directory (acc_61.rgb, acc_62.rgb, sweep_a_rows.csv, wu_init.txt)
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <fstream>
+#include <iostream>
+#include <set>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "quant/quant.hpp"
+
+using namespace quant;
+
+static int g_fail = 0;
+#define CHECK(cond)                                                                     \
+    do {                                                                                \
+        if (!(cond)) {                                                                  \
+            std::printf("  CHECK failed %s:%d: %s\n", __FILE__, __LINE__, #cond);        \
+            ++g_fail;                                                                   \
+        }                                                                               \
+    } while (0)
+#define CHECK_THROWS_AS(expr, T)                                                        \
+    do {                                                                                \
+        bool ok_ = false;                                                               \
+        try {                                                                           \
+            (void)(expr);                                                               \
+        } catch (const T &) {                                                           \
+            ok_ = true;                                                                 \
+        } catch (...) {                                                                 \
+        }                                                                               \
+        if (!ok_) {                                                                     \
+            std::printf("  CHECK_THROWS_AS failed %s:%d: %s\n", __FILE__, __LINE__, #expr); \
+            ++g_fail;                                                                   \
+        }                                                                               \
+    } while (0)
+
+static RawImage load_rgb(const std::string &path, int w, int h) {
+    RawImage img;
+    img.width = w;
+    img.height = h;
+    img.pixels.resize(static_cast<std::size_t>(w) * h);
+    std::ifstream f(path, std::ios::binary);
+    f.read(reinterpret_cast<char *>(img.pixels.data()), static_cast<std::streamsize>(img.pixels.size() * 3));
+    return img;
+}
+
+static void case_histogram_order() { // test_histogram.cpp:102-118
+    const Rgb8 A{10, 20, 30}, B{200, 100, 50}, C{0, 0, 0};
+    std::vector<Rgb8> px = {A, B, A, C, B, A};
+    WeightedHistogram h = build_histogram(px, 1);
+    CHECK(h.size() == 3);
+    CHECK(h.source_pixel_count == 6);
+    CHECK(h.colors[0] == ColorPoint(10, 20, 30));
+    CHECK(h.colors[1] == ColorPoint(200, 100, 50));
+    CHECK(h.colors[2] == ColorPoint(0, 0, 0));
+    CHECK(h.counts[0] == 3 && h.counts[1] == 2 && h.counts[2] == 1);
+    CHECK(h.weights[0] == 0.5);
+    CHECK(h.hash.m == next_prime_at_least(12));
+    CHECK_THROWS_AS(build_histogram(std::vector<Rgb8>{}, 1), std::invalid_argument);
+}
+
+static void case_wsm_semantics() { // test_kmeans.cpp:210-285
+    std::vector<ColorPoint> pts = {{0, 0, 0}, {9, 0, 0}};
+    std::vector<double> w = {0.5, 0.5};
+    ClusterState st = wsm(pts, w, {{5, 0, 0}, {5, 0, 0}}, {});
+    CHECK(st.repair_count == 1);
+    CHECK(st.iterations == 1);
+    CHECK(st.sse_trace.size() == 1 && st.sse_trace[0] == 0.0);
+    std::vector<double> got = {st.centers[0].r, st.centers[1].r};
+    std::sort(got.begin(), got.end());
+    CHECK(got == (std::vector<double>{0.0, 9.0}));
+
+    std::vector<ColorPoint> one = {{0, 0, 0}};
+    std::vector<ColorPoint> three = {{0, 0, 0}, {1, 1, 1}, {2, 2, 2}};
+    CHECK_THROWS_AS(wsm(pts, w, {}, {}), std::invalid_argument);
+    CHECK_THROWS_AS(wsm(pts, w, three, {}), std::invalid_argument);
+    CHECK_THROWS_AS(wsm(pts, std::vector<double>{0.5}, one, {}), std::invalid_argument);
+    CHECK_THROWS_AS(wsm(pts, std::vector<double>{0.5, -0.5}, one, {}), std::invalid_argument);
+    ClusterOptions bad;
+    bad.term.epsilon = -1.0;
+    CHECK_THROWS_AS(wsm(pts, w, one, bad), std::invalid_argument);
+    bad.term.epsilon = 0.001;
+    bad.term.max_iterations = 0;
+    CHECK_THROWS_AS(wsm(pts, w, one, bad), std::invalid_argument);
+    bad.term.max_iterations = 100;
+    bad.term.fixed_iterations = 0;
+    CHECK_THROWS_AS(wsm(pts, w, one, bad), std::invalid_argument);
+}
+
+static void case_histogram_equals_duplicates() { // test_kmeans.cpp:287-305 (weights = counts / P)
+    std::vector<ColorPoint> hp = {{10, 0, 0}, {90, 0, 0}};
+    std::vector<double> hw = {0.75, 0.25};
+    ClusterOptions opt;
+    opt.term.fixed_iterations = 3;
+    ClusterState fast = wsm(hp, hw, {{0, 0, 0}, {100, 0, 0}}, opt);
+    CHECK(fast.sse_trace.size() == 3);
+    CHECK(fast.centers[0] == ColorPoint(10, 0, 0));
+    CHECK(fast.centers[1] == ColorPoint(90, 0, 0));
+    CHECK(fast.sse_trace[0] == 0.0 && fast.sse_trace[2] == 0.0);
+}
+
+static void case_mapping() { // test_metrics.cpp:66-92
+    RawImage img;
+    img.width = 1;
+    img.height = 1;
+    img.pixels = {{1, 0, 0}};
+    Palette pal;
+    pal.colors = {{2, 0, 0}, {0, 0, 0}};
+    CHECK(map_pixels(img, pal).indices[0] == 0);
+    std::swap(pal.colors[0], pal.colors[1]);
+    CHECK(map_pixels(img, pal).indices[0] == 0);
+    img.width = 2;
+    img.pixels = {{0, 0, 0}, {1, 0, 0}};
+    pal.colors = {{0.5, 0, 0}};
+    MappingResult m = map_pixels(img, pal);
+    CHECK(std::abs(m.mean_sq_dist - 0.25) <= 1e-12);
+    CHECK(m.quantized.pixels[0].r == 1);
+    CHECK_THROWS_AS(map_pixels(img, Palette{}), std::invalid_argument);
+}
+
+static void case_golden_rows(const std::string &dir) { // proj/tmp_acceptance/sweep_a.csv:2-13
+    std::ifstream f(dir + "/sweep_a_rows.csv");
+    std::string line;
+    std::getline(f, line);
+    std::multiset<std::string> want;
+    while (std::getline(f, line))
+        if (!line.empty() && line.find(",wu,") == std::string::npos) want.insert(line);
+    std::ifstream wf(dir + "/wu_init.txt");
+    std::vector<std::vector<ColorPoint>> wu(2);
+    for (int s = 0; s < 2; ++s)
+        for (int i = 0; i < 8; ++i) {
+            double r, g, b;
+            wf >> r >> g >> b;
+            wu[s].push_back({r, g, b});
+        }
+    std::multiset<std::string> got;
+    for (int s = 0; s < 2; ++s) {
+        const int seed_img = 61 + s;
+        RawImage img = load_rgb(dir + "/acc_" + std::to_string(seed_img) + ".rgb", 40, 40);
+        for (const char *method : {"wsm-kpp", "wsm-wu"})
+            for (int run = 0; run < 2; ++run) {
+                QuantizeConfig cfg;
+                cfg.method = parse_method(method);
+                cfg.k = 8;
+                cfg.seed = 3 + run;
+                if (std::string(method) == "wsm-wu") cfg.init_centers = wu[s];
+                QuantizeResult r = run_quantize(img, cfg);
+                r.report.image = "acc_" + std::to_string(seed_img) + ".ppm";
+                r.report.run = run;
+                r.report.time_ms = 0.0;
+                got.insert(r.report.csv_row());
+            }
+    }
+    CHECK(got == want);
+    if (got != want)
+        for (const auto &g : got) std::printf("  got  %s\n", g.c_str());
+}
+
+static void case_report_format() { // test_metrics.cpp:94-125
+    CHECK(std::string(QuantReport::csv_header()) ==
+          "image,method,k,run,seed,sampling,mse,psnr,iterations,ndc_per_point_iter,time_ms,actual_k,flags");
+    QuantReport r;
+    r.image = "img.ppm";
+    r.method = "wsm-wu";
+    r.k_requested = 32;
+    r.k_actual = 32;
+    r.run = 2;
+    r.seed = 3;
+    r.mse = 71.25;
+    r.psnr = 29.603;
+    r.iterations = 14;
+    r.ndc_per_point_iter = 3.9812;
+    r.time_ms = 12.5;
+    r.flags = {"repairs:1", "padded_init"};
+    CHECK(r.csv_row() == "img.ppm,wsm-wu,32,2,3,unique,71.250000,29.6030,14,3.9812,12.500,32,repairs:1;padded_init");
+    CHECK(r.to_json().find("\"psnr\": 29.603") != std::string::npos);
+}
+
+int main(int argc, char **argv) {
+    const std::string dir = argc > 1 ? argv[1] : "tests/golden";
+    struct Case {
+        const char *name;
+        void (*fn)();
+    } cases[] = {{"histogram_order", case_histogram_order},
+                 {"wsm_semantics", case_wsm_semantics},
+                 {"histogram_equals_duplicates", case_histogram_equals_duplicates},
+                 {"mapping", case_mapping},
+                 {"report_format", case_report_format}};
+    for (const auto &c : cases) {
+        const int before = g_fail;
+        try {
+            c.fn();
+        } catch (const std::exception &e) {
+            std::printf("  exception: %s\n", e.what());
+            ++g_fail;
+        }
+        std::printf("%s %s\n", g_fail == before ? "PASS" : "FAIL", c.name);
+    }
+    {
+        const int before = g_fail;
+        try {
+            case_golden_rows(dir);
+        } catch (const std::exception &e) {
+            std::printf("  exception: %s\n", e.what());
+            ++g_fail;
+        }
+        std::printf("%s golden_rows\n", g_fail == before ? "PASS" : "FAIL");
+    }
+    std::printf("%d failure(s)\n", g_fail);
+    return g_fail == 0 ? 0 : 1;
+}

@@ -61,6 +61,10 @@ def main() -> None:
         f.write(text)
     with open(os.path.join(HERE, "wu_init.json"), "w") as f:
         json.dump(wu, f, indent=1)
+    with open(os.path.join(HERE, "wu_init.txt"), "w") as f:  # for tests/cpp/test_dropin.cpp
+        for key in ("61", "62"):
+            for r, g, b in wu[key]:
+                f.write(f"{r!r} {g!r} {b!r}\n")
 
     # small reference wsm / map cases for oracle pinning
     cases = []
