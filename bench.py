@@ -56,60 +56,89 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle sampling during the timed region."""
+    """SM clock and throttle reasons sampled DURING the timed region.
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    Uses NVML (nvidia-ml-py) every 2 ms from a background thread (the cfg2
+    timed region is only ~25 ms); falls back to `nvidia-smi -lms 50`."""
+
+    REASONS = {  # nvmlClocksEventReason* bits
+        0x0000000000000008: "hw_slowdown",
+        0x0000000000000040: "hw_thermal_slowdown",
+        0x0000000000000020: "sw_thermal_slowdown",
+        0x0000000000000004: "sw_power_cap",
+    }
 
     def __init__(self, device: int):
         self.device = device
-        self.proc = None
-        self.lines = []
+        self.sm, self.mx, self.reasons = [], [], set()
+        self.stop = threading.Event()
+        self.nvml = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-        except (FileNotFoundError, OSError):
-            self.proc = None
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            self.mx.append(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+            self.t = threading.Thread(target=self._run_nvml, daemon=True)
+        except Exception:
+            self.nvml = None
+            self.t = threading.Thread(target=self._run_smi, daemon=True)
+        self.t.start()
+        time.sleep(0.005)
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _run_nvml(self):
+        nv = self.nvml
+        while not self.stop.is_set():
+            try:
+                self.sm.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                bits = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for b, name in self.REASONS.items():
+                    if bits & b:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def _run_smi(self):
+        fields = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                  "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                  "clocks_event_reasons.sw_power_cap")
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        try:
+            proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={fields}",
+                                     "--format=csv,noheader,nounits", "-lms", "50"],
+                                    stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (FileNotFoundError, OSError):
+            return
+        for line in proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 6:
+                try:
+                    self.sm.append(float(parts[0]))
+                    self.mx.append(float(parts[1]))
+                except ValueError:
+                    pass
+                for nm, v in zip(names, parts[2:6]):
+                    if v.lower() == "active":
+                        self.reasons.add(nm)
+            if self.stop.is_set():
+                break
+        proc.terminate()
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+        self.stop.set()
+        self.t.join(timeout=5)
 
     def summary(self):
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 6:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx.append(float(parts[1]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[2:6]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
-                "reasons": sorted(reasons), "samples": len(sm)}
+        if not self.sm:
+            return {"sm_mhz": None, "sm_max_mhz": max(self.mx) if self.mx else None,
+                    "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": max(self.mx) if self.mx else None,
+                "reasons": sorted(self.reasons), "samples": len(self.sm),
+                "source": "nvml 2 ms" if self.nvml else "nvidia-smi 50 ms"}
 
 
 # ---------------------------------------------------------------------------
@@ -297,32 +326,48 @@ def run_ours(args, cfg):
         dist.all_reduce(v)
         lloyd_rate = float(v.item())
 
-    # roofline of the dominant kernel: the Lloyd sweep (FP32 pipe)
+    # roofline of the dominant kernel (FP32 pipe). Small substrates run the
+    # whole Lloyd loop as ONE persistent kernel (lloyd_persistent_kernel): its
+    # launch duration is timed over the timed region. Large substrates run the
+    # sweep kernel once per iteration inside a CUDA graph: it is timed by
+    # back-to-back launches on the final state (cqg_bench_sweep, CUDA events).
     peaks, peak_kind = measured_peaks()
     sms = torch.cuda.get_device_properties(local).multi_processor_count
     fp32_peak = sms * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
-    sweep_ms = prof.ms[cabi.PROF_SWEEP]
-    sweep_launch = max(int(prof.launches[cabi.PROF_SWEEP]), 1)
-    sweep_units = prof.units[cabi.PROF_SWEEP]
-    achieved = 8.0 * sweep_units / (sweep_ms / 1e3) / 1e12 if sweep_ms > 0 else None
+    names = ["sweep", "map_sweep", "histogram", "pixel_map", "init", "replay", "ndc", "lloyd_loop"]
     stage_share = {}
-    names = ["sweep", "map_sweep", "histogram", "pixel_map", "init", "replay", "ndc"]
     for i, nm in enumerate(names):
         stage_share[nm] = {"ms_per_step": prof.ms[i] / args.steps,
                            "launches_per_step": prof.launches[i] / args.steps}
+    iso_ms, iso_units = ctx.bench_sweep(20)
+    iso_achieved = 8.0 * iso_units / (iso_ms / 1e3) / 1e12
+    persistent = prof.launches[cabi.PROF_SWEEP] == 0 and prof.launches[cabi.PROF_LLOYD] > 0
+    if persistent:
+        kname = "lloyd_persistent_kernel (whole Lloyd loop, one launch per run)"
+        k_ms = prof.ms[cabi.PROF_LLOYD] / max(int(prof.launches[cabi.PROF_LLOYD]), 1)
+        achieved = 8.0 * prof.units[cabi.PROF_LLOYD] / (prof.ms[cabi.PROF_LLOYD] / 1e3) / 1e12
+        k_share = prof.ms[cabi.PROF_LLOYD] / args.steps / ms_per_step
+    else:
+        kname = "sweep_kernel<WALK> (Lloyd assignment, one launch per iteration)"
+        k_ms = iso_ms
+        achieved = iso_achieved
+        iters_all = sum(s.lloyd.iterations for st in all_stats for s in st)
+        k_share = iso_ms * iters_all / args.steps / ms_per_step
     traffic = None
     tpath = os.path.join(ROOT, "profiles", f"ncu_traffic_{cfg.name}.json")
     if os.path.exists(tpath):
         with open(tpath) as f:
-            traffic = json.load(f).get("sweep_dram_bytes_per_launch")
+            traffic = json.load(f).get("dominant_dram_bytes_per_launch")
     roofline = {
-        "bound": "fp32", "kernel": "sweep_kernel (Lloyd assignment)",
+        "bound": "fp32", "kernel": kname,
         "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
         "frac": (achieved / fp32_peak) if achieved else None, "traffic": traffic,
         "peak_source": f"{sms} SMs x 128 FP32 lanes x 2 x sm_max_mhz ({peak_kind} MEASURED_PEAKS.json)",
-        "algorithmic_unit": "8 FLOP per (unique colour, centre) pair, full-sweep equivalent",
-        "avg_launch_ms": sweep_ms / sweep_launch,
-        "launch_share_of_step": (sweep_ms / args.steps) / ms_per_step,
+        "algorithmic_unit": "8 FLOP per (unique colour, centre) pair, full-sweep equivalent N'.K per iteration",
+        "avg_launch_ms": k_ms,
+        "launch_share_of_step": k_share,
+        "sweep_isolated": {"ms_per_launch": iso_ms, "achieved": iso_achieved,
+                           "frac": iso_achieved / fp32_peak, "units_per_launch": iso_units},
     }
     hist_ms = prof.ms[cabi.PROF_HIST]
     pix_ms = prof.ms[cabi.PROF_PIXEL]

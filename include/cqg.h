@@ -114,6 +114,7 @@ const char *cqg_version(void);
 #define CQG_PROF_INIT 4      /* initialiser kernel (units: N' x (K-1) distance updates) */
 #define CQG_PROF_REPLAY 5    /* exact FP64 replays (units: queued points) */
 #define CQG_PROF_NDC 6       /* per-point distance-count (NDC) pass (units: points) */
+#define CQG_PROF_LLOYD 7     /* whole Lloyd loop launches (persistent kernel / graph): units = N' x K x iterations */
 #define CQG_PROF_N 8
 typedef struct {
     double ms[CQG_PROF_N];
@@ -122,6 +123,12 @@ typedef struct {
 } cqg_profile;
 int cqg_set_profiling(cqg_ctx *ctx, int on);
 int cqg_read_profile(cqg_ctx *ctx, cqg_profile *out, int reset);
+/* Kernel microbenchmark on the context's last Lloyd state: `reps` back-to-back
+ * launches of the WALK-mode sweep kernel, bracketed by CUDA events on the
+ * context stream. Returns the average device ms per launch and the
+ * algorithmic units per launch (unique colours x K). Perturbs the context's
+ * Lloyd scratch state (call after the results have been read). */
+int cqg_bench_sweep(cqg_ctx *ctx, int reps, double *ms_per_launch, double *units_per_launch);
 
 /* ---- stage 1: unique colours in first-occurrence order -------------------
  * rgb: P*3 bytes. colors/counts/first: capacity min(P, 2^24) each; `first`

@@ -33,10 +33,10 @@ INIT_GIVEN = 2
 EXPORTS = (
     "cqg_create", "cqg_destroy", "cqg_last_error", "cqg_set_stream", "cqg_launch_count",
     "cqg_version", "cqg_histogram", "cqg_init_maximin", "cqg_init_kmeanspp", "cqg_lloyd",
-    "cqg_map", "cqg_quantize", "cqg_set_profiling", "cqg_read_profile",
+    "cqg_map", "cqg_quantize", "cqg_set_profiling", "cqg_read_profile", "cqg_bench_sweep",
 )
 
-PROF_SWEEP, PROF_MAPSWEEP, PROF_HIST, PROF_PIXEL, PROF_INIT, PROF_REPLAY, PROF_NDC = range(7)
+PROF_SWEEP, PROF_MAPSWEEP, PROF_HIST, PROF_PIXEL, PROF_INIT, PROF_REPLAY, PROF_NDC, PROF_LLOYD = range(8)
 
 
 class Term(C.Structure):
@@ -108,6 +108,8 @@ def load(path: str = LIB_PATH):
                                    C.POINTER(QuantizeStats)]
         L.cqg_set_profiling.argtypes = [vp, i32]
         L.cqg_read_profile.argtypes = [vp, C.POINTER(Profile), i32]
+        L.cqg_bench_sweep.argtypes = [vp, i32, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        L.cqg_bench_sweep.restype = i32
         for name in ("cqg_set_profiling", "cqg_read_profile", "cqg_histogram", "cqg_init_maximin", "cqg_init_kmeanspp", "cqg_lloyd",
                      "cqg_map", "cqg_quantize", "cqg_set_stream"):
             getattr(L, name).restype = i32
@@ -176,6 +178,13 @@ class Context:
         p = Profile()
         check(self.L.cqg_read_profile(self.h, C.byref(p), 1 if reset else 0))
         return p
+
+    def bench_sweep(self, reps: int = 20):
+        """(ms per launch, units per launch) of back-to-back WALK sweeps on the
+        context's last Lloyd state (cqg_bench_sweep)."""
+        ms, units = C.c_double(0), C.c_double(0)
+        check(self.L.cqg_bench_sweep(self.h, reps, C.byref(ms), C.byref(units)))
+        return ms.value, units.value
 
     def set_stream(self, stream_ptr: int | None):
         check(self.L.cqg_set_stream(self.h, stream_ptr))

@@ -115,11 +115,16 @@ int prof_begin(cqg_ctx *ctx) {
     return e;
 }
 
-void prof_end(cqg_ctx *ctx, int cat, int begin, double units) {
-    if (!ctx->prof_on || begin < 0) return;
+int prof_end(cqg_ctx *ctx, int cat, int begin, double units) {
+    if (!ctx->prof_on || begin < 0) return -1;
     const int e = take_event(ctx);
     CQG_CUDA(cudaEventRecord(ctx->ev_pool[e], ctx->stream));
     ctx->prof_recs.push_back({cat, begin, e, units});
+    return (int)ctx->prof_recs.size() - 1;
+}
+
+void prof_add_units(cqg_ctx *ctx, int rec, double units) {
+    if (rec >= 0 && rec < (int)ctx->prof_recs.size()) ctx->prof_recs[rec].units += units;
 }
 
 static void prof_drain(cqg_ctx *ctx) {
@@ -275,6 +280,18 @@ int cqg_read_profile(cqg_ctx *ctx, cqg_profile *out, int reset) {
                 ctx->prof_launches[i] = 0;
             }
         }
+    });
+}
+
+int cqg_bench_sweep(cqg_ctx *ctx, int reps, double *ms_per_launch, double *units_per_launch) {
+    return guarded([&] {
+        use_device(ctx);
+        if (!ctx->have_last_sweep) fail(CQG_E_INVALID, "cqg_bench_sweep: no Lloyd run on this context yet");
+        if (reps < 1) reps = 1;
+        double ms = 0.0, units = 0.0;
+        bench_sweep_dev(ctx, reps, &ms, &units);
+        if (ms_per_launch) *ms_per_launch = ms;
+        if (units_per_launch) *units_per_launch = units;
     });
 }
 

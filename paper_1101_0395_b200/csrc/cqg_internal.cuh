@@ -143,6 +143,9 @@ struct cqg_ctx {
     };
     std::vector<ProfRec> prof_recs;
     double prof_ms[CQG_PROF_N] = {};
+    // last Lloyd sweep launch (for cqg_bench_sweep)
+    unsigned char last_sweep[512] = {};
+    bool have_last_sweep = false;
     double prof_units[CQG_PROF_N] = {};
     unsigned long long prof_launches[CQG_PROF_N] = {};
 };
@@ -188,7 +191,8 @@ __host__ __device__ __forceinline__ unsigned ceil_div(unsigned long long a, unsi
 bool is_device_ptr(const void *p);
 // profiling: prof_begin records a start event (returns -1 when profiling is off)
 int prof_begin(cqg_ctx *ctx);
-void prof_end(cqg_ctx *ctx, int cat, int begin, double units);
+int prof_end(cqg_ctx *ctx, int cat, int begin, double units); // returns the record index (or -1)
+void prof_add_units(cqg_ctx *ctx, int rec, double units);
 void launched(cqg_ctx *ctx, int n = 1);
 void release_graphs(cqg_ctx *ctx);
 // copy `bytes` from user pointer (host or device) into a device buffer and
@@ -213,6 +217,7 @@ LloydOut lloyd_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *count
                    double *centers_d, double *sse_host, uint32_t *hist_labels_user,
                    double *hist_centers_user);
 
+void bench_sweep_dev(cqg_ctx *ctx, int reps, double *ms, double *units);
 double map_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P, const uint32_t *colors_d,
                const uint32_t *counts_d, uint64_t n, const double *pal_d, int k, void *indices_d,
                int index_bytes, uint8_t *quant_d);

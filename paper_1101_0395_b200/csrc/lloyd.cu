@@ -16,7 +16,11 @@
 #include <algorithm>
 #include <cstring>
 
+#include <cooperative_groups.h>
+
 #include "sweep.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace cqg {
 
@@ -98,17 +102,22 @@ struct IterArgs {
     int Kpow;
     cudaGraphConditionalHandle cond;
     int use_cond;
+    int reset_qn; // persistent kernel: clear the replay queue counter
 };
 
-// K blocks. Block 0 finalises the iteration; every block builds one row of the
-// next iteration's walk table from the new centres (kept in shared memory).
-__global__ void __launch_bounds__(1024) iter_end_kernel(IterArgs a) {
-    extern __shared__ double sm[];
+// Finalise one iteration and build the next walk table. Called by every block
+// of a grid (iter_end_kernel, or the persistent kernel's phase C): block 0
+// writes centres / SSE / termination status; every block computes the centres
+// in shared memory; rows of the walk table are distributed over the blocks.
+// fc_dst/tau_dst receive the FP32 sweep table: global (block 0 only) or this
+// block's shared memory (fc_every_block). Returns false when a cluster is empty
+// (status 2 written, nothing else changed).
+__device__ bool iter_end_body(const IterArgs &a, double *sm, float *fc_dst, float *tau_dst, bool fc_every_block) {
     const int K = a.K;
     double *s_c = sm;               // 3K centres
     double *s_a = sm + 3 * K;       // K per-cluster SSE terms (block 0)
-    double *s_d = sm + 4 * K;       // K row distances
-    int *s_rank = reinterpret_cast<int *>(sm + 5 * K);
+    double *s_d = sm + 4 * K;       // Kpow row distances (sort keys)
+    int *s_rank = reinterpret_cast<int *>(sm + 4 * K + a.Kpow); // Kpow payload indices
     __shared__ int s_empty;
     if (threadIdx.x == 0) s_empty = 0;
     __syncthreads();
@@ -135,7 +144,7 @@ __global__ void __launch_bounds__(1024) iter_end_kernel(IterArgs a) {
             a.st->n_flagged = *a.qn;
             if (a.use_cond) cudaGraphSetConditional(a.cond, 0);
         }
-        return;
+        return false;
     }
     if (blockIdx.x == 0) {
         for (int k = threadIdx.x; k < 3 * K; k += blockDim.x) a.cen[k] = s_c[k];
@@ -156,53 +165,126 @@ __global__ void __launch_bounds__(1024) iter_end_kernel(IterArgs a) {
                 if (!done && iter >= a.limit) done = 1;
             }
             if (iter == 1) *a.ndc += (unsigned long long)a.n_points * (unsigned long long)K;
-            *a.flagged += *a.qn;
+            const uint32_t nq = *a.qn;
+            *a.flagged += nq;
+            if (a.reset_qn) *const_cast<uint32_t *>(a.qn) = 0;
             a.st->state = done ? 1 : 0;
             a.st->iteration = iter;
-            a.st->n_flagged = *a.qn;
+            a.st->n_flagged = nq;
             a.st->sse = sse;
             *a.iter_dev = iter;
             if (a.use_cond) cudaGraphSetConditional(a.cond, done ? 0 : 1);
         }
-        fc_block(s_c, K, a.Kp, a.fc, a.tau);
     }
-    // walk table row i (kmeans.cpp:14-38): sort by (d, index), self first
+    if (blockIdx.x == 0 || fc_every_block) fc_block(s_c, K, a.Kp, fc_dst, tau_dst);
+    // walk table row i (kmeans.cpp:14-38): sort by (d, index), then rotate self
+    // to the front. Block bitonic sort over Kpow keys (padding = +inf).
+    const double kInf = __longlong_as_double(0x7FF0000000000000ll);
     for (int i = blockIdx.x; i < K; i += gridDim.x) {
         const double cr = s_c[3 * i], cg = s_c[3 * i + 1], cb = s_c[3 * i + 2];
-        for (int j = threadIdx.x; j < K; j += blockDim.x) {
-            const double d = d2_exact(cr, cg, cb, s_c[3 * j], s_c[3 * j + 1], s_c[3 * j + 2]);
-            s_d[j] = d;
-            a.dtab[(size_t)i * K + j] = d;
-        }
-        __syncthreads();
-        // rank of (d_j, j) by (distance, index): 4 threads per element, each
-        // counting a quarter of the row, combined by shuffles
-        for (int e = threadIdx.x; e < 4 * ((K + 7) & ~7); e += blockDim.x) {
-            const int j = e >> 2, part = e & 3;
-            int rank = 0;
+        for (int j = threadIdx.x; j < a.Kpow; j += blockDim.x) {
+            double d = kInf;
             if (j < K) {
-                const double d = s_d[j];
-                const int t0 = part * ((K + 3) / 4), t1 = min(K, t0 + (K + 3) / 4);
-                for (int t = t0; t < t1; ++t) {
-                    const double v = s_d[t];
-                    rank += (v < d) || (v == d && t < j);
-                }
+                d = d2_exact(cr, cg, cb, s_c[3 * j], s_c[3 * j + 1], s_c[3 * j + 2]);
+                a.dtab[(size_t)i * K + j] = d;
             }
-            rank += __shfl_xor_sync(0xffffffffu, rank, 1);
-            rank += __shfl_xor_sync(0xffffffffu, rank, 2);
-            if (part == 0 && j < K) s_rank[j] = rank;
+            s_d[j] = d;
+            s_rank[j] = j; // index payload
         }
         __syncthreads();
-        const int rself = s_rank[i];
-        for (int j = threadIdx.x; j < K; j += blockDim.x) {
-            const int rk = s_rank[j];
-            const int pos = (j == i) ? 0 : (rk < rself ? rk + 1 : rk);
-            a.order[(size_t)i * K + pos] = (uint32_t)j;
-            a.dsorted[(size_t)i * a.Kpow + pos] = s_d[j];
+        for (int size = 2; size <= a.Kpow; size <<= 1) {
+            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                for (int t = threadIdx.x; t < (a.Kpow >> 1); t += blockDim.x) {
+                    const int lo_i = 2 * t - (t & (stride - 1));
+                    const int hi_i = lo_i + stride;
+                    const bool up = (lo_i & size) == 0;
+                    const double d0 = s_d[lo_i], d1 = s_d[hi_i];
+                    const int i0 = s_rank[lo_i], i1 = s_rank[hi_i];
+                    const bool gt = d0 > d1 || (d0 == d1 && i0 > i1);
+                    if (gt == up) {
+                        s_d[lo_i] = d1;
+                        s_d[hi_i] = d0;
+                        s_rank[lo_i] = i1;
+                        s_rank[hi_i] = i0;
+                    }
+                }
+                __syncthreads();
+            }
         }
-        for (int j = K + threadIdx.x; j < a.Kpow; j += blockDim.x)
-            a.dsorted[(size_t)i * a.Kpow + j] = __longlong_as_double(0x7FF0000000000000ll); // +inf
+        // position of self, then rotate it to the front
+        __shared__ int s_self;
+        for (int p = threadIdx.x; p < K; p += blockDim.x)
+            if (s_rank[p] == i) s_self = p;
         __syncthreads();
+        const int ps = s_self;
+        for (int p = threadIdx.x; p < a.Kpow; p += blockDim.x) {
+            const int np = p < ps ? p + 1 : (p == ps ? 0 : p);
+            if (p < K) a.order[(size_t)i * K + np] = (uint32_t)s_rank[p];
+            a.dsorted[(size_t)i * a.Kpow + np] = s_d[p];
+        }
+        __syncthreads();
+    }
+    return true;
+}
+
+__global__ void __launch_bounds__(1024) iter_end_kernel(IterArgs a) {
+    extern __shared__ double sm[];
+    iter_end_body(a, sm, a.fc, a.tau, false);
+}
+
+// Persistent cooperative Lloyd loop for small substrates: one launch runs all
+// iterations, two grid barriers per iteration (sweep + block-local replay |
+// finalise + walk table). Every block keeps its own FP32 centre table in shared memory.
+// Exits early (state 2) on an empty cluster; the host repairs and relaunches.
+template <int PPT>
+__global__ void __launch_bounds__(kSweepThreads, 2) lloyd_persistent_kernel(SweepArgs a, IterArgs ia, int first_full) {
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ __align__(16) double psm[];
+    const int K = a.K, Kp = a.Kp;
+    float *s_fc = reinterpret_cast<float *>(psm);          // 4 Kp
+    float *s_tau = s_fc + 4 * Kp;                           // 2 (+2 pad)
+    uint32_t *s_acc = reinterpret_cast<uint32_t *>(s_tau + 4); // 10 K u32 (= 5 K u64)
+    unsigned long long *s_acc64 = reinterpret_cast<unsigned long long *>(s_acc);
+    double *s_end = reinterpret_cast<double *>(s_acc + 10 * K); // 5 K doubles + K ints
+    fc_block(a.cen, K, Kp, s_fc, s_tau);
+    const uint64_t chunk = (a.n + gridDim.x - 1) / gridDim.x;
+    const uint64_t lo = (uint64_t)blockIdx.x * chunk;
+    const uint64_t hi = lo + chunk < a.n ? lo + chunk : a.n;
+    const uint32_t warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    __shared__ uint32_t s_qn;
+    SweepArgs la = a; // block-local near-tie queue
+    la.queue = a.queue + lo;
+    la.qn = &s_qn;
+    bool full = first_full != 0;
+    for (;;) {
+        // phase A: NDC, sweep and the exact replay of this block's own queued
+        // points (block-local queue in slots [lo, hi), counter in shared memory)
+        if (threadIdx.x == 0) s_qn = 0;
+        if (full) {
+            for (int i = threadIdx.x; i < K * kAccPerCluster; i += blockDim.x) s_acc[i] = 0;
+            __syncthreads();
+            sweep_range<MODE_FULL, PPT>(la, lo, hi, s_fc, s_acc, s_tau[0], s_tau[1]);
+            __syncthreads();
+            replay_range<MODE_FULL>(la, warp, nw);
+        } else {
+            unsigned long long nd = ndc_range<2>(a.colors, a.labels, lo, hi, 0, 2ull * blockDim.x, a.cen,
+                                                 a.dsorted, a.Kpow);
+            for (int o = 16; o; o >>= 1) nd += __shfl_xor_sync(0xffffffffu, nd, o);
+            if ((threadIdx.x & 31) == 0 && nd) atomicAdd(a.ndc, nd);
+            for (int i = threadIdx.x; i < K * 5; i += blockDim.x) s_acc64[i] = 0;
+            __syncthreads();
+            sweep_range<MODE_WALK, PPT>(la, lo, hi, s_fc, s_acc, s_tau[0], s_tau[1]);
+            __syncthreads();
+            flush_acc64(s_acc64, a.mom, K);
+            replay_range<MODE_WALK>(la, warp, nw);
+        }
+        if (threadIdx.x == 0 && s_qn) atomicAdd(a.qn, s_qn);
+        grid.sync();
+        const bool ok = iter_end_body(ia, s_end, s_fc, s_tau, true);
+        grid.sync();
+        if (!ok) break;
+        if (*reinterpret_cast<volatile int *>(&ia.st->state) != 0) break;
+        full = false;
     }
 }
 
@@ -311,10 +393,16 @@ size_t sweep_smem_bytes(int K, int Kp) {
 
 template <int MODE, int PPT>
 static int sweep_bps(size_t smem) {
+    // occupancy per (kernel, smem): cached so launches do no host-side queries
+    static thread_local size_t c_smem = (size_t)-1;
+    static thread_local int c_bps = 1;
+    if (c_smem == smem) return c_bps;
     int bps = 0;
     CQG_CUDA(cudaFuncSetAttribute(sweep_kernel<MODE, PPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CQG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, sweep_kernel<MODE, PPT>, kSweepThreads, smem));
-    return bps < 1 ? 1 : bps;
+    c_bps = bps < 1 ? 1 : bps;
+    c_smem = smem;
+    return c_bps;
 }
 
 template <int MODE, int PPT>
@@ -333,34 +421,88 @@ static void launch_sweep_mode(cqg_ctx *ctx, const SweepArgs &a) {
     const uint64_t n = a.n;
     const uint64_t sms = (uint64_t)ctx->num_sms;
     if (MODE == MODE_WALK) {
-        const int pn = prof_begin(ctx);
         const size_t csm = a.K <= 2048 ? (size_t)a.K * 24 : 0;
-        if (csm > 48 * 1024) {
-            CQG_CUDA(cudaFuncSetAttribute(ndc_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
-            CQG_CUDA(cudaFuncSetAttribute(ndc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
+        static thread_local bool attr = false;
+        if (!attr && csm > 48 * 1024) {
+            CQG_CUDA(cudaFuncSetAttribute(ndc_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2048 * 24));
+            CQG_CUDA(cudaFuncSetAttribute(ndc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2048 * 24));
+            attr = true;
         }
-        if (n >= (uint64_t)ctx->num_sms * 4 * 256 * 8)
-            ndc_kernel<8><<<pick_grid(ctx, n, 2048, 4), 256, csm, ctx->stream>>>(a.colors, a.labels, n, a.cen,
-                                                                              a.dsorted, a.K, a.Kpow, a.ndc);
+        const bool big = n >= (uint64_t)ctx->num_sms * 4 * 256 * 8;
+        const int g = big ? pick_grid(ctx, n, 2048, 4) : pick_grid(ctx, n, 512, 8);
+        const int pn = prof_begin(ctx);
+        if (big)
+            ndc_kernel<8><<<g, 256, csm, ctx->stream>>>(a.colors, a.labels, n, a.cen, a.dsorted, a.K, a.Kpow, a.ndc);
         else
-            ndc_kernel<2><<<pick_grid(ctx, n, 512, 8), 256, csm, ctx->stream>>>(a.colors, a.labels, n, a.cen,
-                                                                             a.dsorted, a.K, a.Kpow, a.ndc);
+            ndc_kernel<2><<<g, 256, csm, ctx->stream>>>(a.colors, a.labels, n, a.cen, a.dsorted, a.K, a.Kpow, a.ndc);
         prof_end(ctx, CQG_PROF_NDC, pn, (double)n);
         launched(ctx);
     }
-    const int pb = prof_begin(ctx);
     // smallest points-per-thread whose single wave covers all points (fewest
     // idle lanes, most blocks); large inputs loop over 8-point tiles
     const int b2 = sweep_bps<MODE, 2>(smem), b4 = sweep_bps<MODE, 4>(smem), b8 = sweep_bps<MODE, 8>(smem);
-    if (n <= sms * b2 * kSweepThreads * 2) launch_ppt<MODE, 2>(ctx, a, smem, b2);
-    else if (n <= sms * b4 * kSweepThreads * 4) launch_ppt<MODE, 4>(ctx, a, smem, b4);
-    else launch_ppt<MODE, 8>(ctx, a, smem, b8);
+    int ppt, bps;
+    if (n <= sms * b2 * kSweepThreads * 2) ppt = 2, bps = b2;
+    else if (n <= sms * b4 * kSweepThreads * 4) ppt = 4, bps = b4;
+    else ppt = 8, bps = b8;
+    uint64_t grid = sms * (uint64_t)bps;
+    const uint64_t cap = (n + 63) / 64; // at least 64 points per block
+    if (grid > cap) grid = cap;
+    if (grid < 1) grid = 1;
+    const int rg = pick_grid(ctx, n * 32 / 256 + 1, 256, 2);
+    const int pb = prof_begin(ctx);
+    if (ppt == 2) sweep_kernel<MODE, 2><<<(unsigned)grid, kSweepThreads, smem, ctx->stream>>>(a);
+    else if (ppt == 4) sweep_kernel<MODE, 4><<<(unsigned)grid, kSweepThreads, smem, ctx->stream>>>(a);
+    else sweep_kernel<MODE, 8><<<(unsigned)grid, kSweepThreads, smem, ctx->stream>>>(a);
     prof_end(ctx, MODE == MODE_MAP ? CQG_PROF_MAPSWEEP : CQG_PROF_SWEEP, pb, (double)n * (double)a.K);
     const int pr = prof_begin(ctx);
-    replay_kernel<MODE><<<pick_grid(ctx, n * 32 / 256 + 1, 256, 2), 256, 0, ctx->stream>>>(a);
+    replay_kernel<MODE><<<rg, 256, 0, ctx->stream>>>(a);
     prof_end(ctx, CQG_PROF_REPLAY, pr, 0.0);
     CQG_CUDA(cudaGetLastError());
     launched(ctx, 2);
+    if (MODE == MODE_WALK) {
+        static_assert(sizeof(SweepArgs) <= sizeof(ctx->last_sweep), "scratch too small");
+        std::memcpy(ctx->last_sweep, &a, sizeof(SweepArgs));
+        ctx->have_last_sweep = true;
+    }
+}
+
+// Isolated sweep timing (cqg_bench_sweep): reps back-to-back WALK sweeps.
+void bench_sweep_dev(cqg_ctx *ctx, int reps, double *ms, double *units) {
+    SweepArgs a;
+    std::memcpy(&a, ctx->last_sweep, sizeof(SweepArgs));
+    const size_t smem = sweep_smem_bytes(a.K, a.Kp);
+    const uint64_t sms = (uint64_t)ctx->num_sms, n = a.n;
+    const int b2 = sweep_bps<MODE_WALK, 2>(smem), b4 = sweep_bps<MODE_WALK, 4>(smem),
+              b8 = sweep_bps<MODE_WALK, 8>(smem);
+    int ppt, bps;
+    if (n <= sms * b2 * kSweepThreads * 2) ppt = 2, bps = b2;
+    else if (n <= sms * b4 * kSweepThreads * 4) ppt = 4, bps = b4;
+    else ppt = 8, bps = b8;
+    uint64_t grid = sms * (uint64_t)bps;
+    const uint64_t cap = (n + 63) / 64;
+    if (grid > cap) grid = cap;
+    if (grid < 1) grid = 1;
+    cudaEvent_t e0, e1;
+    CQG_CUDA(cudaEventCreate(&e0));
+    CQG_CUDA(cudaEventCreate(&e1));
+    auto one = [&]() {
+        if (ppt == 2) sweep_kernel<MODE_WALK, 2><<<(unsigned)grid, kSweepThreads, smem, ctx->stream>>>(a);
+        else if (ppt == 4) sweep_kernel<MODE_WALK, 4><<<(unsigned)grid, kSweepThreads, smem, ctx->stream>>>(a);
+        else sweep_kernel<MODE_WALK, 8><<<(unsigned)grid, kSweepThreads, smem, ctx->stream>>>(a);
+    };
+    one(); // warm
+    CQG_CUDA(cudaEventRecord(e0, ctx->stream));
+    for (int r = 0; r < reps; ++r) one();
+    CQG_CUDA(cudaEventRecord(e1, ctx->stream));
+    CQG_CUDA(cudaEventSynchronize(e1));
+    float t = 0.f;
+    CQG_CUDA(cudaEventElapsedTime(&t, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    launched(ctx, reps + 1);
+    *ms = (double)t / reps;
+    *units = (double)n * (double)a.K;
 }
 
 void launch_sweep(cqg_ctx *ctx, int mode, const SweepArgs &a) {
@@ -422,13 +564,20 @@ static int repair_loop(cqg_ctx *ctx, const uint32_t *colors, const uint32_t *cou
     return repairs;
 }
 
-static size_t iter_end_smem(int K) { return (size_t)K * (5 * sizeof(double) + sizeof(int)); }
+static int kpow_of(int K) {
+    int p = 1;
+    while (p < K) p <<= 1;
+    return p;
+}
+static size_t iter_end_smem(int K) {
+    return (size_t)K * 4 * sizeof(double) + (size_t)kpow_of(K) * (sizeof(double) + sizeof(int));
+}
 
 static void launch_iter_end(cqg_ctx *ctx, const IterArgs &ia) {
     const size_t smem = iter_end_smem(ia.K);
     if (smem > 48 * 1024)
         CQG_CUDA(cudaFuncSetAttribute(iter_end_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    iter_end_kernel<<<ia.K, ia.K >= 256 ? 1024 : 256, smem, ctx->stream>>>(ia);
+    iter_end_kernel<<<ia.K, 256, smem, ctx->stream>>>(ia);
     launched(ctx);
 }
 
@@ -477,6 +626,43 @@ void release_graphs(cqg_ctx *ctx) {
     ctx->loop_exec = nullptr;
     ctx->loop_graph = nullptr;
     ctx->loop_key.clear();
+}
+
+
+static size_t persist_smem(int K, int Kp) {
+    return (size_t)4 * Kp * sizeof(float) + 4 * sizeof(float) + (size_t)10 * K * sizeof(uint32_t) +
+           iter_end_smem(K);
+}
+
+// Launch the persistent loop if it fits co-resident; returns false otherwise.
+static bool launch_persistent(cqg_ctx *ctx, const SweepArgs &a, IterArgs ia, bool first_full) {
+    const size_t smem = persist_smem(a.K, a.Kp);
+    const int ppt = a.n <= (uint64_t)ctx->num_sms * 2 * kSweepThreads * 2 ? 2 : 4;
+    const void *kern = ppt == 2 ? (const void *)lloyd_persistent_kernel<2> : (const void *)lloyd_persistent_kernel<4>;
+    static thread_local const void *c_kern = nullptr;
+    static thread_local size_t c_smem = 0;
+    static thread_local int c_bps = 0;
+    int bps = c_bps;
+    if (c_kern != kern || c_smem != smem) {
+        CQG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CQG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, kSweepThreads, smem));
+        c_kern = kern;
+        c_smem = smem;
+        c_bps = bps;
+    }
+    if (bps < 1) return false;
+    uint64_t grid = (uint64_t)ctx->num_sms * (uint64_t)bps;
+    const uint64_t cap = (a.n + 63) / 64;
+    if (grid > cap) grid = cap;
+    if (grid < 1) grid = 1;
+    ia.use_cond = 0;
+    ia.reset_qn = 1;
+    SweepArgs aa = a;
+    int ff = first_full ? 1 : 0;
+    void *args[] = {&aa, &ia, &ff};
+    CQG_CUDA(cudaLaunchCooperativeKernel(kern, dim3((unsigned)grid), dim3(kSweepThreads), args, smem, ctx->stream));
+    launched(ctx);
+    return true;
 }
 
 LloydOut lloyd_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *counts_d, uint64_t n,
@@ -535,6 +721,8 @@ LloydOut lloyd_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *count
     a.K = K;
     a.Kp = Kp;
     a.Kpow = Kpow;
+    std::memcpy(ctx->last_sweep, &a, sizeof(SweepArgs)); // for cqg_bench_sweep
+    ctx->have_last_sweep = true;
 
     IterArgs ia{};
     ia.mom = mom;
@@ -562,15 +750,27 @@ LloydOut lloyd_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *count
 
     // The graph path needs no per-iteration host work: used unless history is
     // recorded (per-iteration copies) or kernel profiling is on (per-launch events).
-    const bool use_graph = !hist && !ctx->prof_on && ctx->use_graphs;
+    const bool use_graph = !hist && ctx->use_graphs;
+    // small substrates: the whole loop as one persistent cooperative kernel
+    const bool persistent = use_graph && K <= 1024 &&
+                            n <= (uint64_t)ctx->num_sms * 2 * kSweepThreads * 4 * 2;
     LloydOut out;
     int iter = 0;
     bool done = false;
+    if (persistent) CQG_CUDA(cudaMemsetAsync(qn, 0, 4, s));
     while (!done) {
         const bool first = (iter == 0);
-        if (!first && use_graph) {
+        int rec = -1;
+        const int before = iter;
+        if (persistent) {
+            const int pb = prof_begin(ctx);
+            if (!launch_persistent(ctx, a, ia, first)) fail(CQG_E_CUDA, "persistent Lloyd kernel does not fit");
+            rec = prof_end(ctx, CQG_PROF_LLOYD, pb, 0.0);
+        } else if (!first && use_graph) {
             cudaGraphExec_t ge = loop_graph(ctx, a, ia, qn);
+            const int pb = prof_begin(ctx);
             CQG_CUDA(cudaGraphLaunch(ge, s));
+            rec = prof_end(ctx, CQG_PROF_LLOYD, pb, 0.0);
             launched(ctx, 4);
         } else {
             CQG_CUDA(cudaMemsetAsync(qn, 0, 4, s));
@@ -587,9 +787,12 @@ LloydOut lloyd_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *count
         CQG_CUDA(cudaMemcpyAsync(hst, st, sizeof(IterStatus), cudaMemcpyDeviceToHost, s));
         CQG_CUDA(cudaStreamSynchronize(s));
         iter = hst->iteration;
+        prof_add_units(ctx, rec, (double)n * (double)K * (double)(iter - before));
         if (hst->state == 2) {
             out.repairs += repair_loop(ctx, colors_d, counts_d, n, P, K, labels_d, cen, mom);
-            launch_iter_end(ctx, ia);
+            IterArgs ib = ia;
+            ib.reset_qn = persistent ? 1 : 0;
+            launch_iter_end(ctx, ib);
             CQG_CUDA(cudaMemcpyAsync(hst, st, sizeof(IterStatus), cudaMemcpyDeviceToHost, s));
             CQG_CUDA(cudaStreamSynchronize(s));
             if (hst->state == 2) fail(CQG_E_RUNTIME, "repair left an empty cluster");

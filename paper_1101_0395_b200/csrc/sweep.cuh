@@ -180,30 +180,25 @@ __device__ __forceinline__ uint32_t walk_ndc(double xr, double xg, double xb, in
 
 // NDC of one WALK iteration, before the sweep rewrites the labels: 4 points per
 // thread with their lifting searches interleaved (independent loads in flight).
+// NDC over points [lo, hi) with a thread stride of blockDim.x (per-block range
+// in the persistent kernel, the whole grid range in ndc_kernel).
 template <int Q>
-static __global__ void __launch_bounds__(256, 4) ndc_kernel(const uint32_t *__restrict__ colors,
-                                                  const uint32_t *__restrict__ labels, uint64_t n,
-                                                  const double *__restrict__ cen,
-                                                  const double *__restrict__ dsorted, int K, int Kpow,
-                                                  unsigned long long *ndc) {
-    extern __shared__ double s_cen[];
-    const bool in_smem = K <= 2048;
-    if (in_smem)
-        for (int i = threadIdx.x; i < 3 * K; i += blockDim.x) s_cen[i] = cen[i];
-    __syncthreads();
-    const double *c = in_smem ? s_cen : cen;
+__device__ __forceinline__ unsigned long long ndc_range(const uint32_t *__restrict__ colors,
+                                                        const uint32_t *__restrict__ labels, uint64_t lo,
+                                                        uint64_t hi, uint64_t first, uint64_t stride,
+                                                        const double *c, const double *__restrict__ dsorted,
+                                                        int Kpow) {
     unsigned long long local = 0;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * Q;
-    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x * Q; base < n; base += stride) {
+    for (uint64_t base = lo + first; base < hi; base += stride) {
         double cut[Q];
         const double *row[Q];
         int pos[Q];
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
             const uint64_t i = base + threadIdx.x + (uint64_t)q * blockDim.x;
-            const bool v = i < n;
+            const bool v = i < hi;
             const uint32_t col = v ? __ldg(colors + i) : 0u;
-            const int prev = v ? (int)__ldg(labels + i) : 0;
+            const int prev = v ? (int)labels[i] : 0;
             const double pd = d2_exact((double)((col >> 16) & 255u), (double)((col >> 8) & 255u),
                                        (double)(col & 255u), c[3 * prev], c[3 * prev + 1], c[3 * prev + 2]);
             cut[q] = v ? __dmul_rn(4.0, pd) : -1.0; // -1: counts nothing and adds 0 below
@@ -224,6 +219,24 @@ static __global__ void __launch_bounds__(256, 4) ndc_kernel(const uint32_t *__re
             if (cut[q] >= 0.0) local += (unsigned long long)(pos[q] - (cut[q] > 0.0 ? 1 : 0) + 1);
         }
     }
+    return local;
+}
+
+template <int Q>
+static __global__ void __launch_bounds__(256, 4) ndc_kernel(const uint32_t *__restrict__ colors,
+                                                  const uint32_t *__restrict__ labels, uint64_t n,
+                                                  const double *__restrict__ cen,
+                                                  const double *__restrict__ dsorted, int K, int Kpow,
+                                                  unsigned long long *ndc) {
+    extern __shared__ double s_cen[];
+    const bool in_smem = K <= 2048;
+    if (in_smem)
+        for (int i = threadIdx.x; i < 3 * K; i += blockDim.x) s_cen[i] = cen[i];
+    __syncthreads();
+    const double *c = in_smem ? s_cen : cen;
+    unsigned long long local =
+        ndc_range<Q>(colors, labels, 0, n, (uint64_t)blockIdx.x * blockDim.x * Q,
+                     (uint64_t)gridDim.x * blockDim.x * Q, c, dsorted, Kpow);
     for (int o = 16; o; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
     if ((threadIdx.x & 31) == 0 && local) atomicAdd(ndc, local);
 }
@@ -248,29 +261,17 @@ __device__ __forceinline__ void track_pair(float2 v, float &b1, float &b2) {
     b1 = fminf(b1, lo);
 }
 
+// Sweep points [lo, hi) of this block against the FP32 centre table in shared
+// memory (s_fc: m2r | m2g | m2b | cc, Kp each). FULL/MAP flush the u32 shared
+// accumulators after every tile; WALK leaves its u64 deltas for the caller.
 template <int MODE, int PPT>
-__global__ void __launch_bounds__(kSweepThreads, 2) sweep_kernel(SweepArgs a) {
+__device__ __forceinline__ void sweep_range(const SweepArgs &a, uint64_t lo, uint64_t hi, float *smem,
+                                            uint32_t *s_acc, float tau_abs, float tau_rel) {
     static_assert(PPT % 2 == 0, "points are processed in pairs");
     constexpr int PP = PPT / 2;
-    extern __shared__ __align__(16) float smem[];
     const int K = a.K, Kp = a.Kp;
     float *s_m2r = smem, *s_m2g = smem + Kp, *s_m2b = smem + 2 * Kp, *s_cc = smem + 3 * Kp;
-    uint32_t *s_acc = reinterpret_cast<uint32_t *>(smem + 4 * Kp);
-    // WALK iterations move few points: their moment deltas go to 64-bit shared
-    // accumulators (flushed once per block); FULL/MAP use u32 + per-tile flush
     unsigned long long *s_acc64 = reinterpret_cast<unsigned long long *>(s_acc);
-    for (int i = threadIdx.x; i < 4 * Kp; i += blockDim.x) smem[i] = a.fc[i];
-    if (MODE == MODE_WALK)
-        for (int i = threadIdx.x; i < K * 5; i += blockDim.x) s_acc64[i] = 0;
-    else
-        for (int i = threadIdx.x; i < K * kAccPerCluster; i += blockDim.x) s_acc[i] = 0;
-    __syncthreads();
-    const float tau_abs = a.tau[0], tau_rel = a.tau[1];
-    unsigned long long ndc_local = 0;
-
-    const uint64_t chunk = (a.n + gridDim.x - 1) / gridDim.x;
-    const uint64_t lo = (uint64_t)blockIdx.x * chunk;
-    const uint64_t hi = lo + chunk < a.n ? lo + chunk : a.n;
     const uint64_t tile = (uint64_t)kSweepThreads * PPT;
     for (uint64_t base = lo; base < hi; base += tile) {
         // point pairs: lane .x = point 2p, lane .y = point 2p+1 (FFMA2 with a
@@ -386,12 +387,35 @@ __global__ void __launch_bounds__(kSweepThreads, 2) sweep_kernel(SweepArgs a) {
             __syncthreads();
         }
     }
+}
+
+// Flush the WALK-mode u64 block deltas (laid out as Moments) to the global moments.
+__device__ __forceinline__ void flush_acc64(const unsigned long long *s_acc64, Moments *mom, int K) {
+    for (int e = threadIdx.x; e < K * 5; e += blockDim.x) {
+        const unsigned long long v = s_acc64[e];
+        if (v) atomicAdd(reinterpret_cast<unsigned long long *>(mom) + e, v);
+    }
+}
+
+template <int MODE, int PPT>
+__global__ void __launch_bounds__(kSweepThreads, 2) sweep_kernel(SweepArgs a) {
+    extern __shared__ __align__(16) float smem[];
+    const int K = a.K, Kp = a.Kp;
+    uint32_t *s_acc = reinterpret_cast<uint32_t *>(smem + 4 * Kp);
+    unsigned long long *s_acc64 = reinterpret_cast<unsigned long long *>(s_acc);
+    for (int i = threadIdx.x; i < 4 * Kp; i += blockDim.x) smem[i] = a.fc[i];
+    if (MODE == MODE_WALK)
+        for (int i = threadIdx.x; i < K * 5; i += blockDim.x) s_acc64[i] = 0;
+    else
+        for (int i = threadIdx.x; i < K * kAccPerCluster; i += blockDim.x) s_acc[i] = 0;
+    __syncthreads();
+    const uint64_t chunk = (a.n + gridDim.x - 1) / gridDim.x;
+    const uint64_t lo = (uint64_t)blockIdx.x * chunk;
+    const uint64_t hi = lo + chunk < a.n ? lo + chunk : a.n;
+    sweep_range<MODE, PPT>(a, lo, hi, smem, s_acc, a.tau[0], a.tau[1]);
     if (MODE == MODE_WALK) {
         __syncthreads();
-        for (int e = threadIdx.x; e < K * 5; e += blockDim.x) {
-            const unsigned long long v = s_acc64[e];
-            if (v) atomicAdd(reinterpret_cast<unsigned long long *>(a.mom) + e, v);
-        }
+        flush_acc64(s_acc64, a.mom, K);
     }
 }
 
@@ -415,11 +439,10 @@ __device__ __forceinline__ void warp_min_dp(double &d, int &p) {
 }
 
 template <int MODE>
-__global__ void replay_kernel(SweepArgs a) {
+__device__ __forceinline__ void replay_range(const SweepArgs &a, uint32_t gwarp, uint32_t warps) {
     const uint32_t nq = *a.qn;
     const int lane = threadIdx.x & 31;
-    const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
-    for (uint32_t q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < nq; q += warps) {
+    for (uint32_t q = gwarp; q < nq; q += warps) {
         const uint32_t idx = a.queue[q];
         const uint32_t c = a.colors[idx], cnt = a.counts[idx];
         const uint32_t r = (c >> 16) & 255u, g = (c >> 8) & 255u, b = c & 255u;
@@ -469,9 +492,15 @@ __global__ void replay_kernel(SweepArgs a) {
     }
 }
 
+template <int MODE>
+__global__ void replay_kernel(SweepArgs a) {
+    replay_range<MODE>(a, (blockIdx.x * blockDim.x + threadIdx.x) >> 5, (gridDim.x * blockDim.x) >> 5);
+}
+
 // FP32 centre table + error bound for the sweep (one block).
 //   E <= u*|cc err| + u*|m2c err|*x + 4u*M  with u = 2^-24 and M the largest
 //   magnitude of any partial sum (cc + xx when all coordinates are >= 0).
+__device__ void fc_block(const double *cen, int K, int Kp, float *fc, float *tau);
 __global__ void fc_kernel(const double *cen, int K, int Kp, float *fc, float *tau);
 
 
