@@ -154,6 +154,30 @@ int cqg_lloyd(cqg_ctx *ctx, const uint32_t *colors, const uint32_t *counts, uint
               uint32_t *labels, double *sse_trace, cqg_lloyd_stats *stats,
               uint32_t *hist_labels, double *hist_centers);
 
+/* ---- stages 2+3, sharded over ranks (one huge image) -------
+ * Each rank holds a contiguous slice of the unique colours. Per iteration:
+ *   cqg_shard_assign   local assignment (FULL first, then NDC + WALK sweep +
+ *                      exact replay) and the rank's cumulative local moments
+ *                      -> partial[5K+2] int64 = {K x (n, s_r, s_g, s_b, q),
+ *                      local NDC of this iteration, local near-tie replays}
+ *   (caller)           allreduce(partial, SUM) over the ranks (NCCL / gloo)
+ *   cqg_shard_finalize centres / SSE / termination / walk table from the global
+ *                      moments; identical on every rank. *state: 0 continue,
+ *                      1 done, 2 empty cluster (run the repair protocol, then
+ *                      allreduce cqg_shard_moments and finalize again).
+ * partial/global may be host or device memory. P is the global pixel count. */
+int cqg_shard_begin(cqg_ctx *ctx, const uint32_t *colors, const uint32_t *counts, uint64_t n_local,
+                    uint64_t P, const double *init, int k, const cqg_term *term);
+int cqg_shard_assign(cqg_ctx *ctx, int64_t *partial);
+int cqg_shard_moments(cqg_ctx *ctx, int64_t *partial);
+int cqg_shard_finalize(cqg_ctx *ctx, const int64_t *global, int *state, double *sse);
+/* repair protocol helpers (kmeans.cpp:124-169 across ranks) */
+int cqg_shard_sizes(cqg_ctx *ctx, uint32_t *sizes);
+int cqg_shard_donor(cqg_ctx *ctx, const uint32_t *global_sizes, int fallback, double *value,
+                    uint64_t *local_index, uint32_t *colour, uint32_t *label);
+int cqg_shard_move(cqg_ctx *ctx, uint64_t local_index, int e, uint32_t colour);
+int cqg_shard_end(cqg_ctx *ctx, double *centers, uint32_t *labels, double *sse_trace, int *iterations);
+
 /* ---- stage 4: exact lowest-index nearest palette entry per pixel + MSE ----
  * indices: P entries of index_bytes (4 = uint32 as MappingResult::indices,
  * 1 = uint8, requires k <= 256); may be NULL. quantized: P*3 bytes (palette

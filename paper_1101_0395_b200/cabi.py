@@ -34,6 +34,8 @@ EXPORTS = (
     "cqg_create", "cqg_destroy", "cqg_last_error", "cqg_set_stream", "cqg_launch_count",
     "cqg_version", "cqg_histogram", "cqg_init_maximin", "cqg_init_kmeanspp", "cqg_lloyd",
     "cqg_map", "cqg_quantize", "cqg_set_profiling", "cqg_read_profile", "cqg_bench_sweep",
+    "cqg_shard_begin", "cqg_shard_assign", "cqg_shard_moments", "cqg_shard_finalize", "cqg_shard_sizes",
+    "cqg_shard_donor", "cqg_shard_move", "cqg_shard_end",
 )
 
 PROF_SWEEP, PROF_MAPSWEEP, PROF_HIST, PROF_PIXEL, PROF_INIT, PROF_REPLAY, PROF_NDC, PROF_LLOYD = range(8)
@@ -110,6 +112,18 @@ def load(path: str = LIB_PATH):
         L.cqg_read_profile.argtypes = [vp, C.POINTER(Profile), i32]
         L.cqg_bench_sweep.argtypes = [vp, i32, C.POINTER(C.c_double), C.POINTER(C.c_double)]
         L.cqg_bench_sweep.restype = i32
+        L.cqg_shard_begin.argtypes = [vp, vp, vp, u64, u64, vp, i32, C.POINTER(Term)]
+        L.cqg_shard_assign.argtypes = [vp, vp]
+        L.cqg_shard_moments.argtypes = [vp, vp]
+        L.cqg_shard_finalize.argtypes = [vp, vp, C.POINTER(i32), C.POINTER(C.c_double)]
+        L.cqg_shard_sizes.argtypes = [vp, vp]
+        L.cqg_shard_donor.argtypes = [vp, vp, i32, C.POINTER(C.c_double), C.POINTER(u64),
+                                      C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]
+        L.cqg_shard_move.argtypes = [vp, u64, i32, C.c_uint32]
+        L.cqg_shard_end.argtypes = [vp, vp, vp, vp, C.POINTER(i32)]
+        for name in ("cqg_shard_begin", "cqg_shard_assign", "cqg_shard_moments", "cqg_shard_finalize",
+                     "cqg_shard_sizes", "cqg_shard_donor", "cqg_shard_move", "cqg_shard_end"):
+            getattr(L, name).restype = i32
         for name in ("cqg_set_profiling", "cqg_read_profile", "cqg_histogram", "cqg_init_maximin", "cqg_init_kmeanspp", "cqg_lloyd",
                      "cqg_map", "cqg_quantize", "cqg_set_stream"):
             getattr(L, name).restype = i32

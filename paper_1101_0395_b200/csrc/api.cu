@@ -219,12 +219,13 @@ void cqg_destroy(cqg_ctx *ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     release_graphs(ctx);
+    shard_release(ctx);
     DevBuf *bufs[] = {&ctx->tab, &ctx->list, &ctx->bitmap, &ctx->wordpref, &ctx->scal, &ctx->img,
                       &ctx->colors, &ctx->counts, &ctx->first, &ctx->labels, &ctx->cen, &ctx->fcen,
                       &ctx->dtab, &ctx->dsorted, &ctx->order, &ctx->mom, &ctx->queue, &ctx->ndc,
                       &ctx->status, &ctx->sizes, &ctx->red, &ctx->hist_labels, &ctx->hist_centers,
                       &ctx->sse, &ctx->lut, &ctx->idx_out, &ctx->q_out, &ctx->mom_map, &ctx->mind2,
-                      &ctx->initpart, &ctx->initsel, &ctx->unit_draws};
+                      &ctx->initpart, &ctx->initsel, &ctx->unit_draws, &ctx->mom_g, &ctx->partial};
     for (DevBuf *b : bufs) b->release();
     ctx->pinned.release();
     for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
@@ -375,6 +376,95 @@ int cqg_lloyd(cqg_ctx *ctx, const uint32_t *colors, const uint32_t *counts, uint
             stats->n_points = n;
             stats->flagged_total = o.flagged;
         }
+    });
+}
+
+int cqg_shard_begin(cqg_ctx *ctx, const uint32_t *colors, const uint32_t *counts, uint64_t n_local, uint64_t P,
+                    const double *init, int k, const cqg_term *term) {
+    return guarded([&] {
+        use_device(ctx);
+        if (!term) fail(CQG_E_INVALID, "clustering: null termination");
+        if (k <= 0) fail(CQG_E_INVALID, "clustering: no initial centers");
+        if (term->epsilon < 0.0) fail(CQG_E_INVALID, "clustering: negative epsilon");
+        if (term->max_iterations <= 0) fail(CQG_E_INVALID, "clustering: max_iterations < 1");
+        if (k > 1024) fail(CQG_E_INVALID, "clustering: k > 1024 is not supported by the sharded engine");
+        if (P == 0) fail(CQG_E_INVALID, "wsm: weights must be positive");
+        const uint32_t *col_d = n_local ? static_cast<const uint32_t *>(stage_in(ctx, colors, n_local * 4, ctx->colors))
+                                        : static_cast<const uint32_t *>(ctx->colors.ensure(4));
+        const uint32_t *cnt_d = n_local ? static_cast<const uint32_t *>(stage_in(ctx, counts, n_local * 4, ctx->counts))
+                                        : static_cast<const uint32_t *>(ctx->counts.ensure(4));
+        const double *init_d = static_cast<const double *>(stage_in(ctx, init, 24 * (size_t)k, ctx->initsel));
+        shard_begin_dev(ctx, col_d, cnt_d, n_local, P, init_d, k, *term);
+    });
+}
+
+static int shard_partial(cqg_ctx *ctx, int64_t *partial, bool run) {
+    return guarded([&] {
+        use_device(ctx);
+        const size_t bytes = 8 * (5 * (size_t)shard_k(ctx) + 2);
+        long long *d = is_device_ptr(partial) ? reinterpret_cast<long long *>(partial)
+                                              : static_cast<long long *>(ctx->partial.ensure(bytes));
+        shard_assign_dev(ctx, d, run);
+        copy_out(ctx, partial, d, bytes);
+        CQG_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int cqg_shard_assign(cqg_ctx *ctx, int64_t *partial) { return shard_partial(ctx, partial, true); }
+int cqg_shard_moments(cqg_ctx *ctx, int64_t *partial) { return shard_partial(ctx, partial, false); }
+
+int cqg_shard_finalize(cqg_ctx *ctx, const int64_t *global, int *state, double *sse) {
+    return guarded([&] {
+        use_device(ctx);
+        const size_t bytes = 8 * (5 * (size_t)shard_k(ctx) + 2);
+        const long long *g = static_cast<const long long *>(stage_in(ctx, global, bytes, ctx->partial));
+        const int st = shard_finalize_dev(ctx, g, sse);
+        if (state) *state = st;
+    });
+}
+
+int cqg_shard_sizes(cqg_ctx *ctx, uint32_t *sizes) {
+    return guarded([&] {
+        use_device(ctx);
+        const size_t bytes = 4 * (size_t)shard_k(ctx);
+        uint32_t *d = out_buf<uint32_t>(sizes, ctx->sizes, (size_t)shard_k(ctx));
+        shard_sizes_dev(ctx, d);
+        copy_out(ctx, sizes, d, bytes);
+        CQG_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int cqg_shard_donor(cqg_ctx *ctx, const uint32_t *global_sizes, int fallback, double *value, uint64_t *local_index,
+                    uint32_t *colour, uint32_t *label) {
+    return guarded([&] {
+        use_device(ctx);
+        const uint32_t *g = static_cast<const uint32_t *>(
+            stage_in(ctx, global_sizes, 4 * (size_t)shard_k(ctx), ctx->status));
+        double v;
+        uint64_t i;
+        uint32_t c, l;
+        shard_donor_dev(ctx, g, fallback, &v, &i, &c, &l);
+        if (value) *value = v;
+        if (local_index) *local_index = i;
+        if (colour) *colour = c;
+        if (label) *label = l;
+    });
+}
+
+int cqg_shard_move(cqg_ctx *ctx, uint64_t local_index, int e, uint32_t colour) {
+    return guarded([&] {
+        use_device(ctx);
+        if (e < 0 || e >= shard_k(ctx)) fail(CQG_E_INVALID, "cqg_shard_move: cluster out of range");
+        shard_move_dev(ctx, local_index, e, colour);
+        CQG_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int cqg_shard_end(cqg_ctx *ctx, double *centers, uint32_t *labels, double *sse_trace, int *iterations) {
+    return guarded([&] {
+        use_device(ctx);
+        const int it = shard_end_dev(ctx, centers, labels, sse_trace);
+        if (iterations) *iterations = it;
     });
 }
 

@@ -121,6 +121,8 @@ struct cqg_ctx {
     // Lloyd state
     cqg::DevBuf labels, cen, fcen, dtab, dsorted, order, mom, queue, ndc, status, sizes, red;
     cqg::DevBuf hist_labels, hist_centers, sse;
+    cqg::DevBuf mom_g, partial; // sharded Lloyd: global moments, packed partials
+    void *shard = nullptr;      // cqg::ShardState (lloyd.cu)
     // mapping
     cqg::DevBuf lut, idx_out, q_out, mom_map;
     // init
@@ -218,6 +220,19 @@ LloydOut lloyd_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *count
                    double *hist_centers_user);
 
 void bench_sweep_dev(cqg_ctx *ctx, int reps, double *ms, double *units);
+// sharded Lloyd (lloyd.cu); device pointers unless noted
+void shard_begin_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *counts_d, uint64_t n, uint64_t P,
+                     const double *init_d, int K, const cqg_term &term);
+void shard_assign_dev(cqg_ctx *ctx, long long *partial_d, bool run);
+int shard_finalize_dev(cqg_ctx *ctx, const long long *global_d, double *sse);
+void shard_sizes_dev(cqg_ctx *ctx, uint32_t *sizes_d);
+void shard_donor_dev(cqg_ctx *ctx, const uint32_t *gsizes_d, int fallback, double *value, uint64_t *index,
+                     uint32_t *colour, uint32_t *label);
+void shard_move_dev(cqg_ctx *ctx, uint64_t index, int e, uint32_t colour);
+int shard_end_dev(cqg_ctx *ctx, double *centers_user, uint32_t *labels_user, double *sse_user);
+void shard_release(cqg_ctx *ctx);
+int shard_k(cqg_ctx *ctx);
+uint64_t shard_n(cqg_ctx *ctx);
 double map_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P, const uint32_t *colors_d,
                const uint32_t *counts_d, uint64_t n, const double *pal_d, int k, void *indices_d,
                int index_bytes, uint8_t *quant_d);

@@ -814,4 +814,223 @@ LloydOut lloyd_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *count
     return out;
 }
 
+
+// ---------------------------------------------------------------------------
+// Sharded Lloyd (one huge image over ranks): the caller allreduces the packed
+// partials between cqg_shard_assign and cqg_shard_finalize.
+
+struct ShardState {
+    SweepArgs a;
+    IterArgs ia;
+    uint64_t n = 0, P = 0;
+    int K = 0, iter = 0, limit = 0;
+};
+
+namespace {
+__global__ void pack_partial_kernel(const Moments *mom, int K, const unsigned long long *ndc, const uint32_t *qn,
+                                    long long extra_ndc, int with_counts, long long *out) {
+    const long long *m = reinterpret_cast<const long long *>(mom);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 5 * K; i += gridDim.x * blockDim.x) out[i] = m[i];
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        out[5 * K] = with_counts ? (long long)(*ndc) + extra_ndc : 0;
+        out[5 * K + 1] = with_counts ? (long long)(*qn) : 0;
+    }
+}
+
+__global__ void set_centre_kernel(double *cen, int e, uint32_t c) {
+    if (threadIdx.x == 0) {
+        cen[3 * e] = (double)((c >> 16) & 255u);
+        cen[3 * e + 1] = (double)((c >> 8) & 255u);
+        cen[3 * e + 2] = (double)(c & 255u);
+    }
+}
+} // namespace
+
+static ShardState &shard_state(cqg_ctx *ctx) {
+    if (!ctx->shard) fail(CQG_E_INVALID, "cqg_shard: call cqg_shard_begin first");
+    return *static_cast<ShardState *>(ctx->shard);
+}
+
+void shard_release(cqg_ctx *ctx) {
+    delete static_cast<ShardState *>(ctx->shard);
+    ctx->shard = nullptr;
+}
+int shard_k(cqg_ctx *ctx) { return shard_state(ctx).K; }
+uint64_t shard_n(cqg_ctx *ctx) { return shard_state(ctx).n; }
+
+void shard_begin_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *counts_d, uint64_t n, uint64_t P,
+                     const double *init_d, int K, const cqg_term &term) {
+    cudaStream_t s = ctx->stream;
+    if (!ctx->shard) ctx->shard = new ShardState();
+    ShardState &S = *static_cast<ShardState *>(ctx->shard);
+    const int Kp = (K + 7) & ~7;
+    int Kpow = 1;
+    while (Kpow < K) Kpow <<= 1;
+    S = ShardState();
+    S.n = n;
+    S.P = P;
+    S.K = K;
+    S.limit = term.fixed_iterations > 0 ? term.fixed_iterations : term.max_iterations;
+    double *cen = static_cast<double *>(ctx->cen.ensure(24 * (size_t)K));
+    CQG_CUDA(cudaMemcpyAsync(cen, init_d, 24 * (size_t)K, cudaMemcpyDeviceToDevice, s));
+    float *fc = static_cast<float *>(ctx->fcen.ensure(sizeof(float) * (4 * (size_t)Kp + 8)));
+    double *dtab = static_cast<double *>(ctx->dtab.ensure(sizeof(double) * (size_t)K * K));
+    double *dsorted = static_cast<double *>(ctx->dsorted.ensure(sizeof(double) * (size_t)K * Kpow));
+    uint32_t *order = static_cast<uint32_t *>(ctx->order.ensure(sizeof(uint32_t) * (size_t)K * K));
+    Moments *mom = static_cast<Moments *>(ctx->mom.ensure(sizeof(Moments) * (size_t)K));
+    Moments *mom_g = static_cast<Moments *>(ctx->mom_g.ensure(sizeof(Moments) * (size_t)K));
+    uint32_t *queue = static_cast<uint32_t *>(ctx->queue.ensure(sizeof(uint32_t) * (n + 1)));
+    uint32_t *labels = static_cast<uint32_t *>(ctx->labels.ensure(sizeof(uint32_t) * (n + 1)));
+    uint32_t *qn = static_cast<uint32_t *>(ctx->scal.ensure(256));
+    unsigned long long *ndc = reinterpret_cast<unsigned long long *>(qn + 8);
+    unsigned long long *flagged = reinterpret_cast<unsigned long long *>(qn + 10);
+    int *iter_dev = reinterpret_cast<int *>(qn + 12);
+    IterStatus *st = reinterpret_cast<IterStatus *>(qn + 16);
+    unsigned long long *ndc_unused = reinterpret_cast<unsigned long long *>(qn + 24);
+    double *sse_d = static_cast<double *>(ctx->sse.ensure(sizeof(double) * (size_t)(S.limit + 1)));
+    CQG_CUDA(cudaMemsetAsync(mom, 0, sizeof(Moments) * (size_t)K, s));
+    CQG_CUDA(cudaMemsetAsync(qn, 0, 128, s));
+    fc_kernel<<<1, 256, 0, s>>>(cen, K, Kp, fc, fc + 4 * Kp);
+    launched(ctx);
+    SweepArgs &a = S.a;
+    a = SweepArgs{};
+    a.colors = colors_d;
+    a.counts = counts_d;
+    a.n = n;
+    a.labels = labels;
+    a.fc = fc;
+    a.cen = cen;
+    a.dtab = dtab;
+    a.dsorted = dsorted;
+    a.order = order;
+    a.tau = fc + 4 * Kp;
+    a.queue = queue;
+    a.qn = qn;
+    a.mom = mom;
+    a.ndc = ndc;
+    a.K = K;
+    a.Kp = Kp;
+    a.Kpow = Kpow;
+    IterArgs &ia = S.ia;
+    ia = IterArgs{};
+    ia.mom = mom_g;
+    ia.cen = cen;
+    ia.K = K;
+    ia.Kp = Kp;
+    ia.P = P;
+    ia.n_points = 0; // NDC is summed from the ranks' partials
+    ia.eps = term.epsilon;
+    ia.limit = S.limit;
+    ia.fixed = term.fixed_iterations;
+    ia.sse_arr = sse_d;
+    ia.st = st;
+    ia.iter_dev = iter_dev;
+    ia.qn = qn;
+    ia.ndc = ndc_unused;
+    ia.flagged = flagged;
+    ia.fc = fc;
+    ia.tau = fc + 4 * Kp;
+    ia.dtab = dtab;
+    ia.dsorted = dsorted;
+    ia.order = order;
+    ia.Kpow = Kpow;
+    ia.use_cond = 0;
+    ia.reset_qn = 1;
+}
+
+void shard_assign_dev(cqg_ctx *ctx, long long *partial_d, bool run) {
+    ShardState &S = shard_state(ctx);
+    cudaStream_t s = ctx->stream;
+    long long extra = 0;
+    if (run) {
+        CQG_CUDA(cudaMemsetAsync(S.a.qn, 0, 4, s));
+        CQG_CUDA(cudaMemsetAsync(S.a.ndc, 0, 8, s));
+        if (S.n > 0) {
+            if (S.iter == 0) {
+                launch_sweep(ctx, MODE_FULL, S.a);
+                extra = (long long)S.n * (long long)S.K; // nearest_full: K per point
+            } else {
+                launch_sweep(ctx, MODE_WALK, S.a);
+            }
+        }
+    }
+    pack_partial_kernel<<<1, 256, 0, s>>>(S.a.mom, S.K, S.a.ndc, S.a.qn, extra, run ? 1 : 0, partial_d);
+    launched(ctx);
+    CQG_CUDA(cudaGetLastError());
+}
+
+
+int shard_finalize_dev(cqg_ctx *ctx, const long long *global_d, double *sse) {
+    ShardState &S = shard_state(ctx);
+    cudaStream_t s = ctx->stream;
+    CQG_CUDA(cudaMemcpyAsync(S.ia.mom, global_d, sizeof(Moments) * (size_t)S.K, cudaMemcpyDeviceToDevice, s));
+    launch_iter_end(ctx, S.ia);
+    IterStatus *hst = static_cast<IterStatus *>(ctx->pinned.ensure(4096));
+    CQG_CUDA(cudaMemcpyAsync(hst, S.ia.st, sizeof(IterStatus), cudaMemcpyDeviceToHost, s));
+    CQG_CUDA(cudaStreamSynchronize(s));
+    if (hst->state != 2) S.iter = hst->iteration;
+    if (sse) *sse = hst->sse;
+    return hst->state;
+}
+
+void shard_sizes_dev(cqg_ctx *ctx, uint32_t *sizes_d) {
+    ShardState &S = shard_state(ctx);
+    CQG_CUDA(cudaMemsetAsync(sizes_d, 0, 4 * (size_t)S.K, ctx->stream));
+    if (S.n > 0) sizes_kernel<<<pick_grid(ctx, S.n, 256, 2), 256, 0, ctx->stream>>>(S.a.labels, S.n, sizes_d);
+    launched(ctx);
+}
+
+void shard_donor_dev(cqg_ctx *ctx, const uint32_t *gsizes_d, int fallback, double *value, uint64_t *index,
+                     uint32_t *colour, uint32_t *label) {
+    ShardState &S = shard_state(ctx);
+    cudaStream_t s = ctx->stream;
+    *value = -2.0;
+    *index = ~0ull;
+    *colour = 0;
+    *label = 0;
+    if (S.n == 0) return;
+    const int nparts = pick_grid(ctx, S.n, 256, 2);
+    ValIdx *part = static_cast<ValIdx *>(ctx->red.ensure(sizeof(ValIdx) * (size_t)nparts));
+    argmax_kernel<<<nparts, 256, 0, s>>>(S.a.colors, S.a.counts, S.a.labels, S.n, S.a.cen, 1.0 / (double)S.P,
+                                         gsizes_d, fallback, part);
+    argmax_final<<<1, 32, 0, s>>>(part, nparts);
+    launched(ctx, 2);
+    ValIdx *h = static_cast<ValIdx *>(ctx->pinned.ensure(4096));
+    CQG_CUDA(cudaMemcpyAsync(h, part, sizeof(ValIdx), cudaMemcpyDeviceToHost, s));
+    CQG_CUDA(cudaStreamSynchronize(s));
+    const ValIdx best = *h;
+    *value = best.v;
+    *index = best.i;
+    if (best.i < S.n) {
+        uint32_t *h32 = reinterpret_cast<uint32_t *>(h + 1);
+        CQG_CUDA(cudaMemcpyAsync(h32, S.a.colors + best.i, 4, cudaMemcpyDeviceToHost, s));
+        CQG_CUDA(cudaMemcpyAsync(h32 + 1, S.a.labels + best.i, 4, cudaMemcpyDeviceToHost, s));
+        CQG_CUDA(cudaStreamSynchronize(s));
+        *colour = h32[0];
+        *label = h32[1];
+    }
+}
+
+void shard_move_dev(cqg_ctx *ctx, uint64_t index, int e, uint32_t colour) {
+    ShardState &S = shard_state(ctx);
+    cudaStream_t s = ctx->stream;
+    if (index < S.n) {
+        uint32_t *sizes = static_cast<uint32_t *>(ctx->sizes.ensure((size_t)S.K * 4));
+        apply_move_kernel<<<1, 32, 0, s>>>(S.a.colors, S.a.counts, S.a.labels, S.ia.cen, S.a.mom, sizes, index, e);
+    } else {
+        set_centre_kernel<<<1, 32, 0, s>>>(S.ia.cen, e, colour);
+    }
+    launched(ctx);
+    CQG_CUDA(cudaGetLastError());
+}
+
+int shard_end_dev(cqg_ctx *ctx, double *centers_user, uint32_t *labels_user, double *sse_user) {
+    ShardState &S = shard_state(ctx);
+    copy_out(ctx, centers_user, S.a.cen, 24 * (size_t)S.K);
+    copy_out(ctx, labels_user, S.a.labels, 4 * S.n);
+    copy_out(ctx, sse_user, S.ia.sse_arr, 8 * (size_t)S.iter);
+    CQG_CUDA(cudaStreamSynchronize(ctx->stream));
+    return S.iter;
+}
+
 } // namespace cqg
