@@ -206,6 +206,8 @@ cqg_ctx *cqg_create(int device) {
         ctx->own_stream = true;
         const char *ng = getenv("CQG_NO_GRAPH");
         ctx->use_graphs = !(ng && ng[0] == '1');
+        const char *nc = getenv("CQG_NO_CLUSTER_INIT");
+        ctx->use_cluster_init = !(nc && nc[0] == '1');
     });
     if (rc != CQG_OK) {
         delete ctx;

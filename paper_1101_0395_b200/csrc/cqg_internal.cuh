@@ -131,6 +131,7 @@ struct cqg_ctx {
 
     // cached CUDA graph of the Lloyd WHILE loop (lloyd.cu)
     bool use_graphs = true;
+    bool use_cluster_init = true;
     cudaGraphExec_t loop_exec = nullptr;
     cudaGraph_t loop_graph = nullptr;
     std::vector<uint64_t> loop_key;

@@ -538,6 +538,300 @@ __global__ void __launch_bounds__(kInitThreads) init_kernel(InitArgs a) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// Small substrates: one thread-block CLUSTER (16 CTAs x 1024 threads, one CTA
+// per SM) holds every point in shared memory -- colour, count and ping-pong
+// min-distances -- and runs all K rounds with one cluster barrier per round.
+// Thread t of CTA c owns the contiguous points [c*chunk + t*ppt, +ppt), so
+// thread sums -> warp sums -> CTA sums are in histogram order; every CTA
+// locates each draw redundantly by reading the other CTAs' sums through DSMEM
+// (CTA sums, then the target CTA's 32 warp sums, its 32 thread sums, and the
+// target thread's <= 32 point masses). The arithmetic and the exactness
+// argument are the cooperative kernel's (ExactMass / FixedMass).
+constexpr int kClusterThreads = 1024;
+
+template <class M>
+__device__ uint64_t cluster_sequential_draw(const InitArgs &a, cg::cluster_group &cl, const uint32_t *s_cnt,
+                                            const uint32_t *s_md, uint64_t chunk, double nu, int weights_only) {
+    double total = 0.0;
+    for (uint64_t i = 0; i < a.n; ++i) {
+        const uint32_t r = (uint32_t)(i / chunk), li = (uint32_t)(i % chunk);
+        const uint32_t cnt = *cl.map_shared_rank(s_cnt + li, r);
+        const uint32_t md = weights_only ? kWeightsOnly : *cl.map_shared_rank(s_md + li, r);
+        total = __dadd_rn(total, mass_c(cnt, a.inv, md));
+    }
+    const double u = __dmul_rn(nu, total);
+    double acc = 0.0;
+    for (uint64_t i = 0; i + 1 < a.n; ++i) {
+        const uint32_t r = (uint32_t)(i / chunk), li = (uint32_t)(i % chunk);
+        const uint32_t cnt = *cl.map_shared_rank(s_cnt + li, r);
+        const uint32_t md = weights_only ? kWeightsOnly : *cl.map_shared_rank(s_md + li, r);
+        acc = __dadd_rn(acc, mass_c(cnt, a.inv, md));
+        if (u < acc) return i;
+    }
+    return a.n - 1;
+}
+
+// inclusive warp scan of up to 32 values; returns the first lane whose
+// inclusive prefix exceeds U (or 32) and the exclusive prefix at that lane
+template <class M>
+__device__ __forceinline__ int lane_locate(typename M::T v, typename M::T U, typename M::T *before,
+                                           typename M::T *total) {
+    typedef typename M::T T;
+    const int lane = threadIdx.x & 31;
+    const T incl = warp_incl<M>(v);
+    *total = M::shfl(incl, 31);
+    const unsigned m = __ballot_sync(0xffffffffu, incl > U);
+    if (!m) {
+        *before = *total;
+        return 32;
+    }
+    const int l = __ffs(m) - 1;
+    *before = M::shfl(incl - v, l);
+    return l;
+}
+
+template <class M>
+__global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_kernel(InitArgs a, int ppt) {
+    typedef typename M::T T;
+    cg::cluster_group cl = cg::this_cluster();
+    const int C = (int)cl.num_blocks(), crank = (int)cl.block_rank();
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const uint64_t chunk = (uint64_t)kClusterThreads * ppt;
+    const uint64_t lo = (uint64_t)crank * chunk;
+    const uint64_t hi = lo + chunk < a.n ? lo + chunk : a.n;
+    const int mine = hi > lo ? (int)(hi - lo) : 0;
+    extern __shared__ __align__(16) unsigned char sm_raw[];
+    T *s_tsum = reinterpret_cast<T *>(sm_raw);                 // 2 x 1024
+    T *s_wsum = s_tsum + 2 * kClusterThreads;                  // 2 x 32
+    T *s_csum = s_wsum + 2 * 32;                               // 2
+    unsigned long long *s_key = reinterpret_cast<unsigned long long *>(s_csum + 2); // 2 (maximin)
+    __shared__ unsigned long long s_wkey[32];
+    uint32_t *s_col = reinterpret_cast<uint32_t *>(s_key + 2);
+    uint32_t *s_cnt = s_col + chunk;
+    uint32_t *s_md = s_cnt + chunk;                            // 2 x chunk
+    __shared__ unsigned long long s_pick;
+    __shared__ int s_amb;
+    for (int i = t; i < mine; i += kClusterThreads) {
+        s_col[i] = __ldg(a.colors + lo + i);
+        s_cnt[i] = __ldg(a.counts + lo + i);
+    }
+    __syncthreads();
+    const int p0 = t * ppt, p1 = min(p0 + ppt, mine);
+
+    // one weighted draw over the masses of buffer `par` (md = nullptr: weights only)
+    auto draw = [&](int par, double nu, const uint32_t *mdb) -> uint64_t {
+        // CTA sums of all ranks, then the target rank's warp and thread sums
+        if (warp == 0) {
+            const T cv = lane < C ? *cl.map_shared_rank(s_csum + par, lane) : (T)0;
+            T before, total;
+            const T U = M::target(nu, M::shfl(warp_incl<M>(cv), 31));
+            const int tc = lane_locate<M>(cv, U, &before, &total);
+            uint64_t idx = a.n - 1;
+            bool amb = false;
+            T E = 0, prevE = 0;
+            bool found = false;
+            if (tc < C) {
+                T b2, t2;
+                const T wv = *cl.map_shared_rank(s_wsum + par * 32 + lane, tc);
+                const int tw = lane_locate<M>(wv, U - before, &b2, &t2);
+                T b3, t3;
+                const T tv = *cl.map_shared_rank(s_tsum + par * kClusterThreads + tw * 32 + lane, tc);
+                const int tt = lane_locate<M>(tv, U - before - b2, &b3, &t3);
+                // the target thread's points, one per lane
+                const uint64_t tlo = (uint64_t)tc * chunk;
+                const int q0 = (tw * 32 + tt) * ppt;
+                const uint64_t mine_tc = a.n - tlo < chunk ? a.n - tlo : chunk;
+                const int nq = (uint64_t)q0 >= mine_tc ? 0 : (int)min((uint64_t)ppt, mine_tc - (uint64_t)q0);
+                T mv = 0;
+                if (lane < nq) {
+                    const uint32_t cnt = *cl.map_shared_rank(s_cnt + q0 + lane, tc);
+                    const uint32_t md = mdb ? *cl.map_shared_rank(mdb + q0 + lane, tc) : kWeightsOnly;
+                    mv = M::mass_c(a, cnt, md);
+                }
+                T b4, t4;
+                const int tl = lane_locate<M>(mv, U - before - b2 - b3, &b4, &t4);
+                if (tl < nq) {
+                    idx = tlo + q0 + tl;
+                    prevE = before + b2 + b3 + b4;
+                    E = prevE + M::shfl(mv, tl);
+                    found = true;
+                }
+            }
+            if (!found || idx >= a.n - 1) {
+                idx = a.n - 1;
+                if (!M::exact && a.n > 1) {
+                    const uint32_t r = (uint32_t)((a.n - 1) / chunk), li = (uint32_t)((a.n - 1) % chunk);
+                    const uint32_t cnt = *cl.map_shared_rank(s_cnt + li, r);
+                    const uint32_t md = mdb ? *cl.map_shared_rank(mdb + li, r) : kWeightsOnly;
+                    amb = !(U > total - M::mass_c(a, cnt, md) + M::bound(a.n, total));
+                }
+            } else if (!M::exact) {
+                const T B2 = M::bound(a.n, total);
+                amb = !(E > U + B2) || (idx > 0 && !(U > prevE + B2));
+            }
+            if (lane == 0) {
+                s_pick = idx;
+                s_amb = amb ? 1 : 0;
+            }
+        }
+        __syncthreads();
+        if (s_amb) { // identical in every CTA: uniform extra barrier
+            if (crank == 0 && t == 0) {
+                s_pick = cluster_sequential_draw<M>(a, cl, s_cnt, mdb, chunk, nu, mdb == nullptr);
+                atomicAdd(a.fallbacks, 1ull);
+            }
+            cl.sync();
+            const unsigned long long v = *cl.map_shared_rank(&s_pick, 0);
+            __syncthreads();
+            if (t == 0) s_pick = v;
+            __syncthreads();
+        }
+        return s_pick;
+    };
+
+    auto publish = [&](int par, T ts) {
+        s_tsum[par * kClusterThreads + t] = ts;
+        T w = ts;
+        for (int o = 16; o; o >>= 1) w += M::shfl(w, lane ^ o);
+        if (lane == 0) s_wsum[par * 32 + warp] = w;
+        __syncthreads();
+        if (warp == 0) {
+            T c = s_wsum[par * 32 + lane];
+            for (int o = 16; o; o >>= 1) c += M::shfl(c, lane ^ o);
+            if (lane == 0) s_csum[par] = c;
+        }
+    };
+
+    auto colour_of = [&](uint64_t gi) -> uint32_t {
+        return *cl.map_shared_rank(s_col + (gi % chunk), (unsigned)(gi / chunk));
+    };
+
+    int par = 0;
+    uint64_t first;
+    if (a.kind == 1 || a.weighted_first) {
+        T ts = 0;
+        for (int i = p0; i < p1; ++i) ts += M::mass_c(a, s_cnt[i], kWeightsOnly);
+        publish(par, ts);
+        cl.sync();
+        first = draw(par, a.nu[0], nullptr);
+        par ^= 1;
+    } else {
+        first = a.first_index;
+    }
+    uint32_t clast = colour_of(first);
+    if (crank == 0 && t == 0) {
+        a.cen[0] = (double)((clast >> 16) & 255u);
+        a.cen[1] = (double)((clast >> 8) & 255u);
+        a.cen[2] = (double)(clast & 255u);
+    }
+    for (int k = 1; k < a.K; ++k) {
+        const uint32_t *md_in = s_md + (size_t)((k - 1) & 1) * chunk;
+        uint32_t *md_out = s_md + (size_t)(k & 1) * chunk;
+        uint64_t pick;
+        if (a.kind == 0) {
+            unsigned long long best = 0;
+            for (int i = p0; i < p1; ++i) {
+                const uint32_t d = d2_int(s_col[i], clast);
+                const uint32_t m = k == 1 ? d : min(md_in[i], d);
+                md_out[i] = m;
+                const unsigned long long key = ((unsigned long long)m << 32) | (uint32_t)~(uint32_t)(lo + i);
+                best = key > best ? key : best;
+            }
+            for (int o = 16; o; o >>= 1) {
+                const unsigned long long x = __shfl_xor_sync(0xffffffffu, best, o);
+                best = x > best ? x : best;
+            }
+            if (lane == 0) s_wkey[warp] = best;
+            __syncthreads();
+            if (warp == 0) {
+                unsigned long long b = s_wkey[lane];
+                for (int o = 16; o; o >>= 1) {
+                    const unsigned long long x = __shfl_xor_sync(0xffffffffu, b, o);
+                    b = x > b ? x : b;
+                }
+                if (lane == 0) s_key[par] = b;
+            }
+            cl.sync();
+            if (warp == 0) {
+                unsigned long long b = lane < C ? *cl.map_shared_rank(s_key + par, lane) : 0ull;
+                for (int o = 16; o; o >>= 1) {
+                    const unsigned long long x = __shfl_xor_sync(0xffffffffu, b, o);
+                    b = x > b ? x : b;
+                }
+                if (lane == 0) s_pick = (uint64_t)(uint32_t)~(uint32_t)(b & 0xFFFFFFFFull);
+            }
+            __syncthreads();
+            pick = s_pick;
+        } else {
+            T ts = 0;
+            for (int i = p0; i < p1; ++i) {
+                const uint32_t d = d2_int(s_col[i], clast);
+                const uint32_t m = k == 1 ? d : min(md_in[i], d);
+                md_out[i] = m;
+                ts += M::mass_c(a, s_cnt[i], m);
+            }
+            publish(par, ts);
+            cl.sync();
+            pick = draw(par, a.nu[k], md_out);
+        }
+        par ^= 1;
+        clast = colour_of(pick);
+        if (crank == 0 && t == 0) {
+            a.cen[3 * k] = (double)((clast >> 16) & 255u);
+            a.cen[3 * k + 1] = (double)((clast >> 8) & 255u);
+            a.cen[3 * k + 2] = (double)(clast & 255u);
+        }
+        __syncthreads();
+    }
+    cl.sync(); // no CTA may exit while others still read its shared memory
+}
+
+template <class M>
+static size_t cluster_smem(int ppt) {
+    return sizeof(typename M::T) * (2 * kClusterThreads + 64 + 2) + 16 +
+           (size_t)kClusterThreads * ppt * 4 * sizeof(uint32_t);
+}
+
+// Try the cluster initialiser; false when the substrate does not fit.
+template <class M>
+static bool launch_cluster_init(cqg_ctx *ctx, InitArgs a) {
+    constexpr int C = 16;
+    const uint64_t per = (a.n + C - 1) / C;
+    const int ppt = (int)((per + kClusterThreads - 1) / kClusterThreads);
+    if (ppt < 1 || ppt > 32) return false;
+    const size_t smem = cluster_smem<M>(ppt);
+    if (smem > 227 * 1024) return false;
+    auto kern = init_cluster_kernel<M>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess ||
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(C);
+    cfg.blockDim = dim3(kClusterThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int clusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg) != cudaSuccess || clusters < 1) {
+        cudaGetLastError();
+        return false;
+    }
+    const int pb = prof_begin(ctx);
+    CQG_CUDA(cudaLaunchKernelEx(&cfg, kern, a, ppt));
+    prof_end(ctx, CQG_PROF_INIT, pb, (double)a.n * (double)(a.K - 1));
+    launched(ctx);
+    return true;
+}
+
 void run_init(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *counts_d, uint64_t n, uint64_t P,
               int K, uint64_t seed, int kind, int weighted_first, double *centers_d) {
     cudaStream_t s = ctx->stream;
@@ -557,6 +851,27 @@ void run_init(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *counts_d, 
         for (int i = 0; i < draws; ++i) nu.push_back(unit());
     }
     const bool exact = (P & (P - 1)) == 0 && P <= (1ull << 32);
+    if (ctx->use_cluster_init && n <= 16ull * kClusterThreads * 32) {
+        double *nu_c = static_cast<double *>(ctx->unit_draws.ensure(sizeof(double) * nu.size()));
+        CQG_CUDA(cudaMemcpyAsync(nu_c, nu.data(), sizeof(double) * nu.size(), cudaMemcpyHostToDevice, s));
+        unsigned long long *resc = static_cast<unsigned long long *>(ctx->status.ensure(64));
+        CQG_CUDA(cudaMemsetAsync(resc, 0, 64, s));
+        InitArgs c{};
+        c.colors = colors_d;
+        c.counts = counts_d;
+        c.n = n;
+        c.inv = 1.0 / static_cast<double>(P);
+        c.K = K;
+        c.kind = kind;
+        c.weighted_first = weighted_first;
+        c.exact_sums = exact ? 1 : 0;
+        c.first_index = first_index;
+        c.nu = nu_c;
+        c.result = resc;
+        c.fallbacks = resc + 4;
+        c.cen = centers_d;
+        if (exact ? launch_cluster_init<ExactMass>(ctx, c) : launch_cluster_init<FixedMass>(ctx, c)) return;
+    }
     const void *kern = exact ? (const void *)init_kernel<ExactMass> : (const void *)init_kernel<FixedMass>;
     int occ = 0;
     CQG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kInitThreads, 0));

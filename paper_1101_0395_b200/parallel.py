@@ -45,14 +45,19 @@ class CudaShardEngine:
         self.ctx, self.torch, self.device = ctx, torch, device
 
     def begin(self, colors, counts, P, init, K, term: cabi.Term):
+        """colors/counts/init: numpy arrays or device tensors (used in place)."""
         self.K = K
-        colors = np.ascontiguousarray(colors, np.uint32)
-        counts = np.ascontiguousarray(counts, np.uint32)
-        init = np.ascontiguousarray(np.asarray(init, np.float64).reshape(-1, 3))
-        cabi.check(self.ctx.L.cqg_shard_begin(self.ctx.h, cabi.ptr(colors) if colors.size else None,
-                                              cabi.ptr(counts) if counts.size else None, colors.size,
+        def prep(a, dt):
+            if hasattr(a, "data_ptr") and not isinstance(a, np.ndarray):
+                return a.contiguous()
+            return np.ascontiguousarray(a, dt)
+        colors, counts = prep(colors, np.uint32), prep(counts, np.uint32)
+        init = prep(init if hasattr(init, "data_ptr") else np.asarray(init, np.float64).reshape(-1, 3), np.float64)
+        n = int(colors.numel() if hasattr(colors, "numel") else colors.size)
+        cabi.check(self.ctx.L.cqg_shard_begin(self.ctx.h, cabi.ptr(colors) if n else None,
+                                              cabi.ptr(counts) if n else None, n,
                                               P, cabi.ptr(init), K, C.byref(term)))
-        self.n = colors.size
+        self.n = n
 
     def _partial(self, fn):
         t = self.torch.empty(5 * self.K + 2, dtype=self.torch.int64, device=self.device)
