@@ -75,6 +75,8 @@ typedef struct {
     uint64_t ndc_total;
     uint64_t n_points;
     uint64_t flagged_total; /* points replayed in exact FP64 (diagnostic) */
+    uint64_t swept_total;   /* points evaluated against every centre, summed over iterations;
+                               the rest were proven to keep their label by distance bounds */
 } cqg_lloyd_stats;
 
 typedef struct {

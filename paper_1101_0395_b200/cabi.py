@@ -48,7 +48,8 @@ class Term(C.Structure):
 
 class LloydStats(C.Structure):
     _fields_ = [("iterations", C.c_int), ("repair_count", C.c_int), ("ndc_total", C.c_uint64),
-                ("n_points", C.c_uint64), ("flagged_total", C.c_uint64)]
+                ("n_points", C.c_uint64), ("flagged_total", C.c_uint64),
+                ("swept_total", C.c_uint64)]
 
 
 class QuantizeCfg(C.Structure):

@@ -208,6 +208,10 @@ cqg_ctx *cqg_create(int device) {
         ctx->use_graphs = !(ng && ng[0] == '1');
         const char *nc = getenv("CQG_NO_CLUSTER_INIT");
         ctx->use_cluster_init = !(nc && nc[0] == '1');
+        const char *np = getenv("CQG_NO_PRUNE");
+        ctx->use_prune = !(np && np[0] == '1');
+        const char *nn = getenv("CQG_NO_NDC_CODE");
+        ctx->use_ndc_code = !(nn && nn[0] == '1');
     });
     if (rc != CQG_OK) {
         delete ctx;
@@ -377,6 +381,7 @@ int cqg_lloyd(cqg_ctx *ctx, const uint32_t *colors, const uint32_t *counts, uint
             stats->ndc_total = o.ndc;
             stats->n_points = n;
             stats->flagged_total = o.flagged;
+            stats->swept_total = o.swept;
         }
     });
 }
@@ -558,6 +563,7 @@ int cqg_quantize(cqg_ctx *ctx, const uint8_t *rgb, uint64_t P, const cqg_quantiz
             stats->lloyd.ndc_total = o.ndc;
             stats->lloyd.n_points = n;
             stats->lloyd.flagged_total = o.flagged;
+            stats->lloyd.swept_total = o.swept;
             stats->mean_sq_dist = mse;
             stats->ms_histogram = t_hist;
             stats->ms_init = t_init;

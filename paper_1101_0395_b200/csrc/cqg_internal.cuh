@@ -121,6 +121,7 @@ struct cqg_ctx {
     // Lloyd state
     cqg::DevBuf labels, cen, fcen, dtab, dsorted, order, mom, queue, ndc, status, sizes, red;
     cqg::DevBuf hist_labels, hist_centers, sse;
+    cqg::DevBuf bnd, shift, dcode;     // distance-bound pruning: per-point (ub, lb), centre moves
     cqg::DevBuf mom_g, partial; // sharded Lloyd: global moments, packed partials
     void *shard = nullptr;      // cqg::ShardState (lloyd.cu)
     // mapping
@@ -132,6 +133,8 @@ struct cqg_ctx {
     // cached CUDA graph of the Lloyd WHILE loop (lloyd.cu)
     bool use_graphs = true;
     bool use_cluster_init = true;
+    bool use_ndc_code = true; // shared-memory code table for the NDC count (CQG_NO_NDC_CODE=1: off)
+    bool use_prune = true; // distance-bound pruning of the WALK sweep (CQG_NO_PRUNE=1: off)
     cudaGraphExec_t loop_exec = nullptr;
     cudaGraph_t loop_graph = nullptr;
     std::vector<uint64_t> loop_key;
@@ -214,6 +217,7 @@ struct LloydOut {
     int repairs = 0;
     unsigned long long ndc = 0;
     unsigned long long flagged = 0;
+    unsigned long long swept = 0; // points through the full centre loop, all iterations
 };
 LloydOut lloyd_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *counts_d, uint64_t n,
                    uint64_t P, const double *init_d, int k, const cqg_term &term, uint32_t *labels_d,

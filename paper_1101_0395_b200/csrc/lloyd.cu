@@ -103,7 +103,20 @@ struct IterArgs {
     cudaGraphConditionalHandle cond;
     int use_cond;
     int reset_qn; // persistent kernel: clear the replay queue counter
+    uint16_t *dcode;  // K x Kpow codes of dsorted for ndc_code_kernel, or null
+    float *shift;     // K centre moves (FP64 -> float, rounded up) + {max, 2nd max, argmax}; null = off
+    int *shift_inval; // set by a repair: the next shifts are +inf (all bounds void)
 };
+
+__device__ __forceinline__ void top2_merge(float &m1, int &i1, float &m2, float n1, int j1, float n2) {
+    if (n1 > m1) {
+        m2 = fmaxf(m1, n2);
+        m1 = n1;
+        i1 = j1;
+    } else {
+        m2 = fmaxf(m2, n1);
+    }
+}
 
 // Finalise one iteration and build the next walk table. Called by every block
 // of a grid (iter_end_kernel, or the persistent kernel's phase C): block 0
@@ -147,7 +160,47 @@ __device__ bool iter_end_body(const IterArgs &a, double *sm, float *fc_dst, floa
         return false;
     }
     if (blockIdx.x == 0) {
-        for (int k = threadIdx.x; k < 3 * K; k += blockDim.x) a.cen[k] = s_c[k];
+        // centre moves for the distance bounds, then publish the new centres
+        float m1 = -1.f, m2 = -1.f;
+        int i1 = -1;
+        for (int k = threadIdx.x; k < K; k += blockDim.x) {
+            if (a.shift) {
+                const double dr = __dsub_rn(s_c[3 * k], a.cen[3 * k]);
+                const double dg = __dsub_rn(s_c[3 * k + 1], a.cen[3 * k + 1]);
+                const double db = __dsub_rn(s_c[3 * k + 2], a.cen[3 * k + 2]);
+                const double d = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(dr, dr), __dmul_rn(dg, dg)), __dmul_rn(db, db)));
+                const float f = __double2float_ru(__dmul_ru(d, 1.0 + 0x1.0p-40)); // covers FP64 rounding
+                a.shift[k] = f;
+                top2_merge(m1, i1, m2, f, k, -1.f);
+            }
+            a.cen[3 * k] = s_c[3 * k];
+            a.cen[3 * k + 1] = s_c[3 * k + 1];
+            a.cen[3 * k + 2] = s_c[3 * k + 2];
+        }
+        if (a.shift) {
+            __shared__ float s_m1[32], s_m2[32];
+            __shared__ int s_i1[32];
+            for (int o = 16; o; o >>= 1) {
+                const float n1 = __shfl_xor_sync(0xffffffffu, m1, o), n2 = __shfl_xor_sync(0xffffffffu, m2, o);
+                const int j1 = __shfl_xor_sync(0xffffffffu, i1, o);
+                top2_merge(m1, i1, m2, n1, j1, n2);
+            }
+            if ((threadIdx.x & 31) == 0) {
+                s_m1[threadIdx.x >> 5] = m1;
+                s_m2[threadIdx.x >> 5] = m2;
+                s_i1[threadIdx.x >> 5] = i1;
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                for (int w = 1; w < (int)(blockDim.x >> 5); ++w) top2_merge(m1, i1, m2, s_m1[w], s_i1[w], s_m2[w]);
+                const bool inval = *a.shift_inval != 0;
+                const float inf = __int_as_float(0x7f800000);
+                a.shift[K] = inval ? inf : fmaxf(m1, 0.f);
+                a.shift[K + 1] = inval ? inf : fmaxf(m2, 0.f);
+                a.shift[K + 2] = __int_as_float(i1);
+                *a.shift_inval = 0;
+            }
+        }
         if (threadIdx.x == 0) {
             double tot = 0.0;
             for (int k = 0; k < K; ++k) tot = __dadd_rn(tot, s_a[k]);
@@ -221,6 +274,7 @@ __device__ bool iter_end_body(const IterArgs &a, double *sm, float *fc_dst, floa
             const int np = p < ps ? p + 1 : (p == ps ? 0 : p);
             if (p < K) a.order[(size_t)i * K + np] = (uint32_t)s_rank[p];
             a.dsorted[(size_t)i * a.Kpow + np] = s_d[p];
+            if (a.dcode) a.dcode[(size_t)i * a.Kpow + np] = (uint16_t)code16(s_d[p]);
         }
         __syncthreads();
     }
@@ -237,7 +291,8 @@ __global__ void __launch_bounds__(1024) iter_end_kernel(IterArgs a) {
 // finalise + walk table). Every block keeps its own FP32 centre table in shared memory.
 // Exits early (state 2) on an empty cluster; the host repairs and relaunches.
 template <int PPT>
-__global__ void __launch_bounds__(kSweepThreads, 2) lloyd_persistent_kernel(SweepArgs a, IterArgs ia, int first_full) {
+__global__ void __launch_bounds__(kSweepThreads, 2) lloyd_persistent_kernel(SweepArgs a, IterArgs ia, int first_full,
+                                                                            uint32_t list_cap) {
     cg::grid_group grid = cg::this_grid();
     extern __shared__ __align__(16) double psm[];
     const int K = a.K, Kp = a.Kp;
@@ -246,6 +301,7 @@ __global__ void __launch_bounds__(kSweepThreads, 2) lloyd_persistent_kernel(Swee
     uint32_t *s_acc = reinterpret_cast<uint32_t *>(s_tau + 4); // 10 K u32 (= 5 K u64)
     unsigned long long *s_acc64 = reinterpret_cast<unsigned long long *>(s_acc);
     double *s_end = reinterpret_cast<double *>(s_acc + 10 * K); // 5 K doubles + K ints
+    uint32_t *s_list = reinterpret_cast<uint32_t *>(s_end + 4 * K + ia.Kpow) + ia.Kpow; // prune list
     fc_block(a.cen, K, Kp, s_fc, s_tau);
     const uint64_t chunk = (a.n + gridDim.x - 1) / gridDim.x;
     const uint64_t lo = (uint64_t)blockIdx.x * chunk;
@@ -273,7 +329,8 @@ __global__ void __launch_bounds__(kSweepThreads, 2) lloyd_persistent_kernel(Swee
             if ((threadIdx.x & 31) == 0 && nd) atomicAdd(a.ndc, nd);
             for (int i = threadIdx.x; i < K * 5; i += blockDim.x) s_acc64[i] = 0;
             __syncthreads();
-            sweep_range<MODE_WALK, PPT>(la, lo, hi, s_fc, s_acc, s_tau[0], s_tau[1]);
+            sweep_range<MODE_WALK, PPT>(la, lo, hi, s_fc, s_acc, s_tau[0], s_tau[1], s_list, list_cap,
+                                        reinterpret_cast<float *>(s_list + list_cap + kSweepThreads * 4));
             __syncthreads();
             flush_acc64(s_acc64, a.mom, K);
             replay_range<MODE_WALK>(la, warp, nw);
@@ -349,8 +406,10 @@ __global__ void argmax_final(ValIdx *part, int nparts) {
 
 // move point `donor` into empty cluster e: labels, centre, moments, sizes
 __global__ void apply_move_kernel(const uint32_t *colors, const uint32_t *counts, uint32_t *labels,
-                                  double *cen, Moments *mom, uint32_t *sizes, uint64_t donor, int e) {
+                                  double *cen, Moments *mom, uint32_t *sizes, uint64_t donor, int e,
+                                  int *shift_inval) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (shift_inval) *shift_inval = 1; // labels/centres changed outside the bounds' bookkeeping
     const uint32_t old = labels[donor];
     const uint32_t c = colors[donor], cnt = counts[donor];
     const uint32_t r = (c >> 16) & 255u, g = (c >> 8) & 255u, b = c & 255u;
@@ -384,11 +443,12 @@ int pick_grid(cqg_ctx *ctx, uint64_t work, int per_block, int per_sm) {
 
 } // namespace
 
-size_t sweep_smem_bytes(int K, int Kp) {
-    // u32 accumulators (FULL/MAP) or u64 (WALK): reserve the larger
-    const size_t acc32 = (size_t)K * kAccPerCluster * sizeof(uint32_t);
-    const size_t acc64 = (size_t)K * 5 * sizeof(unsigned long long);
-    return (size_t)4 * Kp * sizeof(float) + (acc64 > acc32 ? acc64 : acc32);
+size_t sweep_smem_bytes(int K, int Kp, int mode) {
+    // FP32 table, u32 accumulators (FULL/MAP) or u64 (WALK): reserve the larger,
+    // and the WALK prune list
+    return (size_t)4 * Kp * sizeof(float) + (size_t)sweep_acc_words(K) * sizeof(uint32_t) +
+           (mode == MODE_WALK ? ((size_t)kPruneChunk + kSweepThreads * 8 + prune_aux_words(K)) * sizeof(uint32_t)
+                              : 0);
 }
 
 template <int MODE, int PPT>
@@ -417,7 +477,7 @@ static void launch_ppt(cqg_ctx *ctx, const SweepArgs &a, size_t smem, int bps) {
 
 template <int MODE>
 static void launch_sweep_mode(cqg_ctx *ctx, const SweepArgs &a) {
-    const size_t smem = sweep_smem_bytes(a.K, a.Kp);
+    const size_t smem = sweep_smem_bytes(a.K, a.Kp, MODE);
     const uint64_t n = a.n;
     const uint64_t sms = (uint64_t)ctx->num_sms;
     if (MODE == MODE_WALK) {
@@ -431,7 +491,18 @@ static void launch_sweep_mode(cqg_ctx *ctx, const SweepArgs &a) {
         const bool big = n >= (uint64_t)ctx->num_sms * 4 * 256 * 8;
         const int g = big ? pick_grid(ctx, n, 2048, 4) : pick_grid(ctx, n, 512, 8);
         const int pn = prof_begin(ctx);
-        if (big)
+        if (a.dcode && a.K <= kNdcCodeMaxK) {
+            const size_t cs = (size_t)a.K * 24 + (size_t)a.K * (a.Kpow + 2) * 2;
+            static thread_local bool cattr = false;
+            if (!cattr) {
+                CQG_CUDA(cudaFuncSetAttribute(ndc_code_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              kNdcCodeMaxK * 24 + kNdcCodeMaxK * (kNdcCodeMaxK + 2) * 2));
+                cattr = true;
+            }
+            const int gc = pick_grid(ctx, n, 1024 * 4, 1);
+            ndc_code_kernel<4><<<gc, 1024, cs, ctx->stream>>>(a.colors, a.labels, n, a.cen, a.dsorted, a.dcode,
+                                                             a.K, a.Kpow, a.ndc);
+        } else if (big)
             ndc_kernel<8><<<g, 256, csm, ctx->stream>>>(a.colors, a.labels, n, a.cen, a.dsorted, a.K, a.Kpow, a.ndc);
         else
             ndc_kernel<2><<<g, 256, csm, ctx->stream>>>(a.colors, a.labels, n, a.cen, a.dsorted, a.K, a.Kpow, a.ndc);
@@ -471,7 +542,8 @@ static void launch_sweep_mode(cqg_ctx *ctx, const SweepArgs &a) {
 void bench_sweep_dev(cqg_ctx *ctx, int reps, double *ms, double *units) {
     SweepArgs a;
     std::memcpy(&a, ctx->last_sweep, sizeof(SweepArgs));
-    const size_t smem = sweep_smem_bytes(a.K, a.Kp);
+    a.bnd = nullptr; // the dense sweep (every point against every centre)
+    const size_t smem = sweep_smem_bytes(a.K, a.Kp, MODE_WALK);
     const uint64_t sms = (uint64_t)ctx->num_sms, n = a.n;
     const int b2 = sweep_bps<MODE_WALK, 2>(smem), b4 = sweep_bps<MODE_WALK, 4>(smem),
               b8 = sweep_bps<MODE_WALK, 8>(smem);
@@ -514,7 +586,7 @@ void launch_sweep(cqg_ctx *ctx, int mode, const SweepArgs &a) {
 // ---------------------------------------------------------------------------
 
 static int repair_loop(cqg_ctx *ctx, const uint32_t *colors, const uint32_t *counts, uint64_t n,
-                       uint64_t P, int K, uint32_t *labels, double *cen, Moments *mom) {
+                       uint64_t P, int K, uint32_t *labels, double *cen, Moments *mom, int *shift_inval) {
     cudaStream_t s = ctx->stream;
     uint32_t *sizes = static_cast<uint32_t *>(ctx->sizes.ensure((size_t)K * 4));
     const int nparts = pick_grid(ctx, n, 256, 2);
@@ -555,7 +627,7 @@ static int repair_loop(cqg_ctx *ctx, const uint32_t *colors, const uint32_t *cou
         CQG_CUDA(cudaMemcpyAsync(&hres[1], labels + best.i, 4, cudaMemcpyDeviceToHost, s));
         CQG_CUDA(cudaStreamSynchronize(s));
         std::memcpy(&old, &hres[1], 4);
-        apply_move_kernel<<<1, 32, 0, s>>>(colors, counts, labels, cen, mom, sizes, best.i, e);
+        apply_move_kernel<<<1, 32, 0, s>>>(colors, counts, labels, cen, mom, sizes, best.i, e, shift_inval);
         launched(ctx);
         hsz[old] -= 1;
         hsz[e] += 1;
@@ -629,14 +701,25 @@ void release_graphs(cqg_ctx *ctx) {
 }
 
 
-static size_t persist_smem(int K, int Kp) {
+static size_t persist_smem(int K, int Kp, size_t list_words) {
     return (size_t)4 * Kp * sizeof(float) + 4 * sizeof(float) + (size_t)10 * K * sizeof(uint32_t) +
-           iter_end_smem(K);
+           iter_end_smem(K) + list_words * sizeof(uint32_t);
 }
+
+// prune-list capacity of the persistent kernel: a block's whole point range
+static size_t persist_list_words(const cqg_ctx *ctx, uint64_t n) {
+    // grid = min(num_sms * bps, ceil(n / 64)): a block owns <= max(ceil(n / num_sms), 64) points
+    uint64_t r = (n + ctx->num_sms - 1) / ctx->num_sms;
+    if (r < 128) r = 128;
+    return (size_t)(r < (uint64_t)kPruneChunk ? r : (uint64_t)kPruneChunk);
+}
+// shared words of the prune list: the chunk plus one carried-over big tile (PPT <= 4)
+static size_t persist_list_alloc(size_t cap, int K) { return cap ? cap + kSweepThreads * 4 + prune_aux_words(K) : 0; }
 
 // Launch the persistent loop if it fits co-resident; returns false otherwise.
 static bool launch_persistent(cqg_ctx *ctx, const SweepArgs &a, IterArgs ia, bool first_full) {
-    const size_t smem = persist_smem(a.K, a.Kp);
+    const uint32_t list_cap = a.bnd ? (uint32_t)persist_list_words(ctx, a.n) : 0u;
+    const size_t smem = persist_smem(a.K, a.Kp, persist_list_alloc(list_cap, a.K));
     const int ppt = a.n <= (uint64_t)ctx->num_sms * 2 * kSweepThreads * 2 ? 2 : 4;
     const void *kern = ppt == 2 ? (const void *)lloyd_persistent_kernel<2> : (const void *)lloyd_persistent_kernel<4>;
     static thread_local const void *c_kern = nullptr;
@@ -659,7 +742,8 @@ static bool launch_persistent(cqg_ctx *ctx, const SweepArgs &a, IterArgs ia, boo
     ia.reset_qn = 1;
     SweepArgs aa = a;
     int ff = first_full ? 1 : 0;
-    void *args[] = {&aa, &ia, &ff};
+    uint32_t lc = list_cap;
+    void *args[] = {&aa, &ia, &ff, &lc};
     CQG_CUDA(cudaLaunchCooperativeKernel(kern, dim3((unsigned)grid), dim3(kSweepThreads), args, smem, ctx->stream));
     launched(ctx);
     return true;
@@ -680,6 +764,9 @@ LloydOut lloyd_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *count
     int Kpow = 1;
     while (Kpow < K) Kpow <<= 1;
     double *dsorted = static_cast<double *>(ctx->dsorted.ensure(sizeof(double) * (size_t)K * Kpow));
+    uint16_t *dcode = K <= kNdcCodeMaxK && ctx->use_ndc_code
+                          ? static_cast<uint16_t *>(ctx->dcode.ensure(sizeof(uint16_t) * (size_t)K * Kpow + 16))
+                          : nullptr;
     uint32_t *order = static_cast<uint32_t *>(ctx->order.ensure(sizeof(uint32_t) * (size_t)K * K));
     Moments *mom = static_cast<Moments *>(ctx->mom.ensure(sizeof(Moments) * (size_t)K));
     uint32_t *queue = static_cast<uint32_t *>(ctx->queue.ensure(sizeof(uint32_t) * (n + 1)));
@@ -688,6 +775,11 @@ LloydOut lloyd_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *count
     unsigned long long *flagged = reinterpret_cast<unsigned long long *>(qn + 10);
     int *iter_dev = reinterpret_cast<int *>(qn + 12);
     IterStatus *st = reinterpret_cast<IterStatus *>(qn + 16);
+    unsigned long long *swept = reinterpret_cast<unsigned long long *>(qn + 32);
+    int *shift_inval = reinterpret_cast<int *>(qn + 36);
+    const bool prune = ctx->use_prune;
+    float2 *bnd = prune ? static_cast<float2 *>(ctx->bnd.ensure(sizeof(float2) * (n + 1))) : nullptr;
+    float *shift = prune ? static_cast<float *>(ctx->shift.ensure(sizeof(float) * ((size_t)K + 4))) : nullptr;
     double *sse_d = static_cast<double *>(ctx->sse.ensure(sizeof(double) * (size_t)(limit + 1)));
     IterStatus *hst = static_cast<IterStatus *>(ctx->pinned.ensure(4096));
     const bool hist = term.record_history && (hist_labels_user || hist_centers_user);
@@ -700,6 +792,7 @@ LloydOut lloyd_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *count
 
     CQG_CUDA(cudaMemsetAsync(mom, 0, sizeof(Moments) * (size_t)K, s));
     CQG_CUDA(cudaMemsetAsync(ndc, 0, 24, s)); // ndc, flagged, iter_dev
+    CQG_CUDA(cudaMemsetAsync(swept, 0, 16, s)); // swept, shift_inval
     fc_kernel<<<1, 256, 0, s>>>(cen, K, Kp, fc, tau);
     launched(ctx);
 
@@ -721,6 +814,10 @@ LloydOut lloyd_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *count
     a.K = K;
     a.Kp = Kp;
     a.Kpow = Kpow;
+    a.bnd = bnd;
+    a.shift = shift;
+    a.dcode = dcode;
+    a.swept = swept;
     std::memcpy(ctx->last_sweep, &a, sizeof(SweepArgs)); // for cqg_bench_sweep
     ctx->have_last_sweep = true;
 
@@ -747,6 +844,9 @@ LloydOut lloyd_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *count
     ia.order = order;
     ia.Kpow = Kpow;
     ia.use_cond = 0;
+    ia.shift = shift;
+    ia.shift_inval = shift_inval;
+    ia.dcode = dcode;
 
     // The graph path needs no per-iteration host work: used unless history is
     // recorded (per-iteration copies) or kernel profiling is on (per-launch events).
@@ -789,7 +889,7 @@ LloydOut lloyd_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *count
         iter = hst->iteration;
         prof_add_units(ctx, rec, (double)n * (double)K * (double)(iter - before));
         if (hst->state == 2) {
-            out.repairs += repair_loop(ctx, colors_d, counts_d, n, P, K, labels_d, cen, mom);
+            out.repairs += repair_loop(ctx, colors_d, counts_d, n, P, K, labels_d, cen, mom, shift_inval);
             IterArgs ib = ia;
             ib.reset_qn = persistent ? 1 : 0;
             launch_iter_end(ctx, ib);
@@ -804,6 +904,7 @@ LloydOut lloyd_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *count
     CQG_CUDA(cudaMemcpyAsync(sse_host, sse_d, sizeof(double) * iter, cudaMemcpyDefault, s));
     unsigned long long *hcnt = reinterpret_cast<unsigned long long *>(hst + 1);
     CQG_CUDA(cudaMemcpyAsync(hcnt, ndc, 16, cudaMemcpyDeviceToHost, s));
+    CQG_CUDA(cudaMemcpyAsync(hcnt + 2, swept, 8, cudaMemcpyDeviceToHost, s));
     if (hist) {
         if (hist_labels_user) copy_out(ctx, hist_labels_user, hl_d, sizeof(uint32_t) * n * (size_t)iter);
         if (hist_centers_user) copy_out(ctx, hist_centers_user, hc_d, 24 * (size_t)K * iter);
@@ -811,6 +912,8 @@ LloydOut lloyd_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *count
     CQG_CUDA(cudaStreamSynchronize(s));
     out.ndc = hcnt[0];
     out.flagged = hcnt[1];
+    // FULL first iteration sweeps every point; WALK iterations count the survivors
+    out.swept = prune ? hcnt[2] + n : n * (unsigned long long)iter;
     return out;
 }
 
@@ -1016,7 +1119,8 @@ void shard_move_dev(cqg_ctx *ctx, uint64_t index, int e, uint32_t colour) {
     cudaStream_t s = ctx->stream;
     if (index < S.n) {
         uint32_t *sizes = static_cast<uint32_t *>(ctx->sizes.ensure((size_t)S.K * 4));
-        apply_move_kernel<<<1, 32, 0, s>>>(S.a.colors, S.a.counts, S.a.labels, S.ia.cen, S.a.mom, sizes, index, e);
+        apply_move_kernel<<<1, 32, 0, s>>>(S.a.colors, S.a.counts, S.a.labels, S.ia.cen, S.a.mom, sizes, index, e,
+                                            nullptr);
     } else {
         set_centre_kernel<<<1, 32, 0, s>>>(S.ia.cen, e, colour);
     }

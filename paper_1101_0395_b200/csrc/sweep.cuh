@@ -46,6 +46,15 @@ struct SweepArgs {
     unsigned long long *ndc;
     int K, Kp;
     int Kpow; // dsorted row stride: next power of two >= K
+    // Distance-bound pruning (WALK/FULL; null = off): per point (ub, lb) with
+    // ub >= d(x, c_label) and lb <= min_{j != label} d(x, c_j) (Euclidean,
+    // directed rounding); shift = K per-centre moves since the bounds were
+    // written + {max, second max, argmax bits}; swept counts the points that
+    // went through the full centre loop.
+    float2 *bnd;
+    const float *shift;
+    unsigned long long *swept;
+    const uint16_t *dcode; // K x Kpow 16-bit monotone codes of dsorted (ndc_code_kernel), or null
 };
 
 __device__ __forceinline__ uint32_t lane_lt_mask() {
@@ -241,6 +250,85 @@ static __global__ void __launch_bounds__(256, 4) ndc_kernel(const uint32_t *__re
     if ((threadIdx.x & 31) == 0 && local) atomicAdd(ndc, local);
 }
 
+// 16-bit monotone code of a non-negative double: the top half of its
+// round-down FP32 value. Bucket property: bf(c) <= v < bf(c + 1), where bf(c)
+// is the float with bits c << 16; so code(D) < code(cut) implies D < cut and
+// code(D) > code(cut) implies D >= cut. Equal codes need the FP64 values.
+__device__ __forceinline__ uint32_t code16(double v) { return __float_as_uint(__double2float_rd(v)) >> 16; }
+
+// NDC with the walk rows as 16-bit codes in shared memory (K <= 256): the
+// branch-free lifting runs on shared memory (a few bank-conflict wavefronts
+// per warp step instead of 32 L1 lines); only a code tie with the cutoff reads
+// the FP64 row. One 1024-thread block per SM, 4 points per thread in flight.
+constexpr int kNdcCodeMaxK = 256;
+template <int Q>
+static __global__ void __launch_bounds__(1024, 1) ndc_code_kernel(const uint32_t *__restrict__ colors,
+                                                                   const uint32_t *__restrict__ labels, uint64_t n,
+                                                                   const double *__restrict__ cen,
+                                                                   const double *__restrict__ dsorted,
+                                                                   const uint16_t *__restrict__ dcode, int K,
+                                                                   int Kpow, unsigned long long *ndc) {
+    extern __shared__ __align__(16) double s_cenc[];
+    // rows padded by one 32-bit word: row r, position p lands in bank
+    // (r + p / 2) mod 32, so a warp searching different rows spreads over the
+    // banks (an unpadded 2^m-byte stride puts position p of every row in one bank)
+    const int rs = Kpow + 2; // row stride in codes
+    uint16_t *s_code = reinterpret_cast<uint16_t *>(s_cenc + 3 * K);
+    for (int i = threadIdx.x; i < 3 * K; i += blockDim.x) s_cenc[i] = cen[i];
+    if (Kpow >= 2) {
+        const int hw = Kpow / 2; // 32-bit words per row
+        const uint32_t *src = reinterpret_cast<const uint32_t *>(dcode);
+        uint32_t *dst = reinterpret_cast<uint32_t *>(s_code);
+        for (int i = threadIdx.x; i < K * hw; i += blockDim.x) {
+            const int r = i / hw, w = i - r * hw;
+            dst[r * (hw + 1) + w] = src[i];
+        }
+    } else {
+        for (int r = threadIdx.x; r < K; r += blockDim.x) s_code[r * rs] = dcode[r];
+    }
+    __syncthreads();
+    unsigned long long local = 0;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * Q;
+    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x * Q; base < n; base += stride) {
+        double cut[Q];
+        uint32_t cc[Q];
+        int prow[Q], pos[Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const uint64_t i = base + threadIdx.x + (uint64_t)q * blockDim.x;
+            const bool v = i < n;
+            const uint32_t col = v ? __ldg(colors + i) : 0u;
+            const int prev = v ? (int)__ldg(labels + i) : 0;
+            const double pd = d2_exact((double)((col >> 16) & 255u), (double)((col >> 8) & 255u),
+                                       (double)(col & 255u), s_cenc[3 * prev], s_cenc[3 * prev + 1],
+                                       s_cenc[3 * prev + 2]);
+            cut[q] = v ? __dmul_rn(4.0, pd) : -1.0;
+            cc[q] = v ? code16(cut[q]) : 0u; // invalid: code 0 counts nothing below
+            prow[q] = prev;
+            pos[q] = 0;
+        }
+        for (int step = Kpow >> 1; step >= 1; step >>= 1) {
+            uint32_t vv[Q];
+#pragma unroll
+            for (int q = 0; q < Q; ++q) vv[q] = s_code[prow[q] * rs + pos[q] + step - 1];
+#pragma unroll
+            for (int q = 0; q < Q; ++q) pos[q] += vv[q] < cc[q] ? step : 0;
+        }
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            if (cut[q] < 0.0) continue;
+            int p = pos[q];
+            const uint16_t *row = s_code + prow[q] * rs;
+            if (p == Kpow - 1 && row[Kpow - 1] < cc[q]) p = Kpow; // whole row below
+            // entries whose code equals the cutoff's: decide with the FP64 values
+            while (p < Kpow && row[p] == cc[q] && __ldg(dsorted + (size_t)prow[q] * Kpow + p) < cut[q]) ++p;
+            local += (unsigned long long)(p - (cut[q] > 0.0 ? 1 : 0) + 1);
+        }
+    }
+    for (int o = 16; o; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+    if ((threadIdx.x & 31) == 0 && local) atomicAdd(ndc, local);
+}
+
 // ---------------------------------------------------------------------------
 // The sweep kernel. Each block owns a contiguous, equal share of the points
 // (balanced across SMs); PPT points per thread amortise the shared-memory
@@ -253,6 +341,10 @@ static __global__ void __launch_bounds__(256, 4) ndc_kernel(const uint32_t *__re
 // recomputing the 8 distances of that group with the identical FP operation
 // sequence (bit-identical values) and taking the first that equals b1.
 constexpr int kGroup = 8;
+// u32 words of the sweep accumulators: u32 x kAccPerCluster (FULL/MAP) or u64 x 5 (WALK)
+__host__ __device__ constexpr int sweep_acc_words(int K) {
+    return K * kAccPerCluster > K * 10 ? K * kAccPerCluster : K * 10;
+}
 constexpr int kSmemCentres = 1024; // FP64 centres staged in shared memory up to this K
 
 __device__ __forceinline__ void track_pair(float2 v, float &b1, float &b2) {
@@ -261,29 +353,34 @@ __device__ __forceinline__ void track_pair(float2 v, float &b1, float &b2) {
     b1 = fminf(b1, lo);
 }
 
-// Sweep points [lo, hi) of this block against the FP32 centre table in shared
-// memory (s_fc: m2r | m2g | m2b | cc, Kp each). FULL/MAP flush the u32 shared
+// Sweep points of this block against the FP32 centre table in shared memory
+// (s_fc: m2r | m2g | m2b | cc, Kp each): slots [lo, hi), point index = the
+// slot (LIST = false) or list[slot]. FULL/MAP flush the u32 shared
 // accumulators after every tile; WALK leaves its u64 deltas for the caller.
-template <int MODE, int PPT>
-__device__ __forceinline__ void sweep_range(const SweepArgs &a, uint64_t lo, uint64_t hi, float *smem,
-                                            uint32_t *s_acc, float tau_abs, float tau_rel) {
+template <int MODE, int PPT, bool LIST>
+__device__ __forceinline__ void sweep_tiles(const SweepArgs &a, uint64_t lo, uint64_t hi, const uint32_t *list,
+                                            float *smem, uint32_t *s_acc, float tau_abs, float tau_rel) {
     static_assert(PPT % 2 == 0, "points are processed in pairs");
     constexpr int PP = PPT / 2;
     const int K = a.K, Kp = a.Kp;
     float *s_m2r = smem, *s_m2g = smem + Kp, *s_m2b = smem + 2 * Kp, *s_cc = smem + 3 * Kp;
     unsigned long long *s_acc64 = reinterpret_cast<unsigned long long *>(s_acc);
+    // per-value error bound of the FP32 distances (tau_abs = 2E*1.0625 + 1e-3)
+    const float ev = 0.5f * tau_abs;
     const uint64_t tile = (uint64_t)kSweepThreads * PPT;
     for (uint64_t base = lo; base < hi; base += tile) {
         // point pairs: lane .x = point 2p, lane .y = point 2p+1 (FFMA2 with a
         // broadcast scalar centre operand evaluates one centre for both)
         float2 xr2[PP], xg2[PP], xb2[PP], xx2[PP];
         uint32_t col[PPT];
+        uint32_t pidx[PPT]; // point index (< 2^24 unique colours)
         float b1[PPT], b2[PPT];
         int g1[PPT];
 #pragma unroll
         for (int i = 0; i < PPT; ++i) {
-            const uint64_t idx = base + threadIdx.x + (uint64_t)i * kSweepThreads;
-            col[i] = idx < hi ? __ldg(a.colors + idx) : 0u;
+            const uint64_t slot = base + threadIdx.x + (uint64_t)i * kSweepThreads;
+            pidx[i] = slot < hi ? (LIST ? list[slot] : (uint32_t)slot) : 0u;
+            col[i] = slot < hi ? __ldg(a.colors + pidx[i]) : 0u;
             const float r = (float)((col[i] >> 16) & 255u), g = (float)((col[i] >> 8) & 255u),
                         b = (float)(col[i] & 255u);
             float xx = r * r + g * g + b * b; // exact: integers < 2^18
@@ -340,8 +437,8 @@ __device__ __forceinline__ void sweep_range(const SweepArgs &a, uint64_t lo, uin
         // resolve
 #pragma unroll
         for (int i = 0; i < PPT; ++i) {
-            const uint64_t idx = base + threadIdx.x + (uint64_t)i * kSweepThreads;
-            const bool valid = idx < hi;
+            const uint32_t idx = pidx[i];
+            const bool valid = base + threadIdx.x + (uint64_t)i * kSweepThreads < hi;
             const float f1 = b1[i], f2 = b2[i];
             const bool flag = valid && !((f2 - f1) > tau_abs + tau_rel * (fabsf(f1) + fabsf(f2)));
             // exact index: first centre of group g1 whose (bit-identical) value is b1
@@ -362,6 +459,13 @@ __device__ __forceinline__ void sweep_range(const SweepArgs &a, uint64_t lo, uin
                     if (found < 0 && d == f1) found = g0 + q;
                 }
                 j1 = found < 0 ? g0 : found;
+            }
+            if (MODE != MODE_MAP && a.bnd && valid) {
+                // new bounds for label j1 (flagged points: replayed, bounds void)
+                const float ub = __fsqrt_ru(__fadd_ru(f1 > 0.f ? f1 : 0.f, ev));
+                const float l2 = __fadd_rd(f2, -ev);
+                const float lb = __fsqrt_rd(l2 > 0.f ? l2 : 0.f);
+                a.bnd[idx] = flag ? make_float2(__int_as_float(0x7f800000), 0.f) : make_float2(ub, lb);
             }
             const uint32_t r = (col[i] >> 16) & 255u, g = (col[i] >> 8) & 255u, b = col[i] & 255u;
             if (MODE == MODE_WALK && valid) {
@@ -389,6 +493,130 @@ __device__ __forceinline__ void sweep_range(const SweepArgs &a, uint64_t lo, uin
     }
 }
 
+// Points per block-local chunk of the pruned WALK sweep (shared-memory list).
+constexpr int kPruneChunk = 4096;
+constexpr float kBoundMargin = 1.0e-3f; // Euclidean gap that keeps the FP64 reference order
+
+// Stay test (exact): after the centres moved by shift[], the label is provably
+// unchanged when ub' + margin < lb* with (directed rounding throughout)
+//   ub' = ub + shift[label], or the own-centre distance recomputed here,
+//   lb* = max(lb - max_{j != label} shift[j],          (Hamerly)
+//             2 s(label) - ub')                        (Elkan: s = half the distance
+//                                                       from c_label to its nearest centre,
+//                                                       dsorted[label][1]).
+// The reference picks the incumbent whenever it is the unique nearest centre
+// (nearest_full and assign_point_sortmeans alike), so skipped points keep
+// their labels and moments. s_aux = {shift[K], 2s[K]} in shared memory.
+// Returns true when the point needs the full sweep.
+__device__ __forceinline__ bool prune_needs_sweep(const SweepArgs &a, uint64_t i, uint32_t lab, float2 bd,
+                                                  uint32_t c, const float *s_fc, const float *s_aux, int Kp,
+                                                  float ev, float smax1, float smax2, int sarg) {
+    const float sl = s_aux[lab];
+    const float two_s = s_aux[a.K + lab];
+    const float so = (int)lab == sarg ? smax2 : smax1;
+    float ub = __fadd_ru(bd.x, sl);
+    const float lbh = __fadd_rd(bd.y, -so);
+    float lb = fmaxf(lbh, __fadd_rd(two_s, -ub));
+    bool stay = __fadd_ru(ub, kBoundMargin) < lb;
+    if (!stay) {
+        // tighten ub with the own-centre FP32 distance (sweep operation order)
+        const float r = (float)((c >> 16) & 255u), g = (float)((c >> 8) & 255u), b = (float)(c & 255u);
+        const float xx = r * r + g * g + b * b;
+        float d = __fadd_rn(xx, s_fc[3 * Kp + lab]);
+        d = __fmaf_rn(r, s_fc[lab], d);
+        d = __fmaf_rn(g, s_fc[Kp + lab], d);
+        d = __fmaf_rn(b, s_fc[2 * Kp + lab], d);
+        ub = __fsqrt_ru(__fadd_ru(d > 0.f ? d : 0.f, ev));
+        lb = fmaxf(lbh, __fadd_rd(two_s, -ub));
+        stay = __fadd_ru(ub, kBoundMargin) < lb;
+    }
+    if (stay) a.bnd[i] = make_float2(ub, lb);
+    return !stay;
+}
+
+// Shared words the pruned WALK sweep needs besides the list: shift[K], 2s[K].
+__host__ __device__ constexpr int prune_aux_words(int K) { return 2 * K; }
+constexpr int kFilterPPT = 8; // points per thread per filter step (loads in flight)
+
+// Sweep points [lo, hi) of this block. WALK with bounds: per chunk, the stay
+// test appends the points that may change label to a shared-memory list
+// (s_list: list_cap + one big tile of entries); full PPT-point tiles are swept
+// as soon as they fill, the remainder carries over to the next chunk, and the
+// final remainder is swept in 2-point tiles. s_aux: prune_aux_words(K) floats.
+template <int MODE, int PPT>
+__device__ __forceinline__ void sweep_range(const SweepArgs &a, uint64_t lo, uint64_t hi, float *smem,
+                                            uint32_t *s_acc, float tau_abs, float tau_rel,
+                                            uint32_t *s_list = nullptr, uint32_t list_cap = kPruneChunk,
+                                            float *s_aux = nullptr) {
+    if (MODE != MODE_WALK || a.bnd == nullptr || s_list == nullptr) {
+        sweep_tiles<MODE, PPT, false>(a, lo, hi, nullptr, smem, s_acc, tau_abs, tau_rel);
+        return;
+    }
+    __shared__ uint32_t s_m;
+    const int Kp = a.Kp, K = a.K;
+    const float ev = 0.5f * tau_abs;
+    const float smax1 = __ldg(a.shift + K), smax2 = __ldg(a.shift + K + 1);
+    const int sarg = __float_as_int(__ldg(a.shift + K + 2));
+    // per-centre terms of the stay test: shift and 2 s (nearest other centre, walk position 1)
+    for (int k = threadIdx.x; k < K; k += blockDim.x) {
+        s_aux[k] = __ldg(a.shift + k);
+        s_aux[K + k] = K > 1 ? __fsqrt_rd(__double2float_rd(
+                                   __dmul_rd(__ldg(a.dsorted + (size_t)k * a.Kpow + 1), 1.0 - 0x1.0p-40)))
+                             : __int_as_float(0x7f800000);
+    }
+    constexpr uint32_t big = kSweepThreads * PPT;
+    unsigned long long swept = 0;
+    if (threadIdx.x == 0) s_m = 0;
+    __syncthreads();
+    for (uint64_t cb = lo; cb < hi; cb += list_cap) {
+        const uint64_t ce = cb + list_cap < hi ? cb + list_cap : hi;
+        for (uint64_t i0 = cb; i0 < ce; i0 += (uint64_t)blockDim.x * kFilterPPT) {
+            uint32_t lab[kFilterPPT], col[kFilterPPT];
+            float2 bd[kFilterPPT];
+#pragma unroll
+            for (int f = 0; f < kFilterPPT; ++f) {
+                const uint64_t i = i0 + threadIdx.x + (uint64_t)f * blockDim.x;
+                const bool v = i < ce;
+                lab[f] = v ? a.labels[i] : 0u;
+                bd[f] = v ? a.bnd[i] : make_float2(0.f, 0.f);
+                col[f] = v ? __ldg(a.colors + i) : 0u;
+            }
+#pragma unroll
+            for (int f = 0; f < kFilterPPT; ++f) {
+                const uint64_t i = i0 + threadIdx.x + (uint64_t)f * blockDim.x;
+                const bool need =
+                    i < ce && prune_needs_sweep(a, i, lab[f], bd[f], col[f], smem, s_aux, Kp, ev, smax1, smax2, sarg);
+                const uint32_t m = __ballot_sync(0xffffffffu, need);
+                if (m) {
+                    const int leader = __ffs(m) - 1;
+                    uint32_t pos = 0;
+                    if ((int)(threadIdx.x & 31) == leader) pos = atomicAdd(&s_m, (uint32_t)__popc(m));
+                    pos = __shfl_sync(0xffffffffu, pos, leader);
+                    if (need) s_list[pos + __popc(m & lane_lt_mask())] = (uint32_t)i;
+                }
+            }
+        }
+        __syncthreads();
+        const uint32_t m = s_m;
+        const uint32_t mb = m / big * big;
+        if (mb) {
+            sweep_tiles<MODE_WALK, PPT, true>(a, 0, mb, s_list, smem, s_acc, tau_abs, tau_rel);
+            swept += mb;
+            __syncthreads();
+            // carry the remainder (< big entries) to the front: [mb, m) -> [0, m - mb), disjoint
+            for (uint32_t t = threadIdx.x; t < m - mb; t += blockDim.x) s_list[t] = s_list[mb + t];
+            __syncthreads();
+            if (threadIdx.x == 0) s_m = m - mb;
+        }
+        __syncthreads();
+    }
+    const uint32_t rest = s_m;
+    if (rest) sweep_tiles<MODE_WALK, 2, true>(a, 0, rest, s_list, smem, s_acc, tau_abs, tau_rel);
+    swept += rest;
+    __syncthreads();
+    if (threadIdx.x == 0 && a.swept && swept) atomicAdd(a.swept, swept);
+}
+
 // Flush the WALK-mode u64 block deltas (laid out as Moments) to the global moments.
 __device__ __forceinline__ void flush_acc64(const unsigned long long *s_acc64, Moments *mom, int K) {
     for (int e = threadIdx.x; e < K * 5; e += blockDim.x) {
@@ -412,7 +640,9 @@ __global__ void __launch_bounds__(kSweepThreads, 2) sweep_kernel(SweepArgs a) {
     const uint64_t chunk = (a.n + gridDim.x - 1) / gridDim.x;
     const uint64_t lo = (uint64_t)blockIdx.x * chunk;
     const uint64_t hi = lo + chunk < a.n ? lo + chunk : a.n;
-    sweep_range<MODE, PPT>(a, lo, hi, smem, s_acc, a.tau[0], a.tau[1]);
+    uint32_t *s_list = reinterpret_cast<uint32_t *>(s_acc) + sweep_acc_words(K);
+    float *s_aux = reinterpret_cast<float *>(s_list + kPruneChunk + kSweepThreads * 8);
+    sweep_range<MODE, PPT>(a, lo, hi, smem, s_acc, a.tau[0], a.tau[1], s_list, kPruneChunk, s_aux);
     if (MODE == MODE_WALK) {
         __syncthreads();
         flush_acc64(s_acc64, a.mom, K);
@@ -504,7 +734,7 @@ __device__ void fc_block(const double *cen, int K, int Kp, float *fc, float *tau
 __global__ void fc_kernel(const double *cen, int K, int Kp, float *fc, float *tau);
 
 
-size_t sweep_smem_bytes(int K, int Kp);
+size_t sweep_smem_bytes(int K, int Kp, int mode);
 void launch_sweep(cqg_ctx *ctx, int mode, const SweepArgs &a);
 
 } // namespace cqg

@@ -152,6 +152,7 @@ class ClusterState:
     repair_count: int = 0
     history: list = field(default_factory=list)
     flagged_total: int = 0  # device diagnostic: points replayed in exact FP64
+    swept_total: int = 0    # device diagnostic: points evaluated against every centre
 
     def ndc_per_point_iter(self, point_count: int) -> float:
         if point_count == 0 or self.iterations == 0:
@@ -204,7 +205,8 @@ def wsm_counts(colors_packed, counts, P: int, init, options: ClusterOptions = No
     if options.record_history:
         hist = [IterationSnapshot(hc[i].copy(), hl[i].copy()) for i in range(it)]
     return ClusterState(centers[:k].copy(), labels[:n].copy(), sse[:it].copy(), it,
-                        int(st.ndc_total), int(st.repair_count), hist, int(st.flagged_total))
+                        int(st.ndc_total), int(st.repair_count), hist, int(st.flagged_total),
+                        int(st.swept_total))
 
 
 def wsm(points, weights, init, options: ClusterOptions = None,
@@ -495,7 +497,7 @@ def run_quantize(image, config: QuantizeConfig, ctx: Optional[cabi.Context] = No
     it = st.lloyd.iterations
     state = ClusterState(palette.copy(), labels[:n].copy(), sse[:it].copy(), it,
                          int(st.lloyd.ndc_total), int(st.lloyd.repair_count), [],
-                         int(st.lloyd.flagged_total))
+                         int(st.lloyd.flagged_total), int(st.lloyd.swept_total))
     mapping = MappingResult(idx, q, float(st.mean_sq_dist), 0)
     rep = QuantReport(method=config.method.token(), k_requested=k, k_actual=k,
                       seed=int(config.seed), sampling=config.sampling, mse=mapping.mean_sq_dist,

@@ -1,0 +1,132 @@
+"""Distance-bound pruning of the WALK sweep.
+
+Points whose label is proven unchanged by the (ub, lb) bounds skip the centre
+loop. The bar is unchanged: labels, iterations, NDC, repairs, centres and SSE
+bit-exact against the oracle. These cases add the paths the other parity tests
+do not reach with pruning on: the CUDA-graph loop (N' above the persistent
+kernel's limit), the persistent kernel without history, repairs after pruned
+iterations, and pruned == unpruned on the same inputs.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from oracle.pyoracle import UPDATE_EXACT
+from paper_1101_0395_b200 import cabi, quant
+from paper_1101_0395_b200.synth import CONFIGS, synth_image
+
+from test_gpu_parity import assert_lloyd_equal
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx_noprune():
+    old = os.environ.get("CQG_NO_PRUNE")
+    os.environ["CQG_NO_PRUNE"] = "1"
+    try:
+        c = cabi.Context(0)
+    finally:
+        if old is None:
+            del os.environ["CQG_NO_PRUNE"]
+        else:
+            os.environ["CQG_NO_PRUNE"] = old
+    yield c
+    c.close()
+
+
+def _run(ctx, c, n, P, init, **term):
+    opts = quant.ClusterOptions(quant.Termination(**term)) if term else quant.ClusterOptions()
+    return quant.wsm_counts(c, n, P, init, opts, ctx=ctx)
+
+
+def test_prune_persistent_path(ctx, ctx_noprune, oracle):
+    # cfg2 substrate (N' = 168K): the persistent cooperative kernel, no history
+    cfg = CONFIGS["cfg2"]
+    img = cfg.image()
+    P = img.shape[0] * img.shape[1]
+    hist = quant.build_histogram(img, ctx=ctx)
+    c, n = hist.packed, hist.counts
+    init = oracle.init_kmeanspp(c, n, P, cfg.k, cfg.seed)
+    dev = _run(ctx, c, n, P, init)
+    ora = oracle.wsm(c, n, P, init, mode=UPDATE_EXACT)
+    assert_lloyd_equal(dev, ora, P)
+    dense = _run(ctx_noprune, c, n, P, init)
+    assert_lloyd_equal(dense, ora, P)
+    assert dense.swept_total == c.size * dense.iterations
+    # pruning is active: later iterations sweep a fraction of the points
+    assert dev.swept_total < 0.6 * c.size * dev.iterations
+
+
+def test_prune_graph_path(ctx, ctx_noprune, oracle):
+    # N' above the persistent limit (148*2*256*8 = 606K): sweep kernels in the CUDA graph loop
+    img = synth_image(1400, 1400, 909, nblobs=40, sigma=30.0, noise=0.5)
+    P = img.shape[0] * img.shape[1]
+    hist = quant.build_histogram(img, ctx=ctx)
+    c, n = hist.packed, hist.counts
+    assert c.size > 620_000
+    init = oracle.init_maximin(c, n, P, 64, 909)
+    dev = _run(ctx, c, n, P, init, max_iterations=25)
+    ora = oracle.wsm(c, n, P, init, max_it=25, mode=UPDATE_EXACT)
+    assert_lloyd_equal(dev, ora, P)
+    assert dev.swept_total < 0.6 * c.size * dev.iterations
+    dense = _run(ctx_noprune, c, n, P, init, max_iterations=25)
+    assert np.array_equal(dense.memberships, dev.memberships)
+    assert np.array_equal(dense.centers.view(np.uint64), dev.centers.view(np.uint64))
+
+
+def test_prune_fixed_iterations_long_run(ctx, oracle):
+    # many iterations after convergence: bounds keep tightening, labels never move
+    img = CONFIGS["cfg1"].image()
+    P = img.shape[0] * img.shape[1]
+    hist = quant.build_histogram(img, ctx=ctx)
+    c, n = hist.packed, hist.counts
+    init = oracle.init_maximin(c, n, P, 32, 101)
+    dev = _run(ctx, c, n, P, init, fixed_iterations=60)
+    ora = oracle.wsm(c, n, P, init, fixed_it=60, mode=UPDATE_EXACT)
+    assert dev.iterations == 60
+    assert_lloyd_equal(dev, ora, P)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_prune_repairs_and_small_substrates(ctx, ctx_noprune, oracle, seed):
+    # few unique colours, K close to N': empty clusters appear (also after
+    # pruned iterations); repairs must void the bounds
+    rng = np.random.default_rng(1000 + seed)
+    nu = int(rng.integers(40, 400))
+    keys = rng.choice(1 << 24, nu, replace=False).astype(np.uint32)
+    counts = rng.integers(1, 50, nu).astype(np.uint32)
+    P = int(counts.sum())
+    K = int(rng.integers(nu // 4, nu // 2 + 2))
+    pts = quant.unpack_colors(keys).astype(np.float64)
+    # clumped init: many centres start near each other -> empties
+    init = pts[rng.integers(0, 6, K)] + rng.normal(0, 0.5, (K, 3))
+    dev = _run(ctx, keys, counts, P, init, max_iterations=40)
+    ora = oracle.wsm(keys, counts, P, init, max_it=40, mode=UPDATE_EXACT)
+    assert_lloyd_equal(dev, ora, P)
+    dense = _run(ctx_noprune, keys, counts, P, init, max_iterations=40)
+    assert_lloyd_equal(dense, ora, P)
+
+
+@pytest.mark.parametrize("history", [True, False])
+def test_ndc_code_table_exact_ties(ctx, oracle, history):
+    # Integer centres 6 apart on the red axis; each cluster = its centre plus
+    # c +- 3 on green / blue, so the means stay integer. From iteration 2 the
+    # NDC cutoff 4*pd = 36 equals the neighbour distance D = 36 exactly: the
+    # 16-bit code of the cutoff ties with the row entry and the FP64 value decides.
+    cen = np.array([[20 + 6 * i, 128, 128] for i in range(36)], np.int64)
+    pts = []
+    for c in cen:
+        pts.append(c)
+        for off in ([0, 3, 0], [0, -3, 0], [0, 0, 3], [0, 0, -3]):
+            pts.append(c + np.array(off))
+    pts = np.array(pts, np.uint8)
+    keys = quant.pack_colors(pts)
+    counts = np.ones(keys.size, np.uint32)
+    P = keys.size
+    init = cen.astype(np.float64) + 0.25
+    opts = quant.ClusterOptions(quant.Termination(fixed_iterations=4), record_history=history)
+    dev = quant.wsm_counts(keys, counts, P, init, opts, ctx=ctx)
+    ora = oracle.wsm(keys, counts, P, init, fixed_it=4, mode=UPDATE_EXACT, history=history)
+    assert_lloyd_equal(dev, ora, P)
