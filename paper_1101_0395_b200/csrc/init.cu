@@ -85,11 +85,14 @@ __device__ __forceinline__ u128 floor_fixed(double u) {
 
 __device__ __forceinline__ double fixed_to_double(u128 x) { return scalbn(u128_to_double(x), -kFix); }
 
+// exact squared distance of two packed 0x00RRGGBB colours with byte dot
+// products: |a-b|^2 = a.a + b.b - 2 a.b (IDP4A x2 + IMAD, all < 2^18)
 __device__ __forceinline__ uint32_t d2_int(uint32_t a, uint32_t b) {
-    const int dr = (int)((a >> 16) & 255u) - (int)((b >> 16) & 255u);
-    const int dg = (int)((a >> 8) & 255u) - (int)((b >> 8) & 255u);
-    const int db = (int)(a & 255u) - (int)(b & 255u);
-    return (uint32_t)(dr * dr + dg * dg + db * db);
+    return __dp4a(a, a, __dp4a(b, b, 0u)) - 2u * __dp4a(a, b, 0u);
+}
+// same with the centre's b.b precomputed
+__device__ __forceinline__ uint32_t d2_int_bb(uint32_t a, uint32_t b, uint32_t bb) {
+    return __dp4a(a, a, bb) - 2u * __dp4a(a, b, 0u);
 }
 
 // the reference's mass: weights[i] (* mind2[i])
@@ -549,6 +552,25 @@ __global__ void __launch_bounds__(kInitThreads) init_kernel(InitArgs a) {
 // target thread's <= 32 point masses). The arithmetic and the exactness
 // argument are the cooperative kernel's (ExactMass / FixedMass).
 constexpr int kClusterThreads = 1024;
+constexpr int kMaxClusterCtas = 16;
+
+// Phase timing of the cluster initialiser (tools/init_timing.py builds with
+// -DCQG_INIT_TIMING): clock64 deltas of CTA 0 / thread 0, summed over rounds.
+#ifdef CQG_INIT_TIMING
+__device__ unsigned long long g_init_timing[8];
+#define ITIME(slot)                                                                  \
+    do {                                                                             \
+        if (crank == 0 && t == 0) {                                                  \
+            const unsigned long long _n = clock64();                                 \
+            g_init_timing[slot] += _n - _tprev;                                      \
+            _tprev = _n;                                                             \
+        }                                                                            \
+    } while (0)
+#else
+#define ITIME(slot) \
+    do {            \
+    } while (0)
+#endif
 
 template <class M>
 __device__ uint64_t cluster_sequential_draw(const InitArgs &a, cg::cluster_group &cl, const uint32_t *s_cnt,
@@ -605,25 +627,35 @@ __global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_kernel(InitAr
     T *s_tsum = reinterpret_cast<T *>(sm_raw);                 // 2 x 1024
     T *s_wsum = s_tsum + 2 * kClusterThreads;                  // 2 x 32
     T *s_csum = s_wsum + 2 * 32;                               // 2
-    unsigned long long *s_key = reinterpret_cast<unsigned long long *>(s_csum + 2); // 2 (maximin)
+    // every rank's CTA sums and warp sums, pushed here by their owners before
+    // the cluster barrier: the first two locate levels read local memory
+    T *s_allc = s_csum + 2;                                    // 2 x kMaxClusterCtas
+    T *s_allw = s_allc + 2 * kMaxClusterCtas;                  // 2 x kMaxClusterCtas x 32
+    unsigned long long *s_key = reinterpret_cast<unsigned long long *>(s_allw + 2 * kMaxClusterCtas * 32); // 2
     __shared__ unsigned long long s_wkey[32];
     uint32_t *s_col = reinterpret_cast<uint32_t *>(s_key + 2);
     uint32_t *s_cnt = s_col + chunk;
     uint32_t *s_md = s_cnt + chunk;                            // 2 x chunk
     __shared__ unsigned long long s_pick;
     __shared__ int s_amb;
-    for (int i = t; i < mine; i += kClusterThreads) {
-        s_col[i] = __ldg(a.colors + lo + i);
-        s_cnt[i] = __ldg(a.counts + lo + i);
+    for (int i = t; i < (int)chunk; i += kClusterThreads) { // padding: colour 0, count 0 (mass 0)
+        s_col[i] = i < mine ? __ldg(a.colors + lo + i) : 0u;
+        s_cnt[i] = i < mine ? __ldg(a.counts + lo + i) : 0u;
     }
     __syncthreads();
+    // ppt is a multiple of 4: each thread's run is 16-byte aligned (128-bit shared loads)
     const int p0 = t * ppt, p1 = min(p0 + ppt, mine);
+    __shared__ uint32_t s_pickcol;
+
+    auto colour_of = [&](uint64_t gi) -> uint32_t {
+        return *cl.map_shared_rank(s_col + (gi % chunk), (unsigned)(gi / chunk));
+    };
 
     // one weighted draw over the masses of buffer `par` (md = nullptr: weights only)
     auto draw = [&](int par, double nu, const uint32_t *mdb) -> uint64_t {
         // CTA sums of all ranks, then the target rank's warp and thread sums
         if (warp == 0) {
-            const T cv = lane < C ? *cl.map_shared_rank(s_csum + par, lane) : (T)0;
+            const T cv = lane < C ? s_allc[par * kMaxClusterCtas + lane] : (T)0;
             T before, total;
             const T U = M::target(nu, M::shfl(warp_incl<M>(cv), 31));
             const int tc = lane_locate<M>(cv, U, &before, &total);
@@ -633,7 +665,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_kernel(InitAr
             bool found = false;
             if (tc < C) {
                 T b2, t2;
-                const T wv = *cl.map_shared_rank(s_wsum + par * 32 + lane, tc);
+                const T wv = s_allw[(par * kMaxClusterCtas + tc) * 32 + lane];
                 const int tw = lane_locate<M>(wv, U - before, &b2, &t2);
                 T b3, t3;
                 const T tv = *cl.map_shared_rank(s_tsum + par * kClusterThreads + tw * 32 + lane, tc);
@@ -644,18 +676,22 @@ __global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_kernel(InitAr
                 const uint64_t mine_tc = a.n - tlo < chunk ? a.n - tlo : chunk;
                 const int nq = (uint64_t)q0 >= mine_tc ? 0 : (int)min((uint64_t)ppt, mine_tc - (uint64_t)q0);
                 T mv = 0;
+                uint32_t cv32 = 0;
                 if (lane < nq) {
                     const uint32_t cnt = *cl.map_shared_rank(s_cnt + q0 + lane, tc);
                     const uint32_t md = mdb ? *cl.map_shared_rank(mdb + q0 + lane, tc) : kWeightsOnly;
+                    cv32 = *cl.map_shared_rank(s_col + q0 + lane, tc); // the pick's colour, same round trip
                     mv = M::mass_c(a, cnt, md);
                 }
                 T b4, t4;
                 const int tl = lane_locate<M>(mv, U - before - b2 - b3, &b4, &t4);
+                const uint32_t pc = __shfl_sync(0xffffffffu, cv32, tl & 31);
                 if (tl < nq) {
                     idx = tlo + q0 + tl;
                     prevE = before + b2 + b3 + b4;
                     E = prevE + M::shfl(mv, tl);
                     found = true;
+                    if (lane == 0) s_pickcol = pc;
                 }
             }
             if (!found || idx >= a.n - 1) {
@@ -673,6 +709,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_kernel(InitAr
             if (lane == 0) {
                 s_pick = idx;
                 s_amb = amb ? 1 : 0;
+                if (!found || idx == a.n - 1) s_pickcol = colour_of(idx);
             }
         }
         __syncthreads();
@@ -684,7 +721,10 @@ __global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_kernel(InitAr
             cl.sync();
             const unsigned long long v = *cl.map_shared_rank(&s_pick, 0);
             __syncthreads();
-            if (t == 0) s_pick = v;
+            if (t == 0) {
+                s_pick = v;
+                s_pickcol = colour_of(v);
+            }
             __syncthreads();
         }
         return s_pick;
@@ -697,15 +737,16 @@ __global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_kernel(InitAr
         if (lane == 0) s_wsum[par * 32 + warp] = w;
         __syncthreads();
         if (warp == 0) {
-            T c = s_wsum[par * 32 + lane];
+            const T wv = s_wsum[par * 32 + lane];
+            T c = wv;
             for (int o = 16; o; o >>= 1) c += M::shfl(c, lane ^ o);
-            if (lane == 0) s_csum[par] = c;
+            // push this CTA's warp sums and CTA sum into every rank (the
+            // cluster barrier's release/acquire publishes them)
+            for (int r = 0; r < C; ++r) *cl.map_shared_rank(s_allw + (par * kMaxClusterCtas + crank) * 32 + lane, r) = wv;
+            if (lane < C) *cl.map_shared_rank(s_allc + par * kMaxClusterCtas + crank, lane) = c;
         }
     };
 
-    auto colour_of = [&](uint64_t gi) -> uint32_t {
-        return *cl.map_shared_rank(s_col + (gi % chunk), (unsigned)(gi / chunk));
-    };
 
     int par = 0;
     uint64_t first;
@@ -718,21 +759,27 @@ __global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_kernel(InitAr
         par ^= 1;
     } else {
         first = a.first_index;
+        if (t == 0) s_pickcol = colour_of(first);
+        __syncthreads();
     }
-    uint32_t clast = colour_of(first);
+    uint32_t clast = s_pickcol;
     if (crank == 0 && t == 0) {
         a.cen[0] = (double)((clast >> 16) & 255u);
         a.cen[1] = (double)((clast >> 8) & 255u);
         a.cen[2] = (double)(clast & 255u);
     }
+#ifdef CQG_INIT_TIMING
+    unsigned long long _tprev = clock64();
+#endif
     for (int k = 1; k < a.K; ++k) {
         const uint32_t *md_in = s_md + (size_t)((k - 1) & 1) * chunk;
         uint32_t *md_out = s_md + (size_t)(k & 1) * chunk;
         uint64_t pick;
+        const uint32_t bb = __dp4a(clast, clast, 0u);
         if (a.kind == 0) {
             unsigned long long best = 0;
             for (int i = p0; i < p1; ++i) {
-                const uint32_t d = d2_int(s_col[i], clast);
+                const uint32_t d = d2_int_bb(s_col[i], clast, bb);
                 const uint32_t m = k == 1 ? d : min(md_in[i], d);
                 md_out[i] = m;
                 const unsigned long long key = ((unsigned long long)m << 32) | (uint32_t)~(uint32_t)(lo + i);
@@ -764,32 +811,52 @@ __global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_kernel(InitAr
             __syncthreads();
             pick = s_pick;
         } else {
+            const double nu_k = __ldg(a.nu + k); // off the locate's critical path
+            // whole 4-point runs (padding has count 0: mass 0)
             T ts = 0;
-            for (int i = p0; i < p1; ++i) {
-                const uint32_t d = d2_int(s_col[i], clast);
-                const uint32_t m = k == 1 ? d : min(md_in[i], d);
-                md_out[i] = m;
-                ts += M::mass_c(a, s_cnt[i], m);
+            for (int i = p0; i < p0 + ppt; i += 4) {
+                const uint4 c4 = *reinterpret_cast<const uint4 *>(s_col + i);
+                const uint4 n4 = *reinterpret_cast<const uint4 *>(s_cnt + i);
+                uint4 m4;
+                m4.x = d2_int_bb(c4.x, clast, bb);
+                m4.y = d2_int_bb(c4.y, clast, bb);
+                m4.z = d2_int_bb(c4.z, clast, bb);
+                m4.w = d2_int_bb(c4.w, clast, bb);
+                if (k > 1) {
+                    const uint4 i4 = *reinterpret_cast<const uint4 *>(md_in + i);
+                    m4.x = min(m4.x, i4.x);
+                    m4.y = min(m4.y, i4.y);
+                    m4.z = min(m4.z, i4.z);
+                    m4.w = min(m4.w, i4.w);
+                }
+                *reinterpret_cast<uint4 *>(md_out + i) = m4;
+                ts += M::mass_c(a, n4.x, m4.x) + M::mass_c(a, n4.y, m4.y) + M::mass_c(a, n4.z, m4.z) +
+                      M::mass_c(a, n4.w, m4.w);
             }
+            ITIME(0);
             publish(par, ts);
+            ITIME(1);
             cl.sync();
-            pick = draw(par, a.nu[k], md_out);
+            ITIME(2);
+            pick = draw(par, nu_k, md_out);
+            ITIME(3);
         }
         par ^= 1;
-        clast = colour_of(pick);
+        clast = a.kind == 0 ? colour_of(pick) : s_pickcol;
         if (crank == 0 && t == 0) {
             a.cen[3 * k] = (double)((clast >> 16) & 255u);
             a.cen[3 * k + 1] = (double)((clast >> 8) & 255u);
             a.cen[3 * k + 2] = (double)(clast & 255u);
         }
         __syncthreads();
+        ITIME(4);
     }
     cl.sync(); // no CTA may exit while others still read its shared memory
 }
 
 template <class M>
 static size_t cluster_smem(int ppt) {
-    return sizeof(typename M::T) * (2 * kClusterThreads + 64 + 2) + 16 +
+    return sizeof(typename M::T) * (2 * kClusterThreads + 64 + 2 + 2 * kMaxClusterCtas * 33) + 16 +
            (size_t)kClusterThreads * ppt * 4 * sizeof(uint32_t);
 }
 
@@ -798,7 +865,7 @@ template <class M>
 static bool launch_cluster_init(cqg_ctx *ctx, InitArgs a) {
     constexpr int C = 16;
     const uint64_t per = (a.n + C - 1) / C;
-    const int ppt = (int)((per + kClusterThreads - 1) / kClusterThreads);
+    const int ppt = ((int)((per + kClusterThreads - 1) / kClusterThreads) + 3) & ~3; // 128-bit runs
     if (ppt < 1 || ppt > 32) return false;
     const size_t smem = cluster_smem<M>(ppt);
     if (smem > 227 * 1024) return false;
@@ -933,3 +1000,14 @@ void init_kmeanspp_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *c
 }
 
 } // namespace cqg
+
+#ifdef CQG_INIT_TIMING
+extern "C" int cqg_dbg_init_timing(unsigned long long *out, int reset) {
+    if (cudaMemcpyFromSymbol(out, cqg::g_init_timing, 8 * sizeof(unsigned long long)) != cudaSuccess) return 1;
+    if (reset) {
+        unsigned long long z[8] = {};
+        cudaMemcpyToSymbol(cqg::g_init_timing, z, sizeof(z));
+    }
+    return 0;
+}
+#endif

@@ -1,0 +1,63 @@
+"""Phase timing of the cluster k-means++ initialiser (design tool, GPU).
+
+Builds a variant of libcqg.so with -DCQG_INIT_TIMING into
+paper_1101_0395_b200/build_timing/, runs the init stage of a config and prints
+the mean cycles per round of: update, publish, cluster barrier, draw, tail.
+
+    python tools/init_timing.py [cfg2]      # build here, run on the GPU box
+"""
+import ctypes as C
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_1101_0395_b200 import _build  # noqa: E402
+
+TLIB = os.path.join(_build.PKG, "libcqg_timing.so")
+
+
+def build():
+    bdir = os.path.join(_build.PKG, "build_timing")
+    os.makedirs(bdir, exist_ok=True)
+    objs = []
+    for src in _build.SOURCES:
+        o = os.path.join(bdir, src.replace(".cu", ".o"))
+        subprocess.check_call([_build.nvcc(), *_build.flags(["-DCQG_INIT_TIMING"]), "-c",
+                               os.path.join(_build.CSRC, src), "-o", o])
+        objs.append(o)
+    subprocess.check_call([_build.nvcc(), *_build.ARCH, "-shared", "--cudart", "static", "-o", TLIB, *objs])
+
+
+def run(name):
+    from paper_1101_0395_b200 import cabi, quant
+    from paper_1101_0395_b200.synth import CONFIGS
+    cabi.load(TLIB)  # the timing variant becomes the process's libcqg
+    cfg = CONFIGS[name]
+    img = cfg.image()
+    ctx = cabi.Context(0)
+    hist = quant.build_histogram(img, ctx=ctx)
+    sc = quant.SeedConfig(k=cfg.k, seed=cfg.seed)
+    initf = quant.init_kmeanspp if cfg.init == "kpp" else quant.init_maximin
+    L = C.CDLL(TLIB)
+    buf = (C.c_ulonglong * 8)()
+    initf(hist, sc, ctx=ctx)
+    L.cqg_dbg_init_timing(buf, 1)
+    reps = 5
+    for _ in range(reps):
+        initf(hist, sc, ctx=ctx)
+    L.cqg_dbg_init_timing(buf, 1)
+    rounds = reps * (cfg.k - 1)
+    names = ["update", "publish", "cluster_sync", "draw", "tail"]
+    tot = sum(buf[i] for i in range(5))
+    for i, nm in enumerate(names):
+        print(f"{nm:14s} {buf[i] / rounds:8.0f} cycles/round  {100 * buf[i] / tot:5.1f}%")
+    print(f"{'total':14s} {tot / rounds:8.0f} cycles/round")
+
+
+if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "build":
+        build()
+    else:
+        run(sys.argv[1] if len(sys.argv) > 1 else "cfg2")
