@@ -231,7 +231,8 @@ void cqg_destroy(cqg_ctx *ctx) {
                       &ctx->dtab, &ctx->dsorted, &ctx->order, &ctx->mom, &ctx->queue, &ctx->ndc,
                       &ctx->status, &ctx->sizes, &ctx->red, &ctx->hist_labels, &ctx->hist_centers,
                       &ctx->sse, &ctx->lut, &ctx->idx_out, &ctx->q_out, &ctx->mom_map, &ctx->mind2,
-                      &ctx->initpart, &ctx->initsel, &ctx->unit_draws, &ctx->mom_g, &ctx->partial};
+                      &ctx->initpart, &ctx->initsel, &ctx->unit_draws, &ctx->mom_g, &ctx->partial,
+                      &ctx->bnd, &ctx->shift, &ctx->dcode};
     for (DevBuf *b : bufs) b->release();
     ctx->pinned.release();
     for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);

@@ -5,18 +5,23 @@
 // sight, so its output order is "by first pixel index". Here:
 //
 //   A  hist_count   per pixel (16 pixels / thread, 3 x 128-bit loads):
-//                   atomicAdd(tab[c].count) with return -> the lane that sees 0
+//                   atomicAdd(count[c]) with return -> the lane that sees 0
 //                   appends c to an (unordered) list (warp-aggregated append);
-//                   atomicMax(tab[c].neg_first, ~p) keeps the minimum index.
+//                   atomicMax(~first[c], ~p) keeps the minimum index.
+//                   Small images: both in one pass over an interleaved
+//                   {count, ~first} table. Large images (P >= 2^22): two passes
+//                   (hist_count, hist_first) over split 64 MiB tables, so each
+//                   pass's table stays in the 126 MB L2.
 //   B  hist_mark    per listed colour: set bit first(c) in a P-bit bitmap.
 //   C  scan         popcount prefix over the bitmap words (2 small kernels).
-//   D  hist_emit    per listed colour: rank = prefix(first(c)) -> write
-//                   (colour, count, first) at that rank, i.e. in first-occurrence
-//                   order; reset tab[c] to zero so the 2^24 table stays clean
-//                   without a 128 MiB memset per call.
+//   D  emit         small: per listed colour, rank = prefix(first(c)), write at
+//                   that rank and zero the table entry. Large: one thread per
+//                   pixel in pixel order -- a set bit is a first occurrence with
+//                   rank = word prefix + bits below, so stores are sequential;
+//                   the tables are reset with one 128 MiB memset.
 //
-// The table (2^24 x {count, ~first}) is 128 MiB and lives in the context; it
-// is zero between calls. HBM bound: 3P bytes read + 8N' written + atomics.
+// The tables (2^24 counts | 2^24 ~first) are 128 MiB and live in the context;
+// they are zero between calls. HBM bound: 6P bytes read + 8N' written + atomics.
 #include "cqg_internal.cuh"
 
 namespace cqg {
@@ -40,11 +45,17 @@ __device__ __forceinline__ uint4 ld_stream(const uint4 *p) {
     return v;
 }
 
-// Count one pixel; returns true if this lane saw the colour first.
-__device__ __forceinline__ bool count_pixel(uint2 *tab, uint32_t c, uint32_t p) {
-    const uint32_t old = atomicAdd(&tab[c].x, 1u);
-    atomicMax(&tab[c].y, ~p);
-    return old == 0;
+// Decode 16 packed RGB pixels from 48 bytes (little-endian words).
+__device__ __forceinline__ void decode16(const uint4 &a, const uint4 &b, const uint4 &d, uint32_t *col) {
+    const uint32_t w[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, d.x, d.y, d.z, d.w};
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        const int o = 3 * j;
+        const uint32_t b0 = (w[o >> 2] >> (8 * (o & 3))) & 255u;
+        const uint32_t b1 = (w[(o + 1) >> 2] >> (8 * ((o + 1) & 3))) & 255u;
+        const uint32_t b2 = (w[(o + 2) >> 2] >> (8 * ((o + 2) & 3))) & 255u;
+        col[j] = (b0 << 16) | (b1 << 8) | b2;
+    }
 }
 
 __device__ __forceinline__ void append(bool isnew, uint32_t c, uint32_t *list, uint32_t *list_n) {
@@ -58,47 +69,136 @@ __device__ __forceinline__ void append(bool isnew, uint32_t c, uint32_t *list, u
     if (isnew) list[base + __popc(m & lanemask_lt())] = c;
 }
 
-__global__ void __launch_bounds__(kThreads) hist_count(const uint8_t *__restrict__ rgb, uint64_t P,
-                                                      uint2 *__restrict__ tab,
-                                                      uint32_t *__restrict__ list,
-                                                      uint32_t *__restrict__ list_n, int aligned) {
+// ---- small images: one interleaved table {count, ~first} (one sector per colour)
+
+__global__ void __launch_bounds__(kThreads) hist_count_fused(const uint8_t *__restrict__ rgb, uint64_t P,
+                                                            uint2 *__restrict__ tab, uint32_t *__restrict__ list,
+                                                            uint32_t *__restrict__ list_n, int aligned) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const uint64_t groups = aligned ? P / 16 : 0;
     for (uint64_t g = tid; g < groups; g += stride) {
         const uint4 *src = reinterpret_cast<const uint4 *>(rgb + g * 48);
-        const uint4 a = ld_stream(src), b = ld_stream(src + 1), d = ld_stream(src + 2);
-        const uint32_t w[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, d.x, d.y, d.z, d.w};
         uint32_t col[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            // bytes 3j, 3j+1, 3j+2 of the 48-byte group (little endian)
-            const int o = 3 * j;
-            const uint32_t b0 = (w[o >> 2] >> (8 * (o & 3))) & 255u;
-            const uint32_t b1 = (w[(o + 1) >> 2] >> (8 * ((o + 1) & 3))) & 255u;
-            const uint32_t b2 = (w[(o + 2) >> 2] >> (8 * ((o + 2) & 3))) & 255u;
-            col[j] = (b0 << 16) | (b1 << 8) | b2;
-        }
+        decode16(ld_stream(src), ld_stream(src + 1), ld_stream(src + 2), col);
         bool isnew[16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) isnew[j] = count_pixel(tab, col[j], (uint32_t)(g * 16 + j));
+        for (int j = 0; j < 16; ++j) {
+            isnew[j] = atomicAdd(&tab[col[j]].x, 1u) == 0;
+            atomicMax(&tab[col[j]].y, ~(uint32_t)(g * 16 + j));
+        }
 #pragma unroll
         for (int j = 0; j < 16; ++j) append(isnew[j], col[j], list, list_n);
     }
     // tail (or everything when the input is not 16-byte aligned)
     for (uint64_t p = groups * 16 + tid; p < P; p += stride) {
         const uint32_t c = ((uint32_t)rgb[3 * p] << 16) | ((uint32_t)rgb[3 * p + 1] << 8) | rgb[3 * p + 2];
-        const bool isnew = count_pixel(tab, c, (uint32_t)p);
+        const bool isnew = atomicAdd(&tab[c].x, 1u) == 0;
+        atomicMax(&tab[c].y, ~(uint32_t)p);
         append(isnew, c, list, list_n);
     }
 }
 
-__global__ void hist_mark(const uint32_t *__restrict__ list, const uint32_t *__restrict__ list_n,
-                          const uint2 *__restrict__ tab, uint32_t *__restrict__ bitmap) {
+__global__ void hist_mark_fused(const uint32_t *__restrict__ list, const uint32_t *__restrict__ list_n,
+                                const uint2 *__restrict__ tab, uint32_t *__restrict__ bitmap) {
     const uint32_t n = *list_n;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const uint32_t f = ~tab[list[i]].y;
         atomicOr(&bitmap[f >> 5], 1u << (f & 31));
+    }
+}
+
+// per listed colour: rank = prefix(first(c)); write at that rank, reset tab[c]
+__global__ void hist_emit_fused(const uint32_t *__restrict__ list, const uint32_t *__restrict__ list_n,
+                                uint2 *__restrict__ tab, const uint32_t *__restrict__ bitmap,
+                                const uint32_t *__restrict__ wpref, uint32_t *__restrict__ colors,
+                                uint32_t *__restrict__ counts, uint32_t *__restrict__ first) {
+    const uint32_t n = *list_n;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t c = list[i];
+        const uint2 t = tab[c];
+        const uint32_t f = ~t.y;
+        const uint32_t w = f >> 5;
+        const uint32_t rank = wpref[w] + __popc(bitmap[w] & ((1u << (f & 31)) - 1u));
+        colors[rank] = c;
+        counts[rank] = t.x;
+        if (first) first[rank] = f;
+        tab[c] = make_uint2(0u, 0u);
+    }
+}
+
+// ---- large images: split tables cnt | negf (64 MiB each), two passes
+
+__global__ void __launch_bounds__(kThreads) hist_count(const uint8_t *__restrict__ rgb, uint64_t P,
+                                                      uint32_t *__restrict__ cnt, uint32_t *__restrict__ list,
+                                                      uint32_t *__restrict__ list_n, int aligned) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t groups = aligned ? P / 16 : 0;
+    for (uint64_t g = tid; g < groups; g += stride) {
+        const uint4 *src = reinterpret_cast<const uint4 *>(rgb + g * 48);
+        uint32_t col[16];
+        decode16(ld_stream(src), ld_stream(src + 1), ld_stream(src + 2), col);
+        bool isnew[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) isnew[j] = atomicAdd(cnt + col[j], 1u) == 0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) append(isnew[j], col[j], list, list_n);
+    }
+    for (uint64_t p = groups * 16 + tid; p < P; p += stride) {
+        const uint32_t c = ((uint32_t)rgb[3 * p] << 16) | ((uint32_t)rgb[3 * p + 1] << 8) | rgb[3 * p + 2];
+        const bool isnew = atomicAdd(cnt + c, 1u) == 0;
+        append(isnew, c, list, list_n);
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) hist_first(const uint8_t *__restrict__ rgb, uint64_t P,
+                                                      uint32_t *__restrict__ negf, int aligned) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t groups = aligned ? P / 16 : 0;
+    for (uint64_t g = tid; g < groups; g += stride) {
+        const uint4 *src = reinterpret_cast<const uint4 *>(rgb + g * 48);
+        uint32_t col[16];
+        decode16(ld_stream(src), ld_stream(src + 1), ld_stream(src + 2), col);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) atomicMax(negf + col[j], ~(uint32_t)(g * 16 + j));
+    }
+    for (uint64_t p = groups * 16 + tid; p < P; p += stride) {
+        const uint32_t c = ((uint32_t)rgb[3 * p] << 16) | ((uint32_t)rgb[3 * p + 1] << 8) | rgb[3 * p + 2];
+        atomicMax(negf + c, ~(uint32_t)p);
+    }
+}
+
+__global__ void hist_mark(const uint32_t *__restrict__ list, const uint32_t *__restrict__ list_n,
+                          const uint32_t *__restrict__ negf, uint32_t *__restrict__ bitmap) {
+    const uint32_t n = *list_n;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t f = ~negf[list[i]];
+        atomicOr(&bitmap[f >> 5], 1u << (f & 31));
+    }
+}
+
+// one thread per pixel, in pixel order: a set bit is a first occurrence whose
+// rank is the word prefix plus the set bits below it, so the stores of a warp
+// land on consecutive ranks (the colour comes from the image itself)
+__global__ void __launch_bounds__(kThreads) hist_emit(const uint8_t *__restrict__ rgb, uint64_t P,
+                                                     const uint32_t *__restrict__ bitmap,
+                                                     const uint32_t *__restrict__ wpref,
+                                                     const uint32_t *__restrict__ cnt,
+                                                     uint32_t *__restrict__ colors, uint32_t *__restrict__ counts,
+                                                     uint32_t *__restrict__ first) {
+    for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < P;
+         p += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t w = p >> 5;
+        const uint32_t bits = __ldg(bitmap + w);
+        const uint32_t b = (uint32_t)(p & 31);
+        if (!((bits >> b) & 1u)) continue;
+        const uint32_t rank = __ldg(wpref + w) + __popc(bits & ((1u << b) - 1u));
+        const uint32_t c = ((uint32_t)rgb[3 * p] << 16) | ((uint32_t)rgb[3 * p + 1] << 8) | rgb[3 * p + 2];
+        colors[rank] = c;
+        counts[rank] = __ldg(cnt + c);
+        if (first) first[rank] = (uint32_t)p;
     }
 }
 
@@ -177,24 +277,6 @@ __global__ void __launch_bounds__(kThreads) scan_words(const uint32_t *__restric
     }
 }
 
-__global__ void hist_emit(const uint32_t *__restrict__ list, const uint32_t *__restrict__ list_n,
-                          uint2 *__restrict__ tab, const uint32_t *__restrict__ bitmap,
-                          const uint32_t *__restrict__ wpref, uint32_t *__restrict__ colors,
-                          uint32_t *__restrict__ counts, uint32_t *__restrict__ first) {
-    const uint32_t n = *list_n;
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const uint32_t c = list[i];
-        const uint2 t = tab[c];
-        const uint32_t f = ~t.y;
-        const uint32_t w = f >> 5;
-        const uint32_t rank = wpref[w] + __popc(bitmap[w] & ((1u << (f & 31)) - 1u));
-        colors[rank] = c;
-        counts[rank] = t.x;
-        if (first) first[rank] = f;
-        tab[c] = make_uint2(0u, 0u);
-    }
-}
-
 } // namespace
 
 void histogram_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P, uint32_t *colors_d,
@@ -222,18 +304,35 @@ void histogram_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P, uint32_t *col
     const unsigned gmax = (unsigned)ctx->num_sms * 8;
     if (grid > gmax) grid = gmax;
     if (grid == 0) grid = 1;
-    hist_count<<<grid, kThreads, 0, s>>>(rgb_d, P, ctx->tab.as<uint2>(), list, n_dev, aligned);
     unsigned lgrid = ceil_div(cap, kThreads);
     if (lgrid > gmax) lgrid = gmax;
-    hist_mark<<<lgrid, kThreads, 0, s>>>(list, n_dev, ctx->tab.as<uint2>(), bitmap);
+    // small images: one pass over the interleaved table (L2-resident anyway),
+    // emit + reset per listed colour. Large images: two passes over split
+    // 64 MiB tables (each fits the L2), emit in pixel order, one memset reset.
+    const bool large = P >= (1ull << 22);
+    uint2 *tab = ctx->tab.as<uint2>();
+    uint32_t *cnt = ctx->tab.as<uint32_t>(), *negf = cnt + (1u << 24);
+    if (!large) {
+        hist_count_fused<<<grid, kThreads, 0, s>>>(rgb_d, P, tab, list, n_dev, aligned);
+        hist_mark_fused<<<lgrid, kThreads, 0, s>>>(list, n_dev, tab, bitmap);
+    } else {
+        hist_count<<<grid, kThreads, 0, s>>>(rgb_d, P, cnt, list, n_dev, aligned);
+        hist_first<<<grid, kThreads, 0, s>>>(rgb_d, P, negf, aligned);
+        hist_mark<<<lgrid, kThreads, 0, s>>>(list, n_dev, negf, bitmap);
+    }
     scan_blocksum<<<nblk, kThreads, 0, s>>>(bitmap, words, bsum);
     scan_blocks<<<1, 1024, 0, s>>>(bsum, nblk);
     scan_words<<<nblk, kThreads, 0, s>>>(bitmap, words, bsum, wpref);
-    hist_emit<<<lgrid, kThreads, 0, s>>>(list, n_dev, ctx->tab.as<uint2>(), bitmap, wpref, colors_d,
-                                         counts_d, first_d);
+    if (!large) {
+        hist_emit_fused<<<lgrid, kThreads, 0, s>>>(list, n_dev, tab, bitmap, wpref, colors_d, counts_d, first_d);
+    } else {
+        const unsigned egrid = (unsigned)ctx->num_sms * 8;
+        hist_emit<<<egrid, kThreads, 0, s>>>(rgb_d, P, bitmap, wpref, cnt, colors_d, counts_d, first_d);
+        CQG_CUDA(cudaMemsetAsync(ctx->tab.p, 0, sizeof(uint2) << 24, s));
+    }
     prof_end(ctx, CQG_PROF_HIST, pb, 3.0 * (double)P); // + 8 N' added by the caller
     CQG_CUDA(cudaGetLastError());
-    launched(ctx, 6);
+    launched(ctx, large ? 7 : 6);
 }
 
 } // namespace cqg

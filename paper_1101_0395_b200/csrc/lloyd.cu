@@ -290,6 +290,22 @@ __global__ void __launch_bounds__(1024) iter_end_kernel(IterArgs a) {
 // iterations, two grid barriers per iteration (sweep + block-local replay |
 // finalise + walk table). Every block keeps its own FP32 centre table in shared memory.
 // Exits early (state 2) on an empty cluster; the host repairs and relaunches.
+#ifdef CQG_INIT_TIMING
+__device__ unsigned long long g_lloyd_timing[8];
+#define PTIME(slot)                                                                  \
+    do {                                                                             \
+        if (blockIdx.x == 0 && threadIdx.x == 0) {                                   \
+            const unsigned long long _n = clock64();                                 \
+            g_lloyd_timing[slot] += _n - _tprev;                                     \
+            _tprev = _n;                                                             \
+        }                                                                            \
+    } while (0)
+#else
+#define PTIME(slot) \
+    do {            \
+    } while (0)
+#endif
+
 template <int PPT>
 __global__ void __launch_bounds__(kSweepThreads, 2) lloyd_persistent_kernel(SweepArgs a, IterArgs ia, int first_full,
                                                                             uint32_t list_cap) {
@@ -312,6 +328,9 @@ __global__ void __launch_bounds__(kSweepThreads, 2) lloyd_persistent_kernel(Swee
     la.queue = a.queue + lo;
     la.qn = &s_qn;
     bool full = first_full != 0;
+#ifdef CQG_INIT_TIMING
+    unsigned long long _tprev = clock64();
+#endif
     for (;;) {
         // phase A: NDC, sweep and the exact replay of this block's own queued
         // points (block-local queue in slots [lo, hi), counter in shared memory)
@@ -329,16 +348,22 @@ __global__ void __launch_bounds__(kSweepThreads, 2) lloyd_persistent_kernel(Swee
             if ((threadIdx.x & 31) == 0 && nd) atomicAdd(a.ndc, nd);
             for (int i = threadIdx.x; i < K * 5; i += blockDim.x) s_acc64[i] = 0;
             __syncthreads();
+            PTIME(0);
             sweep_range<MODE_WALK, PPT>(la, lo, hi, s_fc, s_acc, s_tau[0], s_tau[1], s_list, list_cap,
                                         reinterpret_cast<float *>(s_list + list_cap + kSweepThreads * 4));
             __syncthreads();
+            PTIME(1);
             flush_acc64(s_acc64, a.mom, K);
             replay_range<MODE_WALK>(la, warp, nw);
+            PTIME(2);
         }
         if (threadIdx.x == 0 && s_qn) atomicAdd(a.qn, s_qn);
         grid.sync();
+        PTIME(3);
         const bool ok = iter_end_body(ia, s_end, s_fc, s_tau, true);
+        PTIME(4);
         grid.sync();
+        PTIME(5);
         if (!ok) break;
         if (*reinterpret_cast<volatile int *>(&ia.st->state) != 0) break;
         full = false;
@@ -1138,3 +1163,14 @@ int shard_end_dev(cqg_ctx *ctx, double *centers_user, uint32_t *labels_user, dou
 }
 
 } // namespace cqg
+
+#ifdef CQG_INIT_TIMING
+extern "C" int cqg_dbg_lloyd_timing(unsigned long long *out, int reset) {
+    if (cudaMemcpyFromSymbol(out, cqg::g_lloyd_timing, 8 * sizeof(unsigned long long)) != cudaSuccess) return 1;
+    if (reset) {
+        unsigned long long z[8] = {};
+        cudaMemcpyToSymbol(cqg::g_lloyd_timing, z, sizeof(z));
+    }
+    return 0;
+}
+#endif

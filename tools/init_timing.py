@@ -54,6 +54,21 @@ def run(name):
     for i, nm in enumerate(names):
         print(f"{nm:14s} {buf[i] / rounds:8.0f} cycles/round  {100 * buf[i] / tot:5.1f}%")
     print(f"{'total':14s} {tot / rounds:8.0f} cycles/round")
+    # persistent Lloyd kernel phases (block 0, thread 0), per WALK iteration
+    init = initf(hist, sc, ctx=ctx)
+    opts = quant.ClusterOptions(quant.Termination(fixed_iterations=cfg.fixed_iterations or None))
+    quant.wsm_hist(hist, init, opts, ctx=ctx)
+    L.cqg_dbg_lloyd_timing(buf, 1)
+    st = None
+    for _ in range(reps):
+        st = quant.wsm_hist(hist, init, opts, ctx=ctx)
+    L.cqg_dbg_lloyd_timing(buf, 1)
+    its = reps * (st.iterations - 1)
+    names = ["ndc", "sweep", "flush+replay", "grid_sync_1", "iter_end", "grid_sync_2"]
+    tot = sum(buf[i] for i in range(6))
+    for i, nm in enumerate(names):
+        print(f"{nm:14s} {buf[i] / its:8.0f} cycles/iter  {100 * buf[i] / tot:5.1f}%")
+    print(f"{'total':14s} {tot / its:8.0f} cycles/iter  (swept {st.swept_total / (st.iterations * len(hist.counts)):.3f})")
 
 
 if __name__ == "__main__":
