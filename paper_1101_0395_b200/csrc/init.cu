@@ -41,6 +41,7 @@ constexpr int kFix = 88;        // fixed-point fraction bits
 constexpr int kInitThreads = 256;
 constexpr int kSeg = 1024;      // points per segment (4 per thread)
 constexpr uint32_t kWeightsOnly = 0xFFFFFFFFu;
+constexpr int kLocateMax = 384; // block sums / segments one warp_locate scans (registers)
 
 struct InitArgs {
     const uint32_t *colors;
@@ -54,7 +55,8 @@ struct InitArgs {
     uint64_t first_index;
     uint64_t chunk;      // points per block (multiple of kSeg)
     const double *nu;    // unit draws, in consumption order
-    uint32_t *md;        // 2 x n ping-pong min distances
+    uint32_t *md;        // 2 x n ping-pong min distances (init_kernel) or n x {colour, md} (init_kernel_rec)
+    int mds;             // stride of md values in `md` seen by the locate (1, or 2 for records)
     u128 *parts;         // 2 x gridDim block mass sums
     u128 *segs;          // 2 x nseg segment mass sums
     unsigned long long *mparts; // 2 x gridDim maximin keys
@@ -180,7 +182,7 @@ template <class M>
 __device__ int warp_locate(const typename M::T *arr, int cnt, bool from_total, double nu,
                            typename M::T &U, typename M::T *before, typename M::T *total) {
     typedef typename M::T T;
-    constexpr int RMAX = 12;
+    constexpr int RMAX = kLocateMax / 32; // cnt <= kLocateMax (the host caps grids and segments)
     const int lane = threadIdx.x & 31;
     const int R = (cnt + 31) / 32;
     T v[RMAX];
@@ -251,11 +253,12 @@ __device__ typename M::T block_excl(typename M::T v, typename M::T *s_w, typenam
 // Reference rng.hpp:43-54 replayed sequentially in FP64 (one thread).
 __device__ uint64_t sequential_draw(const InitArgs &a, const uint32_t *md, double nu, int weights_only) {
     double total = 0.0;
-    for (uint64_t i = 0; i < a.n; ++i) total = __dadd_rn(total, mass_of(a, i, weights_only ? kWeightsOnly : md[i]));
+    for (uint64_t i = 0; i < a.n; ++i)
+        total = __dadd_rn(total, mass_of(a, i, weights_only ? kWeightsOnly : md[i * a.mds]));
     const double u = __dmul_rn(nu, total);
     double acc = 0.0;
     for (uint64_t i = 0; i + 1 < a.n; ++i) {
-        acc = __dadd_rn(acc, mass_of(a, i, weights_only ? kWeightsOnly : md[i]));
+        acc = __dadd_rn(acc, mass_of(a, i, weights_only ? kWeightsOnly : md[i * a.mds]));
         if (u < acc) return i;
     }
     return a.n - 1;
@@ -397,7 +400,7 @@ __device__ uint64_t locate_draw(const InitArgs &a, cg::grid_group &grid, int par
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const uint64_t i = base + j;
-            m[j] = i < a.n ? M::mass(a, i, weights_only ? kWeightsOnly : md[i]) : (T)0;
+            m[j] = i < a.n ? M::mass(a, i, weights_only ? kWeightsOnly : md[i * a.mds]) : (T)0;
             loc += m[j];
         }
         T btot;
@@ -423,7 +426,7 @@ __device__ uint64_t locate_draw(const InitArgs &a, cg::grid_group &grid, int par
     if (s_found == ~0ull || s_found >= a.n - 1) {
         idx = a.n - 1; // the reference returns n-1 when no i < n-1 qualifies
         if (!M::exact && a.n > 1) {
-            const T mlast = M::mass(a, a.n - 1, weights_only ? kWeightsOnly : md[a.n - 1]);
+            const T mlast = M::mass(a, a.n - 1, weights_only ? kWeightsOnly : md[(a.n - 1) * a.mds]);
             ambiguous = !(U > tot - mlast + M::bound(a.n, tot));
         }
     } else {
@@ -531,6 +534,226 @@ __global__ void __launch_bounds__(kInitThreads) init_kernel(InitArgs a) {
             pick = locate_draw<M>(a, grid, par, a.nu[k], 0, md_out, s_w);
         }
         par ^= 1;
+        clast = __ldg(a.colors + pick);
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            a.cen[3 * k] = (double)((clast >> 16) & 255u);
+            a.cen[3 * k + 1] = (double)((clast >> 8) & 255u);
+            a.cen[3 * k + 2] = (double)(clast & 255u);
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Large substrates, record layout: rec[i] = {colour, md} (8 bytes, in place).
+// A round reads 8 bytes per point and writes only the points whose min
+// distance drops; k-means++ block/segment mass sums change by the exact
+// difference of those points' masses (counts are read only for them), so a
+// round streams half the bytes of the ping-pong layout. In-place updates need
+// a second grid barrier per k-means++ round (nobody updates before every
+// block has located the draw); maximin locates through the ping-ponged block
+// maxima and keeps one barrier.
+
+constexpr int kRecBatch = 16; // records in flight per lane (32 doubles the registers: 1 block per SM)
+
+#ifdef CQG_INIT_TIMING
+__device__ unsigned long long g_coop_timing[8];
+#define GTIME(slot)                                                                  \
+    do {                                                                             \
+        if (blockIdx.x == 0 && threadIdx.x == 0) {                                   \
+            const unsigned long long _n = clock64();                                 \
+            g_coop_timing[slot] += _n - _gprev;                                      \
+            _gprev = _n;                                                             \
+        }                                                                            \
+    } while (0)
+#else
+#define GTIME(slot) \
+    do {            \
+    } while (0)
+#endif
+
+// k-means++ update over this block's segments (full: first round from the
+// colours; else incremental). The incremental loop is lean: 8-byte record
+// loads, the distance, and a change bitmask; only a warp with a changed point
+// loads counts (all at once) and rewrites md. Records past n carry md = 0 and
+// never change.
+template <class M>
+__device__ void update_rec(const InitArgs &a, bool full, uint32_t clast, uint2 *rec, uint64_t lo, uint64_t hi,
+                           typename M::T *s_w) {
+    typedef typename M::T T;
+    T *segs = reinterpret_cast<T *>(a.segs);
+    T *parts = reinterpret_cast<T *>(a.parts);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const uint32_t bb = __dp4a(clast, clast, 0u);
+    T bsum = 0;
+    for (uint64_t s0 = lo + (uint64_t)warp * kSeg; s0 < hi; s0 += (uint64_t)nw * kSeg) {
+        T loc = 0;
+        if (full) {
+            for (int b = lane; b < kSeg; b += 32) {
+                const uint64_t i = s0 + b;
+                if (i < hi) {
+                    const uint32_t c = __ldg(a.colors + i);
+                    const uint32_t d = d2_int_bb(c, clast, bb);
+                    rec[i] = make_uint2(c, d);
+                    loc += M::mass_c(a, __ldg(a.counts + i), d);
+                }
+            }
+        } else {
+            const bool whole = s0 + kSeg <= hi;
+            for (int b = 0; b < kSeg; b += 32 * kRecBatch) {
+                uint2 r[kRecBatch];
+                if (whole) {
+#pragma unroll
+                    for (int u = 0; u < kRecBatch; ++u) r[u] = rec[s0 + b + u * 32 + lane];
+                } else {
+#pragma unroll
+                    for (int u = 0; u < kRecBatch; ++u) {
+                        const uint64_t i = s0 + b + u * 32 + lane;
+                        r[u] = i < hi ? rec[i] : make_uint2(0u, 0u);
+                    }
+                }
+                uint32_t chg = 0;
+#pragma unroll
+                for (int u = 0; u < kRecBatch; ++u)
+                    chg |= (d2_int_bb(r[u].x, clast, bb) < r[u].y ? 1u : 0u) << u;
+                if (__any_sync(0xffffffffu, chg != 0)) {
+                    uint32_t cn[kRecBatch];
+#pragma unroll
+                    for (int u = 0; u < kRecBatch; ++u)
+                        cn[u] = (chg >> u) & 1u ? __ldg(a.counts + s0 + b + u * 32 + lane) : 0u;
+#pragma unroll
+                    for (int u = 0; u < kRecBatch; ++u) {
+                        if ((chg >> u) & 1u) {
+                            const uint32_t d = d2_int_bb(r[u].x, clast, bb);
+                            loc += M::mass_c(a, cn[u], r[u].y) - M::mass_c(a, cn[u], d); // masses fall with md
+                            rec[s0 + b + u * 32 + lane].y = d;
+                        }
+                    }
+                }
+            }
+        }
+        for (int o = 16; o; o >>= 1) loc += M::shfl(loc, lane ^ o);
+        if (lane == 0) {
+            if (full) segs[s0 / kSeg] = loc;
+            else if (loc != (T)0) segs[s0 / kSeg] -= loc;
+        }
+        bsum += loc;
+    }
+    if (lane == 0) s_w[warp] = bsum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        T t = 0;
+        for (int w = 0; w < nw; ++w) t += s_w[w];
+        if (full) parts[blockIdx.x] = t;
+        else parts[blockIdx.x] -= t;
+    }
+    __syncthreads();
+}
+
+template <class M>
+__global__ void __launch_bounds__(kInitThreads) init_kernel_rec(InitArgs a) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ typename M::T s_w[kInitThreads / 32];
+    __shared__ unsigned long long s_m[kInitThreads / 32];
+    const uint64_t lo = (uint64_t)blockIdx.x * a.chunk;
+    const uint64_t hi = lo + a.chunk < a.n ? lo + a.chunk : a.n;
+    uint2 *rec = reinterpret_cast<uint2 *>(a.md);
+    const uint32_t *mdv = a.md + 1; // md values at stride 2 (a.mds == 2)
+    int par = 0;
+#ifdef CQG_INIT_TIMING
+    unsigned long long _gprev = clock64();
+#endif
+
+    uint64_t first;
+    if (a.kind == 1 || a.weighted_first) {
+        update_masses<M>(a, 0, 1, 0, 0, nullptr, nullptr, lo, hi, s_w);
+        grid.sync();
+        first = locate_draw<M>(a, grid, 0, a.nu[0], 1, nullptr, s_w);
+        grid.sync(); // the block sums are rewritten in place below
+    } else {
+        first = a.first_index;
+    }
+    uint32_t clast = __ldg(a.colors + first);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        a.cen[0] = (double)((clast >> 16) & 255u);
+        a.cen[1] = (double)((clast >> 8) & 255u);
+        a.cen[2] = (double)(clast & 255u);
+    }
+    for (int k = 1; k < a.K; ++k) {
+        uint64_t pick;
+        if (a.kind == 0) {
+            const uint32_t bb = __dp4a(clast, clast, 0u);
+            // per thread: the largest md and, among equal md, the lowest index
+            uint32_t bm = 0, bi = 0xFFFFFFFFu;
+            if (k == 1) {
+                for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+                    const uint32_t c = __ldg(a.colors + i);
+                    const uint32_t m = d2_int_bb(c, clast, bb);
+                    rec[i] = make_uint2(c, m);
+                    if (m > bm || (m == bm && (uint32_t)i < bi)) bm = m, bi = (uint32_t)i;
+                }
+            } else {
+                for (uint64_t i0 = lo + threadIdx.x; i0 < hi; i0 += (uint64_t)kRecBatch * blockDim.x) {
+                    uint2 r[kRecBatch];
+#pragma unroll
+                    for (int u = 0; u < kRecBatch; ++u) {
+                        const uint64_t i = i0 + (uint64_t)u * blockDim.x;
+                        r[u] = i < hi ? rec[i] : make_uint2(0u, 0u);
+                    }
+#pragma unroll
+                    for (int u = 0; u < kRecBatch; ++u) {
+                        const uint32_t d = d2_int_bb(r[u].x, clast, bb);
+                        const uint64_t i = i0 + (uint64_t)u * blockDim.x;
+                        if (d < r[u].y) { // only reachable for i < hi (padding has md 0)
+                            r[u].y = d;
+                            rec[i].y = d;
+                        }
+                        // indices grow with u: strict > keeps the lowest index on ties
+                        if (r[u].y > bm || (bi == 0xFFFFFFFFu && i < hi)) bm = r[u].y, bi = (uint32_t)i;
+                    }
+                }
+            }
+            unsigned long long best = bi == 0xFFFFFFFFu ? 0ull : (((unsigned long long)bm << 32) | (uint32_t)~bi);
+            for (int o = 16; o; o >>= 1) {
+                const unsigned long long t = __shfl_xor_sync(0xffffffffu, best, o);
+                best = t > best ? t : best;
+            }
+            if ((threadIdx.x & 31) == 0) s_m[threadIdx.x >> 5] = best;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                unsigned long long b = 0;
+                for (int i = 0; i < kInitThreads / 32; ++i) b = s_m[i] > b ? s_m[i] : b;
+                a.mparts[(size_t)par * gridDim.x + blockIdx.x] = b;
+            }
+            grid.sync();
+            unsigned long long b = 0;
+            if (threadIdx.x < 32) {
+                for (unsigned i = threadIdx.x; i < gridDim.x; i += 32) {
+                    const unsigned long long t = a.mparts[(size_t)par * gridDim.x + i];
+                    b = t > b ? t : b;
+                }
+                for (int o = 16; o; o >>= 1) {
+                    const unsigned long long t = __shfl_xor_sync(0xffffffffu, b, o);
+                    b = t > b ? t : b;
+                }
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) s_m[0] = b;
+            __syncthreads();
+            b = s_m[0];
+            pick = (uint64_t)(uint32_t)~(uint32_t)(b & 0xFFFFFFFFull);
+            par ^= 1;
+        } else {
+            GTIME(4);
+            update_rec<M>(a, k == 1, clast, rec, lo, hi, s_w);
+            GTIME(0);
+            grid.sync();
+            GTIME(1);
+            pick = locate_draw<M>(a, grid, 0, a.nu[k], 0, mdv, s_w);
+            GTIME(2);
+            grid.sync(); // records and sums are updated in place by the next round
+            GTIME(3);
+        }
         clast = __ldg(a.colors + pick);
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             a.cen[3 * k] = (double)((clast >> 16) & 255u);
@@ -937,19 +1160,24 @@ void run_init(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *counts_d, 
         c.result = resc;
         c.fallbacks = resc + 4;
         c.cen = centers_d;
+        c.mds = 1;
         if (exact ? launch_cluster_init<ExactMass>(ctx, c) : launch_cluster_init<FixedMass>(ctx, c)) return;
     }
-    const void *kern = exact ? (const void *)init_kernel<ExactMass> : (const void *)init_kernel<FixedMass>;
+    const bool rec = ctx->use_init_rec;
+    const void *kern = rec ? (exact ? (const void *)init_kernel_rec<ExactMass> : (const void *)init_kernel_rec<FixedMass>)
+                           : (exact ? (const void *)init_kernel<ExactMass> : (const void *)init_kernel<FixedMass>);
     int occ = 0;
     CQG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kInitThreads, 0));
     if (occ < 1) occ = 1;
     uint64_t grid = (uint64_t)ctx->num_sms * (uint64_t)(occ > 2 ? 2 : occ);
+    if (grid > (uint64_t)kLocateMax) grid = kLocateMax; // warp_locate scans <= kLocateMax block sums
     const uint64_t want = (n + kSeg - 1) / kSeg;
     if (grid > want) grid = want;
     if (grid < 1) grid = 1;
     uint64_t chunk = (n + grid - 1) / grid;
     chunk = (chunk + kSeg - 1) / kSeg * kSeg;
     grid = (n + chunk - 1) / chunk;
+    if (chunk / kSeg > (uint64_t)kLocateMax) fail(CQG_E_RUNTIME, "init: too many segments per block");
     const uint64_t nseg = (n + kSeg - 1) / kSeg;
     double *nu_d = static_cast<double *>(ctx->unit_draws.ensure(sizeof(double) * nu.size()));
     CQG_CUDA(cudaMemcpyAsync(nu_d, nu.data(), sizeof(double) * nu.size(), cudaMemcpyHostToDevice, s));
@@ -973,6 +1201,7 @@ void run_init(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *counts_d, 
     a.chunk = chunk;
     a.nu = nu_d;
     a.md = md;
+    a.mds = rec ? 2 : 1;
     a.parts = parts;
     a.segs = segs;
     a.mparts = mparts;
@@ -1007,6 +1236,17 @@ extern "C" int cqg_dbg_init_timing(unsigned long long *out, int reset) {
     if (reset) {
         unsigned long long z[8] = {};
         cudaMemcpyToSymbol(cqg::g_init_timing, z, sizeof(z));
+    }
+    return 0;
+}
+#endif
+
+#ifdef CQG_INIT_TIMING
+extern "C" int cqg_dbg_coop_timing(unsigned long long *out, int reset) {
+    if (cudaMemcpyFromSymbol(out, cqg::g_coop_timing, 8 * sizeof(unsigned long long)) != cudaSuccess) return 1;
+    if (reset) {
+        unsigned long long z[8] = {};
+        cudaMemcpyToSymbol(cqg::g_coop_timing, z, sizeof(z));
     }
     return 0;
 }

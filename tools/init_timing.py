@@ -51,9 +51,20 @@ def run(name):
     rounds = reps * (cfg.k - 1)
     names = ["update", "publish", "cluster_sync", "draw", "tail"]
     tot = sum(buf[i] for i in range(5))
-    for i, nm in enumerate(names):
-        print(f"{nm:14s} {buf[i] / rounds:8.0f} cycles/round  {100 * buf[i] / tot:5.1f}%")
-    print(f"{'total':14s} {tot / rounds:8.0f} cycles/round")
+    if tot:  # cluster kernel (small substrates)
+        for i, nm in enumerate(names):
+            print(f"{nm:14s} {buf[i] / rounds:8.0f} cycles/round  {100 * buf[i] / tot:5.1f}%")
+        print(f"{'total':14s} {tot / rounds:8.0f} cycles/round")
+    # cooperative record kernel (large substrates; forced with CQG_NO_CLUSTER_INIT=1)
+    L.cqg_dbg_coop_timing(buf, 1)
+    initf(hist, sc, ctx=ctx)
+    L.cqg_dbg_coop_timing(buf, 1)
+    names = ["update", "grid_sync_1", "locate", "grid_sync_2", "tail"]
+    tot = sum(buf[i] for i in range(5))
+    if tot:
+        rounds1 = cfg.k - 1
+        for i, nm in enumerate(names):
+            print(f"coop {nm:14s} {buf[i] / rounds1:8.0f} cycles/round  {100 * buf[i] / tot:5.1f}%")
     # persistent Lloyd kernel phases (block 0, thread 0), per WALK iteration
     init = initf(hist, sc, ctx=ctx)
     opts = quant.ClusterOptions(quant.Termination(fixed_iterations=cfg.fixed_iterations or None))
@@ -66,6 +77,8 @@ def run(name):
     its = reps * (st.iterations - 1)
     names = ["ndc", "sweep", "flush+replay", "grid_sync_1", "iter_end", "grid_sync_2"]
     tot = sum(buf[i] for i in range(6))
+    if not tot:
+        return
     for i, nm in enumerate(names):
         print(f"{nm:14s} {buf[i] / its:8.0f} cycles/iter  {100 * buf[i] / tot:5.1f}%")
     print(f"{'total':14s} {tot / its:8.0f} cycles/iter  (swept {st.swept_total / (st.iterations * len(hist.counts)):.3f})")

@@ -1,3 +1,5 @@
+import signal
+signal.signal(signal.SIGPIPE, signal.SIG_DFL)
 import json,sys
 for f in sys.argv[1:]:
     d=json.loads(open(f).read().strip().split('\n')[-1])
