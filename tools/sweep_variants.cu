@@ -6,6 +6,9 @@
 //   V1  V0 with best-only tracking (3-input min), no second-best
 //   V2  FP only (sum of distances, no tracking)  -> FP pipe limit
 //   V3  V0 with 4 points per thread (higher occupancy)
+//   V4  group-minimum tracking: 3-input min chain per 8-centre group, then
+//       (best, second) over group minima; the winning group's own second value
+//       comes from the index-recovery recompute (not timed here: per point)
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o sweep_variants tools/sweep_variants.cu
 #include <cstdio>
 #include <cstdlib>
@@ -45,9 +48,9 @@ __global__ void __launch_bounds__(256, 2) kern(const unsigned *colors, int n, co
             g1[i] = 0;
         }
         for (int j = 0; j < Kp; j += 8) {
-            float before[PPT];
+            float before[PPT], gm[PPT];
 #pragma unroll
-            for (int i = 0; i < PPT; ++i) before[i] = b1[i];
+            for (int i = 0; i < PPT; ++i) before[i] = b1[i], gm[i] = 3e38f;
 #pragma unroll
             for (int q = 0; q < 8; q += 4) {
                 const float4 r4 = *reinterpret_cast<const float4 *>(m2r + j + q);
@@ -77,6 +80,9 @@ __global__ void __launch_bounds__(256, 2) kern(const unsigned *colors, int n, co
                         track_pair(make_float2(A2.x, A3.x), b1[2 * p], b2[2 * p]);
                         track_pair(make_float2(A0.y, A1.y), b1[2 * p + 1], b2[2 * p + 1]);
                         track_pair(make_float2(A2.y, A3.y), b1[2 * p + 1], b2[2 * p + 1]);
+                    } else if (VAR == 4) {
+                        gm[2 * p] = fminf(fminf(fminf(gm[2 * p], A0.x), A1.x), fminf(A2.x, A3.x));
+                        gm[2 * p + 1] = fminf(fminf(fminf(gm[2 * p + 1], A0.y), A1.y), fminf(A2.y, A3.y));
                     } else if (VAR == 1) {
                         b1[2 * p] = fminf(fminf(b1[2 * p], A0.x), A1.x);
                         b1[2 * p] = fminf(fminf(b1[2 * p], A2.x), A3.x);
@@ -89,7 +95,15 @@ __global__ void __launch_bounds__(256, 2) kern(const unsigned *colors, int n, co
                     }
                 }
             }
-            if (VAR != 2) {
+            if (VAR == 4) {
+#pragma unroll
+                for (int i = 0; i < PPT; ++i) {
+                    const float lo = gm[i];
+                    g1[i] = lo < b1[i] ? j : g1[i];
+                    b2[i] = fminf(b2[i], fmaxf(b1[i], lo));
+                    b1[i] = fminf(b1[i], lo);
+                }
+            } else if (VAR != 2) {
 #pragma unroll
                 for (int i = 0; i < PPT; ++i) g1[i] = b1[i] < before[i] ? j : g1[i];
             }
@@ -149,5 +163,7 @@ int main() {
     run<2, 8>(d_col, n, d_fc, K, d_out, sms);
     run<3, 4>(d_col, n, d_fc, K, d_out, sms);
     run<0, 2>(d_col, n, d_fc, K, d_out, sms);
+    run<4, 8>(d_col, n, d_fc, K, d_out, sms);
+    run<4, 4>(d_col, n, d_fc, K, d_out, sms);
     return 0;
 }
