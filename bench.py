@@ -457,6 +457,25 @@ def run_ours(args, cfg):
         "sweep_isolated": {"ms_per_launch": iso_ms, "achieved": iso_achieved,
                            "frac": iso_achieved / fp32_peak, "units_per_launch": iso_units},
     }
+    # the kernel with the largest device-time share, when it is not the Lloyd kernel
+    dominant = None
+    share = {nm: prof.ms[i] / args.steps / ms_per_step for i, nm in enumerate(names)}
+    top = max(share, key=share.get)
+    if top == "init" and share["init"] > k_share:
+        K0 = ks[0]
+        init_ms = prof.ms[cabi.PROF_INIT] / max(int(prof.launches[cabi.PROF_INIT]), 1)
+        small = all_stats[-1][0].n_unique <= 16 * 1024 * 32
+        dominant = {
+            "kernel": ("init_cluster_kernel (16-CTA cluster, shared-memory state)" if small
+                       else "init_kernel_rec (cooperative grid, in-place records)"),
+            "share_of_step": share["init"], "avg_launch_ms": init_ms,
+            "bound": "latency" if small else "hbm",
+            "rounds": K0 - 1 if cfg.init == "kpp" else K0 - 1,
+            "us_per_round": 1e3 * init_ms / max(K0 - 1, 1),
+            "note": ("a chain of K-1 dependent draws; per-round critical path (tools/init_timing.py): "
+                     "update ~31%, publish ~14%, cluster barrier ~13%, locate ~37%") if small else
+                    "8 B per point per round streamed; see DESIGN.md §8",
+        }
     hist_ms = prof.ms[cabi.PROF_HIST]
     pix_ms = prof.ms[cabi.PROF_PIXEL]
     hbm = peaks.get("hbm_gbs", 6545.6)
@@ -524,7 +543,7 @@ def run_ours(args, cfg):
             "stage_ms_last_step": {"histogram": st0.ms_histogram, "init": st0.ms_init,
                                    "lloyd": st0.ms_lloyd, "map": st0.ms_map},
             "kernels": stage_share, "byte_kernels": byte_kernels,
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roofline, "dominant_kernel": dominant, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(gpu_launches), "clocks": clocks,
         }
         print(json.dumps(line))
