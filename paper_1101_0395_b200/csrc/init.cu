@@ -777,6 +777,15 @@ __global__ void __launch_bounds__(kInitThreads) init_kernel_rec(InitArgs a) {
 constexpr int kClusterThreads = 1024;
 constexpr int kMaxClusterCtas = 16;
 
+// Split cluster barrier: only a warp that wrote data other CTAs (or other
+// warps) will read after the barrier pays the release fence; the rest arrive
+// relaxed. Every warp waits with acquire semantics.
+__device__ __forceinline__ void cluster_barrier(bool release) {
+    if (release) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    else asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+}
+
 // Phase timing of the cluster initialiser (tools/init_timing.py builds with
 // -DCQG_INIT_TIMING): clock64 deltas of CTA 0 / thread 0, summed over rounds.
 #ifdef CQG_INIT_TIMING
@@ -847,20 +856,17 @@ __global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_kernel(InitAr
     const uint64_t hi = lo + chunk < a.n ? lo + chunk : a.n;
     const int mine = hi > lo ? (int)(hi - lo) : 0;
     extern __shared__ __align__(16) unsigned char sm_raw[];
-    T *s_tsum = reinterpret_cast<T *>(sm_raw);                 // 2 x 1024
-    T *s_wsum = s_tsum + 2 * kClusterThreads;                  // 2 x 32
-    T *s_csum = s_wsum + 2 * 32;                               // 2
-    // every rank's CTA sums and warp sums, pushed here by their owners before
-    // the cluster barrier: the first two locate levels read local memory
-    T *s_allc = s_csum + 2;                                    // 2 x kMaxClusterCtas
-    T *s_allw = s_allc + 2 * kMaxClusterCtas;                  // 2 x kMaxClusterCtas x 32
-    unsigned long long *s_key = reinterpret_cast<unsigned long long *>(s_allw + 2 * kMaxClusterCtas * 32); // 2
+    T *s_wsum = reinterpret_cast<T *>(sm_raw);                 // 2 x 32 warp totals
+    T *s_wpre = s_wsum + 2 * 32;                               // 2 x 32 exclusive warp prefixes
+    // every rank's CTA sum, pushed here by its owner before the cluster barrier
+    T *s_allc = s_wpre + 2 * 32;                               // 2 x kMaxClusterCtas
+    unsigned long long *s_key = reinterpret_cast<unsigned long long *>(s_allc + 2 * kMaxClusterCtas); // 2
     __shared__ unsigned long long s_wkey[32];
     uint32_t *s_col = reinterpret_cast<uint32_t *>(s_key + 2);
     uint32_t *s_cnt = s_col + chunk;
     uint32_t *s_md = s_cnt + chunk;                            // 2 x chunk
     __shared__ unsigned long long s_pick;
-    __shared__ int s_amb;
+    __shared__ int s_amb, s_found;
     for (int i = t; i < (int)chunk; i += kClusterThreads) { // padding: colour 0, count 0 (mass 0)
         s_col[i] = i < mine ? __ldg(a.colors + lo + i) : 0u;
         s_cnt[i] = i < mine ? __ldg(a.counts + lo + i) : 0u;
@@ -874,69 +880,94 @@ __global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_kernel(InitAr
         return *cl.map_shared_rank(s_col + (gi % chunk), (unsigned)(gi / chunk));
     };
 
-    // one weighted draw over the masses of buffer `par` (md = nullptr: weights only)
-    auto draw = [&](int par, double nu, const uint32_t *mdb) -> uint64_t {
-        // CTA sums of all ranks, then the target rank's warp and thread sums
+    // Thread sums -> exclusive prefixes inside the CTA (thread part in a
+    // register, warp part in s_wpre) and the CTA sum pushed into every rank.
+    auto publish = [&](int par, T ts, T &tpre) {
+        if (t == 0) s_found = 0; // before this round's first barrier: no owner has written yet
+        const T incl = warp_incl<M>(ts);
+        if (lane == 31) s_wsum[par * 32 + warp] = incl;
+        __syncthreads();
         if (warp == 0) {
-            const T cv = lane < C ? s_allc[par * kMaxClusterCtas + lane] : (T)0;
-            T before, total;
-            const T U = M::target(nu, M::shfl(warp_incl<M>(cv), 31));
-            const int tc = lane_locate<M>(cv, U, &before, &total);
-            uint64_t idx = a.n - 1;
-            bool amb = false;
-            T E = 0, prevE = 0;
-            bool found = false;
-            if (tc < C) {
-                T b2, t2;
-                const T wv = s_allw[(par * kMaxClusterCtas + tc) * 32 + lane];
-                const int tw = lane_locate<M>(wv, U - before, &b2, &t2);
-                T b3, t3;
-                const T tv = *cl.map_shared_rank(s_tsum + par * kClusterThreads + tw * 32 + lane, tc);
-                const int tt = lane_locate<M>(tv, U - before - b2, &b3, &t3);
-                // the target thread's points, one per lane
-                const uint64_t tlo = (uint64_t)tc * chunk;
-                const int q0 = (tw * 32 + tt) * ppt;
-                const uint64_t mine_tc = a.n - tlo < chunk ? a.n - tlo : chunk;
-                const int nq = (uint64_t)q0 >= mine_tc ? 0 : (int)min((uint64_t)ppt, mine_tc - (uint64_t)q0);
-                T mv = 0;
-                uint32_t cv32 = 0;
-                if (lane < nq) {
-                    const uint32_t cnt = *cl.map_shared_rank(s_cnt + q0 + lane, tc);
-                    const uint32_t md = mdb ? *cl.map_shared_rank(mdb + q0 + lane, tc) : kWeightsOnly;
-                    cv32 = *cl.map_shared_rank(s_col + q0 + lane, tc); // the pick's colour, same round trip
-                    mv = M::mass_c(a, cnt, md);
-                }
-                T b4, t4;
-                const int tl = lane_locate<M>(mv, U - before - b2 - b3, &b4, &t4);
-                const uint32_t pc = __shfl_sync(0xffffffffu, cv32, tl & 31);
-                if (tl < nq) {
-                    idx = tlo + q0 + tl;
-                    prevE = before + b2 + b3 + b4;
-                    E = prevE + M::shfl(mv, tl);
-                    found = true;
-                    if (lane == 0) s_pickcol = pc;
-                }
+            const T wv = s_wsum[par * 32 + lane];
+            const T wincl = warp_incl<M>(wv);
+            s_wpre[par * 32 + lane] = wincl - wv;
+            const T c = M::shfl(wincl, 31);
+            if (lane < C) *cl.map_shared_rank(s_allc + par * kMaxClusterCtas + crank, lane) = c;
+        }
+        tpre = incl - ts;
+    };
+
+    // One weighted draw over this round's masses (md = nullptr: weights only),
+    // after the cluster barrier that published every CTA sum. Every thread
+    // places its own mass range [prefix, prefix + ts) in the histogram-order
+    // prefix; the one thread whose range holds the target scans its <= 32
+    // points in local shared memory and writes (index, colour, ambiguity) into
+    // every rank; a second cluster barrier publishes them. No warp walks the
+    // levels of the sum tree.
+    auto draw = [&](int par, double nu, const uint32_t *mdb, T ts, T tpre) -> uint64_t {
+        const T cv = lane < C ? s_allc[par * kMaxClusterCtas + lane] : (T)0;
+        const T cincl = warp_incl<M>(cv);
+        const T total = M::shfl(cincl, 31);
+        const T U = M::target(nu, total);
+        const T wlo = M::shfl(cincl - cv, crank) + s_wpre[par * 32 + warp]; // this warp's first prefix
+        // warp-uniform: does this warp's range [wlo, wlo + warp total) hold U?
+        const T wtot = M::shfl(tpre + ts, 31);
+        if (!(U < wlo) && U < wlo + wtot) {
+            const T lo_t = wlo + tpre;
+            const unsigned hm = __ballot_sync(0xffffffffu, ts != (T)0 && !(U < lo_t) && U < lo_t + ts);
+            const int tl = __ffs(hm) - 1; // the owning lane (exactly one)
+            const T base = M::shfl(lo_t, tl);
+            // the owner's points, one per lane, from local shared memory
+            const int q0 = (warp * 32 + tl) * ppt;
+            const int q = q0 + lane;
+            T m = 0;
+            uint32_t col = 0;
+            if (lane < ppt) {
+                m = M::mass_c(a, s_cnt[q], mdb ? mdb[q] : kWeightsOnly);
+                col = s_col[q];
             }
-            if (!found || idx >= a.n - 1) {
-                idx = a.n - 1;
+            const T mincl = warp_incl<M>(m);
+            const unsigned pm = __ballot_sync(0xffffffffu, lane < ppt && U < base + mincl);
+            const int pl = __ffs(pm) - 1;
+            const T E = base + M::shfl(mincl, pl);
+            const T prevE = E - M::shfl(m, pl);
+            const uint32_t pcol = __shfl_sync(0xffffffffu, col, pl);
+            const uint64_t gi = lo + (uint64_t)(q0 + pl);
+            bool amb = false;
+            if (!M::exact) {
+                const T B2 = M::bound(a.n, total);
+                // the reference returns n-1 when no earlier prefix exceeds u
+                amb = gi == a.n - 1 ? !(U > prevE + B2) : (!(E > U + B2) || (gi > 0 && !(U > prevE + B2)));
+            }
+            if (lane < C) { // one rank per lane
+                *cl.map_shared_rank(&s_pick, lane) = gi;
+                *cl.map_shared_rank(&s_pickcol, lane) = pcol;
+                *cl.map_shared_rank(&s_amb, lane) = amb ? 1 : 0;
+                *cl.map_shared_rank(&s_found, lane) = 1;
+            }
+            cluster_barrier(true);
+        } else {
+            cluster_barrier(false);
+        }
+        if (!s_found) { // the target lies beyond every prefix: the reference returns n-1
+            __syncthreads();
+            if (t == 0) {
+                const uint64_t last = a.n - 1;
+                bool amb = false;
                 if (!M::exact && a.n > 1) {
-                    const uint32_t r = (uint32_t)((a.n - 1) / chunk), li = (uint32_t)((a.n - 1) % chunk);
+                    const uint32_t r = (uint32_t)(last / chunk), li = (uint32_t)(last % chunk);
                     const uint32_t cnt = *cl.map_shared_rank(s_cnt + li, r);
                     const uint32_t md = mdb ? *cl.map_shared_rank(mdb + li, r) : kWeightsOnly;
                     amb = !(U > total - M::mass_c(a, cnt, md) + M::bound(a.n, total));
                 }
-            } else if (!M::exact) {
-                const T B2 = M::bound(a.n, total);
-                amb = !(E > U + B2) || (idx > 0 && !(U > prevE + B2));
-            }
-            if (lane == 0) {
-                s_pick = idx;
+                s_pick = last;
+                s_pickcol = colour_of(last);
                 s_amb = amb ? 1 : 0;
-                if (!found || idx == a.n - 1) s_pickcol = colour_of(idx);
             }
+            __syncthreads();
         }
-        __syncthreads();
         if (s_amb) { // identical in every CTA: uniform extra barrier
+            __syncthreads();
             if (crank == 0 && t == 0) {
                 s_pick = cluster_sequential_draw<M>(a, cl, s_cnt, mdb, chunk, nu, mdb == nullptr);
                 atomicAdd(a.fallbacks, 1ull);
@@ -953,32 +984,14 @@ __global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_kernel(InitAr
         return s_pick;
     };
 
-    auto publish = [&](int par, T ts) {
-        s_tsum[par * kClusterThreads + t] = ts;
-        T w = ts;
-        for (int o = 16; o; o >>= 1) w += M::shfl(w, lane ^ o);
-        if (lane == 0) s_wsum[par * 32 + warp] = w;
-        __syncthreads();
-        if (warp == 0) {
-            const T wv = s_wsum[par * 32 + lane];
-            T c = wv;
-            for (int o = 16; o; o >>= 1) c += M::shfl(c, lane ^ o);
-            // push this CTA's warp sums and CTA sum into every rank (the
-            // cluster barrier's release/acquire publishes them)
-            for (int r = 0; r < C; ++r) *cl.map_shared_rank(s_allw + (par * kMaxClusterCtas + crank) * 32 + lane, r) = wv;
-            if (lane < C) *cl.map_shared_rank(s_allc + par * kMaxClusterCtas + crank, lane) = c;
-        }
-    };
-
-
     int par = 0;
     uint64_t first;
     if (a.kind == 1 || a.weighted_first) {
-        T ts = 0;
+        T ts = 0, tpre;
         for (int i = p0; i < p1; ++i) ts += M::mass_c(a, s_cnt[i], kWeightsOnly);
-        publish(par, ts);
-        cl.sync();
-        first = draw(par, a.nu[0], nullptr);
+        publish(par, ts, tpre);
+        cluster_barrier(warp == 0); // warp 0 pushed the CTA sum and wrote s_wpre
+        first = draw(par, a.nu[0], nullptr, ts, tpre);
         par ^= 1;
     } else {
         first = a.first_index;
@@ -1057,11 +1070,12 @@ __global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_kernel(InitAr
                       M::mass_c(a, n4.w, m4.w);
             }
             ITIME(0);
-            publish(par, ts);
+            T tpre;
+            publish(par, ts, tpre);
             ITIME(1);
-            cl.sync();
+            cluster_barrier(warp == 0); // warp 0 pushed the CTA sum and wrote s_wpre
             ITIME(2);
-            pick = draw(par, nu_k, md_out);
+            pick = draw(par, nu_k, md_out, ts, tpre);
             ITIME(3);
         }
         par ^= 1;
@@ -1079,7 +1093,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_kernel(InitAr
 
 template <class M>
 static size_t cluster_smem(int ppt) {
-    return sizeof(typename M::T) * (2 * kClusterThreads + 64 + 2 + 2 * kMaxClusterCtas * 33) + 16 +
+    return sizeof(typename M::T) * (2 * 32 + 2 * 32 + 2 * kMaxClusterCtas) + 16 +
            (size_t)kClusterThreads * ppt * 4 * sizeof(uint32_t);
 }
 
