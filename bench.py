@@ -29,6 +29,7 @@ import statistics
 import subprocess
 import sys
 import threading
+from concurrent.futures import ThreadPoolExecutor
 import time
 
 import numpy as np
@@ -348,16 +349,48 @@ def run_ours(args, cfg):
     d_idx = [torch.empty(P, dtype=torch.int32, device=dev) for P in P_list]
     d_q = [torch.empty((P, 3), dtype=torch.uint8, device=dev) for P in P_list]
     d_pal = [torch.empty((k, 3), dtype=torch.float64, device=dev) for k in ks]
-    sse = np.zeros(128)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
 
+    # Batches (cfg4): images are independent, so W library contexts, each on
+    # its own CUDA stream and driven by its own host thread, quantize them
+    # concurrently (the 16-SM cluster initialisers of different images share
+    # the GPU; cooperative kernels are chained by the library). One image:
+    # one context on the timing stream.
+    nworkers = max(1, min(args.workers if cfg.images > 1 else 1, len(imgs)))
+    ctxs, wstreams = [ctx], [stream]
+    for _ in range(nworkers - 1):
+        c2 = cabi.Context(local)
+        s2 = torch.cuda.Stream(device=dev)
+        c2.set_stream(s2.cuda_stream)
+        ctxs.append(c2)
+        wstreams.append(s2)
+    if nworkers > 1:
+        s0 = torch.cuda.Stream(device=dev)  # worker 0 off the timing stream too
+        ctx.set_stream(s0.cuda_stream)
+        wstreams[0] = s0
+    sses = [np.zeros(128) for _ in range(nworkers)]
+    pool = ThreadPoolExecutor(nworkers) if nworkers > 1 else None
+
+    def run_batch(srcs, idxs, qs, pals):
+        # every worker stream starts after the timing stream's current point
+        # and the timing stream waits for all of them
+        if nworkers == 1:
+            return [ctx.quantize_raw(srcs[i], P_list[i], mkcfg(ks[i]), None, pals[i], None, sses[0],
+                                     idxs[i], qs[i]) for i in range(len(imgs))]
+        for ws in wstreams:
+            ws.wait_stream(stream)
+
+        def work(w):
+            return [(i, ctxs[w].quantize_raw(srcs[i], P_list[i], mkcfg(ks[i]), None, pals[i], None,
+                                             sses[w], idxs[i], qs[i]))
+                    for i in range(w, len(imgs), nworkers)]
+        res = dict(kv for part in pool.map(work, range(nworkers)) for kv in part)
+        for ws in wstreams:
+            stream.wait_stream(ws)
+        return [res[i] for i in range(len(imgs))]
+
     def step_device():
-        stats = []
-        for i in range(len(imgs)):
-            st = ctx.quantize_raw(d_imgs[i], P_list[i], mkcfg(ks[i]), None, d_pal[i], None, sse,
-                                  d_idx[i], d_q[i])
-            stats.append(st)
-        return stats
+        return run_batch(d_imgs, d_idx, d_q, d_pal)
 
     # warm-up
     for _ in range(args.warmup):
@@ -366,12 +399,13 @@ def run_ours(args, cfg):
     if world > 1:
         dist.barrier()
 
-    ctx.set_profiling(True)
-    ctx.read_profile(reset=True)
+    for c in ctxs:
+        c.set_profiling(True)
+        c.read_profile(reset=True)
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     step_ms, all_stats = [], []
-    launches0 = ctx.launches
+    launches0 = sum(c.launches for c in ctxs)
     with ClockSampler(local) as clk:
         for s in range(args.steps):
             flush.fill_(s & 255)  # L2 flush outside the timed events
@@ -382,9 +416,16 @@ def run_ours(args, cfg):
             torch.cuda.synchronize()
             step_ms.append(ev0.elapsed_time(ev1))
             all_stats.append(st)
-    gpu_launches = ctx.launches - launches0
-    prof = ctx.read_profile(reset=True)
-    ctx.set_profiling(False)
+    gpu_launches = sum(c.launches for c in ctxs) - launches0
+    profs = [c.read_profile(reset=True) for c in ctxs]
+    prof = profs[0]
+    for extra in profs[1:]:
+        for i in range(8):
+            prof.ms[i] += extra.ms[i]
+            prof.units[i] += extra.units[i]
+            prof.launches[i] += extra.launches[i]
+    for c in ctxs:
+        c.set_profiling(False)
     clocks = clk.summary()
 
     total_ms = float(sum(step_ms))
@@ -495,16 +536,13 @@ def run_ours(args, cfg):
         h_q = [torch.empty((P, 3), dtype=torch.uint8).pin_memory() for P in P_list]
         h_pal = [np.empty((k, 3)) for k in ks]
         for _ in range(max(1, args.warmup // 2)):
-            for i in range(len(imgs)):
-                ctx.quantize_raw(h_imgs[i], P_list[i], mkcfg(ks[i]), None, h_pal[i], None, sse, h_idx[i], h_q[i])
+            run_batch(h_imgs, h_idx, h_q, h_pal)
         e_ms = []
         for s in range(args.steps):
             flush.fill_(s & 255)
             torch.cuda.synchronize()
             ev0.record(stream)
-            for i in range(len(imgs)):
-                ctx.quantize_raw(h_imgs[i], P_list[i], mkcfg(ks[i]), None, h_pal[i], None, sse,
-                                 h_idx[i], h_q[i])
+            run_batch(h_imgs, h_idx, h_q, h_pal)
             ev1.record(stream)
             torch.cuda.synchronize()
             e_ms.append(ev0.elapsed_time(ev1))
@@ -532,7 +570,8 @@ def run_ours(args, cfg):
             "config": {"workload": cfg.name, "image": f"{cfg.width}x{cfg.height}",
                        "images_per_rank": len(imgs), "k": cfg.k if not cfg.k_cycle else list(cfg.k_cycle),
                        "init": cfg.init, "fixed_iterations": cfg.fixed_iterations or None,
-                       "parallelism": f"replicas x{world}" if cfg.images == 1 else f"images sharded over {world}",
+                       "parallelism": (f"replicas x{world}" if cfg.images == 1 else
+                                       f"images sharded over {world}; {nworkers} concurrent streams per GPU"),
                        "l2": "flushed (512 MiB write) between timed steps",
                        "arithmetic": "FP32 packed sweep + exact FP64 replay of near-ties + int64 moments",
                        "index_layout": "uint32 per pixel"},
@@ -549,6 +588,10 @@ def run_ours(args, cfg):
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
+    if pool:
+        pool.shutdown()
+    for c in ctxs[1:]:
+        c.close()
     ctx.close()
     return 0
 
@@ -561,6 +604,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--workers", type=int, default=4,
+                    help="batched configs: concurrent library contexts (streams + host threads) per GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--sharded", action="store_true",

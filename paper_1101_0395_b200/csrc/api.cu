@@ -11,6 +11,9 @@
 
 #include "cqg_internal.cuh"
 
+#include <map>
+#include <mutex>
+
 namespace {
 thread_local std::string g_last_error;
 
@@ -577,3 +580,35 @@ int cqg_quantize(cqg_ctx *ctx, const uint8_t *rgb, uint64_t P, const cqg_quantiz
 }
 
 } // extern "C"
+
+namespace cqg {
+cudaError_t launch_cooperative(cqg_ctx *ctx, const void *kern, dim3 grid, dim3 block, void **args, size_t smem) {
+    static std::mutex mu;
+    static std::map<int, cudaEvent_t> last; // per device: the previous cooperative launch
+    std::lock_guard<std::mutex> lock(mu);
+    cudaEvent_t &ev = last[ctx->device];
+    if (!ev) {
+        cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+        if (e != cudaSuccess) return e;
+    } else {
+        cudaError_t e = cudaStreamWaitEvent(ctx->stream, ev, 0);
+        if (e != cudaSuccess) return e;
+    }
+    cudaError_t e = cudaLaunchCooperativeKernel(kern, grid, block, args, smem, ctx->stream);
+    if (e != cudaSuccess) return e;
+    return cudaEventRecord(ev, ctx->stream);
+}
+} // namespace cqg
+
+namespace cqg {
+cudaError_t ensure_smem(const void *kern, size_t bytes) {
+    static std::mutex mu;
+    static std::map<const void *, size_t> cur;
+    std::lock_guard<std::mutex> lock(mu);
+    size_t &c = cur[kern];
+    if (bytes <= c) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) c = bytes;
+    return e;
+}
+} // namespace cqg

@@ -220,6 +220,16 @@ struct LloydOut {
     unsigned long long flagged = 0;
     unsigned long long swept = 0; // points through the full centre loop, all iterations
 };
+// Raise (never lower) a kernel's dynamic shared-memory limit. The attribute is
+// per function and process-wide: contexts on several host threads launching
+// the same kernel with different K must not undo each other's setting.
+cudaError_t ensure_smem(const void *kern, size_t bytes);
+
+// Cooperative launches from several contexts/streams of one process are
+// chained through one event per device: two partially resident grids that
+// each wait in grid.sync() for the other's SMs would deadlock.
+cudaError_t launch_cooperative(cqg_ctx *ctx, const void *kern, dim3 grid, dim3 block, void **args, size_t smem);
+
 LloydOut lloyd_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *counts_d, uint64_t n,
                    uint64_t P, const double *init_d, int k, const cqg_term &term, uint32_t *labels_d,
                    double *centers_d, double *sse_host, uint32_t *hist_labels_user,

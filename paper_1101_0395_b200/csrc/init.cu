@@ -1108,7 +1108,7 @@ static bool launch_cluster_init(cqg_ctx *ctx, InitArgs a) {
     if (smem > 227 * 1024) return false;
     auto kern = init_cluster_kernel<M>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess ||
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+        ensure_smem((const void *)kern, (int)smem) != cudaSuccess) {
         cudaGetLastError();
         return false;
     }
@@ -1224,8 +1224,7 @@ void run_init(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *counts_d, 
     a.cen = centers_d;
     void *args[] = {&a};
     const int pb = prof_begin(ctx);
-    CQG_CUDA(cudaLaunchCooperativeKernel(kern, dim3((unsigned)grid), dim3(kInitThreads),
-                                         args, 0, s));
+    CQG_CUDA(launch_cooperative(ctx, kern, dim3((unsigned)grid), dim3(kInitThreads), args, 0));
     prof_end(ctx, CQG_PROF_INIT, pb, (double)n * (double)(K - 1));
     launched(ctx);
 }

@@ -483,7 +483,7 @@ static int sweep_bps(size_t smem) {
     static thread_local int c_bps = 1;
     if (c_smem == smem) return c_bps;
     int bps = 0;
-    CQG_CUDA(cudaFuncSetAttribute(sweep_kernel<MODE, PPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CQG_CUDA(ensure_smem((const void *)sweep_kernel<MODE, PPT>, smem));
     CQG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, sweep_kernel<MODE, PPT>, kSweepThreads, smem));
     c_bps = bps < 1 ? 1 : bps;
     c_smem = smem;
@@ -509,8 +509,8 @@ static void launch_sweep_mode(cqg_ctx *ctx, const SweepArgs &a) {
         const size_t csm = a.K <= 2048 ? (size_t)a.K * 24 : 0;
         static thread_local bool attr = false;
         if (!attr && csm > 48 * 1024) {
-            CQG_CUDA(cudaFuncSetAttribute(ndc_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2048 * 24));
-            CQG_CUDA(cudaFuncSetAttribute(ndc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2048 * 24));
+            CQG_CUDA(ensure_smem((const void *)ndc_kernel<8>, 2048 * 24));
+            CQG_CUDA(ensure_smem((const void *)ndc_kernel<2>, 2048 * 24));
             attr = true;
         }
         const bool big = n >= (uint64_t)ctx->num_sms * 4 * 256 * 8;
@@ -520,8 +520,7 @@ static void launch_sweep_mode(cqg_ctx *ctx, const SweepArgs &a) {
             const size_t cs = (size_t)a.K * 24 + (size_t)a.K * (a.Kpow + 2) * 2;
             static thread_local bool cattr = false;
             if (!cattr) {
-                CQG_CUDA(cudaFuncSetAttribute(ndc_code_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              kNdcCodeMaxK * 24 + kNdcCodeMaxK * (kNdcCodeMaxK + 2) * 2));
+                CQG_CUDA(ensure_smem((const void *)ndc_code_kernel<4>, kNdcCodeMaxK * 24 + kNdcCodeMaxK * (kNdcCodeMaxK + 2) * 2));
                 cattr = true;
             }
             const int gc = pick_grid(ctx, n, 1024 * 4, 1);
@@ -673,7 +672,7 @@ static size_t iter_end_smem(int K) {
 static void launch_iter_end(cqg_ctx *ctx, const IterArgs &ia) {
     const size_t smem = iter_end_smem(ia.K);
     if (smem > 48 * 1024)
-        CQG_CUDA(cudaFuncSetAttribute(iter_end_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CQG_CUDA(ensure_smem((const void *)iter_end_kernel, (int)smem));
     iter_end_kernel<<<ia.K, 256, smem, ctx->stream>>>(ia);
     launched(ctx);
 }
@@ -752,7 +751,7 @@ static bool launch_persistent(cqg_ctx *ctx, const SweepArgs &a, IterArgs ia, boo
     static thread_local int c_bps = 0;
     int bps = c_bps;
     if (c_kern != kern || c_smem != smem) {
-        CQG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CQG_CUDA(ensure_smem((const void *)kern, (int)smem));
         CQG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, kSweepThreads, smem));
         c_kern = kern;
         c_smem = smem;
@@ -769,7 +768,7 @@ static bool launch_persistent(cqg_ctx *ctx, const SweepArgs &a, IterArgs ia, boo
     int ff = first_full ? 1 : 0;
     uint32_t lc = list_cap;
     void *args[] = {&aa, &ia, &ff, &lc};
-    CQG_CUDA(cudaLaunchCooperativeKernel(kern, dim3((unsigned)grid), dim3(kSweepThreads), args, smem, ctx->stream));
+    CQG_CUDA(launch_cooperative(ctx, kern, dim3((unsigned)grid), dim3(kSweepThreads), args, smem));
     launched(ctx);
     return true;
 }

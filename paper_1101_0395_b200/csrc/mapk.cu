@@ -186,7 +186,7 @@ double map_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P, const uint32_t *c
     launch_sweep(ctx, MODE_MAP, a);
 
     if ((size_t)K * 8 > 48 * 1024)
-        CQG_CUDA(cudaFuncSetAttribute(mse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, K * 8));
+        CQG_CUDA(ensure_smem((const void *)mse_kernel, K * 8));
     mse_kernel<<<1, 256, (size_t)K * 8, s>>>(mom, pal_d, K, P, mse_d);
     launched(ctx);
 
@@ -199,7 +199,7 @@ double map_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P, const uint32_t *c
         if (grid > gmax) grid = gmax;
         const size_t smem = (size_t)K * 4;
         if (smem > 48 * 1024) {
-            CQG_CUDA(cudaFuncSetAttribute(pixel_kernel<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            CQG_CUDA(ensure_smem((const void *)pixel_kernel<4, false>, smem));
         }
         const int pp = prof_begin(ctx);
         if (index_bytes == 1) {
