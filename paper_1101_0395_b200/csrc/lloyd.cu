@@ -125,7 +125,17 @@ __device__ __forceinline__ void top2_merge(float &m1, int &i1, float &m2, float 
 // fc_dst/tau_dst receive the FP32 sweep table: global (block 0 only) or this
 // block's shared memory (fc_every_block). Returns false when a cluster is empty
 // (status 2 written, nothing else changed).
+#ifdef CQG_INIT_TIMING
+__device__ unsigned long long g_lloyd_timing[8];
+#endif
+
 __device__ bool iter_end_body(const IterArgs &a, double *sm, float *fc_dst, float *tau_dst, bool fc_every_block) {
+#ifdef CQG_INIT_TIMING
+    const unsigned long long _ie0 = clock64();
+#endif
+    // the bookkeeping block (SSE, status, shifts, global centres / FP32 table):
+    // the last one, which owns no walk row when the grid exceeds K
+    const bool boss = blockIdx.x == gridDim.x - 1;
     const int K = a.K;
     double *s_c = sm;               // 3K centres
     double *s_a = sm + 3 * K;       // K per-cluster SSE terms (block 0)
@@ -145,13 +155,13 @@ __device__ bool iter_end_body(const IterArgs &a, double *sm, float *fc_dst, floa
         s_c[3 * k] = __ddiv_rn(__ll2double_rn(m.s[0]), nd);
         s_c[3 * k + 1] = __ddiv_rn(__ll2double_rn(m.s[1]), nd);
         s_c[3 * k + 2] = __ddiv_rn(__ll2double_rn(m.s[2]), nd);
-        if (blockIdx.x == 0) s_a[k] = cluster_sse_exact(m.n, m.s, m.q);
+        if (boss) s_a[k] = cluster_sse_exact(m.n, m.s, m.q);
     }
     if (empty) atomicOr(&s_empty, 1);
     __syncthreads();
     const int iter = *a.iter_dev + 1;
     if (s_empty) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (boss && threadIdx.x == 0) {
             a.st->state = 2;
             a.st->iteration = iter;
             a.st->n_flagged = *a.qn;
@@ -159,7 +169,7 @@ __device__ bool iter_end_body(const IterArgs &a, double *sm, float *fc_dst, floa
         }
         return false;
     }
-    if (blockIdx.x == 0) {
+    if (boss) {
         // centre moves for the distance bounds, then publish the new centres
         float m1 = -1.f, m2 = -1.f;
         int i1 = -1;
@@ -229,7 +239,10 @@ __device__ bool iter_end_body(const IterArgs &a, double *sm, float *fc_dst, floa
             if (a.use_cond) cudaGraphSetConditional(a.cond, done ? 0 : 1);
         }
     }
-    if (blockIdx.x == 0 || fc_every_block) fc_block(s_c, K, a.Kp, fc_dst, tau_dst);
+    if (boss || fc_every_block) fc_block(s_c, K, a.Kp, fc_dst, tau_dst);
+#ifdef CQG_INIT_TIMING
+    if (blockIdx.x == 0 && threadIdx.x == 0) g_lloyd_timing[6] += clock64() - _ie0;
+#endif
     // walk table row i (kmeans.cpp:14-38): sort by (d, index), then rotate self
     // to the front. Block bitonic sort over Kpow keys (padding = +inf).
     const double kInf = __longlong_as_double(0x7FF0000000000000ll);
@@ -245,6 +258,46 @@ __device__ bool iter_end_body(const IterArgs &a, double *sm, float *fc_dst, floa
             s_rank[j] = j; // index payload
         }
         __syncthreads();
+        if (a.Kpow <= (int)blockDim.x) {
+            // one element per thread, in registers: strides < 32 by warp
+            // shuffles, larger strides through shared memory
+            const int t = threadIdx.x;
+            double d = t < a.Kpow ? s_d[t] : kInf;
+            int r = t < a.Kpow ? s_rank[t] : 0x7FFFFFFF;
+            for (int size = 2; size <= a.Kpow; size <<= 1) {
+                for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                    double od;
+                    int orr;
+                    if (stride >= 32) {
+                        __syncthreads();
+                        if (t < a.Kpow) {
+                            s_d[t] = d;
+                            s_rank[t] = r;
+                        }
+                        __syncthreads();
+                        od = t < a.Kpow ? s_d[t ^ stride] : kInf;
+                        orr = t < a.Kpow ? s_rank[t ^ stride] : 0x7FFFFFFF;
+                    } else {
+                        od = __shfl_xor_sync(0xffffffffu, d, stride);
+                        orr = __shfl_xor_sync(0xffffffffu, r, stride);
+                    }
+                    const bool up = (t & size) == 0;
+                    const bool low = (t & stride) == 0;
+                    const bool other_less = od < d || (od == d && orr < r);
+                    // the low slot keeps the smaller key when ascending
+                    if (other_less == (low == up)) {
+                        d = od;
+                        r = orr;
+                    }
+                }
+            }
+            __syncthreads();
+            if (t < a.Kpow) {
+                s_d[t] = d;
+                s_rank[t] = r;
+            }
+            __syncthreads();
+        } else {
         for (int size = 2; size <= a.Kpow; size <<= 1) {
             for (int stride = size >> 1; stride > 0; stride >>= 1) {
                 for (int t = threadIdx.x; t < (a.Kpow >> 1); t += blockDim.x) {
@@ -264,6 +317,7 @@ __device__ bool iter_end_body(const IterArgs &a, double *sm, float *fc_dst, floa
                 __syncthreads();
             }
         }
+        }
         // position of self, then rotate it to the front
         __shared__ int s_self;
         for (int p = threadIdx.x; p < K; p += blockDim.x)
@@ -278,6 +332,9 @@ __device__ bool iter_end_body(const IterArgs &a, double *sm, float *fc_dst, floa
         }
         __syncthreads();
     }
+#ifdef CQG_INIT_TIMING
+    if (blockIdx.x == 0 && threadIdx.x == 0) g_lloyd_timing[7] += clock64() - _ie0;
+#endif
     return true;
 }
 
@@ -291,7 +348,6 @@ __global__ void __launch_bounds__(1024) iter_end_kernel(IterArgs a) {
 // finalise + walk table). Every block keeps its own FP32 centre table in shared memory.
 // Exits early (state 2) on an empty cluster; the host repairs and relaunches.
 #ifdef CQG_INIT_TIMING
-__device__ unsigned long long g_lloyd_timing[8];
 #define PTIME(slot)                                                                  \
     do {                                                                             \
         if (blockIdx.x == 0 && threadIdx.x == 0) {                                   \
@@ -318,6 +374,9 @@ __global__ void __launch_bounds__(kSweepThreads, 2) lloyd_persistent_kernel(Swee
     unsigned long long *s_acc64 = reinterpret_cast<unsigned long long *>(s_acc);
     double *s_end = reinterpret_cast<double *>(s_acc + 10 * K); // 5 K doubles + K ints
     uint32_t *s_list = reinterpret_cast<uint32_t *>(s_end + 4 * K + ia.Kpow) + ia.Kpow; // prune list
+    // first kNdcPrefix walk codes of every row (after the list and its aux words)
+    uint16_t *s_pre = reinterpret_cast<uint16_t *>(
+        s_list + (list_cap ? list_cap + kSweepThreads * 4 + prune_aux_words(K) : 0));
     fc_block(a.cen, K, Kp, s_fc, s_tau);
     const uint64_t chunk = (a.n + gridDim.x - 1) / gridDim.x;
     const uint64_t lo = (uint64_t)blockIdx.x * chunk;
@@ -342,8 +401,46 @@ __global__ void __launch_bounds__(kSweepThreads, 2) lloyd_persistent_kernel(Swee
             __syncthreads();
             replay_range<MODE_FULL>(la, warp, nw);
         } else {
-            unsigned long long nd = ndc_range<2>(a.colors, a.labels, lo, hi, 0, 2ull * blockDim.x, a.cen,
-                                                 a.dsorted, a.Kpow);
+            unsigned long long nd;
+            if (a.dcode) {
+                // rows of L = min(Kpow, kNdcPrefix) codes: 128-bit global loads (8
+                // codes), 8 in flight per thread, 32-bit shared stores (row stride
+                // 33 words). L and Kpow are powers of two.
+                const int L = a.Kpow < kNdcPrefix ? a.Kpow : kNdcPrefix;
+                uint32_t *dst = reinterpret_cast<uint32_t *>(s_pre);
+                if (L >= 8) {
+                    const int lq = 31 - __clz(L >> 3), kq = 31 - __clz(a.Kpow >> 3); // log2 of uint4 per row
+                    const uint4 *src = reinterpret_cast<const uint4 *>(a.dcode);
+                    const int total = K << lq;
+                    for (int e0 = threadIdx.x; e0 < total; e0 += 8 * blockDim.x) {
+                        uint4 v[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            const int e = e0 + u * blockDim.x;
+                            if (e < total) v[u] = __ldg(src + (((size_t)(e >> lq)) << kq) + (e & ((1 << lq) - 1)));
+                        }
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            const int e = e0 + u * blockDim.x;
+                            if (e < total) {
+                                uint32_t *d = dst + (e >> lq) * ((kNdcPrefix + 2) / 2) + (e & ((1 << lq) - 1)) * 4;
+                                d[0] = v[u].x;
+                                d[1] = v[u].y;
+                                d[2] = v[u].z;
+                                d[3] = v[u].w;
+                            }
+                        }
+                    }
+                } else {
+                    for (int e = threadIdx.x; e < K * L; e += blockDim.x)
+                        s_pre[(e / L) * (kNdcPrefix + 2) + e % L] = a.dcode[(size_t)(e / L) * a.Kpow + e % L];
+                }
+                __syncthreads();
+                nd = ndc_range_pre<2>(a.colors, a.labels, lo, hi, 0, 2ull * blockDim.x, a.cen, a.dsorted, a.Kpow,
+                                      s_pre);
+            } else {
+                nd = ndc_range<2>(a.colors, a.labels, lo, hi, 0, 2ull * blockDim.x, a.cen, a.dsorted, a.Kpow);
+            }
             for (int o = 16; o; o >>= 1) nd += __shfl_xor_sync(0xffffffffu, nd, o);
             if ((threadIdx.x & 31) == 0 && nd) atomicAdd(a.ndc, nd);
             for (int i = threadIdx.x; i < K * 5; i += blockDim.x) s_acc64[i] = 0;
@@ -725,9 +822,10 @@ void release_graphs(cqg_ctx *ctx) {
 }
 
 
-static size_t persist_smem(int K, int Kp, size_t list_words) {
+static size_t persist_smem(int K, int Kp, size_t list_words, bool pre) {
     return (size_t)4 * Kp * sizeof(float) + 4 * sizeof(float) + (size_t)10 * K * sizeof(uint32_t) +
-           iter_end_smem(K) + list_words * sizeof(uint32_t);
+           iter_end_smem(K) + list_words * sizeof(uint32_t) +
+           (pre ? (size_t)K * (kNdcPrefix + 2) * sizeof(uint16_t) : 0);
 }
 
 // prune-list capacity of the persistent kernel: a block's whole point range
@@ -743,7 +841,7 @@ static size_t persist_list_alloc(size_t cap, int K) { return cap ? cap + kSweepT
 // Launch the persistent loop if it fits co-resident; returns false otherwise.
 static bool launch_persistent(cqg_ctx *ctx, const SweepArgs &a, IterArgs ia, bool first_full) {
     const uint32_t list_cap = a.bnd ? (uint32_t)persist_list_words(ctx, a.n) : 0u;
-    const size_t smem = persist_smem(a.K, a.Kp, persist_list_alloc(list_cap, a.K));
+    const size_t smem = persist_smem(a.K, a.Kp, persist_list_alloc(list_cap, a.K), a.dcode != nullptr);
     const int ppt = a.n <= (uint64_t)ctx->num_sms * 2 * kSweepThreads * 2 ? 2 : 4;
     const void *kern = ppt == 2 ? (const void *)lloyd_persistent_kernel<2> : (const void *)lloyd_persistent_kernel<4>;
     static thread_local const void *c_kern = nullptr;

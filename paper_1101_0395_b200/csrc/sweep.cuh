@@ -187,69 +187,6 @@ __device__ __forceinline__ uint32_t walk_ndc(double xr, double xg, double xb, in
     return walk_positions(__dmul_rn(4.0, pd), dsorted + (size_t)prev * Kpow, Kpow);
 }
 
-// NDC of one WALK iteration, before the sweep rewrites the labels: 4 points per
-// thread with their lifting searches interleaved (independent loads in flight).
-// NDC over points [lo, hi) with a thread stride of blockDim.x (per-block range
-// in the persistent kernel, the whole grid range in ndc_kernel).
-template <int Q>
-__device__ __forceinline__ unsigned long long ndc_range(const uint32_t *__restrict__ colors,
-                                                        const uint32_t *__restrict__ labels, uint64_t lo,
-                                                        uint64_t hi, uint64_t first, uint64_t stride,
-                                                        const double *c, const double *__restrict__ dsorted,
-                                                        int Kpow) {
-    unsigned long long local = 0;
-    for (uint64_t base = lo + first; base < hi; base += stride) {
-        double cut[Q];
-        const double *row[Q];
-        int pos[Q];
-#pragma unroll
-        for (int q = 0; q < Q; ++q) {
-            const uint64_t i = base + threadIdx.x + (uint64_t)q * blockDim.x;
-            const bool v = i < hi;
-            const uint32_t col = v ? __ldg(colors + i) : 0u;
-            const int prev = v ? (int)labels[i] : 0;
-            const double pd = d2_exact((double)((col >> 16) & 255u), (double)((col >> 8) & 255u),
-                                       (double)(col & 255u), c[3 * prev], c[3 * prev + 1], c[3 * prev + 2]);
-            cut[q] = v ? __dmul_rn(4.0, pd) : -1.0; // -1: counts nothing and adds 0 below
-            row[q] = dsorted + (size_t)prev * Kpow;
-            pos[q] = 0;
-        }
-        for (int step = Kpow >> 1; step >= 1; step >>= 1) {
-            double vv[Q];
-#pragma unroll
-            for (int q = 0; q < Q; ++q) vv[q] = __ldg(row[q] + pos[q] + step - 1);
-#pragma unroll
-            for (int q = 0; q < Q; ++q) pos[q] += vv[q] < cut[q] ? step : 0;
-        }
-#pragma unroll
-        for (int q = 0; q < Q; ++q) {
-            // lifting reaches at most Kpow-1: the whole row may lie below the cutoff
-            if (pos[q] == Kpow - 1 && cut[q] >= 0.0 && __ldg(row[q] + Kpow - 1) < cut[q]) pos[q] = Kpow;
-            if (cut[q] >= 0.0) local += (unsigned long long)(pos[q] - (cut[q] > 0.0 ? 1 : 0) + 1);
-        }
-    }
-    return local;
-}
-
-template <int Q>
-static __global__ void __launch_bounds__(256, 4) ndc_kernel(const uint32_t *__restrict__ colors,
-                                                  const uint32_t *__restrict__ labels, uint64_t n,
-                                                  const double *__restrict__ cen,
-                                                  const double *__restrict__ dsorted, int K, int Kpow,
-                                                  unsigned long long *ndc) {
-    extern __shared__ double s_cen[];
-    const bool in_smem = K <= 2048;
-    if (in_smem)
-        for (int i = threadIdx.x; i < 3 * K; i += blockDim.x) s_cen[i] = cen[i];
-    __syncthreads();
-    const double *c = in_smem ? s_cen : cen;
-    unsigned long long local =
-        ndc_range<Q>(colors, labels, 0, n, (uint64_t)blockIdx.x * blockDim.x * Q,
-                     (uint64_t)gridDim.x * blockDim.x * Q, c, dsorted, Kpow);
-    for (int o = 16; o; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
-    if ((threadIdx.x & 31) == 0 && local) atomicAdd(ndc, local);
-}
-
 // 16-bit monotone code of a non-negative double: the top half of its
 // round-down FP32 value. Bucket property: bf(c) <= v < bf(c + 1), where bf(c)
 // is the float with bits c << 16; so code(D) < code(cut) implies D < cut and
@@ -328,6 +265,123 @@ static __global__ void __launch_bounds__(1024, 1) ndc_code_kernel(const uint32_t
     for (int o = 16; o; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
     if ((threadIdx.x & 31) == 0 && local) atomicAdd(ndc, local);
 }
+
+// NDC of one WALK iteration, before the sweep rewrites the labels: 4 points per
+// thread with their lifting searches interleaved (independent loads in flight).
+// NDC over points [lo, hi) with a thread stride of blockDim.x (per-block range
+// in the persistent kernel, the whole grid range in ndc_kernel).
+template <int Q>
+__device__ __forceinline__ unsigned long long ndc_range(const uint32_t *__restrict__ colors,
+                                                        const uint32_t *__restrict__ labels, uint64_t lo,
+                                                        uint64_t hi, uint64_t first, uint64_t stride,
+                                                        const double *c, const double *__restrict__ dsorted,
+                                                        int Kpow) {
+    unsigned long long local = 0;
+    for (uint64_t base = lo + first; base < hi; base += stride) {
+        double cut[Q];
+        const double *row[Q];
+        int pos[Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const uint64_t i = base + threadIdx.x + (uint64_t)q * blockDim.x;
+            const bool v = i < hi;
+            const uint32_t col = v ? __ldg(colors + i) : 0u;
+            const int prev = v ? (int)labels[i] : 0;
+            const double pd = d2_exact((double)((col >> 16) & 255u), (double)((col >> 8) & 255u),
+                                       (double)(col & 255u), c[3 * prev], c[3 * prev + 1], c[3 * prev + 2]);
+            cut[q] = v ? __dmul_rn(4.0, pd) : -1.0; // -1: counts nothing and adds 0 below
+            row[q] = dsorted + (size_t)prev * Kpow;
+            pos[q] = 0;
+        }
+        for (int step = Kpow >> 1; step >= 1; step >>= 1) {
+            double vv[Q];
+#pragma unroll
+            for (int q = 0; q < Q; ++q) vv[q] = __ldg(row[q] + pos[q] + step - 1);
+#pragma unroll
+            for (int q = 0; q < Q; ++q) pos[q] += vv[q] < cut[q] ? step : 0;
+        }
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            // lifting reaches at most Kpow-1: the whole row may lie below the cutoff
+            if (pos[q] == Kpow - 1 && cut[q] >= 0.0 && __ldg(row[q] + Kpow - 1) < cut[q]) pos[q] = Kpow;
+            if (cut[q] >= 0.0) local += (unsigned long long)(pos[q] - (cut[q] > 0.0 ? 1 : 0) + 1);
+        }
+    }
+    return local;
+}
+
+// NDC over [lo, hi) with the first kNdcPrefix walk positions of every row as
+// 16-bit codes in shared memory (s_pre: K rows, stride kNdcPrefix + 2). The
+// count stays in shared memory unless kNdcPrefix or more entries lie below the
+// cutoff (then the FP64 row is searched); code ties read the FP64 entries.
+constexpr int kNdcPrefix = 64;
+template <int Q>
+__device__ __forceinline__ unsigned long long ndc_range_pre(const uint32_t *__restrict__ colors,
+                                                            const uint32_t *__restrict__ labels, uint64_t lo,
+                                                            uint64_t hi, uint64_t first, uint64_t stride,
+                                                            const double *c, const double *__restrict__ dsorted,
+                                                            int Kpow, const uint16_t *s_pre) {
+    constexpr int rs = kNdcPrefix + 2;
+    const int L = Kpow < kNdcPrefix ? Kpow : kNdcPrefix;
+    unsigned long long local = 0;
+    for (uint64_t base = lo + first; base < hi; base += stride) {
+        double cut[Q];
+        uint32_t cc[Q];
+        int prow[Q], pos[Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const uint64_t i = base + threadIdx.x + (uint64_t)q * blockDim.x;
+            const bool v = i < hi;
+            const uint32_t col = v ? __ldg(colors + i) : 0u;
+            const int prev = v ? (int)labels[i] : 0;
+            const double pd = d2_exact((double)((col >> 16) & 255u), (double)((col >> 8) & 255u),
+                                       (double)(col & 255u), c[3 * prev], c[3 * prev + 1], c[3 * prev + 2]);
+            cut[q] = v ? __dmul_rn(4.0, pd) : -1.0;
+            cc[q] = v ? code16(cut[q]) : 0u;
+            prow[q] = prev;
+            pos[q] = 0;
+        }
+        for (int step = L >> 1; step >= 1; step >>= 1) {
+            uint32_t vv[Q];
+#pragma unroll
+            for (int q = 0; q < Q; ++q) vv[q] = s_pre[prow[q] * rs + pos[q] + step - 1];
+#pragma unroll
+            for (int q = 0; q < Q; ++q) pos[q] += vv[q] < cc[q] ? step : 0;
+        }
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            if (cut[q] < 0.0) continue;
+            const uint16_t *row = s_pre + prow[q] * rs;
+            const double *grow = dsorted + (size_t)prow[q] * Kpow;
+            int p = pos[q];
+            if (p == L - 1 && row[L - 1] < cc[q]) p = L;
+            while (p < L && row[p] == cc[q] && __ldg(grow + p) < cut[q]) ++p;
+            if (p == L && L < Kpow) p = (int)walk_positions(cut[q], grow, Kpow) - 1 + (cut[q] > 0.0 ? 1 : 0);
+            local += (unsigned long long)(p - (cut[q] > 0.0 ? 1 : 0) + 1);
+        }
+    }
+    return local;
+}
+
+template <int Q>
+static __global__ void __launch_bounds__(256, 4) ndc_kernel(const uint32_t *__restrict__ colors,
+                                                  const uint32_t *__restrict__ labels, uint64_t n,
+                                                  const double *__restrict__ cen,
+                                                  const double *__restrict__ dsorted, int K, int Kpow,
+                                                  unsigned long long *ndc) {
+    extern __shared__ double s_cen[];
+    const bool in_smem = K <= 2048;
+    if (in_smem)
+        for (int i = threadIdx.x; i < 3 * K; i += blockDim.x) s_cen[i] = cen[i];
+    __syncthreads();
+    const double *c = in_smem ? s_cen : cen;
+    unsigned long long local =
+        ndc_range<Q>(colors, labels, 0, n, (uint64_t)blockIdx.x * blockDim.x * Q,
+                     (uint64_t)gridDim.x * blockDim.x * Q, c, dsorted, Kpow);
+    for (int o = 16; o; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+    if ((threadIdx.x & 31) == 0 && local) atomicAdd(ndc, local);
+}
+
 
 // ---------------------------------------------------------------------------
 // The sweep kernel. Each block owns a contiguous, equal share of the points

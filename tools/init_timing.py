@@ -82,6 +82,7 @@ def run(name):
     for i, nm in enumerate(names):
         print(f"{nm:14s} {buf[i] / its:8.0f} cycles/iter  {100 * buf[i] / tot:5.1f}%")
     print(f"{'total':14s} {tot / its:8.0f} cycles/iter  (swept {st.swept_total / (st.iterations * len(hist.counts)):.3f})")
+    print(f"  iter_end: centres+status+fc {buf[6] / its:8.0f}  whole body {buf[7] / its:8.0f} cycles/iter")
 
 
 if __name__ == "__main__":
