@@ -211,6 +211,8 @@ cqg_ctx *cqg_create(int device) {
         ctx->use_graphs = !(ng && ng[0] == '1');
         const char *nc = getenv("CQG_NO_CLUSTER_INIT");
         ctx->use_cluster_init = !(nc && nc[0] == '1');
+        const char *cp = getenv("CQG_CLUSTER_MAX_PPT");
+        if (cp && atoi(cp) > 0) ctx->cluster_max_ppt = atoi(cp);
         const char *nr = getenv("CQG_NO_INIT_REC");
         ctx->use_init_rec = !(nr && nr[0] == '1');
         const char *np = getenv("CQG_NO_PRUNE");

@@ -864,7 +864,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_kernel(InitAr
     __shared__ unsigned long long s_wkey[32];
     uint32_t *s_col = reinterpret_cast<uint32_t *>(s_key + 2);
     uint32_t *s_cnt = s_col + chunk;
-    uint32_t *s_md = s_cnt + chunk;                            // 2 x chunk
+    uint32_t *s_md = s_cnt + chunk;                            // chunk, updated in place
     __shared__ unsigned long long s_pick;
     __shared__ int s_amb, s_found;
     for (int i = t; i < (int)chunk; i += kClusterThreads) { // padding: colour 0, count 0 (mass 0)
@@ -880,12 +880,15 @@ __global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_kernel(InitAr
         return *cl.map_shared_rank(s_col + (gi % chunk), (unsigned)(gi / chunk));
     };
 
-    // Thread sums -> exclusive prefixes inside the CTA (thread part in a
-    // register, warp part in s_wpre) and the CTA sum pushed into every rank.
-    auto publish = [&](int par, T ts, T &tpre) {
+    // Thread sums -> warp totals (s_wsum) -> exclusive warp prefixes (s_wpre,
+    // warp 0) and the CTA sum pushed into every rank.
+    __shared__ T s_U, s_cpre;
+    __shared__ int s_tw;
+    auto publish = [&](int par, T ts) {
         if (t == 0) s_found = 0; // before this round's first barrier: no owner has written yet
-        const T incl = warp_incl<M>(ts);
-        if (lane == 31) s_wsum[par * 32 + warp] = incl;
+        T w = ts;
+        for (int o = 16; o; o >>= 1) w += M::shfl(w, lane ^ o);
+        if (lane == 0) s_wsum[par * 32 + warp] = w;
         __syncthreads();
         if (warp == 0) {
             const T wv = s_wsum[par * 32 + lane];
@@ -894,26 +897,35 @@ __global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_kernel(InitAr
             const T c = M::shfl(wincl, 31);
             if (lane < C) *cl.map_shared_rank(s_allc + par * kMaxClusterCtas + crank, lane) = c;
         }
-        tpre = incl - ts;
     };
 
     // One weighted draw over this round's masses (md = nullptr: weights only),
-    // after the cluster barrier that published every CTA sum. Every thread
-    // places its own mass range [prefix, prefix + ts) in the histogram-order
-    // prefix; the one thread whose range holds the target scans its <= 32
-    // points in local shared memory and writes (index, colour, ambiguity) into
-    // every rank; a second cluster barrier publishes them. No warp walks the
-    // levels of the sum tree.
-    auto draw = [&](int par, double nu, const uint32_t *mdb, T ts, T tpre) -> uint64_t {
-        const T cv = lane < C ? s_allc[par * kMaxClusterCtas + lane] : (T)0;
-        const T cincl = warp_incl<M>(cv);
-        const T total = M::shfl(cincl, 31);
-        const T U = M::target(nu, total);
-        const T wlo = M::shfl(cincl - cv, crank) + s_wpre[par * 32 + warp]; // this warp's first prefix
-        // warp-uniform: does this warp's range [wlo, wlo + warp total) hold U?
-        const T wtot = M::shfl(tpre + ts, 31);
-        if (!(U < wlo) && U < wlo + wtot) {
-            const T lo_t = wlo + tpre;
+    // after the cluster barrier that published every CTA sum. Warp 0 finds the
+    // target U, this CTA's offset and the warp whose range holds U (if any);
+    // only that warp scans its lanes' sums and searches the owning thread's
+    // <= 32 points in local shared memory, then writes (index, colour,
+    // ambiguity) into every rank; a second cluster barrier publishes them.
+    auto draw = [&](int par, double nu, const uint32_t *mdb, T ts) -> uint64_t {
+        if (warp == 0) {
+            const T cv = lane < C ? s_allc[par * kMaxClusterCtas + lane] : (T)0;
+            const T cincl = warp_incl<M>(cv);
+            const T total = M::shfl(cincl, 31);
+            const T U = M::target(nu, total);
+            const T cpre = M::shfl(cincl - cv, crank);
+            const T wlo = cpre + s_wpre[par * 32 + lane];
+            const T whi = wlo + s_wsum[par * 32 + lane];
+            const unsigned m = __ballot_sync(0xffffffffu, !(U < wlo) && U < whi && s_wsum[par * 32 + lane] != (T)0);
+            if (lane == 0) {
+                s_U = U;
+                s_cpre = cpre;
+                s_tw = m ? __ffs(m) - 1 : -1;
+            }
+        }
+        __syncthreads();
+        const T U = s_U;
+        if (warp == s_tw) {
+            const T incl = warp_incl<M>(ts);
+            const T lo_t = s_cpre + s_wpre[par * 32 + warp] + incl - ts;
             const unsigned hm = __ballot_sync(0xffffffffu, ts != (T)0 && !(U < lo_t) && U < lo_t + ts);
             const int tl = __ffs(hm) - 1; // the owning lane (exactly one)
             const T base = M::shfl(lo_t, tl);
@@ -935,6 +947,8 @@ __global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_kernel(InitAr
             const uint64_t gi = lo + (uint64_t)(q0 + pl);
             bool amb = false;
             if (!M::exact) {
+                T total = 0;
+                for (int r = 0; r < C; ++r) total += s_allc[par * kMaxClusterCtas + r];
                 const T B2 = M::bound(a.n, total);
                 // the reference returns n-1 when no earlier prefix exceeds u
                 amb = gi == a.n - 1 ? !(U > prevE + B2) : (!(E > U + B2) || (gi > 0 && !(U > prevE + B2)));
@@ -955,6 +969,8 @@ __global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_kernel(InitAr
                 const uint64_t last = a.n - 1;
                 bool amb = false;
                 if (!M::exact && a.n > 1) {
+                    T total = 0;
+                    for (int r = 0; r < C; ++r) total += s_allc[par * kMaxClusterCtas + r];
                     const uint32_t r = (uint32_t)(last / chunk), li = (uint32_t)(last % chunk);
                     const uint32_t cnt = *cl.map_shared_rank(s_cnt + li, r);
                     const uint32_t md = mdb ? *cl.map_shared_rank(mdb + li, r) : kWeightsOnly;
@@ -987,11 +1003,11 @@ __global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_kernel(InitAr
     int par = 0;
     uint64_t first;
     if (a.kind == 1 || a.weighted_first) {
-        T ts = 0, tpre;
+        T ts = 0;
         for (int i = p0; i < p1; ++i) ts += M::mass_c(a, s_cnt[i], kWeightsOnly);
-        publish(par, ts, tpre);
+        publish(par, ts);
         cluster_barrier(warp == 0); // warp 0 pushed the CTA sum and wrote s_wpre
-        first = draw(par, a.nu[0], nullptr, ts, tpre);
+        first = draw(par, a.nu[0], nullptr, ts);
         par ^= 1;
     } else {
         first = a.first_index;
@@ -1007,17 +1023,16 @@ __global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_kernel(InitAr
 #ifdef CQG_INIT_TIMING
     unsigned long long _tprev = clock64();
 #endif
+    T ts_run = 0; // this thread's mass sum, kept across rounds (exact deltas)
     for (int k = 1; k < a.K; ++k) {
-        const uint32_t *md_in = s_md + (size_t)((k - 1) & 1) * chunk;
-        uint32_t *md_out = s_md + (size_t)(k & 1) * chunk;
         uint64_t pick;
         const uint32_t bb = __dp4a(clast, clast, 0u);
         if (a.kind == 0) {
             unsigned long long best = 0;
             for (int i = p0; i < p1; ++i) {
                 const uint32_t d = d2_int_bb(s_col[i], clast, bb);
-                const uint32_t m = k == 1 ? d : min(md_in[i], d);
-                md_out[i] = m;
+                const uint32_t m = k == 1 ? d : min(s_md[i], d);
+                s_md[i] = m;
                 const unsigned long long key = ((unsigned long long)m << 32) | (uint32_t)~(uint32_t)(lo + i);
                 best = key > best ? key : best;
             }
@@ -1048,34 +1063,47 @@ __global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_kernel(InitAr
             pick = s_pick;
         } else {
             const double nu_k = __ldg(a.nu + k); // off the locate's critical path
-            // whole 4-point runs (padding has count 0: mass 0)
-            T ts = 0;
-            for (int i = p0; i < p0 + ppt; i += 4) {
-                const uint4 c4 = *reinterpret_cast<const uint4 *>(s_col + i);
-                const uint4 n4 = *reinterpret_cast<const uint4 *>(s_cnt + i);
-                uint4 m4;
-                m4.x = d2_int_bb(c4.x, clast, bb);
-                m4.y = d2_int_bb(c4.y, clast, bb);
-                m4.z = d2_int_bb(c4.z, clast, bb);
-                m4.w = d2_int_bb(c4.w, clast, bb);
-                if (k > 1) {
-                    const uint4 i4 = *reinterpret_cast<const uint4 *>(md_in + i);
-                    m4.x = min(m4.x, i4.x);
-                    m4.y = min(m4.y, i4.y);
-                    m4.z = min(m4.z, i4.z);
-                    m4.w = min(m4.w, i4.w);
+            // whole 4-point runs (padding has count 0: mass 0). md is updated in
+            // place: after the previous round's second barrier nobody reads it.
+            if (k == 1) {
+                for (int i = p0; i < p0 + ppt; i += 4) {
+                    const uint4 c4 = *reinterpret_cast<const uint4 *>(s_col + i);
+                    const uint4 n4 = *reinterpret_cast<const uint4 *>(s_cnt + i);
+                    uint4 m4;
+                    m4.x = d2_int_bb(c4.x, clast, bb);
+                    m4.y = d2_int_bb(c4.y, clast, bb);
+                    m4.z = d2_int_bb(c4.z, clast, bb);
+                    m4.w = d2_int_bb(c4.w, clast, bb);
+                    *reinterpret_cast<uint4 *>(s_md + i) = m4;
+                    ts_run += M::mass_c(a, n4.x, m4.x) + M::mass_c(a, n4.y, m4.y) + M::mass_c(a, n4.z, m4.z) +
+                              M::mass_c(a, n4.w, m4.w);
                 }
-                *reinterpret_cast<uint4 *>(md_out + i) = m4;
-                ts += M::mass_c(a, n4.x, m4.x) + M::mass_c(a, n4.y, m4.y) + M::mass_c(a, n4.z, m4.z) +
-                      M::mass_c(a, n4.w, m4.w);
+            } else {
+                // only points closer to the new centre change: their mass
+                // difference is subtracted from the running sum (exact)
+                T delta = 0;
+                for (int i = p0; i < p0 + ppt; i += 4) {
+                    const uint4 c4 = *reinterpret_cast<const uint4 *>(s_col + i);
+                    uint4 m4 = *reinterpret_cast<const uint4 *>(s_md + i);
+                    const uint32_t dx = d2_int_bb(c4.x, clast, bb), dy = d2_int_bb(c4.y, clast, bb),
+                                   dz = d2_int_bb(c4.z, clast, bb), dw = d2_int_bb(c4.w, clast, bb);
+                    if ((dx < m4.x) | (dy < m4.y) | (dz < m4.z) | (dw < m4.w)) {
+                        const uint4 n4 = *reinterpret_cast<const uint4 *>(s_cnt + i);
+                        if (dx < m4.x) { delta += M::mass_c(a, n4.x, m4.x) - M::mass_c(a, n4.x, dx); m4.x = dx; }
+                        if (dy < m4.y) { delta += M::mass_c(a, n4.y, m4.y) - M::mass_c(a, n4.y, dy); m4.y = dy; }
+                        if (dz < m4.z) { delta += M::mass_c(a, n4.z, m4.z) - M::mass_c(a, n4.z, dz); m4.z = dz; }
+                        if (dw < m4.w) { delta += M::mass_c(a, n4.w, m4.w) - M::mass_c(a, n4.w, dw); m4.w = dw; }
+                        *reinterpret_cast<uint4 *>(s_md + i) = m4;
+                    }
+                }
+                ts_run -= delta;
             }
             ITIME(0);
-            T tpre;
-            publish(par, ts, tpre);
+            publish(par, ts_run);
             ITIME(1);
             cluster_barrier(warp == 0); // warp 0 pushed the CTA sum and wrote s_wpre
             ITIME(2);
-            pick = draw(par, nu_k, md_out, ts, tpre);
+            pick = draw(par, nu_k, s_md, ts_run);
             ITIME(3);
         }
         par ^= 1;
@@ -1094,7 +1122,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_kernel(InitAr
 template <class M>
 static size_t cluster_smem(int ppt) {
     return sizeof(typename M::T) * (2 * 32 + 2 * 32 + 2 * kMaxClusterCtas) + 16 +
-           (size_t)kClusterThreads * ppt * 4 * sizeof(uint32_t);
+           (size_t)kClusterThreads * ppt * 3 * sizeof(uint32_t); // colour, count, md
 }
 
 // Try the cluster initialiser; false when the substrate does not fit.
@@ -1103,7 +1131,7 @@ static bool launch_cluster_init(cqg_ctx *ctx, InitArgs a) {
     constexpr int C = 16;
     const uint64_t per = (a.n + C - 1) / C;
     const int ppt = ((int)((per + kClusterThreads - 1) / kClusterThreads) + 3) & ~3; // 128-bit runs
-    if (ppt < 1 || ppt > 32) return false;
+    if (ppt < 1 || ppt > ctx->cluster_max_ppt) return false;
     const size_t smem = cluster_smem<M>(ppt);
     if (smem > 227 * 1024) return false;
     auto kern = init_cluster_kernel<M>;

@@ -127,6 +127,19 @@ __device__ __forceinline__ void top2_merge(float &m1, int &i1, float &m2, float 
 // (status 2 written, nothing else changed).
 #ifdef CQG_INIT_TIMING
 __device__ unsigned long long g_lloyd_timing[8];
+__device__ unsigned long long g_block_timing[1024 * 3]; // per block: ndc, sweep, replay cycles
+#define BTIME(slot)                                                                  \
+    do {                                                                             \
+        if (threadIdx.x == 0) {                                                      \
+            const unsigned long long _n = clock64();                                 \
+            g_block_timing[blockIdx.x * 3 + (slot)] += _n - _bprev;                  \
+            _bprev = _n;                                                             \
+        }                                                                            \
+    } while (0)
+#else
+#define BTIME(slot) \
+    do {            \
+    } while (0)
 #endif
 
 __device__ bool iter_end_body(const IterArgs &a, double *sm, float *fc_dst, float *tau_dst, bool fc_every_block) {
@@ -389,6 +402,7 @@ __global__ void __launch_bounds__(kSweepThreads, 2) lloyd_persistent_kernel(Swee
     bool full = first_full != 0;
 #ifdef CQG_INIT_TIMING
     unsigned long long _tprev = clock64();
+    unsigned long long _bprev = _tprev;
 #endif
     for (;;) {
         // phase A: NDC, sweep and the exact replay of this block's own queued
@@ -446,17 +460,23 @@ __global__ void __launch_bounds__(kSweepThreads, 2) lloyd_persistent_kernel(Swee
             for (int i = threadIdx.x; i < K * 5; i += blockDim.x) s_acc64[i] = 0;
             __syncthreads();
             PTIME(0);
+            BTIME(0);
             sweep_range<MODE_WALK, PPT>(la, lo, hi, s_fc, s_acc, s_tau[0], s_tau[1], s_list, list_cap,
                                         reinterpret_cast<float *>(s_list + list_cap + kSweepThreads * 4));
             __syncthreads();
             PTIME(1);
+            BTIME(1);
             flush_acc64(s_acc64, a.mom, K);
             replay_range<MODE_WALK>(la, warp, nw);
             PTIME(2);
+            BTIME(2);
         }
         if (threadIdx.x == 0 && s_qn) atomicAdd(a.qn, s_qn);
         grid.sync();
         PTIME(3);
+#ifdef CQG_INIT_TIMING
+        _bprev = clock64();
+#endif
         const bool ok = iter_end_body(ia, s_end, s_fc, s_tau, true);
         PTIME(4);
         grid.sync();
@@ -1267,6 +1287,17 @@ extern "C" int cqg_dbg_lloyd_timing(unsigned long long *out, int reset) {
     if (reset) {
         unsigned long long z[8] = {};
         cudaMemcpyToSymbol(cqg::g_lloyd_timing, z, sizeof(z));
+    }
+    return 0;
+}
+#endif
+
+#ifdef CQG_INIT_TIMING
+extern "C" int cqg_dbg_block_timing(unsigned long long *out, int reset) {
+    if (cudaMemcpyFromSymbol(out, cqg::g_block_timing, 1024 * 3 * sizeof(unsigned long long)) != cudaSuccess) return 1;
+    if (reset) {
+        static unsigned long long z[1024 * 3] = {};
+        cudaMemcpyToSymbol(cqg::g_block_timing, z, sizeof(z));
     }
     return 0;
 }

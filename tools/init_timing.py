@@ -70,11 +70,22 @@ def run(name):
     opts = quant.ClusterOptions(quant.Termination(fixed_iterations=cfg.fixed_iterations or None))
     quant.wsm_hist(hist, init, opts, ctx=ctx)
     L.cqg_dbg_lloyd_timing(buf, 1)
+    L.cqg_dbg_block_timing((C.c_ulonglong * (1024 * 3))(), 1)
     st = None
     for _ in range(reps):
         st = quant.wsm_hist(hist, init, opts, ctx=ctx)
     L.cqg_dbg_lloyd_timing(buf, 1)
     its = reps * (st.iterations - 1)
+    bt = (C.c_ulonglong * (1024 * 3))()
+    L.cqg_dbg_block_timing(bt, 0)
+    import numpy as np
+    arr = np.array(bt[:], dtype=np.float64).reshape(1024, 3)
+    arr = arr[arr.sum(1) > 0] / its
+    for j, nm in enumerate(["ndc", "sweep", "replay"]):
+        col = arr[:, j]
+        print(f"  per-block {nm:7s} min {col.min():8.0f} mean {col.mean():8.0f} max {col.max():8.0f}")
+    tot_b = arr.sum(1)
+    print(f"  per-block total   min {tot_b.min():8.0f} mean {tot_b.mean():8.0f} max {tot_b.max():8.0f}")
     names = ["ndc", "sweep", "flush+replay", "grid_sync_1", "iter_end", "grid_sync_2"]
     tot = sum(buf[i] for i in range(6))
     if not tot:
