@@ -774,6 +774,12 @@ __global__ void __launch_bounds__(kInitThreads) init_kernel_rec(InitArgs a) {
 // (CTA sums, then the target CTA's 32 warp sums, its 32 thread sums, and the
 // target thread's <= 32 point masses). The arithmetic and the exactness
 // argument are the cooperative kernel's (ExactMass / FixedMass).
+#ifndef CQG_EXP_SKIP_UPDATE
+#define CQG_EXP_SKIP_UPDATE 0
+#endif
+#ifndef CQG_EXP_SKIP_BARRIER2
+#define CQG_EXP_SKIP_BARRIER2 0
+#endif
 constexpr int kClusterThreads = 1024;
 constexpr int kMaxClusterCtas = 16;
 
@@ -959,10 +965,11 @@ __global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_kernel(InitAr
                 *cl.map_shared_rank(&s_amb, lane) = amb ? 1 : 0;
                 *cl.map_shared_rank(&s_found, lane) = 1;
             }
-            cluster_barrier(true);
+            if (!CQG_EXP_SKIP_BARRIER2) cluster_barrier(true);
         } else {
-            cluster_barrier(false);
+            if (!CQG_EXP_SKIP_BARRIER2) cluster_barrier(false);
         }
+        if (CQG_EXP_SKIP_BARRIER2) __syncthreads();
         if (!s_found) { // the target lies beyond every prefix: the reference returns n-1
             __syncthreads();
             if (t == 0) {
@@ -1078,6 +1085,8 @@ __global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_kernel(InitAr
                     ts_run += M::mass_c(a, n4.x, m4.x) + M::mass_c(a, n4.y, m4.y) + M::mass_c(a, n4.z, m4.z) +
                               M::mass_c(a, n4.w, m4.w);
                 }
+            } else if (CQG_EXP_SKIP_UPDATE) {
+                // timing experiment only (tools/init_timing.py --skip-update)
             } else {
                 // only points closer to the new centre change: their mass
                 // difference is subtracted from the running sum (exact)

@@ -503,19 +503,38 @@ __device__ __forceinline__ void sweep_tiles(const SweepArgs &a, uint64_t lo, uin
                 const float xg = (i & 1) ? xg2[i / 2].y : xg2[i / 2].x;
                 const float xb = (i & 1) ? xb2[i / 2].y : xb2[i / 2].x;
                 const float xx = (i & 1) ? xx2[i / 2].y : xx2[i / 2].x;
-                int found = -1;
+                // the group's 8 values, two centres per FADD2/FFMA2 (per lane the
+                // same operations as the sweep: bit-identical), 128-bit loads
+                float dv[kGroup];
+#pragma unroll
+                for (int q = 0; q < kGroup; q += 4) {
+                    const float4 c4 = *reinterpret_cast<const float4 *>(s_cc + g0 + q);
+                    const float4 r4 = *reinterpret_cast<const float4 *>(s_m2r + g0 + q);
+                    const float4 gq = *reinterpret_cast<const float4 *>(s_m2g + g0 + q);
+                    const float4 bq = *reinterpret_cast<const float4 *>(s_m2b + g0 + q);
+                    float2 A = __fadd2_rn(make_float2(xx, xx), make_float2(c4.x, c4.y));
+                    A = __ffma2_rn(make_float2(xr, xr), make_float2(r4.x, r4.y), A);
+                    A = __ffma2_rn(make_float2(xg, xg), make_float2(gq.x, gq.y), A);
+                    A = __ffma2_rn(make_float2(xb, xb), make_float2(bq.x, bq.y), A);
+                    float2 B = __fadd2_rn(make_float2(xx, xx), make_float2(c4.z, c4.w));
+                    B = __ffma2_rn(make_float2(xr, xr), make_float2(r4.z, r4.w), B);
+                    B = __ffma2_rn(make_float2(xg, xg), make_float2(gq.z, gq.w), B);
+                    B = __ffma2_rn(make_float2(xb, xb), make_float2(bq.z, bq.w), B);
+                    dv[q] = A.x;
+                    dv[q + 1] = A.y;
+                    dv[q + 2] = B.x;
+                    dv[q + 3] = B.y;
+                }
+                int found = kGroup;
                 float w1 = 3.0e38f, w2 = 3.0e38f;
 #pragma unroll
+                for (int q = kGroup - 1; q >= 0; --q) found = dv[q] == f1 ? q : found; // first match
+#pragma unroll
                 for (int q = 0; q < kGroup; ++q) {
-                    float d = __fadd_rn(xx, s_cc[g0 + q]);
-                    d = __fmaf_rn(xr, s_m2r[g0 + q], d);
-                    d = __fmaf_rn(xg, s_m2g[g0 + q], d);
-                    d = __fmaf_rn(xb, s_m2b[g0 + q], d);
-                    if (found < 0 && d == f1) found = g0 + q;
-                    w2 = fminf(w2, fmaxf(w1, d));
-                    w1 = fminf(w1, d);
+                    w2 = fminf(w2, fmaxf(w1, dv[q]));
+                    w1 = fminf(w1, dv[q]);
                 }
-                j1 = found < 0 ? g0 : found;
+                j1 = g0 + (found < kGroup ? found : 0);
                 f2 = fminf(b2[i], w2);
             }
             const bool flag = valid && !((f2 - f1) > tau_abs + tau_rel * (fabsf(f1) + fabsf(f2)));

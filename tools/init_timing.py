@@ -18,13 +18,13 @@ from paper_1101_0395_b200 import _build  # noqa: E402
 TLIB = os.path.join(_build.PKG, "libcqg_timing.so")
 
 
-def build():
+def build(extra=()):
     bdir = os.path.join(_build.PKG, "build_timing")
     os.makedirs(bdir, exist_ok=True)
     objs = []
     for src in _build.SOURCES:
         o = os.path.join(bdir, src.replace(".cu", ".o"))
-        subprocess.check_call([_build.nvcc(), *_build.flags(["-DCQG_INIT_TIMING"]), "-c",
+        subprocess.check_call([_build.nvcc(), *_build.flags(["-DCQG_INIT_TIMING", *extra]), "-c",
                                os.path.join(_build.CSRC, src), "-o", o])
         objs.append(o)
     subprocess.check_call([_build.nvcc(), *_build.ARCH, "-shared", "--cudart", "static", "-o", TLIB, *objs])
@@ -98,6 +98,6 @@ def run(name):
 
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "build":
-        build()
+        build(sys.argv[2:])  # e.g. -DCQG_EXP_SKIP_UPDATE=1 (timing experiments, wrong results)
     else:
         run(sys.argv[1] if len(sys.argv) > 1 else "cfg2")
