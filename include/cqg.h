@@ -85,7 +85,16 @@ typedef struct {
     uint64_t seed;
     cqg_term term;
     int index_bytes; /* 4: uint32 per pixel (MappingResult::indices layout); 1: uint8 (K <= 256) */
+    int sampling;    /* CQG_SAMPLING_* (QuantizeConfig::sampling, pipeline.cpp:91-116) */
+    int width, height; /* image shape, required by the 2:1 modes (subsample_2to1, histogram.cpp:60-67) */
 } cqg_quantize_cfg;
+
+/* QuantizeConfig::sampling. UNIQUE (the CLI default) clusters the distinct
+ * colours with count weights; NONE / TWO_TO_ONE cluster the (sub)sampled pixels
+ * themselves with weights 1/S; BOTH clusters the distinct colours of the 2:1
+ * subsample. Initialisers always read the histogram of the sampled pixels, and
+ * the mapping always covers the full image. */
+enum { CQG_SAMPLING_UNIQUE = 0, CQG_SAMPLING_NONE = 1, CQG_SAMPLING_TWO_TO_ONE = 2, CQG_SAMPLING_BOTH = 3 };
 
 typedef struct {
     uint64_t n_unique;   /* substrate_points (pipeline.cpp:117) */
@@ -189,7 +198,8 @@ int cqg_map(cqg_ctx *ctx, const uint8_t *rgb, uint64_t P, const double *palette,
 
 /* ---- whole hot path: histogram -> init -> wsm -> map --------------------
  * init: required for CQG_INIT_GIVEN (k x 3), ignored otherwise. palette: k x 3.
- * labels (capacity min(P,2^24)), sse_trace, indices, quantized may be NULL. */
+ * labels (capacity: the substrate -- min(P,2^24) colours, or P pixels for NONE),
+ * sse_trace, indices, quantized may be NULL. stats->n_unique is the substrate size. */
 int cqg_quantize(cqg_ctx *ctx, const uint8_t *rgb, uint64_t P, const cqg_quantize_cfg *cfg,
                  const double *init, double *palette, uint32_t *labels, double *sse_trace,
                  void *indices, uint8_t *quantized, cqg_quantize_stats *stats);

@@ -217,6 +217,7 @@ class RefLib:
                                        C.POINTER(C.c_int), C.POINTER(C.c_int),
                                        C.POINTER(C.c_double), C.POINTER(C.c_double),
                                        C.POINTER(C.c_double), C.c_char_p, C.c_void_p, C.c_void_p]
+        L.ref_run_quantize_s.argtypes = L.ref_run_quantize.argtypes + [C.c_char_p]
         L.ref_time_pipeline.argtypes = [_u8p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64,
                                         C.c_double, C.c_int, C.c_int, _f64p,
                                         C.POINTER(C.c_uint64), C.POINTER(C.c_int),
@@ -288,19 +289,25 @@ class RefLib:
         return idx, q.reshape(P, 3), mse.value, ndc.value
 
     def run_quantize(self, rgb, w, h, method, k, seed, eps=1e-3, max_it=100, fixed_it=0,
-                     name="", run=0):
+                     name="", run=0, sampling="unique", outputs=False):
         rgb = np.ascontiguousarray(rgb, np.uint8).reshape(-1)
         pal = np.zeros(3 * k, np.float64)
         ka, it = C.c_int(0), C.c_int(0)
         ndc, mse, tms = C.c_double(0), C.c_double(0), C.c_double(0)
         csv = C.create_string_buffer(512)
-        self._check(self.L.ref_run_quantize(rgb, w, h, method.encode(), k, seed, eps, max_it,
-                                            fixed_it, name.encode(), run, pal, C.byref(ka),
-                                            C.byref(it), C.byref(ndc), C.byref(mse), C.byref(tms),
-                                            csv, None, None))
-        return dict(palette=pal[: 3 * ka.value].reshape(-1, 3), k_actual=ka.value,
-                    iterations=it.value, ndc_per_point_iter=ndc.value, mse=mse.value,
-                    time_ms=tms.value, csv_row=csv.value.decode())
+        idx = np.zeros(w * h, np.uint32) if outputs else None
+        q = np.zeros(w * h * 3, np.uint8) if outputs else None
+        self._check(self.L.ref_run_quantize_s(rgb, w, h, method.encode(), k, seed, eps, max_it,
+                                              fixed_it, name.encode(), run, pal, C.byref(ka),
+                                              C.byref(it), C.byref(ndc), C.byref(mse), C.byref(tms),
+                                              csv, _nullable(idx), _nullable(q), sampling.encode()))
+        out = dict(palette=pal[: 3 * ka.value].reshape(-1, 3), k_actual=ka.value,
+                   iterations=it.value, ndc_per_point_iter=ndc.value, mse=mse.value,
+                   time_ms=tms.value, csv_row=csv.value.decode())
+        if outputs:
+            out["indices"] = idx
+            out["quantized"] = q.reshape(h, w, 3)
+        return out
 
     def time_pipeline(self, rgb, w, h, init_kind, k, seed, eps=1e-3, max_it=100, fixed_it=0):
         rgb = np.ascontiguousarray(rgb, np.uint8).reshape(-1)

@@ -183,14 +183,31 @@ int ref_map_pixels(const std::uint8_t *rgb, int w, int h, const double *pal, int
 // with image name `name` and time_ms forced to 0 (bench zero_time, bench.cpp:87).
 // stage_s (nullable, 4 doubles) receives histogram / init / wsm / map seconds
 // measured by re-running the public stages separately (bench cpu baseline).
+int ref_run_quantize_s(const std::uint8_t *rgb, int w, int h, const char *method, int k,
+                       std::uint64_t seed, double eps, int max_it, int fixed_it, const char *name,
+                       int run, double *palette, int *k_actual, int *iters, double *ndc_ppi,
+                       double *mse, double *time_ms, char *csv, std::uint32_t *indices,
+                       std::uint8_t *quant, const char *sampling);
+
 int ref_run_quantize(const std::uint8_t *rgb, int w, int h, const char *method, int k,
                      std::uint64_t seed, double eps, int max_it, int fixed_it, const char *name,
                      int run, double *palette, int *k_actual, int *iters, double *ndc_ppi,
                      double *mse, double *time_ms, char *csv, std::uint32_t *indices,
                      std::uint8_t *quant) {
+    return ref_run_quantize_s(rgb, w, h, method, k, seed, eps, max_it, fixed_it, name, run, palette, k_actual,
+                              iters, ndc_ppi, mse, time_ms, csv, indices, quant, "unique");
+}
+
+// run_quantize with QuantizeConfig::sampling given by its token (none|2to1|unique|both)
+int ref_run_quantize_s(const std::uint8_t *rgb, int w, int h, const char *method, int k,
+                       std::uint64_t seed, double eps, int max_it, int fixed_it, const char *name,
+                       int run, double *palette, int *k_actual, int *iters, double *ndc_ppi,
+                       double *mse, double *time_ms, char *csv, std::uint32_t *indices,
+                       std::uint8_t *quant, const char *sampling) {
     try {
         RawImage img = make_image(rgb, w, h);
         QuantizeConfig cfg;
+        cfg.sampling = parse_sampling_mode(sampling ? sampling : "unique");
         cfg.method = parse_method(method);
         cfg.k = k;
         cfg.seed = seed;

@@ -54,7 +54,7 @@ class LloydStats(C.Structure):
 
 class QuantizeCfg(C.Structure):
     _fields_ = [("init_kind", C.c_int), ("k", C.c_int), ("seed", C.c_uint64), ("term", Term),
-                ("index_bytes", C.c_int)]
+                ("index_bytes", C.c_int), ("sampling", C.c_int), ("width", C.c_int), ("height", C.c_int)]
 
 
 class QuantizeStats(C.Structure):

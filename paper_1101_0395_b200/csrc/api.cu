@@ -239,7 +239,8 @@ void cqg_destroy(cqg_ctx *ctx) {
                       &ctx->status, &ctx->sizes, &ctx->red, &ctx->hist_labels, &ctx->hist_centers,
                       &ctx->sse, &ctx->lut, &ctx->idx_out, &ctx->q_out, &ctx->mom_map, &ctx->mind2,
                       &ctx->initpart, &ctx->initsel, &ctx->unit_draws, &ctx->mom_g, &ctx->partial,
-                      &ctx->bnd, &ctx->shift, &ctx->dcode};
+                      &ctx->bnd, &ctx->shift, &ctx->dcode, &ctx->sub_img, &ctx->raw_col, &ctx->raw_cnt,
+                      &ctx->full_col, &ctx->full_cnt};
     for (DevBuf *b : bufs) b->release();
     ctx->pinned.release();
     for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
@@ -522,12 +523,28 @@ int cqg_quantize(cqg_ctx *ctx, const uint8_t *rgb, uint64_t P, const cqg_quantiz
         if (!palette) fail(CQG_E_INVALID, "run_quantize: null palette output");
         const int ib = cfg->index_bytes == 1 ? 1 : 4;
         if (ib == 1 && k > 256) fail(CQG_E_INVALID, "map_pixels: 8-bit indices need k <= 256");
+        const int mode = cfg->sampling;
+        if (mode < CQG_SAMPLING_UNIQUE || mode > CQG_SAMPLING_BOTH)
+            fail(CQG_E_INVALID, "run_quantize: unknown sampling mode");
+        const bool sub = mode == CQG_SAMPLING_TWO_TO_ONE || mode == CQG_SAMPLING_BOTH; // pipeline.cpp:91-92
+        const bool dedup = mode == CQG_SAMPLING_UNIQUE || mode == CQG_SAMPLING_BOTH;   // pipeline.cpp:93-94
+        if (sub && (cfg->width < 1 || cfg->height < 1 || (uint64_t)cfg->width * cfg->height != P))
+            fail(CQG_E_INVALID, "run_quantize: 2:1 sampling needs width * height == pixel count");
         Timer tm(ctx, stats != nullptr);
-        const uint64_t cap = P < (1ull << 24) ? P : (1ull << 24);
         const uint8_t *rgb_d = static_cast<const uint8_t *>(stage_in(ctx, rgb, P * 3, ctx->img));
+        // the sampled pixels (S of them) and their histogram (initialisers, dedup substrate)
+        const uint8_t *smp_d = rgb_d;
+        uint64_t S = P;
+        if (sub) {
+            S = (uint64_t)((cfg->width + 1) / 2) * ((cfg->height + 1) / 2);
+            uint8_t *o = static_cast<uint8_t *>(ctx->sub_img.ensure(3 * S + 16));
+            subsample_2to1_dev(ctx, rgb_d, cfg->width, cfg->height, o);
+            smp_d = o;
+        }
+        const uint64_t cap = S < (1ull << 24) ? S : (1ull << 24);
         uint32_t *col_d = static_cast<uint32_t *>(ctx->colors.ensure(cap * 4));
         uint32_t *cnt_d = static_cast<uint32_t *>(ctx->counts.ensure(cap * 4));
-        const uint64_t n = histogram_into(ctx, rgb_d, P, col_d, cnt_d, nullptr);
+        const uint64_t n = histogram_into(ctx, smp_d, S, col_d, cnt_d, nullptr);
         const double t_hist = tm.lap();
 
         double *init_d = static_cast<double *>(ctx->initsel.ensure(24 * (size_t)k + 64));
@@ -537,39 +554,62 @@ int cqg_quantize(cqg_ctx *ctx, const uint8_t *rgb, uint64_t P, const cqg_quantiz
         } else {
             validate_k_init(k, n);
             double *tmp = static_cast<double *>(ctx->hist_centers.ensure(24 * (size_t)k));
-            if (cfg->init_kind == CQG_INIT_MAXIMIN) init_maximin_dev(ctx, col_d, cnt_d, n, P, k, cfg->seed, 1, tmp);
-            else if (cfg->init_kind == CQG_INIT_KMEANSPP) init_kmeanspp_dev(ctx, col_d, cnt_d, n, P, k, cfg->seed, tmp);
+            if (cfg->init_kind == CQG_INIT_MAXIMIN) init_maximin_dev(ctx, col_d, cnt_d, n, S, k, cfg->seed, 1, tmp);
+            else if (cfg->init_kind == CQG_INIT_KMEANSPP) init_kmeanspp_dev(ctx, col_d, cnt_d, n, S, k, cfg->seed, tmp);
             else fail(CQG_E_INVALID, "run_quantize: unknown initializer kind");
             CQG_CUDA(cudaMemcpyAsync(init_d, tmp, 24 * (size_t)k, cudaMemcpyDeviceToDevice, ctx->stream));
         }
         const double t_init = tm.lap();
 
+        // substrate: the distinct colours (count weights) or every sampled pixel (count 1, weight 1/S)
+        const uint32_t *sub_col = col_d, *sub_cnt = cnt_d;
+        uint64_t ns = n;
+        if (!dedup) {
+            uint32_t *rc = static_cast<uint32_t *>(ctx->raw_col.ensure(S * 4 + 16));
+            uint32_t *rn = static_cast<uint32_t *>(ctx->raw_cnt.ensure(S * 4 + 16));
+            pack_pixels_dev(ctx, smp_d, S, rc, rn);
+            sub_col = rc;
+            sub_cnt = rn;
+            ns = S;
+        }
         cqg_term term = cfg->term;
         term.record_history = 0;
-        validate_run(n, k, term);
-        uint32_t *lab_d = static_cast<uint32_t *>(ctx->labels.ensure(cap * 4));
+        validate_run(ns, k, term);
+        uint32_t *lab_d = static_cast<uint32_t *>(ctx->labels.ensure((ns > cap ? ns : cap) * 4));
         double *cen_d = static_cast<double *>(ctx->cen.ensure(24 * (size_t)k));
         const int limit = term.fixed_iterations > 0 ? term.fixed_iterations : term.max_iterations;
         double *sse_h = static_cast<double *>(ctx->pinned.ensure(4096 + 8 * (size_t)limit)) + 512;
-        LloydOut o = lloyd_dev(ctx, col_d, cnt_d, n, P, init_d, k, term, lab_d, cen_d, sse_h, nullptr, nullptr);
+        LloydOut o = lloyd_dev(ctx, sub_col, sub_cnt, ns, S, init_d, k, term, lab_d, cen_d, sse_h, nullptr, nullptr);
         if (sse_trace) std::memcpy(sse_trace, sse_h, 8 * (size_t)o.iterations);
         const double t_lloyd = tm.lap();
 
+        // mapping over the full image needs its distinct colours: the histogram
+        // above unless the image was subsampled
+        const uint32_t *map_col = col_d, *map_cnt = cnt_d;
+        uint64_t nm = n;
+        if (sub) {
+            const uint64_t capf = P < (1ull << 24) ? P : (1ull << 24);
+            uint32_t *fc = static_cast<uint32_t *>(ctx->full_col.ensure(capf * 4));
+            uint32_t *fn = static_cast<uint32_t *>(ctx->full_cnt.ensure(capf * 4));
+            nm = histogram_into(ctx, rgb_d, P, fc, fn, nullptr);
+            map_col = fc;
+            map_cnt = fn;
+        }
         void *idx_d = indices ? out_buf<uint8_t>(indices, ctx->idx_out, P * (size_t)ib) : nullptr;
         uint8_t *q_d = quantized ? out_buf<uint8_t>(quantized, ctx->q_out, P * 3) : nullptr;
-        const double mse = map_dev(ctx, rgb_d, P, col_d, cnt_d, n, cen_d, k, idx_d, ib, q_d);
+        const double mse = map_dev(ctx, rgb_d, P, map_col, map_cnt, nm, cen_d, k, idx_d, ib, q_d);
         copy_out(ctx, palette, cen_d, 24 * (size_t)k);
-        copy_out(ctx, labels, lab_d, 4 * n);
+        copy_out(ctx, labels, lab_d, 4 * ns);
         copy_out(ctx, indices, idx_d, P * (size_t)ib);
         copy_out(ctx, quantized, q_d, P * 3);
         CQG_CUDA(cudaStreamSynchronize(ctx->stream));
         const double t_map = tm.lap();
         if (stats) {
-            stats->n_unique = n;
+            stats->n_unique = ns;
             stats->lloyd.iterations = o.iterations;
             stats->lloyd.repair_count = o.repairs;
             stats->lloyd.ndc_total = o.ndc;
-            stats->lloyd.n_points = n;
+            stats->lloyd.n_points = ns;
             stats->lloyd.flagged_total = o.flagged;
             stats->lloyd.swept_total = o.swept;
             stats->mean_sq_dist = mse;

@@ -121,7 +121,8 @@ struct cqg_ctx {
     // Lloyd state
     cqg::DevBuf labels, cen, fcen, dtab, dsorted, order, mom, queue, ndc, status, sizes, red;
     cqg::DevBuf hist_labels, hist_centers, sse;
-    cqg::DevBuf bnd, shift, dcode;     // distance-bound pruning: per-point (ub, lb), centre moves
+    cqg::DevBuf bnd, shift, dcode;
+    cqg::DevBuf sub_img, raw_col, raw_cnt, full_col, full_cnt; // sampling modes     // distance-bound pruning: per-point (ub, lb), centre moves
     cqg::DevBuf mom_g, partial; // sharded Lloyd: global moments, packed partials
     void *shard = nullptr;      // cqg::ShardState (lloyd.cu)
     // mapping
@@ -250,6 +251,8 @@ int shard_end_dev(cqg_ctx *ctx, double *centers_user, uint32_t *labels_user, dou
 void shard_release(cqg_ctx *ctx);
 int shard_k(cqg_ctx *ctx);
 uint64_t shard_n(cqg_ctx *ctx);
+void subsample_2to1_dev(cqg_ctx *ctx, const uint8_t *rgb_d, int w, int h, uint8_t *out_d);
+void pack_pixels_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t S, uint32_t *colors_d, uint32_t *counts_d);
 double map_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P, const uint32_t *colors_d,
                const uint32_t *counts_d, uint64_t n, const double *pal_d, int k, void *indices_d,
                int index_bytes, uint8_t *quant_d);

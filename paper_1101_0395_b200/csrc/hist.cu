@@ -277,6 +277,28 @@ __global__ void __launch_bounds__(kThreads) scan_words(const uint32_t *__restric
     }
 }
 
+// subsample_2to1 (histogram.cpp:60-67): pixels at even (x, y), row-major
+__global__ void subsample_kernel(const uint8_t *__restrict__ rgb, int w, int h, uint8_t *__restrict__ out) {
+    const int ws = (w + 1) / 2, hs = (h + 1) / 2;
+    const uint64_t S = (uint64_t)ws * hs;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < S; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t y = i / ws, x = i - y * ws;
+        const uint64_t src = 3 * (2 * y * (uint64_t)w + 2 * x);
+        out[3 * i] = rgb[src];
+        out[3 * i + 1] = rgb[src + 1];
+        out[3 * i + 2] = rgb[src + 2];
+    }
+}
+
+// raw substrate (pipeline.cpp:103-108): every sampled pixel is a point of count 1
+__global__ void pack_kernel(const uint8_t *__restrict__ rgb, uint64_t S, uint32_t *__restrict__ colors,
+                            uint32_t *__restrict__ counts) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < S; i += (uint64_t)gridDim.x * blockDim.x) {
+        colors[i] = ((uint32_t)rgb[3 * i] << 16) | ((uint32_t)rgb[3 * i + 1] << 8) | rgb[3 * i + 2];
+        counts[i] = 1u;
+    }
+}
+
 } // namespace
 
 void histogram_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P, uint32_t *colors_d,
@@ -333,6 +355,23 @@ void histogram_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P, uint32_t *col
     prof_end(ctx, CQG_PROF_HIST, pb, 3.0 * (double)P); // + 8 N' added by the caller
     CQG_CUDA(cudaGetLastError());
     launched(ctx, large ? 7 : 6);
+}
+
+void subsample_2to1_dev(cqg_ctx *ctx, const uint8_t *rgb_d, int w, int h, uint8_t *out_d) {
+    const uint64_t S = (uint64_t)((w + 1) / 2) * ((h + 1) / 2);
+    unsigned grid = ceil_div(S, kThreads);
+    if (grid > (unsigned)ctx->num_sms * 8) grid = ctx->num_sms * 8;
+    subsample_kernel<<<grid ? grid : 1, kThreads, 0, ctx->stream>>>(rgb_d, w, h, out_d);
+    CQG_CUDA(cudaGetLastError());
+    launched(ctx);
+}
+
+void pack_pixels_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t S, uint32_t *colors_d, uint32_t *counts_d) {
+    unsigned grid = ceil_div(S, kThreads);
+    if (grid > (unsigned)ctx->num_sms * 8) grid = ctx->num_sms * 8;
+    pack_kernel<<<grid ? grid : 1, kThreads, 0, ctx->stream>>>(rgb_d, S, colors_d, counts_d);
+    CQG_CUDA(cudaGetLastError());
+    launched(ctx);
 }
 
 } // namespace cqg

@@ -529,8 +529,6 @@ std::vector<std::string> all_method_tokens() {
 QuantizeResult run_quantize(const RawImage &image, const QuantizeConfig &config) { // pipeline.cpp:81-164
     if (image.pixels.empty()) throw std::invalid_argument("run_quantize: empty image");
     if (config.k < 1) throw std::invalid_argument("run_quantize: k must be at least 1");
-    if (config.sampling != SamplingMode::Unique)
-        throw std::invalid_argument("run_quantize: the device path implements sampling 'unique' only");
     if (!config.method.refine)
         throw std::invalid_argument("run_quantize: standalone preclusterers are outside the device path");
     const auto t0 = std::chrono::steady_clock::now();
@@ -544,6 +542,14 @@ QuantizeResult run_quantize(const RawImage &image, const QuantizeConfig &config)
     co.term = config.term;
     cfg.term = to_term(co);
     cfg.index_bytes = 4;
+    switch (config.sampling) { // pipeline.cpp:91-116
+        case SamplingMode::None: cfg.sampling = CQG_SAMPLING_NONE; break;
+        case SamplingMode::TwoToOne: cfg.sampling = CQG_SAMPLING_TWO_TO_ONE; break;
+        case SamplingMode::TwoToOneUnique: cfg.sampling = CQG_SAMPLING_BOTH; break;
+        default: cfg.sampling = CQG_SAMPLING_UNIQUE; break;
+    }
+    cfg.width = image.width;
+    cfg.height = image.height;
     std::vector<double> init;
     if (!config.init_centers.empty()) {
         if (static_cast<int>(config.init_centers.size()) != k)
@@ -560,7 +566,7 @@ QuantizeResult run_quantize(const RawImage &image, const QuantizeConfig &config)
     }
     const int limit = cfg.term.fixed_iterations > 0 ? cfg.term.fixed_iterations : cfg.term.max_iterations;
     std::vector<double> pal(3 * static_cast<std::size_t>(k));
-    std::vector<std::uint32_t> labels(std::min<std::size_t>(P, 1u << 24));
+    std::vector<std::uint32_t> labels(P); // the substrate: <= 2^24 colours, or every sampled pixel
     std::vector<double> sse(std::max(limit, 1));
     out.mapping.indices.resize(P);
     out.mapping.quantized.width = image.width;

@@ -74,6 +74,10 @@ class RawImage:
 SAMPLING_TOKENS = {"none": "None", "2to1": "TwoToOne", "unique": "Unique", "both": "TwoToOneUnique"}
 
 
+# QuantizeConfig::sampling -> CQG_SAMPLING_* (include/cqg.h)
+SAMPLING_CODES = {"unique": 0, "none": 1, "2to1": 2, "both": 3}
+
+
 def parse_sampling_mode(token: str) -> str:
     """histogram.cpp:19-26."""
     if token not in SAMPLING_TOKENS:
@@ -456,8 +460,9 @@ class QuantizeResult:
 
 def run_quantize(image, config: QuantizeConfig, ctx: Optional[cabi.Context] = None) -> QuantizeResult:
     """quant::run_quantize (pipeline.hpp:53, pipeline.cpp:81-164) for the
-    device path: sampling 'unique', refined methods wsm-mmx / wsm-kpp, or any
-    wsm-<x> whose initial centres are supplied in ``config.init_centers``."""
+    device path: every sampling mode (none | 2to1 | unique | both), refined
+    methods wsm-mmx / wsm-kpp, or any wsm-<x> whose initial centres are supplied
+    in ``config.init_centers``."""
     ctx = ctx or cabi.default_context()
     arr, w, h = _pixels(image)
     P = w * h
@@ -465,8 +470,7 @@ def run_quantize(image, config: QuantizeConfig, ctx: Optional[cabi.Context] = No
         raise ValueError("run_quantize: empty image")
     if config.k < 1:
         raise ValueError("run_quantize: k must be at least 1")
-    if config.sampling != "unique":
-        raise ValueError("run_quantize: the device path implements sampling 'unique' only")
+    sampling = SAMPLING_CODES[parse_sampling_mode(config.sampling)]
     if not config.method.refine:
         raise ValueError("run_quantize: standalone preclusterers are outside the device path")
     k = int(config.k)
@@ -482,11 +486,10 @@ def run_quantize(image, config: QuantizeConfig, ctx: Optional[cabi.Context] = No
         raise ValueError(f"run_quantize: initializer '{config.method.base}' is outside the device "
                          "path; pass config.init_centers")
     term = _term_struct(config.term, False)
-    cfg = cabi.QuantizeCfg(kind, k, int(config.seed), term, int(config.index_bytes))
+    cfg = cabi.QuantizeCfg(kind, k, int(config.seed), term, int(config.index_bytes), sampling, w, h)
     limit = term.fixed_iterations if term.fixed_iterations > 0 else term.max_iterations
     palette = np.empty((k, 3), np.float64)
-    cap = min(P, 1 << 24)
-    labels = np.empty(cap, np.uint32)
+    labels = np.empty(P, np.uint32)  # the substrate: <= 2^24 colours, or every sampled pixel
     sse = np.zeros(limit, np.float64)
     idx = np.empty(P, np.uint8 if config.index_bytes == 1 else np.uint32)
     q = np.empty((h, w, 3), np.uint8)

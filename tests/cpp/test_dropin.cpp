@@ -183,6 +183,43 @@ static void case_report_format() { // test_metrics.cpp:94-125
     CHECK(r.to_json().find("\"psnr\": 29.603") != std::string::npos);
 }
 
+static void case_sampling_substrates() { // test_pipeline.cpp:106-134: the substrate per sampling mode
+    RawImage img;
+    img.width = 50;
+    img.height = 40;
+    img.pixels.resize(50 * 40);
+    std::uint32_t st = 33;
+    for (auto &p : img.pixels) { // a few repeated colours plus noise
+        st = st * 1664525u + 1013904223u;
+        const int c = (st >> 28) & 7;
+        p = Rgb8{static_cast<std::uint8_t>(30 * c), static_cast<std::uint8_t>(200 - 20 * c),
+                 static_cast<std::uint8_t>((st >> 16) & ((st >> 27) & 1 ? 255 : 3))};
+    }
+    QuantizeConfig cfg;
+    cfg.method = parse_method("wsm-mmx");
+    cfg.k = 16;
+    cfg.sampling = SamplingMode::None;
+    const QuantizeResult none = run_quantize(img, cfg);
+    CHECK(none.substrate_points == img.pixels.size());
+    CHECK(none.state.memberships.size() == img.pixels.size());
+    cfg.sampling = SamplingMode::TwoToOne;
+    const QuantizeResult half = run_quantize(img, cfg);
+    CHECK(half.substrate_points == 25 * 20);
+    cfg.sampling = SamplingMode::Unique;
+    const QuantizeResult uniq = run_quantize(img, cfg);
+    CHECK(uniq.substrate_points == build_histogram(img.pixels, cfg.seed).size());
+    CHECK(uniq.substrate_points < img.pixels.size());
+    cfg.sampling = SamplingMode::TwoToOneUnique;
+    const QuantizeResult both = run_quantize(img, cfg);
+    CHECK(both.substrate_points <= half.substrate_points);
+    for (const QuantizeResult *r : {&none, &half, &uniq, &both}) {
+        CHECK(r->palette.size() == 16);
+        CHECK(r->report.mse > 0.0);
+        CHECK(r->mapping.indices.size() == img.pixels.size());
+    }
+    CHECK(std::string(sampling_mode_token(both.report.sampling)) == "both");
+}
+
 int main(int argc, char **argv) {
     const std::string dir = argc > 1 ? argv[1] : "tests/golden";
     struct Case {
@@ -192,7 +229,8 @@ int main(int argc, char **argv) {
                  {"wsm_semantics", case_wsm_semantics},
                  {"histogram_equals_duplicates", case_histogram_equals_duplicates},
                  {"mapping", case_mapping},
-                 {"report_format", case_report_format}};
+                 {"report_format", case_report_format},
+                 {"sampling_substrates", case_sampling_substrates}};
     for (const auto &c : cases) {
         const int before = g_fail;
         try {
