@@ -263,7 +263,7 @@ def run_sharded(args, cfg, ctx, dev, world, rank, stream):
     def step():
         n = ctx.histogram_raw(d_img, P, d_col, d_cnt)
         ctx.init_raw(kind, d_col, d_cnt, n, P, K, cfg.seed, d_init)
-        r = parallel.sharded_wsm(eng, d_col[:n], d_cnt[:n], P, d_init, K, term)
+        r = parallel.sharded_wsm(eng, d_col[:n], d_cnt[:n], P, d_init, K, term, labels=False)
         pal = np.ascontiguousarray(r.centers)
         if r1 > r0:
             ctx.map_raw(d_img[r0:r1], (r1 - r0) * W, pal, K, d_idx, 4, d_q)
@@ -315,17 +315,28 @@ def run_ours(args, cfg):
     world = env_int("WORLD_SIZE", 1)
     rank = env_int("RANK", 0)
     local = env_int("LOCAL_RANK", 0)
+    # test hook for the multi-rank logic on a one-GPU box: every rank on device 0,
+    # gloo instead of NCCL (NCCL refuses two ranks on one device). Not a bench mode.
+    share = os.environ.get("CQG_BENCH_SHARE_DEVICE") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
     ctx = cabi.Context(local)
     ctx.set_stream(stream.cuda_stream)
     if args.sharded or (world > 1 and cfg.images == 1 and cfg.name in ("cfg5", "cfg3", "cfg3k64")):
         if world == 1:
-            dist.init_process_group("nccl", rank=0, world_size=1, init_method="tcp://127.0.0.1:29533",
-                                    device_id=torch.device("cuda", local))
+            if share:
+                dist.init_process_group("gloo", rank=0, world_size=1, init_method="tcp://127.0.0.1:29533")
+            else:
+                dist.init_process_group("nccl", rank=0, world_size=1, init_method="tcp://127.0.0.1:29533",
+                                        device_id=torch.device("cuda", local))
         rc = run_sharded(args, cfg, ctx, dev, world, rank, stream)
         dist.destroy_process_group()
         ctx.close()

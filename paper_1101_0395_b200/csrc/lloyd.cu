@@ -1132,9 +1132,19 @@ void shard_begin_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *cou
     int *iter_dev = reinterpret_cast<int *>(qn + 12);
     IterStatus *st = reinterpret_cast<IterStatus *>(qn + 16);
     unsigned long long *ndc_unused = reinterpret_cast<unsigned long long *>(qn + 24);
+    unsigned long long *swept = reinterpret_cast<unsigned long long *>(qn + 32);
+    int *shift_inval = reinterpret_cast<int *>(qn + 36);
+    // distance-bound pruning and the NDC code table, as in lloyd_dev: every rank
+    // finalises identically, so every rank computes the same centre shifts
+    const bool prune = ctx->use_prune;
+    float2 *bnd = prune && n ? static_cast<float2 *>(ctx->bnd.ensure(sizeof(float2) * (n + 1))) : nullptr;
+    float *shift = prune ? static_cast<float *>(ctx->shift.ensure(sizeof(float) * ((size_t)K + 4))) : nullptr;
+    uint16_t *dcode = K <= kNdcCodeMaxK && ctx->use_ndc_code
+                          ? static_cast<uint16_t *>(ctx->dcode.ensure(sizeof(uint16_t) * (size_t)K * Kpow + 16))
+                          : nullptr;
     double *sse_d = static_cast<double *>(ctx->sse.ensure(sizeof(double) * (size_t)(S.limit + 1)));
     CQG_CUDA(cudaMemsetAsync(mom, 0, sizeof(Moments) * (size_t)K, s));
-    CQG_CUDA(cudaMemsetAsync(qn, 0, 128, s));
+    CQG_CUDA(cudaMemsetAsync(qn, 0, 160, s));
     fc_kernel<<<1, 256, 0, s>>>(cen, K, Kp, fc, fc + 4 * Kp);
     launched(ctx);
     SweepArgs &a = S.a;
@@ -1156,8 +1166,15 @@ void shard_begin_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *cou
     a.K = K;
     a.Kp = Kp;
     a.Kpow = Kpow;
+    a.bnd = bnd;
+    a.shift = shift;
+    a.swept = swept;
+    a.dcode = dcode;
     IterArgs &ia = S.ia;
     ia = IterArgs{};
+    ia.shift = shift;
+    ia.shift_inval = shift_inval;
+    ia.dcode = dcode;
     ia.mom = mom_g;
     ia.cen = cen;
     ia.K = K;
@@ -1262,9 +1279,11 @@ void shard_move_dev(cqg_ctx *ctx, uint64_t index, int e, uint32_t colour) {
     if (index < S.n) {
         uint32_t *sizes = static_cast<uint32_t *>(ctx->sizes.ensure((size_t)S.K * 4));
         apply_move_kernel<<<1, 32, 0, s>>>(S.a.colors, S.a.counts, S.a.labels, S.ia.cen, S.a.mom, sizes, index, e,
-                                            nullptr);
+                                            S.ia.shift_inval);
     } else {
         set_centre_kernel<<<1, 32, 0, s>>>(S.ia.cen, e, colour);
+        // the centres moved outside the bounds' bookkeeping on this rank too
+        if (S.ia.shift_inval) CQG_CUDA(cudaMemsetAsync(S.ia.shift_inval, 0x01, 1, s));
     }
     launched(ctx);
     CQG_CUDA(cudaGetLastError());

@@ -92,14 +92,15 @@ class CudaShardEngine:
         idx = (1 << 64) - 1 if local_index is None else int(local_index)
         cabi.check(self.ctx.L.cqg_shard_move(self.ctx.h, idx, int(e), int(colour)))
 
-    def end(self, limit):
+    def end(self, limit, labels=True):
         K = self.K
         cen = np.empty((K, 3), np.float64)
-        lab = np.empty(max(self.n, 1), np.uint32)
+        lab = np.empty(max(self.n, 1), np.uint32) if labels else None
         sse = np.zeros(max(limit, 1), np.float64)
         it = C.c_int(0)
-        cabi.check(self.ctx.L.cqg_shard_end(self.ctx.h, cabi.ptr(cen), cabi.ptr(lab), cabi.ptr(sse), C.byref(it)))
-        return cen, lab[: self.n].copy(), sse[: it.value].copy(), it.value
+        cabi.check(self.ctx.L.cqg_shard_end(self.ctx.h, cabi.ptr(cen), cabi.ptr(lab) if labels else None,
+                                            cabi.ptr(sse), C.byref(it)))
+        return cen, (lab[: self.n] if labels else None), sse[: it.value].copy(), it.value
 
 
 @dataclass
@@ -155,9 +156,11 @@ def _repair(engine, lo: int, K: int, dist, group, torch) -> int:
         repairs += 1
 
 
-def sharded_wsm(engine, colors, counts, P: int, init, K: int, term: cabi.Term, group=None) -> ShardedResult:
+def sharded_wsm(engine, colors, counts, P: int, init, K: int, term: cabi.Term, group=None,
+                labels: bool = True) -> ShardedResult:
     """Weighted sort-means over the unique colours sharded across the ranks of
-    `group`; every rank returns the same centres / trace and its own labels."""
+    `group`; every rank returns the same centres / trace and its own labels
+    (labels=False leaves them on the device: labels_local is None)."""
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group)
@@ -180,5 +183,5 @@ def sharded_wsm(engine, colors, counts, P: int, init, K: int, term: cabi.Term, g
         if state == STATE_DONE:
             break
     limit = term.fixed_iterations if term.fixed_iterations > 0 else term.max_iterations
-    cen, lab, sse, it = engine.end(limit)
+    cen, lab, sse, it = engine.end(limit, labels)
     return ShardedResult(cen, lab, lo, hi, sse, it, ndc, repairs, flagged)

@@ -123,5 +123,5 @@ class NumpyShardEngine:
             self.labels[li] = e
         self.c[e] = [(colour >> 16) & 255, (colour >> 8) & 255, colour & 255]
 
-    def end(self, limit):
-        return self.c.copy(), self.labels.astype(np.uint32), np.array(self.sse), self.iter
+    def end(self, limit, labels=True):
+        return (self.c.copy(), self.labels.astype(np.uint32) if labels else None, np.array(self.sse), self.iter)
