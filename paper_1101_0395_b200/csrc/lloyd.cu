@@ -1321,3 +1321,14 @@ extern "C" int cqg_dbg_block_timing(unsigned long long *out, int reset) {
     return 0;
 }
 #endif
+
+#ifdef CQG_SWEEP_TIMING
+extern "C" int cqg_dbg_sweep_timing(unsigned long long *out, int reset) {
+    if (cudaMemcpyFromSymbol(out, cqg::g_sweep_timing, 4 * sizeof(unsigned long long)) != cudaSuccess) return 1;
+    if (reset) {
+        unsigned long long z[4] = {};
+        cudaMemcpyToSymbol(cqg::g_sweep_timing, z, sizeof(z));
+    }
+    return 0;
+}
+#endif

@@ -571,6 +571,9 @@ __device__ __forceinline__ void sweep_tiles(const SweepArgs &a, uint64_t lo, uin
     }
 }
 
+#ifdef CQG_SWEEP_TIMING
+__device__ unsigned long long g_sweep_timing[4]; // block 0: filter cycles, phase cycles, survivors, calls
+#endif
 // Points per block-local chunk of the pruned WALK sweep (shared-memory list).
 constexpr int kPruneChunk = 4096;
 constexpr float kBoundMargin = 1.0e-3f; // Euclidean gap that keeps the FP64 reference order
@@ -646,6 +649,9 @@ __device__ __forceinline__ void sweep_range(const SweepArgs &a, uint64_t lo, uin
     unsigned long long swept = 0;
     if (threadIdx.x == 0) s_m = 0;
     __syncthreads();
+#ifdef CQG_SWEEP_TIMING
+    unsigned long long _st0 = clock64(), _sf = 0;
+#endif
     for (uint64_t cb = lo; cb < hi; cb += list_cap) {
         const uint64_t ce = cb + list_cap < hi ? cb + list_cap : hi;
         for (uint64_t i0 = cb; i0 < ce; i0 += (uint64_t)blockDim.x * kFilterPPT) {
@@ -675,6 +681,9 @@ __device__ __forceinline__ void sweep_range(const SweepArgs &a, uint64_t lo, uin
             }
         }
         __syncthreads();
+#ifdef CQG_SWEEP_TIMING
+        _sf += clock64() - _st0;
+#endif
         const uint32_t m = s_m;
         const uint32_t mb = m / big * big;
         if (mb) {
@@ -692,6 +701,14 @@ __device__ __forceinline__ void sweep_range(const SweepArgs &a, uint64_t lo, uin
     if (rest) sweep_tiles<MODE_WALK, 2, true>(a, 0, rest, s_list, smem, s_acc, tau_abs, tau_rel);
     swept += rest;
     __syncthreads();
+#ifdef CQG_SWEEP_TIMING
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        g_sweep_timing[0] += _sf;
+        g_sweep_timing[1] += clock64() - _st0;
+        g_sweep_timing[2] += swept;
+        g_sweep_timing[3] += 1;
+    }
+#endif
     if (threadIdx.x == 0 && a.swept && swept) atomicAdd(a.swept, swept);
 }
 

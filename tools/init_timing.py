@@ -71,6 +71,8 @@ def run(name):
     quant.wsm_hist(hist, init, opts, ctx=ctx)
     L.cqg_dbg_lloyd_timing(buf, 1)
     L.cqg_dbg_block_timing((C.c_ulonglong * (1024 * 3))(), 1)
+    if hasattr(L, "cqg_dbg_sweep_timing"):
+        L.cqg_dbg_sweep_timing((C.c_ulonglong * 4)(), 1)
     st = None
     for _ in range(reps):
         st = quant.wsm_hist(hist, init, opts, ctx=ctx)
@@ -94,6 +96,12 @@ def run(name):
         print(f"{nm:14s} {buf[i] / its:8.0f} cycles/iter  {100 * buf[i] / tot:5.1f}%")
     print(f"{'total':14s} {tot / its:8.0f} cycles/iter  (swept {st.swept_total / (st.iterations * len(hist.counts)):.3f})")
     print(f"  iter_end: centres+status+fc {buf[6] / its:8.0f}  whole body {buf[7] / its:8.0f} cycles/iter")
+    if hasattr(L, "cqg_dbg_sweep_timing"):
+        sb = (C.c_ulonglong * 4)()
+        L.cqg_dbg_sweep_timing(sb, 0)
+        calls = max(sb[3], 1)
+        print(f"  pruned sweep (block 0): filter {sb[0] / calls:8.0f}  whole {sb[1] / calls:8.0f} cycles/call, "
+              f"survivors {sb[2] / calls:6.0f}")
 
 
 if __name__ == "__main__":
