@@ -506,6 +506,7 @@ def run_ours(args, cfg):
                              "is the dense N'.K launch"),
         "avg_launch_ms": k_ms,
         "launch_share_of_step": k_share,
+        "concurrent_streams": nworkers,  # > 1: shares sum device time over concurrent streams
         "sweep_isolated": {"ms_per_launch": iso_ms, "achieved": iso_achieved,
                            "frac": iso_achieved / fp32_peak, "units_per_launch": iso_units},
     }
@@ -524,8 +525,9 @@ def run_ours(args, cfg):
             "bound": "latency" if small else "hbm",
             "rounds": K0 - 1 if cfg.init == "kpp" else K0 - 1,
             "us_per_round": 1e3 * init_ms / max(K0 - 1, 1),
-            "note": ("a chain of K-1 dependent draws; per-round critical path (tools/init_timing.py): "
-                     "update ~31%, publish ~14%, cluster barrier ~13%, locate ~37%") if small else
+            "note": ("a chain of K-1 dependent draws, two cluster barriers each; per-round critical path "
+                     "(tools/init_timing.py): update ~32%, publish ~15%, first barrier ~13%, "
+                     "locate + second barrier ~33%") if small else
                     "8 B per point per round streamed; see DESIGN.md §8",
         }
     hist_ms = prof.ms[cabi.PROF_HIST]
