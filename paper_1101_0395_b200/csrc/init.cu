@@ -41,7 +41,7 @@ constexpr int kFix = 88;        // fixed-point fraction bits
 constexpr int kInitThreads = 256;
 constexpr int kSeg = 1024;      // points per segment (4 per thread)
 constexpr uint32_t kWeightsOnly = 0xFFFFFFFFu;
-constexpr int kLocateMax = 384; // block sums / segments one warp_locate scans (registers)
+constexpr int kLocateMax = 448; // block sums / segments one warp_locate scans (registers): 3 x 148 blocks
 
 struct InitArgs {
     const uint32_t *colors;
@@ -651,7 +651,7 @@ __device__ void update_rec(const InitArgs &a, bool full, uint32_t clast, uint2 *
 }
 
 template <class M>
-__global__ void __launch_bounds__(kInitThreads) init_kernel_rec(InitArgs a) {
+__global__ void __launch_bounds__(kInitThreads, 3) init_kernel_rec(InitArgs a) {
     cg::grid_group grid = cg::this_grid();
     __shared__ typename M::T s_w[kInitThreads / 32];
     __shared__ unsigned long long s_m[kInitThreads / 32];
@@ -1220,7 +1220,11 @@ void run_init(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *counts_d, 
     int occ = 0;
     CQG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kInitThreads, 0));
     if (occ < 1) occ = 1;
-    uint64_t grid = (uint64_t)ctx->num_sms * (uint64_t)(occ > 2 ? 2 : occ);
+    // k-means++ record rounds are load-latency bound: 3 blocks per SM (maximin
+    // measured faster with 2: one barrier per round, fewer arrivals)
+    const int per_want = rec && kind == 1 ? 3 : 2;
+    const int per_sm = occ > per_want ? per_want : occ;
+    uint64_t grid = (uint64_t)ctx->num_sms * (uint64_t)per_sm;
     if (grid > (uint64_t)kLocateMax) grid = kLocateMax; // warp_locate scans <= kLocateMax block sums
     const uint64_t want = (n + kSeg - 1) / kSeg;
     if (grid > want) grid = want;
