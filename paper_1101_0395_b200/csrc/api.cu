@@ -243,6 +243,7 @@ void cqg_destroy(cqg_ctx *ctx) {
                       &ctx->full_col, &ctx->full_cnt};
     for (DevBuf *b : bufs) b->release();
     ctx->pinned.release();
+    ctx->pinned_nu.release();
     for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
@@ -597,12 +598,14 @@ int cqg_quantize(cqg_ctx *ctx, const uint8_t *rgb, uint64_t P, const cqg_quantiz
         }
         void *idx_d = indices ? out_buf<uint8_t>(indices, ctx->idx_out, P * (size_t)ib) : nullptr;
         uint8_t *q_d = quantized ? out_buf<uint8_t>(quantized, ctx->q_out, P * 3) : nullptr;
-        const double mse = map_dev(ctx, rgb_d, P, map_col, map_cnt, nm, cen_d, k, idx_d, ib, q_d);
+        double *mse_h = static_cast<double *>(ctx->pinned.ensure(4096)) + 256; // bytes 2048.. (free here)
+        map_dev(ctx, rgb_d, P, map_col, map_cnt, nm, cen_d, k, idx_d, ib, q_d, mse_h);
         copy_out(ctx, palette, cen_d, 24 * (size_t)k);
         copy_out(ctx, labels, lab_d, 4 * ns);
         copy_out(ctx, indices, idx_d, P * (size_t)ib);
         copy_out(ctx, quantized, q_d, P * 3);
-        CQG_CUDA(cudaStreamSynchronize(ctx->stream));
+        CQG_CUDA(cudaStreamSynchronize(ctx->stream)); // the pipeline's last synchronisation
+        const double mse = *mse_h;
         const double t_map = tm.lap();
         if (stats) {
             stats->n_unique = ns;

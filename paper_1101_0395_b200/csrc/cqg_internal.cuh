@@ -130,6 +130,7 @@ struct cqg_ctx {
     // init
     cqg::DevBuf mind2, initpart, initsel, unit_draws;
     cqg::HostBuf pinned;   // status readback and small results
+    cqg::HostBuf pinned_nu; // initialiser unit draws (an async H2D source: no host-blocking copy)
 
     // cached CUDA graph of the Lloyd WHILE loop (lloyd.cu)
     bool use_graphs = true;
@@ -255,7 +256,8 @@ void subsample_2to1_dev(cqg_ctx *ctx, const uint8_t *rgb_d, int w, int h, uint8_
 void pack_pixels_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t S, uint32_t *colors_d, uint32_t *counts_d);
 double map_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P, const uint32_t *colors_d,
                const uint32_t *counts_d, uint64_t n, const double *pal_d, int k, void *indices_d,
-               int index_bytes, uint8_t *quant_d);
+               int index_bytes, uint8_t *quant_d,
+               double *mse_async = nullptr);
 
 void init_maximin_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *counts_d, uint64_t n,
                       uint64_t P, int k, uint64_t seed, int weighted_first, double *centers_d);

@@ -31,6 +31,8 @@
 
 #include "cqg_internal.cuh"
 
+#include <cstring>
+
 namespace cg = cooperative_groups;
 
 namespace cqg {
@@ -1194,7 +1196,9 @@ void run_init(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *counts_d, 
     const bool exact = (P & (P - 1)) == 0 && P <= (1ull << 32);
     if (ctx->use_cluster_init && n <= 16ull * kClusterThreads * 32) {
         double *nu_c = static_cast<double *>(ctx->unit_draws.ensure(sizeof(double) * nu.size()));
-        CQG_CUDA(cudaMemcpyAsync(nu_c, nu.data(), sizeof(double) * nu.size(), cudaMemcpyHostToDevice, s));
+        double *nu_h = static_cast<double *>(ctx->pinned_nu.ensure(sizeof(double) * nu.size()));
+        std::memcpy(nu_h, nu.data(), sizeof(double) * nu.size());
+        CQG_CUDA(cudaMemcpyAsync(nu_c, nu_h, sizeof(double) * nu.size(), cudaMemcpyHostToDevice, s));
         unsigned long long *resc = static_cast<unsigned long long *>(ctx->status.ensure(64));
         CQG_CUDA(cudaMemsetAsync(resc, 0, 64, s));
         InitArgs c{};
@@ -1235,7 +1239,9 @@ void run_init(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *counts_d, 
     if (chunk / kSeg > (uint64_t)kLocateMax) fail(CQG_E_RUNTIME, "init: too many segments per block");
     const uint64_t nseg = (n + kSeg - 1) / kSeg;
     double *nu_d = static_cast<double *>(ctx->unit_draws.ensure(sizeof(double) * nu.size()));
-    CQG_CUDA(cudaMemcpyAsync(nu_d, nu.data(), sizeof(double) * nu.size(), cudaMemcpyHostToDevice, s));
+    double *nu_h = static_cast<double *>(ctx->pinned_nu.ensure(sizeof(double) * nu.size()));
+    std::memcpy(nu_h, nu.data(), sizeof(double) * nu.size());
+    CQG_CUDA(cudaMemcpyAsync(nu_d, nu_h, sizeof(double) * nu.size(), cudaMemcpyHostToDevice, s));
     uint32_t *md = static_cast<uint32_t *>(ctx->mind2.ensure(sizeof(uint32_t) * 2 * n));
     const size_t part_bytes = sizeof(u128) * (2 * grid + 2 * nseg) + 8 * 2 * grid + 64;
     u128 *parts = static_cast<u128 *>(ctx->initpart.ensure(part_bytes));

@@ -923,7 +923,9 @@ LloydOut lloyd_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *count
     float2 *bnd = prune ? static_cast<float2 *>(ctx->bnd.ensure(sizeof(float2) * (n + 1))) : nullptr;
     float *shift = prune ? static_cast<float *>(ctx->shift.ensure(sizeof(float) * ((size_t)K + 4))) : nullptr;
     double *sse_d = static_cast<double *>(ctx->sse.ensure(sizeof(double) * (size_t)(limit + 1)));
-    IterStatus *hst = static_cast<IterStatus *>(ctx->pinned.ensure(4096));
+    // pinned read-back of scalar bytes 32..136: ndc, flagged, iter_dev, IterStatus (byte 64), swept (byte 128)
+    unsigned char *hsc = static_cast<unsigned char *>(ctx->pinned.ensure(4096));
+    IterStatus *hst = reinterpret_cast<IterStatus *>(hsc + 32);
     const bool hist = term.record_history && (hist_labels_user || hist_centers_user);
     uint32_t *hl_d = nullptr;
     double *hc_d = nullptr;
@@ -1026,7 +1028,9 @@ LloydOut lloyd_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *count
             }
             launch_iter_end(ctx, ia);
         }
-        CQG_CUDA(cudaMemcpyAsync(hst, st, sizeof(IterStatus), cudaMemcpyDeviceToHost, s));
+        // one read-back per launch: counters, status (scalars bytes 32..136) and the SSE trace
+        CQG_CUDA(cudaMemcpyAsync(hsc, reinterpret_cast<unsigned char *>(qn) + 32, 104, cudaMemcpyDeviceToHost, s));
+        if (sse_host) CQG_CUDA(cudaMemcpyAsync(sse_host, sse_d, sizeof(double) * (size_t)limit, cudaMemcpyDefault, s));
         CQG_CUDA(cudaStreamSynchronize(s));
         iter = hst->iteration;
         prof_add_units(ctx, rec, (double)n * (double)K * (double)(iter - before));
@@ -1035,7 +1039,8 @@ LloydOut lloyd_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *count
             IterArgs ib = ia;
             ib.reset_qn = persistent ? 1 : 0;
             launch_iter_end(ctx, ib);
-            CQG_CUDA(cudaMemcpyAsync(hst, st, sizeof(IterStatus), cudaMemcpyDeviceToHost, s));
+            CQG_CUDA(cudaMemcpyAsync(hsc, reinterpret_cast<unsigned char *>(qn) + 32, 104, cudaMemcpyDeviceToHost, s));
+            if (sse_host) CQG_CUDA(cudaMemcpyAsync(sse_host, sse_d, sizeof(double) * (size_t)limit, cudaMemcpyDefault, s));
             CQG_CUDA(cudaStreamSynchronize(s));
             if (hst->state == 2) fail(CQG_E_RUNTIME, "repair left an empty cluster");
             iter = hst->iteration;
@@ -1043,19 +1048,16 @@ LloydOut lloyd_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *count
         done = hst->state == 1;
     }
     out.iterations = iter;
-    CQG_CUDA(cudaMemcpyAsync(sse_host, sse_d, sizeof(double) * iter, cudaMemcpyDefault, s));
-    unsigned long long *hcnt = reinterpret_cast<unsigned long long *>(hst + 1);
-    CQG_CUDA(cudaMemcpyAsync(hcnt, ndc, 16, cudaMemcpyDeviceToHost, s));
-    CQG_CUDA(cudaMemcpyAsync(hcnt + 2, swept, 8, cudaMemcpyDeviceToHost, s));
     if (hist) {
         if (hist_labels_user) copy_out(ctx, hist_labels_user, hl_d, sizeof(uint32_t) * n * (size_t)iter);
         if (hist_centers_user) copy_out(ctx, hist_centers_user, hc_d, 24 * (size_t)K * iter);
+        CQG_CUDA(cudaStreamSynchronize(s));
     }
-    CQG_CUDA(cudaStreamSynchronize(s));
+    const unsigned long long *hcnt = reinterpret_cast<const unsigned long long *>(hsc); // ndc, flagged
     out.ndc = hcnt[0];
     out.flagged = hcnt[1];
     // FULL first iteration sweeps every point; WALK iterations count the survivors
-    out.swept = prune ? hcnt[2] + n : n * (unsigned long long)iter;
+    out.swept = prune ? hcnt[12] + n : n * (unsigned long long)iter; // swept: scalar byte 128
     return out;
 }
 

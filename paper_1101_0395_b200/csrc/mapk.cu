@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(256) pixel_kernel(const uint8_t *__restrict__ 
 
 double map_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P, const uint32_t *colors_d,
                const uint32_t *counts_d, uint64_t n, const double *pal_d, int K, void *indices_d,
-               int index_bytes, uint8_t *quant_d) {
+               int index_bytes, uint8_t *quant_d, double *mse_async) {
     cudaStream_t s = ctx->stream;
     const int Kp = (K + 7) & ~7;
     const bool lut8 = K <= 256;
@@ -214,6 +214,10 @@ double map_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P, const uint32_t *c
         launched(ctx);
     }
     CQG_CUDA(cudaGetLastError());
+    if (mse_async) { // the caller reads *mse_async after its own synchronisation
+        CQG_CUDA(cudaMemcpyAsync(mse_async, mse_d, 8, cudaMemcpyDeviceToHost, s));
+        return 0.0;
+    }
     double mse = 0.0;
     double *hm = static_cast<double *>(ctx->pinned.ensure(4096));
     CQG_CUDA(cudaMemcpyAsync(hm, mse_d, 8, cudaMemcpyDeviceToHost, s));
