@@ -108,6 +108,9 @@ def main():
             ubg = ubY[g] + delta[lab]
             st = ubg < lbg.min(1)
             st2 = st | (Dn[ar, lab] < lbg.min(1))
+            # with Elkan's half-nearest-centre test on top
+            ste = st2 | (ubg < s[lab]) | (Dn[ar, lab] < s[lab])
+            res.append(f"Y{g}+E {1 - ste.mean():.3f}")
             res.append(f"Y{g} {1 - st2.mean():.3f}")
             # update Y bounds: swept points recompute all; stayers keep lbg, ub tightened
             full = ~st2
