@@ -211,6 +211,8 @@ cqg_ctx *cqg_create(int device) {
         ctx->use_graphs = !(ng && ng[0] == '1');
         const char *nc = getenv("CQG_NO_CLUSTER_INIT");
         ctx->use_cluster_init = !(nc && nc[0] == '1');
+        const char *nm = getenv("CQG_NO_MBAR_INIT");
+        ctx->use_mbar_init = !(nm && nm[0] == '1');
         const char *cp = getenv("CQG_CLUSTER_MAX_PPT");
         if (cp && atoi(cp) > 0) ctx->cluster_max_ppt = atoi(cp);
         const char *nr = getenv("CQG_NO_INIT_REC");

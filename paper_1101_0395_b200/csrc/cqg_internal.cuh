@@ -135,6 +135,7 @@ struct cqg_ctx {
     // cached CUDA graph of the Lloyd WHILE loop (lloyd.cu)
     bool use_graphs = true;
     bool use_cluster_init = true;
+    bool use_mbar_init = true; // cluster init signals through mbarrier transactions (CQG_NO_MBAR_INIT=1: barriers)
     int cluster_max_ppt = 12; // cluster initialiser up to 16 x 1024 x ppt colours (CQG_CLUSTER_MAX_PPT); 16 measured slower on cfg4
     bool use_init_rec = true; // {colour, md} record layout for large-N init (CQG_NO_INIT_REC=1: off)
     bool use_ndc_code = true; // shared-memory code table for the NDC count (CQG_NO_NDC_CODE=1: off)

@@ -785,6 +785,61 @@ __global__ void __launch_bounds__(kInitThreads, 3) init_kernel_rec(InitArgs a) {
 constexpr int kClusterThreads = 1024;
 constexpr int kMaxClusterCtas = 16;
 
+// ---- DSMEM producer/consumer signalling (mbarrier transaction counts) ----
+// A consumer CTA arrives once on its local mbarrier and expects N bytes; each
+// producer writes into the consumer's shared memory with st.async, which
+// completes those bytes on the consumer's mbarrier. The consumer waits on the
+// barrier's phase parity: no cluster-wide barrier is needed.
+__device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint32_t mapa_rank(uint32_t saddr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_complete_local(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.complete_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+// wait for the barrier phase with the given parity; traps instead of hanging
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    const uint32_t a = smem_addr(bar);
+    for (uint32_t spin = 0;; ++spin) {
+        uint32_t ok;
+        asm volatile("{\n\t.reg .pred p;\n\t"
+                     "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+                     "selp.u32 %0, 1, 0, p;\n\t}"
+                     : "=r"(ok)
+                     : "r"(a), "r"(parity)
+                     : "memory");
+        if (ok) return;
+        if (spin > (1u << 26)) __trap(); // a lost signal: abort the kernel, never hang the GPU
+    }
+}
+__device__ __forceinline__ void st_async_u64(uint32_t raddr, unsigned long long v, uint32_t rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(raddr), "l"(v),
+                 "r"(rbar)
+                 : "memory");
+}
+__device__ __forceinline__ void st_async_v4(uint32_t raddr, uint32_t x, uint32_t y, uint32_t z, uint32_t w,
+                                            uint32_t rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+                     raddr),
+                 "r"(x), "r"(y), "r"(z), "r"(w), "r"(rbar)
+                 : "memory");
+}
+// a mass sum (u64, or u128 as two 64-bit halves)
+__device__ __forceinline__ void st_async_T(uint32_t raddr, unsigned long long v, uint32_t rbar) { st_async_u64(raddr, v, rbar); }
+__device__ __forceinline__ void st_async_T(uint32_t raddr, u128 v, uint32_t rbar) {
+    st_async_v4(raddr, (uint32_t)v, (uint32_t)(v >> 32), (uint32_t)(v >> 64), (uint32_t)(v >> 96), rbar);
+}
+
 // Split cluster barrier: only a warp that wrote data other CTAs (or other
 // warps) will read after the barrier pays the release fence; the rest arrive
 // relaxed. Every warp waits with acquire semantics.
@@ -854,7 +909,7 @@ __device__ __forceinline__ int lane_locate(typename M::T v, typename M::T U, typ
 }
 
 template <class M>
-__global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_kernel(InitArgs a, int ppt) {
+__global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_kernel(InitArgs a, int ppt, int mbar) {
     typedef typename M::T T;
     cg::cluster_group cl = cg::this_cluster();
     const int C = (int)cl.num_blocks(), crank = (int)cl.block_rank();
@@ -883,6 +938,19 @@ __global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_kernel(InitAr
     // ppt is a multiple of 4: each thread's run is 16-byte aligned (128-bit shared loads)
     const int p0 = t * ppt, p1 = min(p0 + ppt, mine);
     __shared__ uint32_t s_pickcol;
+    // mbar: CTA sums and the pick travel by st.async into per-parity slots, each
+    // signalling the receiver's mbarrier (s_bar[par]: sums, s_bar[2 + par]: pick)
+    __shared__ uint64_t s_bar[4];
+    __shared__ __align__(16) uint32_t s_pk4[2][4]; // pick lo, pick hi, colour, ambiguous
+    __shared__ int s_nf;
+    int use_s[2] = {0, 0}, use_p[2] = {0, 0}; // phases consumed per barrier (uniform per CTA)
+    if (mbar) {
+        if (t == 0) {
+            for (int i = 0; i < 4; ++i) mbar_init(&s_bar[i], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        cl.sync(); // every CTA's barriers exist before the first remote signal
+    }
 
     auto colour_of = [&](uint64_t gi) -> uint32_t {
         return *cl.map_shared_rank(s_col + (gi % chunk), (unsigned)(gi / chunk));
@@ -893,7 +961,13 @@ __global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_kernel(InitAr
     __shared__ T s_U, s_cpre;
     __shared__ int s_tw;
     auto publish = [&](int par, T ts) {
-        if (t == 0) s_found = 0; // before this round's first barrier: no owner has written yet
+        if (t == 0) {
+            s_found = 0; // before this round's first barrier: no owner has written yet
+            if (mbar) { // this round's incoming bytes: C CTA sums, one 16-byte pick
+                mbar_arrive_expect(&s_bar[par], (uint32_t)(C * sizeof(T)));
+                mbar_arrive_expect(&s_bar[2 + par], 16u);
+            }
+        }
         T w = ts;
         for (int o = 16; o; o >>= 1) w += M::shfl(w, lane ^ o);
         if (lane == 0) s_wsum[par * 32 + warp] = w;
@@ -903,7 +977,24 @@ __global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_kernel(InitAr
             const T wincl = warp_incl<M>(wv);
             s_wpre[par * 32 + lane] = wincl - wv;
             const T c = M::shfl(wincl, 31);
-            if (lane < C) *cl.map_shared_rank(s_allc + par * kMaxClusterCtas + crank, lane) = c;
+            if (lane < C) {
+                if (mbar)
+                    st_async_T(mapa_rank(smem_addr(s_allc + par * kMaxClusterCtas + crank), lane), c,
+                               mapa_rank(smem_addr(&s_bar[par]), lane));
+                else
+                    *cl.map_shared_rank(s_allc + par * kMaxClusterCtas + crank, lane) = c;
+            }
+        }
+        if (mbar) __syncthreads(); // s_wpre (warp 0) for every warp; the cluster barrier did this before
+    };
+
+    // after publish: every CTA sum has arrived
+    auto wait_sums = [&](int par) {
+        if (mbar) {
+            mbar_wait(&s_bar[par], (uint32_t)(use_s[par] & 1));
+            ++use_s[par];
+        } else {
+            cluster_barrier(warp == 0); // warp 0 pushed the CTA sum and wrote s_wpre
         }
     };
 
@@ -913,7 +1004,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_kernel(InitAr
     // only that warp scans its lanes' sums and searches the owning thread's
     // <= 32 points in local shared memory, then writes (index, colour,
     // ambiguity) into every rank; a second cluster barrier publishes them.
-    auto draw = [&](int par, double nu, const uint32_t *mdb, T ts) -> uint64_t {
+    auto draw = [&](int par, double nu, const uint32_t *mdb, T ts, uint32_t &pick_col) -> uint64_t {
         if (warp == 0) {
             const T cv = lane < C ? s_allc[par * kMaxClusterCtas + lane] : (T)0;
             const T cincl = warp_incl<M>(cv);
@@ -927,6 +1018,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_kernel(InitAr
                 s_U = U;
                 s_cpre = cpre;
                 s_tw = m ? __ffs(m) - 1 : -1;
+                s_nf = U < total ? 0 : 1; // no owner anywhere: identical in every CTA
             }
         }
         __syncthreads();
@@ -962,17 +1054,42 @@ __global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_kernel(InitAr
                 amb = gi == a.n - 1 ? !(U > prevE + B2) : (!(E > U + B2) || (gi > 0 && !(U > prevE + B2)));
             }
             if (lane < C) { // one rank per lane
-                *cl.map_shared_rank(&s_pick, lane) = gi;
-                *cl.map_shared_rank(&s_pickcol, lane) = pcol;
-                *cl.map_shared_rank(&s_amb, lane) = amb ? 1 : 0;
-                *cl.map_shared_rank(&s_found, lane) = 1;
+                if (mbar) {
+                    st_async_v4(mapa_rank(smem_addr(s_pk4[par]), lane), (uint32_t)gi, (uint32_t)(gi >> 32), pcol,
+                                amb ? 1u : 0u, mapa_rank(smem_addr(&s_bar[2 + par]), lane));
+                } else {
+                    *cl.map_shared_rank(&s_pick, lane) = gi;
+                    *cl.map_shared_rank(&s_pickcol, lane) = pcol;
+                    *cl.map_shared_rank(&s_amb, lane) = amb ? 1 : 0;
+                    *cl.map_shared_rank(&s_found, lane) = 1;
+                }
             }
-            if (!CQG_EXP_SKIP_BARRIER2) cluster_barrier(true);
+            if (!mbar && !CQG_EXP_SKIP_BARRIER2) cluster_barrier(true);
         } else {
-            if (!CQG_EXP_SKIP_BARRIER2) cluster_barrier(false);
+            if (!mbar && !CQG_EXP_SKIP_BARRIER2) cluster_barrier(false);
         }
         if (CQG_EXP_SKIP_BARRIER2) __syncthreads();
+        if (mbar) {
+            // no owner: complete this CTA's expected pick bytes itself (the phase must end)
+            if (s_nf && t == 0) mbar_complete_local(&s_bar[2 + par], 16u);
+            mbar_wait(&s_bar[2 + par], (uint32_t)(use_p[par] & 1));
+            ++use_p[par];
+            // the common case: every thread reads the pushed pick itself (the wait
+            // acquired it), no further block barrier
+            if (!s_nf && !s_pk4[par][3]) {
+                pick_col = s_pk4[par][2];
+                return ((unsigned long long)s_pk4[par][1] << 32) | s_pk4[par][0];
+            }
+            if (t == 0 && !s_nf) {
+                s_pick = ((unsigned long long)s_pk4[par][1] << 32) | s_pk4[par][0];
+                s_pickcol = s_pk4[par][2];
+                s_amb = (int)s_pk4[par][3];
+                s_found = 1;
+            }
+            __syncthreads();
+        }
         if (!s_found) { // the target lies beyond every prefix: the reference returns n-1
+            cl.sync(); // uniform; other CTAs' min distances stay untouched while read below
             __syncthreads();
             if (t == 0) {
                 const uint64_t last = a.n - 1;
@@ -990,6 +1107,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_kernel(InitAr
                 s_amb = amb ? 1 : 0;
             }
             __syncthreads();
+            cl.sync(); // nobody updates before every CTA has read
         }
         if (s_amb) { // identical in every CTA: uniform extra barrier
             __syncthreads();
@@ -1006,6 +1124,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_kernel(InitAr
             }
             __syncthreads();
         }
+        pick_col = s_pickcol;
         return s_pick;
     };
 
@@ -1015,8 +1134,12 @@ __global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_kernel(InitAr
         T ts = 0;
         for (int i = p0; i < p1; ++i) ts += M::mass_c(a, s_cnt[i], kWeightsOnly);
         publish(par, ts);
-        cluster_barrier(warp == 0); // warp 0 pushed the CTA sum and wrote s_wpre
-        first = draw(par, a.nu[0], nullptr, ts);
+        wait_sums(par);
+        uint32_t fcol = 0;
+        first = draw(par, a.nu[0], nullptr, ts, fcol);
+        __syncthreads(); // s_pickcol is written by thread 0 below
+        if (t == 0) s_pickcol = fcol;
+        __syncthreads();
         par ^= 1;
     } else {
         first = a.first_index;
@@ -1035,6 +1158,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_kernel(InitAr
     T ts_run = 0; // this thread's mass sum, kept across rounds (exact deltas)
     for (int k = 1; k < a.K; ++k) {
         uint64_t pick;
+        uint32_t kcol = 0;
         const uint32_t bb = __dp4a(clast, clast, 0u);
         if (a.kind == 0) {
             unsigned long long best = 0;
@@ -1112,19 +1236,21 @@ __global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_kernel(InitAr
             ITIME(0);
             publish(par, ts_run);
             ITIME(1);
-            cluster_barrier(warp == 0); // warp 0 pushed the CTA sum and wrote s_wpre
+            wait_sums(par);
             ITIME(2);
-            pick = draw(par, nu_k, s_md, ts_run);
+            pick = draw(par, nu_k, s_md, ts_run, kcol);
             ITIME(3);
         }
         par ^= 1;
-        clast = a.kind == 0 ? colour_of(pick) : s_pickcol;
+        clast = a.kind == 0 ? colour_of(pick) : kcol;
         if (crank == 0 && t == 0) {
             a.cen[3 * k] = (double)((clast >> 16) & 255u);
             a.cen[3 * k + 1] = (double)((clast >> 8) & 255u);
             a.cen[3 * k + 2] = (double)(clast & 255u);
         }
-        __syncthreads();
+        // maximin reuses s_pick every round; k-means++ with mbarrier signalling is
+        // ordered by the next round's signals (slots are per parity)
+        if (a.kind == 0 || !mbar) __syncthreads();
         ITIME(4);
     }
     cl.sync(); // no CTA may exit while others still read its shared memory
@@ -1169,7 +1295,7 @@ static bool launch_cluster_init(cqg_ctx *ctx, InitArgs a) {
         return false;
     }
     const int pb = prof_begin(ctx);
-    CQG_CUDA(cudaLaunchKernelEx(&cfg, kern, a, ppt));
+    CQG_CUDA(cudaLaunchKernelEx(&cfg, kern, a, ppt, ctx->use_mbar_init ? 1 : 0));
     prof_end(ctx, CQG_PROF_INIT, pb, (double)a.n * (double)(a.K - 1));
     launched(ctx);
     return true;
