@@ -530,9 +530,10 @@ def run_ours(args, cfg):
             "bound": "latency" if small else "hbm",
             "rounds": K0 - 1 if cfg.init == "kpp" else K0 - 1,
             "us_per_round": 1e3 * init_ms / max(K0 - 1, 1),
-            "note": ("a chain of K-1 dependent draws, two cluster barriers each; per-round critical path "
-                     "(tools/init_timing.py): update ~32%, publish ~15%, first barrier ~13%, "
-                     "locate + second barrier ~33%") if small else
+            "note": ("a chain of K-1 dependent draws; CTA sums and the pick travel by st.async with mbarrier "
+                     "transaction signalling (no cluster barriers); per-round critical path "
+                     "(tools/init_timing.py): update ~33%, publish ~16%, wait for sums ~7%, "
+                     "locate + pick ~33%") if small else
                     "8 B per point per round streamed; see DESIGN.md §8",
         }
     hist_ms = prof.ms[cabi.PROF_HIST]

@@ -925,6 +925,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_kernel(InitAr
     T *s_allc = s_wpre + 2 * 32;                               // 2 x kMaxClusterCtas
     unsigned long long *s_key = reinterpret_cast<unsigned long long *>(s_allc + 2 * kMaxClusterCtas); // 2
     __shared__ unsigned long long s_wkey[32];
+    __shared__ uint32_t s_wcol[32];
     uint32_t *s_col = reinterpret_cast<uint32_t *>(s_key + 2);
     uint32_t *s_cnt = s_col + chunk;
     uint32_t *s_md = s_cnt + chunk;                            // chunk, updated in place
@@ -942,6 +943,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_kernel(InitAr
     // signalling the receiver's mbarrier (s_bar[par]: sums, s_bar[2 + par]: pick)
     __shared__ uint64_t s_bar[4];
     __shared__ __align__(16) uint32_t s_pk4[2][4]; // pick lo, pick hi, colour, ambiguous
+    __shared__ __align__(16) uint32_t s_mk[2][kMaxClusterCtas][4]; // maximin: every CTA's best key + colour
     __shared__ int s_nf;
     int use_s[2] = {0, 0}, use_p[2] = {0, 0}; // phases consumed per barrier (uniform per CTA)
     if (mbar) {
@@ -1162,13 +1164,62 @@ __global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_kernel(InitAr
         const uint32_t bb = __dp4a(clast, clast, 0u);
         if (a.kind == 0) {
             unsigned long long best = 0;
+            uint32_t bcol = 0;
             for (int i = p0; i < p1; ++i) {
                 const uint32_t d = d2_int_bb(s_col[i], clast, bb);
                 const uint32_t m = k == 1 ? d : min(s_md[i], d);
                 s_md[i] = m;
                 const unsigned long long key = ((unsigned long long)m << 32) | (uint32_t)~(uint32_t)(lo + i);
-                best = key > best ? key : best;
+                if (key > best) {
+                    best = key;
+                    bcol = s_col[i];
+                }
             }
+            if (mbar) {
+                // (key, colour) maxima -> pushed into every CTA; every thread takes the max
+                if (t == 0) mbar_arrive_expect(&s_bar[par], (uint32_t)(C * 16));
+                for (int o = 16; o; o >>= 1) {
+                    const unsigned long long x = __shfl_xor_sync(0xffffffffu, best, o);
+                    const uint32_t xc = __shfl_xor_sync(0xffffffffu, bcol, o);
+                    if (x > best) {
+                        best = x;
+                        bcol = xc;
+                    }
+                }
+                if (lane == 0) {
+                    s_wkey[warp] = best;
+                    s_wcol[warp] = bcol;
+                }
+                __syncthreads();
+                if (warp == 0) {
+                    unsigned long long b = s_wkey[lane];
+                    uint32_t bc = s_wcol[lane];
+                    for (int o = 16; o; o >>= 1) {
+                        const unsigned long long x = __shfl_xor_sync(0xffffffffu, b, o);
+                        const uint32_t xc = __shfl_xor_sync(0xffffffffu, bc, o);
+                        if (x > b) {
+                            b = x;
+                            bc = xc;
+                        }
+                    }
+                    if (lane < C)
+                        st_async_v4(mapa_rank(smem_addr(s_mk[par][crank]), lane), (uint32_t)b, (uint32_t)(b >> 32), bc,
+                                    0u, mapa_rank(smem_addr(&s_bar[par]), lane));
+                }
+                mbar_wait(&s_bar[par], (uint32_t)(use_s[par] & 1));
+                ++use_s[par];
+                unsigned long long b = 0;
+                uint32_t bc = 0;
+                for (int r = 0; r < C; ++r) {
+                    const unsigned long long x = ((unsigned long long)s_mk[par][r][1] << 32) | s_mk[par][r][0];
+                    if (x > b) {
+                        b = x;
+                        bc = s_mk[par][r][2];
+                    }
+                }
+                pick = (uint64_t)(uint32_t)~(uint32_t)(b & 0xFFFFFFFFull);
+                kcol = bc;
+            } else {
             for (int o = 16; o; o >>= 1) {
                 const unsigned long long x = __shfl_xor_sync(0xffffffffu, best, o);
                 best = x > best ? x : best;
@@ -1194,6 +1245,8 @@ __global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_kernel(InitAr
             }
             __syncthreads();
             pick = s_pick;
+            kcol = colour_of(pick);
+            }
         } else {
             const double nu_k = __ldg(a.nu + k); // off the locate's critical path
             // whole 4-point runs (padding has count 0: mass 0). md is updated in
@@ -1242,15 +1295,15 @@ __global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_kernel(InitAr
             ITIME(3);
         }
         par ^= 1;
-        clast = a.kind == 0 ? colour_of(pick) : kcol;
+        clast = kcol;
         if (crank == 0 && t == 0) {
             a.cen[3 * k] = (double)((clast >> 16) & 255u);
             a.cen[3 * k + 1] = (double)((clast >> 8) & 255u);
             a.cen[3 * k + 2] = (double)(clast & 255u);
         }
-        // maximin reuses s_pick every round; k-means++ with mbarrier signalling is
-        // ordered by the next round's signals (slots are per parity)
-        if (a.kind == 0 || !mbar) __syncthreads();
+        // with mbarrier signalling the rounds are ordered by the next round's
+        // signals (slots are per parity); the barrier path reuses s_pick
+        if (!mbar) __syncthreads();
         ITIME(4);
     }
     cl.sync(); // no CTA may exit while others still read its shared memory
