@@ -10,8 +10,11 @@
 //                   atomicMax(~first[c], ~p) keeps the minimum index.
 //                   Small images: both in one pass over an interleaved
 //                   {count, ~first} table. Large images (P >= 2^22): two passes
-//                   (hist_count, hist_first) over split 64 MiB tables, so each
-//                   pass's table stays in the 126 MB L2.
+//                   of fire-and-forget reductions (hist_count_red, hist_first)
+//                   over split 64 MiB tables (each fits the 126 MB L2), then a
+//                   third pass marks the first occurrences straight from the
+//                   image (~first[c] == p) -- no unique-colour list, no global
+//                   append counter; N' is the bitmap's popcount from the scan.
 //   B  hist_mark    per listed colour: set bit first(c) in a P-bit bitmap.
 //   C  scan         popcount prefix over the bitmap words (2 small kernels).
 //   D  emit         small: per listed colour, rank = prefix(first(c)), write at
@@ -152,6 +155,60 @@ __global__ void __launch_bounds__(kThreads) hist_count(const uint8_t *__restrict
     }
 }
 
+// large images: counts by reductions (no return value, no list)
+__global__ void __launch_bounds__(kThreads) hist_count_red(const uint8_t *__restrict__ rgb, uint64_t P,
+                                                          uint32_t *__restrict__ cnt, int aligned) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t groups = aligned ? P / 16 : 0;
+    for (uint64_t g = tid; g < groups; g += stride) {
+        const uint4 *src = reinterpret_cast<const uint4 *>(rgb + g * 48);
+        uint32_t col[16];
+        decode16(ld_stream(src), ld_stream(src + 1), ld_stream(src + 2), col);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) atomicAdd(cnt + col[j], 1u);
+    }
+    for (uint64_t p = groups * 16 + tid; p < P; p += stride) {
+        const uint32_t c = ((uint32_t)rgb[3 * p] << 16) | ((uint32_t)rgb[3 * p + 1] << 8) | rgb[3 * p + 2];
+        atomicAdd(cnt + c, 1u);
+    }
+}
+
+// large images: first-occurrence bitmap straight from the image -- pixel p is
+// a first occurrence iff ~negf[colour(p)] == p. Thread t's 16 pixels are half
+// of bitmap word t/2; the two halves meet by a shuffle (no atomics).
+__global__ void __launch_bounds__(kThreads) hist_mark_pixels(const uint8_t *__restrict__ rgb, uint64_t P,
+                                                            const uint32_t *__restrict__ negf,
+                                                            uint32_t *__restrict__ bitmap, int aligned) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t groups = aligned ? P / 16 : 0;
+    // uniform trip count across the grid (the shuffle needs full warps)
+    for (uint64_t g0 = tid - (tid & 31); g0 < (groups + 31) / 32 * 32; g0 += stride) {
+        const uint64_t g = g0 + (tid & 31);
+        uint32_t mask = 0;
+        if (g < groups) {
+            const uint4 *src = reinterpret_cast<const uint4 *>(rgb + g * 48);
+            uint32_t col[16];
+            decode16(ld_stream(src), ld_stream(src + 1), ld_stream(src + 2), col);
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                mask |= (~__ldg(negf + col[j]) == (uint32_t)(g * 16 + j) ? 1u : 0u) << j;
+        }
+        const uint32_t hi = __shfl_down_sync(0xffffffffu, mask, 1);
+        if (g < groups && (g & 1) == 0) {
+            // the word that also holds tail pixels (odd group count) is shared with the tail loop
+            if (g + 1 < groups) bitmap[g >> 1] = mask | (hi << 16);
+            else atomicOr(&bitmap[g >> 1], mask);
+        }
+    }
+    // tail pixels (or everything when unaligned): one bit each
+    for (uint64_t p = groups * 16 + tid; p < P; p += stride) {
+        const uint32_t c = ((uint32_t)rgb[3 * p] << 16) | ((uint32_t)rgb[3 * p + 1] << 8) | rgb[3 * p + 2];
+        if (~__ldg(negf + c) == (uint32_t)p) atomicOr(&bitmap[p >> 5], 1u << (p & 31));
+    }
+}
+
 __global__ void __launch_bounds__(kThreads) hist_first(const uint8_t *__restrict__ rgb, uint64_t P,
                                                       uint32_t *__restrict__ negf, int aligned) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -222,7 +279,7 @@ __global__ void __launch_bounds__(kThreads) scan_blocksum(const uint32_t *__rest
 }
 
 // exclusive scan of the block sums (one block, sequential chunks)
-__global__ void scan_blocks(uint32_t *__restrict__ bsum, uint32_t nblocks) {
+__global__ void scan_blocks(uint32_t *__restrict__ bsum, uint32_t nblocks, uint32_t *__restrict__ n_out) {
     __shared__ uint32_t carry;
     __shared__ uint32_t tmp[1024];
     if (threadIdx.x == 0) carry = 0;
@@ -243,6 +300,7 @@ __global__ void scan_blocks(uint32_t *__restrict__ bsum, uint32_t nblocks) {
         if (threadIdx.x == 1023) carry += tmp[1023];
         __syncthreads();
     }
+    if (n_out && threadIdx.x == 0) *n_out = carry; // the number of set bits: N'
 }
 
 // per-word exclusive prefix (global)
@@ -338,12 +396,14 @@ void histogram_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P, uint32_t *col
         hist_count_fused<<<grid, kThreads, 0, s>>>(rgb_d, P, tab, list, n_dev, aligned);
         hist_mark_fused<<<lgrid, kThreads, 0, s>>>(list, n_dev, tab, bitmap);
     } else {
-        hist_count<<<grid, kThreads, 0, s>>>(rgb_d, P, cnt, list, n_dev, aligned);
+        // counts and minimum indices by reductions; the bitmap from a third image
+        // pass (no unique-colour list, no global append counter)
+        hist_count_red<<<grid, kThreads, 0, s>>>(rgb_d, P, cnt, aligned);
         hist_first<<<grid, kThreads, 0, s>>>(rgb_d, P, negf, aligned);
-        hist_mark<<<lgrid, kThreads, 0, s>>>(list, n_dev, negf, bitmap);
+        hist_mark_pixels<<<grid, kThreads, 0, s>>>(rgb_d, P, negf, bitmap, aligned);
     }
     scan_blocksum<<<nblk, kThreads, 0, s>>>(bitmap, words, bsum);
-    scan_blocks<<<1, 1024, 0, s>>>(bsum, nblk);
+    scan_blocks<<<1, 1024, 0, s>>>(bsum, nblk, large ? n_dev : nullptr);
     scan_words<<<nblk, kThreads, 0, s>>>(bitmap, words, bsum, wpref);
     if (!large) {
         hist_emit_fused<<<lgrid, kThreads, 0, s>>>(list, n_dev, tab, bitmap, wpref, colors_d, counts_d, first_d);

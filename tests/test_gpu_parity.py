@@ -103,6 +103,37 @@ def test_histogram_device_pointers(ctx, oracle):
     assert np.array_equal(cnt[:n].cpu().numpy().view(np.uint32), k)
 
 
+@pytest.mark.parametrize("case", ["2048sq", "odd2049", "unaligned_large", "few_large"])
+def test_histogram_large_images(ctx, oracle, case):
+    # P >= 2^22: counts and first indices by reductions in two passes, the
+    # first-occurrence bitmap from a third pass over the image, pixel-order emit,
+    # one memset reset (hist.cu large path); odd sizes leave tail pixels that
+    # share a bitmap word with the last 16-pixel group
+    rng = np.random.default_rng(2024)
+    if case == "2048sq":
+        img = synth_image(2048, 2048, 11, nblobs=20, sigma=20.0, noise=0.3)
+    elif case == "odd2049":
+        img = synth_image(2049, 2049, 12, nblobs=20, sigma=20.0, noise=0.3)
+    elif case == "unaligned_large":
+        base = synth_image(2050, 2047, 13, nblobs=10, sigma=25.0, noise=0.5)
+        buf = np.zeros(base.size + 7, np.uint8)
+        buf[7:] = base.reshape(-1)
+        img = buf[7:]
+    else:
+        img = (rng.integers(0, 4, (2100, 2000, 3)) * 60).astype(np.uint8)
+    assert img.size // 3 >= (1 << 22)
+    h = gpu_hist(ctx, img)
+    c, n, f = oracle.histogram(img)
+    assert np.array_equal(h.packed, c)
+    assert np.array_equal(h.counts, n)
+    assert np.array_equal(h.first, f)
+    # the tables are clean for the next (small) call
+    small = synth_image(64, 48, 3, nblobs=3)
+    hs = gpu_hist(ctx, small)
+    cs, ns, _ = oracle.histogram(small)
+    assert np.array_equal(hs.packed, cs) and np.array_equal(hs.counts, ns)
+
+
 def test_histogram_repeated_calls_keep_table_clean(ctx, oracle):
     for seed in range(3):
         img = synth_image(200, 150, 40 + seed, nblobs=5, sigma=9.0, noise=0.05)
