@@ -65,6 +65,7 @@ struct InitArgs {
     unsigned long long *result; // [2] fallback result slots
     unsigned long long *fallbacks;
     double *cen;
+    int force_seq;       // tests only (CQG_DBG_INIT_FORCE_SEQ): 1 every draw ambiguous, 2 every draw "beyond every prefix"
 };
 
 __device__ __forceinline__ u128 to_fixed(double m) {
@@ -1309,22 +1310,328 @@ __global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_kernel(InitAr
     cl.sync(); // no CTA may exit while others still read its shared memory
 }
 
+// Register-resident variant (the default): thread t keeps its PPT colours and
+// min distances in registers, so a round's update reads no shared memory
+// (counts are loaded only for points whose distance falls). Every thread
+// knows its exclusive mass prefix inside its warp (the publish scan) and its
+// warp's prefix inside the CTA, so once the CTA sums arrive each thread tests
+// on its own whether it owns the target; the owner scans its PPT register
+// masses and pushes (index, colour, ambiguity) to every CTA. No block barrier
+// or warp hand-over sits between the sums' arrival and the pick. The rare
+// paths (ambiguous fixed-point decisions, a target beyond every prefix) dump
+// the registers into s_md and replay the reference sequentially as before.
+template <class M, int PPT>
+__global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_reg_kernel(InitArgs a) {
+    typedef typename M::T T;
+    cg::cluster_group cl = cg::this_cluster();
+    const int C = (int)cl.num_blocks(), crank = (int)cl.block_rank();
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    constexpr uint64_t chunk = (uint64_t)kClusterThreads * PPT;
+    const uint64_t lo = (uint64_t)crank * chunk;
+    const uint64_t hi = lo + chunk < a.n ? lo + chunk : a.n;
+    const int mine = hi > lo ? (int)(hi - lo) : 0;
+    extern __shared__ __align__(16) unsigned char sm_raw[];
+    uint32_t *s_col = reinterpret_cast<uint32_t *>(sm_raw);
+    uint32_t *s_cnt = s_col + chunk;
+    uint32_t *s_md = s_cnt + chunk; // written only on the rare sequential paths
+    __shared__ T s_wsum[2][32];
+    __shared__ T s_allc[2][kMaxClusterCtas];
+    __shared__ uint64_t s_bar[4];
+    __shared__ __align__(16) uint32_t s_pk4[2][4];                 // pick lo, pick hi, colour, ambiguous
+    __shared__ __align__(16) uint32_t s_mk[2][kMaxClusterCtas][4]; // maximin: every CTA's best key + colour
+    __shared__ unsigned long long s_wkey[32];
+    __shared__ uint32_t s_wcol[32];
+    __shared__ unsigned long long s_pick, s_fbv;
+    __shared__ uint32_t s_fbc;
+    __shared__ T s_U, s_total, s_base;
+    __shared__ int s_tw, s_nf;
+    for (int i = t; i < (int)chunk; i += kClusterThreads) { // padding: colour 0, count 0 (mass 0)
+        s_col[i] = i < mine ? __ldg(a.colors + lo + i) : 0u;
+        s_cnt[i] = i < mine ? __ldg(a.counts + lo + i) : 0u;
+    }
+    if (t == 0) {
+        for (int i = 0; i < 4; ++i) mbar_init(&s_bar[i], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int p0 = t * PPT;
+    uint32_t rc[PPT], rm[PPT];
+#pragma unroll
+    for (int j = 0; j < PPT; j += 4) {
+        const uint4 c4 = *reinterpret_cast<const uint4 *>(s_col + p0 + j);
+        rc[j] = c4.x, rc[j + 1] = c4.y, rc[j + 2] = c4.z, rc[j + 3] = c4.w;
+        rm[j] = rm[j + 1] = rm[j + 2] = rm[j + 3] = 0u;
+    }
+    cl.sync(); // every CTA's barriers exist (and its points are loaded) before the first remote access
+    uint32_t ph_s = 0, ph_p = 0; // bit par: parity of the next phase to wait for (uniform per CTA)
+
+    auto colour_of = [&](uint64_t gi) -> uint32_t {
+        return *cl.map_shared_rank(s_col + (gi % chunk), (unsigned)(gi / chunk));
+    };
+
+    // Publish this round's thread sum ts: returns the thread's exclusive prefix
+    // inside its warp; warp 0 scans the warp sums (kept in registers for the
+    // draw) and pushes the CTA sum into every rank.
+    T w_excl = 0, w_sum = 0; // warp 0, lane l: warp l's exclusive prefix in the CTA and its sum
+    auto publish = [&](int par, T ts) -> T {
+        if (t == 0) { // this round's incoming bytes: C CTA sums, one 16-byte pick
+            mbar_arrive_expect(&s_bar[par], (uint32_t)(C * sizeof(T)));
+            mbar_arrive_expect(&s_bar[2 + par], 16u);
+        }
+        const T tincl = warp_incl<M>(ts);
+        if (lane == 31) s_wsum[par][warp] = tincl;
+        __syncthreads();
+        if (warp == 0) {
+            w_sum = s_wsum[par][lane];
+            const T wincl = warp_incl<M>(w_sum);
+            w_excl = wincl - w_sum;
+            const T csum = M::shfl(wincl, 31);
+            if (lane < C)
+                st_async_T(mapa_rank(smem_addr(&s_allc[par][crank]), lane), csum,
+                           mapa_rank(smem_addr(&s_bar[par]), lane));
+        }
+        return tincl - ts;
+    };
+
+    // One weighted draw over this round's masses (weights only: counts).
+    // Warp 0 waits for the CTA sums, finds the target U and the warp whose
+    // range holds it; after one block barrier only that warp's lanes test
+    // their own ranges, and the owner scans its registers.
+    auto draw = [&](int par, double nu, bool wo, T ts, T tpre, uint32_t &pick_col) -> uint64_t {
+        if (warp == 0) {
+            mbar_wait(&s_bar[par], (ph_s >> par) & 1u);
+            const T cv = lane < C ? s_allc[par][lane] : (T)0;
+            const T cincl = warp_incl<M>(cv);
+            const T total = M::shfl(cincl, 31);
+            const T U = M::target(nu, total);
+            const T cpre = M::shfl(cincl - cv, crank);
+            const T wlo = cpre + w_excl;
+            const unsigned m = __ballot_sync(0xffffffffu, w_sum != (T)0 && !(U < wlo) && U < wlo + w_sum);
+            const int tw = m ? __ffs(m) - 1 : -1;
+            const T base = M::shfl(wlo, tw < 0 ? 0 : tw);
+            if (lane == 0) {
+                s_U = U;
+                s_total = total;
+                s_base = base;
+                s_tw = tw;
+                s_nf = (U < total && a.force_seq != 2) ? 0 : 1; // no owner anywhere: identical in every CTA
+            }
+        }
+        ph_s ^= 1u << par;
+        __syncthreads();
+        const bool nf = s_nf != 0;
+        const T U = s_U;
+        if (warp == s_tw && !nf) {
+            const T lo_t = s_base + tpre;
+            if (ts != (T)0 && !(U < lo_t) && U < lo_t + ts) { // the owner (exactly one thread in the cluster)
+                const T total = s_total;
+                T run = lo_t, E = 0, prevE = 0;
+                int pl = PPT;
+                uint32_t pcol = 0;
+#pragma unroll
+                for (int j = 0; j < PPT; ++j) {
+                    const T m = M::mass_c(a, s_cnt[p0 + j], wo ? kWeightsOnly : rm[j]);
+                    if (pl == PPT && U < run + m) {
+                        pl = j;
+                        prevE = run;
+                        E = run + m;
+                        pcol = rc[j];
+                    }
+                    run += m;
+                }
+                const uint64_t gi = lo + (uint64_t)(p0 + pl);
+                bool amb = a.force_seq == 1;
+                if (!M::exact) {
+                    const T B2 = M::bound(a.n, total);
+                    // the reference returns n-1 when no earlier prefix exceeds u
+                    amb = amb || (gi == a.n - 1 ? !(U > prevE + B2) : (!(E > U + B2) || (gi > 0 && !(U > prevE + B2))));
+                }
+                for (int r = 0; r < C; ++r)
+                    st_async_v4(mapa_rank(smem_addr(s_pk4[par]), r), (uint32_t)gi, (uint32_t)(gi >> 32), pcol,
+                                amb ? 1u : 0u, mapa_rank(smem_addr(&s_bar[2 + par]), r));
+            }
+        }
+        // no owner: complete this CTA's expected pick bytes itself (the phase must end)
+        if (nf && t == 0) mbar_complete_local(&s_bar[2 + par], 16u);
+        mbar_wait(&s_bar[2 + par], (ph_p >> par) & 1u);
+        ph_p ^= 1u << par;
+        if (!nf && !s_pk4[par][3]) { // the common case: every thread reads the pushed pick itself
+            pick_col = s_pk4[par][2];
+            return ((unsigned long long)s_pk4[par][1] << 32) | s_pk4[par][0];
+        }
+        // rare and uniform across the cluster: a target beyond every prefix (the
+        // reference returns n-1) or an ambiguous fixed-point decision
+        if (!wo) {
+#pragma unroll
+            for (int j = 0; j < PPT; ++j) s_md[p0 + j] = rm[j];
+        }
+        cl.sync(); // every CTA's min distances are in shared memory and stay untouched
+        if (crank == 0 && t == 0) {
+            bool seq = !nf || a.force_seq == 2;
+            unsigned long long v = a.n - 1;
+            const T total = s_total;
+            if (nf && !seq && !M::exact && a.n > 1) {
+                const uint64_t last = a.n - 1;
+                const uint32_t r = (uint32_t)(last / chunk), li = (uint32_t)(last % chunk);
+                const uint32_t cnt = *cl.map_shared_rank(s_cnt + li, r);
+                const uint32_t md = wo ? kWeightsOnly : *cl.map_shared_rank(s_md + li, r);
+                seq = !(U > total - M::mass_c(a, cnt, md) + M::bound(a.n, total));
+            }
+            if (seq) {
+                v = cluster_sequential_draw<M>(a, cl, s_cnt, s_md, chunk, nu, wo ? 1 : 0);
+                atomicAdd(a.fallbacks, 1ull);
+            }
+            s_pick = v;
+        }
+        cl.sync();
+        if (t == 0) {
+            const unsigned long long v = *cl.map_shared_rank(&s_pick, 0);
+            s_fbv = v;
+            s_fbc = colour_of(v);
+        }
+        __syncthreads();
+        pick_col = s_fbc;
+        return s_fbv;
+    };
+
+    int par = 0;
+    uint32_t clast;
+    if (a.kind == 1 || a.weighted_first) {
+        T ts = 0;
+#pragma unroll
+        for (int j = 0; j < PPT; ++j) ts += M::mass_c(a, s_cnt[p0 + j], kWeightsOnly);
+        const T tpre = publish(par, ts);
+        draw(par, a.nu[0], true, ts, tpre, clast);
+        par ^= 1;
+    } else {
+        clast = colour_of(a.first_index);
+    }
+    if (crank == 0 && t == 0) {
+        a.cen[0] = (double)((clast >> 16) & 255u);
+        a.cen[1] = (double)((clast >> 8) & 255u);
+        a.cen[2] = (double)(clast & 255u);
+    }
+#ifdef CQG_INIT_TIMING
+    unsigned long long _tprev = clock64();
+#endif
+    T ts_run = 0; // this thread's mass sum, kept across rounds (exact deltas)
+    for (int k = 1; k < a.K; ++k) {
+        uint32_t kcol = 0;
+        const uint32_t bb = __dp4a(clast, clast, 0u);
+        if (a.kind == 0) {
+            unsigned long long best = 0;
+            uint32_t bcol = 0;
+#pragma unroll
+            for (int j = 0; j < PPT; ++j) {
+                const uint32_t d = d2_int_bb(rc[j], clast, bb);
+                const uint32_t m = k == 1 ? d : min(rm[j], d);
+                rm[j] = m;
+                const unsigned long long key = ((unsigned long long)m << 32) | (uint32_t)~(uint32_t)(lo + p0 + j);
+                if (p0 + j < mine && key > best) {
+                    best = key;
+                    bcol = rc[j];
+                }
+            }
+            // (key, colour) maxima -> pushed into every CTA; every thread takes the max
+            if (t == 0) mbar_arrive_expect(&s_bar[par], (uint32_t)(C * 16));
+            for (int o = 16; o; o >>= 1) {
+                const unsigned long long x = __shfl_xor_sync(0xffffffffu, best, o);
+                const uint32_t xc = __shfl_xor_sync(0xffffffffu, bcol, o);
+                if (x > best) {
+                    best = x;
+                    bcol = xc;
+                }
+            }
+            if (lane == 0) {
+                s_wkey[warp] = best;
+                s_wcol[warp] = bcol;
+            }
+            __syncthreads();
+            if (warp == 0) {
+                unsigned long long b = s_wkey[lane];
+                uint32_t bc = s_wcol[lane];
+                for (int o = 16; o; o >>= 1) {
+                    const unsigned long long x = __shfl_xor_sync(0xffffffffu, b, o);
+                    const uint32_t xc = __shfl_xor_sync(0xffffffffu, bc, o);
+                    if (x > b) {
+                        b = x;
+                        bc = xc;
+                    }
+                }
+                if (lane < C)
+                    st_async_v4(mapa_rank(smem_addr(s_mk[par][crank]), lane), (uint32_t)b, (uint32_t)(b >> 32), bc, 0u,
+                                mapa_rank(smem_addr(&s_bar[par]), lane));
+            }
+            mbar_wait(&s_bar[par], (ph_s >> par) & 1u);
+            ph_s ^= 1u << par;
+            unsigned long long b = 0;
+            uint32_t bc = 0;
+            for (int r = 0; r < C; ++r) {
+                const unsigned long long x = ((unsigned long long)s_mk[par][r][1] << 32) | s_mk[par][r][0];
+                if (x > b) {
+                    b = x;
+                    bc = s_mk[par][r][2];
+                }
+            }
+            kcol = bc;
+        } else {
+            const double nu_k = __ldg(a.nu + k); // off the locate's critical path
+            if (k == 1) {
+#pragma unroll
+                for (int j = 0; j < PPT; ++j) {
+                    rm[j] = d2_int_bb(rc[j], clast, bb);
+                    ts_run += M::mass_c(a, s_cnt[p0 + j], rm[j]);
+                }
+            } else if (!CQG_EXP_SKIP_UPDATE) {
+                // only points closer to the new centre change: their mass
+                // difference is subtracted from the running sum (exact)
+                T delta = 0;
+#pragma unroll
+                for (int j = 0; j < PPT; j += 4) {
+                    uint32_t d[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) d[u] = d2_int_bb(rc[j + u], clast, bb);
+                    if ((d[0] < rm[j]) | (d[1] < rm[j + 1]) | (d[2] < rm[j + 2]) | (d[3] < rm[j + 3])) {
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            if (d[u] < rm[j + u]) {
+                                const uint32_t cnt = s_cnt[p0 + j + u];
+                                delta += M::mass_c(a, cnt, rm[j + u]) - M::mass_c(a, cnt, d[u]);
+                                rm[j + u] = d[u];
+                            }
+                        }
+                    }
+                }
+                ts_run -= delta;
+            }
+            ITIME(0);
+            const T tpre = publish(par, ts_run);
+            ITIME(1);
+            draw(par, nu_k, false, ts_run, tpre, kcol);
+            ITIME(3);
+        }
+        par ^= 1;
+        clast = kcol;
+        if (crank == 0 && t == 0) {
+            a.cen[3 * k] = (double)((clast >> 16) & 255u);
+            a.cen[3 * k + 1] = (double)((clast >> 8) & 255u);
+            a.cen[3 * k + 2] = (double)(clast & 255u);
+        }
+        ITIME(4);
+    }
+    cl.sync(); // no CTA may exit while others still read its shared memory
+}
+
 template <class M>
 static size_t cluster_smem(int ppt) {
     return sizeof(typename M::T) * (2 * 32 + 2 * 32 + 2 * kMaxClusterCtas) + 16 +
            (size_t)kClusterThreads * ppt * 3 * sizeof(uint32_t); // colour, count, md
 }
 
-// Try the cluster initialiser; false when the substrate does not fit.
-template <class M>
-static bool launch_cluster_init(cqg_ctx *ctx, InitArgs a) {
+// launch one 16-CTA cluster of `kern`; false when it cannot be resident
+template <class... KArgs, class... Args>
+static bool launch_cluster(cqg_ctx *ctx, const InitArgs &a, void (*kern)(KArgs...), size_t smem, Args... args) {
     constexpr int C = 16;
-    const uint64_t per = (a.n + C - 1) / C;
-    const int ppt = ((int)((per + kClusterThreads - 1) / kClusterThreads) + 3) & ~3; // 128-bit runs
-    if (ppt < 1 || ppt > ctx->cluster_max_ppt) return false;
-    const size_t smem = cluster_smem<M>(ppt);
-    if (smem > 227 * 1024) return false;
-    auto kern = init_cluster_kernel<M>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess ||
         ensure_smem((const void *)kern, (int)smem) != cudaSuccess) {
         cudaGetLastError();
@@ -1348,10 +1655,30 @@ static bool launch_cluster_init(cqg_ctx *ctx, InitArgs a) {
         return false;
     }
     const int pb = prof_begin(ctx);
-    CQG_CUDA(cudaLaunchKernelEx(&cfg, kern, a, ppt, ctx->use_mbar_init ? 1 : 0));
+    CQG_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
     prof_end(ctx, CQG_PROF_INIT, pb, (double)a.n * (double)(a.K - 1));
     launched(ctx);
     return true;
+}
+
+// Try the cluster initialiser; false when the substrate does not fit.
+template <class M>
+static bool launch_cluster_init(cqg_ctx *ctx, InitArgs a) {
+    constexpr int C = 16;
+    const uint64_t per = (a.n + C - 1) / C;
+    const int ppt = ((int)((per + kClusterThreads - 1) / kClusterThreads) + 3) & ~3; // 128-bit runs
+    if (ppt < 1 || ppt > ctx->cluster_max_ppt) return false;
+    const bool reg = ctx->use_init_reg && ctx->use_mbar_init && ppt <= 12;
+    const size_t smem = reg ? (size_t)kClusterThreads * ppt * 3 * sizeof(uint32_t) : cluster_smem<M>(ppt);
+    if (smem > 227 * 1024) return false;
+    if (reg) {
+        switch (ppt) {
+        case 4: return launch_cluster(ctx, a, init_cluster_reg_kernel<M, 4>, smem, a);
+        case 8: return launch_cluster(ctx, a, init_cluster_reg_kernel<M, 8>, smem, a);
+        default: return launch_cluster(ctx, a, init_cluster_reg_kernel<M, 12>, smem, a);
+        }
+    }
+    return launch_cluster(ctx, a, init_cluster_kernel<M>, smem, a, ppt, ctx->use_mbar_init ? 1 : 0);
 }
 
 void run_init(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *counts_d, uint64_t n, uint64_t P,
@@ -1395,6 +1722,7 @@ void run_init(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *counts_d, 
         c.fallbacks = resc + 4;
         c.cen = centers_d;
         c.mds = 1;
+        c.force_seq = ctx->dbg_init_force_seq;
         if (exact ? launch_cluster_init<ExactMass>(ctx, c) : launch_cluster_init<FixedMass>(ctx, c)) return;
     }
     const bool rec = ctx->use_init_rec;

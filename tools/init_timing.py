@@ -15,7 +15,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_1101_0395_b200 import _build  # noqa: E402
 
-TLIB = os.path.join(_build.PKG, "libcqg_timing.so")
+TLIB = os.environ.get("CQG_TIMING_LIB", os.path.join(_build.PKG, "libcqg_timing.so"))
 
 
 def build(extra=()):
