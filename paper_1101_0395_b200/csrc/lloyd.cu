@@ -1326,9 +1326,9 @@ extern "C" int cqg_dbg_block_timing(unsigned long long *out, int reset) {
 
 #ifdef CQG_SWEEP_TIMING
 extern "C" int cqg_dbg_sweep_timing(unsigned long long *out, int reset) {
-    if (cudaMemcpyFromSymbol(out, cqg::g_sweep_timing, 4 * sizeof(unsigned long long)) != cudaSuccess) return 1;
+    if (cudaMemcpyFromSymbol(out, cqg::g_sweep_timing, 8 * sizeof(unsigned long long)) != cudaSuccess) return 1;
     if (reset) {
-        unsigned long long z[4] = {};
+        unsigned long long z[8] = {};
         cudaMemcpyToSymbol(cqg::g_sweep_timing, z, sizeof(z));
     }
     return 0;

@@ -397,6 +397,23 @@ static __global__ void __launch_bounds__(256, 4) ndc_kernel(const uint32_t *__re
 // identical FP operation sequence (bit-identical values): the index is the
 // first that equals b1, and the true second-best is min(b2, group second).
 constexpr int kGroup = 8;
+#ifdef CQG_SWEEP_TIMING
+// block 0: filter cycles, phase cycles, survivors, calls; list tiles (thread 0):
+// point loads, centre loop, resolve
+__device__ unsigned long long g_sweep_timing[8];
+#define STIME(slot)                                                                  \
+    do {                                                                             \
+        if (LIST && blockIdx.x == 0 && threadIdx.x == 0) {                           \
+            const unsigned long long _n = clock64();                                 \
+            g_sweep_timing[slot] += _n - _tt;                                        \
+            _tt = _n;                                                                \
+        }                                                                            \
+    } while (0)
+#else
+#define STIME(slot) \
+    do {            \
+    } while (0)
+#endif
 // u32 words of the sweep accumulators: u32 x kAccPerCluster (FULL/MAP) or u64 x 5 (WALK)
 __host__ __device__ constexpr int sweep_acc_words(int K) {
     return K * kAccPerCluster > K * 10 ? K * kAccPerCluster : K * 10;
@@ -418,7 +435,17 @@ __device__ __forceinline__ void sweep_tiles(const SweepArgs &a, uint64_t lo, uin
     // per-value error bound of the FP32 distances (tau_abs = 2E*1.0625 + 1e-3)
     const float ev = 0.5f * tau_abs;
     const uint64_t tile = (uint64_t)kSweepThreads * PPT;
+    // slot of point i of this thread: contiguous per i across the block for
+    // ranges (coalesced colour loads); thread-major for lists, so a partial
+    // tile fills whole warps and the warps left without points skip the tile
+    auto slot_of = [&](uint64_t base, int i) -> uint64_t {
+        return LIST ? base + (uint64_t)threadIdx.x * PPT + i : base + threadIdx.x + (uint64_t)i * kSweepThreads;
+    };
     for (uint64_t base = lo; base < hi; base += tile) {
+        if (__any_sync(0xffffffffu, slot_of(base, 0) < hi)) {
+#ifdef CQG_SWEEP_TIMING
+        unsigned long long _tt = clock64();
+#endif
         // point pairs: lane .x = point 2p, lane .y = point 2p+1 (FFMA2 with a
         // broadcast scalar centre operand evaluates one centre for both)
         float2 xr2[PP], xg2[PP], xb2[PP], xx2[PP];
@@ -428,7 +455,7 @@ __device__ __forceinline__ void sweep_tiles(const SweepArgs &a, uint64_t lo, uin
         int g1[PPT];
 #pragma unroll
         for (int i = 0; i < PPT; ++i) {
-            const uint64_t slot = base + threadIdx.x + (uint64_t)i * kSweepThreads;
+            const uint64_t slot = slot_of(base, i);
             pidx[i] = slot < hi ? (LIST ? list[slot] : (uint32_t)slot) : 0u;
             col[i] = slot < hi ? __ldg(a.colors + pidx[i]) : 0u;
             const float r = (float)((col[i] >> 16) & 255u), g = (float)((col[i] >> 8) & 255u),
@@ -447,6 +474,7 @@ __device__ __forceinline__ void sweep_tiles(const SweepArgs &a, uint64_t lo, uin
             b2[i] = 3.0e38f;
             g1[i] = 0;
         }
+        STIME(4);
         for (int j = 0; j < Kp; j += kGroup) {
             float gm[PPT]; // this group's minimum per point
 #pragma unroll
@@ -487,11 +515,12 @@ __device__ __forceinline__ void sweep_tiles(const SweepArgs &a, uint64_t lo, uin
                 b1[i] = fminf(b1[i], lo);
             }
         }
+        STIME(5);
         // resolve
 #pragma unroll
         for (int i = 0; i < PPT; ++i) {
             const uint32_t idx = pidx[i];
-            const bool valid = base + threadIdx.x + (uint64_t)i * kSweepThreads < hi;
+            const bool valid = slot_of(base, i) < hi;
             const float f1 = b1[i];
             // exact index: first centre of group g1 whose (bit-identical) value
             // is b1; the group's second value completes the second-best
@@ -563,6 +592,8 @@ __device__ __forceinline__ void sweep_tiles(const SweepArgs &a, uint64_t lo, uin
             }
             enqueue(flag, (uint32_t)idx, a.queue, a.qn);
         }
+        STIME(6);
+        } // warp has points
         if (MODE != MODE_WALK) {
             __syncthreads();
             flush_acc(s_acc, a.mom, K);
@@ -571,9 +602,6 @@ __device__ __forceinline__ void sweep_tiles(const SweepArgs &a, uint64_t lo, uin
     }
 }
 
-#ifdef CQG_SWEEP_TIMING
-__device__ unsigned long long g_sweep_timing[4]; // block 0: filter cycles, phase cycles, survivors, calls
-#endif
 // Points per block-local chunk of the pruned WALK sweep (shared-memory list).
 constexpr int kPruneChunk = 4096;
 constexpr float kBoundMargin = 1.0e-3f; // Euclidean gap that keeps the FP64 reference order

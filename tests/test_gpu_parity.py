@@ -328,6 +328,20 @@ def test_map_bit_exact(ctx, oracle, reflib, K, ib):
     assert abs(m.mean_sq_dist - mse_r) <= 1e-12 * mse_r
 
 
+@pytest.mark.parametrize("w,h,K,ib", [(1031, 1025, 256, 4), (1024, 1024, 64, 1), (1100, 977, 300, 4)])
+def test_map_large_streaming(ctx, oracle, w, h, K, ib):
+    # P >= 2^20 takes the TMA-fed streaming kernel over 512-pixel warp chunks;
+    # 1031x1025 and 1100x977 leave a remainder for the plain kernel
+    img = synth_image(w, h, 5 + K, nblobs=12, sigma=18.0, noise=0.2)
+    rng = np.random.default_rng(w + K)
+    pal = rng.random((K, 3)) * 255.0
+    m = quant.map_pixels(img, pal, index_bytes=ib, ctx=ctx)
+    idx, q, mse_e, _ = oracle.map_pixels(img, pal, mode=UPDATE_EXACT)
+    assert np.array_equal(m.indices.astype(np.uint32), idx)
+    assert np.array_equal(m.quantized.reshape(-1, 3), q)
+    assert m.mean_sq_dist == mse_e
+
+
 def test_map_reference_cases(ctx):
     # tests/test_metrics.cpp:66-92
     img = np.array([[[1, 0, 0]]], np.uint8)

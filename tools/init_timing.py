@@ -72,7 +72,7 @@ def run(name):
     L.cqg_dbg_lloyd_timing(buf, 1)
     L.cqg_dbg_block_timing((C.c_ulonglong * (1024 * 3))(), 1)
     if hasattr(L, "cqg_dbg_sweep_timing"):
-        L.cqg_dbg_sweep_timing((C.c_ulonglong * 4)(), 1)
+        L.cqg_dbg_sweep_timing((C.c_ulonglong * 8)(), 1)
     st = None
     for _ in range(reps):
         st = quant.wsm_hist(hist, init, opts, ctx=ctx)
@@ -97,11 +97,13 @@ def run(name):
     print(f"{'total':14s} {tot / its:8.0f} cycles/iter  (swept {st.swept_total / (st.iterations * len(hist.counts)):.3f})")
     print(f"  iter_end: centres+status+fc {buf[6] / its:8.0f}  whole body {buf[7] / its:8.0f} cycles/iter")
     if hasattr(L, "cqg_dbg_sweep_timing"):
-        sb = (C.c_ulonglong * 4)()
+        sb = (C.c_ulonglong * 8)()
         L.cqg_dbg_sweep_timing(sb, 0)
         calls = max(sb[3], 1)
         print(f"  pruned sweep (block 0): filter {sb[0] / calls:8.0f}  whole {sb[1] / calls:8.0f} cycles/call, "
               f"survivors {sb[2] / calls:6.0f}")
+        print(f"  list tiles (block 0, thread 0): loads {sb[4] / calls:8.0f}  centre loop {sb[5] / calls:8.0f}  "
+              f"resolve {sb[6] / calls:8.0f} cycles/call")
 
 
 if __name__ == "__main__":
