@@ -221,6 +221,8 @@ cqg_ctx *cqg_create(int device) {
         if (fs) ctx->dbg_init_force_seq = atoi(fs);
         const char *nr = getenv("CQG_NO_INIT_REC");
         ctx->use_init_rec = !(nr && nr[0] == '1');
+        const char *nt = getenv("CQG_NO_INIT_TILE");
+        ctx->use_init_tile = !(nt && nt[0] == '1');
         const char *np = getenv("CQG_NO_PRUNE");
         ctx->use_prune = !(np && np[0] == '1');
         const char *nn = getenv("CQG_NO_NDC_CODE");
@@ -244,7 +246,7 @@ void cqg_destroy(cqg_ctx *ctx) {
                       &ctx->dtab, &ctx->dsorted, &ctx->order, &ctx->mom, &ctx->queue, &ctx->ndc,
                       &ctx->status, &ctx->sizes, &ctx->red, &ctx->hist_labels, &ctx->hist_centers,
                       &ctx->sse, &ctx->lut, &ctx->idx_out, &ctx->q_out, &ctx->mom_map, &ctx->mind2,
-                      &ctx->initpart, &ctx->initsel, &ctx->unit_draws, &ctx->mom_g, &ctx->partial,
+                      &ctx->initpart, &ctx->initsel, &ctx->unit_draws, &ctx->inittile, &ctx->mom_g, &ctx->partial,
                       &ctx->bnd, &ctx->shift, &ctx->dcode, &ctx->sub_img, &ctx->raw_col, &ctx->raw_cnt,
                       &ctx->full_col, &ctx->full_cnt};
     for (DevBuf *b : bufs) b->release();

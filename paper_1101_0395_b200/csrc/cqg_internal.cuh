@@ -128,7 +128,7 @@ struct cqg_ctx {
     // mapping
     cqg::DevBuf lut, idx_out, q_out, mom_map;
     // init
-    cqg::DevBuf mind2, initpart, initsel, unit_draws;
+    cqg::DevBuf mind2, initpart, initsel, unit_draws, inittile;
     cqg::HostBuf pinned;   // status readback and small results
     cqg::HostBuf pinned_nu; // initialiser unit draws (an async H2D source: no host-blocking copy)
 
@@ -140,6 +140,7 @@ struct cqg_ctx {
     int dbg_init_force_seq = 0; // tests only: CQG_DBG_INIT_FORCE_SEQ=1|2 drives the register cluster kernel's sequential paths
     bool use_init_reg = true; // cluster init keeps points in registers (CQG_NO_INIT_REG=1: shared-memory kernel)
     bool use_init_rec = true; // {colour, md} record layout for large-N init (CQG_NO_INIT_REC=1: off)
+    bool use_init_tile = true; // colour-space tiles with box pruning for large-N init (CQG_NO_INIT_TILE=1: off)
     bool use_ndc_code = true; // shared-memory code table for the NDC count (CQG_NO_NDC_CODE=1: off)
     bool use_prune = true; // distance-bound pruning of the WALK sweep (CQG_NO_PRUNE=1: off)
     cudaGraphExec_t loop_exec = nullptr;

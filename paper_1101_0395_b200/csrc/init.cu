@@ -66,7 +66,24 @@ struct InitArgs {
     unsigned long long *fallbacks;
     double *cen;
     int force_seq;       // tests only (CQG_DBG_INIT_FORCE_SEQ): 1 every draw ambiguous, 2 every draw "beyond every prefix"
+    // colour-space tiles (init_kernel_tile): points in Morton order of their
+    // colour, kTile per tile; md values are read through hpos (histogram
+    // index -> tile position) by the locate
+    const uint32_t *hpos; // null: md is indexed by histogram position
+    uint2 *trec;          // {colour, md} in tile order
+    const uint32_t *tidx; // histogram index of each tile-order point
+    const uint32_t *tcnt; // count of each tile-order point (k-means++)
+    const uint2 *tbox;    // per tile: packed min / max colour channels
+    uint32_t *tmax;       // per tile: largest md
+    unsigned long long *tkey; // per tile (maximin): largest (md, ~index)
+    uint64_t ntiles;
+    unsigned long long *tflags; // per block release words (kFlagStride apart), zero at launch
 };
+
+// md of histogram point i (direct, or through the tile layout)
+__device__ __forceinline__ uint32_t md_at(const InitArgs &a, const uint32_t *md, uint64_t i) {
+    return md[(a.hpos ? (uint64_t)a.hpos[i] : i) * (uint64_t)a.mds];
+}
 
 __device__ __forceinline__ u128 to_fixed(double m) {
     if (m == 0.0) return 0;
@@ -257,11 +274,11 @@ __device__ typename M::T block_excl(typename M::T v, typename M::T *s_w, typenam
 __device__ uint64_t sequential_draw(const InitArgs &a, const uint32_t *md, double nu, int weights_only) {
     double total = 0.0;
     for (uint64_t i = 0; i < a.n; ++i)
-        total = __dadd_rn(total, mass_of(a, i, weights_only ? kWeightsOnly : md[i * a.mds]));
+        total = __dadd_rn(total, mass_of(a, i, weights_only ? kWeightsOnly : md_at(a, md, i)));
     const double u = __dmul_rn(nu, total);
     double acc = 0.0;
     for (uint64_t i = 0; i + 1 < a.n; ++i) {
-        acc = __dadd_rn(acc, mass_of(a, i, weights_only ? kWeightsOnly : md[i * a.mds]));
+        acc = __dadd_rn(acc, mass_of(a, i, weights_only ? kWeightsOnly : md_at(a, md, i)));
         if (u < acc) return i;
     }
     return a.n - 1;
@@ -403,7 +420,7 @@ __device__ uint64_t locate_draw(const InitArgs &a, cg::grid_group &grid, int par
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const uint64_t i = base + j;
-            m[j] = i < a.n ? M::mass(a, i, weights_only ? kWeightsOnly : md[i * a.mds]) : (T)0;
+            m[j] = i < a.n ? M::mass(a, i, weights_only ? kWeightsOnly : md_at(a, md, i)) : (T)0;
             loc += m[j];
         }
         T btot;
@@ -429,7 +446,7 @@ __device__ uint64_t locate_draw(const InitArgs &a, cg::grid_group &grid, int par
     if (s_found == ~0ull || s_found >= a.n - 1) {
         idx = a.n - 1; // the reference returns n-1 when no i < n-1 qualifies
         if (!M::exact && a.n > 1) {
-            const T mlast = M::mass(a, a.n - 1, weights_only ? kWeightsOnly : md[(a.n - 1) * a.mds]);
+            const T mlast = M::mass(a, a.n - 1, weights_only ? kWeightsOnly : md_at(a, md, a.n - 1));
             ambiguous = !(U > tot - mlast + M::bound(a.n, tot));
         }
     } else {
@@ -560,7 +577,10 @@ __global__ void __launch_bounds__(kInitThreads) init_kernel(InitArgs a) {
 constexpr int kRecBatch = 16; // records in flight per lane (32 doubles the registers: 1 block per SM)
 
 #ifdef CQG_INIT_TIMING
-__device__ unsigned long long g_coop_timing[8];
+__device__ unsigned long long g_coop_timing[8]; // [5] tiles updated, [6] points changed, [7] slowest block's update
+__device__ unsigned long long g_tile_round_max;
+__device__ unsigned long long g_tile_rounds[1024][2]; // per round: slowest block update, block 0 locate
+__device__ unsigned long long g_loc_phase[4];
 #define GTIME(slot)                                                                  \
     do {                                                                             \
         if (blockIdx.x == 0 && threadIdx.x == 0) {                                   \
@@ -764,6 +784,596 @@ __global__ void __launch_bounds__(kInitThreads, 3) init_kernel_rec(InitArgs a) {
             a.cen[3 * k + 2] = (double)(clast & 255u);
         }
         __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Large substrates, colour-space tiles. The points are laid out in Morton
+// order of their colour (kTile consecutive points per tile, each tile a
+// compact colour box), so a round of the update only visits the tiles the new
+// centre can reach: a tile whose box is at squared distance >= its largest md
+// from the new centre keeps every min distance (md only falls when
+// d2(x, c) < md, and d2(x, c) >= d2(box, c) for every x in the box). All in
+// exact integers, so the set of updated points -- and every md -- is exactly
+// the full sweep's. k-means++ keeps its mass sums in HISTOGRAM order (the
+// reference's prefix order): a changed point subtracts its exact mass drop
+// from its segment's and its part's sum (atomics); the locate is the record
+// kernel's, reading md through hpos. Maximin keeps per-tile maxima of
+// (md, ~index); untouched tiles keep theirs.
+constexpr int kTile = 256;       // points per tile (8 per lane of one warp)
+constexpr int kFlagStride = 32;  // u64 words between two blocks' release flags (256 B)
+
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u64(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+constexpr int kTileBitmapWords = 1 << 19; // 2^24 Morton slots
+
+__device__ __forceinline__ uint32_t tile_spread8(uint32_t x) {
+    x = (x | (x << 8)) & 0x0000F00Fu;
+    x = (x | (x << 4)) & 0x000C30C3u;
+    x = (x | (x << 2)) & 0x00249249u;
+    return x;
+}
+__device__ __forceinline__ uint32_t tile_morton(uint32_t c) {
+    return (tile_spread8((c >> 16) & 255u) << 2) | (tile_spread8((c >> 8) & 255u) << 1) | tile_spread8(c & 255u);
+}
+
+// setup 1: one bit per present Morton slot; a second point on a slot
+// (duplicate colours: raw-pixel substrates) raises *dup
+__global__ void tile_mark_kernel(const uint32_t *__restrict__ colors, uint64_t n, uint32_t *__restrict__ bits,
+                                 uint32_t *dup) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t m = tile_morton(__ldg(colors + i));
+        const uint32_t bit = 1u << (m & 31u);
+        if (atomicOr(bits + (m >> 5), bit) & bit) *dup = 1u;
+    }
+}
+
+// setup 2: exclusive popcount prefix of the bitmap words (1024 words per
+// block; block offsets from a second, single-block pass over the block sums)
+__device__ __forceinline__ uint32_t block_excl_u32(uint32_t v, uint32_t *s_w, uint32_t *total) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t incl = v;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    if (lane == 31) s_w[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        const uint32_t x = lane < (int)(blockDim.x >> 5) ? s_w[lane] : 0u;
+        uint32_t xi = x;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, xi, o);
+            if (lane >= o) xi += t;
+        }
+        s_w[lane] = xi - x;
+        if (lane == 31) s_w[32] = xi;
+    }
+    __syncthreads();
+    const uint32_t r = s_w[wid] + incl - v;
+    if (total) *total = s_w[32];
+    __syncthreads();
+    return r;
+}
+__global__ void __launch_bounds__(1024) tile_scan_blocks(const uint32_t *__restrict__ bits, uint32_t *__restrict__ pref,
+                                                         uint32_t *__restrict__ bsum) {
+    __shared__ uint32_t s_w[33];
+    const uint32_t w = blockIdx.x * 1024u + threadIdx.x;
+    uint32_t tot;
+    pref[w] = block_excl_u32((uint32_t)__popc(bits[w]), s_w, &tot);
+    if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
+}
+__global__ void __launch_bounds__(1024) tile_scan_top(uint32_t *bsum, int nb) {
+    __shared__ uint32_t s_w[33];
+    const uint32_t v = (int)threadIdx.x < nb ? bsum[threadIdx.x] : 0u;
+    const uint32_t e = block_excl_u32(v, s_w, nullptr);
+    if ((int)threadIdx.x < nb) bsum[threadIdx.x] = e;
+}
+
+// setup 3: place every point at its Morton rank
+__global__ void tile_place_kernel(const uint32_t *__restrict__ colors, const uint32_t *__restrict__ counts, uint64_t n,
+                                  const uint32_t *__restrict__ bits, const uint32_t *__restrict__ pref,
+                                  const uint32_t *__restrict__ bsum, uint2 *__restrict__ trec,
+                                  uint32_t *__restrict__ tidx, uint32_t *__restrict__ tcnt, uint32_t *__restrict__ hpos) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t c = __ldg(colors + i);
+        const uint32_t m = tile_morton(c), w = m >> 5;
+        const uint32_t pos = bsum[w >> 10] + pref[w] + (uint32_t)__popc(bits[w] & ((1u << (m & 31u)) - 1u));
+        trec[pos] = make_uint2(c, 0xFFFFFFFFu);
+        tidx[pos] = (uint32_t)i;
+        if (tcnt) tcnt[pos] = __ldg(counts + i);
+        if (hpos) hpos[i] = pos;
+    }
+}
+
+// setup 4: per tile the colour box (one warp per tile)
+__global__ void tile_box_kernel(const uint2 *__restrict__ trec, uint64_t n, uint64_t ntiles, uint2 *__restrict__ tbox,
+                                uint32_t *__restrict__ tmax) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t t = gw; t < ntiles; t += nw) {
+        uint32_t lr = 255, lg = 255, lb = 255, hr = 0, hg = 0, hb = 0;
+        for (int u = 0; u < kTile / 32; ++u) {
+            const uint64_t p = t * kTile + u * 32 + lane;
+            if (p < n) {
+                const uint32_t c = trec[p].x;
+                const uint32_t r = (c >> 16) & 255u, g = (c >> 8) & 255u, b = c & 255u;
+                lr = min(lr, r), lg = min(lg, g), lb = min(lb, b);
+                hr = max(hr, r), hg = max(hg, g), hb = max(hb, b);
+            }
+        }
+        for (int o = 16; o; o >>= 1) {
+            lr = min(lr, __shfl_xor_sync(0xffffffffu, lr, o));
+            lg = min(lg, __shfl_xor_sync(0xffffffffu, lg, o));
+            lb = min(lb, __shfl_xor_sync(0xffffffffu, lb, o));
+            hr = max(hr, __shfl_xor_sync(0xffffffffu, hr, o));
+            hg = max(hg, __shfl_xor_sync(0xffffffffu, hg, o));
+            hb = max(hb, __shfl_xor_sync(0xffffffffu, hb, o));
+        }
+        if (lane == 0) {
+            tbox[t] = make_uint2((lr << 16) | (lg << 8) | lb, (hr << 16) | (hg << 8) | hb);
+            tmax[t] = 0xFFFFFFFFu;
+        }
+    }
+}
+
+// squared distance from colour c to the box {lo, hi} (exact integers)
+__device__ __forceinline__ uint32_t box_d2(uint2 box, uint32_t c) {
+    uint32_t s = 0;
+#pragma unroll
+    for (int sh = 16; sh >= 0; sh -= 8) {
+        const int v = (int)((c >> sh) & 255u), lo = (int)((box.x >> sh) & 255u), hi = (int)((box.y >> sh) & 255u);
+        const int d = v < lo ? lo - v : (v > hi ? v - hi : 0);
+        s += (uint32_t)(d * d);
+    }
+    return s;
+}
+
+__device__ __forceinline__ void atomic_sub_mass(unsigned long long *p, unsigned long long v) {
+    atomicAdd(p, 0ull - v);
+}
+__device__ __forceinline__ void atomic_sub_mass(u128 *p, u128 v) {
+    // two's complement add of -v, low word first with its carry (the value is
+    // consistent again once every update of the round has landed)
+    const u128 nv = (u128)0 - v;
+    unsigned long long *q = reinterpret_cast<unsigned long long *>(p);
+    const unsigned long long lo = (unsigned long long)nv, hi = (unsigned long long)(nv >> 64);
+    const unsigned long long old = atomicAdd(q, lo);
+    const unsigned long long carry = old + lo < old ? 1ull : 0ull;
+    if (hi + carry) atomicAdd(q + 1, hi + carry);
+}
+
+// One round of the tile update for the new centre clast. full: first round
+// (every tile, md := d2). Each warp owns tiles gw, gw + W, ...; its lanes test
+// 32 of them at once, then the warp updates the reached ones (8 points per
+// lane). k-means++: changed points subtract their exact mass drop from their
+// histogram segment and part sums. Maximin: returns the warp's largest
+// (md, ~index) over all its tiles.
+template <class M>
+__device__ unsigned long long update_tiles(const InitArgs &a, bool full, uint32_t clast) {
+    typedef typename M::T T;
+    T *segs = reinterpret_cast<T *>(a.segs);
+    const int lane = threadIdx.x & 31;
+    const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t W = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint32_t bb = __dp4a(clast, clast, 0u);
+    unsigned long long best = 0;
+    for (uint64_t j0 = 0; gw + j0 * W < a.ntiles; j0 += 32) {
+        const uint64_t t = gw + (j0 + lane) * W;
+        // branch-free metadata loads (clamped tile index, masked result)
+        const bool tin = t < a.ntiles;
+        const uint64_t tc = tin ? t : 0;
+        const uint2 bx = a.tbox[tc];
+        const uint32_t tm = a.tmax[tc];
+        const unsigned long long tk = a.kind == 0 ? a.tkey[tc] : 0ull;
+        const bool need = tin && (full || box_d2(bx, clast) < tm);
+        if (tin && !need) best = max(best, tk);
+        unsigned m = __ballot_sync(0xffffffffu, need);
+        while (m) {
+            const int l = __ffs(m) - 1;
+            m &= m - 1;
+            const uint64_t tt = gw + (j0 + l) * W;
+            // every load of the tile issued at once (clamped indices: the
+            // last tile's padding lanes re-read point n-1 and are masked)
+            uint2 r[kTile / 32];
+            uint32_t cn[kTile / 32], hx[kTile / 32];
+#pragma unroll
+            for (int u = 0; u < kTile / 32; ++u) {
+                const uint64_t p = tt * kTile + u * 32 + lane;
+                const uint64_t pc = p < a.n ? p : a.n - 1;
+                r[u] = a.trec[pc];
+                cn[u] = (a.kind == 1 && !full) ? __ldg(a.tcnt + pc) : 0u;
+                hx[u] = (a.kind == 0 || !full) ? __ldg(a.tidx + pc) : 0u;
+            }
+            uint32_t mx = 0;
+            unsigned long long kb = 0;
+            uint32_t dn[kTile / 32], chg = 0;
+#pragma unroll
+            for (int u = 0; u < kTile / 32; ++u) {
+                const uint64_t p = tt * kTile + u * 32 + lane;
+                dn[u] = d2_int_bb(r[u].x, clast, bb);
+                if (p < a.n && dn[u] < r[u].y) chg |= 1u << u; // first round: md = 0xFFFFFFFF
+            }
+#pragma unroll
+            for (int u = 0; u < kTile / 32; ++u) {
+                const uint64_t p = tt * kTile + u * 32 + lane;
+                if ((chg >> u) & 1u) {
+                    a.trec[p].y = dn[u];
+                    if (a.kind == 1 && !full) {
+                        const T dm = M::mass_c(a, cn[u], r[u].y) - M::mass_c(a, cn[u], dn[u]);
+                        if (dm != (T)0) atomic_sub_mass(segs + hx[u] / kSeg, dm);
+                    }
+                    r[u].y = dn[u];
+                }
+                if (p < a.n) {
+                    mx = max(mx, r[u].y);
+                    if (a.kind == 0) kb = max(kb, ((unsigned long long)r[u].y << 32) | (uint32_t)~hx[u]);
+                }
+            }
+            for (int o = 16; o; o >>= 1) {
+                mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                kb = max(kb, __shfl_xor_sync(0xffffffffu, kb, o));
+            }
+            if (lane == 0) {
+                a.tmax[tt] = mx;
+                if (a.kind == 0) a.tkey[tt] = kb;
+            }
+#ifdef CQG_INIT_TIMING
+            {
+                unsigned nc = __popc(chg);
+                for (int o = 16; o; o >>= 1) nc += __shfl_xor_sync(0xffffffffu, nc, o);
+                if (lane == 0) {
+                    atomicAdd(&g_coop_timing[5], 1ull);
+                    atomicAdd(&g_coop_timing[6], (unsigned long long)nc);
+                }
+            }
+#endif
+            best = max(best, kb);
+        }
+    }
+    for (int o = 16; o; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+    return best;
+}
+
+// first k-means++ round: the segment mass sums in histogram order (one warp
+// per kSeg segment), md = d2(x, c0) (the tiles hold the same values)
+template <class M>
+__device__ void tile_first_sums(const InitArgs &a, uint32_t clast) {
+    typedef typename M::T T;
+    T *segs = reinterpret_cast<T *>(a.segs);
+    const int lane = threadIdx.x & 31;
+    const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t W = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint32_t bb = __dp4a(clast, clast, 0u);
+    const uint64_t nseg = (a.n + kSeg - 1) / kSeg;
+    for (uint64_t sg = gw; sg < nseg; sg += W) {
+        T loc = 0;
+#pragma unroll 4
+        for (int b = lane; b < kSeg; b += 32) {
+            const uint64_t i = sg * kSeg + b;
+            if (i < a.n) loc += M::mass_c(a, __ldg(a.counts + i), d2_int_bb(__ldg(a.colors + i), clast, bb));
+        }
+        for (int o = 16; o; o >>= 1) loc += M::shfl(loc, lane ^ o);
+        if (lane == 0) segs[sg] = loc;
+    }
+}
+
+// The draw of one k-means++ round, located by ONE block over the segment sums
+// (no per-block part sums: those would be the atomics' hot spot): thread
+// sums over runs of segments, a block scan, the owner's run, then the
+// segment's points (md through hpos) exactly as locate_draw does, including
+// its n-1 rule and the fixed-point ambiguity fallback.
+template <class M>
+__device__ uint64_t locate_one_block(const InitArgs &a, double nu, const uint32_t *md, typename M::T *s_w) {
+    typedef typename M::T T;
+    __shared__ T s_U, s_T, s_before, s_prevE, s_E;
+    __shared__ long long s_ts;
+    __shared__ unsigned long long s_found;
+    const T *segs = reinterpret_cast<const T *>(a.segs);
+    const uint64_t nseg = (a.n + kSeg - 1) / kSeg;
+    // The segment sums are read in coalesced waves: wave j covers segments
+    // [j*256*V, (j+1)*256*V), thread t the V = 16/sizeof(T) segments at
+    // j*256*V + t*V (one 16-byte load). Level 1: per-wave sums (a transposed
+    // warp reduction of up to 32 waves per pass, then across warps); level 2:
+    // the target wave reloaded and scanned by the block.
+    constexpr int V = 16 / (int)sizeof(T);
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const uint64_t per_wave = (uint64_t)kInitThreads * V;
+    const int W = (int)((nseg + per_wave - 1) / per_wave); // <= 64 (n <= 2^24)
+    __shared__ T s_C[64];
+    __shared__ T s_wc[kInitThreads / 32][32];
+#ifdef CQG_INIT_TIMING
+    unsigned long long _q = clock64();
+#define LTIME(i) do { if (threadIdx.x == 0) { const unsigned long long _n = clock64(); g_loc_phase[i] += _n - _q; _q = _n; } } while (0)
+#else
+#define LTIME(i) do { } while (0)
+#endif
+    // this thread's V segment sums of wave j (0 past the end): e0, e1 (V == 2)
+#define WAVE_ELEM(j, e0, e1)                                                                     \
+    do { /* branch-free: clamped address, masked value (loads stay in flight together) */       \
+        const uint64_t s_ = (uint64_t)(j) * per_wave + (uint64_t)t * V;                          \
+        const bool in0_ = s_ < nseg, in1_ = s_ + 1 < nseg;                                       \
+        const uint64_t sc_ = in0_ ? s_ : 0;                                                      \
+        if (V == 2) {                                                                            \
+            const uint4 q_ = __ldcg(reinterpret_cast<const uint4 *>(segs + sc_));                \
+            e0 = in0_ ? (T)(((unsigned long long)q_.y << 32) | q_.x) : (T)0;                     \
+            e1 = in1_ ? (T)(((unsigned long long)q_.w << 32) | q_.z) : (T)0;                     \
+        } else {                                                                                 \
+            const T q_ = segs[sc_];                                                              \
+            e0 = in0_ ? q_ : (T)0;                                                               \
+            e1 = 0;                                                                              \
+        }                                                                                        \
+    } while (0)
+    for (int g = 0; g < W; g += 32) {
+        T v[32];
+#pragma unroll
+        for (int u = 0; u < 32; ++u) {
+            T e0, e1;
+            WAVE_ELEM(g + u, e0, e1); // waves past W read as 0 (s_ >= nseg)
+            v[u] = e0 + e1;
+        }
+        // transposed reduction: lane l ends with the warp's sum of v[l]
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) {
+            const bool up = (lane & off) != 0;
+#pragma unroll
+            for (int i = 0; i < off; ++i) {
+                const T send = up ? v[i] : v[i + off];
+                const T keep = up ? v[i + off] : v[i];
+                v[i] = keep + M::shfl(send, lane ^ off);
+            }
+        }
+        s_wc[warp][lane] = v[0];
+        __syncthreads();
+        if (t < 32) {
+            T c = 0;
+#pragma unroll
+            for (int w = 0; w < kInitThreads / 32; ++w) c += s_wc[w][t];
+            if (g + t < 64) s_C[g + t] = c;
+        }
+        __syncthreads();
+    }
+    LTIME(0);
+    // total, target and the wave holding it (warp 0: up to 64 wave sums)
+    __shared__ int s_wv;
+    __shared__ T s_wbefore;
+    if (warp == 0) {
+        const T c0 = lane < W ? s_C[lane] : (T)0, c1 = lane + 32 < W ? s_C[lane + 32] : (T)0;
+        const T i0 = warp_incl<M>(c0);
+        const T tot0 = M::shfl(i0, 31);
+        const T i1 = warp_incl<M>(c1) + tot0;
+        const T tot = M::shfl(i1, 31);
+        const T U = M::target(nu, tot);
+        const unsigned m0 = __ballot_sync(0xffffffffu, i0 > U), m1 = __ballot_sync(0xffffffffu, i1 > U);
+        int wv = -1;
+        T before = 0;
+        if (m0) {
+            const int l = __ffs(m0) - 1;
+            wv = l;
+            before = M::shfl(i0 - c0, l);
+        } else if (m1) {
+            const int l = __ffs(m1) - 1;
+            wv = 32 + l;
+            before = M::shfl(i1 - c1, l);
+        }
+        if (lane == 0) {
+            s_U = U;
+            s_T = tot;
+            s_wv = wv;
+            s_wbefore = before;
+            s_ts = -1;
+            s_found = ~0ull;
+        }
+    }
+    __syncthreads();
+    const T U = s_U, tot = s_T;
+    if (s_wv >= 0) { // the wave: a block scan over the threads' V-segment groups
+        T e0, e1;
+        WAVE_ELEM(s_wv, e0, e1);
+        const T l = e0 + e1;
+        T btot;
+        const T start = s_wbefore + block_excl<M>(l, s_w, &btot);
+        if (start <= U && start + l > U) {
+            const uint64_t s0 = (uint64_t)s_wv * per_wave + (uint64_t)t * V;
+            if (V == 1 || start + e0 > U) {
+                s_ts = (long long)s0;
+                s_before = start;
+            } else {
+                s_ts = (long long)(s0 + 1);
+                s_before = start + e0;
+            }
+        }
+    }
+    __syncthreads();
+    LTIME(1);
+    const long long ts = s_ts;
+    if (ts >= 0) {
+        const uint64_t base = (uint64_t)ts * kSeg + 4ull * threadIdx.x;
+        // branch-free gathers (clamped indices, masked masses): all in flight
+        T m[4];
+        T l4 = 0;
+        uint32_t hp[4], cn[4], mv[4];
+        bool ok[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint64_t i = base + j;
+            ok[j] = 4 * threadIdx.x + j < (unsigned)kSeg && i < a.n;
+            const uint64_t ic = ok[j] ? i : 0;
+            hp[j] = a.hpos ? __ldg(a.hpos + ic) : (uint32_t)ic;
+            cn[j] = __ldg(a.counts + ic);
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) mv[j] = md[(uint64_t)hp[j] * (uint64_t)a.mds];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            m[j] = ok[j] ? M::mass_c(a, cn[j], mv[j]) : (T)0;
+            l4 += m[j];
+        }
+        T btot;
+        const T start = s_before + block_excl<M>(l4, s_w, &btot);
+        if (start <= U && start + l4 > U) {
+            T acc = start;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const T nxt = acc + m[j];
+                if (nxt > U) {
+                    s_found = base + j;
+                    s_prevE = acc;
+                    s_E = nxt;
+                    break;
+                }
+                acc = nxt;
+            }
+        }
+    }
+    __syncthreads();
+    LTIME(2);
+    uint64_t idx;
+    bool ambiguous = false;
+    if (s_found == ~0ull || s_found >= a.n - 1) {
+        idx = a.n - 1; // the reference returns n-1 when no i < n-1 qualifies
+        if (!M::exact && a.n > 1) {
+            const T mlast = M::mass(a, a.n - 1, md_at(a, md, a.n - 1));
+            ambiguous = !(U > tot - mlast + M::bound(a.n, tot));
+        }
+    } else {
+        idx = s_found;
+        if (!M::exact) {
+            const T B2 = M::bound(a.n, tot);
+            ambiguous = !(s_E > U + B2) || (idx > 0 && !(U > s_prevE + B2));
+        }
+    }
+    if (ambiguous) { // uniform in the block
+        __shared__ unsigned long long s_seq;
+        if (threadIdx.x == 0) {
+            s_seq = sequential_draw(a, md, nu, 0);
+            atomicAdd(a.fallbacks, 1ull);
+        }
+        __syncthreads();
+        idx = s_seq;
+    }
+    __syncthreads();
+    return idx;
+}
+
+template <class M>
+__global__ void __launch_bounds__(kInitThreads, 3) init_kernel_tile(InitArgs a) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ typename M::T s_w[kInitThreads / 32];
+    __shared__ unsigned long long s_m[kInitThreads / 32];
+    const uint32_t *mdv = reinterpret_cast<const uint32_t *>(a.trec) + 1; // md at stride 2, via hpos
+    int par = 0;
+#ifdef CQG_INIT_TIMING
+    unsigned long long _gprev = clock64();
+#endif
+    uint64_t first;
+    if (a.kind == 1 || a.weighted_first) {
+        const uint64_t lo = (uint64_t)blockIdx.x * a.chunk;
+        const uint64_t hi = lo + a.chunk < a.n ? lo + a.chunk : a.n;
+        update_masses<M>(a, 0, 1, 0, 0, nullptr, nullptr, lo, hi, s_w);
+        grid.sync();
+        first = locate_draw<M>(a, grid, 0, a.nu[0], 1, nullptr, s_w);
+        grid.sync(); // the sums are rewritten below
+    } else {
+        first = a.first_index;
+    }
+    uint32_t clast = __ldg(a.colors + first);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        a.cen[0] = (double)((clast >> 16) & 255u);
+        a.cen[1] = (double)((clast >> 8) & 255u);
+        a.cen[2] = (double)(clast & 255u);
+    }
+    // Rounds: every block updates its tiles and arrives on a counter; block 0
+    // alone waits for all arrivals, picks the next centre (maximin: the max of
+    // the block maxima; k-means++: the draw) and publishes it; the others poll
+    // the published round number with back-off (a spinning grid barrier
+    // would load the memory system under block 0's locate).
+    unsigned long long *arrive = a.result + 6;
+    unsigned long long *flag = a.tflags + (size_t)blockIdx.x * kFlagStride; // this block's release word
+    const unsigned long long G = gridDim.x;
+    for (int k = 1; k < a.K; ++k) {
+        GTIME(4);
+        if (a.kind == 1 && k == 1) tile_first_sums<M>(a, clast);
+#ifdef CQG_INIT_TIMING
+        const unsigned long long _u0 = clock64();
+#endif
+        const unsigned long long wb = update_tiles<M>(a, k == 1, clast);
+        if (a.kind == 0 && (threadIdx.x & 31) == 0) s_m[threadIdx.x >> 5] = wb;
+        __syncthreads();
+#ifdef CQG_INIT_TIMING
+        if (threadIdx.x == 0) atomicMax(&g_tile_round_max, clock64() - _u0);
+#endif
+        if (threadIdx.x == 0) {
+            if (a.kind == 0) {
+                unsigned long long bm = 0;
+                for (int i = 0; i < kInitThreads / 32; ++i) bm = s_m[i] > bm ? s_m[i] : bm;
+                a.mparts[blockIdx.x] = bm;
+            }
+            __threadfence();
+            atomicAdd(arrive, 1ull);
+        }
+        GTIME(0);
+        if (blockIdx.x == 0) {
+            if (threadIdx.x == 0)
+                while (ld_acquire_u64(arrive) < G * (unsigned long long)k) __nanosleep(32);
+            __syncthreads();
+            GTIME(1);
+#ifdef CQG_INIT_TIMING
+            if (threadIdx.x == 0) {
+                g_coop_timing[7] += g_tile_round_max;
+                if (k < 1024) g_tile_rounds[k][0] += g_tile_round_max;
+                g_tile_round_max = 0;
+            }
+            const unsigned long long _l0 = clock64();
+#endif
+            uint64_t v;
+            if (a.kind == 0) {
+                unsigned long long bm = 0;
+                if (threadIdx.x < 32) {
+                    for (unsigned i = threadIdx.x; i < gridDim.x; i += 32) {
+                        const unsigned long long t = a.mparts[i];
+                        bm = t > bm ? t : bm;
+                    }
+                    for (int o = 16; o; o >>= 1) {
+                        const unsigned long long t = __shfl_xor_sync(0xffffffffu, bm, o);
+                        bm = t > bm ? t : bm;
+                    }
+                }
+                v = (uint64_t)(uint32_t)~(uint32_t)(bm & 0xFFFFFFFFull); // thread 0's value is used
+            } else {
+                v = locate_one_block<M>(a, a.nu[k], mdv, s_w);
+            }
+#ifdef CQG_INIT_TIMING
+            if (threadIdx.x == 0 && k < 1024) g_tile_rounds[k][1] += clock64() - _l0;
+#endif
+            if (threadIdx.x == 0) a.result[2] = v;
+            __syncthreads();
+            // release every block through its own word (no single hot L2 line)
+            for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x)
+                st_release_u64(a.tflags + (size_t)b * kFlagStride, (unsigned long long)k);
+            __syncthreads(); // block 0's own threads read the pick below
+            GTIME(2);
+        } else {
+            if (threadIdx.x == 0)
+                while (ld_acquire_u64(flag) < (unsigned long long)k) __nanosleep(64);
+            __syncthreads();
+            GTIME(3);
+        }
+        const uint64_t pick = *reinterpret_cast<volatile unsigned long long *>(a.result + 2);
+        __syncthreads(); // every thread has the pick before block 0 can overwrite it next round
+        clast = __ldg(a.colors + pick);
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            a.cen[3 * k] = (double)((clast >> 16) & 255u);
+            a.cen[3 * k + 1] = (double)((clast >> 8) & 255u);
+            a.cen[3 * k + 2] = (double)(clast & 255u);
+        }
     }
 }
 
@@ -1681,6 +2291,12 @@ static bool launch_cluster_init(cqg_ctx *ctx, InitArgs a) {
     return launch_cluster(ctx, a, init_cluster_kernel<M>, smem, a, ppt, ctx->use_mbar_init ? 1 : 0);
 }
 
+static int tile_grid(const cqg_ctx *ctx, uint64_t threads) {
+    uint64_t g = (threads + 255) / 256;
+    const uint64_t gmax = (uint64_t)ctx->num_sms * 8;
+    return (int)(g < 1 ? 1 : (g > gmax ? gmax : g));
+}
+
 void run_init(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *counts_d, uint64_t n, uint64_t P,
               int K, uint64_t seed, int kind, int weighted_first, double *centers_d) {
     cudaStream_t s = ctx->stream;
@@ -1726,14 +2342,40 @@ void run_init(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *counts_d, 
         if (exact ? launch_cluster_init<ExactMass>(ctx, c) : launch_cluster_init<FixedMass>(ctx, c)) return;
     }
     const bool rec = ctx->use_init_rec;
-    const void *kern = rec ? (exact ? (const void *)init_kernel_rec<ExactMass> : (const void *)init_kernel_rec<FixedMass>)
-                           : (exact ? (const void *)init_kernel<ExactMass> : (const void *)init_kernel<FixedMass>);
+    // colour-space tiles: every colour on its own Morton slot (a duplicate
+    // colour -- raw-pixel substrates -- keeps the record layout)
+    bool tile = rec && ctx->use_init_tile && n <= 0xFFFFFFFFull;
+    const uint64_t ntiles = (n + kTile - 1) / kTile;
+    uint32_t *tbits = nullptr, *tpref = nullptr, *tbsum = nullptr;
+    if (tile) {
+        const size_t words = kTileBitmapWords;
+        const size_t need = sizeof(uint32_t) * (2 * words + 1024 + 8) + sizeof(uint2) * n + sizeof(uint32_t) * 3 * n +
+                            (sizeof(uint2) + sizeof(uint32_t) + sizeof(unsigned long long)) * ntiles + 512 +
+                            sizeof(unsigned long long) * kFlagStride * (kLocateMax + 1);
+        unsigned char *base = static_cast<unsigned char *>(ctx->inittile.ensure(need));
+        tbits = reinterpret_cast<uint32_t *>(base);
+        tpref = tbits + words;
+        tbsum = tpref + words;
+        uint32_t *dup_d = tbsum + 1024;
+        CQG_CUDA(cudaMemsetAsync(tbits, 0, sizeof(uint32_t) * words, s));
+        CQG_CUDA(cudaMemsetAsync(dup_d, 0, sizeof(uint32_t), s));
+        const int g = tile_grid(ctx, n);
+        tile_mark_kernel<<<g, 256, 0, s>>>(colors_d, n, tbits, dup_d);
+        launched(ctx);
+        uint32_t *dup_h = static_cast<uint32_t *>(ctx->pinned.ensure(4096));
+        CQG_CUDA(cudaMemcpyAsync(dup_h, dup_d, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+        CQG_CUDA(cudaStreamSynchronize(s));
+        tile = *dup_h == 0;
+    }
+    const void *kern = tile  ? (exact ? (const void *)init_kernel_tile<ExactMass> : (const void *)init_kernel_tile<FixedMass>)
+                       : rec ? (exact ? (const void *)init_kernel_rec<ExactMass> : (const void *)init_kernel_rec<FixedMass>)
+                             : (exact ? (const void *)init_kernel<ExactMass> : (const void *)init_kernel<FixedMass>);
     int occ = 0;
     CQG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kInitThreads, 0));
     if (occ < 1) occ = 1;
     // k-means++ record rounds are load-latency bound: 3 blocks per SM (maximin
     // measured faster with 2: one barrier per round, fewer arrivals)
-    const int per_want = rec && kind == 1 ? 3 : 2;
+    const int per_want = (rec && kind == 1) || tile ? 3 : 2;
     const int per_sm = occ > per_want ? per_want : occ;
     uint64_t grid = (uint64_t)ctx->num_sms * (uint64_t)per_sm;
     if (grid > (uint64_t)kLocateMax) grid = kLocateMax; // warp_locate scans <= kLocateMax block sums
@@ -1776,6 +2418,38 @@ void run_init(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *counts_d, 
     a.result = res;
     a.fallbacks = res + 4;
     a.cen = centers_d;
+    if (tile) {
+        unsigned char *tb = reinterpret_cast<unsigned char *>(tbsum + 1024 + 8);
+        uint2 *trec = reinterpret_cast<uint2 *>(tb);
+        uint32_t *tidx = reinterpret_cast<uint32_t *>(trec + n);
+        uint32_t *tcnt = tidx + n;
+        uint32_t *hpos = tcnt + n;
+        uint2 *tbox = reinterpret_cast<uint2 *>((reinterpret_cast<uintptr_t>(hpos + n) + 7) & ~(uintptr_t)7);
+        uint32_t *tmax = reinterpret_cast<uint32_t *>(tbox + ntiles);
+        unsigned long long *tkey = reinterpret_cast<unsigned long long *>(
+            (reinterpret_cast<uintptr_t>(tmax + ntiles) + 7) & ~(uintptr_t)7);
+        tile_scan_blocks<<<kTileBitmapWords / 1024, 1024, 0, s>>>(tbits, tpref, tbsum);
+        tile_scan_top<<<1, 1024, 0, s>>>(tbsum, kTileBitmapWords / 1024);
+        const int g = tile_grid(ctx, n);
+        tile_place_kernel<<<g, 256, 0, s>>>(colors_d, counts_d, n, tbits, tpref, tbsum, trec, tidx,
+                                            kind == 1 ? tcnt : nullptr, kind == 1 ? hpos : nullptr);
+        tile_box_kernel<<<tile_grid(ctx, ntiles * 32), 256, 0, s>>>(trec, n, ntiles, tbox, tmax);
+        launched(ctx, 4);
+        a.md = nullptr;
+        a.mds = 2;
+        a.hpos = kind == 1 ? hpos : nullptr;
+        a.trec = trec;
+        a.tidx = tidx;
+        a.tcnt = tcnt;
+        a.tbox = tbox;
+        a.tmax = tmax;
+        a.tkey = tkey;
+        a.ntiles = ntiles;
+        unsigned long long *fl = reinterpret_cast<unsigned long long *>(
+            (reinterpret_cast<uintptr_t>(tkey + ntiles) + 255) & ~(uintptr_t)255);
+        CQG_CUDA(cudaMemsetAsync(fl, 0, sizeof(unsigned long long) * kFlagStride * grid, s));
+        a.tflags = fl;
+    }
     void *args[] = {&a};
     const int pb = prof_begin(ctx);
     CQG_CUDA(launch_cooperative(ctx, kern, dim3((unsigned)grid), dim3(kInitThreads), args, 0));
@@ -1809,6 +2483,24 @@ extern "C" int cqg_dbg_init_timing(unsigned long long *out, int reset) {
 #endif
 
 #ifdef CQG_INIT_TIMING
+extern "C" int cqg_dbg_loc_phase(unsigned long long *out, int reset) {
+    if (cudaMemcpyFromSymbol(out, cqg::g_loc_phase, sizeof(cqg::g_loc_phase)) != cudaSuccess) return 1;
+    if (reset) {
+        unsigned long long z[4] = {};
+        cudaMemcpyToSymbol(cqg::g_loc_phase, z, sizeof(z));
+    }
+    return 0;
+}
+
+extern "C" int cqg_dbg_tile_rounds(unsigned long long *out, int reset) {
+    if (cudaMemcpyFromSymbol(out, cqg::g_tile_rounds, sizeof(cqg::g_tile_rounds)) != cudaSuccess) return 1;
+    if (reset) {
+        static unsigned long long z[1024 * 2];
+        cudaMemcpyToSymbol(cqg::g_tile_rounds, z, sizeof(z));
+    }
+    return 0;
+}
+
 extern "C" int cqg_dbg_coop_timing(unsigned long long *out, int reset) {
     if (cudaMemcpyFromSymbol(out, cqg::g_coop_timing, 8 * sizeof(unsigned long long)) != cudaSuccess) return 1;
     if (reset) {

@@ -1,9 +1,12 @@
 """Initialisers on the cooperative (large substrate) kernels: bit-exact
-against the oracle for both grid layouts -- {colour, md} records updated in
-place (default) and the ping-pong layout (CQG_NO_INIT_REC=1) -- and for both
-mass arithmetics (P a power of two: exact integers; otherwise 2^-88 fixed
-point with the sequential FP64 fallback). Small inputs reach the same kernels
-with the cluster initialiser switched off (CQG_NO_CLUSTER_INIT=1).
+against the oracle for the three grid layouts -- colour-space tiles with box
+pruning (default), {colour, md} records in histogram order
+(CQG_NO_INIT_TILE=1) and the ping-pong layout (CQG_NO_INIT_REC=1) -- and for
+both mass arithmetics (P a power of two: exact integers; otherwise 2^-88
+fixed point with the sequential FP64 fallback). Small inputs reach the same
+kernels with the cluster initialiser switched off (CQG_NO_CLUSTER_INIT=1).
+A substrate with repeated colours (no one-colour-per-slot tile layout) falls
+back to the record layout.
 """
 import os
 
@@ -31,7 +34,8 @@ def _ctx(**env):
 
 @pytest.fixture(scope="module")
 def ctxs():
-    cs = {"rec": _ctx(CQG_NO_CLUSTER_INIT="1"),
+    cs = {"tile": _ctx(CQG_NO_CLUSTER_INIT="1"),
+          "rec": _ctx(CQG_NO_CLUSTER_INIT="1", CQG_NO_INIT_TILE="1"),
           "pingpong": _ctx(CQG_NO_CLUSTER_INIT="1", CQG_NO_INIT_REC="1")}
     yield cs
     for c in cs.values():
@@ -51,14 +55,14 @@ def _check(ctx, oracle, img, K, seed):
     return c.size
 
 
-@pytest.mark.parametrize("layout", ["rec", "pingpong"])
+@pytest.mark.parametrize("layout", ["tile", "rec", "pingpong"])
 @pytest.mark.parametrize("w,h,K,seed", [(40, 40, 8, 3), (300, 200, 64, 9), (512, 512, 33, 5)])
 def test_init_cooperative_small(ctxs, oracle, layout, w, h, K, seed):
     img = synth_image(w, h, seed, nblobs=10, sigma=15.0, noise=0.02)
     _check(ctxs[layout], oracle, img, K, seed)
 
 
-@pytest.mark.parametrize("layout", ["rec", "pingpong"])
+@pytest.mark.parametrize("layout", ["tile", "rec", "pingpong"])
 @pytest.mark.parametrize("w,h", [(1024, 1024), (1100, 900)])  # P = 2^20 (exact) / not a power of two
 def test_init_cooperative_large(ctxs, ctx, oracle, layout, w, h):
     img = synth_image(w, h, 4242, nblobs=30, sigma=25.0, noise=0.7)
@@ -66,6 +70,42 @@ def test_init_cooperative_large(ctxs, ctx, oracle, layout, w, h):
     assert n > 16 * 1024 * 32  # beyond the cluster initialiser
     # the default context takes the same path at this size
     _check(ctx, oracle, img, 64, 4242)
+
+
+@pytest.mark.parametrize("kind", ["kpp", "mmx"])
+def test_init_tile_repeated_colours(ctxs, oracle, kind):
+    # every colour twice (with different counts): two points share a Morton
+    # slot, so the tile layout declines and the record layout runs
+    rng = np.random.default_rng(17)
+    base = np.unique(rng.integers(0, 1 << 24, 150_000, dtype=np.uint32))
+    c = np.concatenate([base, base[::-1]]).astype(np.uint32)
+    n = rng.integers(1, 5, c.size).astype(np.uint32)
+    P = int(n.sum())
+    hist = quant.WeightedHistogram(colors=quant.unpack_colors(c), weights=n / P, counts=n,
+                                   source_pixel_count=P, packed=c)
+    sc = quant.SeedConfig(k=48, seed=6)
+    f, o = (quant.init_kmeanspp, oracle.init_kmeanspp) if kind == "kpp" else (quant.init_maximin, oracle.init_maximin)
+    for layout in ("tile", "rec"):
+        assert np.array_equal(f(hist, sc, ctx=ctxs[layout]), o(c, n, P, 48, 6))
+
+
+def test_init_tile_sparse_colours(ctxs, oracle):
+    # colours spread thin over the cube (large tile boxes, little pruning) and
+    # clustered ones (tight boxes) in one substrate
+    rng = np.random.default_rng(23)
+    sparse = rng.integers(0, 1 << 24, 200_000, dtype=np.uint32)
+    blob = (np.clip(rng.normal(128, 6, (600_000, 3)), 0, 255).astype(np.uint32))
+    dense = (blob[:, 0] << 16) | (blob[:, 1] << 8) | blob[:, 2]
+    c = np.unique(np.concatenate([sparse, dense]))
+    rng.shuffle(c)
+    c = c.astype(np.uint32)
+    n = rng.integers(1, 4, c.size).astype(np.uint32)
+    P = int(n.sum())
+    hist = quant.WeightedHistogram(colors=quant.unpack_colors(c), weights=n / P, counts=n,
+                                   source_pixel_count=P, packed=c)
+    sc = quant.SeedConfig(k=96, seed=11)
+    assert np.array_equal(quant.init_kmeanspp(hist, sc, ctx=ctxs["tile"]), oracle.init_kmeanspp(c, n, P, 96, 11))
+    assert np.array_equal(quant.init_maximin(hist, sc, ctx=ctxs["tile"]), oracle.init_maximin(c, n, P, 96, 11))
 
 
 @pytest.mark.slow

@@ -57,14 +57,33 @@ def run(name):
         print(f"{'total':14s} {tot / rounds:8.0f} cycles/round")
     # cooperative record kernel (large substrates; forced with CQG_NO_CLUSTER_INIT=1)
     L.cqg_dbg_coop_timing(buf, 1)
+    tr = (C.c_ulonglong * 2048)()
+    lp = (C.c_ulonglong * 4)()
+    if hasattr(L, "cqg_dbg_tile_rounds"):
+        L.cqg_dbg_tile_rounds(tr, 1)
+        L.cqg_dbg_loc_phase(lp, 1)
     initf(hist, sc, ctx=ctx)
     L.cqg_dbg_coop_timing(buf, 1)
+    if hasattr(L, "cqg_dbg_tile_rounds"):
+        L.cqg_dbg_tile_rounds(tr, 0)
+        L.cqg_dbg_loc_phase(lp, 0)
+        if lp[0]:
+            r1 = cfg.k - 1
+            print(f"tile locate: segment sums {lp[0] / r1:8.0f}  owner run {lp[1] / r1:8.0f}  "
+                  f"points {lp[2] / r1:8.0f} cycles/round")
+        sel = [1, 2, 3, 5, 8, 12, 20, 40, 80, 160, cfg.k - 1]
+        if any(tr[2 * r] for r in sel if r < 1024):
+            print("tile rounds (slowest block update / block-0 locate, cycles): " +
+                  "  ".join(f"r{r}:{tr[2 * r]}/{tr[2 * r + 1]}" for r in sel if r < min(cfg.k, 1024)))
     names = ["update", "grid_sync_1", "locate", "grid_sync_2", "tail"]
     tot = sum(buf[i] for i in range(5))
     if tot:
         rounds1 = cfg.k - 1
         for i, nm in enumerate(names):
             print(f"coop {nm:14s} {buf[i] / rounds1:8.0f} cycles/round  {100 * buf[i] / tot:5.1f}%")
+        if buf[5]:  # tile layout
+            print(f"coop tiles updated {buf[5] / rounds1:10.0f}/round  points changed {buf[6] / rounds1:10.0f}/round  "
+                  f"slowest block update {buf[7] / rounds1:8.0f} cycles/round")
     # persistent Lloyd kernel phases (block 0, thread 0), per WALK iteration
     init = initf(hist, sc, ctx=ctx)
     opts = quant.ClusterOptions(quant.Termination(fixed_iterations=cfg.fixed_iterations or None))
