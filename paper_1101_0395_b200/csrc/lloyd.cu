@@ -400,6 +400,7 @@ __global__ void __launch_bounds__(kSweepThreads, 2) lloyd_persistent_kernel(Swee
     la.queue = a.queue + lo;
     la.qn = &s_qn;
     bool full = first_full != 0;
+    bool cen_smem = false; // s_end[0, 3K) holds the current centres (after a finalise)
 #ifdef CQG_INIT_TIMING
     unsigned long long _tprev = clock64();
     unsigned long long _bprev = _tprev;
@@ -450,8 +451,10 @@ __global__ void __launch_bounds__(kSweepThreads, 2) lloyd_persistent_kernel(Swee
                         s_pre[(e / L) * (kNdcPrefix + 2) + e % L] = a.dcode[(size_t)(e / L) * a.Kpow + e % L];
                 }
                 __syncthreads();
-                nd = ndc_range_pre<2>(a.colors, a.labels, lo, hi, 0, 2ull * blockDim.x, a.cen, a.dsorted, a.Kpow,
-                                      s_pre);
+                // centres: this block's shared copy from the last finalise
+                // (a relaunch after a repair starts from the global ones)
+                nd = ndc_range_pre<2>(a.colors, a.labels, lo, hi, 0, 2ull * blockDim.x, cen_smem ? s_end : a.cen,
+                                      a.dsorted, a.Kpow, s_pre);
             } else {
                 nd = ndc_range<2>(a.colors, a.labels, lo, hi, 0, 2ull * blockDim.x, a.cen, a.dsorted, a.Kpow);
             }
@@ -478,6 +481,7 @@ __global__ void __launch_bounds__(kSweepThreads, 2) lloyd_persistent_kernel(Swee
         _bprev = clock64();
 #endif
         const bool ok = iter_end_body(ia, s_end, s_fc, s_tau, true);
+        cen_smem = true;
         PTIME(4);
         grid.sync();
         PTIME(5);

@@ -451,6 +451,10 @@ __device__ __forceinline__ void sweep_tiles(const SweepArgs &a, uint64_t lo, uin
         float2 xr2[PP], xg2[PP], xb2[PP], xx2[PP];
         uint32_t col[PPT];
         uint32_t pidx[PPT]; // point index (< 2^24 unique colours)
+        // small tiles: the resolve's label and count issued with the colour
+        // (one memory round trip per tile instead of two more per point)
+        constexpr bool kPre = PPT <= 4;
+        uint32_t plab[kPre ? PPT : 1], pcnt[kPre ? PPT : 1];
         float b1[PPT], b2[PPT];
         int g1[PPT];
 #pragma unroll
@@ -458,6 +462,10 @@ __device__ __forceinline__ void sweep_tiles(const SweepArgs &a, uint64_t lo, uin
             const uint64_t slot = slot_of(base, i);
             pidx[i] = slot < hi ? (LIST ? list[slot] : (uint32_t)slot) : 0u;
             col[i] = slot < hi ? __ldg(a.colors + pidx[i]) : 0u;
+            if (kPre) {
+                plab[kPre ? i : 0] = MODE == MODE_WALK ? a.labels[pidx[i]] : 0u;
+                pcnt[kPre ? i : 0] = __ldg(a.counts + pidx[i]);
+            }
             const float r = (float)((col[i] >> 16) & 255u), g = (float)((col[i] >> 8) & 255u),
                         b = (float)(col[i] & 255u);
             float xx = r * r + g * g + b * b; // exact: integers < 2^18
@@ -475,6 +483,7 @@ __device__ __forceinline__ void sweep_tiles(const SweepArgs &a, uint64_t lo, uin
             g1[i] = 0;
         }
         STIME(4);
+#pragma unroll 2
         for (int j = 0; j < Kp; j += kGroup) {
             float gm[PPT]; // this group's minimum per point
 #pragma unroll
@@ -576,15 +585,15 @@ __device__ __forceinline__ void sweep_tiles(const SweepArgs &a, uint64_t lo, uin
             }
             const uint32_t r = (col[i] >> 16) & 255u, g = (col[i] >> 8) & 255u, b = col[i] & 255u;
             if (MODE == MODE_WALK && valid) {
-                const int prev = (int)a.labels[idx];
+                const int prev = kPre ? (int)plab[kPre ? i : 0] : (int)a.labels[idx];
                 if (!flag && j1 != prev) {
-                    const uint32_t cnt = __ldg(a.counts + idx);
+                    const uint32_t cnt = kPre ? pcnt[kPre ? i : 0] : __ldg(a.counts + idx);
                     a.labels[idx] = (uint32_t)j1;
                     accumulate64(s_acc64, j1, cnt, r, g, b, +1);
                     accumulate64(s_acc64, prev, cnt, r, g, b, -1);
                 }
             } else if (valid && !flag) {
-                const uint32_t cnt = __ldg(a.counts + idx);
+                const uint32_t cnt = kPre ? pcnt[kPre ? i : 0] : __ldg(a.counts + idx);
                 if (MODE == MODE_FULL) a.labels[idx] = (uint32_t)j1;
                 else if (a.lut8) a.lut8[col[i]] = (uint8_t)j1;
                 else a.lut32[col[i]] = (uint32_t)j1;
