@@ -142,6 +142,43 @@ __device__ unsigned long long g_block_timing[1024 * 3]; // per block: ndc, sweep
     } while (0)
 #endif
 
+// Bitonic sort of KP (key, index) pairs held one per thread (threads >= KP
+// idle in the exchanges): strides < 32 by warp shuffles, larger strides
+// through shared memory (s_key / s_idx, KP entries). All stages unrolled.
+template <int KP>
+__device__ __forceinline__ void bitonic_reg(unsigned long long &key, int &r, int t, unsigned long long *s_key,
+                                            int *s_idx) {
+    const bool in = t < KP;
+#pragma unroll
+    for (int size = 2; size <= KP; size <<= 1) {
+#pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            unsigned long long ok;
+            int orr;
+            if (stride >= 32) {
+                __syncthreads();
+                if (in) {
+                    s_key[t] = key;
+                    s_idx[t] = r;
+                }
+                __syncthreads();
+                ok = in ? s_key[t ^ stride] : ~0ull;
+                orr = in ? s_idx[t ^ stride] : 0x7FFFFFFF;
+            } else {
+                ok = __shfl_xor_sync(0xffffffffu, key, stride);
+                orr = __shfl_xor_sync(0xffffffffu, r, stride);
+            }
+            const bool up = (t & size) == 0;
+            const bool low = (t & stride) == 0;
+            const bool other_less = ok < key || (ok == key && orr < r);
+            if (other_less == (low == up)) { // the low slot keeps the smaller key when ascending
+                key = ok;
+                r = orr;
+            }
+        }
+    }
+}
+
 __device__ bool iter_end_body(const IterArgs &a, double *sm, float *fc_dst, float *tau_dst, bool fc_every_block) {
 #ifdef CQG_INIT_TIMING
     const unsigned long long _ie0 = clock64();
@@ -272,41 +309,22 @@ __device__ bool iter_end_body(const IterArgs &a, double *sm, float *fc_dst, floa
         }
         __syncthreads();
         if (a.Kpow <= (int)blockDim.x) {
-            // one element per thread, in registers: strides < 32 by warp
-            // shuffles, larger strides through shared memory
+            // one element per thread, in registers, the stage loops unrolled
+            // for the padded row length; keys compare as (u64 bits of d >= 0, index)
             const int t = threadIdx.x;
-            double d = t < a.Kpow ? s_d[t] : kInf;
+            unsigned long long key = t < a.Kpow ? (unsigned long long)__double_as_longlong(s_d[t]) : ~0ull;
             int r = t < a.Kpow ? s_rank[t] : 0x7FFFFFFF;
-            for (int size = 2; size <= a.Kpow; size <<= 1) {
-                for (int stride = size >> 1; stride > 0; stride >>= 1) {
-                    double od;
-                    int orr;
-                    if (stride >= 32) {
-                        __syncthreads();
-                        if (t < a.Kpow) {
-                            s_d[t] = d;
-                            s_rank[t] = r;
-                        }
-                        __syncthreads();
-                        od = t < a.Kpow ? s_d[t ^ stride] : kInf;
-                        orr = t < a.Kpow ? s_rank[t ^ stride] : 0x7FFFFFFF;
-                    } else {
-                        od = __shfl_xor_sync(0xffffffffu, d, stride);
-                        orr = __shfl_xor_sync(0xffffffffu, r, stride);
-                    }
-                    const bool up = (t & size) == 0;
-                    const bool low = (t & stride) == 0;
-                    const bool other_less = od < d || (od == d && orr < r);
-                    // the low slot keeps the smaller key when ascending
-                    if (other_less == (low == up)) {
-                        d = od;
-                        r = orr;
-                    }
-                }
+            unsigned long long *s_key = reinterpret_cast<unsigned long long *>(s_d);
+            switch (a.Kpow) {
+                case 512: bitonic_reg<512>(key, r, t, s_key, s_rank); break;
+                case 256: bitonic_reg<256>(key, r, t, s_key, s_rank); break;
+                case 128: bitonic_reg<128>(key, r, t, s_key, s_rank); break;
+                case 64: bitonic_reg<64>(key, r, t, s_key, s_rank); break;
+                default: bitonic_reg<32>(key, r, t, s_key, s_rank); break; // Kpow <= 32: padding lanes sort last
             }
             __syncthreads();
             if (t < a.Kpow) {
-                s_d[t] = d;
+                s_d[t] = __longlong_as_double((long long)key);
                 s_rank[t] = r;
             }
             __syncthreads();
