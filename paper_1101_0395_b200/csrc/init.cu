@@ -70,7 +70,8 @@ struct InitArgs {
     // colour, kTile per tile; md values are read through hpos (histogram
     // index -> tile position) by the locate
     const uint32_t *hpos; // null: md is indexed by histogram position
-    uint2 *trec;          // {colour, md} in tile order
+    const uint32_t *tcol; // colour of each tile-order point
+    uint32_t *tmd;        // md of each tile-order point
     const uint32_t *tidx; // histogram index of each tile-order point
     const uint32_t *tcnt; // count of each tile-order point (k-means++)
     const uint2 *tbox;    // per tile: packed min / max colour channels
@@ -876,24 +877,26 @@ __global__ void __launch_bounds__(1024) tile_scan_top(uint32_t *bsum, int nb) {
     if ((int)threadIdx.x < nb) bsum[threadIdx.x] = e;
 }
 
-// setup 3: place every point at its Morton rank
+// setup 3: place every point at its Morton rank, one destination array per
+// launch (which = 0: colour, 1: histogram index (+ hpos), 2: count), so each
+// pass's random 4-byte stores land in an L2-resident 4n-byte array and merge
+// into whole sectors before write-back (one pass writing all of them
+// thrashed L2 with partial-sector read-modify-writes)
 __global__ void tile_place_kernel(const uint32_t *__restrict__ colors, const uint32_t *__restrict__ counts, uint64_t n,
                                   const uint32_t *__restrict__ bits, const uint32_t *__restrict__ pref,
-                                  const uint32_t *__restrict__ bsum, uint2 *__restrict__ trec,
-                                  uint32_t *__restrict__ tidx, uint32_t *__restrict__ tcnt, uint32_t *__restrict__ hpos) {
+                                  const uint32_t *__restrict__ bsum, uint32_t *__restrict__ dst, int which,
+                                  uint32_t *__restrict__ hpos) {
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t c = __ldg(colors + i);
         const uint32_t m = tile_morton(c), w = m >> 5;
         const uint32_t pos = bsum[w >> 10] + pref[w] + (uint32_t)__popc(bits[w] & ((1u << (m & 31u)) - 1u));
-        trec[pos] = make_uint2(c, 0xFFFFFFFFu);
-        tidx[pos] = (uint32_t)i;
-        if (tcnt) tcnt[pos] = __ldg(counts + i);
-        if (hpos) hpos[i] = pos;
+        dst[pos] = which == 0 ? c : (which == 1 ? (uint32_t)i : __ldg(counts + i));
+        if (which == 1 && hpos) hpos[i] = pos;
     }
 }
 
 // setup 4: per tile the colour box (one warp per tile)
-__global__ void tile_box_kernel(const uint2 *__restrict__ trec, uint64_t n, uint64_t ntiles, uint2 *__restrict__ tbox,
+__global__ void tile_box_kernel(const uint32_t *__restrict__ tcol, uint64_t n, uint64_t ntiles, uint2 *__restrict__ tbox,
                                 uint32_t *__restrict__ tmax) {
     const int lane = threadIdx.x & 31;
     const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -903,7 +906,7 @@ __global__ void tile_box_kernel(const uint2 *__restrict__ trec, uint64_t n, uint
         for (int u = 0; u < kTile / 32; ++u) {
             const uint64_t p = t * kTile + u * 32 + lane;
             if (p < n) {
-                const uint32_t c = trec[p].x;
+                const uint32_t c = tcol[p];
                 const uint32_t r = (c >> 16) & 255u, g = (c >> 8) & 255u, b = c & 255u;
                 lr = min(lr, r), lg = min(lg, g), lb = min(lb, b);
                 hr = max(hr, r), hg = max(hg, g), hb = max(hb, b);
@@ -988,7 +991,7 @@ __device__ unsigned long long update_tiles(const InitArgs &a, bool full, uint32_
             for (int u = 0; u < kTile / 32; ++u) {
                 const uint64_t p = tt * kTile + u * 32 + lane;
                 const uint64_t pc = p < a.n ? p : a.n - 1;
-                r[u] = a.trec[pc];
+                r[u] = make_uint2(__ldg(a.tcol + pc), a.tmd[pc]);
                 cn[u] = (a.kind == 1 && !full) ? __ldg(a.tcnt + pc) : 0u;
                 hx[u] = (a.kind == 0 || !full) ? __ldg(a.tidx + pc) : 0u;
             }
@@ -1005,7 +1008,7 @@ __device__ unsigned long long update_tiles(const InitArgs &a, bool full, uint32_
             for (int u = 0; u < kTile / 32; ++u) {
                 const uint64_t p = tt * kTile + u * 32 + lane;
                 if ((chg >> u) & 1u) {
-                    a.trec[p].y = dn[u];
+                    a.tmd[p] = dn[u];
                     if (a.kind == 1 && !full) {
                         const T dm = M::mass_c(a, cn[u], r[u].y) - M::mass_c(a, cn[u], dn[u]);
                         if (dm != (T)0) atomic_sub_mass(segs + hx[u] / kSeg, dm);
@@ -1268,7 +1271,7 @@ __global__ void __launch_bounds__(kInitThreads, 3) init_kernel_tile(InitArgs a) 
     cg::grid_group grid = cg::this_grid();
     __shared__ typename M::T s_w[kInitThreads / 32];
     __shared__ unsigned long long s_m[kInitThreads / 32];
-    const uint32_t *mdv = reinterpret_cast<const uint32_t *>(a.trec) + 1; // md at stride 2, via hpos
+    const uint32_t *mdv = a.tmd; // md via hpos
     int par = 0;
 #ifdef CQG_INIT_TIMING
     unsigned long long _gprev = clock64();
@@ -2420,8 +2423,9 @@ void run_init(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *counts_d, 
     a.cen = centers_d;
     if (tile) {
         unsigned char *tb = reinterpret_cast<unsigned char *>(tbsum + 1024 + 8);
-        uint2 *trec = reinterpret_cast<uint2 *>(tb);
-        uint32_t *tidx = reinterpret_cast<uint32_t *>(trec + n);
+        uint32_t *tcol = reinterpret_cast<uint32_t *>(tb);
+        uint32_t *tmd = tcol + n;
+        uint32_t *tidx = tmd + n;
         uint32_t *tcnt = tidx + n;
         uint32_t *hpos = tcnt + n;
         uint2 *tbox = reinterpret_cast<uint2 *>((reinterpret_cast<uintptr_t>(hpos + n) + 7) & ~(uintptr_t)7);
@@ -2431,14 +2435,18 @@ void run_init(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *counts_d, 
         tile_scan_blocks<<<kTileBitmapWords / 1024, 1024, 0, s>>>(tbits, tpref, tbsum);
         tile_scan_top<<<1, 1024, 0, s>>>(tbsum, kTileBitmapWords / 1024);
         const int g = tile_grid(ctx, n);
-        tile_place_kernel<<<g, 256, 0, s>>>(colors_d, counts_d, n, tbits, tpref, tbsum, trec, tidx,
-                                            kind == 1 ? tcnt : nullptr, kind == 1 ? hpos : nullptr);
-        tile_box_kernel<<<tile_grid(ctx, ntiles * 32), 256, 0, s>>>(trec, n, ntiles, tbox, tmax);
-        launched(ctx, 4);
+        tile_place_kernel<<<g, 256, 0, s>>>(colors_d, counts_d, n, tbits, tpref, tbsum, tcol, 0, nullptr);
+        tile_place_kernel<<<g, 256, 0, s>>>(colors_d, counts_d, n, tbits, tpref, tbsum, tidx, 1,
+                                            kind == 1 ? hpos : nullptr);
+        if (kind == 1) tile_place_kernel<<<g, 256, 0, s>>>(colors_d, counts_d, n, tbits, tpref, tbsum, tcnt, 2, nullptr);
+        CQG_CUDA(cudaMemsetAsync(tmd, 0xFF, sizeof(uint32_t) * n, s));
+        tile_box_kernel<<<tile_grid(ctx, ntiles * 32), 256, 0, s>>>(tcol, n, ntiles, tbox, tmax);
+        launched(ctx, kind == 1 ? 6 : 5);
         a.md = nullptr;
-        a.mds = 2;
+        a.mds = 1;
         a.hpos = kind == 1 ? hpos : nullptr;
-        a.trec = trec;
+        a.tcol = tcol;
+        a.tmd = tmd;
         a.tidx = tidx;
         a.tcnt = tcnt;
         a.tbox = tbox;
