@@ -223,6 +223,8 @@ cqg_ctx *cqg_create(int device) {
         ctx->use_init_rec = !(nr && nr[0] == '1');
         const char *nt = getenv("CQG_NO_INIT_TILE");
         ctx->use_init_tile = !(nt && nt[0] == '1');
+        const char *tm = getenv("CQG_INIT_TILE_MIN");
+        if (tm) ctx->init_tile_min = strtoull(tm, nullptr, 10);
         const char *np = getenv("CQG_NO_PRUNE");
         ctx->use_prune = !(np && np[0] == '1');
         const char *nn = getenv("CQG_NO_NDC_CODE");

@@ -141,6 +141,7 @@ struct cqg_ctx {
     bool use_init_reg = true; // cluster init keeps points in registers (CQG_NO_INIT_REG=1: shared-memory kernel)
     bool use_init_rec = true; // {colour, md} record layout for large-N init (CQG_NO_INIT_REC=1: off)
     bool use_init_tile = true; // colour-space tiles with box pruning for large-N init (CQG_NO_INIT_TILE=1: off)
+    uint64_t init_tile_min = 1ull << 20; // ... from this many points (CQG_INIT_TILE_MIN; below, the record layout is as fast)
     bool use_ndc_code = true; // shared-memory code table for the NDC count (CQG_NO_NDC_CODE=1: off)
     bool use_prune = true; // distance-bound pruning of the WALK sweep (CQG_NO_PRUNE=1: off)
     cudaGraphExec_t loop_exec = nullptr;

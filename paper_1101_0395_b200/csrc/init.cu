@@ -2347,7 +2347,7 @@ void run_init(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *counts_d, 
     const bool rec = ctx->use_init_rec;
     // colour-space tiles: every colour on its own Morton slot (a duplicate
     // colour -- raw-pixel substrates -- keeps the record layout)
-    bool tile = rec && ctx->use_init_tile && n <= 0xFFFFFFFFull;
+    bool tile = rec && ctx->use_init_tile && n >= ctx->init_tile_min && n <= (1ull << 24);
     const uint64_t ntiles = (n + kTile - 1) / kTile;
     uint32_t *tbits = nullptr, *tpref = nullptr, *tbsum = nullptr;
     if (tile) {

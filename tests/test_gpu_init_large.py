@@ -34,7 +34,7 @@ def _ctx(**env):
 
 @pytest.fixture(scope="module")
 def ctxs():
-    cs = {"tile": _ctx(CQG_NO_CLUSTER_INIT="1"),
+    cs = {"tile": _ctx(CQG_NO_CLUSTER_INIT="1", CQG_INIT_TILE_MIN="0"),
           "rec": _ctx(CQG_NO_CLUSTER_INIT="1", CQG_NO_INIT_TILE="1"),
           "pingpong": _ctx(CQG_NO_CLUSTER_INIT="1", CQG_NO_INIT_REC="1")}
     yield cs
