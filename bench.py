@@ -522,19 +522,24 @@ def run_ours(args, cfg):
     if top == "init" and share["init"] > k_share:
         K0 = ks[0]
         init_ms = prof.ms[cabi.PROF_INIT] / max(int(prof.launches[cabi.PROF_INIT]), 1)
-        small = all_stats[-1][0].n_unique <= 16 * 1024 * 32
+        nu = all_stats[-1][0].n_unique
+        small = nu <= 16 * 1024 * 12
+        tiled = nu >= (1 << 20)
         dominant = {
-            "kernel": ("init_cluster_kernel (16-CTA cluster, shared-memory state)" if small
+            "kernel": ("init_cluster_reg_kernel (16-CTA cluster, register-resident points)" if small
+                       else "init_kernel_tile (colour-space tiles, box-pruned rounds)" if tiled
                        else "init_kernel_rec (cooperative grid, in-place records)"),
             "share_of_step": share["init"], "avg_launch_ms": init_ms,
-            "bound": "latency" if small else "hbm",
-            "rounds": K0 - 1 if cfg.init == "kpp" else K0 - 1,
+            "bound": "latency" if small or tiled else "hbm",
+            "rounds": K0 - 1,
             "us_per_round": 1e3 * init_ms / max(K0 - 1, 1),
             "note": ("a chain of K-1 dependent draws; CTA sums and the pick travel by st.async with mbarrier "
                      "transaction signalling (no cluster barriers); per-round critical path "
-                     "(tools/init_timing.py): update ~33%, publish ~16%, wait for sums ~7%, "
-                     "locate + pick ~33%") if small else
-                    "8 B per point per round streamed; see DESIGN.md §8",
+                     "(tools/init_timing.py): update ~32%, publish ~15%, draw (wait for sums, locate, "
+                     "pick broadcast) ~42%, tail ~11%") if small else
+                    ("a round updates only the tiles the new centre can reach; block 0 locates the draw and "
+                     "releases the others; see DESIGN.md section 4/8") if tiled else
+                    "8 B per point per round streamed; see DESIGN.md section 8",
         }
     hist_ms = prof.ms[cabi.PROF_HIST]
     pix_ms = prof.ms[cabi.PROF_PIXEL]
