@@ -609,7 +609,9 @@ int cqg_quantize(cqg_ctx *ctx, const uint8_t *rgb, uint64_t P, const cqg_quantiz
         void *idx_d = indices ? out_buf<uint8_t>(indices, ctx->idx_out, P * (size_t)ib) : nullptr;
         uint8_t *q_d = quantized ? out_buf<uint8_t>(quantized, ctx->q_out, P * 3) : nullptr;
         double *mse_h = static_cast<double *>(ctx->pinned.ensure(4096)) + 256; // bytes 2048.. (free here)
-        map_dev(ctx, rgb_d, P, map_col, map_cnt, nm, cen_d, k, idx_d, ib, q_d, mse_h);
+        // 'unique': the mapping's colours are Lloyd's substrate, so its bounds prune the mapping sweep
+        map_dev(ctx, rgb_d, P, map_col, map_cnt, nm, cen_d, k, idx_d, ib, q_d, mse_h,
+                mode == CQG_SAMPLING_UNIQUE ? &o : nullptr);
         copy_out(ctx, palette, cen_d, 24 * (size_t)k);
         copy_out(ctx, labels, lab_d, 4 * ns);
         copy_out(ctx, indices, idx_d, P * (size_t)ib);

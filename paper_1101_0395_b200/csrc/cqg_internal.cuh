@@ -227,6 +227,13 @@ struct LloydOut {
     unsigned long long ndc = 0;
     unsigned long long flagged = 0;
     unsigned long long swept = 0; // points through the full centre loop, all iterations
+    // final state for a bound-pruned mapping of the same substrate (bnd null: none)
+    const uint32_t *labels = nullptr;
+    float2 *bnd = nullptr;
+    const float *shift = nullptr;
+    const double *dsorted = nullptr;
+    const Moments *mom = nullptr;
+    int Kpow = 0;
 };
 // Raise (never lower) a kernel's dynamic shared-memory limit. The attribute is
 // per function and process-wide: contexts on several host threads launching
@@ -259,10 +266,13 @@ int shard_k(cqg_ctx *ctx);
 uint64_t shard_n(cqg_ctx *ctx);
 void subsample_2to1_dev(cqg_ctx *ctx, const uint8_t *rgb_d, int w, int h, uint8_t *out_d);
 void pack_pixels_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t S, uint32_t *colors_d, uint32_t *counts_d);
+// lloyd: the run that produced pal_d on this same substrate (colors_d, counts_d),
+// or null; with its distance bounds the mapping sweep only re-examines the
+// points whose label can change (MODE_MAPW).
 double map_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P, const uint32_t *colors_d,
                const uint32_t *counts_d, uint64_t n, const double *pal_d, int k, void *indices_d,
                int index_bytes, uint8_t *quant_d,
-               double *mse_async = nullptr);
+               double *mse_async = nullptr, const LloydOut *lloyd = nullptr);
 
 void init_maximin_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *counts_d, uint64_t n,
                       uint64_t P, int k, uint64_t seed, int weighted_first, double *centers_d);

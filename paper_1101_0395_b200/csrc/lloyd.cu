@@ -611,7 +611,7 @@ size_t sweep_smem_bytes(int K, int Kp, int mode) {
     // FP32 table, u32 accumulators (FULL/MAP) or u64 (WALK): reserve the larger,
     // and the WALK prune list
     return (size_t)4 * Kp * sizeof(float) + (size_t)sweep_acc_words(K) * sizeof(uint32_t) +
-           (mode == MODE_WALK ? ((size_t)kPruneChunk + kSweepThreads * 8 + prune_aux_words(K)) * sizeof(uint32_t)
+           (mode_delta(mode) ? ((size_t)kPruneChunk + kSweepThreads * 8 + prune_aux_words(K)) * sizeof(uint32_t)
                               : 0);
 }
 
@@ -688,7 +688,8 @@ static void launch_sweep_mode(cqg_ctx *ctx, const SweepArgs &a) {
     if (ppt == 2) sweep_kernel<MODE, 2><<<(unsigned)grid, kSweepThreads, smem, ctx->stream>>>(a);
     else if (ppt == 4) sweep_kernel<MODE, 4><<<(unsigned)grid, kSweepThreads, smem, ctx->stream>>>(a);
     else sweep_kernel<MODE, 8><<<(unsigned)grid, kSweepThreads, smem, ctx->stream>>>(a);
-    prof_end(ctx, MODE == MODE_MAP ? CQG_PROF_MAPSWEEP : CQG_PROF_SWEEP, pb, (double)n * (double)a.K);
+    prof_end(ctx, MODE == MODE_MAP || MODE == MODE_MAPW ? CQG_PROF_MAPSWEEP : CQG_PROF_SWEEP, pb,
+             (double)n * (double)a.K);
     const int pr = prof_begin(ctx);
     replay_kernel<MODE><<<rg, 256, 0, ctx->stream>>>(a);
     prof_end(ctx, CQG_PROF_REPLAY, pr, 0.0);
@@ -743,6 +744,7 @@ void bench_sweep_dev(cqg_ctx *ctx, int reps, double *ms, double *units) {
 void launch_sweep(cqg_ctx *ctx, int mode, const SweepArgs &a) {
     if (mode == MODE_FULL) launch_sweep_mode<MODE_FULL>(ctx, a);
     else if (mode == MODE_WALK) launch_sweep_mode<MODE_WALK>(ctx, a);
+    else if (mode == MODE_MAPW) launch_sweep_mode<MODE_MAPW>(ctx, a);
     else launch_sweep_mode<MODE_MAP>(ctx, a);
 }
 
@@ -1080,6 +1082,14 @@ LloydOut lloyd_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *count
     out.flagged = hcnt[1];
     // FULL first iteration sweeps every point; WALK iterations count the survivors
     out.swept = prune ? hcnt[12] + n : n * (unsigned long long)iter; // swept: scalar byte 128
+    if (prune) { // bounds of the last assignment, shifts to the final centres, their walk table
+        out.labels = labels_d;
+        out.bnd = bnd;
+        out.shift = shift;
+        out.dsorted = dsorted;
+        out.mom = mom;
+        out.Kpow = Kpow;
+    }
     return out;
 }
 

@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(256) pixel_kernel(const uint8_t *__restrict__ 
 
 double map_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P, const uint32_t *colors_d,
                const uint32_t *counts_d, uint64_t n, const double *pal_d, int K, void *indices_d,
-               int index_bytes, uint8_t *quant_d, double *mse_async) {
+               int index_bytes, uint8_t *quant_d, double *mse_async, const LloydOut *lloyd) {
     cudaStream_t s = ctx->stream;
     const int Kp = (K + 7) & ~7;
     const bool lut8 = K <= 256;
@@ -164,7 +164,12 @@ double map_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P, const uint32_t *c
     uint32_t *queue = static_cast<uint32_t *>(ctx->queue.ensure(sizeof(uint32_t) * (n + 1)));
     uint32_t *qn = static_cast<uint32_t *>(ctx->scal.ensure(256));
 
-    CQG_CUDA(cudaMemsetAsync(mom, 0, sizeof(Moments) * (size_t)K, s));
+    // bound-pruned mapping: the moments start from Lloyd's final ones (its labels)
+    const bool pruned = lloyd && lloyd->bnd && ctx->use_prune;
+    if (pruned)
+        CQG_CUDA(cudaMemcpyAsync(mom, lloyd->mom, sizeof(Moments) * (size_t)K, cudaMemcpyDeviceToDevice, s));
+    else
+        CQG_CUDA(cudaMemsetAsync(mom, 0, sizeof(Moments) * (size_t)K, s));
     CQG_CUDA(cudaMemsetAsync(qn, 0, 4, s));
     fc_kernel<<<1, 256, 0, s>>>(pal_d, K, Kp, fc, tau);
     launched(ctx);
@@ -183,7 +188,16 @@ double map_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P, const uint32_t *c
     a.mom = mom;
     a.K = K;
     a.Kp = Kp;
-    launch_sweep(ctx, MODE_MAP, a);
+    if (pruned) {
+        a.labels = const_cast<uint32_t *>(lloyd->labels); // read only in MODE_MAPW
+        a.bnd = lloyd->bnd;                                  // read only in MODE_MAPW
+        a.shift = lloyd->shift;
+        a.dsorted = lloyd->dsorted;
+        a.Kpow = lloyd->Kpow;
+        launch_sweep(ctx, MODE_MAPW, a);
+    } else {
+        launch_sweep(ctx, MODE_MAP, a);
+    }
 
     if ((size_t)K * 8 > 48 * 1024)
         CQG_CUDA(ensure_smem((const void *)mse_kernel, K * 8));

@@ -21,7 +21,12 @@ constexpr int kSweepThreads = 256;
 constexpr int kAccPerCluster = 6; // n, s_r, s_g, s_b, q_lo16, q_hi
 constexpr uint32_t kHeavyCount = 2048; // counts >= this bypass the u32 smem accumulators
 
-enum { MODE_FULL = 0, MODE_WALK = 1, MODE_MAP = 2 };
+// MAPW: the mapping sweep of the substrate Lloyd just ran on, pruned by its
+// distance bounds (palette = the final centres): labels are read, never
+// written; moments start from Lloyd's final ones and take +new -old deltas.
+enum { MODE_FULL = 0, MODE_WALK = 1, MODE_MAP = 2, MODE_MAPW = 3 };
+// modes that keep u64 moment deltas and run the bound filter
+__host__ __device__ constexpr bool mode_delta(int m) { return m == MODE_WALK || m == MODE_MAPW; }
 
 // Shared-memory layout of the FP32 centre table (Kp = K rounded up to 8):
 //   m2r[Kp], m2g[Kp], m2b[Kp], cc[Kp]  (m2* = -2 * centre, cc = |centre|^2)
@@ -463,7 +468,7 @@ __device__ __forceinline__ void sweep_tiles(const SweepArgs &a, uint64_t lo, uin
             pidx[i] = slot < hi ? (LIST ? list[slot] : (uint32_t)slot) : 0u;
             col[i] = slot < hi ? __ldg(a.colors + pidx[i]) : 0u;
             if (kPre) {
-                plab[kPre ? i : 0] = MODE == MODE_WALK ? a.labels[pidx[i]] : 0u;
+                plab[kPre ? i : 0] = mode_delta(MODE) ? a.labels[pidx[i]] : 0u;
                 pcnt[kPre ? i : 0] = __ldg(a.counts + pidx[i]);
             }
             const float r = (float)((col[i] >> 16) & 255u), g = (float)((col[i] >> 8) & 255u),
@@ -576,7 +581,7 @@ __device__ __forceinline__ void sweep_tiles(const SweepArgs &a, uint64_t lo, uin
                 f2 = fminf(b2[i], w2);
             }
             const bool flag = valid && !((f2 - f1) > tau_abs + tau_rel * (fabsf(f1) + fabsf(f2)));
-            if (MODE != MODE_MAP && a.bnd && valid) {
+            if (MODE != MODE_MAP && MODE != MODE_MAPW && a.bnd && valid) {
                 // new bounds for label j1 (flagged points: replayed, bounds void)
                 const float ub = __fsqrt_ru(__fadd_ru(f1 > 0.f ? f1 : 0.f, ev));
                 const float l2 = __fadd_rd(f2, -ev);
@@ -584,11 +589,15 @@ __device__ __forceinline__ void sweep_tiles(const SweepArgs &a, uint64_t lo, uin
                 a.bnd[idx] = flag ? make_float2(__int_as_float(0x7f800000), 0.f) : make_float2(ub, lb);
             }
             const uint32_t r = (col[i] >> 16) & 255u, g = (col[i] >> 8) & 255u, b = col[i] & 255u;
-            if (MODE == MODE_WALK && valid) {
+            if (mode_delta(MODE) && valid) {
                 const int prev = kPre ? (int)plab[kPre ? i : 0] : (int)a.labels[idx];
+                if (MODE == MODE_MAPW && !flag) {
+                    if (a.lut8) a.lut8[col[i]] = (uint8_t)j1;
+                    else a.lut32[col[i]] = (uint32_t)j1;
+                }
                 if (!flag && j1 != prev) {
                     const uint32_t cnt = kPre ? pcnt[kPre ? i : 0] : __ldg(a.counts + idx);
-                    a.labels[idx] = (uint32_t)j1;
+                    if (MODE == MODE_WALK) a.labels[idx] = (uint32_t)j1;
                     accumulate64(s_acc64, j1, cnt, r, g, b, +1);
                     accumulate64(s_acc64, prev, cnt, r, g, b, -1);
                 }
@@ -603,7 +612,7 @@ __device__ __forceinline__ void sweep_tiles(const SweepArgs &a, uint64_t lo, uin
         }
         STIME(6);
         } // warp has points
-        if (MODE != MODE_WALK) {
+        if (!mode_delta(MODE)) {
             __syncthreads();
             flush_acc(s_acc, a.mom, K);
             __syncthreads();
@@ -628,7 +637,8 @@ constexpr float kBoundMargin = 1.0e-3f; // Euclidean gap that keeps the FP64 ref
 // Returns true when the point needs the full sweep.
 __device__ __forceinline__ bool prune_needs_sweep(const SweepArgs &a, uint64_t i, uint32_t lab, float2 bd,
                                                   uint32_t c, const float *s_fc, const float *s_aux, int Kp,
-                                                  float ev, float smax1, float smax2, int sarg) {
+                                                  float ev, float smax1, float smax2, int sarg,
+                                                  bool keep_bounds = true) {
     const float sl = s_aux[lab];
     const float two_s = s_aux[a.K + lab];
     const float so = (int)lab == sarg ? smax2 : smax1;
@@ -648,7 +658,7 @@ __device__ __forceinline__ bool prune_needs_sweep(const SweepArgs &a, uint64_t i
         lb = fmaxf(lbh, __fadd_rd(two_s, -ub));
         stay = __fadd_ru(ub, kBoundMargin) < lb;
     }
-    if (stay) a.bnd[i] = make_float2(ub, lb);
+    if (stay && keep_bounds) a.bnd[i] = make_float2(ub, lb);
     return !stay;
 }
 
@@ -666,7 +676,7 @@ __device__ __forceinline__ void sweep_range(const SweepArgs &a, uint64_t lo, uin
                                             uint32_t *s_acc, float tau_abs, float tau_rel,
                                             uint32_t *s_list = nullptr, uint32_t list_cap = kPruneChunk,
                                             float *s_aux = nullptr) {
-    if (MODE != MODE_WALK || a.bnd == nullptr || s_list == nullptr) {
+    if (!mode_delta(MODE) || a.bnd == nullptr || s_list == nullptr) {
         sweep_tiles<MODE, PPT, false>(a, lo, hi, nullptr, smem, s_acc, tau_abs, tau_rel);
         return;
     }
@@ -705,8 +715,12 @@ __device__ __forceinline__ void sweep_range(const SweepArgs &a, uint64_t lo, uin
 #pragma unroll
             for (int f = 0; f < kFilterPPT; ++f) {
                 const uint64_t i = i0 + threadIdx.x + (uint64_t)f * blockDim.x;
-                const bool need =
-                    i < ce && prune_needs_sweep(a, i, lab[f], bd[f], col[f], smem, s_aux, Kp, ev, smax1, smax2, sarg);
+                const bool need = i < ce && prune_needs_sweep(a, i, lab[f], bd[f], col[f], smem, s_aux, Kp, ev, smax1,
+                                                              smax2, sarg, MODE == MODE_WALK);
+                if (MODE == MODE_MAPW && i < ce && !need) { // provably keeps its label under the palette
+                    if (a.lut8) a.lut8[col[f]] = (uint8_t)lab[f];
+                    else a.lut32[col[f]] = lab[f];
+                }
                 const uint32_t m = __ballot_sync(0xffffffffu, need);
                 if (m) {
                     const int leader = __ffs(m) - 1;
@@ -724,7 +738,7 @@ __device__ __forceinline__ void sweep_range(const SweepArgs &a, uint64_t lo, uin
         const uint32_t m = s_m;
         const uint32_t mb = m / big * big;
         if (mb) {
-            sweep_tiles<MODE_WALK, PPT, true>(a, 0, mb, s_list, smem, s_acc, tau_abs, tau_rel);
+            sweep_tiles<MODE, PPT, true>(a, 0, mb, s_list, smem, s_acc, tau_abs, tau_rel);
             swept += mb;
             __syncthreads();
             // carry the remainder (< big entries) to the front: [mb, m) -> [0, m - mb), disjoint
@@ -735,7 +749,7 @@ __device__ __forceinline__ void sweep_range(const SweepArgs &a, uint64_t lo, uin
         __syncthreads();
     }
     const uint32_t rest = s_m;
-    if (rest) sweep_tiles<MODE_WALK, 2, true>(a, 0, rest, s_list, smem, s_acc, tau_abs, tau_rel);
+    if (rest) sweep_tiles<MODE, 2, true>(a, 0, rest, s_list, smem, s_acc, tau_abs, tau_rel);
     swept += rest;
     __syncthreads();
 #ifdef CQG_SWEEP_TIMING
@@ -764,7 +778,7 @@ __global__ void __launch_bounds__(kSweepThreads, 2) sweep_kernel(SweepArgs a) {
     uint32_t *s_acc = reinterpret_cast<uint32_t *>(smem + 4 * Kp);
     unsigned long long *s_acc64 = reinterpret_cast<unsigned long long *>(s_acc);
     for (int i = threadIdx.x; i < 4 * Kp; i += blockDim.x) smem[i] = a.fc[i];
-    if (MODE == MODE_WALK)
+    if (mode_delta(MODE))
         for (int i = threadIdx.x; i < K * 5; i += blockDim.x) s_acc64[i] = 0;
     else
         for (int i = threadIdx.x; i < K * kAccPerCluster; i += blockDim.x) s_acc[i] = 0;
@@ -775,7 +789,7 @@ __global__ void __launch_bounds__(kSweepThreads, 2) sweep_kernel(SweepArgs a) {
     uint32_t *s_list = reinterpret_cast<uint32_t *>(s_acc) + sweep_acc_words(K);
     float *s_aux = reinterpret_cast<float *>(s_list + kPruneChunk + kSweepThreads * 8);
     sweep_range<MODE, PPT>(a, lo, hi, smem, s_acc, a.tau[0], a.tau[1], s_list, kPruneChunk, s_aux);
-    if (MODE == MODE_WALK) {
+    if (mode_delta(MODE)) {
         __syncthreads();
         flush_acc64(s_acc64, a.mom, K);
     }
@@ -848,7 +862,15 @@ __device__ __forceinline__ void replay_range(const SweepArgs &a, uint32_t gwarp,
                 if (MODE == MODE_FULL) a.labels[idx] = (uint32_t)best;
                 else if (a.lut8) a.lut8[c] = (uint8_t)best;
                 else a.lut32[c] = (uint32_t)best;
-                accumulate_global(a.mom, best, cnt, r, g, b, +1);
+                if (MODE == MODE_MAPW) { // moments hold Lloyd's final labels: move the point
+                    const int prev = (int)a.labels[idx];
+                    if (best != prev) {
+                        accumulate_global(a.mom, best, cnt, r, g, b, +1);
+                        accumulate_global(a.mom, prev, cnt, r, g, b, -1);
+                    }
+                } else {
+                    accumulate_global(a.mom, best, cnt, r, g, b, +1);
+                }
             }
         }
     }

@@ -130,3 +130,24 @@ def test_ndc_code_table_exact_ties(ctx, oracle, history):
     dev = quant.wsm_counts(keys, counts, P, init, opts, ctx=ctx)
     ora = oracle.wsm(keys, counts, P, init, fixed_it=4, mode=UPDATE_EXACT, history=history)
     assert_lloyd_equal(dev, ora, P)
+
+
+@pytest.mark.parametrize("w,h,k,fixed", [(300, 200, 32, 1), (300, 200, 32, 2), (700, 500, 64, 0), (900, 800, 16, 0)])
+def test_pruned_mapping(ctx, ctx_noprune, oracle, w, h, k, fixed):
+    # run_quantize ('unique' sampling) maps the image through the bounds Lloyd
+    # left behind (MODE_MAPW): after the FULL iteration only (fixed 1), after a
+    # WALK iteration, through the persistent kernel (<= 606K colours) and the
+    # graph loop (900x800 with noise). Indices, pixels and MSE are bit-exact
+    # against the oracle's mapping and against the unpruned context.
+    img = synth_image(w, h, 77 + k, nblobs=10, sigma=14.0, noise=0.5 if w == 900 else 0.03)
+    qc = quant.QuantizeConfig(method=quant.parse_method("wsm-kpp"), k=k, seed=k,
+                              term=quant.Termination(fixed_iterations=fixed or None))
+    r = quant.run_quantize(img, qc, ctx=ctx)
+    idx, q, mse_e, _ = oracle.map_pixels(img, r.palette, mode=UPDATE_EXACT)
+    assert np.array_equal(r.mapping.indices, idx)
+    assert np.array_equal(r.mapping.quantized.reshape(-1, 3), q)
+    assert r.report.mse == mse_e
+    r0 = quant.run_quantize(img, qc, ctx=ctx_noprune)
+    assert np.array_equal(r0.palette, r.palette)
+    assert np.array_equal(r0.mapping.indices, r.mapping.indices)
+    assert r0.report.mse == r.report.mse
