@@ -221,9 +221,23 @@ static __global__ void __launch_bounds__(1024, 1) ndc_code_kernel(const uint32_t
         const int hw = Kpow / 2; // 32-bit words per row
         const uint32_t *src = reinterpret_cast<const uint32_t *>(dcode);
         uint32_t *dst = reinterpret_cast<uint32_t *>(s_code);
-        for (int i = threadIdx.x; i < K * hw; i += blockDim.x) {
-            const int r = i / hw, w = i - r * hw;
-            dst[r * (hw + 1) + w] = src[i];
+        const int total = K * hw;
+        // 8 loads in flight per thread (clamped source, masked store)
+        for (int i0 = threadIdx.x; i0 < total; i0 += 8 * blockDim.x) {
+            uint32_t v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int i = i0 + u * blockDim.x;
+                v[u] = __ldg(src + (i < total ? i : 0));
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int i = i0 + u * blockDim.x;
+                if (i < total) {
+                    const int r = i / hw, w = i - r * hw;
+                    dst[r * (hw + 1) + w] = v[u];
+                }
+            }
         }
     } else {
         for (int r = threadIdx.x; r < K; r += blockDim.x) s_code[r * rs] = dcode[r];
@@ -231,7 +245,21 @@ static __global__ void __launch_bounds__(1024, 1) ndc_code_kernel(const uint32_t
     __syncthreads();
     unsigned long long local = 0;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * Q;
-    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x * Q; base < n; base += stride) {
+    // software-pipelined: the next batch's colours and labels are loaded
+    // (clamped, branch-free) while this batch runs its lifting
+    uint32_t ncol[Q], nlab[Q];
+    auto load_batch = [&](uint64_t b) {
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const uint64_t i = b + threadIdx.x + (uint64_t)q * blockDim.x;
+            const uint64_t ic = i < n ? i : 0;
+            ncol[q] = __ldg(colors + ic);
+            nlab[q] = __ldg(labels + ic);
+        }
+    };
+    uint64_t base = (uint64_t)blockIdx.x * blockDim.x * Q;
+    if (base < n) load_batch(base);
+    for (; base < n; base += stride) {
         double cut[Q];
         uint32_t cc[Q];
         int prow[Q], pos[Q];
@@ -239,8 +267,8 @@ static __global__ void __launch_bounds__(1024, 1) ndc_code_kernel(const uint32_t
         for (int q = 0; q < Q; ++q) {
             const uint64_t i = base + threadIdx.x + (uint64_t)q * blockDim.x;
             const bool v = i < n;
-            const uint32_t col = v ? __ldg(colors + i) : 0u;
-            const int prev = v ? (int)__ldg(labels + i) : 0;
+            const uint32_t col = ncol[q];
+            const int prev = v ? (int)nlab[q] : 0;
             const double pd = d2_exact((double)((col >> 16) & 255u), (double)((col >> 8) & 255u),
                                        (double)(col & 255u), s_cenc[3 * prev], s_cenc[3 * prev + 1],
                                        s_cenc[3 * prev + 2]);
@@ -249,6 +277,7 @@ static __global__ void __launch_bounds__(1024, 1) ndc_code_kernel(const uint32_t
             prow[q] = prev;
             pos[q] = 0;
         }
+        if (base + stride < n) load_batch(base + stride);
         for (int step = Kpow >> 1; step >= 1; step >>= 1) {
             uint32_t vv[Q];
 #pragma unroll
