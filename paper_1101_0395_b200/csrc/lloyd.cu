@@ -25,8 +25,8 @@ namespace cg = cooperative_groups;
 namespace cqg {
 
 // FP32 centre table and sweep error bound from FP64 centres (device helper,
-// block-cooperative). E <= u|cc err| + u|m2c err| x + 4 u M, u = 2^-24, M the
-// largest |partial sum| (cc + xx when all coordinates are >= 0).
+// block-cooperative). E <= u|cc err| + u|m2c err| x + 3 u M, u = 2^-24, M the
+// largest |partial sum| of the FMA chain (<= 3C^2 + 6XC).
 __device__ void fc_block(const double *cen, int K, int Kp, float *fc, float *tau) {
     __shared__ float s_max[32];
     __shared__ int s_neg[32];
@@ -65,11 +65,15 @@ __device__ void fc_block(const double *cen, int K, int Kp, float *fc, float *tau
             C = fmax(C, (double)s_max[i]);
             anyneg |= s_neg[i];
         }
+        // e = fma(b, m2b, fma(g, m2g, fma(r, m2r, cc))): the FP32 table's own
+        // rounding (cc, m2) plus one rounding per FMA of a partial sum bounded
+        // by |cc| + sum |x m2| <= 3C^2 + 6XC
+        (void)anyneg;
         const double u = 0x1.0p-24, X = 255.0;
         const double cc_err = u * 3.0 * C * C;
         const double m2c_err = u * 2.0 * X * 3.0 * C;
-        const double M = anyneg ? 3.0 * C * C + 3.0 * X * X + 6.0 * X * C : 3.0 * C * C + 3.0 * X * X;
-        const double E = cc_err + m2c_err + 4.0 * u * M;
+        const double M = 3.0 * C * C + 6.0 * X * C;
+        const double E = cc_err + m2c_err + 3.0 * u * M;
         tau[0] = (float)(2.0 * E * 1.0625 + 1.0e-3);
         tau[1] = 0x1.0p-20f; // rounding of the FP32 gap test itself
     }

@@ -422,6 +422,9 @@ static __global__ void __launch_bounds__(256, 4) ndc_kernel(const uint32_t *__re
 // (balanced across SMs); PPT points per thread amortise the shared-memory
 // centre loads (one LDS.128 per 4 centres per operand array).
 //
+// The sweep ranks centres by e_j = |c_j|^2 - 2 c_j.x (three FMAs per distance;
+// |x|^2 is the same for every centre of a point and is added back, rounded
+// outward, only for the distance bounds).
 // Per point, each 8-centre GROUP's minimum is formed with a 3-input float min
 // chain (0.5 ALU op per distance); the group minima feed the best (b1) and the
 // second-best (b2) over groups and the index of the group that last improved
@@ -482,7 +485,7 @@ __device__ __forceinline__ void sweep_tiles(const SweepArgs &a, uint64_t lo, uin
 #endif
         // point pairs: lane .x = point 2p, lane .y = point 2p+1 (FFMA2 with a
         // broadcast scalar centre operand evaluates one centre for both)
-        float2 xr2[PP], xg2[PP], xb2[PP], xx2[PP];
+        float2 xr2[PP], xg2[PP], xb2[PP];
         uint32_t col[PPT];
         uint32_t pidx[PPT]; // point index (< 2^24 unique colours)
         // small tiles: the resolve's label and count issued with the colour
@@ -502,15 +505,14 @@ __device__ __forceinline__ void sweep_tiles(const SweepArgs &a, uint64_t lo, uin
             }
             const float r = (float)((col[i] >> 16) & 255u), g = (float)((col[i] >> 8) & 255u),
                         b = (float)(col[i] & 255u);
-            float xx = r * r + g * g + b * b; // exact: integers < 2^18
             // opaque copies: keep the floats resident instead of letting ptxas
             // rematerialise them from the packed colour inside the centre loop
             float rr = r, gg = g, bb = b;
-            asm volatile("" : "+f"(rr), "+f"(gg), "+f"(bb), "+f"(xx));
+            asm volatile("" : "+f"(rr), "+f"(gg), "+f"(bb));
             if (i & 1) {
-                xr2[i / 2].y = rr; xg2[i / 2].y = gg; xb2[i / 2].y = bb; xx2[i / 2].y = xx;
+                xr2[i / 2].y = rr; xg2[i / 2].y = gg; xb2[i / 2].y = bb;
             } else {
-                xr2[i / 2].x = rr; xg2[i / 2].x = gg; xb2[i / 2].x = bb; xx2[i / 2].x = xx;
+                xr2[i / 2].x = rr; xg2[i / 2].x = gg; xb2[i / 2].x = bb;
             }
             b1[i] = 3.0e38f;
             b2[i] = 3.0e38f;
@@ -530,20 +532,16 @@ __device__ __forceinline__ void sweep_tiles(const SweepArgs &a, uint64_t lo, uin
                 const float4 c4 = *reinterpret_cast<const float4 *>(s_cc + j + q);
 #pragma unroll
                 for (int p = 0; p < PP; ++p) {
-                    float2 A0 = __fadd2_rn(xx2[p], make_float2(c4.x, c4.x));
-                    A0 = __ffma2_rn(xr2[p], make_float2(r4.x, r4.x), A0);
+                    float2 A0 = __ffma2_rn(xr2[p], make_float2(r4.x, r4.x), make_float2(c4.x, c4.x));
                     A0 = __ffma2_rn(xg2[p], make_float2(g4.x, g4.x), A0);
                     A0 = __ffma2_rn(xb2[p], make_float2(b4.x, b4.x), A0);
-                    float2 A1 = __fadd2_rn(xx2[p], make_float2(c4.y, c4.y));
-                    A1 = __ffma2_rn(xr2[p], make_float2(r4.y, r4.y), A1);
+                    float2 A1 = __ffma2_rn(xr2[p], make_float2(r4.y, r4.y), make_float2(c4.y, c4.y));
                     A1 = __ffma2_rn(xg2[p], make_float2(g4.y, g4.y), A1);
                     A1 = __ffma2_rn(xb2[p], make_float2(b4.y, b4.y), A1);
-                    float2 A2 = __fadd2_rn(xx2[p], make_float2(c4.z, c4.z));
-                    A2 = __ffma2_rn(xr2[p], make_float2(r4.z, r4.z), A2);
+                    float2 A2 = __ffma2_rn(xr2[p], make_float2(r4.z, r4.z), make_float2(c4.z, c4.z));
                     A2 = __ffma2_rn(xg2[p], make_float2(g4.z, g4.z), A2);
                     A2 = __ffma2_rn(xb2[p], make_float2(b4.z, b4.z), A2);
-                    float2 A3 = __fadd2_rn(xx2[p], make_float2(c4.w, c4.w));
-                    A3 = __ffma2_rn(xr2[p], make_float2(r4.w, r4.w), A3);
+                    float2 A3 = __ffma2_rn(xr2[p], make_float2(r4.w, r4.w), make_float2(c4.w, c4.w));
                     A3 = __ffma2_rn(xg2[p], make_float2(g4.w, g4.w), A3);
                     A3 = __ffma2_rn(xb2[p], make_float2(b4.w, b4.w), A3);
                     gm[2 * p] = fminf(fminf(fminf(gm[2 * p], A0.x), A1.x), fminf(A2.x, A3.x));
@@ -574,9 +572,8 @@ __device__ __forceinline__ void sweep_tiles(const SweepArgs &a, uint64_t lo, uin
                 const float xr = (i & 1) ? xr2[i / 2].y : xr2[i / 2].x;
                 const float xg = (i & 1) ? xg2[i / 2].y : xg2[i / 2].x;
                 const float xb = (i & 1) ? xb2[i / 2].y : xb2[i / 2].x;
-                const float xx = (i & 1) ? xx2[i / 2].y : xx2[i / 2].x;
-                // the group's 8 values, two centres per FADD2/FFMA2 (per lane the
-                // same operations as the sweep: bit-identical), 128-bit loads
+                // the group's 8 values, two centres per FFMA2 (per lane the same
+                // operations as the sweep: bit-identical), 128-bit loads
                 float dv[kGroup];
 #pragma unroll
                 for (int q = 0; q < kGroup; q += 4) {
@@ -584,12 +581,10 @@ __device__ __forceinline__ void sweep_tiles(const SweepArgs &a, uint64_t lo, uin
                     const float4 r4 = *reinterpret_cast<const float4 *>(s_m2r + g0 + q);
                     const float4 gq = *reinterpret_cast<const float4 *>(s_m2g + g0 + q);
                     const float4 bq = *reinterpret_cast<const float4 *>(s_m2b + g0 + q);
-                    float2 A = __fadd2_rn(make_float2(xx, xx), make_float2(c4.x, c4.y));
-                    A = __ffma2_rn(make_float2(xr, xr), make_float2(r4.x, r4.y), A);
+                    float2 A = __ffma2_rn(make_float2(xr, xr), make_float2(r4.x, r4.y), make_float2(c4.x, c4.y));
                     A = __ffma2_rn(make_float2(xg, xg), make_float2(gq.x, gq.y), A);
                     A = __ffma2_rn(make_float2(xb, xb), make_float2(bq.x, bq.y), A);
-                    float2 B = __fadd2_rn(make_float2(xx, xx), make_float2(c4.z, c4.w));
-                    B = __ffma2_rn(make_float2(xr, xr), make_float2(r4.z, r4.w), B);
+                    float2 B = __ffma2_rn(make_float2(xr, xr), make_float2(r4.z, r4.w), make_float2(c4.z, c4.w));
                     B = __ffma2_rn(make_float2(xg, xg), make_float2(gq.z, gq.w), B);
                     B = __ffma2_rn(make_float2(xb, xb), make_float2(bq.z, bq.w), B);
                     dv[q] = A.x;
@@ -612,8 +607,13 @@ __device__ __forceinline__ void sweep_tiles(const SweepArgs &a, uint64_t lo, uin
             const bool flag = valid && !((f2 - f1) > tau_abs + tau_rel * (fabsf(f1) + fabsf(f2)));
             if (MODE != MODE_MAP && MODE != MODE_MAPW && a.bnd && valid) {
                 // new bounds for label j1 (flagged points: replayed, bounds void)
-                const float ub = __fsqrt_ru(__fadd_ru(f1 > 0.f ? f1 : 0.f, ev));
-                const float l2 = __fadd_rd(f2, -ev);
+                // back from the xx-free values to squared distances, outward
+                const float cr = (float)((col[i] >> 16) & 255u), cg = (float)((col[i] >> 8) & 255u),
+                            cb = (float)(col[i] & 255u);
+                const float xx = cr * cr + cg * cg + cb * cb; // exact
+                const float d1 = __fadd_ru(f1, xx), d2 = __fadd_rd(f2, xx);
+                const float ub = __fsqrt_ru(__fadd_ru(d1 > 0.f ? d1 : 0.f, ev));
+                const float l2 = __fadd_rd(d2, -ev);
                 const float lb = __fsqrt_rd(l2 > 0.f ? l2 : 0.f);
                 a.bnd[idx] = flag ? make_float2(__int_as_float(0x7f800000), 0.f) : make_float2(ub, lb);
             }
@@ -679,10 +679,10 @@ __device__ __forceinline__ bool prune_needs_sweep(const SweepArgs &a, uint64_t i
         // tighten ub with the own-centre FP32 distance (sweep operation order)
         const float r = (float)((c >> 16) & 255u), g = (float)((c >> 8) & 255u), b = (float)(c & 255u);
         const float xx = r * r + g * g + b * b;
-        float d = __fadd_rn(xx, s_fc[3 * Kp + lab]);
-        d = __fmaf_rn(r, s_fc[lab], d);
-        d = __fmaf_rn(g, s_fc[Kp + lab], d);
-        d = __fmaf_rn(b, s_fc[2 * Kp + lab], d);
+        float e = __fmaf_rn(r, s_fc[lab], s_fc[3 * Kp + lab]);
+        e = __fmaf_rn(g, s_fc[Kp + lab], e);
+        e = __fmaf_rn(b, s_fc[2 * Kp + lab], e);
+        const float d = __fadd_ru(e, xx);
         ub = __fsqrt_ru(__fadd_ru(d > 0.f ? d : 0.f, ev));
         lb = fmaxf(lbh, __fadd_rd(two_s, -ub));
         stay = __fadd_ru(ub, kBoundMargin) < lb;
@@ -911,7 +911,7 @@ __global__ void replay_kernel(SweepArgs a) {
 }
 
 // FP32 centre table + error bound for the sweep (one block).
-//   E <= u*|cc err| + u*|m2c err|*x + 4u*M  with u = 2^-24 and M the largest
+//   E <= u*|cc err| + u*|m2c err|*x + 3u*M  with u = 2^-24 and M the largest
 //   magnitude of any partial sum (cc + xx when all coordinates are >= 0).
 __device__ void fc_block(const double *cen, int K, int Kp, float *fc, float *tau);
 __global__ void fc_kernel(const double *cen, int K, int Kp, float *fc, float *tau);
