@@ -174,38 +174,25 @@ __global__ void __launch_bounds__(kThreads) hist_count_red(const uint8_t *__rest
     }
 }
 
-// large images: first-occurrence bitmap straight from the image -- pixel p is
-// a first occurrence iff ~negf[colour(p)] == p. Thread t's 16 pixels are half
-// of bitmap word t/2; the two halves meet by a shuffle (no atomics).
-__global__ void __launch_bounds__(kThreads) hist_mark_pixels(const uint8_t *__restrict__ rgb, uint64_t P,
-                                                            const uint32_t *__restrict__ negf,
-                                                            uint32_t *__restrict__ bitmap, int aligned) {
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const uint64_t groups = aligned ? P / 16 : 0;
-    // uniform trip count across the grid (the shuffle needs full warps)
-    for (uint64_t g0 = tid - (tid & 31); g0 < (groups + 31) / 32 * 32; g0 += stride) {
-        const uint64_t g = g0 + (tid & 31);
-        uint32_t mask = 0;
-        if (g < groups) {
-            const uint4 *src = reinterpret_cast<const uint4 *>(rgb + g * 48);
-            uint32_t col[16];
-            decode16(ld_stream(src), ld_stream(src + 1), ld_stream(src + 2), col);
+// large images: first-occurrence bitmap from the ~first table instead of a
+// third image pass: every present colour sets the bit of its first pixel
+// (coalesced 16-byte reads of the 64 MiB table, one reduction per colour into
+// the L2-resident bitmap; a pass over the image re-read it and looked up the
+// table per pixel: 865 MB of DRAM reads on an 8192^2 image)
+__global__ void __launch_bounds__(kThreads) hist_mark_table(const uint32_t *__restrict__ negf,
+                                                           uint32_t *__restrict__ bitmap) {
+    const uint4 *t4 = reinterpret_cast<const uint4 *>(negf);
+    constexpr uint32_t n4 = (1u << 24) / 4;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += gridDim.x * blockDim.x) {
+        const uint4 v = __ldcs(t4 + i);
+        const uint32_t f[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-            for (int j = 0; j < 16; ++j)
-                mask |= (~__ldg(negf + col[j]) == (uint32_t)(g * 16 + j) ? 1u : 0u) << j;
+        for (int j = 0; j < 4; ++j) {
+            if (f[j]) {
+                const uint32_t p = ~f[j];
+                atomicOr(&bitmap[p >> 5], 1u << (p & 31));
+            }
         }
-        const uint32_t hi = __shfl_down_sync(0xffffffffu, mask, 1);
-        if (g < groups && (g & 1) == 0) {
-            // the word that also holds tail pixels (odd group count) is shared with the tail loop
-            if (g + 1 < groups) bitmap[g >> 1] = mask | (hi << 16);
-            else atomicOr(&bitmap[g >> 1], mask);
-        }
-    }
-    // tail pixels (or everything when unaligned): one bit each
-    for (uint64_t p = groups * 16 + tid; p < P; p += stride) {
-        const uint32_t c = ((uint32_t)rgb[3 * p] << 16) | ((uint32_t)rgb[3 * p + 1] << 8) | rgb[3 * p + 2];
-        if (~__ldg(negf + c) == (uint32_t)p) atomicOr(&bitmap[p >> 5], 1u << (p & 31));
     }
 }
 
@@ -396,11 +383,11 @@ void histogram_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P, uint32_t *col
         hist_count_fused<<<grid, kThreads, 0, s>>>(rgb_d, P, tab, list, n_dev, aligned);
         hist_mark_fused<<<lgrid, kThreads, 0, s>>>(list, n_dev, tab, bitmap);
     } else {
-        // counts and minimum indices by reductions; the bitmap from a third image
-        // pass (no unique-colour list, no global append counter)
+        // counts and minimum indices by reductions; the bitmap from the
+        // first-index table (no unique-colour list, no global append counter)
         hist_count_red<<<grid, kThreads, 0, s>>>(rgb_d, P, cnt, aligned);
         hist_first<<<grid, kThreads, 0, s>>>(rgb_d, P, negf, aligned);
-        hist_mark_pixels<<<grid, kThreads, 0, s>>>(rgb_d, P, negf, bitmap, aligned);
+        hist_mark_table<<<(unsigned)ctx->num_sms * 8, kThreads, 0, s>>>(negf, bitmap);
     }
     scan_blocksum<<<nblk, kThreads, 0, s>>>(bitmap, words, bsum);
     scan_blocks<<<1, 1024, 0, s>>>(bsum, nblk, large ? n_dev : nullptr);
