@@ -1,6 +1,9 @@
 """Run one stage of the hot path once (for ncu / compute-sanitizer captures).
 
-    python tools/prof_stage.py --config cfg5 --stage init|lloyd|hist|map [--repeat N]
+    python tools/prof_stage.py --config cfg5 --stage init|lloyd|hist|map|sweep [--repeat N]
+
+`sweep` runs Lloyd once, then the isolated dense sweep (cqg_bench_sweep, one
+warm-up + one timed launch) on its final state: capture with -s 1 -c 1.
 
 Builds the histogram (and init centres for the later stages) first, then runs
 the requested stage `repeat` times through the C-ABI.
@@ -45,6 +48,10 @@ def main():
             quant.build_histogram(img, ctx=ctx)
         elif args.stage == "map":
             quant.map_pixels(img, init, ctx=ctx)
+        elif args.stage == "sweep":
+            st = quant.wsm_hist(hist, init, opts, ctx=ctx)
+            ctx.bench_sweep(1)
+            print(f"lloyd iterations={st.iterations}")
     dt = (time.perf_counter() - t0) / args.repeat
     print(f"{args.config} {args.stage}: N'={hist.size()} {dt * 1e3:.3f} ms/call")
 
