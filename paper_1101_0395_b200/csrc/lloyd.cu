@@ -711,6 +711,9 @@ void bench_sweep_dev(cqg_ctx *ctx, int reps, double *ms, double *units) {
     SweepArgs a;
     std::memcpy(&a, ctx->last_sweep, sizeof(SweepArgs));
     a.bnd = nullptr; // the dense sweep (every point against every centre)
+    // the global FP32 table of the final centres (the persistent kernel kept its own)
+    fc_kernel<<<1, 256, 0, ctx->stream>>>(a.cen, a.K, a.Kp, const_cast<float *>(a.fc), const_cast<float *>(a.tau));
+    launched(ctx);
     const size_t smem = sweep_smem_bytes(a.K, a.Kp, MODE_WALK);
     const uint64_t sms = (uint64_t)ctx->num_sms, n = a.n;
     const int b2 = sweep_bps<MODE_WALK, 2>(smem), b4 = sweep_bps<MODE_WALK, 4>(smem),
@@ -962,11 +965,18 @@ LloydOut lloyd_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *count
         hc_d = static_cast<double *>(ctx->hist_centers.ensure(sizeof(double) * 3 * (size_t)K * limit));
     }
 
+    const bool use_graph = !hist && ctx->use_graphs;
+    // small substrates: the whole loop as one persistent cooperative kernel
+    // (every block builds its own FP32 table: no fc_kernel launch)
+    const bool persistent = use_graph && K <= 1024 &&
+                            n <= (uint64_t)ctx->num_sms * 2 * kSweepThreads * 4 * 2;
     CQG_CUDA(cudaMemsetAsync(mom, 0, sizeof(Moments) * (size_t)K, s));
-    CQG_CUDA(cudaMemsetAsync(ndc, 0, 24, s)); // ndc, flagged, iter_dev
-    CQG_CUDA(cudaMemsetAsync(swept, 0, 16, s)); // swept, shift_inval
-    fc_kernel<<<1, 256, 0, s>>>(cen, K, Kp, fc, tau);
-    launched(ctx);
+    // one memset for the scalars: queue counter, ndc, flagged, iter_dev, status, swept, shift_inval
+    CQG_CUDA(cudaMemsetAsync(qn, 0, 160, s));
+    if (!persistent) {
+        fc_kernel<<<1, 256, 0, s>>>(cen, K, Kp, fc, tau);
+        launched(ctx);
+    }
 
     SweepArgs a{};
     a.colors = colors_d;
@@ -1022,14 +1032,9 @@ LloydOut lloyd_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *count
 
     // The graph path needs no per-iteration host work: used unless history is
     // recorded (per-iteration copies) or kernel profiling is on (per-launch events).
-    const bool use_graph = !hist && ctx->use_graphs;
-    // small substrates: the whole loop as one persistent cooperative kernel
-    const bool persistent = use_graph && K <= 1024 &&
-                            n <= (uint64_t)ctx->num_sms * 2 * kSweepThreads * 4 * 2;
     LloydOut out;
     int iter = 0;
     bool done = false;
-    if (persistent) CQG_CUDA(cudaMemsetAsync(qn, 0, 4, s));
     while (!done) {
         const bool first = (iter == 0);
         int rec = -1;
