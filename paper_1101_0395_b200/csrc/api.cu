@@ -59,30 +59,32 @@ void validate_pixels(uint64_t P, const char *who) {
 }
 
 struct Timer {
+    // stage boundaries as events on the stream, read after the pipeline's own
+    // final synchronisation (no host synchronisation between stages)
     cqg_ctx *ctx;
     bool on;
-    cudaEvent_t a, b;
+    cudaEvent_t ev[8];
+    int n = 0;
     Timer(cqg_ctx *c, bool enable) : ctx(c), on(enable) {
         if (on) {
-            cudaEventCreate(&a);
-            cudaEventCreate(&b);
-            cudaEventRecord(a, ctx->stream);
+            for (auto &e : ev) cudaEventCreate(&e);
+            cudaEventRecord(ev[n++], ctx->stream);
         }
     }
-    double lap() {
-        if (!on) return 0.0;
-        cudaEventRecord(b, ctx->stream);
-        cudaEventSynchronize(b);
-        float ms = 0.f;
-        cudaEventElapsedTime(&ms, a, b);
-        std::swap(a, b);
-        return ms;
+    int lap() {
+        if (!on || n >= 8) return 0;
+        cudaEventRecord(ev[n], ctx->stream);
+        return n++;
+    }
+    double ms(int i) const { // stage ending at lap i; call after the stream is synchronised
+        if (!on || i <= 0) return 0.0;
+        float t = 0.f;
+        cudaEventElapsedTime(&t, ev[i - 1], ev[i]);
+        return t;
     }
     ~Timer() {
-        if (on) {
-            cudaEventDestroy(a);
-            cudaEventDestroy(b);
-        }
+        if (on)
+            for (auto &e : ev) cudaEventDestroy(e);
     }
 };
 
@@ -556,7 +558,7 @@ int cqg_quantize(cqg_ctx *ctx, const uint8_t *rgb, uint64_t P, const cqg_quantiz
         uint32_t *col_d = static_cast<uint32_t *>(ctx->colors.ensure(cap * 4));
         uint32_t *cnt_d = static_cast<uint32_t *>(ctx->counts.ensure(cap * 4));
         const uint64_t n = histogram_into(ctx, smp_d, S, col_d, cnt_d, nullptr);
-        const double t_hist = tm.lap();
+        const int t_hist = tm.lap();
 
         double *init_d = static_cast<double *>(ctx->initsel.ensure(24 * (size_t)k + 64));
         if (cfg->init_kind == CQG_INIT_GIVEN) {
@@ -570,7 +572,7 @@ int cqg_quantize(cqg_ctx *ctx, const uint8_t *rgb, uint64_t P, const cqg_quantiz
             else fail(CQG_E_INVALID, "run_quantize: unknown initializer kind");
             CQG_CUDA(cudaMemcpyAsync(init_d, tmp, 24 * (size_t)k, cudaMemcpyDeviceToDevice, ctx->stream));
         }
-        const double t_init = tm.lap();
+        const int t_init = tm.lap();
 
         // substrate: the distinct colours (count weights) or every sampled pixel (count 1, weight 1/S)
         const uint32_t *sub_col = col_d, *sub_cnt = cnt_d;
@@ -592,7 +594,7 @@ int cqg_quantize(cqg_ctx *ctx, const uint8_t *rgb, uint64_t P, const cqg_quantiz
         double *sse_h = static_cast<double *>(ctx->pinned.ensure(4096 + 8 * (size_t)limit)) + 512;
         LloydOut o = lloyd_dev(ctx, sub_col, sub_cnt, ns, S, init_d, k, term, lab_d, cen_d, sse_h, nullptr, nullptr);
         if (sse_trace) std::memcpy(sse_trace, sse_h, 8 * (size_t)o.iterations);
-        const double t_lloyd = tm.lap();
+        const int t_lloyd = tm.lap();
 
         // mapping over the full image needs its distinct colours: the histogram
         // above unless the image was subsampled
@@ -618,7 +620,7 @@ int cqg_quantize(cqg_ctx *ctx, const uint8_t *rgb, uint64_t P, const cqg_quantiz
         copy_out(ctx, quantized, q_d, P * 3);
         CQG_CUDA(cudaStreamSynchronize(ctx->stream)); // the pipeline's last synchronisation
         const double mse = *mse_h;
-        const double t_map = tm.lap();
+        const int t_map = tm.lap();
         if (stats) {
             stats->n_unique = ns;
             stats->lloyd.iterations = o.iterations;
@@ -628,10 +630,11 @@ int cqg_quantize(cqg_ctx *ctx, const uint8_t *rgb, uint64_t P, const cqg_quantiz
             stats->lloyd.flagged_total = o.flagged;
             stats->lloyd.swept_total = o.swept;
             stats->mean_sq_dist = mse;
-            stats->ms_histogram = t_hist;
-            stats->ms_init = t_init;
-            stats->ms_lloyd = t_lloyd;
-            stats->ms_map = t_map;
+            CQG_CUDA(cudaEventSynchronize(tm.ev[t_map]));
+            stats->ms_histogram = tm.ms(t_hist);
+            stats->ms_init = tm.ms(t_init);
+            stats->ms_lloyd = tm.ms(t_lloyd);
+            stats->ms_map = tm.ms(t_map);
         }
     });
 }
