@@ -592,8 +592,13 @@ int cqg_quantize(cqg_ctx *ctx, const uint8_t *rgb, uint64_t P, const cqg_quantiz
         double *cen_d = static_cast<double *>(ctx->cen.ensure(24 * (size_t)k));
         const int limit = term.fixed_iterations > 0 ? term.fixed_iterations : term.max_iterations;
         double *sse_h = static_cast<double *>(ctx->pinned.ensure(4096 + 8 * (size_t)limit)) + 512;
-        LloydOut o = lloyd_dev(ctx, sub_col, sub_cnt, ns, S, init_d, k, term, lab_d, cen_d, sse_h, nullptr, nullptr);
-        if (sse_trace) std::memcpy(sse_trace, sse_h, 8 * (size_t)o.iterations);
+        // the persistent Lloyd kernel's status is checked after the pipeline's
+        // final synchronisation (not before the mapping is enqueued); the
+        // subsampled modes read a histogram count in between, so they do not defer
+        const bool defer = !sub;
+        LloydOut o = lloyd_dev(ctx, sub_col, sub_cnt, ns, S, init_d, k, term, lab_d, cen_d, sse_h, nullptr, nullptr,
+                               defer);
+        if (!o.pending && sse_trace) std::memcpy(sse_trace, sse_h, 8 * (size_t)o.iterations);
         const int t_lloyd = tm.lap();
 
         // mapping over the full image needs its distinct colours: the histogram
@@ -611,14 +616,25 @@ int cqg_quantize(cqg_ctx *ctx, const uint8_t *rgb, uint64_t P, const cqg_quantiz
         void *idx_d = indices ? out_buf<uint8_t>(indices, ctx->idx_out, P * (size_t)ib) : nullptr;
         uint8_t *q_d = quantized ? out_buf<uint8_t>(quantized, ctx->q_out, P * 3) : nullptr;
         double *mse_h = static_cast<double *>(ctx->pinned.ensure(4096)) + 256; // bytes 2048.. (free here)
-        // 'unique': the mapping's colours are Lloyd's substrate, so its bounds prune the mapping sweep
-        map_dev(ctx, rgb_d, P, map_col, map_cnt, nm, cen_d, k, idx_d, ib, q_d, mse_h,
-                mode == CQG_SAMPLING_UNIQUE ? &o : nullptr);
-        copy_out(ctx, palette, cen_d, 24 * (size_t)k);
-        copy_out(ctx, labels, lab_d, 4 * ns);
-        copy_out(ctx, indices, idx_d, P * (size_t)ib);
-        copy_out(ctx, quantized, q_d, P * 3);
-        CQG_CUDA(cudaStreamSynchronize(ctx->stream)); // the pipeline's last synchronisation
+        auto map_and_copy = [&]() {
+            // 'unique': the mapping's colours are Lloyd's substrate, so its bounds prune the mapping sweep
+            map_dev(ctx, rgb_d, P, map_col, map_cnt, nm, cen_d, k, idx_d, ib, q_d, mse_h,
+                    mode == CQG_SAMPLING_UNIQUE ? &o : nullptr);
+            copy_out(ctx, palette, cen_d, 24 * (size_t)k);
+            copy_out(ctx, labels, lab_d, 4 * ns);
+            copy_out(ctx, indices, idx_d, P * (size_t)ib);
+            copy_out(ctx, quantized, q_d, P * 3);
+            CQG_CUDA(cudaStreamSynchronize(ctx->stream)); // the pipeline's last synchronisation
+        };
+        map_and_copy();
+        if (o.pending) {
+            if (lloyd_finish(ctx, o, ns, k) != 1) {
+                // an empty cluster: the synchronous loop (with repairs), then the mapping again
+                o = lloyd_dev(ctx, sub_col, sub_cnt, ns, S, init_d, k, term, lab_d, cen_d, sse_h, nullptr, nullptr);
+                map_and_copy();
+            }
+            if (sse_trace) std::memcpy(sse_trace, sse_h, 8 * (size_t)o.iterations);
+        }
         const double mse = *mse_h;
         const int t_map = tm.lap();
         if (stats) {

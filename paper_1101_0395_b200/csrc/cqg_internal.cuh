@@ -144,6 +144,7 @@ struct cqg_ctx {
     uint64_t init_tile_min = 1ull << 20; // ... from this many points (CQG_INIT_TILE_MIN; below, the record layout is as fast)
     bool use_ndc_code = true; // shared-memory code table for the NDC count (CQG_NO_NDC_CODE=1: off)
     bool use_prune = true; // distance-bound pruning of the WALK sweep (CQG_NO_PRUNE=1: off)
+    bool lloyd_prune_pending = false; // the deferred Lloyd run pruned (lloyd_finish)
     cudaGraphExec_t loop_exec = nullptr;
     cudaGraph_t loop_graph = nullptr;
     std::vector<uint64_t> loop_key;
@@ -234,6 +235,11 @@ struct LloydOut {
     const double *dsorted = nullptr;
     const Moments *mom = nullptr;
     int Kpow = 0;
+    // deferred completion (lloyd_dev(..., allow_defer)): the persistent kernel
+    // and its status read-back are enqueued, nothing synchronised yet; after
+    // the caller's own synchronisation lloyd_finish() fills the counters
+    bool pending = false;
+    int prof_rec = -1;
 };
 // Raise (never lower) a kernel's dynamic shared-memory limit. The attribute is
 // per function and process-wide: contexts on several host threads launching
@@ -245,10 +251,14 @@ cudaError_t ensure_smem(const void *kern, size_t bytes);
 // each wait in grid.sync() for the other's SMs would deadlock.
 cudaError_t launch_cooperative(cqg_ctx *ctx, const void *kern, dim3 grid, dim3 block, void **args, size_t smem);
 
+// After a deferred lloyd_dev and a stream synchronisation: iterations, NDC,
+// counters from the pinned read-back; returns the final state (1 done, 2 an
+// empty cluster: the caller reruns lloyd_dev without deferral, which repairs).
+int lloyd_finish(cqg_ctx *ctx, LloydOut &out, uint64_t n, int K);
 LloydOut lloyd_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *counts_d, uint64_t n,
                    uint64_t P, const double *init_d, int k, const cqg_term &term, uint32_t *labels_d,
                    double *centers_d, double *sse_host, uint32_t *hist_labels_user,
-                   double *hist_centers_user);
+                   double *hist_centers_user, bool allow_defer = false);
 
 void bench_sweep_dev(cqg_ctx *ctx, int reps, double *ms, double *units);
 // sharded Lloyd (lloyd.cu); device pointers unless noted

@@ -922,10 +922,23 @@ static bool launch_persistent(cqg_ctx *ctx, const SweepArgs &a, IterArgs ia, boo
     return true;
 }
 
+int lloyd_finish(cqg_ctx *ctx, LloydOut &out, uint64_t n, int K) {
+    const unsigned char *hsc = static_cast<const unsigned char *>(ctx->pinned.p);
+    const IterStatus *hst = reinterpret_cast<const IterStatus *>(hsc + 32);
+    const unsigned long long *hcnt = reinterpret_cast<const unsigned long long *>(hsc); // ndc, flagged
+    out.pending = false;
+    out.iterations = hst->iteration;
+    prof_add_units(ctx, out.prof_rec, (double)n * (double)K * (double)out.iterations);
+    out.ndc = hcnt[0];
+    out.flagged = hcnt[1];
+    out.swept = ctx->lloyd_prune_pending ? hcnt[12] + n : n * (unsigned long long)out.iterations;
+    return hst->state;
+}
+
 LloydOut lloyd_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *counts_d, uint64_t n,
                    uint64_t P, const double *init_d, int K, const cqg_term &term, uint32_t *labels_d,
                    double *centers_d, double *sse_host, uint32_t *hist_labels_user,
-                   double *hist_centers_user) {
+                   double *hist_centers_user, bool allow_defer) {
     cudaStream_t s = ctx->stream;
     const int Kp = (K + 7) & ~7;
     const int limit = term.fixed_iterations > 0 ? term.fixed_iterations : term.max_iterations;
@@ -1064,6 +1077,23 @@ LloydOut lloyd_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *count
         // one read-back per launch: counters, status (scalars bytes 32..136) and the SSE trace
         CQG_CUDA(cudaMemcpyAsync(hsc, reinterpret_cast<unsigned char *>(qn) + 32, 104, cudaMemcpyDeviceToHost, s));
         if (sse_host) CQG_CUDA(cudaMemcpyAsync(sse_host, sse_d, sizeof(double) * (size_t)limit, cudaMemcpyDefault, s));
+        if (persistent && first && allow_defer) {
+            // the persistent kernel ends done (state 1) or on an empty cluster
+            // (state 2): let the caller enqueue the mapping behind it and check
+            // after its own synchronisation (lloyd_finish)
+            out.pending = true;
+            out.prof_rec = rec;
+            if (prune) {
+                out.labels = labels_d;
+                out.bnd = bnd;
+                out.shift = shift;
+                out.dsorted = dsorted;
+                out.mom = mom;
+                out.Kpow = Kpow;
+            }
+            ctx->lloyd_prune_pending = prune;
+            return out;
+        }
         CQG_CUDA(cudaStreamSynchronize(s));
         iter = hst->iteration;
         prof_add_units(ctx, rec, (double)n * (double)K * (double)(iter - before));

@@ -151,3 +151,30 @@ def test_pruned_mapping(ctx, ctx_noprune, oracle, w, h, k, fixed):
     assert np.array_equal(r0.palette, r.palette)
     assert np.array_equal(r0.mapping.indices, r.mapping.indices)
     assert r0.report.mse == r.report.mse
+
+
+@pytest.mark.parametrize("dup", [1, 3])
+def test_quantize_repair_after_deferred_check(ctx, oracle, dup):
+    # run_quantize checks the persistent Lloyd kernel's status only after the
+    # mapping is enqueued; duplicated initial centres leave clusters empty in
+    # the first iteration, so the run must fall back to the repairing loop and
+    # map again. Everything bit-exact against the oracle pipeline.
+    img = synth_image(96, 80, 41 + dup, nblobs=7, sigma=16.0, noise=0.05)
+    P = 96 * 80
+    rng = np.random.default_rng(dup)
+    init = rng.integers(0, 256, (12, 3)).astype(np.float64)
+    init[1:1 + dup] = init[0]  # clusters 1..dup tie with 0 and lose: empty
+    qc = quant.QuantizeConfig(method=quant.parse_method("wsm-kpp"), k=12, seed=1, init_centers=init)
+    r = quant.run_quantize(img, qc, ctx=ctx)
+    c, n, _ = oracle.histogram(img)
+    ora = oracle.wsm(c, n, P, init, mode=UPDATE_EXACT)
+    assert ora.repairs >= 1
+    assert r.state.repair_count == ora.repairs
+    assert r.state.iterations == ora.iterations
+    assert r.state.ndc_total == ora.ndc_total
+    assert np.array_equal(r.palette, ora.centers)
+    assert np.array_equal(r.state.memberships, ora.labels)
+    idx, q, mse_e, _ = oracle.map_pixels(img, ora.centers, mode=UPDATE_EXACT)
+    assert np.array_equal(r.mapping.indices, idx)
+    assert np.array_equal(r.mapping.quantized.reshape(-1, 3), q)
+    assert r.report.mse == mse_e
