@@ -378,6 +378,12 @@ def run_ours(args, cfg):
     if nworkers > 1:
         s0 = torch.cuda.Stream(device=dev)  # worker 0 off the timing stream too
         ctx.set_stream(s0.cuda_stream)
+        # each worker's grids (and cooperative kernels) on its own slice of the SMs
+        if args.sm_budget != 0:
+            sms = torch.cuda.get_device_properties(dev).multi_processor_count
+            budget = args.sm_budget if args.sm_budget > 0 else sms // nworkers
+            for c in ctxs:
+                c.set_sm_budget(budget)
         wstreams[0] = s0
     sses = [np.zeros(128) for _ in range(nworkers)]
     pool = ThreadPoolExecutor(nworkers) if nworkers > 1 else None
@@ -628,6 +634,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sm-budget", type=int, default=-1,
+                    help="batched configs: SMs per worker context (-1: SMs / workers, 0: whole device each)")
     ap.add_argument("--workers", type=int, default=4,
                     help="batched configs: concurrent library contexts (streams + host threads) per GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")

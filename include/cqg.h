@@ -109,6 +109,12 @@ void cqg_destroy(cqg_ctx *ctx);
 const char *cqg_last_error(void);
 /* Use an existing cudaStream_t (NULL = the context's own stream). */
 int cqg_set_stream(cqg_ctx *ctx, void *cuda_stream);
+/* Restrict the context's grids to `sms` streaming multiprocessors (0: the
+ * whole device). Contexts whose budgets sum to at most the device's SM count
+ * may run their cooperative (grid-barrier) kernels concurrently, e.g. one
+ * context per host thread and stream quantizing a batch of images; budgeted
+ * contexts are ordered only behind whole-device cooperative launches. */
+int cqg_set_sm_budget(cqg_ctx *ctx, int sms);
 /* Number of library kernels launched by this context so far (bench evidence). */
 uint64_t cqg_launch_count(const cqg_ctx *ctx);
 const char *cqg_version(void);

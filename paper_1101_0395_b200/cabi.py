@@ -31,7 +31,7 @@ INIT_GIVEN = 2
 
 # Every symbol include/cqg.h declares (checked by tests/test_cabi_symbols.py).
 EXPORTS = (
-    "cqg_create", "cqg_destroy", "cqg_last_error", "cqg_set_stream", "cqg_launch_count",
+    "cqg_create", "cqg_destroy", "cqg_last_error", "cqg_set_stream", "cqg_set_sm_budget", "cqg_launch_count",
     "cqg_version", "cqg_histogram", "cqg_init_maximin", "cqg_init_kmeanspp", "cqg_lloyd",
     "cqg_map", "cqg_quantize", "cqg_set_profiling", "cqg_read_profile", "cqg_bench_sweep",
     "cqg_shard_begin", "cqg_shard_assign", "cqg_shard_moments", "cqg_shard_finalize", "cqg_shard_sizes",
@@ -98,6 +98,8 @@ def load(path: str = LIB_PATH):
         L.cqg_destroy.argtypes = [vp]
         L.cqg_last_error.restype = C.c_char_p
         L.cqg_set_stream.argtypes = [vp, vp]
+        L.cqg_set_sm_budget.argtypes = [vp, i32]
+        L.cqg_set_sm_budget.restype = i32
         L.cqg_launch_count.restype = u64
         L.cqg_launch_count.argtypes = [vp]
         L.cqg_version.restype = C.c_char_p
@@ -200,6 +202,11 @@ class Context:
         ms, units = C.c_double(0), C.c_double(0)
         check(self.L.cqg_bench_sweep(self.h, reps, C.byref(ms), C.byref(units)))
         return ms.value, units.value
+
+    def set_sm_budget(self, sms: int):
+        """Restrict this context's grids to `sms` SMs (0: the whole device), so
+        several contexts can run their cooperative kernels side by side."""
+        check(self.L.cqg_set_sm_budget(self.h, int(sms)))
 
     def set_stream(self, stream_ptr: int | None):
         check(self.L.cqg_set_stream(self.h, stream_ptr))

@@ -207,6 +207,7 @@ cqg_ctx *cqg_create(int device) {
         ctx = new cqg_ctx();
         ctx->device = device;
         ctx->num_sms = prop.multiProcessorCount;
+        ctx->dev_sms = prop.multiProcessorCount;
         CQG_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
         ctx->own_stream = true;
         const char *ng = getenv("CQG_NO_GRAPH");
@@ -282,6 +283,17 @@ int cqg_set_stream(cqg_ctx *ctx, void *stream) {
 }
 
 uint64_t cqg_launch_count(const cqg_ctx *ctx) { return ctx ? ctx->launches : 0; }
+
+int cqg_set_sm_budget(cqg_ctx *ctx, int sms) {
+    return guarded([&] {
+        if (!ctx) fail(CQG_E_INVALID, "cqg_set_sm_budget: null context");
+        if (sms < 0) fail(CQG_E_INVALID, "cqg_set_sm_budget: negative SM count");
+        use_device(ctx);
+        CQG_CUDA(cudaStreamSynchronize(ctx->stream));
+        ctx->num_sms = (sms == 0 || sms >= ctx->dev_sms) ? ctx->dev_sms : (sms < 16 ? 16 : sms);
+        release_graphs(ctx); // captured launch geometries follow the budget
+    });
+}
 
 int cqg_set_profiling(cqg_ctx *ctx, int on) {
     return guarded([&] {
@@ -659,19 +671,29 @@ int cqg_quantize(cqg_ctx *ctx, const uint8_t *rgb, uint64_t P, const cqg_quantiz
 
 namespace cqg {
 cudaError_t launch_cooperative(cqg_ctx *ctx, const void *kern, dim3 grid, dim3 block, void **args, size_t smem) {
+    // Two cooperative kernels sized for the whole device could each get part
+    // of the SMs and wait in their grid barriers forever, so whole-device
+    // launches are chained (each waits for every earlier cooperative launch).
+    // Contexts with an SM budget (cqg_set_sm_budget; budgets summing to at
+    // most the device) fit side by side: they wait only for the last
+    // whole-device launch.
+    struct Chain {
+        cudaEvent_t full = nullptr;                         // last whole-device launch
+        std::map<const cqg_ctx *, cudaEvent_t> budgeted;    // last launch per budgeted context
+    };
     static std::mutex mu;
-    static std::map<int, cudaEvent_t> last; // per device: the previous cooperative launch
+    static std::map<int, Chain> chains;
     std::lock_guard<std::mutex> lock(mu);
-    cudaEvent_t &ev = last[ctx->device];
-    if (!ev) {
-        cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-        if (e != cudaSuccess) return e;
-    } else {
-        cudaError_t e = cudaStreamWaitEvent(ctx->stream, ev, 0);
-        if (e != cudaSuccess) return e;
-    }
-    cudaError_t e = cudaLaunchCooperativeKernel(kern, grid, block, args, smem, ctx->stream);
-    if (e != cudaSuccess) return e;
+    Chain &c = chains[ctx->device];
+    const bool budget = ctx->num_sms < ctx->dev_sms;
+    cudaError_t e;
+    if (c.full && (e = cudaStreamWaitEvent(ctx->stream, c.full, 0)) != cudaSuccess) return e;
+    if (!budget)
+        for (auto &kv : c.budgeted)
+            if ((e = cudaStreamWaitEvent(ctx->stream, kv.second, 0)) != cudaSuccess) return e;
+    cudaEvent_t &ev = budget ? c.budgeted[ctx] : c.full;
+    if (!ev && (e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) return e;
+    if ((e = cudaLaunchCooperativeKernel(kern, grid, block, args, smem, ctx->stream)) != cudaSuccess) return e;
     return cudaEventRecord(ev, ctx->stream);
 }
 } // namespace cqg

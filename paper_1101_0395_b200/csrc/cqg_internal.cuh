@@ -104,7 +104,8 @@ struct Moments {
 
 struct cqg_ctx {
     int device = 0;
-    int num_sms = 148;
+    int num_sms = 148;     // grid sizing: the device's SMs, or the cqg_set_sm_budget slice
+    int dev_sms = 148;     // the device's SMs (size limits of the persistent kernel)
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     unsigned long long launches = 0;

@@ -982,7 +982,7 @@ LloydOut lloyd_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *count
     // small substrates: the whole loop as one persistent cooperative kernel
     // (every block builds its own FP32 table: no fc_kernel launch)
     const bool persistent = use_graph && K <= 1024 &&
-                            n <= (uint64_t)ctx->num_sms * 2 * kSweepThreads * 4 * 2;
+                            n <= (uint64_t)ctx->dev_sms * 2 * kSweepThreads * 4 * 2;
     CQG_CUDA(cudaMemsetAsync(mom, 0, sizeof(Moments) * (size_t)K, s));
     // one memset for the scalars: queue counter, ndc, flagged, iter_dev, status, swept, shift_inval
     CQG_CUDA(cudaMemsetAsync(qn, 0, 160, s));
