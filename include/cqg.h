@@ -17,6 +17,9 @@
  *                                               (src/kmeans.cpp:173-277)
  *   cqg_map            quant::map_pixels        include/quant/metrics.hpp:28
  *                                               (src/metrics.cpp:15-55)
+ *   cqg_coarse_histogram[_weighted]
+ *                      quant::build_coarse_histogram include/quant/precluster.hpp:32-34
+ *                                               (src/precluster.cpp:13-47)
  *   cqg_quantize       quant::run_quantize      include/quant/pipeline.hpp:53
  *                                               (src/pipeline.cpp:81-164), for
  *                                               methods wsm-mmx / wsm-kpp and
@@ -201,6 +204,22 @@ int cqg_shard_end(cqg_ctx *ctx, double *centers, uint32_t *labels, double *sse_t
  * rendered with channel_to_u8, color.hpp:63-72); may be NULL. */
 int cqg_map(cqg_ctx *ctx, const uint8_t *rgb, uint64_t P, const double *palette, int k,
             void *indices, int index_bytes, uint8_t *quantized, double *mean_sq_dist);
+
+/* ---- coarse 32x32x32 histogram (quant::build_coarse_histogram,
+ * include/quant/precluster.hpp:32-34; src/precluster.cpp:13-47): the
+ * preclusterers' input (median cut / Wan / Wu, the CLI's default wsm-wu).
+ * Bin (r>>3, g>>3, b>>3) in r-major order; per bin the pixel count and the
+ * exact sums of r, g, b and r^2+g^2+b^2 over the ORIGINAL 8-bit values. Each
+ * output array holds CQG_COARSE_BINS entries (host or device pointers). */
+#define CQG_COARSE_BINS 32768
+/* from an image (rgb: P x 3 bytes); "build_coarse_histogram: no pixels" */
+int cqg_coarse_histogram(cqg_ctx *ctx, const uint8_t *rgb, uint64_t P, uint64_t *count, int64_t *sum_r,
+                         int64_t *sum_g, int64_t *sum_b, int64_t *sum_sq);
+/* from a weighted histogram (packed 0x00RRGGBB colours, counts, n entries);
+ * "build_coarse_histogram: empty histogram" */
+int cqg_coarse_histogram_weighted(cqg_ctx *ctx, const uint32_t *colors, const uint32_t *counts, uint64_t n,
+                                  uint64_t *count, int64_t *sum_r, int64_t *sum_g, int64_t *sum_b,
+                                  int64_t *sum_sq);
 
 /* ---- whole hot path: histogram -> init -> wsm -> map --------------------
  * init: required for CQG_INIT_GIVEN (k x 3), ignored otherwise. palette: k x 3.

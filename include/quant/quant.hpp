@@ -83,6 +83,16 @@ struct RawImage {
     const Rgb8 &at(int x, int y) const { return pixels[static_cast<std::size_t>(y) * width + x]; }
 };
 
+// image.hpp:26-44: PPM (P6, maxval 255) on the host; PNG needs libpng, which
+// this build does not link (load/save report it as unsupported).
+struct LoadedImage {
+    RawImage image;
+    std::vector<std::string> warnings;
+};
+LoadedImage load_image(const std::string &path);
+void save_image(const RawImage &image, const std::string &path);
+void save_ppm(const RawImage &image, const std::string &path);
+
 // ---- histogram.hpp:19-60 --------------------------------------------------
 enum class SamplingMode { None, TwoToOne, Unique, TwoToOneUnique };
 const char *sampling_mode_token(SamplingMode mode);
@@ -178,6 +188,22 @@ struct SeedConfig {
 };
 std::vector<ColorPoint> init_maximin(const WeightedHistogram &hist, const SeedConfig &cfg);
 std::vector<ColorPoint> init_kmeanspp(const WeightedHistogram &hist, const SeedConfig &cfg);
+
+// ---- precluster.hpp:16-34: the coarse grid the preclusterers read -------
+struct CoarseHistogram {
+    static constexpr int grid = 32;
+    static constexpr std::size_t bins = 32768;
+    std::vector<std::uint64_t> count;
+    std::vector<std::int64_t> sum_r, sum_g, sum_b, sum_sq;
+    CoarseHistogram() : count(bins, 0), sum_r(bins, 0), sum_g(bins, 0), sum_b(bins, 0), sum_sq(bins, 0) {}
+    static std::size_t bin_index(int br, int bg, int bb) {
+        return (static_cast<std::size_t>(br) * grid + bg) * grid + bb;
+    }
+    static std::size_t bin_of(Rgb8 c) { return bin_index(c.r >> 3, c.g >> 3, c.b >> 3); }
+};
+// on the device (cqg_coarse_histogram / _weighted)
+CoarseHistogram build_coarse_histogram(std::span<const Rgb8> pixels);
+CoarseHistogram build_coarse_histogram(const WeightedHistogram &hist);
 
 // ---- metrics.hpp:14-57 ----------------------------------------------------
 struct MappingResult {

@@ -585,3 +585,24 @@ CQO_API double cqo_psnr(double mse) {
     if (mse == 0.0) return INFINITY;
     return 20.0 * log10(255.0 / sqrt(mse));
 }
+
+/* coarse 32x32x32 histogram (precluster.cpp:13-47; bin_index/bin_of,
+ * precluster.hpp:26-29): per bin (r>>3, g>>3, b>>3), r-major, the count and
+ * the sums of r, g, b and r^2+g^2+b^2 over the original values, weighted by
+ * each distinct colour's pixel count (the weighted overload; the pixel
+ * overload is the same with every pixel counted once).
+ * out: 5 x 32768 int64 -- count | sum_r | sum_g | sum_b | sum_sq. */
+CQO_API void cqo_coarse_histogram(const uint32_t *colors, const uint32_t *counts, uint64_t n, int64_t *out) {
+    const size_t B = 32768;
+    memset(out, 0, sizeof(int64_t) * 5 * B);
+    for (uint64_t i = 0; i < n; ++i) {
+        const int64_t r = (colors[i] >> 16) & 255, g = (colors[i] >> 8) & 255, b = colors[i] & 255;
+        const int64_t c = counts[i];
+        const size_t bin = ((size_t)(r >> 3) * 32 + (size_t)(g >> 3)) * 32 + (size_t)(b >> 3);
+        out[bin] += c;
+        out[B + bin] += c * r;
+        out[2 * B + bin] += c * g;
+        out[3 * B + bin] += c * b;
+        out[4 * B + bin] += c * (r * r + g * g + b * b);
+    }
+}

@@ -68,6 +68,8 @@ class Oracle:
         self.L = L
         L.cqo_histogram.restype = C.c_int64
         L.cqo_histogram.argtypes = [_u8p, C.c_uint64, _u32p, _u32p, C.c_void_p]
+        L.cqo_coarse_histogram.restype = None
+        L.cqo_coarse_histogram.argtypes = [_u32p, _u32p, C.c_uint64, C.c_void_p]
         L.cqo_weights.argtypes = [_u32p, C.c_uint64, C.c_uint64, _f64p]
         L.cqo_center_table.argtypes = [_f64p, C.c_int, _f64p, _u32p]
         L.cqo_wsm.restype = C.c_int
@@ -184,6 +186,13 @@ class Oracle:
     def psnr(self, mse: float) -> float:
         return self.L.cqo_psnr(mse)
 
+    def coarse_histogram(self, colors, counts):
+        """(count, sum_r, sum_g, sum_b, sum_sq), 32768 int64 each (precluster.cpp:13-47)."""
+        out = np.empty(5 * 32768, np.int64)
+        self.L.cqo_coarse_histogram(np.ascontiguousarray(colors, np.uint32), np.ascontiguousarray(counts, np.uint32),
+                                    len(colors), out.ctypes.data_as(C.c_void_p))
+        return out.reshape(5, 32768)
+
     # --- rng ------------------------------------------------------------------
     def rng(self, seed: int):
         buf = C.create_string_buffer(self.L.cqo_rng_size())
@@ -201,6 +210,9 @@ class RefLib:
         self.L = L
         L.ref_last_error.restype = C.c_char_p
         L.ref_synthetic_photo.argtypes = [C.c_int, C.c_int, C.c_uint64, _u8p]
+        L.ref_coarse_histogram.restype = C.c_int
+        L.ref_coarse_histogram.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64,
+                                           C.c_void_p]
         L.ref_histogram.restype = C.c_int64
         L.ref_histogram.argtypes = [_u8p, C.c_uint64, C.c_uint64, _u32p, _u32p, C.c_void_p]
         L.ref_init.argtypes = [C.c_int, _u32p, _u32p, C.c_uint64, C.c_uint64, C.c_int, C.c_uint64,
@@ -226,6 +238,22 @@ class RefLib:
     def _check(self, rc):
         if rc != 0:
             raise ValueError(self.L.ref_last_error().decode())
+
+    def coarse_histogram(self, rgb=None, colors=None, counts=None):
+        """quant::build_coarse_histogram from pixels (rgb) or from a weighted
+        histogram (colors, counts): a (5, 32768) int64 array."""
+        out = np.empty(5 * 32768, np.int64)
+        if colors is None:
+            px = np.ascontiguousarray(rgb, np.uint8).reshape(-1)
+            rc = self.L.ref_coarse_histogram(px.ctypes.data_as(C.c_void_p), px.size // 3, None, None, 0,
+                                             out.ctypes.data_as(C.c_void_p))
+        else:
+            c = np.ascontiguousarray(colors, np.uint32)
+            n = np.ascontiguousarray(counts, np.uint32)
+            rc = self.L.ref_coarse_histogram(None, 0, c.ctypes.data_as(C.c_void_p), n.ctypes.data_as(C.c_void_p),
+                                             c.size, out.ctypes.data_as(C.c_void_p))
+        self._check(rc)
+        return out.reshape(5, 32768)
 
     def synthetic_photo(self, w, h, seed):
         out = np.empty(w * h * 3, np.uint8)

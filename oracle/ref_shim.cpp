@@ -11,6 +11,7 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <span>
 #include <string>
 #include <vector>
 
@@ -83,6 +84,35 @@ std::int64_t ref_histogram(const std::uint8_t *rgb, std::uint64_t P, std::uint64
             if (weights) weights[i] = h.weights[i];
         }
         return static_cast<std::int64_t>(h.size());
+    } catch (const std::exception &e) {
+        return fail(e);
+    }
+}
+
+// quant::build_coarse_histogram (precluster.hpp:32-34), both overloads:
+// from pixels (colors == nullptr) or from a weighted histogram. out: 5 x 32768
+// (count | sum_r | sum_g | sum_b | sum_sq, as int64 bit patterns).
+int ref_coarse_histogram(const std::uint8_t *rgb, std::uint64_t P, const std::uint32_t *colors,
+                         const std::uint32_t *counts, std::uint64_t n, std::int64_t *out) {
+    try {
+        CoarseHistogram ch;
+        if (!colors) {
+            std::vector<Rgb8> px(P);
+            if (P) std::memcpy(px.data(), rgb, P * 3);
+            ch = build_coarse_histogram(std::span<const Rgb8>(px));
+        } else {
+            std::uint64_t total = 0;
+            for (std::uint64_t i = 0; i < n; ++i) total += counts[i];
+            ch = build_coarse_histogram(make_hist(colors, counts, n, total ? total : 1));
+        }
+        for (std::size_t b = 0; b < CoarseHistogram::bins; ++b) {
+            out[b] = static_cast<std::int64_t>(ch.count[b]);
+            out[CoarseHistogram::bins + b] = ch.sum_r[b];
+            out[2 * CoarseHistogram::bins + b] = ch.sum_g[b];
+            out[3 * CoarseHistogram::bins + b] = ch.sum_b[b];
+            out[4 * CoarseHistogram::bins + b] = ch.sum_sq[b];
+        }
+        return 0;
     } catch (const std::exception &e) {
         return fail(e);
     }

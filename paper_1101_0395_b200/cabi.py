@@ -33,7 +33,8 @@ INIT_GIVEN = 2
 EXPORTS = (
     "cqg_create", "cqg_destroy", "cqg_last_error", "cqg_set_stream", "cqg_set_sm_budget", "cqg_launch_count",
     "cqg_version", "cqg_histogram", "cqg_init_maximin", "cqg_init_kmeanspp", "cqg_lloyd",
-    "cqg_map", "cqg_quantize", "cqg_set_profiling", "cqg_read_profile", "cqg_bench_sweep",
+    "cqg_map", "cqg_coarse_histogram", "cqg_coarse_histogram_weighted", "cqg_quantize", "cqg_set_profiling",
+    "cqg_read_profile", "cqg_bench_sweep",
     "cqg_shard_begin", "cqg_shard_assign", "cqg_shard_moments", "cqg_shard_finalize", "cqg_shard_sizes",
     "cqg_shard_donor", "cqg_shard_move", "cqg_shard_end",
 )
@@ -100,6 +101,10 @@ def load(path: str = LIB_PATH):
         L.cqg_set_stream.argtypes = [vp, vp]
         L.cqg_set_sm_budget.argtypes = [vp, i32]
         L.cqg_set_sm_budget.restype = i32
+        L.cqg_coarse_histogram.argtypes = [vp, vp, u64, vp, vp, vp, vp, vp]
+        L.cqg_coarse_histogram.restype = i32
+        L.cqg_coarse_histogram_weighted.argtypes = [vp, vp, vp, u64, vp, vp, vp, vp, vp]
+        L.cqg_coarse_histogram_weighted.restype = i32
         L.cqg_launch_count.restype = u64
         L.cqg_launch_count.argtypes = [vp]
         L.cqg_version.restype = C.c_char_p
@@ -202,6 +207,15 @@ class Context:
         ms, units = C.c_double(0), C.c_double(0)
         check(self.L.cqg_bench_sweep(self.h, reps, C.byref(ms), C.byref(units)))
         return ms.value, units.value
+
+    def coarse_histogram_raw(self, rgb, P, out):
+        """cqg_coarse_histogram into out (5 x 32768 int64: count, sum_r, sum_g, sum_b, sum_sq)."""
+        check(self.L.cqg_coarse_histogram(self.h, ptr(rgb), P, ptr(out[0]), ptr(out[1]), ptr(out[2]),
+                                          ptr(out[3]), ptr(out[4])))
+
+    def coarse_histogram_weighted_raw(self, colors, counts, n, out):
+        check(self.L.cqg_coarse_histogram_weighted(self.h, ptr(colors), ptr(counts), n, ptr(out[0]), ptr(out[1]),
+                                                   ptr(out[2]), ptr(out[3]), ptr(out[4])))
 
     def set_sm_budget(self, sms: int):
         """Restrict this context's grids to `sms` SMs (0: the whole device), so

@@ -250,7 +250,7 @@ void cqg_destroy(cqg_ctx *ctx) {
                       &ctx->colors, &ctx->counts, &ctx->first, &ctx->labels, &ctx->cen, &ctx->fcen,
                       &ctx->dtab, &ctx->dsorted, &ctx->order, &ctx->mom, &ctx->queue, &ctx->ndc,
                       &ctx->status, &ctx->sizes, &ctx->red, &ctx->hist_labels, &ctx->hist_centers,
-                      &ctx->sse, &ctx->lut, &ctx->idx_out, &ctx->q_out, &ctx->mom_map, &ctx->mind2,
+                      &ctx->sse, &ctx->lut, &ctx->idx_out, &ctx->q_out, &ctx->mom_map, &ctx->coarse, &ctx->mind2,
                       &ctx->initpart, &ctx->initsel, &ctx->unit_draws, &ctx->inittile, &ctx->mom_g, &ctx->partial,
                       &ctx->bnd, &ctx->shift, &ctx->dcode, &ctx->sub_img, &ctx->raw_col, &ctx->raw_cnt,
                       &ctx->full_col, &ctx->full_cnt};
@@ -506,6 +506,48 @@ int cqg_shard_end(cqg_ctx *ctx, double *centers, uint32_t *labels, double *sse_t
         use_device(ctx);
         const int it = shard_end_dev(ctx, centers, labels, sse_trace);
         if (iterations) *iterations = it;
+    });
+}
+
+static void coarse_out(cqg_ctx *ctx, const unsigned long long *tab, uint64_t *count, int64_t *sum_r,
+                       int64_t *sum_g, int64_t *sum_b, int64_t *sum_sq) {
+    void *outs[5] = {count, sum_r, sum_g, sum_b, sum_sq};
+    for (int f = 0; f < 5; ++f) copy_out(ctx, outs[f], tab + (size_t)f * 32768, sizeof(uint64_t) * 32768);
+    CQG_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+int cqg_coarse_histogram(cqg_ctx *ctx, const uint8_t *rgb, uint64_t P, uint64_t *count, int64_t *sum_r,
+                         int64_t *sum_g, int64_t *sum_b, int64_t *sum_sq) {
+    return guarded([&] {
+        use_device(ctx);
+        if (P == 0 || !rgb) fail(CQG_E_INVALID, "build_coarse_histogram: no pixels");
+        if (!count || !sum_r || !sum_g || !sum_b || !sum_sq) fail(CQG_E_INVALID, "build_coarse_histogram: null output");
+        validate_pixels(P, "build_coarse_histogram");
+        // the distinct colours and their counts first (the same device
+        // histogram as build_histogram), then 5 reductions per colour
+        const uint64_t cap = P < (1ull << 24) ? P : (1ull << 24);
+        const uint8_t *rgb_d = static_cast<const uint8_t *>(stage_in(ctx, rgb, P * 3, ctx->img));
+        uint32_t *col_d = static_cast<uint32_t *>(ctx->colors.ensure(cap * 4));
+        uint32_t *cnt_d = static_cast<uint32_t *>(ctx->counts.ensure(cap * 4));
+        const uint64_t n = histogram_into(ctx, rgb_d, P, col_d, cnt_d, nullptr);
+        unsigned long long *tab = static_cast<unsigned long long *>(ctx->coarse.ensure(sizeof(uint64_t) * 5 * 32768));
+        coarse_hist_dev(ctx, col_d, cnt_d, n, tab);
+        coarse_out(ctx, tab, count, sum_r, sum_g, sum_b, sum_sq);
+    });
+}
+
+int cqg_coarse_histogram_weighted(cqg_ctx *ctx, const uint32_t *colors, const uint32_t *counts, uint64_t n,
+                                  uint64_t *count, int64_t *sum_r, int64_t *sum_g, int64_t *sum_b,
+                                  int64_t *sum_sq) {
+    return guarded([&] {
+        use_device(ctx);
+        if (n == 0 || !colors || !counts) fail(CQG_E_INVALID, "build_coarse_histogram: empty histogram");
+        if (!count || !sum_r || !sum_g || !sum_b || !sum_sq) fail(CQG_E_INVALID, "build_coarse_histogram: null output");
+        const uint32_t *col_d = static_cast<const uint32_t *>(stage_in(ctx, colors, n * 4, ctx->raw_col));
+        const uint32_t *cnt_d = static_cast<const uint32_t *>(stage_in(ctx, counts, n * 4, ctx->raw_cnt));
+        unsigned long long *tab = static_cast<unsigned long long *>(ctx->coarse.ensure(sizeof(uint64_t) * 5 * 32768));
+        coarse_hist_dev(ctx, col_d, cnt_d, n, tab);
+        coarse_out(ctx, tab, count, sum_r, sum_g, sum_b, sum_sq);
     });
 }
 

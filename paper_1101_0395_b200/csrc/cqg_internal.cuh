@@ -128,6 +128,7 @@ struct cqg_ctx {
     void *shard = nullptr;      // cqg::ShardState (lloyd.cu)
     // mapping
     cqg::DevBuf lut, idx_out, q_out, mom_map;
+    cqg::DevBuf coarse; // 5 x 32768 u64 coarse histogram (cqg_coarse_histogram)
     // init
     cqg::DevBuf mind2, initpart, initsel, unit_draws, inittile;
     cqg::HostBuf pinned;   // status readback and small results
@@ -280,6 +281,8 @@ void pack_pixels_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t S, uint32_t *c
 // lloyd: the run that produced pal_d on this same substrate (colors_d, counts_d),
 // or null; with its distance bounds the mapping sweep only re-examines the
 // points whose label can change (MODE_MAPW).
+void coarse_hist_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *counts_d, uint64_t n,
+                     unsigned long long *tab_d);
 double map_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P, const uint32_t *colors_d,
                const uint32_t *counts_d, uint64_t n, const double *pal_d, int k, void *indices_d,
                int index_bytes, uint8_t *quant_d,

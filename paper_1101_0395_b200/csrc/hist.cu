@@ -422,3 +422,45 @@ void pack_pixels_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t S, uint32_t *c
 }
 
 } // namespace cqg
+
+// ---------------------------------------------------------------------------
+// Coarse 32x32x32 histogram (quant::build_coarse_histogram,
+// src/precluster.cpp:13-47): per bin (r>>3, g>>3, b>>3) the pixel count and
+// exact sums of r, g, b and r^2+g^2+b^2. Built from the distinct colours and
+// their counts (5 reductions per colour instead of per pixel; the totals are
+// the same integers), straight into the L2-resident 1.3 MiB table as
+// fire-and-forget u64 adds (the colours come in first-occurrence order, not
+// grouped by bin, so a shared-memory slice per block would not localise them).
+namespace cqg {
+namespace {
+__global__ void __launch_bounds__(256) coarse_hist_kernel(const uint32_t *__restrict__ colors,
+                                                         const uint32_t *__restrict__ counts, uint64_t n,
+                                                         unsigned long long *__restrict__ tab) {
+    // tab: 5 x 32768 u64 -- count | sum_r | sum_g | sum_b | sum_sq
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t c = __ldg(colors + i);
+        const unsigned long long cnt = __ldg(counts + i);
+        const uint32_t r = (c >> 16) & 255u, g = (c >> 8) & 255u, b = c & 255u;
+        const uint32_t bin = ((r >> 3) << 10) | ((g >> 3) << 5) | (b >> 3);
+        atomicAdd(tab + bin, cnt);
+        atomicAdd(tab + 32768 + bin, cnt * r);
+        atomicAdd(tab + 2 * 32768 + bin, cnt * g);
+        atomicAdd(tab + 3 * 32768 + bin, cnt * b);
+        atomicAdd(tab + 4 * 32768 + bin, cnt * (unsigned long long)(r * r + g * g + b * b));
+    }
+}
+} // namespace
+
+void coarse_hist_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *counts_d, uint64_t n,
+                     unsigned long long *tab_d) {
+    cudaStream_t s = ctx->stream;
+    CQG_CUDA(cudaMemsetAsync(tab_d, 0, sizeof(unsigned long long) * 5 * 32768, s));
+    unsigned grid = (unsigned)((n + 255) / 256);
+    const unsigned gmax = (unsigned)ctx->num_sms * 8;
+    if (grid > gmax) grid = gmax;
+    if (grid == 0) grid = 1;
+    coarse_hist_kernel<<<grid, 256, 0, s>>>(colors_d, counts_d, n, tab_d);
+    CQG_CUDA(cudaGetLastError());
+    launched(ctx);
+}
+} // namespace cqg

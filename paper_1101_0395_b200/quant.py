@@ -68,6 +68,76 @@ class RawImage:
         return self.width * self.height
 
 
+def load_image(path: str) -> RawImage:
+    """quant::load_image (image.hpp:36) for binary PPM (P6, maxval 255): header
+    tokens separated by whitespace, '#' comments to end of line, exactly one
+    whitespace byte before the raster. Errors are the reference's
+    RuntimeError messages "<path>: <what>". PNG needs libpng (not linked)."""
+    try:
+        data = open(path, "rb").read()
+    except OSError:
+        raise RuntimeError(f"{path}: cannot open file") from None
+    if len(data) < 2:
+        raise RuntimeError(f"{path}: file too short to identify")
+    if data[:2] == b"\x89P":
+        raise RuntimeError(f"{path}: PNG input needs libpng, which this build does not link")
+    if data[:2] != b"P6":
+        raise RuntimeError(f"{path}: unsupported format (expected binary PPM 'P6' or PNG)")
+    pos = 2
+
+    def field(name):
+        nonlocal pos
+        tok = b""
+        while pos < len(data):
+            c = data[pos:pos + 1]
+            pos += 1
+            if c == b"#":
+                while pos < len(data) and data[pos:pos + 1] != b"\n":
+                    pos += 1
+                pos += 1 if pos < len(data) else 0
+                continue
+            if c.isspace():
+                if tok:
+                    break
+                continue
+            tok += c
+        if not tok:
+            raise RuntimeError(f"{path}: truncated PPM header (missing {name})")
+        try:
+            return int(tok.decode("ascii"), 10)
+        except ValueError:
+            raise RuntimeError(f"{path}: malformed PPM {name} '{tok.decode('latin-1')}'") from None
+
+    w, h, maxval = field("width"), field("height"), field("maxval")
+    if w <= 0 or h <= 0:
+        raise RuntimeError(f"{path}: non-positive PPM dimensions")
+    if maxval != 255:
+        raise RuntimeError(f"{path}: unsupported PPM maxval {maxval} (only 255)")
+    need = w * h * 3
+    raster = data[pos:pos + need]
+    if len(raster) != need:
+        raise RuntimeError(f"{path}: truncated PPM pixel data (expected {need} bytes, got {len(raster)})")
+    return RawImage(w, h, np.frombuffer(raster, np.uint8).reshape(h, w, 3).copy())
+
+
+def save_image(image: RawImage, path: str) -> None:
+    """quant::save_image / save_ppm (image.hpp:39-42): "P6\\n<w> <h>\\n255\\n" + raw RGB."""
+    low = path.lower()
+    if low.endswith(".png"):
+        raise RuntimeError(f"{path}: PNG output needs libpng, which this build does not link")
+    if not low.endswith(".ppm"):
+        raise RuntimeError(f"{path}: unknown output extension (use .ppm or .png)")
+    px = np.ascontiguousarray(image.pixels, np.uint8)
+    if image.width <= 0 or image.height <= 0 or px.size != image.width * image.height * 3:
+        raise ValueError("save_ppm: inconsistent image dimensions")
+    try:
+        with open(path, "wb") as f:
+            f.write(f"P6\n{image.width} {image.height}\n255\n".encode("ascii"))
+            f.write(px.tobytes())
+    except OSError:
+        raise RuntimeError(f"{path}: cannot open file for writing") from None
+
+
 # ---------------------------------------------------------------------------
 # stage 1 (histogram.hpp:19-60)
 
@@ -118,6 +188,44 @@ def build_histogram(pixels, seed: int = 1, ctx: Optional[cabi.Context] = None) -
     inv = 1.0 / float(P)
     weights = counts.astype(np.float64) * inv
     return WeightedHistogram(unpack_colors(colors), weights, counts, P, colors, first)
+
+
+@dataclass
+class CoarseHistogram:
+    """quant::CoarseHistogram (precluster.hpp:16-30): 32x32x32 bins (5 bits per
+    channel, r-major), per bin the pixel count and the sums of the original
+    r, g, b and r^2+g^2+b^2."""
+    count: np.ndarray   # (32768,) uint64
+    sum_r: np.ndarray   # (32768,) int64
+    sum_g: np.ndarray
+    sum_b: np.ndarray
+    sum_sq: np.ndarray
+    grid = 32
+    bins = 32768
+
+    @staticmethod
+    def bin_index(br: int, bg: int, bb: int) -> int:
+        return (br * 32 + bg) * 32 + bb
+
+
+def build_coarse_histogram(source, ctx: Optional[cabi.Context] = None) -> CoarseHistogram:
+    """quant::build_coarse_histogram (precluster.hpp:32-34, precluster.cpp:13-47)
+    on the device, from pixels or from a WeightedHistogram (same integers)."""
+    ctx = ctx or cabi.default_context()
+    out = np.empty((5, 32768), np.int64)
+    if isinstance(source, WeightedHistogram):
+        if source.size() == 0:
+            raise ValueError("build_coarse_histogram: empty histogram")
+        packed = source.packed if source.packed is not None else pack_colors(source.colors)
+        ctx.coarse_histogram_weighted_raw(np.ascontiguousarray(packed, np.uint32),
+                                          np.ascontiguousarray(source.counts, np.uint32), source.size(), out)
+    else:
+        arr, w, h = _pixels(source)
+        if w * h == 0:
+            raise ValueError("build_coarse_histogram: no pixels")
+        ctx.coarse_histogram_raw(arr, w * h, out)
+    return CoarseHistogram(out[0].view(np.uint64).copy(), out[1].copy(), out[2].copy(), out[3].copy(),
+                           out[4].copy())
 
 
 # ---------------------------------------------------------------------------

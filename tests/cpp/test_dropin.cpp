@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstring>
 #include <fstream>
 #include <iostream>
 #include <set>
@@ -220,6 +221,76 @@ static void case_sampling_substrates() { // test_pipeline.cpp:106-134: the subst
     CHECK(std::string(sampling_mode_token(both.report.sampling)) == "both");
 }
 
+static void case_coarse_histogram() { // precluster.cpp:13-47, both overloads, exact integers
+    std::vector<Rgb8> px;
+    std::uint64_t st = 12345;
+    for (int i = 0; i < 5000; ++i) {
+        st = st * 6364136223846793005ull + 1442695040888963407ull;
+        px.push_back(Rgb8{static_cast<std::uint8_t>(st >> 56), static_cast<std::uint8_t>(st >> 48),
+                          static_cast<std::uint8_t>((st >> 40) & 0x3f)});
+    }
+    CoarseHistogram want;
+    for (const Rgb8 &p : px) {
+        const std::size_t b = CoarseHistogram::bin_of(p);
+        want.count[b] += 1;
+        want.sum_r[b] += p.r;
+        want.sum_g[b] += p.g;
+        want.sum_b[b] += p.b;
+        want.sum_sq[b] += static_cast<std::int64_t>(p.r) * p.r + static_cast<std::int64_t>(p.g) * p.g +
+                          static_cast<std::int64_t>(p.b) * p.b;
+    }
+    const CoarseHistogram a = build_coarse_histogram(std::span<const Rgb8>(px));
+    const CoarseHistogram b = build_coarse_histogram(build_histogram(px, 1));
+    for (const CoarseHistogram *g : {&a, &b}) {
+        CHECK(g->count == want.count);
+        CHECK(g->sum_r == want.sum_r && g->sum_g == want.sum_g && g->sum_b == want.sum_b);
+        CHECK(g->sum_sq == want.sum_sq);
+    }
+    bool threw = false;
+    try {
+        build_coarse_histogram(std::span<const Rgb8>());
+    } catch (const std::invalid_argument &e) {
+        threw = std::string(e.what()) == "build_coarse_histogram: no pixels";
+    }
+    CHECK(threw);
+}
+
+static void case_ppm_roundtrip() { // image.hpp:41-42: "P6\n<w> <h>\n255\n" + raw RGB
+    RawImage img;
+    img.width = 3;
+    img.height = 2;
+    for (int i = 0; i < 6; ++i)
+        img.pixels.push_back(Rgb8{static_cast<std::uint8_t>(i * 40), static_cast<std::uint8_t>(255 - i),
+                                  static_cast<std::uint8_t>(i)});
+    const std::string path = "/tmp/cqg_dropin_test.ppm";
+    save_image(img, path);
+    {
+        std::FILE *f = std::fopen(path.c_str(), "rb");
+        char head[12] = {};
+        CHECK(f && std::fread(head, 1, 11, f) == 11);
+        if (f) std::fclose(f);
+        CHECK(std::string(head, 11) == "P6\n3 2\n255\n");
+    }
+    const LoadedImage back = load_image(path);
+    CHECK(back.image.width == 3 && back.image.height == 2);
+    CHECK(std::memcmp(back.image.pixels.data(), img.pixels.data(), 18) == 0);
+    // a comment between header tokens; a truncated raster
+    {
+        std::FILE *f = std::fopen(path.c_str(), "wb");
+        const char data[] = "P6 # c\n3 2\n255\nabc";
+        std::fwrite(data, 1, sizeof(data) - 1, f);
+        std::fclose(f);
+    }
+    bool threw = false;
+    try {
+        load_image(path);
+    } catch (const std::runtime_error &e) {
+        threw = std::string(e.what()) == path + ": truncated PPM pixel data (expected 18 bytes, got 3)";
+    }
+    CHECK(threw);
+    std::remove(path.c_str());
+}
+
 int main(int argc, char **argv) {
     const std::string dir = argc > 1 ? argv[1] : "tests/golden";
     struct Case {
@@ -230,7 +301,9 @@ int main(int argc, char **argv) {
                  {"histogram_equals_duplicates", case_histogram_equals_duplicates},
                  {"mapping", case_mapping},
                  {"report_format", case_report_format},
-                 {"sampling_substrates", case_sampling_substrates}};
+                 {"sampling_substrates", case_sampling_substrates},
+                 {"coarse_histogram", case_coarse_histogram},
+                 {"ppm_roundtrip", case_ppm_roundtrip}};
     for (const auto &c : cases) {
         const int before = g_fail;
         try {

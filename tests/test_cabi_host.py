@@ -135,3 +135,35 @@ def test_wsm_validation_messages_before_device():
     bad = quant.ClusterOptions(quant.Termination(fixed_iterations=0))
     with pytest.raises(ValueError, match="fixed_iterations"):
         quant.wsm_counts(np.array([1, 2], np.uint32), np.array([1, 1], np.uint32), 2, one, bad)
+
+
+# ---- PPM I/O on the host (image.hpp:26-44) -----------------------------------
+
+def test_ppm_roundtrip_and_errors(tmp_path):
+    from paper_1101_0395_b200 import quant
+    rng = np.random.default_rng(3)
+    img = quant.RawImage(5, 3, rng.integers(0, 256, (3, 5, 3), dtype=np.uint8))
+    p = str(tmp_path / "a.ppm")
+    quant.save_image(img, p)
+    raw = open(p, "rb").read()
+    assert raw[:11] == b"P6\n5 3\n255\n" and len(raw) == 11 + 45
+    back = quant.load_image(p)
+    assert back.width == 5 and back.height == 3 and np.array_equal(back.pixels, img.pixels)
+    # comments between tokens; error messages of the reference (image.cpp)
+    q = str(tmp_path / "b.ppm")
+    open(q, "wb").write(b"P6 # note\n2 1\n255\n" + bytes(range(6)))
+    assert np.array_equal(quant.load_image(q).pixels.reshape(-1), np.arange(6, dtype=np.uint8))
+    cases = {b"P6\n2 1\n255\nab": "truncated PPM pixel data (expected 6 bytes, got 2)",
+             b"P6\n2 x\n255\n": "malformed PPM height 'x'",
+             b"P6\n2 1\n65535\n": "unsupported PPM maxval 65535 (only 255)",
+             b"P6\n0 1\n255\n": "non-positive PPM dimensions",
+             b"P6\n2": "truncated PPM header (missing height)",
+             b"P3\n": "unsupported format (expected binary PPM 'P6' or PNG)",
+             b"P": "file too short to identify"}
+    for data, msg in cases.items():
+        open(q, "wb").write(data)
+        with pytest.raises(RuntimeError) as ei:
+            quant.load_image(q)
+        assert str(ei.value) == f"{q}: {msg}"
+    with pytest.raises(RuntimeError, match="unknown output extension"):
+        quant.save_image(img, str(tmp_path / "a.bmp"))

@@ -106,9 +106,9 @@ def test_histogram_device_pointers(ctx, oracle):
 @pytest.mark.parametrize("case", ["2048sq", "odd2049", "unaligned_large", "few_large"])
 def test_histogram_large_images(ctx, oracle, case):
     # P >= 2^22: counts and first indices by reductions in two passes, the
-    # first-occurrence bitmap from a third pass over the image, pixel-order emit,
-    # one memset reset (hist.cu large path); odd sizes leave tail pixels that
-    # share a bitmap word with the last 16-pixel group
+    # first-occurrence bitmap from a scan of the first-index table, pixel-order
+    # emit, one memset reset (hist.cu large path); odd sizes and unaligned
+    # buffers take the scalar tail loops
     rng = np.random.default_rng(2024)
     if case == "2048sq":
         img = synth_image(2048, 2048, 11, nblobs=20, sigma=20.0, noise=0.3)
@@ -410,3 +410,30 @@ def test_pipeline_vs_reference(ctx, oracle, reflib, name):
     assert np.array_equal(r.mapping.indices, idx)
     assert np.array_equal(r.mapping.quantized.reshape(-1, 3), q)
     assert r.report.mse == mse_e
+
+
+# ---------------------------------------------------------------------------
+# coarse histogram (precluster.cpp:13-47): exact integers, both overloads
+
+@pytest.mark.parametrize("w,h,noise", [(160, 120, 0.05), (1031, 1025, 0.3), (1, 1, 0.0)])
+def test_coarse_histogram_vs_reference(ctx, oracle, reflib, w, h, noise):
+    img = synth_image(w, h, 11 + w, nblobs=9, sigma=14.0, noise=noise)
+    ch = quant.build_coarse_histogram(img, ctx=ctx)
+    ref_px = reflib.coarse_histogram(rgb=img)
+    got = np.stack([ch.count.view(np.int64), ch.sum_r, ch.sum_g, ch.sum_b, ch.sum_sq])
+    assert np.array_equal(got, ref_px)
+    hist = quant.build_histogram(img, ctx=ctx)
+    chw = quant.build_coarse_histogram(hist, ctx=ctx)
+    got_w = np.stack([chw.count.view(np.int64), chw.sum_r, chw.sum_g, chw.sum_b, chw.sum_sq])
+    assert np.array_equal(got_w, reflib.coarse_histogram(colors=hist.packed, counts=hist.counts))
+    assert np.array_equal(got_w, oracle.coarse_histogram(hist.packed, hist.counts))
+    assert int(ch.count.sum()) == w * h
+
+
+def test_coarse_histogram_errors(ctx):
+    with pytest.raises(ValueError, match="build_coarse_histogram: no pixels"):
+        quant.build_coarse_histogram(np.zeros((0, 3), np.uint8), ctx=ctx)
+    empty = quant.WeightedHistogram(colors=np.zeros((0, 3)), weights=np.zeros(0), counts=np.zeros(0, np.uint32),
+                                    source_pixel_count=0, packed=np.zeros(0, np.uint32))
+    with pytest.raises(ValueError, match="build_coarse_histogram: empty histogram"):
+        quant.build_coarse_histogram(empty, ctx=ctx)
