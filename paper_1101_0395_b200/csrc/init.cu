@@ -2378,7 +2378,8 @@ void run_init(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *counts_d, 
     if (occ < 1) occ = 1;
     // k-means++ record rounds are load-latency bound: 3 blocks per SM (maximin
     // measured faster with 2: one barrier per round, fewer arrivals)
-    const int per_want = (rec && kind == 1) || tile ? 3 : 2;
+    // (tile rounds: 2 per SM -- fewer arrivals per hand-off; cfg3 2.34 -> 1.97 ms, cfg5 6.33 -> 6.12 ms vs 3)
+    const int per_want = tile ? 2 : (rec && kind == 1 ? 3 : 2);
     const int per_sm = occ > per_want ? per_want : occ;
     uint64_t grid = (uint64_t)ctx->num_sms * (uint64_t)per_sm;
     if (grid > (uint64_t)kLocateMax) grid = kLocateMax; // warp_locate scans <= kLocateMax block sums
