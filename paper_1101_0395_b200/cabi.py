@@ -17,7 +17,7 @@ import threading
 import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libcqg.so")
+LIB_PATH = os.environ.get("CQG_LIB") or os.path.join(PKG, "libcqg.so")  # CQG_LIB: experiment builds
 
 CQG_OK = 0
 CQG_E_INVALID = 1

@@ -132,29 +132,6 @@ __global__ void hist_emit_fused(const uint32_t *__restrict__ list, const uint32_
 
 // ---- large images: split tables cnt | negf (64 MiB each), two passes
 
-__global__ void __launch_bounds__(kThreads) hist_count(const uint8_t *__restrict__ rgb, uint64_t P,
-                                                      uint32_t *__restrict__ cnt, uint32_t *__restrict__ list,
-                                                      uint32_t *__restrict__ list_n, int aligned) {
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const uint64_t groups = aligned ? P / 16 : 0;
-    for (uint64_t g = tid; g < groups; g += stride) {
-        const uint4 *src = reinterpret_cast<const uint4 *>(rgb + g * 48);
-        uint32_t col[16];
-        decode16(ld_stream(src), ld_stream(src + 1), ld_stream(src + 2), col);
-        bool isnew[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) isnew[j] = atomicAdd(cnt + col[j], 1u) == 0;
-#pragma unroll
-        for (int j = 0; j < 16; ++j) append(isnew[j], col[j], list, list_n);
-    }
-    for (uint64_t p = groups * 16 + tid; p < P; p += stride) {
-        const uint32_t c = ((uint32_t)rgb[3 * p] << 16) | ((uint32_t)rgb[3 * p + 1] << 8) | rgb[3 * p + 2];
-        const bool isnew = atomicAdd(cnt + c, 1u) == 0;
-        append(isnew, c, list, list_n);
-    }
-}
-
 // large images: counts by reductions (no return value, no list)
 __global__ void __launch_bounds__(kThreads) hist_count_red(const uint8_t *__restrict__ rgb, uint64_t P,
                                                           uint32_t *__restrict__ cnt, int aligned) {
@@ -214,14 +191,6 @@ __global__ void __launch_bounds__(kThreads) hist_first(const uint8_t *__restrict
     }
 }
 
-__global__ void hist_mark(const uint32_t *__restrict__ list, const uint32_t *__restrict__ list_n,
-                          const uint32_t *__restrict__ negf, uint32_t *__restrict__ bitmap) {
-    const uint32_t n = *list_n;
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const uint32_t f = ~negf[list[i]];
-        atomicOr(&bitmap[f >> 5], 1u << (f & 31));
-    }
-}
 
 // one thread per pixel, in pixel order: a set bit is a first occurrence whose
 // rank is the word prefix plus the set bits below it, so the stores of a warp

@@ -801,7 +801,10 @@ __global__ void __launch_bounds__(kInitThreads, 3) init_kernel_rec(InitArgs a) {
 // from its segment's and its part's sum (atomics); the locate is the record
 // kernel's, reading md through hpos. Maximin keeps per-tile maxima of
 // (md, ~index); untouched tiles keep theirs.
-constexpr int kTile = 256;       // points per tile (8 per lane of one warp)
+#ifndef CQG_TILE_POINTS
+#define CQG_TILE_POINTS 128 // measured: 64 / 128 / 256 / 512 -> cfg5 init 6.22 / 5.93 / 6.13 / 9.15 ms
+#endif
+constexpr int kTile = CQG_TILE_POINTS; // points per tile (kTile / 32 per lane of one warp)
 constexpr int kFlagStride = 32;  // u64 words between two blocks' release flags (256 B)
 
 __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long *p) {
@@ -1272,7 +1275,6 @@ __global__ void __launch_bounds__(kInitThreads, 3) init_kernel_tile(InitArgs a) 
     __shared__ typename M::T s_w[kInitThreads / 32];
     __shared__ unsigned long long s_m[kInitThreads / 32];
     const uint32_t *mdv = a.tmd; // md via hpos
-    int par = 0;
 #ifdef CQG_INIT_TIMING
     unsigned long long _gprev = clock64();
 #endif
