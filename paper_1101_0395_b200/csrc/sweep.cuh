@@ -650,7 +650,10 @@ __device__ __forceinline__ void sweep_tiles(const SweepArgs &a, uint64_t lo, uin
 }
 
 // Points per block-local chunk of the pruned WALK sweep (shared-memory list).
-constexpr int kPruneChunk = 4096;
+#ifndef CQG_PRUNE_CHUNK
+#define CQG_PRUNE_CHUNK 4096
+#endif
+constexpr int kPruneChunk = CQG_PRUNE_CHUNK;
 constexpr float kBoundMargin = 1.0e-3f; // Euclidean gap that keeps the FP64 reference order
 
 // Stay test (exact): after the centres moved by shift[], the label is provably
@@ -693,7 +696,10 @@ __device__ __forceinline__ bool prune_needs_sweep(const SweepArgs &a, uint64_t i
 
 // Shared words the pruned WALK sweep needs besides the list: shift[K], 2s[K].
 __host__ __device__ constexpr int prune_aux_words(int K) { return 2 * K; }
-constexpr int kFilterPPT = 8; // points per thread per filter step (loads in flight)
+#ifndef CQG_FILTER_PPT
+#define CQG_FILTER_PPT 8
+#endif
+constexpr int kFilterPPT = CQG_FILTER_PPT; // points per thread per filter step (loads in flight)
 
 // Sweep points [lo, hi) of this block. WALK with bounds: per chunk, the stay
 // test appends the points that may change label to a shared-memory list
