@@ -1398,7 +1398,10 @@ __global__ void __launch_bounds__(kInitThreads, 3) init_kernel_tile(InitArgs a) 
 #ifndef CQG_EXP_SKIP_BARRIER2
 #define CQG_EXP_SKIP_BARRIER2 0
 #endif
-constexpr int kClusterThreads = 1024;
+#ifndef CQG_CLUSTER_THREADS
+#define CQG_CLUSTER_THREADS 1024
+#endif
+constexpr int kClusterThreads = CQG_CLUSTER_THREADS;
 constexpr int kMaxClusterCtas = 16;
 
 // ---- DSMEM producer/consumer signalling (mbarrier transaction counts) ----
@@ -1997,7 +2000,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_reg_kernel(In
         if (lane == 31) s_wsum[par][warp] = tincl;
         __syncthreads();
         if (warp == 0) {
-            w_sum = s_wsum[par][lane];
+            w_sum = lane < kClusterThreads / 32 ? s_wsum[par][lane] : (T)0; // fewer warps than lanes: zero
             const T wincl = warp_incl<M>(w_sum);
             w_excl = wincl - w_sum;
             const T csum = M::shfl(wincl, 31);
@@ -2163,8 +2166,8 @@ __global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_reg_kernel(In
             }
             __syncthreads();
             if (warp == 0) {
-                unsigned long long b = s_wkey[lane];
-                uint32_t bc = s_wcol[lane];
+                unsigned long long b = lane < kClusterThreads / 32 ? s_wkey[lane] : 0ull;
+                uint32_t bc = lane < kClusterThreads / 32 ? s_wcol[lane] : 0u;
                 for (int o = 16; o; o >>= 1) {
                     const unsigned long long x = __shfl_xor_sync(0xffffffffu, b, o);
                     const uint32_t xc = __shfl_xor_sync(0xffffffffu, bc, o);
@@ -2283,13 +2286,18 @@ static bool launch_cluster_init(cqg_ctx *ctx, InitArgs a) {
     const uint64_t per = (a.n + C - 1) / C;
     const int ppt = ((int)((per + kClusterThreads - 1) / kClusterThreads) + 3) & ~3; // 128-bit runs
     if (ppt < 1 || ppt > ctx->cluster_max_ppt) return false;
-    const bool reg = ctx->use_init_reg && ctx->use_mbar_init && ppt <= 12;
+    const bool reg = ctx->use_init_reg && ctx->use_mbar_init && (ppt <= 12 || (kClusterThreads < 1024 && ppt <= 24));
     const size_t smem = reg ? (size_t)kClusterThreads * ppt * 3 * sizeof(uint32_t) : cluster_smem<M>(ppt);
     if (smem > 227 * 1024) return false;
     if (reg) {
         switch (ppt) {
         case 4: return launch_cluster(ctx, a, init_cluster_reg_kernel<M, 4>, smem, a);
         case 8: return launch_cluster(ctx, a, init_cluster_reg_kernel<M, 8>, smem, a);
+#if CQG_CLUSTER_THREADS < 1024
+        case 16: return launch_cluster(ctx, a, init_cluster_reg_kernel<M, 16>, smem, a);
+        case 20: return launch_cluster(ctx, a, init_cluster_reg_kernel<M, 20>, smem, a);
+        case 24: return launch_cluster(ctx, a, init_cluster_reg_kernel<M, 24>, smem, a);
+#endif
         default: return launch_cluster(ctx, a, init_cluster_reg_kernel<M, 12>, smem, a);
         }
     }
