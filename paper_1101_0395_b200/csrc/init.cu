@@ -1938,13 +1938,13 @@ __global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_kernel(InitAr
 // or warp hand-over sits between the sums' arrival and the pick. The rare
 // paths (ambiguous fixed-point decisions, a target beyond every prefix) dump
 // the registers into s_md and replay the reference sequentially as before.
-template <class M, int PPT>
-__global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_reg_kernel(InitArgs a) {
+template <class M, int PPT, int NT>
+__global__ void __launch_bounds__(NT, 1) init_cluster_reg_kernel(InitArgs a) {
     typedef typename M::T T;
     cg::cluster_group cl = cg::this_cluster();
     const int C = (int)cl.num_blocks(), crank = (int)cl.block_rank();
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    constexpr uint64_t chunk = (uint64_t)kClusterThreads * PPT;
+    constexpr uint64_t chunk = (uint64_t)NT * PPT;
     const uint64_t lo = (uint64_t)crank * chunk;
     const uint64_t hi = lo + chunk < a.n ? lo + chunk : a.n;
     const int mine = hi > lo ? (int)(hi - lo) : 0;
@@ -1963,7 +1963,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_reg_kernel(In
     __shared__ uint32_t s_fbc;
     __shared__ T s_U, s_total, s_base;
     __shared__ int s_tw, s_nf;
-    for (int i = t; i < (int)chunk; i += kClusterThreads) { // padding: colour 0, count 0 (mass 0)
+    for (int i = t; i < (int)chunk; i += NT) { // padding: colour 0, count 0 (mass 0)
         s_col[i] = i < mine ? __ldg(a.colors + lo + i) : 0u;
         s_cnt[i] = i < mine ? __ldg(a.counts + lo + i) : 0u;
     }
@@ -2000,7 +2000,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_reg_kernel(In
         if (lane == 31) s_wsum[par][warp] = tincl;
         __syncthreads();
         if (warp == 0) {
-            w_sum = lane < kClusterThreads / 32 ? s_wsum[par][lane] : (T)0; // fewer warps than lanes: zero
+            w_sum = lane < NT / 32 ? s_wsum[par][lane] : (T)0; // fewer warps than lanes: zero
             const T wincl = warp_incl<M>(w_sum);
             w_excl = wincl - w_sum;
             const T csum = M::shfl(wincl, 31);
@@ -2166,8 +2166,8 @@ __global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_reg_kernel(In
             }
             __syncthreads();
             if (warp == 0) {
-                unsigned long long b = lane < kClusterThreads / 32 ? s_wkey[lane] : 0ull;
-                uint32_t bc = lane < kClusterThreads / 32 ? s_wcol[lane] : 0u;
+                unsigned long long b = lane < NT / 32 ? s_wkey[lane] : 0ull;
+                uint32_t bc = lane < NT / 32 ? s_wcol[lane] : 0u;
                 for (int o = 16; o; o >>= 1) {
                     const unsigned long long x = __shfl_xor_sync(0xffffffffu, b, o);
                     const uint32_t xc = __shfl_xor_sync(0xffffffffu, bc, o);
@@ -2248,7 +2248,8 @@ static size_t cluster_smem(int ppt) {
 
 // launch one 16-CTA cluster of `kern`; false when it cannot be resident
 template <class... KArgs, class... Args>
-static bool launch_cluster(cqg_ctx *ctx, const InitArgs &a, void (*kern)(KArgs...), size_t smem, Args... args) {
+static bool launch_cluster(cqg_ctx *ctx, const InitArgs &a, int nt, void (*kern)(KArgs...), size_t smem,
+                           Args... args) {
     constexpr int C = 16;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess ||
         ensure_smem((const void *)kern, (int)smem) != cudaSuccess) {
@@ -2257,7 +2258,7 @@ static bool launch_cluster(cqg_ctx *ctx, const InitArgs &a, void (*kern)(KArgs..
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(C);
-    cfg.blockDim = dim3(kClusterThreads);
+    cfg.blockDim = dim3(nt);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = ctx->stream;
     cudaLaunchAttribute attr[1];
@@ -2284,24 +2285,42 @@ template <class M>
 static bool launch_cluster_init(cqg_ctx *ctx, InitArgs a) {
     constexpr int C = 16;
     const uint64_t per = (a.n + C - 1) / C;
+    // maximin rounds are one max-reduction: 512-thread CTAs (16 warps) shorten
+    // the reduction and the barrier; k-means++ keeps 1024 (its prefix scan
+    // wants the shorter per-thread run). Own limit: 24 points per thread.
+    if (a.kind == 0 && ctx->use_init_reg && ctx->use_mbar_init && ctx->cluster_nt512) {
+        const int p5 = ((int)((per + 511) / 512) + 3) & ~3;
+        const size_t sm5 = (size_t)512 * p5 * 3 * sizeof(uint32_t);
+        if (p5 <= 24) {
+            switch (p5) {
+            case 4: return launch_cluster(ctx, a, 512, init_cluster_reg_kernel<M, 4, 512>, sm5, a);
+            case 8: return launch_cluster(ctx, a, 512, init_cluster_reg_kernel<M, 8, 512>, sm5, a);
+            case 12: return launch_cluster(ctx, a, 512, init_cluster_reg_kernel<M, 12, 512>, sm5, a);
+            case 16: return launch_cluster(ctx, a, 512, init_cluster_reg_kernel<M, 16, 512>, sm5, a);
+            case 20: return launch_cluster(ctx, a, 512, init_cluster_reg_kernel<M, 20, 512>, sm5, a);
+            default: return launch_cluster(ctx, a, 512, init_cluster_reg_kernel<M, 24, 512>, sm5, a);
+            }
+        }
+    }
     const int ppt = ((int)((per + kClusterThreads - 1) / kClusterThreads) + 3) & ~3; // 128-bit runs
     if (ppt < 1 || ppt > ctx->cluster_max_ppt) return false;
     const bool reg = ctx->use_init_reg && ctx->use_mbar_init && (ppt <= 12 || (kClusterThreads < 1024 && ppt <= 24));
     const size_t smem = reg ? (size_t)kClusterThreads * ppt * 3 * sizeof(uint32_t) : cluster_smem<M>(ppt);
     if (smem > 227 * 1024) return false;
+    constexpr int NT = kClusterThreads;
     if (reg) {
         switch (ppt) {
-        case 4: return launch_cluster(ctx, a, init_cluster_reg_kernel<M, 4>, smem, a);
-        case 8: return launch_cluster(ctx, a, init_cluster_reg_kernel<M, 8>, smem, a);
+        case 4: return launch_cluster(ctx, a, NT, init_cluster_reg_kernel<M, 4, NT>, smem, a);
+        case 8: return launch_cluster(ctx, a, NT, init_cluster_reg_kernel<M, 8, NT>, smem, a);
 #if CQG_CLUSTER_THREADS < 1024
-        case 16: return launch_cluster(ctx, a, init_cluster_reg_kernel<M, 16>, smem, a);
-        case 20: return launch_cluster(ctx, a, init_cluster_reg_kernel<M, 20>, smem, a);
-        case 24: return launch_cluster(ctx, a, init_cluster_reg_kernel<M, 24>, smem, a);
+        case 16: return launch_cluster(ctx, a, NT, init_cluster_reg_kernel<M, 16, NT>, smem, a);
+        case 20: return launch_cluster(ctx, a, NT, init_cluster_reg_kernel<M, 20, NT>, smem, a);
+        case 24: return launch_cluster(ctx, a, NT, init_cluster_reg_kernel<M, 24, NT>, smem, a);
 #endif
-        default: return launch_cluster(ctx, a, init_cluster_reg_kernel<M, 12>, smem, a);
+        default: return launch_cluster(ctx, a, NT, init_cluster_reg_kernel<M, 12, NT>, smem, a);
         }
     }
-    return launch_cluster(ctx, a, init_cluster_kernel<M>, smem, a, ppt, ctx->use_mbar_init ? 1 : 0);
+    return launch_cluster(ctx, a, NT, init_cluster_kernel<M>, smem, a, ppt, ctx->use_mbar_init ? 1 : 0);
 }
 
 static int tile_grid(const cqg_ctx *ctx, uint64_t threads) {

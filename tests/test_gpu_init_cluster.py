@@ -36,6 +36,7 @@ def ctxs():
     cs = {"reg": _ctx(),
           "smem": _ctx(CQG_NO_INIT_REG="1"),
           "barrier": _ctx(CQG_NO_MBAR_INIT="1"),
+          "nt1024": _ctx(CQG_NO_CLUSTER_NT512="1"),
           "force_amb": _ctx(CQG_DBG_INIT_FORCE_SEQ="1"),
           "force_nf": _ctx(CQG_DBG_INIT_FORCE_SEQ="2")}
     yield cs
@@ -67,7 +68,7 @@ CASES = [(256, 256, 0.3, 64, 3, 4), (300, 200, 0.02, 64, 9, 4),
          (512, 512, 0.02, 256, 5, 12), (384, 384, 0.6, 200, 11, 12)]
 
 
-@pytest.mark.parametrize("variant", ["reg", "smem", "barrier"])
+@pytest.mark.parametrize("variant", ["reg", "smem", "barrier", "nt1024"])
 @pytest.mark.parametrize("w,h,noise,K,seed,ppt", CASES)
 def test_init_cluster_variants(ctxs, oracle, variant, w, h, noise, K, seed, ppt):
     img = synth_image(w, h, 5, nblobs=10, sigma=15.0, noise=noise)
@@ -80,6 +81,16 @@ def test_init_cluster_variants(ctxs, oracle, variant, w, h, noise, K, seed, ppt)
 def test_init_cluster_sequential_paths(ctxs, oracle, variant, w, h, K, seed):
     img = synth_image(w, h, seed, nblobs=10, sigma=15.0, noise=0.02)
     _check(ctxs[variant], oracle, img, K, seed)
+
+
+@pytest.mark.parametrize("variant", ["reg", "nt1024"])
+@pytest.mark.parametrize("w,h,p512", [(400, 400, 20), (448, 400, 24)])
+def test_init_cluster_maximin_512_runs(ctxs, oracle, variant, w, h, p512):
+    # near-all-unique colours: the 512-thread maximin kernel at 20 and 24
+    # points per thread (the 1024-thread one at 12), both against the oracle
+    img = np.random.default_rng(w + h).integers(0, 256, size=(h, w, 3), dtype=np.uint8)
+    n = _check(ctxs[variant], oracle, img, 64, 4)
+    assert ((-(-(-(-n // 16)) // 512) + 3) & ~3) == p512
 
 
 def test_init_cluster_tiny_and_duplicates(ctxs, oracle):
