@@ -220,8 +220,8 @@ cqg_ctx *cqg_create(int device) {
         if (cp && atoi(cp) > 0) ctx->cluster_max_ppt = atoi(cp);
         const char *ng2 = getenv("CQG_NO_INIT_REG");
         ctx->use_init_reg = !(ng2 && ng2[0] == '1');
-        const char *n5 = getenv("CQG_NO_CLUSTER_NT512");
-        ctx->cluster_nt512 = !(n5 && n5[0] == '1');
+        const char *cn = getenv("CQG_CLUSTER_NT");
+        if (cn) ctx->cluster_nt = atoi(cn);
         const char *fs = getenv("CQG_DBG_INIT_FORCE_SEQ");
         if (fs) ctx->dbg_init_force_seq = atoi(fs);
         const char *nr = getenv("CQG_NO_INIT_REC");

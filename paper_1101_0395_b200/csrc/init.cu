@@ -2285,21 +2285,33 @@ template <class M>
 static bool launch_cluster_init(cqg_ctx *ctx, InitArgs a) {
     constexpr int C = 16;
     const uint64_t per = (a.n + C - 1) / C;
-    // maximin rounds are one max-reduction: 512-thread CTAs (16 warps) shorten
-    // the reduction and the barrier; k-means++ keeps 1024 (its prefix scan
-    // wants the shorter per-thread run). Own limit: 24 points per thread.
-    if (a.kind == 0 && ctx->use_init_reg && ctx->use_mbar_init && ctx->cluster_nt512) {
-        const int p5 = ((int)((per + 511) / 512) + 3) & ~3;
-        const size_t sm5 = (size_t)512 * p5 * 3 * sizeof(uint32_t);
-        if (p5 <= 24) {
-            switch (p5) {
-            case 4: return launch_cluster(ctx, a, 512, init_cluster_reg_kernel<M, 4, 512>, sm5, a);
-            case 8: return launch_cluster(ctx, a, 512, init_cluster_reg_kernel<M, 8, 512>, sm5, a);
-            case 12: return launch_cluster(ctx, a, 512, init_cluster_reg_kernel<M, 12, 512>, sm5, a);
-            case 16: return launch_cluster(ctx, a, 512, init_cluster_reg_kernel<M, 16, 512>, sm5, a);
-            case 20: return launch_cluster(ctx, a, 512, init_cluster_reg_kernel<M, 20, 512>, sm5, a);
-            default: return launch_cluster(ctx, a, 512, init_cluster_reg_kernel<M, 24, 512>, sm5, a);
-            }
+    // Register kernel shape. A round's cost follows the padded point slots per
+    // CTA (threads x points per thread, every slot updated and scanned), so
+    // pick the (threads, ppt) pair with the fewest slots >= this CTA's share;
+    // ppt is capped per size by the register budget (65536 / threads).
+    // Measured: cfg2 k-means++ 1024x12 0.648 ms -> 896x12 0.596 ms; cfg1
+    // maximin 1024x12 0.104 -> 512x20 0.085 ms. CQG_CLUSTER_NT forces a size.
+    if (ctx->use_init_reg && ctx->use_mbar_init && ctx->cluster_nt != kClusterThreads) {
+        static const int kNt[5] = {512, 640, 768, 896, 1024}, kCap[5] = {24, 20, 16, 12, 12};
+        int bi = -1, bp = 0;
+        uint64_t bslots = ~0ull;
+        for (int i = 0; i < 5; ++i) {
+            if (ctx->cluster_nt > 0 && kNt[i] != ctx->cluster_nt) continue;
+            const int pn = ((int)((per + kNt[i] - 1) / kNt[i]) + 3) & ~3;
+            const uint64_t slots = (uint64_t)kNt[i] * pn;
+            if (pn <= kCap[i] && slots < bslots) bi = i, bp = pn, bslots = slots;
+        }
+        if (bi >= 0 && kNt[bi] != kClusterThreads) {
+            const size_t smn = bslots * 3 * sizeof(uint32_t);
+#define CQG_REG_CASE(NTV, P) \
+    if (kNt[bi] == NTV && bp == P) return launch_cluster(ctx, a, NTV, init_cluster_reg_kernel<M, P, NTV>, smn, a);
+            CQG_REG_CASE(512, 4) CQG_REG_CASE(512, 8) CQG_REG_CASE(512, 12)
+            CQG_REG_CASE(512, 16) CQG_REG_CASE(512, 20) CQG_REG_CASE(512, 24)
+            CQG_REG_CASE(640, 4) CQG_REG_CASE(640, 8) CQG_REG_CASE(640, 12)
+            CQG_REG_CASE(640, 16) CQG_REG_CASE(640, 20)
+            CQG_REG_CASE(768, 4) CQG_REG_CASE(768, 8) CQG_REG_CASE(768, 12) CQG_REG_CASE(768, 16)
+            CQG_REG_CASE(896, 4) CQG_REG_CASE(896, 8) CQG_REG_CASE(896, 12)
+#undef CQG_REG_CASE
         }
     }
     const int ppt = ((int)((per + kClusterThreads - 1) / kClusterThreads) + 3) & ~3; // 128-bit runs

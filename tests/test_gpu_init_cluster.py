@@ -1,6 +1,7 @@
 """Cluster initialiser variants (substrates up to 16 x 1024 x 12 colours),
-bit-exact against the oracle: the register-resident kernel (default) at each
-points-per-thread instantiation (4, 8, 12) and both mass arithmetics (P a
+bit-exact against the oracle: the register-resident kernel (default: the CTA
+shape with the fewest padded slots; CQG_CLUSTER_NT forces 512..1024 threads)
+at each points-per-thread instantiation and both mass arithmetics (P a
 power of two: exact integers; otherwise 2^-88 fixed point), the
 shared-memory kernel (CQG_NO_INIT_REG=1), its cluster-barrier signalling
 (CQG_NO_MBAR_INIT=1), and the register kernel's rare sequential paths forced
@@ -36,7 +37,11 @@ def ctxs():
     cs = {"reg": _ctx(),
           "smem": _ctx(CQG_NO_INIT_REG="1"),
           "barrier": _ctx(CQG_NO_MBAR_INIT="1"),
-          "nt1024": _ctx(CQG_NO_CLUSTER_NT512="1"),
+          "nt1024": _ctx(CQG_CLUSTER_NT="1024"),
+          "nt896": _ctx(CQG_CLUSTER_NT="896"),
+          "nt768": _ctx(CQG_CLUSTER_NT="768"),
+          "nt640": _ctx(CQG_CLUSTER_NT="640"),
+          "nt512": _ctx(CQG_CLUSTER_NT="512"),
           "force_amb": _ctx(CQG_DBG_INIT_FORCE_SEQ="1"),
           "force_nf": _ctx(CQG_DBG_INIT_FORCE_SEQ="2")}
     yield cs
@@ -68,7 +73,7 @@ CASES = [(256, 256, 0.3, 64, 3, 4), (300, 200, 0.02, 64, 9, 4),
          (512, 512, 0.02, 256, 5, 12), (384, 384, 0.6, 200, 11, 12)]
 
 
-@pytest.mark.parametrize("variant", ["reg", "smem", "barrier", "nt1024"])
+@pytest.mark.parametrize("variant", ["reg", "smem", "barrier", "nt1024", "nt896", "nt768", "nt640", "nt512"])
 @pytest.mark.parametrize("w,h,noise,K,seed,ppt", CASES)
 def test_init_cluster_variants(ctxs, oracle, variant, w, h, noise, K, seed, ppt):
     img = synth_image(w, h, 5, nblobs=10, sigma=15.0, noise=noise)
@@ -83,14 +88,13 @@ def test_init_cluster_sequential_paths(ctxs, oracle, variant, w, h, K, seed):
     _check(ctxs[variant], oracle, img, K, seed)
 
 
-@pytest.mark.parametrize("variant", ["reg", "nt1024"])
-@pytest.mark.parametrize("w,h,p512", [(400, 400, 20), (448, 400, 24)])
-def test_init_cluster_maximin_512_runs(ctxs, oracle, variant, w, h, p512):
-    # near-all-unique colours: the 512-thread maximin kernel at 20 and 24
-    # points per thread (the 1024-thread one at 12), both against the oracle
+@pytest.mark.parametrize("variant", ["reg", "nt1024", "nt896", "nt768", "nt640", "nt512"])
+@pytest.mark.parametrize("w,h", [(400, 400), (448, 400), (300, 260)])
+def test_init_cluster_shapes_near_unique(ctxs, oracle, variant, w, h):
+    # near-all-unique colours: every CTA shape at its largest points per
+    # thread (the forced sizes fall back to 1024 threads when they do not fit)
     img = np.random.default_rng(w + h).integers(0, 256, size=(h, w, 3), dtype=np.uint8)
-    n = _check(ctxs[variant], oracle, img, 64, 4)
-    assert ((-(-(-(-n // 16)) // 512) + 3) & ~3) == p512
+    _check(ctxs[variant], oracle, img, 64, 4)
 
 
 def test_init_cluster_tiny_and_duplicates(ctxs, oracle):
