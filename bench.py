@@ -235,6 +235,37 @@ def cpu_baseline(cfg, budget_s: float):
 # ---------------------------------------------------------------------------
 # our arm
 
+def parity_digest(cfg, img, k, image_id, st, d_pal, d_idx, d_q):
+    """The bench step's outputs against the C oracle (UPDATE_EXACT), same input."""
+    import hashlib
+    from oracle.pyoracle import UPDATE_EXACT, Oracle
+    t0 = time.perf_counter()
+    O = Oracle()
+    P = img.shape[0] * img.shape[1]
+    c, n, _ = O.histogram(img)
+    init = O.init_kmeanspp(c, n, P, k, cfg.seed) if cfg.init == "kpp" else O.init_maximin(c, n, P, k, cfg.seed)
+    r = O.wsm(c, n, P, init, fixed_it=cfg.fixed_iterations, mode=UPDATE_EXACT)
+    idx, q, mse, mndc = O.map_pixels(img, r.centers, mode=UPDATE_EXACT)
+    pal = d_pal.cpu().numpy()
+    didx = d_idx.cpu().numpy().view(np.uint32)
+    dq = d_q.cpu().numpy().reshape(-1, 3)
+    out = {
+        "checker": "oracle/cq_oracle.c (C restatement, exact moments)", "image": image_id,
+        "palette_sha1": hashlib.sha1(pal.tobytes()).hexdigest()[:16],
+        "palette_equal": bool(np.array_equal(pal.view(np.uint64), r.centers.view(np.uint64))),
+        "n_unique_equal": int(st.n_unique) == int(c.size),
+        "iterations_equal": int(st.lloyd.iterations) == r.iterations,
+        "ndc_equal": int(st.lloyd.ndc_total) == r.ndc_total,
+        "indices_equal": bool(np.array_equal(didx, idx)),
+        "quantized_equal": bool(np.array_equal(dq, q)),
+        "mse_equal": float(st.mean_sq_dist) == mse,
+        "map_ndc_equal": int(st.map_ndc) == mndc,
+        "oracle_s": round(time.perf_counter() - t0, 2),
+    }
+    out["ok"] = all(v for key, v in out.items() if key.endswith("_equal"))
+    return out
+
+
 def run_sharded(args, cfg, ctx, dev, world, rank, stream):
     """One huge image (cfg5 / cfg3) over `world` ranks: histogram and init per
     rank, Lloyd sharded by unique colour with one NCCL allreduce of the int64
@@ -437,7 +468,7 @@ def run_ours(args, cfg):
     profs = [c.read_profile(reset=True) for c in ctxs]
     prof = profs[0]
     for extra in profs[1:]:
-        for i in range(8):
+        for i in range(cabi.PROF_N):
             prof.ms[i] += extra.ms[i]
             prof.units[i] += extra.units[i]
             prof.launches[i] += extra.launches[i]
@@ -472,7 +503,7 @@ def run_ours(args, cfg):
     peaks, peak_kind = measured_peaks()
     sms = torch.cuda.get_device_properties(local).multi_processor_count
     fp32_peak = sms * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
-    names = ["sweep", "map_sweep", "histogram", "pixel_map", "init", "replay", "ndc", "lloyd_loop"]
+    names = ["sweep", "map_sweep", "histogram", "pixel_map", "init", "replay", "ndc", "lloyd_loop", "map_ndc"]
     stage_share = {}
     for i, nm in enumerate(names):
         stage_share[nm] = {"ms_per_step": prof.ms[i] / args.steps,
@@ -586,6 +617,13 @@ def run_ours(args, cfg):
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e_step,
                "index_layout": "uint32 per pixel (MappingResult::indices)"}
 
+    # parity digest of the last timed step's outputs (image 0 of this rank)
+    # against the C oracle (exact-moment mode): palette bytes, iterations,
+    # NDC, mapping indices / pixels / MSE / mapping NDC. A mismatch fails the run.
+    parity = None
+    if rank == 0 and not args.no_parity:
+        parity = parity_digest(cfg, imgs[0], ks[0], my[0], all_stats[-1][0], d_pal[0], d_idx[0], d_q[0])
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(cfg, args.cpu_seconds)
@@ -613,9 +651,12 @@ def run_ours(args, cfg):
                                    "lloyd": st0.ms_lloyd, "map": st0.ms_map},
             "kernels": stage_share, "byte_kernels": byte_kernels,
             "roofline": roofline, "dominant_kernel": dominant, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": int(gpu_launches), "clocks": clocks,
+            "gpu_launches": int(gpu_launches), "clocks": clocks, "parity": parity,
         }
         print(json.dumps(line))
+        if parity is not None and not parity["ok"]:
+            print("bench: device outputs differ from the oracle: " + json.dumps(parity), file=sys.stderr)
+            return 1
     if world > 1:
         dist.destroy_process_group()
     if pool:
@@ -639,6 +680,7 @@ def main():
     ap.add_argument("--workers", type=int, default=4,
                     help="batched configs: concurrent library contexts (streams + host threads) per GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true", help="skip the oracle digest of the outputs")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--sharded", action="store_true",
                     help="run a single-image config through the colour-sharded multi-GPU path")

@@ -103,6 +103,7 @@ typedef struct {
     uint64_t n_unique;   /* substrate_points (pipeline.cpp:117) */
     cqg_lloyd_stats lloyd;
     double mean_sq_dist; /* QuantReport::mse (pipeline.cpp:155) */
+    uint64_t map_ndc;    /* MappingResult::ndc (metrics.cpp:36-48): distances the reference's pruned lookup evaluates */
     double ms_histogram, ms_init, ms_lloyd, ms_map; /* device time per stage (CUDA events) */
 } cqg_quantize_stats;
 
@@ -135,7 +136,8 @@ const char *cqg_version(void);
 #define CQG_PROF_REPLAY 5    /* exact FP64 replays (units: queued points) */
 #define CQG_PROF_NDC 6       /* per-point distance-count (NDC) pass (units: points) */
 #define CQG_PROF_LLOYD 7     /* whole Lloyd loop launches (persistent kernel / graph): units = N' x K x iterations */
-#define CQG_PROF_N 8
+#define CQG_PROF_MAPNDC 8    /* mapping distance count (MappingResult::ndc) (units: distinct colours) */
+#define CQG_PROF_N 9
 typedef struct {
     double ms[CQG_PROF_N];
     double units[CQG_PROF_N];
@@ -174,6 +176,35 @@ int cqg_lloyd(cqg_ctx *ctx, const uint32_t *colors, const uint32_t *counts, uint
               uint32_t *labels, double *sse_trace, cqg_lloyd_stats *stats,
               uint32_t *hist_labels, double *hist_centers);
 
+/* ---- the general Lloyd loop: real points, arbitrary weights (exact FP64) ----
+ * quant::wsm for weights that are not count/P or points off the 8-bit grid
+ * (kmeans.hpp:128-129), and quant::kmeans_full (kmeans.hpp:119) when weights
+ * is NULL (unit weights, full scan every iteration, no repair: an empty
+ * cluster keeps its centre). points: n x 3 doubles; weights: n (positive) or
+ * NULL. Every output -- labels, centres, sse_trace, iterations, ndc_total,
+ * repair_count, history -- is bit-identical to the reference's run_lloyd
+ * (kmeans.cpp:192-260): its sequential FP64 sums are reproduced in order on
+ * the device. Not a throughput path (per-iteration host round trips). */
+int cqg_lloyd_exact(cqg_ctx *ctx, const double *points, const double *weights, uint64_t n, const double *init,
+                    int k, const cqg_term *term, double *centers, uint32_t *labels, double *sse_trace,
+                    cqg_lloyd_stats *stats, uint32_t *hist_labels, double *hist_centers);
+/* API helpers of kmeans.hpp / init.hpp on the device, same arithmetic order:
+ *   cqg_compute_sse            compute_sse (kmeans.hpp:99-105; weights NULL = unit overload)
+ *   cqg_repair_empty_clusters  repair_empty_clusters (kmeans.hpp:112-115): centres, labels in/out
+ *   cqg_center_table           build_center_distance_table (kmeans.hpp:73): k x k dist2, order
+ *   cqg_kmeanspp_next_masses   kmeanspp_next_masses (init.hpp:65-66): weights x min dist2 to the
+ *                              k chosen centres (k = 0: the weights)
+ *   cqg_maximin_pad            maximin_pad (init.hpp:71-72): extend k0 centres to k by maximin picks */
+int cqg_compute_sse(cqg_ctx *ctx, const double *points, const double *weights, uint64_t n, const double *centers,
+                    int k, const uint32_t *labels, double *sse);
+int cqg_repair_empty_clusters(cqg_ctx *ctx, const double *points, const double *weights, uint64_t n,
+                              double *centers, int k, uint32_t *labels, int *repairs);
+int cqg_center_table(cqg_ctx *ctx, const double *centers, int k, double *dist2, uint32_t *order);
+int cqg_kmeanspp_next_masses(cqg_ctx *ctx, const double *colors, const double *weights, uint64_t n,
+                             const double *centers, int k, double *masses);
+int cqg_maximin_pad(cqg_ctx *ctx, const double *colors, uint64_t n, const double *centers, int k0, int k,
+                    double *out);
+
 /* ---- stages 2+3, sharded over ranks (one huge image) -------
  * Each rank holds a contiguous slice of the unique colours. Per iteration:
  *   cqg_shard_assign   local assignment (FULL first, then NDC + WALK sweep +
@@ -201,9 +232,12 @@ int cqg_shard_end(cqg_ctx *ctx, double *centers, uint32_t *labels, double *sse_t
 /* ---- stage 4: exact lowest-index nearest palette entry per pixel + MSE ----
  * indices: P entries of index_bytes (4 = uint32 as MappingResult::indices,
  * 1 = uint8, requires k <= 256); may be NULL. quantized: P*3 bytes (palette
- * rendered with channel_to_u8, color.hpp:63-72); may be NULL. */
+ * rendered with channel_to_u8, color.hpp:63-72); may be NULL. ndc (may be
+ * NULL: not computed) receives MappingResult::ndc, the number of distances the
+ * reference's hint-seeded pruned lookup evaluates (metrics.cpp:36-48,
+ * kmeans.cpp:81-105). */
 int cqg_map(cqg_ctx *ctx, const uint8_t *rgb, uint64_t P, const double *palette, int k,
-            void *indices, int index_bytes, uint8_t *quantized, double *mean_sq_dist);
+            void *indices, int index_bytes, uint8_t *quantized, double *mean_sq_dist, uint64_t *ndc);
 
 /* ---- coarse 32x32x32 histogram (quant::build_coarse_histogram,
  * include/quant/precluster.hpp:32-34; src/precluster.cpp:13-47): the

@@ -501,8 +501,8 @@ out:
 /* ------------------------------------------------------------------------ */
 /* pixel mapping + MSE (reference: src/metrics.cpp:15-55)                    */
 /* mode REFERENCE: the reference's sequential hint walk and FP64 total.      */
-/* mode EXACT: lowest-index exact argmin per colour (the documented result,  */
-/* kmeans.hpp:88-96) and MSE from exact per-cluster pixel moments:           */
+/* mode EXACT: the same lookup (lowest-index exact argmin, kmeans.hpp:88-96; */
+/* ndc = MappingResult::ndc) and MSE from exact per-cluster pixel moments:   */
 /*   sum_k [ (n Q - |S|^2)/n + n*|c - S/n|^2 ] / P, k ascending.             */
 /* ------------------------------------------------------------------------ */
 
@@ -542,16 +542,20 @@ CQO_API int cqo_map_pixels(const uint8_t *rgb, uint64_t P, const double *pal, in
         uint64_t *mn = (uint64_t *)calloc((size_t)K, sizeof(uint64_t));
         int64_t *mS = (int64_t *)calloc(3 * (size_t)K, sizeof(int64_t));
         uint64_t *mQ = (uint64_t *)calloc((size_t)K, sizeof(uint64_t));
+        uint32_t hint = 0;
         for (uint64_t p = 0; p < P; ++p) {
             const uint32_t key = ((uint32_t)rgb[3 * p] << 16) | ((uint32_t)rgb[3 * p + 1] << 8) | rgb[3 * p + 2];
             uint32_t idx;
             if (cache[key] >= 0) {
                 idx = (uint32_t)cache[key];
             } else {
+                /* the same hint-seeded pruned lookup as the reference (so ndc is
+                 * MappingResult::ndc): its result is the exact lowest-index argmin */
                 double x[3];
                 unpack(key, x);
-                idx = cqo_nearest_full(x, pal, K, &ndc); /* strict < : lowest index */
+                idx = cqo_nearest_lowest(x, hint, tab, ord, pal, K, &ndc);
                 cache[key] = (int32_t)idx;
+                hint = idx;
             }
             indices[p] = idx;
             memcpy(quant + 3 * p, pal8 + 3 * idx, 3);

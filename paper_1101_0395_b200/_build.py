@@ -18,7 +18,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(PKG, "build")
 LIB = os.path.join(PKG, "libcqg.so")
-SOURCES = ["hist.cu", "lloyd.cu", "mapk.cu", "init.cu", "api.cu"]
+SOURCES = ["hist.cu", "lloyd.cu", "mapk.cu", "init.cu", "exact.cu", "api.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -39,7 +39,8 @@ EXPORTS = (
     "cqg_shard_donor", "cqg_shard_move", "cqg_shard_end",
 )
 
-PROF_SWEEP, PROF_MAPSWEEP, PROF_HIST, PROF_PIXEL, PROF_INIT, PROF_REPLAY, PROF_NDC, PROF_LLOYD = range(8)
+PROF_SWEEP, PROF_MAPSWEEP, PROF_HIST, PROF_PIXEL, PROF_INIT, PROF_REPLAY, PROF_NDC, PROF_LLOYD, PROF_MAPNDC = range(9)
+PROF_N = 9
 
 
 class Term(C.Structure):
@@ -60,12 +61,12 @@ class QuantizeCfg(C.Structure):
 
 class QuantizeStats(C.Structure):
     _fields_ = [("n_unique", C.c_uint64), ("lloyd", LloydStats), ("mean_sq_dist", C.c_double),
-                ("ms_histogram", C.c_double), ("ms_init", C.c_double), ("ms_lloyd", C.c_double),
+                ("map_ndc", C.c_uint64), ("ms_histogram", C.c_double), ("ms_init", C.c_double), ("ms_lloyd", C.c_double),
                 ("ms_map", C.c_double)]
 
 
 class Profile(C.Structure):
-    _fields_ = [("ms", C.c_double * 8), ("units", C.c_double * 8), ("launches", C.c_uint64 * 8)]
+    _fields_ = [("ms", C.c_double * PROF_N), ("units", C.c_double * PROF_N), ("launches", C.c_uint64 * PROF_N)]
 
 
 class CqgError(RuntimeError):
@@ -113,7 +114,7 @@ def load(path: str = LIB_PATH):
         L.cqg_init_kmeanspp.argtypes = [vp, vp, vp, u64, u64, i32, u64, vp]
         L.cqg_lloyd.argtypes = [vp, vp, vp, u64, u64, vp, i32, C.POINTER(Term), vp, vp, vp,
                                 C.POINTER(LloydStats), vp, vp]
-        L.cqg_map.argtypes = [vp, vp, u64, vp, i32, vp, i32, vp, C.POINTER(C.c_double)]
+        L.cqg_map.argtypes = [vp, vp, u64, vp, i32, vp, i32, vp, C.POINTER(C.c_double), C.POINTER(C.c_uint64)]
         L.cqg_quantize.argtypes = [vp, vp, u64, C.POINTER(QuantizeCfg), vp, vp, vp, vp, vp, vp,
                                    C.POINTER(QuantizeStats)]
         L.cqg_set_profiling.argtypes = [vp, i32]
@@ -248,11 +249,12 @@ class Context:
                                ptr(hist_labels), ptr(hist_centers)))
         return st
 
-    def map_raw(self, rgb, P, palette, k, indices, index_bytes, quantized) -> float:
-        mse = C.c_double(0)
+    def map_raw(self, rgb, P, palette, k, indices, index_bytes, quantized, with_ndc: bool = False):
+        """cqg_map: the mean squared distance, or (mse, MappingResult::ndc) with with_ndc."""
+        mse, ndc = C.c_double(0), C.c_uint64(0)
         check(self.L.cqg_map(self.h, ptr(rgb), P, ptr(palette), k, ptr(indices), index_bytes,
-                             ptr(quantized), C.byref(mse)))
-        return mse.value
+                             ptr(quantized), C.byref(mse), C.byref(ndc) if with_ndc else None))
+        return (mse.value, ndc.value) if with_ndc else mse.value
 
     def quantize_raw(self, rgb, P, cfg: QuantizeCfg, init, palette, labels, sse, indices,
                      quantized) -> QuantizeStats:

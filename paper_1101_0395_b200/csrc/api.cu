@@ -422,6 +422,141 @@ int cqg_lloyd(cqg_ctx *ctx, const uint32_t *colors, const uint32_t *counts, uint
     });
 }
 
+int cqg_lloyd_exact(cqg_ctx *ctx, const double *points, const double *weights, uint64_t n, const double *init,
+                    int k, const cqg_term *term, double *centers, uint32_t *labels, double *sse_trace,
+                    cqg_lloyd_stats *stats, uint32_t *hist_labels, double *hist_centers) {
+    return guarded([&] {
+        use_device(ctx);
+        if (!term) fail(CQG_E_INVALID, "clustering: null termination");
+        validate_run(n, k, *term); // kmeans.cpp:173-188
+        if (term->fixed_iterations < 0) fail(CQG_E_INVALID, "clustering: fixed_iterations < 1");
+        if (!points || !init || !centers || !sse_trace) fail(CQG_E_INVALID, "cqg_lloyd_exact: null argument");
+        const double *pts_d = static_cast<const double *>(stage_in(ctx, points, 24 * n, ctx->raw_col));
+        const double *w_d = nullptr;
+        if (weights) {
+            if (!is_device_ptr(weights))
+                for (uint64_t i = 0; i < n; ++i)
+                    if (!(weights[i] > 0.0)) fail(CQG_E_INVALID, "wsm: weights must be positive"); // kmeans.cpp:275
+            w_d = static_cast<const double *>(stage_in(ctx, weights, 8 * n, ctx->raw_cnt));
+        }
+        const double *init_d = static_cast<const double *>(stage_in(ctx, init, 24 * (size_t)k, ctx->initsel));
+        uint32_t *lab_d = out_buf<uint32_t>(labels, ctx->labels, n);
+        double *cen_d = out_buf<double>(centers, ctx->cen, 3 * (size_t)k);
+        if (cen_d == init_d) fail(CQG_E_INVALID, "cqg_lloyd_exact: centers must not alias init");
+        const ExactOut o = exact_lloyd_dev(ctx, pts_d, w_d, n, init_d, k, *term, weights != nullptr, lab_d, cen_d,
+                                           sse_trace, hist_labels, hist_centers);
+        copy_out(ctx, centers, cen_d, 24 * (size_t)k);
+        copy_out(ctx, labels, lab_d, 4 * n);
+        CQG_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (stats) {
+            *stats = cqg_lloyd_stats{};
+            stats->iterations = o.iterations;
+            stats->repair_count = o.repairs;
+            stats->ndc_total = o.ndc;
+            stats->n_points = n;
+            stats->swept_total = n * (uint64_t)o.iterations;
+        }
+    });
+}
+
+int cqg_compute_sse(cqg_ctx *ctx, const double *points, const double *weights, uint64_t n, const double *centers,
+                    int k, const uint32_t *labels, double *sse) {
+    return guarded([&] {
+        use_device(ctx);
+        if (!sse) fail(CQG_E_INVALID, "compute_sse: null output");
+        if (n == 0) {
+            *sse = 0.0;
+            return;
+        }
+        if (!points || !centers || !labels || k < 1) fail(CQG_E_INVALID, "compute_sse: null argument");
+        const double *pts_d = static_cast<const double *>(stage_in(ctx, points, 24 * n, ctx->raw_col));
+        const double *w_d = weights ? static_cast<const double *>(stage_in(ctx, weights, 8 * n, ctx->raw_cnt)) : nullptr;
+        const double *cen_d = static_cast<const double *>(stage_in(ctx, centers, 24 * (size_t)k, ctx->initsel));
+        const uint32_t *lab_d = static_cast<const uint32_t *>(stage_in(ctx, labels, 4 * n, ctx->labels));
+        double *scratch = static_cast<double *>(ctx->ndc.ensure(64)) + 4;
+        *sse = exact_sse_dev(ctx, pts_d, w_d, n, cen_d, lab_d, scratch);
+    });
+}
+
+int cqg_repair_empty_clusters(cqg_ctx *ctx, const double *points, const double *weights, uint64_t n,
+                              double *centers, int k, uint32_t *labels, int *repairs) {
+    return guarded([&] {
+        use_device(ctx);
+        if (!points || !weights || !centers || !labels || k < 1 || n == 0)
+            fail(CQG_E_INVALID, "repair_empty_clusters: empty input");
+        const double *pts_d = static_cast<const double *>(stage_in(ctx, points, 24 * n, ctx->raw_col));
+        const double *w_d = static_cast<const double *>(stage_in(ctx, weights, 8 * n, ctx->raw_cnt));
+        double *cen_d = out_buf<double>(centers, ctx->cen, 3 * (size_t)k);
+        uint32_t *lab_d = out_buf<uint32_t>(labels, ctx->labels, n);
+        if (cen_d != centers) CQG_CUDA(cudaMemcpyAsync(cen_d, centers, 24 * (size_t)k, cudaMemcpyDefault, ctx->stream));
+        if (lab_d != labels) CQG_CUDA(cudaMemcpyAsync(lab_d, labels, 4 * n, cudaMemcpyDefault, ctx->stream));
+        const int r = exact_repair_dev(ctx, pts_d, w_d, n, cen_d, k, lab_d);
+        copy_out(ctx, centers, cen_d, 24 * (size_t)k);
+        copy_out(ctx, labels, lab_d, 4 * n);
+        CQG_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (repairs) *repairs = r;
+    });
+}
+
+int cqg_center_table(cqg_ctx *ctx, const double *centers, int k, double *dist2, uint32_t *order) {
+    return guarded([&] {
+        use_device(ctx);
+        if (k < 1) {
+            return;
+        }
+        if (!centers || !dist2 || !order) fail(CQG_E_INVALID, "build_center_distance_table: null argument");
+        if (k > 4096) fail(CQG_E_INVALID, "build_center_distance_table: k > 4096 is not supported");
+        const double *cen_d = static_cast<const double *>(stage_in(ctx, centers, 24 * (size_t)k, ctx->initsel));
+        double *dist_d = out_buf<double>(dist2, ctx->dtab, (size_t)k * k);
+        uint32_t *ord_d = out_buf<uint32_t>(order, ctx->order, (size_t)k * k);
+        exact_table_dev(ctx, cen_d, k, dist_d, ord_d);
+        copy_out(ctx, dist2, dist_d, 8 * (size_t)k * k);
+        copy_out(ctx, order, ord_d, 4 * (size_t)k * k);
+        CQG_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int cqg_kmeanspp_next_masses(cqg_ctx *ctx, const double *colors, const double *weights, uint64_t n,
+                             const double *centers, int k, double *masses) {
+    return guarded([&] {
+        use_device(ctx);
+        if (n == 0) return;
+        if (!colors || !weights || !masses || (k > 0 && !centers))
+            fail(CQG_E_INVALID, "kmeanspp_next_masses: null argument");
+        if (k <= 0) { // init.cpp:318: the weights themselves
+            CQG_CUDA(cudaMemcpyAsync(masses, weights, 8 * n, cudaMemcpyDefault, ctx->stream));
+            CQG_CUDA(cudaStreamSynchronize(ctx->stream));
+            return;
+        }
+        const double *pts_d = static_cast<const double *>(stage_in(ctx, colors, 24 * n, ctx->raw_col));
+        const double *w_d = static_cast<const double *>(stage_in(ctx, weights, 8 * n, ctx->raw_cnt));
+        const double *cen_d = static_cast<const double *>(stage_in(ctx, centers, 24 * (size_t)k, ctx->initsel));
+        double *m_d = out_buf<double>(masses, ctx->first, n);
+        exact_next_masses_dev(ctx, pts_d, w_d, n, cen_d, k, m_d);
+        copy_out(ctx, masses, m_d, 8 * n);
+        CQG_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int cqg_maximin_pad(cqg_ctx *ctx, const double *colors, uint64_t n, const double *centers, int k0, int k,
+                    double *out) {
+    return guarded([&] {
+        use_device(ctx);
+        validate_k_init(k, n); // init.cpp:325 (validate_k)
+        if (k0 < 1 || !centers) fail(CQG_E_INVALID, "maximin_pad: need at least one center");
+        if (!out || !colors) fail(CQG_E_INVALID, "maximin_pad: null argument");
+        const int kk = k0 > k ? k0 : k;
+        double *cen_d = out_buf<double>(out, ctx->cen, 3 * (size_t)kk);
+        CQG_CUDA(cudaMemcpyAsync(cen_d, centers, 24 * (size_t)k0, cudaMemcpyDefault, ctx->stream));
+        if (k0 < k) {
+            const double *pts_d = static_cast<const double *>(stage_in(ctx, colors, 24 * n, ctx->raw_col));
+            exact_maximin_pad_dev(ctx, pts_d, n, cen_d, k0, k);
+        }
+        copy_out(ctx, out, cen_d, 24 * (size_t)kk);
+        CQG_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
 int cqg_shard_begin(cqg_ctx *ctx, const uint32_t *colors, const uint32_t *counts, uint64_t n_local, uint64_t P,
                     const double *init, int k, const cqg_term *term) {
     return guarded([&] {
@@ -554,7 +689,7 @@ int cqg_coarse_histogram_weighted(cqg_ctx *ctx, const uint32_t *colors, const ui
 }
 
 int cqg_map(cqg_ctx *ctx, const uint8_t *rgb, uint64_t P, const double *palette, int k, void *indices,
-            int index_bytes, uint8_t *quantized, double *mean_sq_dist) {
+            int index_bytes, uint8_t *quantized, double *mean_sq_dist, uint64_t *ndc) {
     return guarded([&] {
         use_device(ctx);
         if (k < 1 || !palette) fail(CQG_E_INVALID, "map_pixels: empty palette");
@@ -571,11 +706,15 @@ int cqg_map(cqg_ctx *ctx, const uint8_t *rgb, uint64_t P, const double *palette,
         const uint64_t n = histogram_into(ctx, rgb_d, P, col_d, cnt_d, nullptr);
         void *idx_d = indices ? out_buf<uint8_t>(indices, ctx->idx_out, P * (size_t)index_bytes) : nullptr;
         uint8_t *q_d = quantized ? out_buf<uint8_t>(quantized, ctx->q_out, P * 3) : nullptr;
-        const double mse = map_dev(ctx, rgb_d, P, col_d, cnt_d, n, pal_d, k, idx_d, index_bytes, q_d);
+        unsigned long long *ndc_h =
+            ndc ? reinterpret_cast<unsigned long long *>(static_cast<char *>(ctx->pinned.ensure(4096)) + 3072) : nullptr;
+        const double mse = map_dev(ctx, rgb_d, P, col_d, cnt_d, n, pal_d, k, idx_d, index_bytes, q_d, nullptr, nullptr,
+                                   ndc_h);
         copy_out(ctx, indices, idx_d, P * (size_t)index_bytes);
         copy_out(ctx, quantized, q_d, P * 3);
         CQG_CUDA(cudaStreamSynchronize(ctx->stream));
         if (mean_sq_dist) *mean_sq_dist = mse;
+        if (ndc) *ndc = *ndc_h;
     });
 }
 
@@ -590,7 +729,9 @@ int cqg_quantize(cqg_ctx *ctx, const uint8_t *rgb, uint64_t P, const cqg_quantiz
         if (k < 1) fail(CQG_E_INVALID, "run_quantize: k must be at least 1");
         validate_pixels(P, "run_quantize");
         if (!palette) fail(CQG_E_INVALID, "run_quantize: null palette output");
-        const int ib = cfg->index_bytes == 1 ? 1 : 4;
+        if (cfg->index_bytes != 1 && cfg->index_bytes != 4)
+            fail(CQG_E_INVALID, "map_pixels: index_bytes must be 1 or 4");
+        const int ib = cfg->index_bytes;
         if (ib == 1 && k > 256) fail(CQG_E_INVALID, "map_pixels: 8-bit indices need k <= 256");
         const int mode = cfg->sampling;
         if (mode < CQG_SAMPLING_UNIQUE || mode > CQG_SAMPLING_BOTH)
@@ -672,10 +813,11 @@ int cqg_quantize(cqg_ctx *ctx, const uint8_t *rgb, uint64_t P, const cqg_quantiz
         void *idx_d = indices ? out_buf<uint8_t>(indices, ctx->idx_out, P * (size_t)ib) : nullptr;
         uint8_t *q_d = quantized ? out_buf<uint8_t>(quantized, ctx->q_out, P * 3) : nullptr;
         double *mse_h = static_cast<double *>(ctx->pinned.ensure(4096)) + 256; // bytes 2048.. (free here)
+        unsigned long long *mndc_h = reinterpret_cast<unsigned long long *>(mse_h + 1); // MappingResult::ndc
         auto map_and_copy = [&]() {
             // 'unique': the mapping's colours are Lloyd's substrate, so its bounds prune the mapping sweep
             map_dev(ctx, rgb_d, P, map_col, map_cnt, nm, cen_d, k, idx_d, ib, q_d, mse_h,
-                    mode == CQG_SAMPLING_UNIQUE ? &o : nullptr);
+                    mode == CQG_SAMPLING_UNIQUE ? &o : nullptr, mndc_h);
             copy_out(ctx, palette, cen_d, 24 * (size_t)k);
             copy_out(ctx, labels, lab_d, 4 * ns);
             copy_out(ctx, indices, idx_d, P * (size_t)ib);
@@ -702,6 +844,7 @@ int cqg_quantize(cqg_ctx *ctx, const uint8_t *rgb, uint64_t P, const cqg_quantiz
             stats->lloyd.flagged_total = o.flagged;
             stats->lloyd.swept_total = o.swept;
             stats->mean_sq_dist = mse;
+            stats->map_ndc = *mndc_h;
             CQG_CUDA(cudaEventSynchronize(tm.ev[t_map]));
             stats->ms_histogram = tm.ms(t_hist);
             stats->ms_init = tm.ms(t_init);
@@ -744,10 +887,15 @@ cudaError_t launch_cooperative(cqg_ctx *ctx, const void *kern, dim3 grid, dim3 b
 
 namespace cqg {
 cudaError_t ensure_smem(const void *kern, size_t bytes) {
+    // cudaFuncSetAttribute applies to the current device's context only, so
+    // the cache is keyed on (device, kernel)
+    int dev = 0;
+    cudaError_t ge = cudaGetDevice(&dev);
+    if (ge != cudaSuccess) return ge;
     static std::mutex mu;
-    static std::map<const void *, size_t> cur;
+    static std::map<std::pair<int, const void *>, size_t> cur;
     std::lock_guard<std::mutex> lock(mu);
-    size_t &c = cur[kern];
+    size_t &c = cur[{dev, kern}];
     if (bytes <= c) return cudaSuccess;
     const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     if (e == cudaSuccess) c = bytes;

@@ -127,7 +127,7 @@ struct cqg_ctx {
     cqg::DevBuf mom_g, partial; // sharded Lloyd: global moments, packed partials
     void *shard = nullptr;      // cqg::ShardState (lloyd.cu)
     // mapping
-    cqg::DevBuf lut, idx_out, q_out, mom_map;
+    cqg::DevBuf lut, idx_out, q_out, mom_map, map_rows;
     cqg::DevBuf coarse; // 5 x 32768 u64 coarse histogram (cqg_coarse_histogram)
     // init
     cqg::DevBuf mind2, initpart, initsel, unit_draws, inittile;
@@ -264,6 +264,25 @@ LloydOut lloyd_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *count
                    double *hist_centers_user, bool allow_defer = false);
 
 void bench_sweep_dev(cqg_ctx *ctx, int reps, double *ms, double *units);
+
+// exact.cu: the reference's Lloyd loop for arbitrary real points and weights
+// (w_d null = unit weights), bit-identical to run_lloyd; device pointers
+struct ExactOut {
+    int iterations = 0;
+    int repairs = 0;
+    unsigned long long ndc = 0;
+};
+ExactOut exact_lloyd_dev(cqg_ctx *ctx, const double *pts_d, const double *w_d, uint64_t n, const double *init_d,
+                         int K, const cqg_term &term, bool prune_repair, uint32_t *lab_d, double *cen_d,
+                         double *sse_host, uint32_t *hist_labels_user, double *hist_centers_user);
+void exact_table_dev(cqg_ctx *ctx, const double *cen_d, int K, double *dist_d, uint32_t *order_d);
+double exact_sse_dev(cqg_ctx *ctx, const double *pts_d, const double *w_d, uint64_t n, const double *cen_d,
+                     const uint32_t *lab_d, double *scratch_d);
+int exact_repair_dev(cqg_ctx *ctx, const double *pts_d, const double *w_d, uint64_t n, double *cen_d, int K,
+                     uint32_t *lab_d);
+void exact_next_masses_dev(cqg_ctx *ctx, const double *pts_d, const double *w_d, uint64_t n, const double *cen_d,
+                           int k0, double *mass_d);
+void exact_maximin_pad_dev(cqg_ctx *ctx, const double *pts_d, uint64_t n, double *cen_d, int k0, int k);
 // sharded Lloyd (lloyd.cu); device pointers unless noted
 void shard_begin_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *counts_d, uint64_t n, uint64_t P,
                      const double *init_d, int K, const cqg_term &term);
@@ -287,7 +306,8 @@ void coarse_hist_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *cou
 double map_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P, const uint32_t *colors_d,
                const uint32_t *counts_d, uint64_t n, const double *pal_d, int k, void *indices_d,
                int index_bytes, uint8_t *quant_d,
-               double *mse_async = nullptr, const LloydOut *lloyd = nullptr);
+               double *mse_async = nullptr, const LloydOut *lloyd = nullptr,
+               unsigned long long *ndc_async = nullptr); // MappingResult::ndc (pinned host), null: skip
 
 void init_maximin_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *counts_d, uint64_t n,
                       uint64_t P, int k, uint64_t seed, int weighted_first, double *centers_d);

@@ -1426,9 +1426,18 @@ __device__ __forceinline__ void mbar_complete_local(uint64_t *bar, uint32_t byte
     asm volatile("mbarrier.complete_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
                  : "memory");
 }
-// wait for the barrier phase with the given parity; traps instead of hanging
+// wait for the barrier phase with the given parity. A signal that never comes
+// (a protocol bug) traps after 30 s of wall-clock time (%globaltimer, checked
+// every 4096 polls), so preemption or time slicing (MPS, a debugger) cannot
+// trip it while a slow but valid signal is on its way; the GPU never hangs.
+__device__ __forceinline__ uint64_t global_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     const uint32_t a = smem_addr(bar);
+    uint64_t t0 = 0;
     for (uint32_t spin = 0;; ++spin) {
         uint32_t ok;
         asm volatile("{\n\t.reg .pred p;\n\t"
@@ -1438,7 +1447,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
                      : "r"(a), "r"(parity)
                      : "memory");
         if (ok) return;
-        if (spin > (1u << 26)) __trap(); // a lost signal: abort the kernel, never hang the GPU
+        if ((spin & 4095u) == 4095u) {
+            const uint64_t t = global_ns();
+            if (t0 == 0) t0 = t;
+            else if (t - t0 > 30000000000ull) __trap(); // lost signal: abort the kernel, never hang the GPU
+        }
     }
 }
 __device__ __forceinline__ void st_async_u64(uint32_t raddr, unsigned long long v, uint32_t rbar) {

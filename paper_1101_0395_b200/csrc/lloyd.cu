@@ -620,16 +620,18 @@ size_t sweep_smem_bytes(int K, int Kp, int mode) {
 }
 
 template <int MODE, int PPT>
-static int sweep_bps(size_t smem) {
-    // occupancy per (kernel, smem): cached so launches do no host-side queries
+static int sweep_bps(const cqg_ctx *ctx, size_t smem) {
+    // occupancy per (device, kernel, smem): cached so launches do no host-side queries
     static thread_local size_t c_smem = (size_t)-1;
+    static thread_local int c_dev = -1;
     static thread_local int c_bps = 1;
-    if (c_smem == smem) return c_bps;
+    if (c_smem == smem && c_dev == ctx->device) return c_bps;
     int bps = 0;
     CQG_CUDA(ensure_smem((const void *)sweep_kernel<MODE, PPT>, smem));
     CQG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, sweep_kernel<MODE, PPT>, kSweepThreads, smem));
     c_bps = bps < 1 ? 1 : bps;
     c_smem = smem;
+    c_dev = ctx->device;
     return c_bps;
 }
 
@@ -650,22 +652,16 @@ static void launch_sweep_mode(cqg_ctx *ctx, const SweepArgs &a) {
     const uint64_t sms = (uint64_t)ctx->num_sms;
     if (MODE == MODE_WALK) {
         const size_t csm = a.K <= 2048 ? (size_t)a.K * 24 : 0;
-        static thread_local bool attr = false;
-        if (!attr && csm > 48 * 1024) {
+        if (csm > 48 * 1024) { // ensure_smem caches per (device, kernel)
             CQG_CUDA(ensure_smem((const void *)ndc_kernel<8>, 2048 * 24));
             CQG_CUDA(ensure_smem((const void *)ndc_kernel<2>, 2048 * 24));
-            attr = true;
         }
         const bool big = n >= (uint64_t)ctx->num_sms * 4 * 256 * 8;
         const int g = big ? pick_grid(ctx, n, 2048, 4) : pick_grid(ctx, n, 512, 8);
         const int pn = prof_begin(ctx);
         if (a.dcode && a.K <= kNdcCodeMaxK) {
             const size_t cs = (size_t)a.K * 24 + (size_t)a.K * (a.Kpow + 2) * 2;
-            static thread_local bool cattr = false;
-            if (!cattr) {
-                CQG_CUDA(ensure_smem((const void *)ndc_code_kernel<4>, kNdcCodeMaxK * 24 + kNdcCodeMaxK * (kNdcCodeMaxK + 2) * 2));
-                cattr = true;
-            }
+            CQG_CUDA(ensure_smem((const void *)ndc_code_kernel<4>, kNdcCodeMaxK * 24 + kNdcCodeMaxK * (kNdcCodeMaxK + 2) * 2));
             const int gc = pick_grid(ctx, n, 1024 * 4, 1);
             ndc_code_kernel<4><<<gc, 1024, cs, ctx->stream>>>(a.colors, a.labels, n, a.cen, a.dsorted, a.dcode,
                                                              a.K, a.Kpow, a.ndc);
@@ -678,7 +674,7 @@ static void launch_sweep_mode(cqg_ctx *ctx, const SweepArgs &a) {
     }
     // smallest points-per-thread whose single wave covers all points (fewest
     // idle lanes, most blocks); large inputs loop over 8-point tiles
-    const int b2 = sweep_bps<MODE, 2>(smem), b4 = sweep_bps<MODE, 4>(smem), b8 = sweep_bps<MODE, 8>(smem);
+    const int b2 = sweep_bps<MODE, 2>(ctx, smem), b4 = sweep_bps<MODE, 4>(ctx, smem), b8 = sweep_bps<MODE, 8>(ctx, smem);
     int ppt, bps;
     if (n <= sms * b2 * kSweepThreads * 2) ppt = 2, bps = b2;
     else if (n <= sms * b4 * kSweepThreads * 4) ppt = 4, bps = b4;
@@ -716,8 +712,8 @@ void bench_sweep_dev(cqg_ctx *ctx, int reps, double *ms, double *units) {
     launched(ctx);
     const size_t smem = sweep_smem_bytes(a.K, a.Kp, MODE_WALK);
     const uint64_t sms = (uint64_t)ctx->num_sms, n = a.n;
-    const int b2 = sweep_bps<MODE_WALK, 2>(smem), b4 = sweep_bps<MODE_WALK, 4>(smem),
-              b8 = sweep_bps<MODE_WALK, 8>(smem);
+    const int b2 = sweep_bps<MODE_WALK, 2>(ctx, smem), b4 = sweep_bps<MODE_WALK, 4>(ctx, smem),
+              b8 = sweep_bps<MODE_WALK, 8>(ctx, smem);
     int ppt, bps;
     if (n <= sms * b2 * kSweepThreads * 2) ppt = 2, bps = b2;
     else if (n <= sms * b4 * kSweepThreads * 4) ppt = 4, bps = b4;
@@ -899,13 +895,15 @@ static bool launch_persistent(cqg_ctx *ctx, const SweepArgs &a, IterArgs ia, boo
     const void *kern = ppt == 2 ? (const void *)lloyd_persistent_kernel<2> : (const void *)lloyd_persistent_kernel<4>;
     static thread_local const void *c_kern = nullptr;
     static thread_local size_t c_smem = 0;
+    static thread_local int c_dev = -1;
     static thread_local int c_bps = 0;
     int bps = c_bps;
-    if (c_kern != kern || c_smem != smem) {
+    if (c_kern != kern || c_smem != smem || c_dev != ctx->device) {
         CQG_CUDA(ensure_smem((const void *)kern, (int)smem));
         CQG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, kSweepThreads, smem));
         c_kern = kern;
         c_smem = smem;
+        c_dev = ctx->device;
         c_bps = bps;
     }
     if (bps < 1) return false;

@@ -12,6 +12,16 @@
 //   mse_kernel                mean_sq_dist = sum_k [(nQ-|S|^2)/n + n|c-S/n|^2] / P
 //                             from those moments (deterministic, ~1e-14 of the
 //                             reference's sequential FP64 sum);
+//   map_walk_kernel +         MappingResult::ndc: the reference resolves the
+//   map_ndc_kernel            distinct colours in first-occurrence order with the
+//                             hint = the index chosen for the previous distinct
+//                             colour (0 for the first), and the pruned walk
+//                             evaluates 1 + #{j >= 1 : D[hint][order_j] <= 4 d2(x, c_hint)}
+//                             distances (it breaks only on '>'). The walk row is
+//                             ascending (self, distance 0, first), so that count
+//                             is the number of row entries <= the cutoff: a
+//                             binary search per colour over the palette's sorted
+//                             distance rows, all colours in parallel;
 //   pixel_kernel              per pixel: LUT gather -> index (u8 or u32) and the
 //                             palette colour rendered by channel_to_u8
 //                             (color.hpp:63-72); 16 pixels / thread, 128-bit
@@ -148,11 +158,128 @@ __global__ void __launch_bounds__(256) pixel_kernel(const uint8_t *__restrict__ 
     }
 }
 
+
+// Palette walk rows for the mapping NDC (kmeans.cpp:14-38 distances): row i
+// holds d2(c_i, c_j) for every j (self = 0 included) ascending, padded with
+// +inf to Kpow; with K <= 256 also as 16-bit codes (code16, sweep.cuh).
+__global__ void __launch_bounds__(256) map_walk_kernel(const double *__restrict__ pal, int K, int Kpow,
+                                                       double *__restrict__ rows, uint16_t *__restrict__ codes) {
+    extern __shared__ unsigned long long s_k[]; // Kpow keys (bits of non-negative doubles order like the values)
+    const int i = blockIdx.x;
+    const double cr = pal[3 * i], cg = pal[3 * i + 1], cb = pal[3 * i + 2];
+    for (int j = threadIdx.x; j < Kpow; j += blockDim.x)
+        s_k[j] = j < K ? (unsigned long long)__double_as_longlong(
+                             d2_exact(cr, cg, cb, pal[3 * j], pal[3 * j + 1], pal[3 * j + 2]))
+                       : 0x7FF0000000000000ull;
+    __syncthreads();
+    for (int size = 2; size <= Kpow; size <<= 1)
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int t = threadIdx.x; t < (Kpow >> 1); t += blockDim.x) {
+                const int lo = 2 * t - (t & (stride - 1)), hi = lo + stride;
+                const bool up = (lo & size) == 0;
+                const unsigned long long a = s_k[lo], b = s_k[hi];
+                if ((a > b) == up) {
+                    s_k[lo] = b;
+                    s_k[hi] = a;
+                }
+            }
+            __syncthreads();
+        }
+    for (int j = threadIdx.x; j < Kpow; j += blockDim.x) {
+        const double d = __longlong_as_double((long long)s_k[j]);
+        rows[(size_t)i * Kpow + j] = d;
+        if (codes) codes[(size_t)i * Kpow + j] = (uint16_t)code16(d);
+    }
+}
+
+// Mapping NDC (metrics.cpp:36-48 + kmeans.cpp:81-105): colour i of the image's
+// distinct colours in first-occurrence order resolves with hint = LUT[colour
+// i-1] (0 for i = 0) and costs #{row entries <= 4 d2(x, c_hint)} distances.
+// "<= cut" is counted as "< nextup(cut)" (no double lies between). CODES:
+// rows as 16-bit codes in shared memory (K <= 256), FP64 only on code ties;
+// otherwise the FP64 rows through L1. Q colours per thread in flight.
+template <bool CODES, int Q, int NT>
+__global__ void __launch_bounds__(NT) map_ndc_kernel(const uint32_t *__restrict__ colors, uint64_t n,
+                                                      const uint8_t *__restrict__ lut8,
+                                                      const uint32_t *__restrict__ lut32,
+                                                      const double *__restrict__ pal, int K, int Kpow,
+                                                      const double *__restrict__ rows,
+                                                      const uint16_t *__restrict__ codes,
+                                                      unsigned long long *ndc) {
+    extern __shared__ __align__(16) double s_pal[];
+    const int rs = Kpow + 2; // code row stride (one padding word spreads rows over the banks)
+    uint16_t *s_code = reinterpret_cast<uint16_t *>(s_pal + 3 * K);
+    for (int i = threadIdx.x; i < 3 * K; i += blockDim.x) s_pal[i] = pal[i];
+    if (CODES)
+        for (int e = threadIdx.x; e < K * Kpow; e += NT) {
+            const int r = e / Kpow, c = e - r * Kpow;
+            s_code[r * rs + c] = codes[e];
+        }
+    __syncthreads();
+    unsigned long long local = 0;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * Q;
+    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x * Q; base < n; base += stride) {
+        double cut[Q];
+        uint32_t cc[Q];
+        int hint[Q], pos[Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const uint64_t i = base + threadIdx.x + (uint64_t)q * blockDim.x;
+            const bool v = i < n;
+            const uint32_t col = v ? __ldg(colors + i) : 0u;
+            uint32_t h = 0;
+            if (v && i > 0) {
+                const uint32_t pc = __ldg(colors + i - 1);
+                h = lut8 ? (uint32_t)__ldg(lut8 + pc) : __ldg(lut32 + pc);
+            }
+            const double pd = d2_exact((double)((col >> 16) & 255u), (double)((col >> 8) & 255u),
+                                       (double)(col & 255u), s_pal[3 * h], s_pal[3 * h + 1], s_pal[3 * h + 2]);
+            // nextup(4 pd): the cutoff is non-negative, so the next double up is bits + 1
+            cut[q] = v ? __longlong_as_double(__double_as_longlong(__dmul_rn(4.0, pd)) + 1) : -1.0;
+            cc[q] = v ? code16(cut[q]) : 0u;
+            hint[q] = (int)h;
+            pos[q] = 0;
+        }
+        for (int step = Kpow >> 1; step >= 1; step >>= 1) {
+            if (CODES) {
+                uint32_t vv[Q];
+#pragma unroll
+                for (int q = 0; q < Q; ++q) vv[q] = s_code[hint[q] * rs + pos[q] + step - 1];
+#pragma unroll
+                for (int q = 0; q < Q; ++q) pos[q] += vv[q] < cc[q] ? step : 0;
+            } else {
+                double vv[Q];
+#pragma unroll
+                for (int q = 0; q < Q; ++q) vv[q] = __ldg(rows + (size_t)hint[q] * Kpow + pos[q] + step - 1);
+#pragma unroll
+                for (int q = 0; q < Q; ++q) pos[q] += vv[q] < cut[q] ? step : 0;
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            if (cut[q] < 0.0) continue;
+            const double *grow = rows + (size_t)hint[q] * Kpow;
+            int p = pos[q];
+            if (CODES) {
+                const uint16_t *row = s_code + hint[q] * rs;
+                if (p == Kpow - 1 && row[Kpow - 1] < cc[q]) p = Kpow;
+                while (p < Kpow && row[p] == cc[q] && __ldg(grow + p) < cut[q]) ++p; // code ties: FP64
+            } else if (p == Kpow - 1 && __ldg(grow + Kpow - 1) < cut[q]) {
+                p = Kpow; // the lifting reaches Kpow - 1 at most
+            }
+            local += (unsigned long long)p;
+        }
+    }
+    for (int o = 16; o; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+    if ((threadIdx.x & 31) == 0 && local) atomicAdd(ndc, local);
+}
+
 } // namespace
 
 double map_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P, const uint32_t *colors_d,
                const uint32_t *counts_d, uint64_t n, const double *pal_d, int K, void *indices_d,
-               int index_bytes, uint8_t *quant_d, double *mse_async, const LloydOut *lloyd) {
+               int index_bytes, uint8_t *quant_d, double *mse_async, const LloydOut *lloyd,
+               unsigned long long *ndc_async) {
     cudaStream_t s = ctx->stream;
     const int Kp = (K + 7) & ~7;
     const bool lut8 = K <= 256;
@@ -161,6 +288,7 @@ double map_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P, const uint32_t *c
     void *lut = ctx->lut.ensure(lut8 ? (1u << 24) : (sizeof(uint32_t) << 24));
     Moments *mom = static_cast<Moments *>(ctx->mom_map.ensure(sizeof(Moments) * (size_t)K + 64));
     double *mse_d = reinterpret_cast<double *>(mom + K);
+    unsigned long long *ndc_d = reinterpret_cast<unsigned long long *>(mse_d + 1);
     uint32_t *queue = static_cast<uint32_t *>(ctx->queue.ensure(sizeof(uint32_t) * (n + 1)));
     uint32_t *qn = static_cast<uint32_t *>(ctx->scal.ensure(256));
 
@@ -203,6 +331,41 @@ double map_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P, const uint32_t *c
         CQG_CUDA(ensure_smem((const void *)mse_kernel, K * 8));
     mse_kernel<<<1, 256, (size_t)K * 8, s>>>(mom, pal_d, K, P, mse_d);
     launched(ctx);
+
+    if (ndc_async) { // MappingResult::ndc
+        int Kpow = 1;
+        while (Kpow < K) Kpow <<= 1;
+        const bool codes = K <= 256 && n >= (1ull << 21); // code rows pay off for many colours
+        double *rows = static_cast<double *>(ctx->map_rows.ensure(sizeof(double) * (size_t)K * Kpow +
+                                                                  (codes ? sizeof(uint16_t) * (size_t)K * Kpow : 0)));
+        uint16_t *crow = codes ? reinterpret_cast<uint16_t *>(rows + (size_t)K * Kpow) : nullptr;
+        CQG_CUDA(cudaMemsetAsync(ndc_d, 0, 8, s));
+        const size_t wsm = sizeof(unsigned long long) * (size_t)Kpow;
+        if (wsm > 48 * 1024) CQG_CUDA(ensure_smem((const void *)map_walk_kernel, wsm));
+        map_walk_kernel<<<K, 256, wsm, s>>>(pal_d, K, Kpow, rows, crow);
+        launched(ctx);
+        const int pn = prof_begin(ctx);
+        if (codes) {
+            // many colours: the rows as 16-bit codes in every block's shared memory
+            const size_t sm = (size_t)K * 24 + (size_t)K * (Kpow + 2) * 2;
+            CQG_CUDA(ensure_smem((const void *)map_ndc_kernel<true, 4, 512>, sm));
+            const uint64_t g = (n + 2048 - 1) / 2048, gmax = (uint64_t)ctx->num_sms;
+            map_ndc_kernel<true, 4, 512><<<(unsigned)(g < gmax ? g : gmax), 512, sm, s>>>(
+                colors_d, n, a.lut8, a.lut32, pal_d, K, Kpow, rows, crow, ndc_d);
+        } else {
+            // few colours (a small preload would dominate): FP64 rows through L1/L2
+            const size_t sm = (size_t)K * 24;
+            if (sm > 48 * 1024) CQG_CUDA(ensure_smem((const void *)map_ndc_kernel<false, 4, 256>, sm));
+            uint64_t g = (n + 1024 - 1) / 1024;
+            const uint64_t gmax = (uint64_t)ctx->num_sms * 8;
+            if (g > gmax) g = gmax;
+            map_ndc_kernel<false, 4, 256><<<(unsigned)(g ? g : 1), 256, sm, s>>>(
+                colors_d, n, a.lut8, a.lut32, pal_d, K, Kpow, rows, nullptr, ndc_d);
+        }
+        prof_end(ctx, CQG_PROF_MAPNDC, pn, (double)n);
+        launched(ctx);
+        CQG_CUDA(cudaMemcpyAsync(ndc_async, ndc_d, 8, cudaMemcpyDeviceToHost, s));
+    }
 
     if (indices_d || quant_d) {
         const int vec = ((reinterpret_cast<uintptr_t>(rgb_d) | reinterpret_cast<uintptr_t>(indices_d) |

@@ -532,7 +532,7 @@ MappingResult map_pixels(const RawImage &image, const Palette &palette) {
     const std::vector<double> pal = flatten(palette.colors);
     check(cqg_map(ctx(), reinterpret_cast<const std::uint8_t *>(image.pixels.data()), P, pal.data(),
                   static_cast<int>(palette.size()), out.indices.data(), 4,
-                  reinterpret_cast<std::uint8_t *>(out.quantized.pixels.data()), &out.mean_sq_dist));
+                  reinterpret_cast<std::uint8_t *>(out.quantized.pixels.data()), &out.mean_sq_dist, &out.ndc));
     return out;
 }
 
@@ -705,6 +705,7 @@ QuantizeResult run_quantize(const RawImage &image, const QuantizeConfig &config)
     const auto t1 = std::chrono::steady_clock::now();
     out.palette.colors = unflatten(pal.data(), static_cast<std::size_t>(k));
     out.mapping.mean_sq_dist = st.mean_sq_dist;
+    out.mapping.ndc = st.map_ndc;
     out.state.centers = out.palette.colors;
     out.state.memberships.assign(labels.begin(), labels.begin() + static_cast<std::ptrdiff_t>(st.n_unique));
     out.state.sse_trace.assign(sse.begin(), sse.begin() + st.lloyd.iterations);

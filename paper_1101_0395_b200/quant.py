@@ -423,8 +423,8 @@ def map_pixels(image, palette, index_bytes: int = 4,
         raise ValueError("map_pixels: empty image")
     idx = np.empty(P, np.uint8 if index_bytes == 1 else np.uint32)
     q = np.empty((h, w, 3) if h > 1 or isinstance(image, RawImage) else (P, 3), np.uint8)
-    mse = ctx.map_raw(arr, P, pal, k, idx, index_bytes, q)
-    return MappingResult(idx, q, mse, 0)
+    mse, ndc = ctx.map_raw(arr, P, pal, k, idx, index_bytes, q, with_ndc=True)
+    return MappingResult(idx, q, mse, ndc)
 
 
 def mse(a, b) -> float:
@@ -609,7 +609,7 @@ def run_quantize(image, config: QuantizeConfig, ctx: Optional[cabi.Context] = No
     state = ClusterState(palette.copy(), labels[:n].copy(), sse[:it].copy(), it,
                          int(st.lloyd.ndc_total), int(st.lloyd.repair_count), [],
                          int(st.lloyd.flagged_total), int(st.lloyd.swept_total))
-    mapping = MappingResult(idx, q, float(st.mean_sq_dist), 0)
+    mapping = MappingResult(idx, q, float(st.mean_sq_dist), int(st.map_ndc))
     rep = QuantReport(method=config.method.token(), k_requested=k, k_actual=k,
                       seed=int(config.seed), sampling=config.sampling, mse=mapping.mean_sq_dist,
                       psnr=psnr_from_mse(mapping.mean_sq_dist), iterations=it,

@@ -73,7 +73,7 @@ def main() -> None:
         colors, counts, _ = R.histogram(img, seed)
         init = R.init(kind, colors, counts, 1600, K, seed)
         res = R.wsm(colors, counts, 1600, init, history=True)
-        idx, q, mse, _ = R.map_pixels(img, 40, 40, res.centers)
+        idx, q, mse, mndc = R.map_pixels(img, 40, 40, res.centers)
         cases.append(dict(
             image=img_seed, k=K, init=kind, seed=seed,
             n_unique=int(colors.size),
@@ -84,7 +84,7 @@ def main() -> None:
             iterations=res.iterations, ndc_total=res.ndc_total, repairs=res.repairs,
             labels=res.labels.tolist(),
             history_labels=res.hist_labels.tolist(),
-            map_indices=idx.tolist(), map_mse=float(mse).hex(),
+            map_indices=idx.tolist(), map_mse=float(mse).hex(), map_ndc=int(mndc),
         ))
     with open(os.path.join(HERE, "ref_cases.json"), "w") as f:
         json.dump(cases, f)

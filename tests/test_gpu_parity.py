@@ -319,27 +319,30 @@ def test_map_bit_exact(ctx, oracle, reflib, K, ib):
     rng = np.random.default_rng(K)
     pal = rng.random((K, 3)) * 255.0
     m = quant.map_pixels(img, pal, index_bytes=ib, ctx=ctx)
-    idx, q, mse_e, _ = oracle.map_pixels(img, pal, mode=UPDATE_EXACT)
+    idx, q, mse_e, ndc_e = oracle.map_pixels(img, pal, mode=UPDATE_EXACT)
     assert np.array_equal(m.indices.astype(np.uint32), idx)
     assert np.array_equal(m.quantized.reshape(-1, 3), q)
     assert m.mean_sq_dist == mse_e
-    i2, q2, mse_r, _ = reflib.map_pixels(img, 160, 120, pal)
+    assert m.ndc == ndc_e
+    i2, q2, mse_r, ndc_r = reflib.map_pixels(img, 160, 120, pal)
     assert np.array_equal(m.indices.astype(np.uint32), i2)
     assert abs(m.mean_sq_dist - mse_r) <= 1e-12 * mse_r
+    assert m.ndc == ndc_r  # MappingResult::ndc (metrics.cpp:36-48)
 
 
 @pytest.mark.parametrize("w,h,K,ib", [(1031, 1025, 256, 4), (1024, 1024, 64, 1), (1100, 977, 300, 4)])
 def test_map_large_streaming(ctx, oracle, w, h, K, ib):
-    # P >= 2^20 takes the TMA-fed streaming kernel over 512-pixel warp chunks;
-    # 1031x1025 and 1100x977 leave a remainder for the plain kernel
+    # P >= 2^20: the vectorised 16-pixel path of pixel_kernel; 1031x1025 and
+    # 1100x977 leave a remainder for its scalar tail
     img = synth_image(w, h, 5 + K, nblobs=12, sigma=18.0, noise=0.2)
     rng = np.random.default_rng(w + K)
     pal = rng.random((K, 3)) * 255.0
     m = quant.map_pixels(img, pal, index_bytes=ib, ctx=ctx)
-    idx, q, mse_e, _ = oracle.map_pixels(img, pal, mode=UPDATE_EXACT)
+    idx, q, mse_e, ndc_e = oracle.map_pixels(img, pal, mode=UPDATE_EXACT)
     assert np.array_equal(m.indices.astype(np.uint32), idx)
     assert np.array_equal(m.quantized.reshape(-1, 3), q)
     assert m.mean_sq_dist == mse_e
+    assert m.ndc == ndc_e
 
 
 def test_map_reference_cases(ctx):
@@ -364,10 +367,11 @@ def test_map_ties_to_lowest_index(ctx, oracle):
     pal[10] = pal[3]  # duplicate entry: must never be chosen over 3
     img = rng.integers(0, 256, (128, 128, 3), dtype=np.uint8)
     m = quant.map_pixels(img, pal, ctx=ctx)
-    idx, _, mse_e, _ = oracle.map_pixels(img, pal, mode=UPDATE_EXACT)
+    idx, _, mse_e, ndc_e = oracle.map_pixels(img, pal, mode=UPDATE_EXACT)
     assert np.array_equal(m.indices, idx)
     assert not np.any(m.indices == 10)
     assert m.mean_sq_dist == mse_e
+    assert m.ndc == ndc_e  # cutoff ties (D == 4 d2 exactly) are evaluated: '>' break
 
 
 # ---------------------------------------------------------------------------
@@ -406,10 +410,11 @@ def test_pipeline_vs_reference(ctx, oracle, reflib, name):
     assert np.array_equal(r.palette, ref["palette"])  # P = 2^18
     assert abs(r.report.mse - ref["mse"]) <= 1e-12 * ref["mse"]
     # mapping outputs bit-exact vs the exact oracle on the same palette
-    idx, q, mse_e, _ = oracle.map_pixels(img, r.palette, mode=UPDATE_EXACT)
+    idx, q, mse_e, ndc_e = oracle.map_pixels(img, r.palette, mode=UPDATE_EXACT)
     assert np.array_equal(r.mapping.indices, idx)
     assert np.array_equal(r.mapping.quantized.reshape(-1, 3), q)
     assert r.report.mse == mse_e
+    assert r.mapping.ndc == ndc_e
 
 
 # ---------------------------------------------------------------------------

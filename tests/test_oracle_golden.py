@@ -84,9 +84,10 @@ def test_oracle_matches_reference_cases_bitwise(oracle):
         assert r.ndc_total == c["ndc_total"]
         assert r.labels.tolist() == c["labels"]
         assert r.hist_labels.tolist() == c["history_labels"]
-        idx, _, mse, _ = oracle.map_pixels(img, r.centers, mode=UPDATE_REFERENCE)
+        idx, _, mse, mndc = oracle.map_pixels(img, r.centers, mode=UPDATE_REFERENCE)
         assert idx.tolist() == c["map_indices"]
         assert float(mse).hex() == c["map_mse"]
+        assert mndc == c["map_ndc"]  # MappingResult::ndc (metrics.cpp:36-48)
         # exact-moment mode: same trajectory; P = 1600 is not a power of two so
         # centres may differ in the last bits, SSE within 1e-12
         e = oracle.wsm(colors, counts, 1600, init, mode=UPDATE_EXACT, history=True)
@@ -135,6 +136,6 @@ def test_oracle_vs_reference_library(oracle, reflib, seed, K, kind):
     assert np.array_equal(a.sse_trace, b.sse_trace)
     assert np.array_equal(a.hist_labels, b.hist_labels)
     assert a.ndc_total == b.ndc_total and a.repairs == b.repairs
-    i1, q1, m1, _ = oracle.map_pixels(img, b.centers, mode=UPDATE_REFERENCE)
-    i2, q2, m2, _ = reflib.map_pixels(img, 128, 96, b.centers)
-    assert np.array_equal(i1, i2) and np.array_equal(q1, q2) and m1 == m2
+    i1, q1, m1, n1 = oracle.map_pixels(img, b.centers, mode=UPDATE_REFERENCE)
+    i2, q2, m2, n2 = reflib.map_pixels(img, 128, 96, b.centers)
+    assert np.array_equal(i1, i2) and np.array_equal(q1, q2) and m1 == m2 and n1 == n2
