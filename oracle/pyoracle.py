@@ -230,6 +230,20 @@ class RefLib:
                                        C.POINTER(C.c_double), C.POINTER(C.c_double),
                                        C.POINTER(C.c_double), C.c_char_p, C.c_void_p, C.c_void_p]
         L.ref_run_quantize_s.argtypes = L.ref_run_quantize.argtypes + [C.c_char_p]
+        for nm in ("ref_lloyd_general", "ref_compute_sse", "ref_repair", "ref_center_table", "ref_next_masses",
+                   "ref_maximin_pad"):
+            getattr(L, nm).restype = C.c_int
+        L.ref_lloyd_general.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_int, C.c_double,
+                                        C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_int),
+                                        C.POINTER(C.c_uint64), C.POINTER(C.c_int), C.c_void_p, C.c_void_p]
+        L.ref_compute_sse.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_int, C.c_void_p,
+                                      C.POINTER(C.c_double)]
+        L.ref_repair.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_int, C.c_void_p,
+                                 C.POINTER(C.c_int)]
+        L.ref_center_table.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
+        L.ref_next_masses.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_int, C.c_void_p]
+        L.ref_maximin_pad.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_int, C.c_int,
+                                      C.c_void_p, C.POINTER(C.c_int)]
         L.ref_time_pipeline.argtypes = [_u8p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64,
                                         C.c_double, C.c_int, C.c_int, _f64p,
                                         C.POINTER(C.c_uint64), C.POINTER(C.c_int),
@@ -238,6 +252,80 @@ class RefLib:
     def _check(self, rc):
         if rc != 0:
             raise ValueError(self.L.ref_last_error().decode())
+
+    # --- the general API (real points, arbitrary weights) ---------------------
+    def lloyd_general(self, points, weights, init, eps=1e-3, max_it=100, fixed_it=0, history=False):
+        """wsm(points, weights, init) or, with weights None, kmeans_full(points, init)."""
+        pts = np.ascontiguousarray(points, np.float64).reshape(-1, 3)
+        init = np.ascontiguousarray(init, np.float64).reshape(-1, 3)
+        n, K = pts.shape[0], init.shape[0]
+        limit = fixed_it if fixed_it > 0 else max_it
+        centers = np.empty((K, 3), np.float64)
+        labels = np.empty(n, np.uint32)
+        sse = np.zeros(limit, np.float64)
+        it, ndc, rep = C.c_int(0), C.c_uint64(0), C.c_int(0)
+        hl = np.empty((limit, n), np.uint32) if history else None
+        hc = np.empty((limit, K, 3), np.float64) if history else None
+        w = None if weights is None else np.ascontiguousarray(weights, np.float64)
+        self._check(self.L.ref_lloyd_general(pts.ctypes.data_as(C.c_void_p), _nullable(w), n,
+                                             init.ctypes.data_as(C.c_void_p), K, eps, max_it, fixed_it,
+                                             centers.ctypes.data_as(C.c_void_p), labels.ctypes.data_as(C.c_void_p),
+                                             sse.ctypes.data_as(C.c_void_p), C.byref(it), C.byref(ndc),
+                                             C.byref(rep), _nullable(hl), _nullable(hc)))
+        iters = it.value
+        return LloydResult(centers, labels, sse[:iters].copy(), iters, ndc.value, rep.value,
+                           None if hl is None else hl[:iters].copy(), None if hc is None else hc[:iters].copy())
+
+    def compute_sse(self, points, weights, centers, labels):
+        pts = np.ascontiguousarray(points, np.float64)
+        c = np.ascontiguousarray(centers, np.float64)
+        m = np.ascontiguousarray(labels, np.uint32)
+        w = None if weights is None else np.ascontiguousarray(weights, np.float64)
+        out = C.c_double(0)
+        self._check(self.L.ref_compute_sse(pts.ctypes.data_as(C.c_void_p), _nullable(w), m.size,
+                                           c.ctypes.data_as(C.c_void_p), c.size // 3, m.ctypes.data_as(C.c_void_p),
+                                           C.byref(out)))
+        return out.value
+
+    def repair(self, points, weights, centers, labels):
+        pts = np.ascontiguousarray(points, np.float64)
+        c = np.array(centers, np.float64, copy=True, order="C")
+        m = np.array(labels, np.uint32, copy=True, order="C")
+        w = np.ascontiguousarray(weights, np.float64)
+        r = C.c_int(0)
+        self._check(self.L.ref_repair(pts.ctypes.data_as(C.c_void_p), w.ctypes.data_as(C.c_void_p), m.size,
+                                      c.ctypes.data_as(C.c_void_p), c.size // 3, m.ctypes.data_as(C.c_void_p),
+                                      C.byref(r)))
+        return r.value, c, m
+
+    def center_table(self, centers):
+        c = np.ascontiguousarray(centers, np.float64)
+        K = c.size // 3
+        d = np.empty((K, K), np.float64)
+        o = np.empty((K, K), np.uint32)
+        self._check(self.L.ref_center_table(c.ctypes.data_as(C.c_void_p), K, d.ctypes.data_as(C.c_void_p),
+                                            o.ctypes.data_as(C.c_void_p)))
+        return d, o
+
+    def next_masses(self, colors, weights, centers):
+        cols = np.ascontiguousarray(colors, np.float64)
+        w = np.ascontiguousarray(weights, np.float64)
+        c = np.ascontiguousarray(centers, np.float64).reshape(-1, 3)
+        out = np.empty(w.size, np.float64)
+        self._check(self.L.ref_next_masses(cols.ctypes.data_as(C.c_void_p), w.ctypes.data_as(C.c_void_p), w.size,
+                                           c.ctypes.data_as(C.c_void_p), c.shape[0], out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def maximin_pad(self, colors, weights, centers, k):
+        cols = np.ascontiguousarray(colors, np.float64)
+        w = np.ascontiguousarray(weights, np.float64)
+        c = np.ascontiguousarray(centers, np.float64).reshape(-1, 3)
+        out = np.empty((max(k, c.shape[0], 1), 3), np.float64)
+        ko = C.c_int(0)
+        self._check(self.L.ref_maximin_pad(cols.ctypes.data_as(C.c_void_p), w.ctypes.data_as(C.c_void_p), w.size,
+                                           c.ctypes.data_as(C.c_void_p), c.shape[0], k,
+                                           out.ctypes.data_as(C.c_void_p), C.byref(ko)))
+        return out[:ko.value].copy()
 
     def coarse_histogram(self, rgb=None, colors=None, counts=None):
         """quant::build_coarse_histogram from pixels (rgb) or from a weighted

@@ -312,3 +312,127 @@ int ref_time_pipeline(const std::uint8_t *rgb, int w, int h, int init_kind, int 
 }
 
 } // extern "C"
+
+// ---- the general API: real points, arbitrary weights (kmeans.hpp / init.hpp)
+namespace {
+std::vector<ColorPoint> pts_of(const double *p, std::uint64_t n) {
+    std::vector<ColorPoint> v;
+    v.reserve(n);
+    for (std::uint64_t i = 0; i < n; ++i) v.emplace_back(p[3 * i], p[3 * i + 1], p[3 * i + 2]);
+    return v;
+}
+void put_pts(const std::vector<ColorPoint> &v, double *out) {
+    for (std::size_t i = 0; i < v.size(); ++i) {
+        out[3 * i] = v[i].r;
+        out[3 * i + 1] = v[i].g;
+        out[3 * i + 2] = v[i].b;
+    }
+}
+WeightedHistogram hist_of(const double *colors, const double *weights, std::uint64_t n) {
+    WeightedHistogram h;
+    h.colors = pts_of(colors, n);
+    h.weights.assign(weights, weights + n);
+    h.counts.assign(n, 1);
+    h.source_pixel_count = n;
+    return h;
+}
+} // namespace
+
+extern "C" {
+// wsm(points, weights, ...) or, with weights == NULL, kmeans_full(points, ...)
+int ref_lloyd_general(const double *points, const double *weights, std::uint64_t n, const double *init, int k,
+                      double eps, int max_it, int fixed_it, double *centers_out, std::uint32_t *labels_out,
+                      double *sse_trace, int *iters, std::uint64_t *ndc, int *repairs, std::uint32_t *hist_labels,
+                      double *hist_centers) {
+    try {
+        const std::vector<ColorPoint> pts = pts_of(points, n);
+        std::vector<ColorPoint> c0 = pts_of(init, static_cast<std::uint64_t>(k));
+        ClusterOptions opt;
+        opt.term.epsilon = eps;
+        opt.term.max_iterations = max_it;
+        if (fixed_it > 0) opt.term.fixed_iterations = fixed_it;
+        opt.record_history = hist_labels != nullptr || hist_centers != nullptr;
+        ClusterState st = weights ? wsm(pts, std::span<const double>(weights, n), std::move(c0), opt)
+                                  : kmeans_full(pts, std::move(c0), opt);
+        put_pts(st.centers, centers_out);
+        std::memcpy(labels_out, st.memberships.data(), n * 4);
+        for (std::size_t i = 0; i < st.sse_trace.size(); ++i) sse_trace[i] = st.sse_trace[i];
+        *iters = st.iterations;
+        *ndc = st.ndc_total;
+        *repairs = st.repair_count;
+        for (std::size_t it = 0; it < st.history.size(); ++it) {
+            if (hist_labels) std::memcpy(hist_labels + it * n, st.history[it].memberships.data(), n * 4);
+            if (hist_centers) put_pts(st.history[it].centers, hist_centers + it * 3 * k);
+        }
+        return 0;
+    } catch (const std::exception &e) {
+        return fail(e);
+    }
+}
+
+int ref_compute_sse(const double *points, const double *weights, std::uint64_t n, const double *centers, int k,
+                    const std::uint32_t *labels, double *out) {
+    try {
+        const std::vector<ColorPoint> pts = pts_of(points, n), c = pts_of(centers, static_cast<std::uint64_t>(k));
+        std::span<const std::uint32_t> m(labels, n);
+        *out = weights ? compute_sse(pts, std::span<const double>(weights, n), c, m) : compute_sse(pts, c, m);
+        return 0;
+    } catch (const std::exception &e) {
+        return fail(e);
+    }
+}
+
+int ref_repair(const double *points, const double *weights, std::uint64_t n, double *centers, int k,
+               std::uint32_t *labels, int *repairs) {
+    try {
+        const std::vector<ColorPoint> pts = pts_of(points, n);
+        std::vector<ColorPoint> c = pts_of(centers, static_cast<std::uint64_t>(k));
+        std::vector<std::uint32_t> m(labels, labels + n);
+        *repairs = repair_empty_clusters(pts, std::span<const double>(weights, n), c, m);
+        put_pts(c, centers);
+        std::memcpy(labels, m.data(), n * 4);
+        return 0;
+    } catch (const std::exception &e) {
+        return fail(e);
+    }
+}
+
+int ref_center_table(const double *centers, int k, double *dist, std::uint32_t *order) {
+    try {
+        const std::vector<ColorPoint> c = pts_of(centers, static_cast<std::uint64_t>(k));
+        const CenterDistanceTable t = build_center_distance_table(c);
+        std::memcpy(dist, t.dist2.data(), t.dist2.size() * 8);
+        std::memcpy(order, t.order.data(), t.order.size() * 4);
+        return 0;
+    } catch (const std::exception &e) {
+        return fail(e);
+    }
+}
+
+int ref_next_masses(const double *colors, const double *weights, std::uint64_t n, const double *centers, int k,
+                    double *masses) {
+    try {
+        const WeightedHistogram h = hist_of(colors, weights, n);
+        const std::vector<ColorPoint> c = pts_of(centers, static_cast<std::uint64_t>(k));
+        const std::vector<double> m = kmeanspp_next_masses(h, c);
+        std::memcpy(masses, m.data(), m.size() * 8);
+        return 0;
+    } catch (const std::exception &e) {
+        return fail(e);
+    }
+}
+
+int ref_maximin_pad(const double *colors, const double *weights, std::uint64_t n, const double *centers, int k0,
+                    int k, double *out, int *k_out) {
+    try {
+        const WeightedHistogram h = hist_of(colors, weights, n);
+        std::vector<ColorPoint> c = pts_of(centers, static_cast<std::uint64_t>(k0));
+        const std::vector<ColorPoint> r = maximin_pad(h, std::move(c), k);
+        put_pts(r, out);
+        *k_out = static_cast<int>(r.size());
+        return 0;
+    } catch (const std::exception &e) {
+        return fail(e);
+    }
+}
+} // extern "C"

@@ -80,16 +80,24 @@ CPP_TEST_SRC = os.path.join(ROOT, "tests", "cpp", "test_dropin.cpp")
 CPP_TEST_BIN = os.path.join(ROOT, "tests", "cpp", "test_dropin")
 
 
+HOST_SOURCES = ["context.cpp", "colour_rng.cpp", "image_io.cpp", "histogram_api.cpp", "cluster.cpp", "seeding.cpp",
+                "report.cpp", "sweep.cpp"]
+
+
 def build_host(force: bool = False) -> str:
-    """libquant_b200.so: the reference's quant:: C++ API over libcqg.so, plus
-    the C++ drop-in test binary."""
+    """libquant_b200.so: the reference's quant:: C++ API (include/quant/*.hpp)
+    over libcqg.so, plus the C++ drop-in test binary."""
     cxx = shutil.which("g++") or "g++"
     inc = ["-I" + os.path.join(ROOT, "include")]
-    src = os.path.join(PKG, "host", "quant_b200.cpp")
-    hdrs = [os.path.join(ROOT, "include", "quant", "quant.hpp"), os.path.join(ROOT, "include", "cqg.h")]
-    if force or _newer([src, LIB, *hdrs], HOST_LIB):
-        cmd = [cxx, "-std=c++20", "-O2", "-fPIC", "-shared", *inc, src, "-o", HOST_LIB, "-L" + PKG, "-l:libcqg.so",
-               "-Wl,-rpath,$ORIGIN"]
+    host = os.path.join(PKG, "host")
+    srcs = [os.path.join(host, f) for f in HOST_SOURCES]
+    qdir = os.path.join(ROOT, "include", "quant")
+    hdrs = [os.path.join(qdir, h) for h in os.listdir(qdir)] + [os.path.join(ROOT, "include", "cqg.h"),
+                                                                 os.path.join(host, "context.hpp")]
+    if force or _newer([*srcs, LIB, *hdrs], HOST_LIB):
+        # -ffp-contract=off: no FMA contraction, like the reference's Release build
+        cmd = [cxx, "-std=c++20", "-O2", "-ffp-contract=off", "-fPIC", "-shared", *inc, *srcs, "-o", HOST_LIB,
+               "-L" + PKG, "-l:libcqg.so", "-Wl,-rpath,$ORIGIN"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError("host library build failed:\n" + r.stdout + r.stderr)

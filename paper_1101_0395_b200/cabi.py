@@ -37,6 +37,8 @@ EXPORTS = (
     "cqg_read_profile", "cqg_bench_sweep",
     "cqg_shard_begin", "cqg_shard_assign", "cqg_shard_moments", "cqg_shard_finalize", "cqg_shard_sizes",
     "cqg_shard_donor", "cqg_shard_move", "cqg_shard_end",
+    "cqg_lloyd_exact", "cqg_compute_sse", "cqg_repair_empty_clusters", "cqg_center_table",
+    "cqg_kmeanspp_next_masses", "cqg_maximin_pad",
 )
 
 PROF_SWEEP, PROF_MAPSWEEP, PROF_HIST, PROF_PIXEL, PROF_INIT, PROF_REPLAY, PROF_NDC, PROF_LLOYD, PROF_MAPNDC = range(9)
@@ -130,6 +132,16 @@ def load(path: str = LIB_PATH):
                                       C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]
         L.cqg_shard_move.argtypes = [vp, u64, i32, C.c_uint32]
         L.cqg_shard_end.argtypes = [vp, vp, vp, vp, C.POINTER(i32)]
+        L.cqg_lloyd_exact.argtypes = [vp, vp, vp, u64, vp, i32, C.POINTER(Term), vp, vp, vp,
+                                      C.POINTER(LloydStats), vp, vp]
+        L.cqg_compute_sse.argtypes = [vp, vp, vp, u64, vp, i32, vp, C.POINTER(C.c_double)]
+        L.cqg_repair_empty_clusters.argtypes = [vp, vp, vp, u64, vp, i32, vp, C.POINTER(i32)]
+        L.cqg_center_table.argtypes = [vp, vp, i32, vp, vp]
+        L.cqg_kmeanspp_next_masses.argtypes = [vp, vp, vp, u64, vp, i32, vp]
+        L.cqg_maximin_pad.argtypes = [vp, vp, u64, vp, i32, i32, vp]
+        for name in ("cqg_lloyd_exact", "cqg_compute_sse", "cqg_repair_empty_clusters", "cqg_center_table",
+                     "cqg_kmeanspp_next_masses", "cqg_maximin_pad"):
+            getattr(L, name).restype = i32
         for name in ("cqg_shard_begin", "cqg_shard_assign", "cqg_shard_moments", "cqg_shard_finalize",
                      "cqg_shard_sizes", "cqg_shard_donor", "cqg_shard_move", "cqg_shard_end"):
             getattr(L, name).restype = i32
@@ -248,6 +260,36 @@ class Context:
                                C.byref(term), ptr(centers), ptr(labels), ptr(sse), C.byref(st),
                                ptr(hist_labels), ptr(hist_centers)))
         return st
+
+    def lloyd_exact_raw(self, points, weights, n, init, k, term: Term, centers, labels, sse,
+                        hist_labels=None, hist_centers=None) -> LloydStats:
+        """cqg_lloyd_exact: wsm for arbitrary weights, kmeans_full when weights is None."""
+        st = LloydStats()
+        check(self.L.cqg_lloyd_exact(self.h, ptr(points), ptr(weights), n, ptr(init), k, C.byref(term),
+                                     ptr(centers), ptr(labels), ptr(sse), C.byref(st), ptr(hist_labels),
+                                     ptr(hist_centers)))
+        return st
+
+    def compute_sse_raw(self, points, weights, n, centers, k, labels) -> float:
+        out = C.c_double(0)
+        check(self.L.cqg_compute_sse(self.h, ptr(points), ptr(weights), n, ptr(centers), k, ptr(labels),
+                                     C.byref(out)))
+        return out.value
+
+    def repair_raw(self, points, weights, n, centers, k, labels) -> int:
+        r = C.c_int(0)
+        check(self.L.cqg_repair_empty_clusters(self.h, ptr(points), ptr(weights), n, ptr(centers), k,
+                                               ptr(labels), C.byref(r)))
+        return r.value
+
+    def center_table_raw(self, centers, k, dist, order):
+        check(self.L.cqg_center_table(self.h, ptr(centers), k, ptr(dist), ptr(order)))
+
+    def next_masses_raw(self, colors, weights, n, centers, k, masses):
+        check(self.L.cqg_kmeanspp_next_masses(self.h, ptr(colors), ptr(weights), n, ptr(centers), k, ptr(masses)))
+
+    def maximin_pad_raw(self, colors, n, centers, k0, k, out):
+        check(self.L.cqg_maximin_pad(self.h, ptr(colors), n, ptr(centers), k0, k, ptr(out)))
 
     def map_raw(self, rgb, P, palette, k, indices, index_bytes, quantized, with_ndc: bool = False):
         """cqg_map: the mean squared distance, or (mse, MappingResult::ndc) with with_ndc."""

@@ -236,6 +236,7 @@ struct LloydOut {
     float2 *bnd = nullptr;
     const float *shift = nullptr;
     const double *dsorted = nullptr;
+    const uint16_t *dcode = nullptr; // 16-bit codes of dsorted (K <= 256), or null
     const Moments *mom = nullptr;
     int Kpow = 0;
     // deferred completion (lloyd_dev(..., allow_defer)): the persistent kernel

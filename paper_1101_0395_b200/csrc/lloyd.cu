@@ -1088,6 +1088,7 @@ LloydOut lloyd_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *count
                 out.bnd = bnd;
                 out.shift = shift;
                 out.dsorted = dsorted;
+                out.dcode = dcode;
                 out.mom = mom;
                 out.Kpow = Kpow;
             }
@@ -1126,6 +1127,7 @@ LloydOut lloyd_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *count
         out.bnd = bnd;
         out.shift = shift;
         out.dsorted = dsorted;
+                out.dcode = dcode;
         out.mom = mom;
         out.Kpow = Kpow;
     }

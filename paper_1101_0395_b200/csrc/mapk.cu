@@ -207,14 +207,36 @@ __global__ void __launch_bounds__(NT) map_ndc_kernel(const uint32_t *__restrict_
                                                       const uint16_t *__restrict__ codes,
                                                       unsigned long long *ndc) {
     extern __shared__ __align__(16) double s_pal[];
-    const int rs = Kpow + 2; // code row stride (one padding word spreads rows over the banks)
+    const int rs = Kpow + 2; // code row stride: one padding word spreads rows over the banks
     uint16_t *s_code = reinterpret_cast<uint16_t *>(s_pal + 3 * K);
     for (int i = threadIdx.x; i < 3 * K; i += blockDim.x) s_pal[i] = pal[i];
-    if (CODES)
-        for (int e = threadIdx.x; e < K * Kpow; e += NT) {
-            const int r = e / Kpow, c = e - r * Kpow;
-            s_code[r * rs + c] = codes[e];
+    if (CODES) {
+        // 8 codes per 16-byte load, 8 loads in flight per thread; stored as
+        // 32-bit words into rows padded by one word (Kpow >= 8 here)
+        const uint4 *src = reinterpret_cast<const uint4 *>(codes);
+        uint32_t *dst = reinterpret_cast<uint32_t *>(s_code);
+        const int total = K * Kpow / 8, q4 = Kpow / 8, hw = Kpow / 2;
+        for (int e0 = threadIdx.x; e0 < total; e0 += 8 * NT) {
+            uint4 v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int e = e0 + u * NT;
+                v[u] = __ldg(src + (e < total ? e : 0));
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int e = e0 + u * NT;
+                if (e < total) {
+                    const int r = e / q4, w = (e - r * q4) * 4;
+                    uint32_t *d = dst + r * (hw + 1) + w;
+                    d[0] = v[u].x;
+                    d[1] = v[u].y;
+                    d[2] = v[u].z;
+                    d[3] = v[u].w;
+                }
+            }
         }
+    }
     __syncthreads();
     unsigned long long local = 0;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * Q;
@@ -335,25 +357,35 @@ double map_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P, const uint32_t *c
     if (ndc_async) { // MappingResult::ndc
         int Kpow = 1;
         while (Kpow < K) Kpow <<= 1;
-        const bool codes = K <= 256 && n >= (1ull << 21); // code rows pay off for many colours
-        double *rows = static_cast<double *>(ctx->map_rows.ensure(sizeof(double) * (size_t)K * Kpow +
-                                                                  (codes ? sizeof(uint16_t) * (size_t)K * Kpow : 0)));
-        uint16_t *crow = codes ? reinterpret_cast<uint16_t *>(rows + (size_t)K * Kpow) : nullptr;
         CQG_CUDA(cudaMemsetAsync(ndc_d, 0, 8, s));
-        const size_t wsm = sizeof(unsigned long long) * (size_t)Kpow;
-        if (wsm > 48 * 1024) CQG_CUDA(ensure_smem((const void *)map_walk_kernel, wsm));
-        map_walk_kernel<<<K, 256, wsm, s>>>(pal_d, K, Kpow, rows, crow);
-        launched(ctx);
+        const double *rows;
+        const uint16_t *crow;
+        if (lloyd && lloyd->dsorted && lloyd->Kpow == Kpow && (K > 256 || K < 8 || lloyd->dcode)) {
+            // the palette is Lloyd's final centres: its last iteration built their walk table
+            rows = lloyd->dsorted;
+            crow = K <= 256 && K >= 8 ? lloyd->dcode : nullptr;
+        } else {
+            const bool codes = K <= 256 && K >= 8;
+            double *r = static_cast<double *>(ctx->map_rows.ensure(sizeof(double) * (size_t)K * Kpow +
+                                                                 (codes ? sizeof(uint16_t) * (size_t)K * Kpow : 0)));
+            uint16_t *c = codes ? reinterpret_cast<uint16_t *>(r + (size_t)K * Kpow) : nullptr;
+            const size_t wsm = sizeof(unsigned long long) * (size_t)Kpow;
+            if (wsm > 48 * 1024) CQG_CUDA(ensure_smem((const void *)map_walk_kernel, wsm));
+            map_walk_kernel<<<K, 256, wsm, s>>>(pal_d, K, Kpow, r, c);
+            launched(ctx);
+            rows = r;
+            crow = c;
+        }
         const int pn = prof_begin(ctx);
-        if (codes) {
-            // many colours: the rows as 16-bit codes in every block's shared memory
+        if (crow) {
+            // the rows as 16-bit codes in every block's shared memory (K <= 256)
             const size_t sm = (size_t)K * 24 + (size_t)K * (Kpow + 2) * 2;
             CQG_CUDA(ensure_smem((const void *)map_ndc_kernel<true, 4, 512>, sm));
             const uint64_t g = (n + 2048 - 1) / 2048, gmax = (uint64_t)ctx->num_sms;
             map_ndc_kernel<true, 4, 512><<<(unsigned)(g < gmax ? g : gmax), 512, sm, s>>>(
                 colors_d, n, a.lut8, a.lut32, pal_d, K, Kpow, rows, crow, ndc_d);
         } else {
-            // few colours (a small preload would dominate): FP64 rows through L1/L2
+            // FP64 rows through L1/L2
             const size_t sm = (size_t)K * 24;
             if (sm > 48 * 1024) CQG_CUDA(ensure_smem((const void *)map_ndc_kernel<false, 4, 256>, sm));
             uint64_t g = (n + 1024 - 1) / 1024;

@@ -323,11 +323,12 @@ def wsm_counts(colors_packed, counts, P: int, init, options: ClusterOptions = No
 
 def wsm(points, weights, init, options: ClusterOptions = None,
         ctx: Optional[cabi.Context] = None) -> ClusterState:
-    """quant::wsm(points, weights, init, options) for count-weighted substrates.
+    """quant::wsm(points, weights, init, options) (kmeans.hpp:128-129).
 
-    The device engine keeps exact integer moments, so the weights must be
-    count / P for integer counts and the points must lie on the 8-bit grid
-    (every substrate run_quantize builds). Other inputs raise ValueError."""
+    Count-weighted substrates on the 8-bit grid (w_i == c_i * (1/P), what
+    run_quantize builds) run on the hot-path engine (exact integer moments);
+    any other points or positive weights run on the general exact-FP64 device
+    engine (cqg_lloyd_exact), which reproduces the reference's sequential sums."""
     pts = np.asarray(points, np.float64).reshape(-1, 3)
     w = np.asarray(weights, np.float64).reshape(-1)
     init = np.asarray(init, np.float64).reshape(-1, 3)
@@ -343,7 +344,7 @@ def wsm(points, weights, init, options: ClusterOptions = None,
     if not np.all(w > 0.0):
         raise ValueError("wsm: weights must be positive")
     if np.any(pts != np.round(pts)) or pts.min() < 0 or pts.max() > 255:
-        raise ValueError("wsm: device engine needs points on the 8-bit colour grid")
+        return _lloyd_exact(pts, w, init, options, ctx)
     # recover integer counts: w_i = c_i * (1/P) exactly (histogram.cpp:99-102)
     wmin = float(w.min())
     counts, P = None, None
@@ -356,9 +357,100 @@ def wsm(points, weights, init, options: ClusterOptions = None,
             counts, P = c, cand_p
             break
     if P is None:
-        raise ValueError("wsm: device engine needs weights of the form count/P")
+        return _lloyd_exact(pts, w, init, options, ctx)
     packed = pack_colors(pts.astype(np.uint8))
     return wsm_counts(packed, np.asarray(counts, np.uint32), P, init, options, ctx)
+
+
+def _lloyd_exact(pts, w, init, options, ctx):
+    """The general exact-FP64 engine (cqg_lloyd_exact): wsm when w is given,
+    kmeans_full when w is None."""
+    options = options or ClusterOptions()
+    term = _term_struct(options.term, options.record_history)
+    ctx = ctx or cabi.default_context()
+    pts = np.ascontiguousarray(pts, np.float64).reshape(-1, 3)
+    init = np.ascontiguousarray(np.asarray(init, np.float64).reshape(-1, 3))
+    n, k = pts.shape[0], init.shape[0]
+    limit = term.fixed_iterations if term.fixed_iterations > 0 else max(term.max_iterations, 1)
+    centers = np.empty((max(k, 1), 3), np.float64)
+    labels = np.empty(max(n, 1), np.uint32)
+    sse = np.zeros(limit, np.float64)
+    hl = np.empty((limit, max(n, 1)), np.uint32) if options.record_history else None
+    hc = np.empty((limit, max(k, 1), 3), np.float64) if options.record_history else None
+    wv = None if w is None else np.ascontiguousarray(w, np.float64)
+    st = ctx.lloyd_exact_raw(pts if n else np.zeros((1, 3)), wv, n, init if k else np.zeros((1, 3)), k, term,
+                             centers, labels, sse, hl, hc)
+    it = st.iterations
+    hist = [IterationSnapshot(hc[i].copy(), hl[i][:n].copy()) for i in range(it)] if options.record_history else []
+    return ClusterState(centers[:k].copy(), labels[:n].copy(), sse[:it].copy(), it, int(st.ndc_total),
+                        int(st.repair_count), hist, 0, int(st.swept_total))
+
+
+def kmeans_full(points, init, options: ClusterOptions = None,
+                ctx: Optional[cabi.Context] = None) -> ClusterState:
+    """quant::kmeans_full (kmeans.hpp:119, kmeans.cpp:263-268): plain k-means on
+    unweighted points -- full scan every iteration, arithmetic means, no
+    repair (an empty cluster keeps its centre); on the device."""
+    pts = np.asarray(points, np.float64).reshape(-1, 3)
+    return _lloyd_exact(pts, None, init, options, ctx)
+
+
+def compute_sse(points, *args, ctx: Optional[cabi.Context] = None) -> float:
+    """quant::compute_sse (kmeans.hpp:99-105): compute_sse(points, weights,
+    centers, memberships) or the unit-weight compute_sse(points, centers,
+    memberships); one sequential FP64 chain in point order, on the device."""
+    if len(args) == 3:
+        weights, centers, memberships = args
+    elif len(args) == 2:
+        weights, (centers, memberships) = None, args
+    else:
+        raise TypeError("compute_sse(points, [weights,] centers, memberships)")
+    ctx = ctx or cabi.default_context()
+    pts = np.ascontiguousarray(points, np.float64).reshape(-1, 3)
+    c = np.ascontiguousarray(centers, np.float64).reshape(-1, 3)
+    m = np.ascontiguousarray(memberships, np.uint32)
+    w = None if weights is None else np.ascontiguousarray(weights, np.float64)
+    return ctx.compute_sse_raw(pts, w, pts.shape[0], c, c.shape[0], m)
+
+
+def repair_empty_clusters(points, weights, centers: np.ndarray, memberships: np.ndarray,
+                          ctx: Optional[cabi.Context] = None) -> int:
+    """quant::repair_empty_clusters (kmeans.hpp:112-115, kmeans.cpp:124-169) on
+    the device; ``centers`` (k, 3) float64 and ``memberships`` uint32 are
+    updated in place. Returns the number of clusters repaired."""
+    ctx = ctx or cabi.default_context()
+    pts = np.ascontiguousarray(points, np.float64).reshape(-1, 3)
+    w = np.ascontiguousarray(weights, np.float64)
+    if not (centers.dtype == np.float64 and centers.flags["C_CONTIGUOUS"] and
+            memberships.dtype == np.uint32 and memberships.flags["C_CONTIGUOUS"]):
+        raise ValueError("repair_empty_clusters: centers float64 and memberships uint32, C-contiguous")
+    return ctx.repair_raw(pts, w, pts.shape[0], centers, centers.shape[0], memberships)
+
+
+@dataclass
+class CenterDistanceTable:
+    """quant::CenterDistanceTable (kmeans.hpp:62-69)."""
+    k: int
+    dist2: np.ndarray  # (k, k) float64
+    order: np.ndarray  # (k, k) uint32, order[i, 0] == i
+
+    def d2(self, i: int, j: int) -> float:
+        return float(self.dist2[i, j])
+
+    def order_at(self, i: int, n: int) -> int:
+        return int(self.order[i, n])
+
+
+def build_center_distance_table(centers, ctx: Optional[cabi.Context] = None) -> CenterDistanceTable:
+    """quant::build_center_distance_table (kmeans.hpp:73, kmeans.cpp:14-38) on the device."""
+    ctx = ctx or cabi.default_context()
+    c = np.ascontiguousarray(centers, np.float64).reshape(-1, 3)
+    k = c.shape[0]
+    dist = np.zeros((k, k), np.float64)
+    order = np.zeros((k, k), np.uint32)
+    if k:
+        ctx.center_table_raw(c, k, dist, order)
+    return CenterDistanceTable(k, dist, order)
 
 
 # ---------------------------------------------------------------------------
@@ -383,6 +475,30 @@ def init_kmeanspp(hist: WeightedHistogram, cfg: SeedConfig,
                   ctx: Optional[cabi.Context] = None) -> np.ndarray:
     """quant::init_kmeanspp (init.hpp:60, init.cpp:295-314)."""
     return _init(cabi.INIT_KMEANSPP, hist, cfg, ctx)
+
+
+def kmeanspp_next_masses(hist: WeightedHistogram, centers, ctx: Optional[cabi.Context] = None) -> np.ndarray:
+    """quant::kmeanspp_next_masses (init.hpp:65-66, init.cpp:316-323): weight x
+    min squared distance to the chosen centres (the weights when none), on the device."""
+    ctx = ctx or cabi.default_context()
+    c = np.ascontiguousarray(np.asarray(centers, np.float64).reshape(-1, 3))
+    cols = np.ascontiguousarray(hist.colors, np.float64)
+    w = np.ascontiguousarray(hist.weights, np.float64)
+    out = np.empty(max(hist.size(), 1), np.float64)
+    ctx.next_masses_raw(cols, w, hist.size(), c if c.shape[0] else None, c.shape[0], out)
+    return out[:hist.size()].copy()
+
+
+def maximin_pad(hist: WeightedHistogram, centers, k: int, ctx: Optional[cabi.Context] = None) -> np.ndarray:
+    """quant::maximin_pad (init.hpp:71-72, init.cpp:325-335): extend a short
+    centre set to k by maximin picks over the histogram, on the device."""
+    ctx = ctx or cabi.default_context()
+    c = np.ascontiguousarray(np.asarray(centers, np.float64).reshape(-1, 3))
+    k0 = c.shape[0]
+    out = np.empty((max(k, k0, 1), 3), np.float64)
+    ctx.maximin_pad_raw(np.ascontiguousarray(hist.colors, np.float64), hist.size(), c if k0 else None, k0, int(k),
+                        out)
+    return out[:max(k, k0)].copy()
 
 
 def _init(kind, hist, cfg, ctx):
@@ -542,16 +658,14 @@ def all_method_tokens() -> list[str]:
 
 @dataclass
 class QuantizeConfig:
-    """quant::QuantizeConfig (pipeline.hpp:33-40). ``init_centers`` is this
-    build's hook for initialisers that are outside the device path (e.g. a
-    preclusterer palette for wsm-wu): when given, it seeds the device engine."""
+    """quant::QuantizeConfig (pipeline.hpp:33-40), the reference's fields.
+    ``index_bytes`` (1 or 4) is this build's option for the mapping indices."""
     method: MethodSpec = field(default_factory=lambda: parse_method("wsm-mmx"))
     k: int = 8
     sampling: str = "unique"
     seed: int = 1
     term: Termination = field(default_factory=Termination)
     record_history: bool = False
-    init_centers: Optional[np.ndarray] = None
     index_bytes: int = 4
 
 
@@ -566,11 +680,14 @@ class QuantizeResult:
     stage_ms: dict = field(default_factory=dict)
 
 
-def run_quantize(image, config: QuantizeConfig, ctx: Optional[cabi.Context] = None) -> QuantizeResult:
+def run_quantize(image, config: QuantizeConfig, ctx: Optional[cabi.Context] = None,
+                 init_centers=None) -> QuantizeResult:
     """quant::run_quantize (pipeline.hpp:53, pipeline.cpp:81-164) for the
     device path: every sampling mode (none | 2to1 | unique | both), refined
-    methods wsm-mmx / wsm-kpp, or any wsm-<x> whose initial centres are supplied
-    in ``config.init_centers``."""
+    methods wsm-mmx / wsm-kpp, or any wsm-<x> whose k initial centres are
+    supplied as ``init_centers`` (the C++ overload run_quantize(image, config,
+    init_centers)). ``config.record_history`` is forwarded to the engine
+    (pipeline.cpp:126-130): the stages then run as separate device calls."""
     ctx = ctx or cabi.default_context()
     arr, w, h = _pixels(image)
     P = w * h
@@ -582,17 +699,19 @@ def run_quantize(image, config: QuantizeConfig, ctx: Optional[cabi.Context] = No
     if not config.method.refine:
         raise ValueError("run_quantize: standalone preclusterers are outside the device path")
     k = int(config.k)
-    if config.init_centers is not None:
+    if init_centers is not None:
         kind = cabi.INIT_GIVEN
-        init = np.ascontiguousarray(np.asarray(config.init_centers, np.float64).reshape(-1, 3))
+        init = np.ascontiguousarray(np.asarray(init_centers, np.float64).reshape(-1, 3))
         if init.shape[0] != k:
-            raise ValueError("run_quantize: init_centers must have k rows")
+            raise ValueError("run_quantize: init_centers must hold k centres")
     elif config.method.base in DEVICE_INITS:
         kind = DEVICE_INITS[config.method.base]
         init = None
     else:
         raise ValueError(f"run_quantize: initializer '{config.method.base}' is outside the device "
-                         "path; pass config.init_centers")
+                         "path; supply init_centers")
+    if config.record_history:
+        return _run_quantize_history(arr, w, h, config, kind, init, ctx)
     term = _term_struct(config.term, False)
     cfg = cabi.QuantizeCfg(kind, k, int(config.seed), term, int(config.index_bytes), sampling, w, h)
     limit = term.fixed_iterations if term.fixed_iterations > 0 else term.max_iterations
@@ -620,3 +739,36 @@ def run_quantize(image, config: QuantizeConfig, ctx: Optional[cabi.Context] = No
     return QuantizeResult(palette, mapping, state, rep, n,
                           dict(histogram=st.ms_histogram, init=st.ms_init, lloyd=st.ms_lloyd,
                                map=st.ms_map))
+
+
+def _run_quantize_history(arr, w, h, config: QuantizeConfig, kind, init, ctx) -> QuantizeResult:
+    """run_quantize with record_history: histogram -> initialiser -> wsm (with
+    per-iteration snapshots) -> mapping as separate device calls."""
+    if hasattr(arr, "data_ptr") and not isinstance(arr, np.ndarray):
+        arr = arr.cpu().numpy()
+    img = np.ascontiguousarray(arr, np.uint8).reshape(h, w, 3)
+    sub = config.sampling in ("2to1", "both")
+    dedup = config.sampling in ("unique", "both")
+    sampled = img[::2, ::2] if sub else img
+    t0 = time.perf_counter()
+    hist = build_histogram(sampled, config.seed, ctx=ctx)
+    if init is None:
+        sc = SeedConfig(k=int(config.k), seed=int(config.seed))
+        init = init_maximin(hist, sc, ctx=ctx) if kind == cabi.INIT_MAXIMIN else init_kmeanspp(hist, sc, ctx=ctx)
+    opt = ClusterOptions(term=config.term, record_history=True)
+    if dedup:
+        st = wsm_hist(hist, init, opt, ctx=ctx)
+        n = hist.size()
+    else:
+        px = pack_colors(sampled)
+        st = wsm_counts(px, np.ones(px.size, np.uint32), px.size, init, opt, ctx=ctx)
+        n = px.size
+    mapping = map_pixels(img, st.centers, index_bytes=config.index_bytes, ctx=ctx)
+    t1 = time.perf_counter()
+    k = int(config.k)
+    rep = QuantReport(method=config.method.token(), k_requested=k, k_actual=k, seed=int(config.seed),
+                      sampling=config.sampling, mse=mapping.mean_sq_dist, psnr=psnr_from_mse(mapping.mean_sq_dist),
+                      iterations=st.iterations, ndc_per_point_iter=st.ndc_per_point_iter(n), time_ms=(t1 - t0) * 1e3)
+    if st.repair_count > 0:
+        rep.flags.append(f"repairs:{st.repair_count}")
+    return QuantizeResult(st.centers.copy(), mapping, st, rep, n)

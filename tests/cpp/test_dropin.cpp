@@ -151,8 +151,8 @@ static void case_golden_rows(const std::string &dir) { // proj/tmp_acceptance/sw
                 cfg.method = parse_method(method);
                 cfg.k = 8;
                 cfg.seed = 3 + run;
-                if (std::string(method) == "wsm-wu") cfg.init_centers = wu[s];
-                QuantizeResult r = run_quantize(img, cfg);
+                QuantizeResult r = std::string(method) == "wsm-wu" ? run_quantize(img, cfg, wu[s])
+                                                                    : run_quantize(img, cfg);
                 r.report.image = "acc_" + std::to_string(seed_img) + ".ppm";
                 r.report.run = run;
                 r.report.time_ms = 0.0;

@@ -388,9 +388,8 @@ def test_pipeline_golden_sweep_rows(ctx):
         for method in ("wsm-kpp", "wsm-wu"):
             for run in (0, 1):
                 cfg = quant.QuantizeConfig(method=quant.parse_method(method), k=8, seed=3 + run)
-                if method == "wsm-wu":
-                    cfg.init_centers = np.array(wu[str(img_seed)])
-                r = quant.run_quantize(img, cfg, ctx=ctx)
+                init = np.array(wu[str(img_seed)]) if method == "wsm-wu" else None
+                r = quant.run_quantize(img, cfg, ctx=ctx, init_centers=init)
                 rep = r.report
                 rep.image, rep.run, rep.time_ms = f"acc_{img_seed}.ppm", run, 0.0
                 got.append(rep.csv_row())

@@ -164,8 +164,8 @@ def test_quantize_repair_after_deferred_check(ctx, oracle, dup):
     rng = np.random.default_rng(dup)
     init = rng.integers(0, 256, (12, 3)).astype(np.float64)
     init[1:1 + dup] = init[0]  # clusters 1..dup tie with 0 and lose: empty
-    qc = quant.QuantizeConfig(method=quant.parse_method("wsm-kpp"), k=12, seed=1, init_centers=init)
-    r = quant.run_quantize(img, qc, ctx=ctx)
+    qc = quant.QuantizeConfig(method=quant.parse_method("wsm-kpp"), k=12, seed=1)
+    r = quant.run_quantize(img, qc, ctx=ctx, init_centers=init)
     c, n, _ = oracle.histogram(img)
     ora = oracle.wsm(c, n, P, init, mode=UPDATE_EXACT)
     assert ora.repairs >= 1
