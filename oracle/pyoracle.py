@@ -35,6 +35,10 @@ def build(quiet: bool = True) -> None:
         raise RuntimeError("oracle build failed:\n" + out.stdout + out.stderr)
     if not quiet:
         print(out.stdout)
+    # the reference's unit tests against the drop-in (needs libquant_b200.so)
+    if os.path.exists(os.path.join(os.path.dirname(HERE), "paper_1101_0395_b200", "libquant_b200.so")):
+        from oracle import refsuite
+        refsuite.build(quiet=quiet)
 
 
 def _nullable(arr):

@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <iostream>
@@ -291,8 +292,53 @@ static void case_ppm_roundtrip() { // image.hpp:41-42: "P6\n<w> <h>\n255\n" + ra
     std::remove(path.c_str());
 }
 
+// bench.hpp (bench.cpp:27-113): the sweep through the device run_quantize on
+// the golden 40x40 images saved as PPM; zero_time reruns byte-identical; a
+// method outside the device path ("wu") gives error rows and the sweep goes on.
+// argv[2] (optional) receives the CSV for the comparison with the reference
+// library's rows (tests/test_gpu_cpp.py).
+static void case_bench_sweep(const std::string &dir, const std::string &csv_out) {
+    const std::string tmp = "/tmp/cqg_bench_sweep";
+    std::string mk = "mkdir -p " + tmp;
+    CHECK(std::system(mk.c_str()) == 0);
+    BenchConfig bc;
+    for (int seed_img : {61, 62}) {
+        RawImage img;
+        img.width = img.height = 40;
+        img.pixels.resize(1600);
+        std::ifstream f(dir + "/acc_" + std::to_string(seed_img) + ".rgb", std::ios::binary);
+        f.read(reinterpret_cast<char *>(img.pixels.data()), 1600 * 3);
+        CHECK(f.gcount() == 1600 * 3);
+        const std::string path = tmp + "/acc_" + std::to_string(seed_img) + ".ppm";
+        save_ppm(img, path);
+        bc.image_paths.push_back(path);
+    }
+    bc.methods = {"wsm-kpp", "wsm-mmx", "wu"};
+    bc.ks = {4, 8};
+    bc.runs = 2;
+    bc.seed_base = 3;
+    bc.zero_time = true;
+    std::ostringstream log;
+    const BenchResults a = run_bench(bc, &log);
+    CHECK(a.rows.size() == 2u * 3u * 2u * 2u);
+    CHECK(a.error_count == 8); // "wu": a standalone preclusterer, outside the device path
+    const std::string c1 = tmp + "/a.csv", c2 = tmp + "/b.csv";
+    write_bench_csv(a, c1);
+    write_bench_csv(run_bench(bc, nullptr), c2);
+    auto slurp = [](const std::string &p) {
+        std::ifstream f(p, std::ios::binary);
+        return std::string(std::istreambuf_iterator<char>(f), {});
+    };
+    CHECK(slurp(c1) == slurp(c2));
+    CHECK(slurp(c1).rfind("image,method,k,run,seed,sampling,", 0) == 0);
+    const RankSummary rs = rank_aggregate(a);
+    CHECK(rs.methods == std::vector<std::string>({"wsm-kpp", "wsm-mmx"})); // error rows do not rank
+    if (!csv_out.empty()) write_bench_csv(a, csv_out);
+}
+
 int main(int argc, char **argv) {
     const std::string dir = argc > 1 ? argv[1] : "tests/golden";
+    const std::string csv_out = argc > 2 ? argv[2] : "";
     struct Case {
         const char *name;
         void (*fn)();
@@ -323,6 +369,16 @@ int main(int argc, char **argv) {
             ++g_fail;
         }
         std::printf("%s golden_rows\n", g_fail == before ? "PASS" : "FAIL");
+    }
+    {
+        const int before = g_fail;
+        try {
+            case_bench_sweep(dir, csv_out);
+        } catch (const std::exception &e) {
+            std::printf("  exception: %s\n", e.what());
+            ++g_fail;
+        }
+        std::printf("%s bench_sweep\n", g_fail == before ? "PASS" : "FAIL");
     }
     std::printf("%d failure(s)\n", g_fail);
     return g_fail == 0 ? 0 : 1;
