@@ -116,6 +116,7 @@ struct cqg_ctx {
     cqg::DevBuf bitmap;    // P bits: first-occurrence marks
     cqg::DevBuf wordpref;  // per-bitmap-block exclusive prefix
     cqg::DevBuf scal;      // small device scalars (counters)
+    cqg::DevBuf pcnt, pent, pseg; // large images: per-colour counts (2^24), bucketed pixel entries, bucket offsets
     // input / substrate staging
     cqg::DevBuf img;       // image bytes when the caller passes host memory
     cqg::DevBuf colors, counts, first;

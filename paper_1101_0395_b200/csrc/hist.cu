@@ -4,27 +4,20 @@
 // reference dedups through a seeded chained hash and appends colours on first
 // sight, so its output order is "by first pixel index". Here:
 //
-//   A  hist_count   per pixel (16 pixels / thread, 3 x 128-bit loads):
-//                   atomicAdd(count[c]) with return -> the lane that sees 0
-//                   appends c to an (unordered) list (warp-aggregated append);
-//                   atomicMax(~first[c], ~p) keeps the minimum index.
-//                   Small images: both in one pass over an interleaved
-//                   {count, ~first} table. Large images (P >= 2^22): two passes
-//                   of fire-and-forget reductions (hist_count_red, hist_first)
-//                   over split 64 MiB tables (each fits the 126 MB L2), then a
-//                   third pass marks the first occurrences straight from the
-//                   image (~first[c] == p) -- no unique-colour list, no global
-//                   append counter; N' is the bitmap's popcount from the scan.
-//   B  hist_mark    per listed colour: set bit first(c) in a P-bit bitmap.
-//   C  scan         popcount prefix over the bitmap words (2 small kernels).
-//   D  emit         small: per listed colour, rank = prefix(first(c)), write at
-//                   that rank and zero the table entry. Large: one thread per
-//                   pixel in pixel order -- a set bit is a first occurrence with
-//                   rank = word prefix + bits below, so stores are sequential;
-//                   the tables are reset with one 128 MiB memset.
-//
-// The tables (2^24 counts | 2^24 ~first) are 128 MiB and live in the context;
-// they are zero between calls. HBM bound: 6P bytes read + 8N' written + atomics.
+// Small images (P < 2^22): one pass over an interleaved {count, ~first} table
+//   of 2^24 entries (L2-resident): per pixel atomicAdd(count) with return (the
+//   lane that sees 0 appends the colour to a list, warp-aggregated) and
+//   atomicMax(~first); per listed colour one bit at its first pixel in a P-bit
+//   bitmap; popcount scan; per listed colour rank = prefix(first), write at
+//   that rank and zero the table entry.
+// Large images (P >= 2^22): the random L2 atomics per pixel (two per pixel,
+//   ~156 G/s on B200) are replaced by a colour-bucketed partition with the
+//   aggregation in shared memory (part_count -> part_scatter -> bucket_agg,
+//   below); bucket_agg writes the dense per-colour counts and marks each
+//   colour's first pixel in the bitmap; popcount scan; one pass over the
+//   pixels in pixel order emits every first occurrence at rank = word prefix
+//   + bits below (sequential stores), its count gathered from the table.
+// Only distinct colours touch L2 at random (bitmap mark, count gather).
 #include "cqg_internal.cuh"
 
 namespace cqg {
@@ -130,68 +123,6 @@ __global__ void hist_emit_fused(const uint32_t *__restrict__ list, const uint32_
     }
 }
 
-// ---- large images: split tables cnt | negf (64 MiB each), two passes
-
-// large images: counts by reductions (no return value, no list)
-__global__ void __launch_bounds__(kThreads) hist_count_red(const uint8_t *__restrict__ rgb, uint64_t P,
-                                                          uint32_t *__restrict__ cnt, int aligned) {
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const uint64_t groups = aligned ? P / 16 : 0;
-    for (uint64_t g = tid; g < groups; g += stride) {
-        const uint4 *src = reinterpret_cast<const uint4 *>(rgb + g * 48);
-        uint32_t col[16];
-        decode16(ld_stream(src), ld_stream(src + 1), ld_stream(src + 2), col);
-#pragma unroll
-        for (int j = 0; j < 16; ++j) atomicAdd(cnt + col[j], 1u);
-    }
-    for (uint64_t p = groups * 16 + tid; p < P; p += stride) {
-        const uint32_t c = ((uint32_t)rgb[3 * p] << 16) | ((uint32_t)rgb[3 * p + 1] << 8) | rgb[3 * p + 2];
-        atomicAdd(cnt + c, 1u);
-    }
-}
-
-// large images: first-occurrence bitmap from the ~first table instead of a
-// third image pass: every present colour sets the bit of its first pixel
-// (coalesced 16-byte reads of the 64 MiB table, one reduction per colour into
-// the L2-resident bitmap; a pass over the image re-read it and looked up the
-// table per pixel: 865 MB of DRAM reads on an 8192^2 image)
-__global__ void __launch_bounds__(kThreads) hist_mark_table(const uint32_t *__restrict__ negf,
-                                                           uint32_t *__restrict__ bitmap) {
-    const uint4 *t4 = reinterpret_cast<const uint4 *>(negf);
-    constexpr uint32_t n4 = (1u << 24) / 4;
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += gridDim.x * blockDim.x) {
-        const uint4 v = __ldcs(t4 + i);
-        const uint32_t f[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            if (f[j]) {
-                const uint32_t p = ~f[j];
-                atomicOr(&bitmap[p >> 5], 1u << (p & 31));
-            }
-        }
-    }
-}
-
-__global__ void __launch_bounds__(kThreads) hist_first(const uint8_t *__restrict__ rgb, uint64_t P,
-                                                      uint32_t *__restrict__ negf, int aligned) {
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const uint64_t groups = aligned ? P / 16 : 0;
-    for (uint64_t g = tid; g < groups; g += stride) {
-        const uint4 *src = reinterpret_cast<const uint4 *>(rgb + g * 48);
-        uint32_t col[16];
-        decode16(ld_stream(src), ld_stream(src + 1), ld_stream(src + 2), col);
-#pragma unroll
-        for (int j = 0; j < 16; ++j) atomicMax(negf + col[j], ~(uint32_t)(g * 16 + j));
-    }
-    for (uint64_t p = groups * 16 + tid; p < P; p += stride) {
-        const uint32_t c = ((uint32_t)rgb[3 * p] << 16) | ((uint32_t)rgb[3 * p + 1] << 8) | rgb[3 * p + 2];
-        atomicMax(negf + c, ~(uint32_t)p);
-    }
-}
-
-
 // one thread per pixel, in pixel order: a set bit is a first occurrence whose
 // rank is the word prefix plus the set bits below it, so the stores of a warp
 // land on consecutive ranks (the colour comes from the image itself)
@@ -208,10 +139,278 @@ __global__ void __launch_bounds__(kThreads) hist_emit(const uint8_t *__restrict_
         const uint32_t b = (uint32_t)(p & 31);
         if (!((bits >> b) & 1u)) continue;
         const uint32_t rank = __ldg(wpref + w) + __popc(bits & ((1u << b) - 1u));
-        const uint32_t c = ((uint32_t)rgb[3 * p] << 16) | ((uint32_t)rgb[3 * p + 1] << 8) | rgb[3 * p + 2];
+        // image bytes streamed (evict-first), so the per-colour counts stay in L2
+        const uint32_t c = ((uint32_t)__ldcs(rgb + 3 * p) << 16) | ((uint32_t)__ldcs(rgb + 3 * p + 1) << 8) |
+                           __ldcs(rgb + 3 * p + 2);
         colors[rank] = c;
         counts[rank] = __ldg(cnt + c);
         if (first) first[rank] = (uint32_t)p;
+    }
+}
+
+
+// ---- large images: colour-bucketed partition, aggregation in shared memory
+//
+// Colour c splits into bucket c >> 14 (1024 buckets) and slot c & 0x3FFF
+// (16384 colours, whose count and minimum pixel index fit one block's shared
+// memory). The image is cut into G chunks of at most 2^18 pixels, so a pixel
+// travels as one u32 entry (chunk offset << 14 | slot):
+//   part_count    per chunk: pixels per bucket (shared-memory counters)
+//   seg_scan      per bucket: chunk segment offsets; bucket sizes
+//   bucket_scan   bucket starts; buckets ordered by size (largest first)
+//   part_scatter  per chunk, 8192-pixel tiles: counting sort by bucket in
+//                 shared memory, then runs of consecutive entries per bucket
+//   bucket_agg    one block per bucket: count (add) and first pixel (min) per
+//                 colour with shared-memory atomics; dense per-colour counts
+//                 out, and the first pixel of every present colour marked in
+//                 the P-bit first-occurrence bitmap
+// then the scan and the pixel-order emit as before. Every pixel costs shared-
+// memory atomics and streamed bytes; only distinct colours touch L2 randomly.
+constexpr int kBucketBits = 10;
+constexpr int kSlotBits = 14;
+constexpr int kBuckets = 1 << kBucketBits;
+constexpr int kSlots = 1 << kSlotBits;
+constexpr int kChunkBits = 18; // offset within a chunk: 18 bits + slot: 14 bits
+constexpr int kPartThreads = 1024;
+constexpr int kTilePix = kPartThreads * 16; // 16384 pixels per scatter tile: runs of ~16 entries per bucket
+constexpr int kAggThreads = 1024;
+
+__device__ __forceinline__ void decode_group(const uint8_t *rgb, uint64_t p0, int n, bool vec, uint32_t *col) {
+    if (vec && n == 16) {
+        const uint4 *src = reinterpret_cast<const uint4 *>(rgb + p0 * 3);
+        decode16(ld_stream(src), ld_stream(src + 1), ld_stream(src + 2), col);
+    } else {
+        for (int j = 0; j < 16; ++j) {
+            const uint64_t p = p0 + j;
+            col[j] = j < n ? ((uint32_t)rgb[3 * p] << 16) | ((uint32_t)rgb[3 * p + 1] << 8) | rgb[3 * p + 2] : 0u;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kPartThreads) part_count(const uint8_t *__restrict__ rgb, uint64_t P, uint64_t chunk,
+                                                           int vec, uint32_t *__restrict__ gcnt, int G) {
+    __shared__ uint32_t s_cnt[kBuckets];
+    for (int b = threadIdx.x; b < kBuckets; b += kPartThreads) s_cnt[b] = 0;
+    __syncthreads();
+    const uint64_t base = (uint64_t)blockIdx.x * chunk;
+    const uint64_t end = base + chunk < P ? base + chunk : P;
+    for (uint64_t p0 = base + 16ull * threadIdx.x; p0 < end; p0 += 16ull * kPartThreads) {
+        const int n = end - p0 < 16 ? (int)(end - p0) : 16;
+        uint32_t col[16];
+        decode_group(rgb, p0, n, vec, col);
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            if (j < n) atomicAdd(&s_cnt[col[j] >> kSlotBits], 1u);
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < kBuckets; b += kPartThreads) gcnt[(size_t)b * G + blockIdx.x] = s_cnt[b];
+}
+
+// per bucket: exclusive scan of its G chunk counts (in place) and the bucket size
+__global__ void __launch_bounds__(256) seg_scan(uint32_t *__restrict__ gcnt, int G, uint32_t *__restrict__ bsize) {
+    __shared__ uint32_t s_w[8];
+    __shared__ uint32_t s_carry;
+    uint32_t *row = gcnt + (size_t)blockIdx.x * G;
+    if (threadIdx.x == 0) s_carry = 0;
+    __syncthreads();
+    for (int base = 0; base < G; base += 256) {
+        const int i = base + threadIdx.x;
+        const uint32_t v = i < G ? row[i] : 0u;
+        uint32_t x = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, x, o);
+            if ((threadIdx.x & 31) >= (unsigned)o) x += t;
+        }
+        if ((threadIdx.x & 31) == 31) s_w[threadIdx.x >> 5] = x;
+        __syncthreads();
+        uint32_t woff = 0;
+        for (int w = 0; w < (int)(threadIdx.x >> 5); ++w) woff += s_w[w];
+        const uint32_t carry = s_carry;
+        if (i < G) row[i] = carry + woff + x - v;
+        __syncthreads();
+        if (threadIdx.x == 255) s_carry = carry + woff + x;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) bsize[blockIdx.x] = s_carry;
+}
+
+// bucket starts (exclusive scan of the sizes) and the aggregation order:
+// buckets by decreasing size, so the largest start first (one block)
+__global__ void __launch_bounds__(kBuckets) bucket_scan(const uint32_t *__restrict__ bsize,
+                                                        uint32_t *__restrict__ bstart, uint32_t *__restrict__ border) {
+    __shared__ uint32_t s_x[kBuckets];
+    __shared__ unsigned long long s_k[kBuckets];
+    const int t = threadIdx.x;
+    const uint32_t v = bsize[t];
+    s_x[t] = v;
+    s_k[t] = ((unsigned long long)(~v) << 32) | (uint32_t)t; // ascending key = descending size
+    __syncthreads();
+    for (int o = 1; o < kBuckets; o <<= 1) {
+        const uint32_t add = t >= o ? s_x[t - o] : 0u;
+        __syncthreads();
+        s_x[t] += add;
+        __syncthreads();
+    }
+    bstart[t] = s_x[t] - v;
+    for (int size = 2; size <= kBuckets; size <<= 1)
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            const int o = t ^ stride;
+            if (o > t) {
+                const bool up = (t & size) == 0;
+                const unsigned long long a = s_k[t], b = s_k[o];
+                if ((a > b) == up) {
+                    s_k[t] = b;
+                    s_k[o] = a;
+                }
+            }
+            __syncthreads();
+        }
+    border[t] = (uint32_t)(s_k[t] & 0xFFFFFFFFu);
+}
+
+constexpr size_t kScatterSmem = sizeof(uint32_t) * (3 * kBuckets + kPartThreads / 32 + kTilePix) +
+                                sizeof(uint16_t) * kTilePix;
+__global__ void __launch_bounds__(kPartThreads) part_scatter(const uint8_t *__restrict__ rgb, uint64_t P,
+                                                             uint64_t chunk, int vec,
+                                                             const uint32_t *__restrict__ gcnt, int G,
+                                                             const uint32_t *__restrict__ bstart,
+                                                             uint32_t *__restrict__ ent) {
+    extern __shared__ uint32_t s_part[];
+    uint32_t *s_cur = s_part;             // next global slot of this chunk's segment per bucket
+    uint32_t *s_tc = s_cur + kBuckets;    // tile: entries per bucket
+    uint32_t *s_ts = s_tc + kBuckets;     // tile: exclusive start per bucket
+    uint32_t *s_w = s_ts + kBuckets;      // scan: warp totals
+    uint32_t *s_e = s_w + kPartThreads / 32; // tile entries sorted by bucket
+    uint16_t *s_b = reinterpret_cast<uint16_t *>(s_e + kTilePix); // their buckets
+    for (int b = threadIdx.x; b < kBuckets; b += kPartThreads)
+        s_cur[b] = bstart[b] + gcnt[(size_t)b * G + blockIdx.x];
+    const uint64_t base = (uint64_t)blockIdx.x * chunk;
+    const uint64_t end = base + chunk < P ? base + chunk : P;
+    // the next tile's 48 bytes per thread are loaded while this tile is sorted
+    uint4 nx[3] = {};
+    auto prefetch = [&](uint64_t t) {
+        const uint64_t q = t + 16ull * threadIdx.x;
+        if (vec && q + 16 <= end) {
+            const uint4 *src = reinterpret_cast<const uint4 *>(rgb + q * 3);
+            nx[0] = ld_stream(src);
+            nx[1] = ld_stream(src + 1);
+            nx[2] = ld_stream(src + 2);
+        }
+    };
+    if (base < end) prefetch(base);
+    for (uint64_t t0 = base; t0 < end; t0 += kTilePix) {
+        for (int b = threadIdx.x; b < kBuckets; b += kPartThreads) s_tc[b] = 0;
+        __syncthreads();
+        const uint64_t p0 = t0 + 16ull * threadIdx.x;
+        const int n = p0 < end ? (end - p0 < 16 ? (int)(end - p0) : 16) : 0;
+        uint32_t col[16], rank[16];
+        if (vec && n == 16) decode16(nx[0], nx[1], nx[2], col);
+        else decode_group(rgb, p0, n, false, col);
+        if (t0 + kTilePix < end) prefetch(t0 + kTilePix);
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            rank[j] = j < n ? atomicAdd(&s_tc[col[j] >> kSlotBits], 1u) : 0u;
+        __syncthreads();
+        // exclusive scan of the 1024 tile counts: one per thread
+        static_assert(kPartThreads == kBuckets, "one bucket per thread in the tile scan");
+        const uint32_t a0 = s_tc[threadIdx.x];
+        uint32_t x = a0;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, x, o);
+            if ((threadIdx.x & 31) >= (unsigned)o) x += t;
+        }
+        if ((threadIdx.x & 31) == 31) s_w[threadIdx.x >> 5] = x;
+        __syncthreads();
+        uint32_t woff = 0;
+        for (int w = 0; w < (int)(threadIdx.x >> 5); ++w) woff += s_w[w];
+        s_ts[threadIdx.x] = woff + x - a0;
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            if (j < n) {
+                const uint32_t b = col[j] >> kSlotBits;
+                const uint32_t pos = s_ts[b] + rank[j];
+                s_e[pos] = ((uint32_t)(p0 + j - base) << kSlotBits) | (col[j] & (kSlots - 1));
+                s_b[pos] = (uint16_t)b;
+            }
+        __syncthreads();
+        // runs of consecutive entries per bucket go to consecutive global slots
+        const int tn = end - t0 < (uint64_t)kTilePix ? (int)(end - t0) : kTilePix;
+        for (int j = threadIdx.x; j < tn; j += kPartThreads) {
+            const uint32_t b = s_b[j];
+            ent[s_cur[b] + (j - s_ts[b])] = s_e[j];
+        }
+        __syncthreads();
+        for (int b = threadIdx.x; b < kBuckets; b += kPartThreads) s_cur[b] += s_tc[b];
+        __syncthreads();
+    }
+}
+
+// one block per bucket (largest first): count and first pixel per colour in
+// shared memory. A warp walks one chunk segment at a time, so every entry's
+// pixel index is chunk * g + offset without a search.
+__global__ void __launch_bounds__(kAggThreads) bucket_agg(const uint32_t *__restrict__ ent,
+                                                          const uint32_t *__restrict__ gcnt, int G, uint64_t chunk,
+                                                          const uint32_t *__restrict__ bstart,
+                                                          const uint32_t *__restrict__ bsize,
+                                                          const uint32_t *__restrict__ border,
+                                                          uint32_t *__restrict__ cnt_out,
+                                                          uint32_t *__restrict__ bitmap) {
+    extern __shared__ uint32_t s_tab[]; // kSlots counts | kSlots minimum pixel indices
+    uint32_t *s_cnt = s_tab, *s_min = s_tab + kSlots;
+    const uint32_t b = border[blockIdx.x];
+    for (int i = threadIdx.x; i < kSlots; i += kAggThreads) {
+        s_cnt[i] = 0u;
+        s_min[i] = 0xFFFFFFFFu;
+    }
+    __syncthreads();
+    const uint32_t *row = gcnt + (size_t)b * G; // segment starts within the bucket
+    const uint32_t bs = bstart[b], bn = bsize[b];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int U = 4; // entries per lane in flight
+    for (int g = warp; g < G; g += kAggThreads / 32) {
+        const uint32_t s0 = row[g], s1 = g + 1 < G ? row[g + 1] : bn;
+        const uint64_t pbase = (uint64_t)g * chunk;
+        for (uint32_t e0 = s0; e0 < s1; e0 += 32 * U) { // warp-uniform trip count
+            uint32_t x[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t e = e0 + u * 32 + lane;
+                x[u] = e < s1 ? __ldcs(ent + bs + e) : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t e = e0 + u * 32 + lane;
+                const bool v = e < s1;
+                if (!__any_sync(0xffffffffu, v)) break;
+                const uint32_t slot = x[u] & (kSlots - 1);
+                const uint32_t p = (uint32_t)(pbase + (x[u] >> kSlotBits));
+                const uint32_t act = __ballot_sync(0xffffffffu, v);
+                const int lead = __ffs(act) - 1;
+                const uint32_t s_first = __shfl_sync(0xffffffffu, slot, lead);
+                if (__all_sync(0xffffffffu, !v || slot == s_first)) {
+                    // one colour across the warp (flat images): one update per warp
+                    const uint32_t pm = __reduce_min_sync(0xffffffffu, v ? p : 0xFFFFFFFFu);
+                    if (lane == lead) {
+                        atomicAdd(&s_cnt[slot], (uint32_t)__popc(act));
+                        atomicMin(&s_min[slot], pm);
+                    }
+                } else if (v) {
+                    atomicAdd(&s_cnt[slot], 1u);
+                    if (p < s_min[slot]) atomicMin(&s_min[slot], p); // most later occurrences skip the atomic
+                }
+            }
+        }
+    }
+    __syncthreads();
+    uint32_t *dst = cnt_out + ((size_t)b << kSlotBits);
+    for (int i = threadIdx.x; i < kSlots; i += kAggThreads) {
+        const uint32_t c = s_cnt[i];
+        dst[i] = c; // stays in L2 for the emit's gathers
+        if (c) {
+            const uint32_t f = s_min[i];
+            atomicOr(&bitmap[f >> 5], 1u << (f & 31));
+        }
     }
 }
 
@@ -315,20 +514,48 @@ __global__ void pack_kernel(const uint8_t *__restrict__ rgb, uint64_t S, uint32_
 
 } // namespace
 
+// large images: the bucketed partition (part_count .. bucket_agg) into the
+// first-occurrence bitmap and the per-colour counts
+static void histogram_partitioned(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P, uint32_t *bitmap,
+                                  uint32_t *&cnt_out) {
+    cudaStream_t s = ctx->stream;
+    // chunks of at most 2^18 pixels (an entry's offset field), a multiple of 16
+    // pixels (48-byte vector loads), about 4 per SM
+    uint64_t chunk = (P + (uint64_t)ctx->num_sms * 4 - 1) / ((uint64_t)ctx->num_sms * 4);
+    chunk = (chunk + 15) & ~15ull;
+    if (chunk > (1ull << kChunkBits)) chunk = 1ull << kChunkBits;
+    const int G = (int)((P + chunk - 1) / chunk);
+    const int vec = (reinterpret_cast<uintptr_t>(rgb_d) & 15) == 0;
+    uint32_t *gcnt = static_cast<uint32_t *>(ctx->pseg.ensure(sizeof(uint32_t) * ((size_t)kBuckets * G + 3 * kBuckets)));
+    uint32_t *bsize = gcnt + (size_t)kBuckets * G, *bstart = bsize + kBuckets, *border = bstart + kBuckets;
+    uint32_t *ent = static_cast<uint32_t *>(ctx->pent.ensure(sizeof(uint32_t) * P));
+    cnt_out = static_cast<uint32_t *>(ctx->pcnt.ensure(sizeof(uint32_t) << 24));
+    part_count<<<G, kPartThreads, 0, s>>>(rgb_d, P, chunk, vec, gcnt, G);
+    seg_scan<<<kBuckets, 256, 0, s>>>(gcnt, G, bsize);
+    bucket_scan<<<1, kBuckets, 0, s>>>(bsize, bstart, border);
+    CQG_CUDA(ensure_smem((const void *)part_scatter, kScatterSmem));
+    part_scatter<<<G, kPartThreads, kScatterSmem, s>>>(rgb_d, P, chunk, vec, gcnt, G, bstart, ent);
+    const size_t agg_smem = sizeof(uint32_t) * 2 * kSlots;
+    CQG_CUDA(ensure_smem((const void *)bucket_agg, agg_smem));
+    bucket_agg<<<kBuckets, kAggThreads, agg_smem, s>>>(ent, gcnt, G, chunk, bstart, bsize, border, cnt_out, bitmap);
+    launched(ctx, 5);
+}
+
 void histogram_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P, uint32_t *colors_d,
                    uint32_t *counts_d, uint32_t *first_d, uint32_t *n_dev) {
     cudaStream_t s = ctx->stream;
-    if (ctx->tab.cap < (sizeof(uint2) << 24)) {
-        ctx->tab.ensure(sizeof(uint2) << 24);
-        CQG_CUDA(cudaMemsetAsync(ctx->tab.p, 0, sizeof(uint2) << 24, s));
-    }
     const uint64_t cap = P < (1ull << 24) ? P : (1ull << 24);
-    uint32_t *list = static_cast<uint32_t *>(ctx->list.ensure(cap * 4));
     const uint64_t words = (P + 31) / 32;
     const uint32_t nblk = ceil_div(words, kWordsPerBlock);
     uint32_t *bitmap = static_cast<uint32_t *>(ctx->bitmap.ensure(words * 4 + 16));
     uint32_t *wpref = static_cast<uint32_t *>(ctx->wordpref.ensure(words * 4 + 16 + (size_t)nblk * 4));
     uint32_t *bsum = wpref + words + 4;
+    const bool large = P >= (1ull << 22);
+    if (!large && ctx->tab.cap < (sizeof(uint2) << 24)) {
+        ctx->tab.ensure(sizeof(uint2) << 24);
+        CQG_CUDA(cudaMemsetAsync(ctx->tab.p, 0, sizeof(uint2) << 24, s));
+    }
+    uint32_t *list = large ? nullptr : static_cast<uint32_t *>(ctx->list.ensure(cap * 4));
 
     const int pb = prof_begin(ctx);
     CQG_CUDA(cudaMemsetAsync(n_dev, 0, 4, s));
@@ -343,20 +570,15 @@ void histogram_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P, uint32_t *col
     unsigned lgrid = ceil_div(cap, kThreads);
     if (lgrid > gmax) lgrid = gmax;
     // small images: one pass over the interleaved table (L2-resident anyway),
-    // emit + reset per listed colour. Large images: two passes over split
-    // 64 MiB tables (each fits the L2), emit in pixel order, one memset reset.
-    const bool large = P >= (1ull << 22);
+    // emit + reset per listed colour. Large images: the bucketed partition,
+    // emit in pixel order.
     uint2 *tab = ctx->tab.as<uint2>();
-    uint32_t *cnt = ctx->tab.as<uint32_t>(), *negf = cnt + (1u << 24);
+    uint32_t *cnt = nullptr;
     if (!large) {
         hist_count_fused<<<grid, kThreads, 0, s>>>(rgb_d, P, tab, list, n_dev, aligned);
         hist_mark_fused<<<lgrid, kThreads, 0, s>>>(list, n_dev, tab, bitmap);
     } else {
-        // counts and minimum indices by reductions; the bitmap from the
-        // first-index table (no unique-colour list, no global append counter)
-        hist_count_red<<<grid, kThreads, 0, s>>>(rgb_d, P, cnt, aligned);
-        hist_first<<<grid, kThreads, 0, s>>>(rgb_d, P, negf, aligned);
-        hist_mark_table<<<(unsigned)ctx->num_sms * 8, kThreads, 0, s>>>(negf, bitmap);
+        histogram_partitioned(ctx, rgb_d, P, bitmap, cnt);
     }
     scan_blocksum<<<nblk, kThreads, 0, s>>>(bitmap, words, bsum);
     scan_blocks<<<1, 1024, 0, s>>>(bsum, nblk, large ? n_dev : nullptr);
@@ -366,11 +588,10 @@ void histogram_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P, uint32_t *col
     } else {
         const unsigned egrid = (unsigned)ctx->num_sms * 8;
         hist_emit<<<egrid, kThreads, 0, s>>>(rgb_d, P, bitmap, wpref, cnt, colors_d, counts_d, first_d);
-        CQG_CUDA(cudaMemsetAsync(ctx->tab.p, 0, sizeof(uint2) << 24, s));
     }
     prof_end(ctx, CQG_PROF_HIST, pb, 3.0 * (double)P); // + 8 N' added by the caller
     CQG_CUDA(cudaGetLastError());
-    launched(ctx, large ? 7 : 6);
+    launched(ctx, large ? 4 : 6);
 }
 
 void subsample_2to1_dev(cqg_ctx *ctx, const uint8_t *rgb_d, int w, int h, uint8_t *out_d) {

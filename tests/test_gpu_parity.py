@@ -103,12 +103,13 @@ def test_histogram_device_pointers(ctx, oracle):
     assert np.array_equal(cnt[:n].cpu().numpy().view(np.uint32), k)
 
 
-@pytest.mark.parametrize("case", ["2048sq", "odd2049", "unaligned_large", "few_large"])
+@pytest.mark.parametrize("case", ["2048sq", "odd2049", "unaligned_large", "few_large", "flat_large",
+                                  "one_bucket", "two_colours"])
 def test_histogram_large_images(ctx, oracle, case):
-    # P >= 2^22: counts and first indices by reductions in two passes, the
-    # first-occurrence bitmap from a scan of the first-index table, pixel-order
-    # emit, one memset reset (hist.cu large path); odd sizes and unaligned
-    # buffers take the scalar tail loops
+    # P >= 2^22: the colour-bucketed partition (hist.cu: part_count ->
+    # part_scatter -> bucket_agg in shared memory), first-occurrence bitmap,
+    # pixel-order emit; odd sizes and unaligned buffers take the scalar paths,
+    # a flat image puts every pixel in one bucket and one shared-memory slot
     rng = np.random.default_rng(2024)
     if case == "2048sq":
         img = synth_image(2048, 2048, 11, nblobs=20, sigma=20.0, noise=0.3)
@@ -119,6 +120,14 @@ def test_histogram_large_images(ctx, oracle, case):
         buf = np.zeros(base.size + 7, np.uint8)
         buf[7:] = base.reshape(-1)
         img = buf[7:]
+    elif case == "flat_large":
+        img = np.full((2048, 2049, 3), 77, np.uint8)
+    elif case == "one_bucket":  # r = 0, g < 64: bucket 0 holds every pixel
+        img = rng.integers(0, 256, (2048, 2050, 3)).astype(np.uint8)
+        img[..., 0] = 0
+        img[..., 1] &= 63
+    elif case == "two_colours":
+        img = np.where(rng.random((2051, 2048, 1)) < 0.999, 10, 200).astype(np.uint8).repeat(3, axis=2)
     else:
         img = (rng.integers(0, 4, (2100, 2000, 3)) * 60).astype(np.uint8)
     assert img.size // 3 >= (1 << 22)
