@@ -1,20 +1,26 @@
 """Benchmark: quantized MPixel/s (and Lloyd colour-centre distances/s) of the
-B200-native hot path on BASELINE.json's configuration.
+B200-native hot path on BASELINE.json's configurations.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config cfg2|cfg1|cfg3|cfg3k64|cfg4|cfg5]
+                    [--config cfg2|cfg1|cfg3|cfg3k64|cfg4|cfg5] [--sharded]
 
 A step is one pass of the hot path (histogram -> init -> weighted Lloyd ->
 mapping + MSE, i.e. quant::run_quantize) over one batch of synthetic input.
-Default workload: BASELINE.json configs[1] (512x512, K=256, k-means++), the
-configuration the metric ("... at K=256") is quoted on that fits one GPU.
+The line's `value` is BASELINE.json configs[1] (cfg2: 512x512, K=256,
+k-means++), the K=256 configuration the reference's CPU build also runs in
+seconds; the other single-GPU K=256 configurations are reported in the same
+line under `by_config` (N=1: cfg3 4096^2 maximin, cfg5 8192^2 k-means++, each
+with its own roofline fractions, e2e, parity digest and 1-core reference
+baseline); cfg1 is the reference's own small case.
 
-Multi-GPU (torchrun, one rank per GPU): single-image configs run one
-independent replica per rank (the path does not shard below ~1M colours;
-"replicas only"); cfg4 shards its 64 images across ranks. Timing: W untimed
-warm-up steps, then K steps, each bracketed by CUDA events on the launching
-stream with an L2 flush (write of a 512 MiB buffer) between steps outside the
-timed events; the per-rank device time is max-reduced over ranks.
+Multi-GPU (one rank per GPU; `--gpus N` starts torch.distributed.run itself
+when WORLD_SIZE is unset): cfg2 runs one independent replica per rank (the
+path does not shard below ~1M colours: "replicas only"); by_config then adds
+cfg4 (64 images sharded across ranks, no collective) and cfg5 sharded by
+unique colour (one NCCL allreduce of the int64 moments per iteration).
+Timing: W untimed warm-up steps, then K steps, each bracketed by CUDA events
+on the launching stream with an L2 flush (write of a 512 MiB buffer) between
+steps outside the timed events; the per-rank device time is max-reduced.
 
 --impl reference times the reference's own CPU implementation (the reference
 sources compiled in place: oracle/_ref/libquantref.so, through its public
@@ -235,8 +241,9 @@ def cpu_baseline(cfg, budget_s: float):
 # ---------------------------------------------------------------------------
 # our arm
 
-def parity_digest(cfg, img, k, image_id, st, d_pal, d_idx, d_q):
-    """The bench step's outputs against the C oracle (UPDATE_EXACT), same input."""
+def parity_digest(cfg, img, k, image_id, st, pal, didx, dq):
+    """The bench step's outputs (host copies) against the C oracle
+    (UPDATE_EXACT) on the same input."""
     import hashlib
     from oracle.pyoracle import UPDATE_EXACT, Oracle
     t0 = time.perf_counter()
@@ -246,9 +253,6 @@ def parity_digest(cfg, img, k, image_id, st, d_pal, d_idx, d_q):
     init = O.init_kmeanspp(c, n, P, k, cfg.seed) if cfg.init == "kpp" else O.init_maximin(c, n, P, k, cfg.seed)
     r = O.wsm(c, n, P, init, fixed_it=cfg.fixed_iterations, mode=UPDATE_EXACT)
     idx, q, mse, mndc = O.map_pixels(img, r.centers, mode=UPDATE_EXACT)
-    pal = d_pal.cpu().numpy()
-    didx = d_idx.cpu().numpy().view(np.uint32)
-    dq = d_q.cpu().numpy().reshape(-1, 3)
     out = {
         "checker": "oracle/cq_oracle.c (C restatement, exact moments)", "image": image_id,
         "palette_sha1": hashlib.sha1(pal.tobytes()).hexdigest()[:16],
@@ -266,14 +270,20 @@ def parity_digest(cfg, img, k, image_id, st, d_pal, d_idx, d_q):
     return out
 
 
-def run_sharded(args, cfg, ctx, dev, world, rank, stream):
-    """One huge image (cfg5 / cfg3) over `world` ranks: histogram and init per
-    rank, Lloyd sharded by unique colour with one NCCL allreduce of the int64
-    moment partials per iteration (parallel.sharded_wsm), mapping of this
-    rank's rows. Total work is fixed as ranks are added (strong scaling)."""
+def sharded_measure(args, cfg, env, steps, warmup):
+    """One huge image (cfg5 / cfg3) over the ranks: histogram and init per
+    rank, Lloyd sharded by unique colour with one allreduce of the int64
+    moment partials per iteration (parallel.sharded_wsm; NCCL over NVLink),
+    mapping of this rank's rows, the global MSE by an allreduce of the per-rank
+    squared-distance sums. Total work is fixed as ranks are added (strong
+    scaling). Device time per step is the max over ranks; e2e adds the H2D of
+    the image and the D2H of this rank's rows from / to pinned host memory."""
     import torch
     import torch.distributed as dist
     from paper_1101_0395_b200 import cabi, parallel
+    world, rank, local, dev, stream = env["world"], env["rank"], env["local"], env["dev"], env["stream"]
+    ctx = cabi.Context(local)
+    ctx.set_stream(stream.cuda_stream)
     img = cfg.image()
     H, W = img.shape[:2]
     P = H * W
@@ -285,64 +295,98 @@ def run_sharded(args, cfg, ctx, dev, world, rank, stream):
     d_cnt = torch.empty(cap, dtype=torch.int32, device=dev)
     d_init = torch.empty((K, 3), dtype=torch.float64, device=dev)
     r0, r1 = parallel.shard_bounds(H, world, rank)
-    d_idx = torch.empty((r1 - r0) * W, dtype=torch.int32, device=dev)
-    d_q = torch.empty(((r1 - r0) * W, 3), dtype=torch.uint8, device=dev)
+    Pr = (r1 - r0) * W
+    d_idx = torch.empty(max(Pr, 1), dtype=torch.int32, device=dev)
+    d_q = torch.empty((max(Pr, 1), 3), dtype=torch.uint8, device=dev)
     term = cabi.Term(1e-3, 100, cfg.fixed_iterations, 0)
     eng = parallel.CudaShardEngine(ctx, dev)
     info = {}
 
-    def step():
+    def step(src=d_img, idx=d_idx, q=d_q):
+        if src is not d_img:
+            d_img.copy_(src, non_blocking=True)
         n = ctx.histogram_raw(d_img, P, d_col, d_cnt)
         ctx.init_raw(kind, d_col, d_cnt, n, P, K, cfg.seed, d_init)
         r = parallel.sharded_wsm(eng, d_col[:n], d_cnt[:n], P, d_init, K, term, labels=False)
         pal = np.ascontiguousarray(r.centers)
-        if r1 > r0:
-            ctx.map_raw(d_img[r0:r1], (r1 - r0) * W, pal, K, d_idx, 4, d_q)
-        info.update(n=n, it=r.iterations, ndc=r.ndc_total)
+        mse_r = ctx.map_raw(d_img[r0:r1], Pr, pal, K, d_idx, 4, d_q) if Pr else 0.0
+        if idx is not d_idx and Pr:
+            idx[:Pr].copy_(d_idx[:Pr], non_blocking=True)
+            q[:Pr].copy_(d_q[:Pr], non_blocking=True)
+        tot = torch.tensor([mse_r * Pr], dtype=torch.float64, device=dev)
+        dist.all_reduce(tot)  # global MSE: sum of the ranks' squared-distance sums / P
+        info.update(n=n, it=r.iterations, ndc=r.ndc_total, mse=float(tot.item()) / P, pal=pal)
         return r
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    dist.barrier()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
-    tot = 0.0
-    launches0 = ctx.launches
-    with ClockSampler(int(os.environ.get("LOCAL_RANK", 0))) as clk:
-        for s_ in range(args.steps):
+    def timed(run, nsteps):
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+        tot = 0.0
+        for s_ in range(nsteps):
             flush.fill_(s_ & 255)
             torch.cuda.synchronize()
             dist.barrier()
             ev0.record(stream)
-            step()
+            run()
             ev1.record(stream)
             torch.cuda.synchronize()
             tot += ev0.elapsed_time(ev1)
-    t = torch.tensor([tot], dtype=torch.float64, device=dev)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item()) / args.steps
-    if rank == 0:
-        print(json.dumps({
-            "metric": METRIC, "value": P / (ms / 1e3) / 1e6, "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": cfg.name, "image": f"{W}x{H}", "k": K, "init": cfg.init,
-                       "parallelism": f"unique colours sharded over {world} (moment allreduce per iteration)",
-                       "l2": "flushed (512 MiB write) between timed steps"},
-            "lloyd_distances_per_s": info["n"] * K * info["it"] / (ms / 1e3),
-            "n_unique": info["n"], "iterations": info["it"],
-            "gpu_launches": int(ctx.launches - launches0), "clocks": clk.summary(),
-            "e2e": None, "roofline": None, "cpu_baseline": None}))
+        t = torch.tensor([tot], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item()) / nsteps
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    launches0 = ctx.launches
+    with ClockSampler(local) as clk:
+        ms = timed(step, steps)
+    launches = ctx.launches - launches0
+    h_img = torch.from_numpy(img).pin_memory()
+    h_idx = torch.empty(max(Pr, 1), dtype=torch.int32).pin_memory()
+    h_q = torch.empty((max(Pr, 1), 3), dtype=torch.uint8).pin_memory()
+    e_ms = timed(lambda: step(h_img, h_idx, h_q), steps)
+    ctx.close()
+    return {
+        "workload": cfg.name, "value": P / (ms / 1e3) / 1e6, "unit": UNIT, "n_gpus": world, "steps": steps,
+        "ms_per_step": ms, "scaling": "strong",
+        "parallelism": (f"unique colours sharded over {world} ranks (int64 moment allreduce per iteration); "
+                        "histogram and initialiser replicated per rank; rows sharded for the mapping"),
+        "lloyd_distances_per_s": info["n"] * K * info["it"] / (ms / 1e3), "n_unique": info["n"],
+        "iterations": info["it"], "ndc_total": info["ndc"], "mse": info["mse"],
+        "e2e": {"value": P / (e_ms / 1e3) / 1e6, "unit": UNIT, "ms_per_step": e_ms, "h2d_bytes_per_step": 3 * P,
+                "d2h_bytes_per_step": 7 * Pr + 24 * K},
+        "gpu_launches": int(launches), "clocks": clk.summary(),
+    }
+
+
+def run_sharded_line(args, cfg, env):
+    """--sharded: the colour-sharded path as the bench line itself."""
+    import torch
+    import torch.distributed as dist
+    if env["world"] == 1:
+        backend = "gloo" if env["share"] else "nccl"
+        kw = {} if env["share"] else {"device_id": torch.device("cuda", env["local"])}
+        dist.init_process_group(backend, rank=0, world_size=1, init_method="tcp://127.0.0.1:29533", **kw)
+    res = sharded_measure(args, cfg, env, args.steps, args.warmup)
+    if env["rank"] == 0:
+        line = {"metric": METRIC, "higher_is_better": True, "warmup": args.warmup, "vs_baseline": None,
+                "dtype": "f32", "data": "synthetic",
+                "config": {"workload": cfg.name, "image": f"{cfg.width}x{cfg.height}", "k": cfg.k, "init": cfg.init,
+                           "parallelism": res.pop("parallelism"), "l2": "flushed (512 MiB write) between timed steps"},
+                "roofline": None, "cpu_baseline": None, **res}
+        print(json.dumps(line))
+    dist.destroy_process_group()
     return 0
 
 
-def run_ours(args, cfg):
+HOSTPOOL = ThreadPoolExecutor(4)  # parity digests and 1-core CPU baselines, overlapped with device work
+
+
+def setup_env(args):
     import torch
     import torch.distributed as dist
-    from paper_1101_0395_b200 import cabi, quant
-
     world = env_int("WORLD_SIZE", 1)
     rank = env_int("RANK", 0)
     local = env_int("LOCAL_RANK", 0)
@@ -357,21 +401,93 @@ def run_ours(args, cfg):
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local)
-    stream = torch.cuda.current_stream()
+    return {"world": world, "rank": rank, "local": local, "share": share,
+            "dev": torch.device("cuda", local), "stream": torch.cuda.current_stream()}
+
+
+def summarize(res, cpu):
+    """The by_config entry of one workload."""
+    rf = res["roofline"]
+    return {
+        "workload": res["config"]["workload"], "value": res["value"], "unit": UNIT,
+        "ms_per_step": res["ms_per_step"], "steps": res["steps"], "n_unique": res["n_unique"],
+        "iterations": res["iterations"], "lloyd_distances_per_s": res["lloyd_distances_per_s"],
+        "stage_ms_last_step": res["stage_ms_last_step"],
+        "lloyd_kernel": {"kernel": rf["kernel"], "achieved_tflops": rf["achieved"], "frac_fp32": rf["frac"],
+                         "dense_sweep_frac_fp32": rf["sweep_isolated"]["frac"]},
+        "histogram_hbm_frac": res["byte_kernels"]["histogram"]["frac"],
+        "pixel_map_hbm_frac": res["byte_kernels"]["pixel_map"]["frac"],
+        "byte_kernels": res["byte_kernels"], "e2e": res["e2e"], "cpu_baseline": cpu,
+        "parity": res["parity"], "gpu_launches": res["gpu_launches"], "clocks": res["clocks"],
+    }
+
+
+def resolve(x):
+    return x.result() if hasattr(x, "result") else x
+
+
+def run_ours(args, cfg):
+    import torch.distributed as dist
+    from paper_1101_0395_b200.synth import CONFIGS
+    env = setup_env(args)
+    world, rank = env["world"], env["rank"]
+    if args.sharded or (world > 1 and cfg.images == 1 and cfg.name in ("cfg5", "cfg3", "cfg3k64")):
+        return run_sharded_line(args, cfg, env)
+    cpu_on = rank == 0 and world == 1 and not args.no_cpu_baseline
+    extra = [] if args.no_by_config or cfg.name not in ("cfg2",) else (["cfg3", "cfg5"] if world == 1 else ["cfg4"])
+    # 1-core reference baselines run on host threads while the device measures
+    cpu_jobs = {}
+    if cpu_on:
+        cpu_jobs[cfg.name] = HOSTPOOL.submit(cpu_baseline, cfg, args.cpu_seconds)
+        for name in extra:
+            cpu_jobs[name] = HOSTPOOL.submit(cpu_baseline, CONFIGS[name], 0.0)  # one pipeline
+    line = measure(args, cfg, env, args.steps, args.warmup, not args.no_e2e, not args.no_parity)
+    by_config = {}
+    for name in extra:
+        res = measure(args, CONFIGS[name], env, 3, 3, not args.no_e2e, not args.no_parity)
+        if rank == 0:
+            by_config[name] = res
+    if world > 1 and not args.no_by_config and cfg.name == "cfg2":
+        res = sharded_measure(args, CONFIGS["cfg5"], env, 3, 3)
+        if rank == 0:
+            by_config["cfg5_sharded"] = res  # strong scaling of the huge image
+    rc = 0
+    if rank == 0:
+        line["cpu_baseline"] = resolve(cpu_jobs.get(cfg.name))
+        line["parity"] = resolve(line["parity"])
+        out = {}
+        for name, res in by_config.items():
+            if "roofline" in res:
+                res["parity"] = resolve(res["parity"])
+                out[name] = summarize(res, resolve(cpu_jobs.get(name)))
+            else:
+                out[name] = res
+        if out:
+            line["by_config"] = out
+        print(json.dumps(line))
+        bad = [n for n, p in [(cfg.name, line["parity"])] + [(n, r.get("parity")) for n, r in out.items()]
+               if p is not None and not p["ok"]]
+        if bad:
+            print("bench: device outputs differ from the oracle on " + ", ".join(bad), file=sys.stderr)
+            rc = 1
+    if world > 1:
+        dist.destroy_process_group()
+    return rc
+
+
+def measure(args, cfg, env, steps, warmup, e2e_on=True, parity_on=True):
+    """One workload on this rank: W warm-ups, `steps` timed steps (device
+    events, L2 flushed between steps, max over ranks), the stage profile, the
+    roofline of the dominant kernel, e2e through the C-ABI with pinned host
+    buffers, and the oracle parity digest (a future on the host pool).
+    Returns the fields of a bench line."""
+    import torch
+    import torch.distributed as dist
+    from paper_1101_0395_b200 import cabi, quant
+
+    world, rank, local, dev, stream = env["world"], env["rank"], env["local"], env["dev"], env["stream"]
     ctx = cabi.Context(local)
     ctx.set_stream(stream.cuda_stream)
-    if args.sharded or (world > 1 and cfg.images == 1 and cfg.name in ("cfg5", "cfg3", "cfg3k64")):
-        if world == 1:
-            if share:
-                dist.init_process_group("gloo", rank=0, world_size=1, init_method="tcp://127.0.0.1:29533")
-            else:
-                dist.init_process_group("nccl", rank=0, world_size=1, init_method="tcp://127.0.0.1:29533",
-                                        device_id=torch.device("cuda", local))
-        rc = run_sharded(args, cfg, ctx, dev, world, rank, stream)
-        dist.destroy_process_group()
-        ctx.close()
-        return rc
 
     # work owned by this rank
     if cfg.images > 1:
@@ -441,7 +557,7 @@ def run_ours(args, cfg):
         return run_batch(d_imgs, d_idx, d_q, d_pal)
 
     # warm-up
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         step_device()
     torch.cuda.synchronize()
     if world > 1:
@@ -455,7 +571,7 @@ def run_ours(args, cfg):
     step_ms, all_stats = [], []
     launches0 = sum(c.launches for c in ctxs)
     with ClockSampler(local) as clk:
-        for s in range(args.steps):
+        for s in range(steps):
             flush.fill_(s & 255)  # L2 flush outside the timed events
             torch.cuda.synchronize()
             ev0.record(stream)
@@ -482,7 +598,7 @@ def run_ours(args, cfg):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.barrier()
     total_ms = float(t.item())
-    ms_per_step = total_ms / args.steps
+    ms_per_step = total_ms / steps
     pixels_per_step_all = cfg.images * P_list[0] * (1 if cfg.images > 1 else world)
     value = pixels_per_step_all / (ms_per_step / 1e3) / 1e6
 
@@ -506,8 +622,8 @@ def run_ours(args, cfg):
     names = ["sweep", "map_sweep", "histogram", "pixel_map", "init", "replay", "ndc", "lloyd_loop", "map_ndc"]
     stage_share = {}
     for i, nm in enumerate(names):
-        stage_share[nm] = {"ms_per_step": prof.ms[i] / args.steps,
-                           "launches_per_step": prof.launches[i] / args.steps}
+        stage_share[nm] = {"ms_per_step": prof.ms[i] / steps,
+                           "launches_per_step": prof.launches[i] / steps}
     iso_ms, iso_units = ctx.bench_sweep(20)
     iso_achieved = 8.0 * iso_units / (iso_ms / 1e3) / 1e12
     persistent = prof.launches[cabi.PROF_SWEEP] == 0 and prof.launches[cabi.PROF_LLOYD] > 0
@@ -524,14 +640,14 @@ def run_ours(args, cfg):
         k_ms = prof.ms[cabi.PROF_LLOYD] / max(int(prof.launches[cabi.PROF_LLOYD]), 1)
         achieved = 8.0 * prof.units[cabi.PROF_LLOYD] / (prof.ms[cabi.PROF_LLOYD] / 1e3) / 1e12
         achieved_actual = 8.0 * actual_units / (prof.ms[cabi.PROF_LLOYD] / 1e3) / 1e12
-        k_share = prof.ms[cabi.PROF_LLOYD] / args.steps / ms_per_step
+        k_share = prof.ms[cabi.PROF_LLOYD] / steps / ms_per_step
     else:
         kname = "sweep_kernel<WALK> (Lloyd assignment, one launch per iteration)"
         k_ms = iso_ms
         achieved = iso_achieved
         achieved_actual = iso_achieved
         iters_all = sum(s.lloyd.iterations for st in all_stats for s in st)
-        k_share = iso_ms * iters_all / args.steps / ms_per_step
+        k_share = iso_ms * iters_all / steps / ms_per_step
     traffic = None
     tpath = os.path.join(ROOT, "profiles", f"ncu_traffic_{cfg.name}.json")
     if os.path.exists(tpath):
@@ -554,7 +670,7 @@ def run_ours(args, cfg):
     }
     # the kernel with the largest device-time share, when it is not the Lloyd kernel
     dominant = None
-    share = {nm: prof.ms[i] / args.steps / ms_per_step for i, nm in enumerate(names)}
+    share = {nm: prof.ms[i] / steps / ms_per_step for i, nm in enumerate(names)}
     top = max(share, key=share.get)
     if top == "init" and share["init"] > k_share:
         K0 = ks[0]
@@ -582,24 +698,27 @@ def run_ours(args, cfg):
     pix_ms = prof.ms[cabi.PROF_PIXEL]
     hbm = peaks.get("hbm_gbs", 6545.6)
     n_unique = all_stats[-1][0].n_unique
-    byte_kernels = {
-        "histogram": {"achieved_gbs": (prof.units[cabi.PROF_HIST] + 8.0 * n_unique * args.steps * len(imgs)) / (hist_ms / 1e3) / 1e9 if hist_ms else None,
-                      "peak_gbs": hbm},
-        "pixel_map": {"achieved_gbs": prof.units[cabi.PROF_PIXEL] / (pix_ms / 1e3) / 1e9 if pix_ms else None,
-                      "peak_gbs": hbm},
+    hist_gbs = ((prof.units[cabi.PROF_HIST] + 8.0 * n_unique * steps * len(imgs)) / (hist_ms / 1e3) / 1e9
+                if hist_ms else None)
+    pix_gbs = prof.units[cabi.PROF_PIXEL] / (pix_ms / 1e3) / 1e9 if pix_ms else None
+    byte_kernels = {  # algorithmic bytes: histogram 3P + 8N', pixel map 3P in + 7P out
+        "histogram": {"achieved_gbs": hist_gbs, "peak_gbs": hbm, "frac": hist_gbs / hbm if hist_gbs else None,
+                      "ms_per_step": hist_ms / steps},
+        "pixel_map": {"achieved_gbs": pix_gbs, "peak_gbs": hbm, "frac": pix_gbs / hbm if pix_gbs else None,
+                      "ms_per_step": pix_ms / steps},
     }
 
     # end-to-end through the C-ABI with pinned HOST buffers (H2D + D2H inside the timed region)
     e2e = None
-    if not args.no_e2e:
+    if e2e_on:
         h_imgs = [torch.from_numpy(im).pin_memory() for im in imgs]
         h_idx = [torch.empty(P, dtype=torch.int32).pin_memory() for P in P_list]
         h_q = [torch.empty((P, 3), dtype=torch.uint8).pin_memory() for P in P_list]
         h_pal = [np.empty((k, 3)) for k in ks]
-        for _ in range(max(1, args.warmup // 2)):
+        for _ in range(max(1, warmup // 2)):
             run_batch(h_imgs, h_idx, h_q, h_pal)
         e_ms = []
-        for s in range(args.steps):
+        for s in range(steps):
             flush.fill_(s & 255)
             torch.cuda.synchronize()
             ev0.record(stream)
@@ -610,7 +729,7 @@ def run_ours(args, cfg):
         et = torch.tensor([sum(e_ms)], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
-        e_step = float(et.item()) / args.steps
+        e_step = float(et.item()) / steps
         h2d = sum(3 * P for P in P_list)
         d2h = sum(7 * P + 24 * k + 8 * 100 for P, k in zip(P_list, ks))
         e2e = {"value": pixels_per_step_all / (e_step / 1e3) / 1e6, "unit": UNIT,
@@ -621,18 +740,16 @@ def run_ours(args, cfg):
     # against the C oracle (exact-moment mode): palette bytes, iterations,
     # NDC, mapping indices / pixels / MSE / mapping NDC. A mismatch fails the run.
     parity = None
-    if rank == 0 and not args.no_parity:
-        parity = parity_digest(cfg, imgs[0], ks[0], my[0], all_stats[-1][0], d_pal[0], d_idx[0], d_q[0])
+    if rank == 0 and parity_on:
+        outs = (d_pal[0].cpu().numpy(), d_idx[0].cpu().numpy().view(np.uint32), d_q[0].cpu().numpy().reshape(-1, 3))
+        parity = HOSTPOOL.submit(parity_digest, cfg, imgs[0], ks[0], my[0], all_stats[-1][0], *outs)
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(cfg, args.cpu_seconds)
-
+    line = None
     if rank == 0:
         st0 = all_stats[-1][0]
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
+            "warmup": warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak" if cfg.images == 1 else "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
             "config": {"workload": cfg.name, "image": f"{cfg.width}x{cfg.height}",
@@ -650,21 +767,17 @@ def run_ours(args, cfg):
             "stage_ms_last_step": {"histogram": st0.ms_histogram, "init": st0.ms_init,
                                    "lloyd": st0.ms_lloyd, "map": st0.ms_map},
             "kernels": stage_share, "byte_kernels": byte_kernels,
-            "roofline": roofline, "dominant_kernel": dominant, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roofline, "dominant_kernel": dominant, "cpu_baseline": None, "e2e": e2e,
             "gpu_launches": int(gpu_launches), "clocks": clocks, "parity": parity,
         }
-        print(json.dumps(line))
-        if parity is not None and not parity["ok"]:
-            print("bench: device outputs differ from the oracle: " + json.dumps(parity), file=sys.stderr)
-            return 1
-    if world > 1:
-        dist.destroy_process_group()
     if pool:
         pool.shutdown()
     for c in ctxs[1:]:
         c.close()
     ctx.close()
-    return 0
+    return line
+
+
 
 
 def main():
@@ -684,8 +797,23 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--sharded", action="store_true",
                     help="run a single-image config through the colour-sharded multi-GPU path")
+    ap.add_argument("--no-by-config", action="store_true",
+                    help="skip the by_config measurements (cfg3 / cfg5 at N=1; cfg4 and sharded cfg5 at N>1)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # launched as `python bench.py --gpus N`: start the N ranks ourselves
+        # (one process per GPU, torch.distributed over NCCL, rendezvous on 127.0.0.1)
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+        return subprocess.call(cmd)
+    if args.impl == "ours" and env_int("WORLD_SIZE", 1) != args.gpus:
+        print(f"bench: --gpus {args.gpus} but WORLD_SIZE={env_int('WORLD_SIZE', 1)}", file=sys.stderr)
+        return 2
     from paper_1101_0395_b200.synth import CONFIGS
     cfg = CONFIGS[args.config]
     if args.impl == "reference":

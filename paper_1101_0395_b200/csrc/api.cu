@@ -255,7 +255,7 @@ void cqg_destroy(cqg_ctx *ctx) {
                       &ctx->sse, &ctx->lut, &ctx->idx_out, &ctx->q_out, &ctx->mom_map, &ctx->coarse, &ctx->mind2,
                       &ctx->initpart, &ctx->initsel, &ctx->unit_draws, &ctx->inittile, &ctx->mom_g, &ctx->partial,
                       &ctx->bnd, &ctx->shift, &ctx->dcode, &ctx->sub_img, &ctx->raw_col, &ctx->raw_cnt,
-                      &ctx->full_col, &ctx->full_cnt, &ctx->map_rows, &ctx->pcnt, &ctx->pent, &ctx->pseg};
+                      &ctx->full_col, &ctx->full_cnt, &ctx->map_rows, &ctx->map_lab, &ctx->pcnt, &ctx->pent, &ctx->pseg};
     for (DevBuf *b : bufs) b->release();
     ctx->pinned.release();
     ctx->pinned_nu.release();

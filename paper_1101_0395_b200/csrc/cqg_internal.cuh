@@ -128,7 +128,7 @@ struct cqg_ctx {
     cqg::DevBuf mom_g, partial; // sharded Lloyd: global moments, packed partials
     void *shard = nullptr;      // cqg::ShardState (lloyd.cu)
     // mapping
-    cqg::DevBuf lut, idx_out, q_out, mom_map, map_rows;
+    cqg::DevBuf lut, idx_out, q_out, mom_map, map_rows, map_lab;
     cqg::DevBuf coarse; // 5 x 32768 u64 coarse histogram (cqg_coarse_histogram)
     // init
     cqg::DevBuf mind2, initpart, initsel, unit_draws, inittile;

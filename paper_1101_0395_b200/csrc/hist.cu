@@ -347,8 +347,10 @@ __global__ void __launch_bounds__(kPartThreads) part_scatter(const uint8_t *__re
 }
 
 // one block per bucket (largest first): count and first pixel per colour in
-// shared memory. A warp walks one chunk segment at a time, so every entry's
-// pixel index is chunk * g + offset without a search.
+// shared memory. Each warp takes a contiguous slice of the bucket's entries;
+// a lane tracks the chunk segment its entry falls in (the segment starts are
+// in shared memory, entries only move forward), so the pixel index is
+// chunk * g + offset with no search and no idle lanes at segment ends.
 __global__ void __launch_bounds__(kAggThreads) bucket_agg(const uint32_t *__restrict__ ent,
                                                           const uint32_t *__restrict__ gcnt, int G, uint64_t chunk,
                                                           const uint32_t *__restrict__ bstart,
@@ -356,49 +358,62 @@ __global__ void __launch_bounds__(kAggThreads) bucket_agg(const uint32_t *__rest
                                                           const uint32_t *__restrict__ border,
                                                           uint32_t *__restrict__ cnt_out,
                                                           uint32_t *__restrict__ bitmap) {
-    extern __shared__ uint32_t s_tab[]; // kSlots counts | kSlots minimum pixel indices
-    uint32_t *s_cnt = s_tab, *s_min = s_tab + kSlots;
+    extern __shared__ uint32_t s_tab[]; // kSlots counts | kSlots minimum pixel indices | G + 1 segment starts
+    uint32_t *s_cnt = s_tab, *s_min = s_tab + kSlots, *s_seg = s_tab + 2 * kSlots;
     const uint32_t b = border[blockIdx.x];
+    const uint32_t bs = bstart[b], bn = bsize[b];
     for (int i = threadIdx.x; i < kSlots; i += kAggThreads) {
         s_cnt[i] = 0u;
         s_min[i] = 0xFFFFFFFFu;
     }
+    for (int g = threadIdx.x; g < G; g += kAggThreads) s_seg[g] = gcnt[(size_t)b * G + g];
+    if (threadIdx.x == 0) s_seg[G] = bn;
     __syncthreads();
-    const uint32_t *row = gcnt + (size_t)b * G; // segment starts within the bucket
-    const uint32_t bs = bstart[b], bn = bsize[b];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    constexpr int U = 4; // entries per lane in flight
-    for (int g = warp; g < G; g += kAggThreads / 32) {
-        const uint32_t s0 = row[g], s1 = g + 1 < G ? row[g + 1] : bn;
-        const uint64_t pbase = (uint64_t)g * chunk;
-        for (uint32_t e0 = s0; e0 < s1; e0 += 32 * U) { // warp-uniform trip count
-            uint32_t x[U];
+    constexpr int kWarps = kAggThreads / 32, U = 4; // U entries per lane in flight
+    const uint32_t per = (bn + kWarps - 1) / kWarps;
+    const uint32_t w0 = per * warp < bn ? per * warp : bn, w1 = w0 + per < bn ? w0 + per : bn;
+    // the segment of entry w0 + lane: first g with s_seg[g + 1] > e
+    int g = 0;
+    {
+        int lo = 0, hi = G - 1;
+        const uint32_t e = w0 + lane;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (s_seg[mid] <= e) lo = mid;
+            else hi = mid - 1;
+        }
+        g = lo;
+    }
+    for (uint32_t e0 = w0; e0 < w1; e0 += 32 * U) { // warp-uniform trip count
+        uint32_t x[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const uint32_t e = e0 + u * 32 + lane;
-                x[u] = e < s1 ? __ldcs(ent + bs + e) : 0u;
-            }
+        for (int u = 0; u < U; ++u) {
+            const uint32_t e = e0 + u * 32 + lane;
+            x[u] = e < w1 ? __ldcs(ent + bs + e) : 0u;
+        }
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const uint32_t e = e0 + u * 32 + lane;
-                const bool v = e < s1;
-                if (!__any_sync(0xffffffffu, v)) break;
-                const uint32_t slot = x[u] & (kSlots - 1);
-                const uint32_t p = (uint32_t)(pbase + (x[u] >> kSlotBits));
-                const uint32_t act = __ballot_sync(0xffffffffu, v);
-                const int lead = __ffs(act) - 1;
-                const uint32_t s_first = __shfl_sync(0xffffffffu, slot, lead);
-                if (__all_sync(0xffffffffu, !v || slot == s_first)) {
-                    // one colour across the warp (flat images): one update per warp
-                    const uint32_t pm = __reduce_min_sync(0xffffffffu, v ? p : 0xFFFFFFFFu);
-                    if (lane == lead) {
-                        atomicAdd(&s_cnt[slot], (uint32_t)__popc(act));
-                        atomicMin(&s_min[slot], pm);
-                    }
-                } else if (v) {
-                    atomicAdd(&s_cnt[slot], 1u);
-                    if (p < s_min[slot]) atomicMin(&s_min[slot], p); // most later occurrences skip the atomic
+        for (int u = 0; u < U; ++u) {
+            const uint32_t e = e0 + u * 32 + lane;
+            const bool v = e < w1;
+            if (!__any_sync(0xffffffffu, v)) break;
+            if (v)
+                while (s_seg[g + 1] <= e) ++g; // entries only move forward
+            const uint32_t slot = x[u] & (kSlots - 1);
+            const uint32_t p = (uint32_t)((uint64_t)g * chunk + (x[u] >> kSlotBits));
+            const uint32_t act = __ballot_sync(0xffffffffu, v);
+            const int lead = __ffs(act) - 1;
+            const uint32_t s_first = __shfl_sync(0xffffffffu, slot, lead);
+            if (__all_sync(0xffffffffu, !v || slot == s_first)) {
+                // one colour across the warp (flat images): one update per warp
+                const uint32_t pm = __reduce_min_sync(0xffffffffu, v ? p : 0xFFFFFFFFu);
+                if (lane == lead) {
+                    atomicAdd(&s_cnt[slot], (uint32_t)__popc(act));
+                    atomicMin(&s_min[slot], pm);
                 }
+            } else if (v) {
+                atomicAdd(&s_cnt[slot], 1u);
+                if (p < s_min[slot]) atomicMin(&s_min[slot], p); // most later occurrences skip the atomic
             }
         }
     }
@@ -535,7 +550,7 @@ static void histogram_partitioned(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P
     bucket_scan<<<1, kBuckets, 0, s>>>(bsize, bstart, border);
     CQG_CUDA(ensure_smem((const void *)part_scatter, kScatterSmem));
     part_scatter<<<G, kPartThreads, kScatterSmem, s>>>(rgb_d, P, chunk, vec, gcnt, G, bstart, ent);
-    const size_t agg_smem = sizeof(uint32_t) * 2 * kSlots;
+    const size_t agg_smem = sizeof(uint32_t) * (2 * kSlots + (size_t)G + 1);
     CQG_CUDA(ensure_smem((const void *)bucket_agg, agg_smem));
     bucket_agg<<<kBuckets, kAggThreads, agg_smem, s>>>(ent, gcnt, G, chunk, bstart, bsize, border, cnt_out, bitmap);
     launched(ctx, 5);

@@ -193,19 +193,20 @@ __global__ void __launch_bounds__(256) map_walk_kernel(const double *__restrict_
 }
 
 // Mapping NDC (metrics.cpp:36-48 + kmeans.cpp:81-105): colour i of the image's
-// distinct colours in first-occurrence order resolves with hint = LUT[colour
-// i-1] (0 for i = 0) and costs #{row entries <= 4 d2(x, c_hint)} distances.
-// "<= cut" is counted as "< nextup(cut)" (no double lies between). CODES:
-// rows as 16-bit codes in shared memory (K <= 256), FP64 only on code ties;
-// otherwise the FP64 rows through L1. Q colours per thread in flight.
+// distinct colours in first-occurrence order resolves with hint = the label of
+// colour i-1 (0 for i = 0; the sweep stored the labels in substrate order) and
+// costs #{row entries <= 4 d2(x, c_hint)} distances. "<= cut" is counted as
+// "< nextup(cut)" (no double lies between). CODES: rows as 16-bit codes in
+// shared memory (K <= 256), FP64 only on code ties; otherwise the FP64 rows
+// through L1. Q colours per thread, the next batch's loads in flight.
 template <bool CODES, int Q, int NT>
 __global__ void __launch_bounds__(NT) map_ndc_kernel(const uint32_t *__restrict__ colors, uint64_t n,
-                                                      const uint8_t *__restrict__ lut8,
-                                                      const uint32_t *__restrict__ lut32,
-                                                      const double *__restrict__ pal, int K, int Kpow,
-                                                      const double *__restrict__ rows,
-                                                      const uint16_t *__restrict__ codes,
-                                                      unsigned long long *ndc) {
+                                                     const uint8_t *__restrict__ lab8,
+                                                     const uint32_t *__restrict__ lab32,
+                                                     const double *__restrict__ pal, int K, int Kpow,
+                                                     const double *__restrict__ rows,
+                                                     const uint16_t *__restrict__ codes,
+                                                     unsigned long long *ndc) {
     extern __shared__ __align__(16) double s_pal[];
     const int rs = Kpow + 2; // code row stride: one padding word spreads rows over the banks
     uint16_t *s_code = reinterpret_cast<uint16_t *>(s_pal + 3 * K);
@@ -239,21 +240,28 @@ __global__ void __launch_bounds__(NT) map_ndc_kernel(const uint32_t *__restrict_
     }
     __syncthreads();
     unsigned long long local = 0;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * Q;
-    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x * Q; base < n; base += stride) {
+    const uint64_t stride = (uint64_t)gridDim.x * NT * Q;
+    uint32_t ncol[Q], nhint[Q];
+    auto load_batch = [&](uint64_t b) {
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const uint64_t i = b + threadIdx.x + (uint64_t)q * NT;
+            const uint64_t ic = i < n ? i : 0;
+            ncol[q] = __ldg(colors + ic);
+            nhint[q] = ic == 0 ? 0u : (lab8 ? (uint32_t)__ldg(lab8 + ic - 1) : __ldg(lab32 + ic - 1));
+        }
+    };
+    uint64_t base = (uint64_t)blockIdx.x * NT * Q;
+    if (base < n) load_batch(base);
+    for (; base < n; base += stride) {
         double cut[Q];
         uint32_t cc[Q];
         int hint[Q], pos[Q];
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
-            const uint64_t i = base + threadIdx.x + (uint64_t)q * blockDim.x;
+            const uint64_t i = base + threadIdx.x + (uint64_t)q * NT;
             const bool v = i < n;
-            const uint32_t col = v ? __ldg(colors + i) : 0u;
-            uint32_t h = 0;
-            if (v && i > 0) {
-                const uint32_t pc = __ldg(colors + i - 1);
-                h = lut8 ? (uint32_t)__ldg(lut8 + pc) : __ldg(lut32 + pc);
-            }
+            const uint32_t col = ncol[q], h = nhint[q];
             const double pd = d2_exact((double)((col >> 16) & 255u), (double)((col >> 8) & 255u),
                                        (double)(col & 255u), s_pal[3 * h], s_pal[3 * h + 1], s_pal[3 * h + 2]);
             // nextup(4 pd): the cutoff is non-negative, so the next double up is bits + 1
@@ -262,6 +270,7 @@ __global__ void __launch_bounds__(NT) map_ndc_kernel(const uint32_t *__restrict_
             hint[q] = (int)h;
             pos[q] = 0;
         }
+        if (base + stride < n) load_batch(base + stride);
         for (int step = Kpow >> 1; step >= 1; step >>= 1) {
             if (CODES) {
                 uint32_t vv[Q];
@@ -338,6 +347,11 @@ double map_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P, const uint32_t *c
     a.mom = mom;
     a.K = K;
     a.Kp = Kp;
+    if (ndc_async) { // the labels in substrate order for the mapping-NDC pass
+        void *ml = ctx->map_lab.ensure((size_t)(n + 1) * (lut8 ? 1 : 4));
+        a.maplab8 = lut8 ? static_cast<uint8_t *>(ml) : nullptr;
+        a.maplab32 = lut8 ? nullptr : static_cast<uint32_t *>(ml);
+    }
     if (pruned) {
         a.labels = const_cast<uint32_t *>(lloyd->labels); // read only in MODE_MAPW
         a.bnd = lloyd->bnd;                                  // read only in MODE_MAPW
@@ -383,7 +397,7 @@ double map_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P, const uint32_t *c
             CQG_CUDA(ensure_smem((const void *)map_ndc_kernel<true, 4, 512>, sm));
             const uint64_t g = (n + 2048 - 1) / 2048, gmax = (uint64_t)ctx->num_sms;
             map_ndc_kernel<true, 4, 512><<<(unsigned)(g < gmax ? g : gmax), 512, sm, s>>>(
-                colors_d, n, a.lut8, a.lut32, pal_d, K, Kpow, rows, crow, ndc_d);
+                colors_d, n, a.maplab8, a.maplab32, pal_d, K, Kpow, rows, crow, ndc_d);
         } else {
             // FP64 rows through L1/L2
             const size_t sm = (size_t)K * 24;
@@ -392,7 +406,7 @@ double map_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P, const uint32_t *c
             const uint64_t gmax = (uint64_t)ctx->num_sms * 8;
             if (g > gmax) g = gmax;
             map_ndc_kernel<false, 4, 256><<<(unsigned)(g ? g : 1), 256, sm, s>>>(
-                colors_d, n, a.lut8, a.lut32, pal_d, K, Kpow, rows, nullptr, ndc_d);
+                colors_d, n, a.maplab8, a.maplab32, pal_d, K, Kpow, rows, nullptr, ndc_d);
         }
         prof_end(ctx, CQG_PROF_MAPNDC, pn, (double)n);
         launched(ctx);

@@ -39,6 +39,8 @@ struct SweepArgs {
     uint32_t *labels;       // FULL/WALK: per-point label (WALK reads prev, writes new)
     uint8_t *lut8;          // MAP, K <= 256: 2^24 LUT colour -> label
     uint32_t *lut32;        // MAP, K > 256
+    uint8_t *maplab8;       // MAP: the label per distinct colour, in substrate order (K <= 256), or null
+    uint32_t *maplab32;     // MAP, K > 256
     const float *fc;        // 4*Kp floats (layout above)
     const double *cen;      // K x 3 FP64 centres
     const double *dtab;     // K x K, dist2 between centres (WALK replay)
@@ -61,6 +63,18 @@ struct SweepArgs {
     unsigned long long *swept;
     const uint16_t *dcode; // K x Kpow 16-bit monotone codes of dsorted (ndc_code_kernel), or null
 };
+
+// mapping result of distinct colour idx (colour c): the LUT the pixel pass
+// reads, and the label in substrate order the mapping-NDC pass reads
+__device__ __forceinline__ void map_store(const SweepArgs &a, uint32_t c, uint64_t idx, uint32_t label) {
+    if (a.lut8) {
+        a.lut8[c] = (uint8_t)label;
+        if (a.maplab8) a.maplab8[idx] = (uint8_t)label;
+    } else {
+        a.lut32[c] = label;
+        if (a.maplab32) a.maplab32[idx] = label;
+    }
+}
 
 __device__ __forceinline__ uint32_t lane_lt_mask() {
     uint32_t m;
@@ -620,10 +634,7 @@ __device__ __forceinline__ void sweep_tiles(const SweepArgs &a, uint64_t lo, uin
             const uint32_t r = (col[i] >> 16) & 255u, g = (col[i] >> 8) & 255u, b = col[i] & 255u;
             if (mode_delta(MODE) && valid) {
                 const int prev = kPre ? (int)plab[kPre ? i : 0] : (int)a.labels[idx];
-                if (MODE == MODE_MAPW && !flag) {
-                    if (a.lut8) a.lut8[col[i]] = (uint8_t)j1;
-                    else a.lut32[col[i]] = (uint32_t)j1;
-                }
+                if (MODE == MODE_MAPW && !flag) map_store(a, col[i], idx, (uint32_t)j1);
                 if (!flag && j1 != prev) {
                     const uint32_t cnt = kPre ? pcnt[kPre ? i : 0] : __ldg(a.counts + idx);
                     if (MODE == MODE_WALK) a.labels[idx] = (uint32_t)j1;
@@ -633,8 +644,7 @@ __device__ __forceinline__ void sweep_tiles(const SweepArgs &a, uint64_t lo, uin
             } else if (valid && !flag) {
                 const uint32_t cnt = kPre ? pcnt[kPre ? i : 0] : __ldg(a.counts + idx);
                 if (MODE == MODE_FULL) a.labels[idx] = (uint32_t)j1;
-                else if (a.lut8) a.lut8[col[i]] = (uint8_t)j1;
-                else a.lut32[col[i]] = (uint32_t)j1;
+                else map_store(a, col[i], idx, (uint32_t)j1);
                 accumulate(s_acc, a.mom, j1, cnt, r, g, b, +1);
             }
             enqueue(flag, (uint32_t)idx, a.queue, a.qn);
@@ -752,10 +762,8 @@ __device__ __forceinline__ void sweep_range(const SweepArgs &a, uint64_t lo, uin
                 const uint64_t i = i0 + threadIdx.x + (uint64_t)f * blockDim.x;
                 const bool need = i < ce && prune_needs_sweep(a, i, lab[f], bd[f], col[f], smem, s_aux, Kp, ev, smax1,
                                                               smax2, sarg, MODE == MODE_WALK);
-                if (MODE == MODE_MAPW && i < ce && !need) { // provably keeps its label under the palette
-                    if (a.lut8) a.lut8[col[f]] = (uint8_t)lab[f];
-                    else a.lut32[col[f]] = lab[f];
-                }
+                if (MODE == MODE_MAPW && i < ce && !need) // provably keeps its label under the palette
+                    map_store(a, col[f], i, lab[f]);
                 const uint32_t m = __ballot_sync(0xffffffffu, need);
                 if (m) {
                     const int leader = __ffs(m) - 1;
@@ -895,8 +903,7 @@ __device__ __forceinline__ void replay_range(const SweepArgs &a, uint32_t gwarp,
             best = bp;
             if (lane == 0) {
                 if (MODE == MODE_FULL) a.labels[idx] = (uint32_t)best;
-                else if (a.lut8) a.lut8[c] = (uint8_t)best;
-                else a.lut32[c] = (uint32_t)best;
+                else map_store(a, c, idx, (uint32_t)best);
                 if (MODE == MODE_MAPW) { // moments hold Lloyd's final labels: move the point
                     const int prev = (int)a.labels[idx];
                     if (best != prev) {
