@@ -210,6 +210,9 @@ cqg_ctx *cqg_create(int device) {
         ctx->dev_sms = prop.multiProcessorCount;
         CQG_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
         ctx->own_stream = true;
+        CQG_CUDA(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
+        CQG_CUDA(cudaEventCreateWithFlags(&ctx->aux_fork, cudaEventDisableTiming));
+        CQG_CUDA(cudaEventCreateWithFlags(&ctx->aux_join, cudaEventDisableTiming));
         const char *ng = getenv("CQG_NO_GRAPH");
         ctx->use_graphs = !(ng && ng[0] == '1');
         const char *nc = getenv("CQG_NO_CLUSTER_INIT");
@@ -261,6 +264,12 @@ void cqg_destroy(cqg_ctx *ctx) {
     ctx->pinned_nu.release();
     for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+    if (ctx->aux) {
+        cudaStreamSynchronize(ctx->aux);
+        cudaStreamDestroy(ctx->aux);
+        cudaEventDestroy(ctx->aux_fork);
+        cudaEventDestroy(ctx->aux_join);
+    }
     delete ctx;
 }
 

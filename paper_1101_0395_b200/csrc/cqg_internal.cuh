@@ -108,6 +108,8 @@ struct cqg_ctx {
     int dev_sms = 148;     // the device's SMs (size limits of the persistent kernel)
     cudaStream_t stream = nullptr;
     bool own_stream = false;
+    cudaStream_t aux = nullptr;            // side stream for independent work (mapping NDC)
+    cudaEvent_t aux_fork = nullptr, aux_join = nullptr;
     unsigned long long launches = 0;
 
     // stage 1 scratch

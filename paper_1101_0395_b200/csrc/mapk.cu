@@ -363,12 +363,17 @@ double map_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P, const uint32_t *c
         launch_sweep(ctx, MODE_MAP, a);
     }
 
-    if ((size_t)K * 8 > 48 * 1024)
-        CQG_CUDA(ensure_smem((const void *)mse_kernel, K * 8));
-    mse_kernel<<<1, 256, (size_t)K * 8, s>>>(mom, pal_d, K, P, mse_d);
-    launched(ctx);
-
-    if (ndc_async) { // MappingResult::ndc
+    bool ndc_pending = false;
+    if (ndc_async) { // MappingResult::ndc, on the side stream beside the MSE and the pixel pass
+        CQG_CUDA(cudaEventRecord(ctx->aux_fork, s));
+        CQG_CUDA(cudaStreamWaitEvent(ctx->aux, ctx->aux_fork, 0));
+        struct SideStream { // launches and profiling events below go to the side stream
+            cqg_ctx *c;
+            cudaStream_t main;
+            ~SideStream() { c->stream = main; }
+        } side{ctx, s};
+        s = ctx->aux;
+        ctx->stream = ctx->aux;
         int Kpow = 1;
         while (Kpow < K) Kpow <<= 1;
         CQG_CUDA(cudaMemsetAsync(ndc_d, 0, 8, s));
@@ -411,7 +416,15 @@ double map_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P, const uint32_t *c
         prof_end(ctx, CQG_PROF_MAPNDC, pn, (double)n);
         launched(ctx);
         CQG_CUDA(cudaMemcpyAsync(ndc_async, ndc_d, 8, cudaMemcpyDeviceToHost, s));
+        CQG_CUDA(cudaEventRecord(ctx->aux_join, s));
+        s = side.main;
+        ndc_pending = true;
     }
+
+    if ((size_t)K * 8 > 48 * 1024)
+        CQG_CUDA(ensure_smem((const void *)mse_kernel, K * 8));
+    mse_kernel<<<1, 256, (size_t)K * 8, s>>>(mom, pal_d, K, P, mse_d);
+    launched(ctx);
 
     if (indices_d || quant_d) {
         const int vec = ((reinterpret_cast<uintptr_t>(rgb_d) | reinterpret_cast<uintptr_t>(indices_d) |
@@ -436,6 +449,7 @@ double map_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P, const uint32_t *c
                  (double)P * (3.0 + (indices_d ? (double)index_bytes : 0.0) + (quant_d ? 3.0 : 0.0)));
         launched(ctx);
     }
+    if (ndc_pending) CQG_CUDA(cudaStreamWaitEvent(s, ctx->aux_join, 0)); // join the side stream
     CQG_CUDA(cudaGetLastError());
     if (mse_async) { // the caller reads *mse_async after its own synchronisation
         CQG_CUDA(cudaMemcpyAsync(mse_async, mse_d, 8, cudaMemcpyDeviceToHost, s));

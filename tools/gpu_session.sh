@@ -1,7 +1,7 @@
 mkdir -p gpurun_out
-timeout 300 python tools/hist_timing.py cfg3 cfg5 > gpurun_out/r2_hist.log 2>&1; echo "hist rc=$?"
-cat gpurun_out/r2_hist.log | tail -8
-timeout 600 python -m pytest tests/test_gpu_parity.py -k histogram -q -x > gpurun_out/r2_t6.log 2>&1; echo "tests rc=$?"
-tail -3 gpurun_out/r2_t6.log
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r2_hist_ncu3.csv python tools/hist_timing.py cfg3 > /dev/null 2>&1
-python tools/ncu_csv.py gpurun_out/r2_hist_ncu3.csv 2>/dev/null | tail -10
+timeout 900 python -m pytest tests/test_gpu_prune.py tests/test_gpu_parity.py tests/test_gpu_batch.py -q -x > gpurun_out/r2_t7.log 2>&1; echo "tests rc=$?"
+tail -5 gpurun_out/r2_t7.log
+for i in 1 2; do timeout 300 python bench.py --no-by-config --no-cpu-baseline > gpurun_out/r2_bench_cfg2c.json 2> gpurun_out/r2_bench_cfg2c.err; echo "bench rc=$?"
+python -c "
+import json; d=json.loads(open('gpurun_out/r2_bench_cfg2c.json').read().strip().splitlines()[-1])
+print(d['value'], d['e2e']['value'], d['stage_ms_last_step'], {k:round(v['ms_per_step'],4) for k,v in d['kernels'].items()}, d['parity']['ok'])"; done
