@@ -1,7 +1,8 @@
-mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_prune.py tests/test_gpu_parity.py tests/test_gpu_batch.py -q -x > gpurun_out/r2_t7.log 2>&1; echo "tests rc=$?"
-tail -5 gpurun_out/r2_t7.log
-for i in 1 2; do timeout 300 python bench.py --no-by-config --no-cpu-baseline > gpurun_out/r2_bench_cfg2c.json 2> gpurun_out/r2_bench_cfg2c.err; echo "bench rc=$?"
-python -c "
-import json; d=json.loads(open('gpurun_out/r2_bench_cfg2c.json').read().strip().splitlines()[-1])
-print(d['value'], d['e2e']['value'], d['stage_ms_last_step'], {k:round(v['ms_per_step'],4) for k,v in d['kernels'].items()}, d['parity']['ok'])"; done
+mkdir -p gpurun_out/sanitize
+timeout 300 python tools/sanitize_run.py 2>&1 | tail -3
+for tool in memcheck racecheck synccheck initcheck; do
+  start=$(date +%s)
+  timeout 900 compute-sanitizer --tool $tool --error-exitcode 99 python tools/sanitize_run.py > gpurun_out/sanitize/${tool}_default.log 2>&1
+  rc=$?
+  echo "$tool rc=$rc $(( $(date +%s) - start ))s $(grep -E 'ERROR SUMMARY|RACECHECK SUMMARY|all checks passed|FAILURES' gpurun_out/sanitize/${tool}_default.log | tr '\n' ' ')"
+done
