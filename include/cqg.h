@@ -222,6 +222,14 @@ int cqg_shard_begin(cqg_ctx *ctx, const uint32_t *colors, const uint32_t *counts
 int cqg_shard_assign(cqg_ctx *ctx, int64_t *partial);
 int cqg_shard_moments(cqg_ctx *ctx, int64_t *partial);
 int cqg_shard_finalize(cqg_ctx *ctx, const int64_t *global, int *state, double *sse);
+/* The same without a host round trip (global: device memory): the state is
+ * logged on the device and the next cqg_shard_assign walks as if the run went
+ * on. cqg_shard_status reads the log once: *state 0 = every logged iteration
+ * continued, 1 = the last one finished the run, 2 = an empty cluster or an
+ * early stop occurred (redo the run with cqg_shard_finalize). For fixed
+ * iteration counts (BASELINE cfg5) the loop needs no per-iteration sync. */
+int cqg_shard_finalize_async(cqg_ctx *ctx, const int64_t *global);
+int cqg_shard_status(cqg_ctx *ctx, int *state, int *iterations);
 /* repair protocol helpers (kmeans.cpp:124-169 across ranks) */
 int cqg_shard_sizes(cqg_ctx *ctx, uint32_t *sizes);
 int cqg_shard_donor(cqg_ctx *ctx, const uint32_t *global_sizes, int fallback, double *value,

@@ -36,7 +36,7 @@ EXPORTS = (
     "cqg_map", "cqg_coarse_histogram", "cqg_coarse_histogram_weighted", "cqg_quantize", "cqg_set_profiling",
     "cqg_read_profile", "cqg_bench_sweep",
     "cqg_shard_begin", "cqg_shard_assign", "cqg_shard_moments", "cqg_shard_finalize", "cqg_shard_sizes",
-    "cqg_shard_donor", "cqg_shard_move", "cqg_shard_end",
+    "cqg_shard_donor", "cqg_shard_move", "cqg_shard_end", "cqg_shard_finalize_async", "cqg_shard_status",
     "cqg_lloyd_exact", "cqg_compute_sse", "cqg_repair_empty_clusters", "cqg_center_table",
     "cqg_kmeanspp_next_masses", "cqg_maximin_pad",
 )
@@ -128,6 +128,10 @@ def load(path: str = LIB_PATH):
         L.cqg_shard_moments.argtypes = [vp, vp]
         L.cqg_shard_finalize.argtypes = [vp, vp, C.POINTER(i32), C.POINTER(C.c_double)]
         L.cqg_shard_sizes.argtypes = [vp, vp]
+        L.cqg_shard_finalize_async.argtypes = [vp, vp]
+        L.cqg_shard_finalize_async.restype = i32
+        L.cqg_shard_status.argtypes = [vp, C.POINTER(i32), C.POINTER(i32)]
+        L.cqg_shard_status.restype = i32
         L.cqg_shard_donor.argtypes = [vp, vp, i32, C.POINTER(C.c_double), C.POINTER(u64),
                                       C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]
         L.cqg_shard_move.argtypes = [vp, u64, i32, C.c_uint32]

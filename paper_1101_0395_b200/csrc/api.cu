@@ -256,7 +256,7 @@ void cqg_destroy(cqg_ctx *ctx) {
                       &ctx->dtab, &ctx->dsorted, &ctx->order, &ctx->mom, &ctx->queue, &ctx->ndc,
                       &ctx->status, &ctx->sizes, &ctx->red, &ctx->hist_labels, &ctx->hist_centers,
                       &ctx->sse, &ctx->lut, &ctx->idx_out, &ctx->q_out, &ctx->mom_map, &ctx->coarse, &ctx->mind2,
-                      &ctx->initpart, &ctx->initsel, &ctx->unit_draws, &ctx->inittile, &ctx->mom_g, &ctx->partial,
+                      &ctx->initpart, &ctx->initsel, &ctx->unit_draws, &ctx->inittile, &ctx->mom_g, &ctx->partial, &ctx->shard_log,
                       &ctx->bnd, &ctx->shift, &ctx->dcode, &ctx->sub_img, &ctx->raw_col, &ctx->raw_cnt,
                       &ctx->full_col, &ctx->full_cnt, &ctx->map_rows, &ctx->map_lab, &ctx->pcnt, &ctx->pent, &ctx->pseg};
     for (DevBuf *b : bufs) b->release();
@@ -606,6 +606,22 @@ int cqg_shard_finalize(cqg_ctx *ctx, const int64_t *global, int *state, double *
         const size_t bytes = 8 * (5 * (size_t)shard_k(ctx) + 2);
         const long long *g = static_cast<const long long *>(stage_in(ctx, global, bytes, ctx->partial));
         const int st = shard_finalize_dev(ctx, g, sse);
+        if (state) *state = st;
+    });
+}
+
+int cqg_shard_finalize_async(cqg_ctx *ctx, const int64_t *global) {
+    return guarded([&] {
+        use_device(ctx);
+        if (!is_device_ptr(global)) fail(CQG_E_INVALID, "cqg_shard_finalize_async: global must be device memory");
+        shard_finalize_async_dev(ctx, reinterpret_cast<const long long *>(global));
+    });
+}
+
+int cqg_shard_status(cqg_ctx *ctx, int *state, int *iterations) {
+    return guarded([&] {
+        use_device(ctx);
+        const int st = shard_status_dev(ctx, iterations);
         if (state) *state = st;
     });
 }

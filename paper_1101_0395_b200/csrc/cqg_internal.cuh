@@ -127,7 +127,7 @@ struct cqg_ctx {
     cqg::DevBuf hist_labels, hist_centers, sse;
     cqg::DevBuf bnd, shift, dcode;
     cqg::DevBuf sub_img, raw_col, raw_cnt, full_col, full_cnt; // sampling modes     // distance-bound pruning: per-point (ub, lb), centre moves
-    cqg::DevBuf mom_g, partial; // sharded Lloyd: global moments, packed partials
+    cqg::DevBuf mom_g, partial, shard_log; // sharded Lloyd: global moments, packed partials, state log
     void *shard = nullptr;      // cqg::ShardState (lloyd.cu)
     // mapping
     cqg::DevBuf lut, idx_out, q_out, mom_map, map_rows, map_lab;
@@ -292,6 +292,8 @@ void shard_begin_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *cou
                      const double *init_d, int K, const cqg_term &term);
 void shard_assign_dev(cqg_ctx *ctx, long long *partial_d, bool run);
 int shard_finalize_dev(cqg_ctx *ctx, const long long *global_d, double *sse);
+void shard_finalize_async_dev(cqg_ctx *ctx, const long long *global_d);
+int shard_status_dev(cqg_ctx *ctx, int *iterations);
 void shard_sizes_dev(cqg_ctx *ctx, uint32_t *sizes_d);
 void shard_donor_dev(cqg_ctx *ctx, const uint32_t *gsizes_d, int fallback, double *value, uint64_t *index,
                      uint32_t *colour, uint32_t *label);

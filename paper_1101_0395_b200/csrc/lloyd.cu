@@ -1144,6 +1144,8 @@ struct ShardState {
     IterArgs ia;
     uint64_t n = 0, P = 0;
     int K = 0, iter = 0, limit = 0;
+    int pending = 0;        // iterations finalised without a host read (cqg_shard_finalize_async)
+    int32_t *slog = nullptr; // device log: the state of each pending iteration
 };
 
 namespace {
@@ -1296,6 +1298,41 @@ void shard_assign_dev(cqg_ctx *ctx, long long *partial_d, bool run) {
     CQG_CUDA(cudaGetLastError());
 }
 
+
+// Finalise without a host synchronisation: the iteration's state is appended
+// to a device log and the host assumes "continue" (iter + 1). shard_status_dev
+// reads the log once: a fixed-iteration run needs no per-iteration round trip.
+void shard_finalize_async_dev(cqg_ctx *ctx, const long long *global_d) {
+    ShardState &S = shard_state(ctx);
+    cudaStream_t s = ctx->stream;
+    if (!S.slog) S.slog = static_cast<int32_t *>(ctx->shard_log.ensure(sizeof(int32_t) * 4096));
+    if (S.pending >= 4096) fail(CQG_E_INVALID, "cqg_shard_finalize_async: more than 4096 pending iterations");
+    CQG_CUDA(cudaMemcpyAsync(S.ia.mom, global_d, sizeof(Moments) * (size_t)S.K, cudaMemcpyDeviceToDevice, s));
+    launch_iter_end(ctx, S.ia);
+    CQG_CUDA(cudaMemcpyAsync(S.slog + S.pending, &S.ia.st->state, sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+    ++S.pending;
+    ++S.iter; // the next assignment walks (WALK mode) unless the log says otherwise
+}
+
+// 0: every pending iteration continued, 1: the last one finished and none
+// before it stopped, 2: some iteration hit an empty cluster or stopped early
+// (the run must be redone with the synchronous protocol)
+int shard_status_dev(cqg_ctx *ctx, int *iterations) {
+    ShardState &S = shard_state(ctx);
+    int result = 0;
+    if (S.pending) {
+        std::vector<int32_t> h(S.pending);
+        CQG_CUDA(cudaMemcpyAsync(h.data(), S.slog, sizeof(int32_t) * S.pending, cudaMemcpyDeviceToHost, ctx->stream));
+        CQG_CUDA(cudaStreamSynchronize(ctx->stream));
+        for (int i = 0; i < S.pending; ++i) {
+            if (h[i] == 2 || (h[i] == 1 && i + 1 < S.pending)) result = 2;
+            else if (h[i] == 1 && result == 0) result = 1;
+        }
+        S.pending = 0;
+    }
+    if (iterations) *iterations = S.iter;
+    return result;
+}
 
 int shard_finalize_dev(cqg_ctx *ctx, const long long *global_d, double *sse) {
     ShardState &S = shard_state(ctx);

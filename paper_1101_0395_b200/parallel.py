@@ -75,6 +75,16 @@ class CudaShardEngine:
         cabi.check(self.ctx.L.cqg_shard_finalize(self.ctx.h, glob.data_ptr(), C.byref(st), C.byref(sse)))
         return st.value, sse.value
 
+    def finalize_async(self, glob):
+        """Finalise without a host read (the state is logged on the device)."""
+        cabi.check(self.ctx.L.cqg_shard_finalize_async(self.ctx.h, glob.data_ptr()))
+
+    def status(self):
+        """(0 continue | 1 done | 2 redo synchronously, iterations) of the logged run."""
+        st, it = C.c_int(0), C.c_int(0)
+        cabi.check(self.ctx.L.cqg_shard_status(self.ctx.h, C.byref(st), C.byref(it)))
+        return st.value, it.value
+
     def sizes(self):
         t = self.torch.empty(self.K, dtype=self.torch.int32, device=self.device)
         cabi.check(self.ctx.L.cqg_shard_sizes(self.ctx.h, t.data_ptr()))
@@ -168,6 +178,26 @@ def sharded_wsm(engine, colors, counts, P: int, init, K: int, term: cabi.Term, g
     n = len(colors)
     lo, hi = shard_bounds(n, world, rank)
     engine.begin(colors[lo:hi], counts[lo:hi], P, init, K, term)
+    if term.fixed_iterations > 0 and hasattr(engine, "finalize_async"):
+        # a fixed iteration count needs no per-iteration host round trip: the
+        # moments allreduce and every rank's finalise stay on the device (NCCL
+        # is ordered on the stream), the states are checked once at the end;
+        # an empty cluster (or an early stop) sends the run to the protocol below
+        acc = None
+        for _ in range(term.fixed_iterations):
+            part = engine.assign()
+            dist.all_reduce(part, group=group)
+            cnt = part[5 * K:5 * K + 2].clone()
+            acc = cnt if acc is None else acc + cnt
+            engine.finalize_async(part)
+        state, _ = engine.status()
+        ok = torch.tensor([1 if state == STATE_DONE else 0], dtype=torch.int32, device=part.device)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+        if int(ok.item()) == 1:
+            cen, lab, sse, it = engine.end(term.fixed_iterations, labels)
+            tot = acc.cpu().tolist()
+            return ShardedResult(cen, lab, lo, hi, sse, it, int(tot[0]), 0, int(tot[1]))
+        engine.begin(colors[lo:hi], counts[lo:hi], P, init, K, term)
     ndc, flagged, repairs = 0, 0, 0
     while True:
         part = engine.assign()

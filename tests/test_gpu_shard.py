@@ -100,3 +100,58 @@ def test_sharded_wsm_nccl_single_rank(oracle):
         assert np.array_equal(r.labels_local, ref.labels)
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("adv", [False, True])
+def test_sharded_wsm_fixed_iterations_no_host_sync(oracle, adv):
+    # fixed iteration counts (BASELINE cfg5) take the asynchronous path: the
+    # states are logged on the device and read once; an empty cluster (the
+    # adversarial init) sends the run to the synchronous repair protocol
+    import torch
+    import torch.distributed as dist
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        colors, counts, P, init = case(oracle, 21, 24, adversarial=adv)
+        ref = oracle.wsm(colors, counts, P, init, fixed_it=12, mode=UPDATE_EXACT)
+        eng = parallel.CudaShardEngine(cabi.Context(0), torch.device("cuda", 0))
+        r = parallel.sharded_wsm(eng, colors, counts, P, init, 24, cabi.Term(1e-3, 100, 12, 0))
+        assert r.iterations == 12 == ref.iterations
+        assert r.ndc_total == ref.ndc_total and r.repair_count == ref.repairs
+        assert np.array_equal(r.centers, ref.centers)
+        assert np.array_equal(r.sse_trace.view(np.uint64), ref.sse_trace.view(np.uint64))
+        assert np.array_equal(r.labels_local, ref.labels)
+        if adv:
+            assert ref.repairs > 0
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_shards_async_finalize(oracle):
+    # two engines in lockstep, every finalise without a host read
+    import torch
+    colors, counts, P, init = case(oracle, 31, 40)
+    ref = oracle.wsm(colors, counts, P, init, fixed_it=9, mode=UPDATE_EXACT)
+    n = colors.size
+    slices = [parallel.shard_bounds(n, 2, r) for r in range(2)]
+    engines = [parallel.CudaShardEngine(cabi.Context(0), torch.device("cuda", 0)) for _ in range(2)]
+    term = cabi.Term(1e-3, 100, 9, 0)
+    for e, (lo, hi) in zip(engines, slices):
+        e.begin(colors[lo:hi], counts[lo:hi], P, init, 40, term)
+    ndc = 0
+    for _ in range(9):
+        glob = sum(e.assign().cpu() for e in engines).cuda()
+        ndc += int(glob[5 * 40])
+        for e in engines:
+            e.finalize_async(glob)
+    assert all(e.status()[0] == parallel.STATE_DONE for e in engines)
+    outs = [e.end(9) for e in engines]
+    for cen, lab, sse, it in outs:
+        assert it == 9 and np.array_equal(cen, ref.centers)
+    assert np.array_equal(np.concatenate([o[1] for o in outs]), ref.labels)
+    assert ndc == ref.ndc_total

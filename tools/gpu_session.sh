@@ -1,8 +1,5 @@
-mkdir -p gpurun_out/sanitize
-timeout 300 python tools/sanitize_run.py 2>&1 | tail -3
-for tool in memcheck racecheck synccheck initcheck; do
-  start=$(date +%s)
-  timeout 900 compute-sanitizer --tool $tool --error-exitcode 99 python tools/sanitize_run.py > gpurun_out/sanitize/${tool}_default.log 2>&1
-  rc=$?
-  echo "$tool rc=$rc $(( $(date +%s) - start ))s $(grep -E 'ERROR SUMMARY|RACECHECK SUMMARY|all checks passed|FAILURES' gpurun_out/sanitize/${tool}_default.log | tr '\n' ' ')"
-done
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_shard.py tests/test_gpu_parity.py -q -x > gpurun_out/r2_t8.log 2>&1; echo "tests rc=$?"
+tail -15 gpurun_out/r2_t8.log
+timeout 600 python bench.py --config cfg5 --sharded --steps 3 > gpurun_out/r2_sharded5.json 2>gpurun_out/r2_sharded5.err; echo "sharded rc=$?"
+tail -c 1200 gpurun_out/r2_sharded5.json; tail -3 gpurun_out/r2_sharded5.err
