@@ -563,9 +563,8 @@ def measure(args, cfg, env, steps, warmup, e2e_on=True, parity_on=True):
     if world > 1:
         dist.barrier()
 
-    for c in ctxs:
-        c.set_profiling(True)
-        c.read_profile(reset=True)
+    # timed steps: the library as a user runs it (no kernel-level profiling
+    # events between its kernels)
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     step_ms, all_stats = [], []
@@ -581,6 +580,18 @@ def measure(args, cfg, env, steps, warmup, e2e_on=True, parity_on=True):
             step_ms.append(ev0.elapsed_time(ev1))
             all_stats.append(st)
     gpu_launches = sum(c.launches for c in ctxs) - launches0
+    # then the per-kernel profile (CUDA events around the library's kernels on
+    # its stream) over separate, untimed steps
+    prof_steps = min(steps, 5)
+    for c in ctxs:
+        c.set_profiling(True)
+        c.read_profile(reset=True)
+    prof_stats = []
+    for s in range(prof_steps):
+        flush.fill_(s & 255)
+        torch.cuda.synchronize()
+        prof_stats.append(step_device())
+        torch.cuda.synchronize()
     profs = [c.read_profile(reset=True) for c in ctxs]
     prof = profs[0]
     for extra in profs[1:]:
@@ -603,8 +614,9 @@ def measure(args, cfg, env, steps, warmup, e2e_on=True, parity_on=True):
     value = pixels_per_step_all / (ms_per_step / 1e3) / 1e6
 
     # Lloyd distances/s (full-sweep equivalent N'.K.iters over Lloyd device time)
-    dist_n = sum(s.n_unique * k * s.lloyd.iterations for st in all_stats for s, k in zip(st, ks))
-    lloyd_ms = sum(s.ms_lloyd for st in all_stats for s in st)
+    # (stage times come from the profiled steps: the timed ones record no stage events)
+    dist_n = sum(s.n_unique * k * s.lloyd.iterations for st in prof_stats for s, k in zip(st, ks))
+    lloyd_ms = sum(s.ms_lloyd for st in prof_stats for s in st)
     lloyd_rate = dist_n / (lloyd_ms / 1e3) if lloyd_ms > 0 else None
     if world > 1:
         v = torch.tensor([lloyd_rate or 0.0], dtype=torch.float64, device=dev)
@@ -622,8 +634,8 @@ def measure(args, cfg, env, steps, warmup, e2e_on=True, parity_on=True):
     names = ["sweep", "map_sweep", "histogram", "pixel_map", "init", "replay", "ndc", "lloyd_loop", "map_ndc"]
     stage_share = {}
     for i, nm in enumerate(names):
-        stage_share[nm] = {"ms_per_step": prof.ms[i] / steps,
-                           "launches_per_step": prof.launches[i] / steps}
+        stage_share[nm] = {"ms_per_step": prof.ms[i] / prof_steps,
+                           "launches_per_step": prof.launches[i] / prof_steps}
     iso_ms, iso_units = ctx.bench_sweep(20)
     iso_achieved = 8.0 * iso_units / (iso_ms / 1e3) / 1e12
     persistent = prof.launches[cabi.PROF_SWEEP] == 0 and prof.launches[cabi.PROF_LLOYD] > 0
@@ -640,14 +652,14 @@ def measure(args, cfg, env, steps, warmup, e2e_on=True, parity_on=True):
         k_ms = prof.ms[cabi.PROF_LLOYD] / max(int(prof.launches[cabi.PROF_LLOYD]), 1)
         achieved = 8.0 * prof.units[cabi.PROF_LLOYD] / (prof.ms[cabi.PROF_LLOYD] / 1e3) / 1e12
         achieved_actual = 8.0 * actual_units / (prof.ms[cabi.PROF_LLOYD] / 1e3) / 1e12
-        k_share = prof.ms[cabi.PROF_LLOYD] / steps / ms_per_step
+        k_share = prof.ms[cabi.PROF_LLOYD] / prof_steps / ms_per_step
     else:
         kname = "sweep_kernel<WALK> (Lloyd assignment, one launch per iteration)"
         k_ms = iso_ms
         achieved = iso_achieved
         achieved_actual = iso_achieved
         iters_all = sum(s.lloyd.iterations for st in all_stats for s in st)
-        k_share = iso_ms * iters_all / steps / ms_per_step
+        k_share = iso_ms * iters_all / steps / ms_per_step  # iterations summed over the timed steps
     traffic = None
     tpath = os.path.join(ROOT, "profiles", f"ncu_traffic_{cfg.name}.json")
     if os.path.exists(tpath):
@@ -670,7 +682,7 @@ def measure(args, cfg, env, steps, warmup, e2e_on=True, parity_on=True):
     }
     # the kernel with the largest device-time share, when it is not the Lloyd kernel
     dominant = None
-    share = {nm: prof.ms[i] / steps / ms_per_step for i, nm in enumerate(names)}
+    share = {nm: prof.ms[i] / prof_steps / ms_per_step for i, nm in enumerate(names)}
     top = max(share, key=share.get)
     if top == "init" and share["init"] > k_share:
         K0 = ks[0]
@@ -698,14 +710,14 @@ def measure(args, cfg, env, steps, warmup, e2e_on=True, parity_on=True):
     pix_ms = prof.ms[cabi.PROF_PIXEL]
     hbm = peaks.get("hbm_gbs", 6545.6)
     n_unique = all_stats[-1][0].n_unique
-    hist_gbs = ((prof.units[cabi.PROF_HIST] + 8.0 * n_unique * steps * len(imgs)) / (hist_ms / 1e3) / 1e9
+    hist_gbs = ((prof.units[cabi.PROF_HIST] + 8.0 * n_unique * prof_steps * len(imgs)) / (hist_ms / 1e3) / 1e9
                 if hist_ms else None)
     pix_gbs = prof.units[cabi.PROF_PIXEL] / (pix_ms / 1e3) / 1e9 if pix_ms else None
     byte_kernels = {  # algorithmic bytes: histogram 3P + 8N', pixel map 3P in + 7P out
         "histogram": {"achieved_gbs": hist_gbs, "peak_gbs": hbm, "frac": hist_gbs / hbm if hist_gbs else None,
-                      "ms_per_step": hist_ms / steps},
+                      "ms_per_step": hist_ms / prof_steps},
         "pixel_map": {"achieved_gbs": pix_gbs, "peak_gbs": hbm, "frac": pix_gbs / hbm if pix_gbs else None,
-                      "ms_per_step": pix_ms / steps},
+                      "ms_per_step": pix_ms / prof_steps},
     }
 
     # end-to-end through the C-ABI with pinned HOST buffers (H2D + D2H inside the timed region)
@@ -764,8 +776,9 @@ def measure(args, cfg, env, steps, warmup, e2e_on=True, parity_on=True):
             "n_unique": int(st0.n_unique), "iterations": int(st0.lloyd.iterations),
             "flagged_per_step": int(st0.lloyd.flagged_total),
             "swept_fraction": swept / pt_iters if pt_iters else None,
-            "stage_ms_last_step": {"histogram": st0.ms_histogram, "init": st0.ms_init,
-                                   "lloyd": st0.ms_lloyd, "map": st0.ms_map},
+            "stage_ms_last_step": {"histogram": prof_stats[-1][0].ms_histogram, "init": prof_stats[-1][0].ms_init,
+                                   "lloyd": prof_stats[-1][0].ms_lloyd, "map": prof_stats[-1][0].ms_map,
+                                   "note": "from a profiled step (stage events), not a timed one"},
             "kernels": stage_share, "byte_kernels": byte_kernels,
             "roofline": roofline, "dominant_kernel": dominant, "cpu_baseline": None, "e2e": e2e,
             "gpu_launches": int(gpu_launches), "clocks": clocks, "parity": parity,

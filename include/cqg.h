@@ -104,7 +104,8 @@ typedef struct {
     cqg_lloyd_stats lloyd;
     double mean_sq_dist; /* QuantReport::mse (pipeline.cpp:155) */
     uint64_t map_ndc;    /* MappingResult::ndc (metrics.cpp:36-48): distances the reference's pruned lookup evaluates */
-    double ms_histogram, ms_init, ms_lloyd, ms_map; /* device time per stage (CUDA events) */
+    double ms_histogram, ms_init, ms_lloyd, ms_map; /* device time per stage (CUDA events), filled when
+                                                      kernel profiling is on (cqg_set_profiling), else 0 */
 } cqg_quantize_stats;
 
 /* ---- context ------------------------------------------------------------ */

@@ -60,14 +60,16 @@ void validate_pixels(uint64_t P, const char *who) {
 
 struct Timer {
     // stage boundaries as events on the stream, read after the pipeline's own
-    // final synchronisation (no host synchronisation between stages)
+    // final synchronisation (no host synchronisation between stages); the
+    // events belong to the context (created once, not per call)
     cqg_ctx *ctx;
     bool on;
-    cudaEvent_t ev[8];
+    cudaEvent_t *ev;
     int n = 0;
-    Timer(cqg_ctx *c, bool enable) : ctx(c), on(enable) {
+    Timer(cqg_ctx *c, bool enable) : ctx(c), on(enable), ev(c->stage_ev) {
         if (on) {
-            for (auto &e : ev) cudaEventCreate(&e);
+            if (!ev[0])
+                for (int i = 0; i < 8; ++i) cudaEventCreate(&ev[i]);
             cudaEventRecord(ev[n++], ctx->stream);
         }
     }
@@ -82,10 +84,7 @@ struct Timer {
         cudaEventElapsedTime(&t, ev[i - 1], ev[i]);
         return t;
     }
-    ~Timer() {
-        if (on)
-            for (auto &e : ev) cudaEventDestroy(e);
-    }
+    ~Timer() = default;
 };
 
 } // namespace
@@ -264,6 +263,8 @@ void cqg_destroy(cqg_ctx *ctx) {
     ctx->pinned_nu.release();
     for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+    for (cudaEvent_t e : ctx->stage_ev)
+        if (e) cudaEventDestroy(e);
     if (ctx->aux) {
         cudaStreamSynchronize(ctx->aux);
         cudaStreamDestroy(ctx->aux);
@@ -765,7 +766,7 @@ int cqg_quantize(cqg_ctx *ctx, const uint8_t *rgb, uint64_t P, const cqg_quantiz
         const bool dedup = mode == CQG_SAMPLING_UNIQUE || mode == CQG_SAMPLING_BOTH;   // pipeline.cpp:93-94
         if (sub && (cfg->width < 1 || cfg->height < 1 || (uint64_t)cfg->width * cfg->height != P))
             fail(CQG_E_INVALID, "run_quantize: 2:1 sampling needs width * height == pixel count");
-        Timer tm(ctx, stats != nullptr);
+        Timer tm(ctx, stats != nullptr && ctx->prof_on); // stage events only when profiling
         const uint8_t *rgb_d = static_cast<const uint8_t *>(stage_in(ctx, rgb, P * 3, ctx->img));
         // the sampled pixels (S of them) and their histogram (initialisers, dedup substrate)
         const uint8_t *smp_d = rgb_d;
@@ -870,7 +871,7 @@ int cqg_quantize(cqg_ctx *ctx, const uint8_t *rgb, uint64_t P, const cqg_quantiz
             stats->lloyd.swept_total = o.swept;
             stats->mean_sq_dist = mse;
             stats->map_ndc = *mndc_h;
-            CQG_CUDA(cudaEventSynchronize(tm.ev[t_map]));
+            if (tm.on) CQG_CUDA(cudaEventSynchronize(tm.ev[t_map]));
             stats->ms_histogram = tm.ms(t_hist);
             stats->ms_init = tm.ms(t_init);
             stats->ms_lloyd = tm.ms(t_lloyd);

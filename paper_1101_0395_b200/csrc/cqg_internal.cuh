@@ -110,6 +110,7 @@ struct cqg_ctx {
     bool own_stream = false;
     cudaStream_t aux = nullptr;            // side stream for independent work (mapping NDC)
     cudaEvent_t aux_fork = nullptr, aux_join = nullptr;
+    cudaEvent_t stage_ev[8] = {}; // cqg_quantize stage timing (created once per context)
     unsigned long long launches = 0;
 
     // stage 1 scratch
@@ -203,6 +204,29 @@ __device__ __forceinline__ double cluster_sse_exact(unsigned long long n, const 
                                  (unsigned __int128)((__int128)s[1] * s[1]) +
                                  (unsigned __int128)((__int128)s[2] * s[2]);
     return __ddiv_rn(u128_to_double(nq - ss), __ull2double_rn(n));
+}
+
+// Programmatic dependent launch: a kernel launched with launch_pdl starts
+// while the previous kernel on the stream drains and waits here for its
+// results (a no-op without the launch attribute)
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// let the next kernel on the stream launch now (its blocks wait in pdl_wait
+// until this grid has completed and its memory is visible)
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CQG_CUDA(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
 }
 
 __host__ __device__ __forceinline__ unsigned ceil_div(unsigned long long a, unsigned long long b) {

@@ -70,6 +70,7 @@ __device__ __forceinline__ void append(bool isnew, uint32_t c, uint32_t *list, u
 __global__ void __launch_bounds__(kThreads) hist_count_fused(const uint8_t *__restrict__ rgb, uint64_t P,
                                                             uint2 *__restrict__ tab, uint32_t *__restrict__ list,
                                                             uint32_t *__restrict__ list_n, int aligned) {
+    pdl_trigger();
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const uint64_t groups = aligned ? P / 16 : 0;
@@ -97,6 +98,8 @@ __global__ void __launch_bounds__(kThreads) hist_count_fused(const uint8_t *__re
 
 __global__ void hist_mark_fused(const uint32_t *__restrict__ list, const uint32_t *__restrict__ list_n,
                                 const uint2 *__restrict__ tab, uint32_t *__restrict__ bitmap) {
+    pdl_wait();
+    pdl_trigger();
     const uint32_t n = *list_n;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const uint32_t f = ~tab[list[i]].y;
@@ -109,6 +112,8 @@ __global__ void hist_emit_fused(const uint32_t *__restrict__ list, const uint32_
                                 uint2 *__restrict__ tab, const uint32_t *__restrict__ bitmap,
                                 const uint32_t *__restrict__ wpref, uint32_t *__restrict__ colors,
                                 uint32_t *__restrict__ counts, uint32_t *__restrict__ first) {
+    pdl_wait();
+    pdl_trigger();
     const uint32_t n = *list_n;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const uint32_t c = list[i];
@@ -132,6 +137,8 @@ __global__ void __launch_bounds__(kThreads) hist_emit(const uint8_t *__restrict_
                                                      const uint32_t *__restrict__ cnt,
                                                      uint32_t *__restrict__ colors, uint32_t *__restrict__ counts,
                                                      uint32_t *__restrict__ first) {
+    pdl_wait();
+    pdl_trigger();
     for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < P;
          p += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t w = p >> 5;
@@ -189,6 +196,7 @@ __device__ __forceinline__ void decode_group(const uint8_t *rgb, uint64_t p0, in
 
 __global__ void __launch_bounds__(kPartThreads) part_count(const uint8_t *__restrict__ rgb, uint64_t P, uint64_t chunk,
                                                            int vec, uint32_t *__restrict__ gcnt, int G) {
+    pdl_trigger();
     __shared__ uint32_t s_cnt[kBuckets];
     for (int b = threadIdx.x; b < kBuckets; b += kPartThreads) s_cnt[b] = 0;
     __syncthreads();
@@ -208,6 +216,8 @@ __global__ void __launch_bounds__(kPartThreads) part_count(const uint8_t *__rest
 
 // per bucket: exclusive scan of its G chunk counts (in place) and the bucket size
 __global__ void __launch_bounds__(256) seg_scan(uint32_t *__restrict__ gcnt, int G, uint32_t *__restrict__ bsize) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ uint32_t s_w[8];
     __shared__ uint32_t s_carry;
     uint32_t *row = gcnt + (size_t)blockIdx.x * G;
@@ -238,6 +248,8 @@ __global__ void __launch_bounds__(256) seg_scan(uint32_t *__restrict__ gcnt, int
 // buckets by decreasing size, so the largest start first (one block)
 __global__ void __launch_bounds__(kBuckets) bucket_scan(const uint32_t *__restrict__ bsize,
                                                         uint32_t *__restrict__ bstart, uint32_t *__restrict__ border) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ uint32_t s_x[kBuckets];
     __shared__ unsigned long long s_k[kBuckets];
     const int t = threadIdx.x;
@@ -275,6 +287,8 @@ __global__ void __launch_bounds__(kPartThreads) part_scatter(const uint8_t *__re
                                                              const uint32_t *__restrict__ gcnt, int G,
                                                              const uint32_t *__restrict__ bstart,
                                                              uint32_t *__restrict__ ent) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ uint32_t s_part[];
     uint32_t *s_cur = s_part;             // next global slot of this chunk's segment per bucket
     uint32_t *s_tc = s_cur + kBuckets;    // tile: entries per bucket
@@ -358,6 +372,8 @@ __global__ void __launch_bounds__(kAggThreads) bucket_agg(const uint32_t *__rest
                                                           const uint32_t *__restrict__ border,
                                                           uint32_t *__restrict__ cnt_out,
                                                           uint32_t *__restrict__ bitmap) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ uint32_t s_tab[]; // kSlots counts | kSlots minimum pixel indices | G + 1 segment starts
     uint32_t *s_cnt = s_tab, *s_min = s_tab + kSlots, *s_seg = s_tab + 2 * kSlots;
     const uint32_t b = border[blockIdx.x];
@@ -432,6 +448,8 @@ __global__ void __launch_bounds__(kAggThreads) bucket_agg(const uint32_t *__rest
 // block sums of popcounts over kWordsPerBlock words
 __global__ void __launch_bounds__(kThreads) scan_blocksum(const uint32_t *__restrict__ bitmap,
                                                           uint64_t words, uint32_t *__restrict__ bsum) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ uint32_t red[kThreads / 32];
     const uint64_t base = (uint64_t)blockIdx.x * kWordsPerBlock + (uint64_t)threadIdx.x * kWordsPerThread;
     uint32_t s = 0;
@@ -450,6 +468,8 @@ __global__ void __launch_bounds__(kThreads) scan_blocksum(const uint32_t *__rest
 
 // exclusive scan of the block sums (one block, sequential chunks)
 __global__ void scan_blocks(uint32_t *__restrict__ bsum, uint32_t nblocks, uint32_t *__restrict__ n_out) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ uint32_t carry;
     __shared__ uint32_t tmp[1024];
     if (threadIdx.x == 0) carry = 0;
@@ -477,6 +497,8 @@ __global__ void scan_blocks(uint32_t *__restrict__ bsum, uint32_t nblocks, uint3
 __global__ void __launch_bounds__(kThreads) scan_words(const uint32_t *__restrict__ bitmap, uint64_t words,
                                                        const uint32_t *__restrict__ bsum,
                                                        uint32_t *__restrict__ wpref) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ uint32_t wsum[kThreads / 32];
     const uint64_t base = (uint64_t)blockIdx.x * kWordsPerBlock + (uint64_t)threadIdx.x * kWordsPerThread;
     uint32_t pc[kWordsPerThread];
@@ -546,13 +568,13 @@ static void histogram_partitioned(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P
     uint32_t *ent = static_cast<uint32_t *>(ctx->pent.ensure(sizeof(uint32_t) * P));
     cnt_out = static_cast<uint32_t *>(ctx->pcnt.ensure(sizeof(uint32_t) << 24));
     part_count<<<G, kPartThreads, 0, s>>>(rgb_d, P, chunk, vec, gcnt, G);
-    seg_scan<<<kBuckets, 256, 0, s>>>(gcnt, G, bsize);
-    bucket_scan<<<1, kBuckets, 0, s>>>(bsize, bstart, border);
+    launch_pdl(seg_scan, kBuckets, 256, 0, s, gcnt, G, bsize);
+    launch_pdl(bucket_scan, 1, kBuckets, 0, s, bsize, bstart, border);
     CQG_CUDA(ensure_smem((const void *)part_scatter, kScatterSmem));
-    part_scatter<<<G, kPartThreads, kScatterSmem, s>>>(rgb_d, P, chunk, vec, gcnt, G, bstart, ent);
+    launch_pdl(part_scatter, G, kPartThreads, kScatterSmem, s, rgb_d, P, chunk, vec, gcnt, G, bstart, ent);
     const size_t agg_smem = sizeof(uint32_t) * (2 * kSlots + (size_t)G + 1);
     CQG_CUDA(ensure_smem((const void *)bucket_agg, agg_smem));
-    bucket_agg<<<kBuckets, kAggThreads, agg_smem, s>>>(ent, gcnt, G, chunk, bstart, bsize, border, cnt_out, bitmap);
+    launch_pdl(bucket_agg, kBuckets, kAggThreads, agg_smem, s, ent, gcnt, G, chunk, bstart, bsize, border, cnt_out, bitmap);
     launched(ctx, 5);
 }
 
@@ -591,18 +613,18 @@ void histogram_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P, uint32_t *col
     uint32_t *cnt = nullptr;
     if (!large) {
         hist_count_fused<<<grid, kThreads, 0, s>>>(rgb_d, P, tab, list, n_dev, aligned);
-        hist_mark_fused<<<lgrid, kThreads, 0, s>>>(list, n_dev, tab, bitmap);
+        launch_pdl(hist_mark_fused, lgrid, kThreads, 0, s, list, n_dev, tab, bitmap);
     } else {
         histogram_partitioned(ctx, rgb_d, P, bitmap, cnt);
     }
-    scan_blocksum<<<nblk, kThreads, 0, s>>>(bitmap, words, bsum);
-    scan_blocks<<<1, 1024, 0, s>>>(bsum, nblk, large ? n_dev : nullptr);
-    scan_words<<<nblk, kThreads, 0, s>>>(bitmap, words, bsum, wpref);
+    launch_pdl(scan_blocksum, nblk, kThreads, 0, s, bitmap, words, bsum);
+    launch_pdl(scan_blocks, 1, 1024, 0, s, bsum, nblk, large ? n_dev : nullptr);
+    launch_pdl(scan_words, nblk, kThreads, 0, s, bitmap, words, bsum, wpref);
     if (!large) {
-        hist_emit_fused<<<lgrid, kThreads, 0, s>>>(list, n_dev, tab, bitmap, wpref, colors_d, counts_d, first_d);
+        launch_pdl(hist_emit_fused, lgrid, kThreads, 0, s, list, n_dev, tab, bitmap, wpref, colors_d, counts_d, first_d);
     } else {
         const unsigned egrid = (unsigned)ctx->num_sms * 8;
-        hist_emit<<<egrid, kThreads, 0, s>>>(rgb_d, P, bitmap, wpref, cnt, colors_d, counts_d, first_d);
+        launch_pdl(hist_emit, egrid, kThreads, 0, s, rgb_d, P, bitmap, wpref, cnt, colors_d, counts_d, first_d);
     }
     prof_end(ctx, CQG_PROF_HIST, pb, 3.0 * (double)P); // + 8 N' added by the caller
     CQG_CUDA(cudaGetLastError());

@@ -81,6 +81,7 @@ __device__ void fc_block(const double *cen, int K, int Kp, float *fc, float *tau
 }
 
 __global__ void fc_kernel(const double *cen, int K, int Kp, float *fc, float *tau) {
+    pdl_trigger();
     fc_block(cen, K, Kp, fc, tau);
 }
 
@@ -642,7 +643,10 @@ static void launch_ppt(cqg_ctx *ctx, const SweepArgs &a, size_t smem, int bps) {
     const uint64_t cap = (a.n + 63) / 64; // at least 64 points per block
     if (grid > cap) grid = cap;
     if (grid < 1) grid = 1;
-    sweep_kernel<MODE, PPT><<<(unsigned)grid, kSweepThreads, smem, ctx->stream>>>(a);
+    // chained to the previous kernel by programmatic dependent launch, except
+    // in the captured Lloyd loop (WALK), whose graph keeps plain edges
+    if (MODE == MODE_WALK) sweep_kernel<MODE, PPT><<<(unsigned)grid, kSweepThreads, smem, ctx->stream>>>(a);
+    else launch_pdl(sweep_kernel<MODE, PPT>, (unsigned)grid, kSweepThreads, smem, ctx->stream, a);
 }
 
 template <int MODE>
@@ -691,7 +695,8 @@ static void launch_sweep_mode(cqg_ctx *ctx, const SweepArgs &a) {
     prof_end(ctx, MODE == MODE_MAP || MODE == MODE_MAPW ? CQG_PROF_MAPSWEEP : CQG_PROF_SWEEP, pb,
              (double)n * (double)a.K);
     const int pr = prof_begin(ctx);
-    replay_kernel<MODE><<<rg, 256, 0, ctx->stream>>>(a);
+    if (MODE == MODE_WALK) replay_kernel<MODE><<<rg, 256, 0, ctx->stream>>>(a);
+    else launch_pdl(replay_kernel<MODE>, rg, 256, 0, ctx->stream, a);
     prof_end(ctx, CQG_PROF_REPLAY, pr, 0.0);
     CQG_CUDA(cudaGetLastError());
     launched(ctx, 2);

@@ -32,6 +32,8 @@ namespace cqg {
 namespace {
 
 __global__ void mse_kernel(const Moments *mom, const double *pal, int K, uint64_t P, double *out) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ double s_t[];
     for (int k = threadIdx.x; k < K; k += blockDim.x) {
         const Moments m = mom[k];
@@ -83,6 +85,8 @@ __global__ void __launch_bounds__(256) pixel_kernel(const uint8_t *__restrict__ 
                                                    const double *__restrict__ pal, int K,
                                                    void *__restrict__ idx_out,
                                                    uint8_t *__restrict__ q_out, int vec) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ uint32_t s_pal8[]; // packed 0x00BBGGRR little-endian bytes r,g,b
     for (int k = threadIdx.x; k < K; k += blockDim.x)
         s_pal8[k] = (uint32_t)channel_to_u8(pal[3 * k]) | ((uint32_t)channel_to_u8(pal[3 * k + 1]) << 8) |
@@ -423,7 +427,7 @@ double map_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P, const uint32_t *c
 
     if ((size_t)K * 8 > 48 * 1024)
         CQG_CUDA(ensure_smem((const void *)mse_kernel, K * 8));
-    mse_kernel<<<1, 256, (size_t)K * 8, s>>>(mom, pal_d, K, P, mse_d);
+    launch_pdl(mse_kernel, 1, 256, (size_t)K * 8, s, mom, pal_d, K, P, mse_d);
     launched(ctx);
 
     if (indices_d || quant_d) {
@@ -439,11 +443,11 @@ double map_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P, const uint32_t *c
         }
         const int pp = prof_begin(ctx);
         if (index_bytes == 1) {
-            if (lut8) pixel_kernel<1, true><<<(unsigned)grid, 256, smem, s>>>(rgb_d, P, lut, pal_d, K, indices_d, quant_d, vec);
+            if (lut8) launch_pdl(pixel_kernel<1, true>, (unsigned)grid, 256, smem, s, rgb_d, P, lut, pal_d, K, indices_d, quant_d, vec);
             else fail(CQG_E_INVALID, "map_pixels: 8-bit indices need k <= 256");
         } else {
-            if (lut8) pixel_kernel<4, true><<<(unsigned)grid, 256, smem, s>>>(rgb_d, P, lut, pal_d, K, indices_d, quant_d, vec);
-            else pixel_kernel<4, false><<<(unsigned)grid, 256, smem, s>>>(rgb_d, P, lut, pal_d, K, indices_d, quant_d, vec);
+            if (lut8) launch_pdl(pixel_kernel<4, true>, (unsigned)grid, 256, smem, s, rgb_d, P, lut, pal_d, K, indices_d, quant_d, vec);
+            else launch_pdl(pixel_kernel<4, false>, (unsigned)grid, 256, smem, s, rgb_d, P, lut, pal_d, K, indices_d, quant_d, vec);
         }
         prof_end(ctx, CQG_PROF_PIXEL, pp,
                  (double)P * (3.0 + (indices_d ? (double)index_bytes : 0.0) + (quant_d ? 3.0 : 0.0)));

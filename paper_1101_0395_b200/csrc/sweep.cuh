@@ -816,6 +816,8 @@ __device__ __forceinline__ void flush_acc64(const unsigned long long *s_acc64, M
 
 template <int MODE, int PPT>
 __global__ void __launch_bounds__(kSweepThreads, 2) sweep_kernel(SweepArgs a) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ __align__(16) float smem[];
     const int K = a.K, Kp = a.Kp;
     uint32_t *s_acc = reinterpret_cast<uint32_t *>(smem + 4 * Kp);
@@ -920,6 +922,8 @@ __device__ __forceinline__ void replay_range(const SweepArgs &a, uint32_t gwarp,
 
 template <int MODE>
 __global__ void replay_kernel(SweepArgs a) {
+    pdl_wait();
+    pdl_trigger();
     replay_range<MODE>(a, (blockIdx.x * blockDim.x + threadIdx.x) >> 5, (gridDim.x * blockDim.x) >> 5);
 }
 
