@@ -316,6 +316,17 @@ enum {
     CQO_E_MASS = -21,         /* rng.hpp:47 */
 };
 
+/* The exact-moment SSE's summation order over clusters: pairwise on a complete
+ * binary tree over the next power of two >= K (zero padding), left + right at
+ * every node, in place. The device sums the same tree level by level in
+ * parallel (tree_sum_block, lloyd.cu). The reference sums points sequentially
+ * (kmeans.cpp:107-114); every order is within its recursive-sum error bound. */
+static double tree_sum(double *a, int K) {
+    for (int st = 1; st < K; st <<= 1)
+        for (int i = 0; i + st < K; i += 2 * st) a[i] = a[i] + a[i + st];
+    return K > 0 ? a[0] : 0.0;
+}
+
 /* SSE of one cluster from exact moments: (n*Q - |S|^2)/n, numerator in int128 */
 static double cluster_sse_exact(uint64_t n, const int64_t *S, uint64_t Q) {
     const unsigned __int128 nq = (unsigned __int128)n * Q;
@@ -354,6 +365,7 @@ CQO_API int cqo_wsm(const uint32_t *colors, const uint32_t *counts, uint64_t n, 
     uint64_t *mn = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)K);
     int64_t *mS = (int64_t *)malloc(sizeof(int64_t) * 3 * (size_t)K);
     uint64_t *mQ = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)K);
+    double *sterm = (double *)malloc(sizeof(double) * (size_t)K);
 
     uint64_t ndc = 0;
     int repairs = 0, iter, rc = CQO_OK;
@@ -405,16 +417,16 @@ CQO_API int cqo_wsm(const uint32_t *colors, const uint32_t *counts, uint64_t n, 
                 mS[3 * k + 2] += (int64_t)q * b;
                 mQ[k] += (uint64_t)q * (uint64_t)(r * r + g * g + b * b);
             }
-            double tot = 0.0;
             for (int k = 0; k < K; ++k) {
+                sterm[k] = 0.0;
                 if (mn[k] == 0) continue;
                 const double nd = (double)mn[k];
                 c[3 * k] = (double)mS[3 * k] / nd;
                 c[3 * k + 1] = (double)mS[3 * k + 1] / nd;
                 c[3 * k + 2] = (double)mS[3 * k + 2] / nd;
-                tot += cluster_sse_exact(mn[k], mS + 3 * k, mQ[k]);
+                sterm[k] = cluster_sse_exact(mn[k], mS + 3 * k, mQ[k]);
             }
-            sse = tot / (double)P;
+            sse = tree_sum(sterm, K) / (double)P;
         }
         sse_trace[iter - 1] = sse;
 
@@ -430,7 +442,7 @@ CQO_API int cqo_wsm(const uint32_t *colors, const uint32_t *counts, uint64_t n, 
     *iters_out = iter;
     *ndc_out = ndc;
     *repairs_out = repairs;
-    free(pts); free(w); free(tab); free(ord); free(sum); free(mn); free(mS); free(mQ);
+    free(pts); free(w); free(tab); free(ord); free(sum); free(mn); free(mS); free(mQ); free(sterm);
     return rc;
 }
 

@@ -236,6 +236,8 @@ cqg_ctx *cqg_create(int device) {
         ctx->use_prune = !(np && np[0] == '1');
         const char *nn = getenv("CQG_NO_NDC_CODE");
         ctx->use_ndc_code = !(nn && nn[0] == '1');
+        const char *nw = getenv("CQG_DBG_NDC_WIN");
+        if (nw) ctx->dbg_ndc_win = atoi(nw);
     });
     if (rc != CQG_OK) {
         delete ctx;
@@ -256,7 +258,8 @@ void cqg_destroy(cqg_ctx *ctx) {
                       &ctx->status, &ctx->sizes, &ctx->red, &ctx->hist_labels, &ctx->hist_centers,
                       &ctx->sse, &ctx->lut, &ctx->idx_out, &ctx->q_out, &ctx->mom_map, &ctx->coarse, &ctx->mind2,
                       &ctx->initpart, &ctx->initsel, &ctx->unit_draws, &ctx->inittile, &ctx->mom_g, &ctx->partial, &ctx->shard_log,
-                      &ctx->bnd, &ctx->shift, &ctx->dcode, &ctx->sub_img, &ctx->raw_col, &ctx->raw_cnt,
+                      &ctx->bnd, &ctx->shift, &ctx->dcode, &ctx->rowmin, &ctx->snap_cen, &ctx->snap_lab, &ctx->ndc_keys, &ctx->dmom, &ctx->rmpub,
+                      &ctx->sub_img, &ctx->raw_col, &ctx->raw_cnt,
                       &ctx->full_col, &ctx->full_cnt, &ctx->map_rows, &ctx->map_lab, &ctx->pcnt, &ctx->pent, &ctx->pseg};
     for (DevBuf *b : bufs) b->release();
     ctx->pinned.release();

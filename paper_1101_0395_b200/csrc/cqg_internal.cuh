@@ -127,6 +127,7 @@ struct cqg_ctx {
     cqg::DevBuf labels, cen, fcen, dtab, dsorted, order, mom, queue, ndc, status, sizes, red;
     cqg::DevBuf hist_labels, hist_centers, sse;
     cqg::DevBuf bnd, shift, dcode;
+    cqg::DevBuf rowmin, snap_cen, snap_lab, ndc_keys, dmom, rmpub; // persistent Lloyd: stay-test row minima, deferred-NDC snapshots
     cqg::DevBuf sub_img, raw_col, raw_cnt, full_col, full_cnt; // sampling modes     // distance-bound pruning: per-point (ub, lb), centre moves
     cqg::DevBuf mom_g, partial, shard_log; // sharded Lloyd: global moments, packed partials, state log
     void *shard = nullptr;      // cqg::ShardState (lloyd.cu)
@@ -144,6 +145,7 @@ struct cqg_ctx {
     bool use_mbar_init = true; // cluster init signals through mbarrier transactions (CQG_NO_MBAR_INIT=1: barriers)
     int cluster_max_ppt = 12; // cluster initialiser up to 16 x 1024 x ppt colours (CQG_CLUSTER_MAX_PPT); 16 measured slower on cfg4
     int dbg_init_force_seq = 0; // tests only: CQG_DBG_INIT_FORCE_SEQ=1|2 drives the register cluster kernel's sequential paths
+    int dbg_ndc_win = 0; // tests only: CQG_DBG_NDC_WIN=n caps the persistent loop's deferred-NDC window (relaunches)
     int cluster_nt = 0; // cluster init CTA size: 0 fewest padded slots, else forced (CQG_CLUSTER_NT=512..1024)
     bool use_init_reg = true; // cluster init keeps points in registers (CQG_NO_INIT_REG=1: shared-memory kernel)
     bool use_init_rec = true; // {colour, md} record layout for large-N init (CQG_NO_INIT_REC=1: off)
@@ -193,7 +195,7 @@ __device__ __forceinline__ double u128_to_double(unsigned __int128 x) {
     unsigned long long v = (unsigned long long)(x >> s);
     const unsigned __int128 lostmask = (((unsigned __int128)1) << s) - 1;
     if ((x & lostmask) != 0) v |= 1ULL;
-    return scalbn(__ull2double_rn(v), s);
+    return __dmul_rn(__ull2double_rn(v), __longlong_as_double((long long)(1023 + s) << 52)); // exact: x 2^s
 }
 
 // (n*Q - |S|^2) / n for one cluster, exact numerator (cluster_sse_exact in the oracle)
@@ -264,6 +266,7 @@ struct LloydOut {
     const float *shift = nullptr;
     const double *dsorted = nullptr;
     const uint16_t *dcode = nullptr; // 16-bit codes of dsorted (K <= 256), or null
+    const double *rowmin = nullptr;  // nearest-other-centre distances (when dsorted is null)
     const Moments *mom = nullptr;
     int Kpow = 0;
     // deferred completion (lloyd_dev(..., allow_defer)): the persistent kernel

@@ -111,6 +111,18 @@ struct IterArgs {
     uint16_t *dcode;  // K x Kpow codes of dsorted for ndc_code_kernel, or null
     float *shift;     // K centre moves (FP64 -> float, rounded up) + {max, 2nd max, argmax}; null = off
     int *shift_inval; // set by a repair: the next shifts are +inf (all bounds void)
+    // persistent kernel: no walk rows in the loop (no_walk_rows), only each
+    // centre's nearest-other distance rowmin[K] for the stay test; snapshots of
+    // the labels (snap_lab, n per iteration) and centres (snap_cen, 3K) each
+    // WALK iteration starts from, for the deferred NDC (ndc_post_kernel), in
+    // win slots
+    int no_walk_rows;
+    double *rowmin;
+    double *snap_cen;
+    uint16_t *snap_lab;
+    int win;
+    Moments *dmom; // persistent kernel: 3 x K moment deltas (iteration t into slot t % 3)
+    double *rmpub; // persistent kernel: 2 x 5K three nearest neighbours per centre (d1, d2, d3, j1, j2), published across the grid barrier
 };
 
 __device__ __forceinline__ void top2_merge(float &m1, int &i1, float &m2, float n1, int j1, float n2) {
@@ -182,6 +194,105 @@ __device__ __forceinline__ void bitonic_reg(unsigned long long &key, int &r, int
             }
         }
     }
+}
+
+// Nearest other centres per row of D[i][j] = dist2(c_i, c_j), j != i (the
+// stay test's Elkan term), rows spread over the blocks of the grid. TOP3:
+// out[5i..5i+4] = {d1, d2, d3, j1, j2}, the three smallest and the indices of
+// the first two; otherwise out[i] = d1.
+struct Near3 {
+    double d1, d2, d3;
+    int j1, j2;
+};
+__device__ __forceinline__ void near3_insert(Near3 &a, double d, int j) {
+    if (d < a.d1) {
+        a.d3 = a.d2;
+        a.d2 = a.d1;
+        a.j2 = a.j1;
+        a.d1 = d;
+        a.j1 = j;
+    } else if (d < a.d2) {
+        a.d3 = a.d2;
+        a.d2 = d;
+        a.j2 = j;
+    } else if (d < a.d3) {
+        a.d3 = d;
+    }
+}
+// merge b into a: b's third entry has no index, but only a's first two need one
+__device__ __forceinline__ void near3_merge(Near3 &a, const Near3 &b) {
+    near3_insert(a, b.d1, b.j1);
+    near3_insert(a, b.d2, b.j2);
+    if (b.d3 < a.d3) a.d3 = b.d3; // b.d3 can only land third: two smaller entries exist
+}
+__device__ __forceinline__ Near3 near3_shfl(const Near3 &a, int o) {
+    Near3 b;
+    b.d1 = __shfl_xor_sync(0xffffffffu, a.d1, o);
+    b.d2 = __shfl_xor_sync(0xffffffffu, a.d2, o);
+    b.d3 = __shfl_xor_sync(0xffffffffu, a.d3, o);
+    b.j1 = __shfl_xor_sync(0xffffffffu, a.j1, o);
+    b.j2 = __shfl_xor_sync(0xffffffffu, a.j2, o);
+    return b;
+}
+template <bool TOP3>
+__device__ void rowmin_rows(const double *c, int K, double *out) {
+    __shared__ Near3 s_rn[32];
+    const double kInf = __longlong_as_double(0x7FF0000000000000ll);
+    for (int i = blockIdx.x; i < K; i += gridDim.x) {
+        const double cr = c[3 * i], cg = c[3 * i + 1], cb = c[3 * i + 2];
+        Near3 m{kInf, kInf, kInf, -1, -1};
+        for (int j = threadIdx.x; j < K; j += blockDim.x)
+            if (j != i) near3_insert(m, d2_exact(cr, cg, cb, c[3 * j], c[3 * j + 1], c[3 * j + 2]), j);
+        for (int o = 16; o; o >>= 1) near3_merge(m, near3_shfl(m, o));
+        if ((threadIdx.x & 31) == 0) s_rn[threadIdx.x >> 5] = m;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int w = 1; w < (int)(blockDim.x >> 5); ++w) near3_merge(m, s_rn[w]);
+            if (TOP3) {
+                out[5 * i] = m.d1;
+                out[5 * i + 1] = m.d2;
+                out[5 * i + 2] = m.d3;
+                out[5 * i + 3] = (double)m.j1;
+                out[5 * i + 4] = (double)m.j2;
+            } else {
+                out[i] = m.d1;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// The exact-moment SSE's summation order (shared with the oracle's
+// tree_sum): pairwise on a complete binary tree over the next power of two
+// >= K, left + right at every node, in place in shared memory, one level per
+// step. Every thread of the block calls it; the sum is a[0].
+__device__ double tree_sum_block(double *a, int K) {
+    for (int st = 1; st < K; st <<= 1) {
+        __syncthreads();
+        for (int i = 2 * st * (int)threadIdx.x; i + st < K; i += 2 * st * (int)blockDim.x)
+            a[i] = __dadd_rn(a[i], a[i + st]);
+    }
+    __syncthreads();
+    return a[0];
+}
+
+// The same tree by one warp (no block barrier): lane l first reduces its
+// aligned segment of L = N / 32 entries in place (the tree's lower levels),
+// then the upper levels run across lanes by shuffles. The sum is in lane 0.
+__device__ double tree_sum_warp(double *a, int K) {
+    const int lane = threadIdx.x & 31;
+    int N = 32;
+    while (N < K) N <<= 1;
+    const int L = N >> 5, base = lane * L;
+    for (int st = 1; st < L; st <<= 1)
+        for (int i = base; i + st < base + L; i += 2 * st)
+            if (i + st < K) a[i] = __dadd_rn(a[i], a[i + st]);
+    double v = base < K ? a[base] : 0.0;
+    for (int o = 1; o < 32; o <<= 1) {
+        const double w = __shfl_down_sync(0xffffffffu, v, o);
+        if ((lane & (2 * o - 1)) == 0) v = __dadd_rn(v, w);
+    }
+    return v;
 }
 
 __device__ bool iter_end_body(const IterArgs &a, double *sm, float *fc_dst, float *tau_dst, bool fc_every_block) {
@@ -266,9 +377,8 @@ __device__ bool iter_end_body(const IterArgs &a, double *sm, float *fc_dst, floa
                 *a.shift_inval = 0;
             }
         }
+        const double tot = tree_sum_block(s_a, K);
         if (threadIdx.x == 0) {
-            double tot = 0.0;
-            for (int k = 0; k < K; ++k) tot = __dadd_rn(tot, s_a[k]);
             const double sse = __ddiv_rn(tot, __ull2double_rn(a.P));
             a.sse_arr[iter - 1] = sse;
             int done;
@@ -298,9 +408,11 @@ __device__ bool iter_end_body(const IterArgs &a, double *sm, float *fc_dst, floa
 #ifdef CQG_INIT_TIMING
     if (blockIdx.x == 0 && threadIdx.x == 0) g_lloyd_timing[6] += clock64() - _ie0;
 #endif
+    const double kInf = __longlong_as_double(0x7FF0000000000000ll);
+    if (a.rowmin) rowmin_rows<false>(s_c, K, a.rowmin);
+    if (a.no_walk_rows) return true;
     // walk table row i (kmeans.cpp:14-38): sort by (d, index), then rotate self
     // to the front. Block bitonic sort over Kpow keys (padding = +inf).
-    const double kInf = __longlong_as_double(0x7FF0000000000000ll);
     for (int i = blockIdx.x; i < K; i += gridDim.x) {
         const double cr = s_c[3 * i], cg = s_c[3 * i + 1], cb = s_c[3 * i + 2];
         for (int j = threadIdx.x; j < a.Kpow; j += blockDim.x) {
@@ -398,120 +510,493 @@ __global__ void __launch_bounds__(1024) iter_end_kernel(IterArgs a) {
     } while (0)
 #endif
 
+// The stay test's Elkan term as a Euclidean lower bound: sqrt of the squared
+// nearest-other-centre distance rm, rounded down.
+__device__ __forceinline__ float two_s_of(double rm) {
+    return __fsqrt_rd(__double2float_rd(__dmul_rd(rm, 1.0 - 0x1.0p-40)));
+}
+
+// Persistent cooperative Lloyd loop for small substrates: one launch runs all
+// iterations with ONE grid barrier per iteration. Per iteration t:
+//   sweep t (centres C_t) + block-local exact replay; moment deltas into
+//   dmom[t % 3]; this block's rows of the exact row minima of C_t into
+//   rmpub[t % 2]; block 0 clears dmom[(t + 1) % 3]
+//   | grid barrier |
+//   every block finalises redundantly: absolute moments M_t (shared copy) +=
+//   dmom[t % 3], centres C_{t+1} = S / n, centre shifts, per-cluster SSE, the
+//   reference's SSE sum in cluster order and its termination test
+//   (kmeans.cpp:249-257), the FP32 table, and the stay test's terms for
+//   C_{t+1}: 2 s from the row minima of C_t minus the shifts (d(c'_k, c'_j) >=
+//   d(c_k, c_j) - shift_k - shift_j), rounded down.
+// Deltas are read one barrier after they are written and cleared one barrier
+// before they are reused (three slots); row minima alternate between two.
+// The walk table and the NDC leave the loop (snapshots + ndc_post_kernel).
+// On exit (done, window full, empty cluster) block 0 publishes the state the
+// host and a relaunch start from: centres, absolute moments, shifts, exact
+// row minima (one more barrier), status.
 template <int PPT>
 __global__ void __launch_bounds__(kSweepThreads, 2) lloyd_persistent_kernel(SweepArgs a, IterArgs ia, int first_full,
                                                                             uint32_t list_cap) {
     cg::grid_group grid = cg::this_grid();
     extern __shared__ __align__(16) double psm[];
     const int K = a.K, Kp = a.Kp;
-    float *s_fc = reinterpret_cast<float *>(psm);          // 4 Kp
-    float *s_tau = s_fc + 4 * Kp;                           // 2 (+2 pad)
+    const int tid = threadIdx.x;
+    Moments *s_M = reinterpret_cast<Moments *>(psm);          // K absolute moments
+    double *s_cen = reinterpret_cast<double *>(s_M + K);      // 2 x 3K centres (current / next)
+    double *s_sse = s_cen + 6 * K;                            // K per-cluster SSE terms
+    float *s_fc = reinterpret_cast<float *>(s_sse + K);       // 4 Kp
+    float *s_tau = s_fc + 4 * Kp;                             // 2 (+2 pad)
     uint32_t *s_acc = reinterpret_cast<uint32_t *>(s_tau + 4); // 10 K u32 (= 5 K u64)
     unsigned long long *s_acc64 = reinterpret_cast<unsigned long long *>(s_acc);
-    double *s_end = reinterpret_cast<double *>(s_acc + 10 * K); // 5 K doubles + K ints
-    uint32_t *s_list = reinterpret_cast<uint32_t *>(s_end + 4 * K + ia.Kpow) + ia.Kpow; // prune list
-    // first kNdcPrefix walk codes of every row (after the list and its aux words)
-    uint16_t *s_pre = reinterpret_cast<uint16_t *>(
-        s_list + (list_cap ? list_cap + kSweepThreads * 4 + prune_aux_words(K) : 0));
-    fc_block(a.cen, K, Kp, s_fc, s_tau);
+    uint32_t *s_list = s_acc + 10 * K;                        // prune list + carried tile
+    float *s_aux = reinterpret_cast<float *>(s_list + list_cap + kSweepThreads * 4); // 2K + 4
+    __shared__ float s_rmax[8], s_rm1[8], s_rm2[8];
+    __shared__ int s_ri1[8], s_rempty[8];
+    __shared__ int s_state;
+    __shared__ double s_ssev;
+    __shared__ uint32_t s_qn;
+
     const uint64_t chunk = (a.n + gridDim.x - 1) / gridDim.x;
     const uint64_t lo = (uint64_t)blockIdx.x * chunk;
     const uint64_t hi = lo + chunk < a.n ? lo + chunk : a.n;
-    const uint32_t warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    __shared__ uint32_t s_qn;
+    const uint32_t warp = tid >> 5, nw = blockDim.x >> 5;
     SweepArgs la = a; // block-local near-tie queue
     la.queue = a.queue + lo;
     la.qn = &s_qn;
+    la.aux_ready = 1;
+
+    // entry state: centres C_t, moments M_{t-1} (zero before iteration 1)
     bool full = first_full != 0;
-    bool cen_smem = false; // s_end[0, 3K) holds the current centres (after a finalise)
+    int t = *ia.iter_dev + 1; // the iteration about to run
+    const int t0 = full ? t + 1 : t; // first WALK iteration: snapshot slot 0
+    double *cen = s_cen, *cnx = s_cen + 3 * K;
+    for (int i = tid; i < 3 * K; i += blockDim.x) cen[i] = a.cen[i];
+    {
+        unsigned long long *m = reinterpret_cast<unsigned long long *>(s_M);
+        const unsigned long long *g = reinterpret_cast<const unsigned long long *>(ia.mom);
+        for (int i = tid; i < 5 * K; i += blockDim.x) m[i] = full ? 0ull : g[i];
+    }
+    double sse_prev = (!full && t >= 2) ? ia.sse_arr[t - 2] : 0.0;
+    if (!full && a.bnd) { // a relaunch: the host-side finalise left shifts and exact row minima
+        for (int k = tid; k < K; k += blockDim.x) {
+            s_aux[k] = a.shift[k];
+            s_aux[K + k] = K > 1 ? two_s_of(ia.rowmin[k]) : __int_as_float(0x7f800000);
+        }
+        if (tid < 3) s_aux[2 * K + tid] = a.shift[K + tid];
+    }
+    __syncthreads();                   // cen[] is read across threads below
+    fc_block(cen, K, Kp, s_fc, s_tau); // ends with a block barrier
 #ifdef CQG_INIT_TIMING
     unsigned long long _tprev = clock64();
     unsigned long long _bprev = _tprev;
 #endif
     for (;;) {
-        // phase A: NDC, sweep and the exact replay of this block's own queued
-        // points (block-local queue in slots [lo, hi), counter in shared memory)
-        if (threadIdx.x == 0) s_qn = 0;
+        Moments *dst = ia.dmom + (size_t)(t % 3) * K;
+        SweepArgs wa = la;
+        wa.cen = cen;
+        wa.mom = dst;
+        if (tid == 0) s_qn = 0;
         if (full) {
-            for (int i = threadIdx.x; i < K * kAccPerCluster; i += blockDim.x) s_acc[i] = 0;
+            for (int i = tid; i < K * kAccPerCluster; i += blockDim.x) s_acc[i] = 0;
             __syncthreads();
-            sweep_range<MODE_FULL, PPT>(la, lo, hi, s_fc, s_acc, s_tau[0], s_tau[1]);
+            sweep_range<MODE_FULL, PPT>(wa, lo, hi, s_fc, s_acc, s_tau[0], s_tau[1]);
             __syncthreads();
-            replay_range<MODE_FULL>(la, warp, nw);
+            replay_range<MODE_FULL>(wa, warp, nw);
         } else {
-            unsigned long long nd;
-            if (a.dcode) {
-                // rows of L = min(Kpow, kNdcPrefix) codes: 128-bit global loads (8
-                // codes), 8 in flight per thread, 32-bit shared stores (row stride
-                // 33 words). L and Kpow are powers of two.
-                const int L = a.Kpow < kNdcPrefix ? a.Kpow : kNdcPrefix;
-                uint32_t *dst = reinterpret_cast<uint32_t *>(s_pre);
-                if (L >= 8) {
-                    const int lq = 31 - __clz(L >> 3), kq = 31 - __clz(a.Kpow >> 3); // log2 of uint4 per row
-                    const uint4 *src = reinterpret_cast<const uint4 *>(a.dcode);
-                    const int total = K << lq;
-                    for (int e0 = threadIdx.x; e0 < total; e0 += 8 * blockDim.x) {
-                        uint4 v[8];
-#pragma unroll
-                        for (int u = 0; u < 8; ++u) {
-                            const int e = e0 + u * blockDim.x;
-                            if (e < total) v[u] = __ldg(src + (((size_t)(e >> lq)) << kq) + (e & ((1 << lq) - 1)));
-                        }
-#pragma unroll
-                        for (int u = 0; u < 8; ++u) {
-                            const int e = e0 + u * blockDim.x;
-                            if (e < total) {
-                                uint32_t *d = dst + (e >> lq) * ((kNdcPrefix + 2) / 2) + (e & ((1 << lq) - 1)) * 4;
-                                d[0] = v[u].x;
-                                d[1] = v[u].y;
-                                d[2] = v[u].z;
-                                d[3] = v[u].w;
-                            }
-                        }
-                    }
-                } else {
-                    for (int e = threadIdx.x; e < K * L; e += blockDim.x)
-                        s_pre[(e / L) * (kNdcPrefix + 2) + e % L] = a.dcode[(size_t)(e / L) * a.Kpow + e % L];
-                }
-                __syncthreads();
-                // centres: this block's shared copy from the last finalise
-                // (a relaunch after a repair starts from the global ones)
-                nd = ndc_range_pre<2>(a.colors, a.labels, lo, hi, 0, 2ull * blockDim.x, cen_smem ? s_end : a.cen,
-                                      a.dsorted, a.Kpow, s_pre);
-            } else {
-                nd = ndc_range<2>(a.colors, a.labels, lo, hi, 0, 2ull * blockDim.x, a.cen, a.dsorted, a.Kpow);
-            }
-            for (int o = 16; o; o >>= 1) nd += __shfl_xor_sync(0xffffffffu, nd, o);
-            if ((threadIdx.x & 31) == 0 && nd) atomicAdd(a.ndc, nd);
-            for (int i = threadIdx.x; i < K * 5; i += blockDim.x) s_acc64[i] = 0;
+            // the NDC of this iteration is counted after the loop (ndc_post_kernel)
+            // from the labels and centres it starts from
+            const int slot = t - t0;
+            if (blockIdx.x == 0)
+                for (int i = tid; i < 3 * K; i += blockDim.x) ia.snap_cen[(size_t)slot * 3 * K + i] = cen[i];
+            wa.lab_snap = ia.snap_lab + (size_t)slot * a.n;
+            if (a.bnd == nullptr) // no filter pass: copy the labels here
+                for (uint64_t i = lo + tid; i < hi; i += blockDim.x) wa.lab_snap[i] = (uint16_t)a.labels[i];
+            for (int i = tid; i < K * 5; i += blockDim.x) s_acc64[i] = 0;
             __syncthreads();
             PTIME(0);
             BTIME(0);
-            sweep_range<MODE_WALK, PPT>(la, lo, hi, s_fc, s_acc, s_tau[0], s_tau[1], s_list, list_cap,
-                                        reinterpret_cast<float *>(s_list + list_cap + kSweepThreads * 4));
+            sweep_range<MODE_WALK, PPT>(wa, lo, hi, s_fc, s_acc, s_tau[0], s_tau[1], s_list, list_cap, s_aux);
             __syncthreads();
             PTIME(1);
             BTIME(1);
-            flush_acc64(s_acc64, a.mom, K);
-            replay_range<MODE_WALK>(la, warp, nw);
+            flush_acc64(s_acc64, dst, K);
+            replay_walk_tableless(wa, warp, nw);
             PTIME(2);
             BTIME(2);
         }
-        if (threadIdx.x == 0 && s_qn) atomicAdd(a.qn, s_qn);
+        __syncthreads();
+        if (tid == 0 && s_qn) atomicAdd(ia.flagged, (unsigned long long)s_qn);
+        if (a.bnd) rowmin_rows<true>(cen, K, ia.rmpub + (size_t)(t & 1) * 5 * K);
+        if (blockIdx.x == 0) {
+            unsigned long long *z = reinterpret_cast<unsigned long long *>(ia.dmom + (size_t)((t + 1) % 3) * K);
+            for (int i = tid; i < 5 * K; i += blockDim.x) z[i] = 0ull;
+        }
         grid.sync();
         PTIME(3);
 #ifdef CQG_INIT_TIMING
         _bprev = clock64();
 #endif
-        const bool ok = iter_end_body(ia, s_end, s_fc, s_tau, true);
-        cen_smem = true;
+        // ---- finalise iteration t (every block, identical results) ----
+        // pass 1, per cluster: moments += deltas, centre, shift, SSE term, FP32
+        // table row, and the neighbour terms of C_t (two nearest, rounded down)
+        float cm = 0.f, m1 = -1.f, m2 = -1.f;
+        int i1 = -1, empty = 0;
+        const double *rm = ia.rmpub + (size_t)(t & 1) * 5 * K;
+        float *s_td3 = reinterpret_cast<float *>(s_acc); // scratch until the next sweep
+        int *s_j1 = reinterpret_cast<int *>(s_acc + K), *s_j2 = reinterpret_cast<int *>(s_acc + 2 * K);
+        for (int k = tid; k < K; k += blockDim.x) {
+            // L2 reads (written by other blocks before the barrier), all issued first
+            const unsigned long long *dq = reinterpret_cast<const unsigned long long *>(dst + k);
+            const unsigned long long d0 = __ldcg(dq), d1s = __ldcg(dq + 1), d2s = __ldcg(dq + 2),
+                                     d3s = __ldcg(dq + 3), d4 = __ldcg(dq + 4);
+            double n3 = 0.0, nj1 = 0.0, nj2 = 0.0;
+            if (a.bnd) {
+                n3 = __ldcg(rm + 5 * k + 2);
+                nj1 = __ldcg(rm + 5 * k + 3);
+                nj2 = __ldcg(rm + 5 * k + 4);
+            }
+            Moments &m = s_M[k];
+            m.n += d0;
+            m.s[0] += (long long)d1s;
+            m.s[1] += (long long)d2s;
+            m.s[2] += (long long)d3s;
+            m.q += d4;
+            s_sse[k] = 0.0;
+            if (a.bnd) {
+                s_td3[k] = two_s_of(n3);
+                s_j1[k] = (int)nj1;
+                s_j2[k] = (int)nj2;
+            }
+            if (m.n == 0) {
+                empty = 1;
+                continue;
+            }
+            const double nd = __ull2double_rn(m.n);
+            const double r = __ddiv_rn(__ll2double_rn(m.s[0]), nd);
+            const double g = __ddiv_rn(__ll2double_rn(m.s[1]), nd);
+            const double b = __ddiv_rn(__ll2double_rn(m.s[2]), nd);
+            cnx[3 * k] = r;
+            cnx[3 * k + 1] = g;
+            cnx[3 * k + 2] = b;
+            s_sse[k] = cluster_sse_exact(m.n, m.s, m.q);
+            const double dr = __dsub_rn(r, cen[3 * k]), dg = __dsub_rn(g, cen[3 * k + 1]),
+                         db = __dsub_rn(b, cen[3 * k + 2]);
+            const double dd = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(dr, dr), __dmul_rn(dg, dg)), __dmul_rn(db, db)));
+            const float f = __double2float_ru(__dmul_ru(dd, 1.0 + 0x1.0p-40)); // covers FP64 rounding
+            s_aux[k] = f;
+            top2_merge(m1, i1, m2, f, k, -1.f);
+            // FP32 sweep table of the new centre (fc_block's arithmetic)
+            s_fc[k] = __double2float_rn(__dmul_rn(-2.0, r));
+            s_fc[Kp + k] = __double2float_rn(__dmul_rn(-2.0, g));
+            s_fc[2 * Kp + k] = __double2float_rn(__dmul_rn(-2.0, b));
+            s_fc[3 * Kp + k] =
+                __double2float_rn(__dadd_rn(__dadd_rn(__dmul_rn(r, r), __dmul_rn(g, g)), __dmul_rn(b, b)));
+            cm = fmaxf(cm, __double2float_ru(fmax(fabs(r), fmax(fabs(g), fabs(b)))));
+        }
+        for (int o = 16; o; o >>= 1) {
+            cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, o));
+            empty |= __shfl_xor_sync(0xffffffffu, empty, o);
+            const float n1 = __shfl_xor_sync(0xffffffffu, m1, o), n2 = __shfl_xor_sync(0xffffffffu, m2, o);
+            const int j1 = __shfl_xor_sync(0xffffffffu, i1, o);
+            top2_merge(m1, i1, m2, n1, j1, n2);
+        }
+        if ((tid & 31) == 0) {
+            s_rmax[warp] = cm;
+            s_rempty[warp] = empty;
+            s_rm1[warp] = m1;
+            s_rm2[warp] = m2;
+            s_ri1[warp] = i1;
+        }
+        __syncthreads();
+#ifdef CQG_INIT_TIMING
+        if (blockIdx.x == 0 && tid == 0) g_lloyd_timing[6] += clock64() - _bprev;
+#endif
+        if (warp == 0) {
+            // the SSE in the oracle's tree order, the status and the sweep's error bound
+            const double tot = tree_sum_warp(s_sse, K);
+            if (tid == 0) {
+                for (int w = 1; w < (int)nw; ++w) {
+                    cm = fmaxf(cm, s_rmax[w]);
+                    empty |= s_rempty[w];
+                }
+                int state = 0;
+                if (empty) {
+                    state = 2;
+                } else {
+                    const double sse = __ddiv_rn(tot, __ull2double_rn(ia.P));
+                    int done;
+                    if (ia.fixed > 0) {
+                        done = t >= ia.limit;
+                    } else {
+                        done = (sse == 0.0);
+                        if (!done && t >= 2) done = __ddiv_rn(__dsub_rn(sse_prev, sse), sse) <= ia.eps;
+                        if (!done && t >= ia.limit) done = 1;
+                    }
+                    state = done ? 1 : (t + 1 - t0 >= ia.win ? 3 : 0);
+                    s_ssev = sse;
+                    const double u = 0x1.0p-24, X = 255.0, C = (double)cm;
+                    const double E =
+                        u * 3.0 * C * C + u * 2.0 * X * 3.0 * C + 3.0 * u * (3.0 * C * C + 6.0 * X * C);
+                    s_tau[0] = (float)(2.0 * E * 1.0625 + 1.0e-3);
+                    s_tau[1] = 0x1.0p-20f;
+                    if (blockIdx.x == 0) {
+                        ia.sse_arr[t - 1] = sse;
+                        if (t == 1) *ia.ndc += (unsigned long long)ia.n_points * (unsigned long long)K;
+                    }
+                }
+                s_state = state;
+            }
+        } else {
+            // the other warps: the two largest shifts (each thread merges the
+            // warp partials itself) and the stay test's 2 s for C_{t+1}: the
+            // distances to the two nearest neighbours of C_t, recomputed on
+            // C_{t+1}, and for every other j the third-nearest distance lowered
+            // by the two moves: d(c'_k, c'_j) >= d3 - shift_k - (largest shift
+            // outside {k, j1, j2}); rounded down
+            m1 = s_rm1[0];
+            m2 = s_rm2[0];
+            i1 = s_ri1[0];
+            for (int w = 1; w < (int)nw; ++w) top2_merge(m1, i1, m2, s_rm1[w], s_ri1[w], s_rm2[w]);
+            const float sm1 = fmaxf(m1, 0.f), sm2 = fmaxf(m2, 0.f);
+            if (tid == 32) {
+                s_aux[2 * K] = sm1;
+                s_aux[2 * K + 1] = sm2;
+                s_aux[2 * K + 2] = __int_as_float(i1);
+            }
+            if (a.bnd) {
+                for (int k = tid - 32; k < K; k += blockDim.x - 32) {
+                    float v = __int_as_float(0x7f800000);
+                    if (K > 1) {
+                        const int j1 = s_j1[k], j2 = s_j2[k];
+                        const double cr = cnx[3 * k], cg = cnx[3 * k + 1], cb = cnx[3 * k + 2];
+                        v = two_s_of(d2_exact(cr, cg, cb, cnx[3 * j1], cnx[3 * j1 + 1], cnx[3 * j1 + 2]));
+                        if (j2 >= 0) {
+                            v = fminf(v, two_s_of(d2_exact(cr, cg, cb, cnx[3 * j2], cnx[3 * j2 + 1], cnx[3 * j2 + 2])));
+                            const float sx = (i1 == k || i1 == j1 || i1 == j2) ? sm2 : sm1;
+                            v = fminf(v, __fadd_rd(__fadd_rd(s_td3[k], -s_aux[k]), -sx));
+                        }
+                        v = fmaxf(v, 0.f);
+                    }
+                    s_aux[K + k] = v;
+                }
+            }
+        }
+        __syncthreads();
+#ifdef CQG_INIT_TIMING
+        if (blockIdx.x == 0 && tid == 0) g_lloyd_timing[7] += clock64() - _bprev;
+#endif
+        const int state = s_state;
+        if (state == 2) {
+            // an empty cluster: the host repairs from the centres of this
+            // iteration's assignment and the absolute moments
+            if (blockIdx.x == 0) {
+                for (int i = tid; i < 3 * K; i += blockDim.x) ia.cen[i] = cen[i];
+                unsigned long long *g = reinterpret_cast<unsigned long long *>(ia.mom);
+                const unsigned long long *m = reinterpret_cast<const unsigned long long *>(s_M);
+                for (int i = tid; i < 5 * K; i += blockDim.x) g[i] = m[i];
+                if (tid == 0) {
+                    ia.st->state = 2;
+                    ia.st->iteration = t;
+                    ia.st->n_flagged = 0;
+                }
+            }
+            break;
+        }
         PTIME(4);
-        grid.sync();
-        PTIME(5);
-        if (!ok) break;
-        if (*reinterpret_cast<volatile int *>(&ia.st->state) != 0) break;
+        if (state != 0) {
+            // done or window full: publish C_{t+1}, shifts, moments, exact row minima
+            if (blockIdx.x == 0) {
+                for (int i = tid; i < 3 * K; i += blockDim.x) ia.cen[i] = cnx[i];
+                unsigned long long *g = reinterpret_cast<unsigned long long *>(ia.mom);
+                const unsigned long long *m = reinterpret_cast<const unsigned long long *>(s_M);
+                for (int i = tid; i < 5 * K; i += blockDim.x) g[i] = m[i];
+                if (ia.shift) {
+                    const bool inval = *ia.shift_inval != 0;
+                    const float inf = __int_as_float(0x7f800000);
+                    for (int k = tid; k < K; k += blockDim.x) ia.shift[k] = s_aux[k];
+                    if (tid == 0) {
+                        ia.shift[K] = inval ? inf : s_aux[2 * K];
+                        ia.shift[K + 1] = inval ? inf : s_aux[2 * K + 1];
+                        ia.shift[K + 2] = s_aux[2 * K + 2];
+                    }
+                }
+                if (tid == 0) {
+                    ia.st->state = state;
+                    ia.st->iteration = t;
+                    ia.st->n_flagged = 0;
+                    ia.st->sse = s_ssev;
+                    *ia.iter_dev = t;
+                }
+            }
+            if (ia.rowmin) rowmin_rows<false>(cnx, K, ia.rowmin);
+            break;
+        }
+        sse_prev = s_ssev;
+        double *tmp = cen;
+        cen = cnx;
+        cnx = tmp;
+        ++t;
         full = false;
+        __syncthreads();
+        PTIME(5);
     }
+}
+
+// ---- deferred NDC of the persistent loop ----------------------------------
+// The reference counts, for iteration t >= 2, 1 + #{j != prev : D_t[prev][j] <
+// 4 d2(x, c_t,prev)} distances per point (assign_point_sortmeans). The
+// persistent kernel keeps only the labels and centres each WALK iteration
+// started from; after the loop, walk_keys_kernel sorts every iteration's
+// rows as 32-bit keys (code16(D) << 16 | j) and ndc_post_kernel counts by
+// binary lifting over the codes (FP64 only for entries whose code equals the
+// cutoff's), all iterations at once.
+template <int KS>
+__device__ __forceinline__ void bitonic_u32(uint32_t &key, int t, uint32_t *s_key) {
+#pragma unroll
+    for (int size = 2; size <= KS; size <<= 1) {
+#pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            uint32_t ok;
+            if (stride >= 32) {
+                __syncthreads();
+                s_key[t] = key;
+                __syncthreads();
+                ok = s_key[t ^ stride];
+            } else {
+                ok = __shfl_xor_sync(0xffffffffu, key, stride);
+            }
+            const bool up = (t & size) == 0;
+            const bool low = (t & stride) == 0;
+            if ((ok < key) == (low == up)) key = ok;
+        }
+    }
+}
+
+// rows of every snapshot table: KS (>= 32, >= K, power of two) keys per row,
+// 1024 / KS rows per block, padding keys 0xFFFFFFFF
+template <int KS>
+__global__ void __launch_bounds__(1024) walk_keys_kernel(const double *__restrict__ snap_cen, int K,
+                                                         const IterStatus *st, int t0, uint32_t *__restrict__ keys) {
+    constexpr int RPB = 1024 / KS;
+    __shared__ uint32_t s_key[1024];
+    extern __shared__ double s_c[]; // 3 K
+    const int nt = st->iteration - t0 + 1;
+    if (nt <= 0) return;
+    const int groups = (K + RPB - 1) / RPB;
+    const int t = threadIdx.x & (KS - 1), rr = threadIdx.x / KS;
+    for (int it = blockIdx.x; it < nt * groups; it += gridDim.x) {
+        const int tab = it / groups, row = (it - tab * groups) * RPB + rr;
+        const double *cen = snap_cen + (size_t)tab * 3 * K;
+        __syncthreads();
+        for (int i = threadIdx.x; i < 3 * K; i += blockDim.x) s_c[i] = cen[i];
+        __syncthreads();
+        uint32_t key = 0xFFFFFFFFu;
+        if (row < K && t < K)
+            key = (code16(d2_exact(s_c[3 * row], s_c[3 * row + 1], s_c[3 * row + 2], s_c[3 * t], s_c[3 * t + 1],
+                                   s_c[3 * t + 2]))
+                   << 16) |
+                  (uint32_t)t;
+        bitonic_u32<KS>(key, t, s_key + rr * KS);
+        if (row < K) keys[((size_t)tab * K + row) * KS + t] = key;
+    }
+}
+
+constexpr int kNdcPostThreads = 512;
+constexpr int kNdcPostChunk = 4096;
+// Per block a contiguous range of (table, point chunk) items; the table's
+// centres and the first L codes of each of its rows live in shared memory.
+template <int Q>
+__global__ void __launch_bounds__(kNdcPostThreads) ndc_post_kernel(const uint32_t *__restrict__ colors, uint64_t n,
+                                                                  const uint16_t *__restrict__ snap_lab,
+                                                                  const double *__restrict__ snap_cen,
+                                                                  const uint32_t *__restrict__ keys, int K, int KS,
+                                                                  int L, const IterStatus *st, int t0,
+                                                                  unsigned long long *ndc) {
+    extern __shared__ __align__(16) double s_c2[]; // 3 K centres, then K rows of L + 2 codes
+    uint16_t *s_pre = reinterpret_cast<uint16_t *>(s_c2 + 3 * K);
+    const int rs = L + 2;
+    const int nt = st->iteration - t0 + 1;
+    if (nt <= 0) return;
+    const uint64_t nch = (n + kNdcPostChunk - 1) / kNdcPostChunk;
+    const uint64_t items = (uint64_t)nt * nch;
+    const uint64_t per = (items + gridDim.x - 1) / gridDim.x;
+    const uint64_t i0 = (uint64_t)blockIdx.x * per, i1 = i0 + per < items ? i0 + per : items;
+    unsigned long long local = 0;
+    int cur = -1;
+    for (uint64_t it = i0; it < i1; ++it) {
+        const int tab = (int)(it / nch);
+        const uint64_t p0 = (it - (uint64_t)tab * nch) * kNdcPostChunk;
+        const uint64_t p1 = p0 + kNdcPostChunk < n ? p0 + kNdcPostChunk : n;
+        const uint32_t *tkeys = keys + (size_t)tab * K * KS;
+        if (tab != cur) {
+            __syncthreads();
+            for (int i = threadIdx.x; i < 3 * K; i += blockDim.x) s_c2[i] = snap_cen[(size_t)tab * 3 * K + i];
+            for (int e = threadIdx.x; e < K * L; e += blockDim.x) {
+                const int r = e / L, p = e - r * L;
+                s_pre[r * rs + p] = (uint16_t)(__ldg(tkeys + (size_t)r * KS + p) >> 16);
+            }
+            __syncthreads();
+            cur = tab;
+        }
+        const uint16_t *lab = snap_lab + (size_t)tab * n;
+        for (uint64_t base = p0; base < p1; base += (uint64_t)Q * kNdcPostThreads) {
+            double cut[Q];
+            uint32_t cc[Q];
+            int prow[Q], pos[Q];
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+                const uint64_t i = base + threadIdx.x + (uint64_t)q * kNdcPostThreads;
+                const bool v = i < p1;
+                const uint32_t col = v ? __ldg(colors + i) : 0u;
+                const int prev = v ? (int)__ldg(lab + i) : 0;
+                const double pd = d2_exact((double)((col >> 16) & 255u), (double)((col >> 8) & 255u),
+                                           (double)(col & 255u), s_c2[3 * prev], s_c2[3 * prev + 1],
+                                           s_c2[3 * prev + 2]);
+                cut[q] = v ? __dmul_rn(4.0, pd) : -1.0;
+                cc[q] = v ? code16(cut[q]) : 0u;
+                prow[q] = prev;
+                pos[q] = 0;
+            }
+            for (int step = L >> 1; step >= 1; step >>= 1) {
+                uint32_t vv[Q];
+#pragma unroll
+                for (int q = 0; q < Q; ++q) vv[q] = s_pre[prow[q] * rs + pos[q] + step - 1];
+#pragma unroll
+                for (int q = 0; q < Q; ++q) pos[q] += vv[q] < cc[q] ? step : 0;
+            }
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+                if (cut[q] < 0.0) continue;
+                const uint16_t *row = s_pre + prow[q] * rs;
+                const uint32_t *grow = tkeys + (size_t)prow[q] * KS;
+                int p = pos[q];
+                if (p == L - 1 && row[L - 1] < cc[q]) p = L;
+                if (p == L && L < KS) {
+                    // beyond the prefix: the entries with a smaller code, by lifting over the keys
+                    const uint32_t kc = cc[q] << 16;
+                    int b = 0;
+                    for (int step = KS >> 1; step >= 1; step >>= 1)
+                        if (__ldg(grow + b + step - 1) < kc) b += step;
+                    if (b == KS - 1 && __ldg(grow + KS - 1) < kc) b = KS;
+                    p = b;
+                }
+                int cnt = p;
+                // entries whose code equals the cutoff's (sorted by index): decide in FP64
+                if (p < KS && (p < L ? (uint32_t)row[p] : (__ldg(grow + p) >> 16)) == cc[q]) {
+                    const double cr = s_c2[3 * prow[q]], cg = s_c2[3 * prow[q] + 1], cb = s_c2[3 * prow[q] + 2];
+                    for (; p < KS; ++p) {
+                        const uint32_t key = __ldg(grow + p);
+                        if ((key >> 16) != cc[q]) break;
+                        const int j = (int)(key & 0xFFFFu);
+                        cnt += d2_exact(cr, cg, cb, s_c2[3 * j], s_c2[3 * j + 1], s_c2[3 * j + 2]) < cut[q];
+                    }
+                }
+                local += (unsigned long long)(cnt - (cut[q] > 0.0 ? 1 : 0) + 1);
+            }
+        }
+    }
+    for (int o = 16; o; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+    if ((threadIdx.x & 31) == 0 && local) atomicAdd(ndc, local);
 }
 
 // ---- repair helpers (kmeans.cpp:124-169) ----------------------------------
@@ -874,10 +1359,12 @@ void release_graphs(cqg_ctx *ctx) {
 }
 
 
-static size_t persist_smem(int K, int Kp, size_t list_words, bool pre) {
-    return (size_t)4 * Kp * sizeof(float) + 4 * sizeof(float) + (size_t)10 * K * sizeof(uint32_t) +
-           iter_end_smem(K) + list_words * sizeof(uint32_t) +
-           (pre ? (size_t)K * (kNdcPrefix + 2) * sizeof(uint16_t) : 0);
+static size_t persist_smem(int K, int Kp, size_t list_cap) {
+    // moments, 2 x centres, SSE terms, FP32 table + tau, accumulators, prune
+    // list + carried tile + stay-test terms (lloyd_persistent_kernel's layout)
+    return (size_t)K * sizeof(Moments) + (size_t)7 * K * sizeof(double) + (size_t)4 * Kp * sizeof(float) +
+           4 * sizeof(float) + (size_t)10 * K * sizeof(uint32_t) +
+           (list_cap + kSweepThreads * 4 + prune_aux_words(K)) * sizeof(uint32_t);
 }
 
 // prune-list capacity of the persistent kernel: a block's whole point range
@@ -887,13 +1374,11 @@ static size_t persist_list_words(const cqg_ctx *ctx, uint64_t n) {
     if (r < 128) r = 128;
     return (size_t)(r < (uint64_t)kPruneChunk ? r : (uint64_t)kPruneChunk);
 }
-// shared words of the prune list: the chunk plus one carried-over big tile (PPT <= 4)
-static size_t persist_list_alloc(size_t cap, int K) { return cap ? cap + kSweepThreads * 4 + prune_aux_words(K) : 0; }
 
 // Launch the persistent loop if it fits co-resident; returns false otherwise.
 static bool launch_persistent(cqg_ctx *ctx, const SweepArgs &a, IterArgs ia, bool first_full) {
     const uint32_t list_cap = a.bnd ? (uint32_t)persist_list_words(ctx, a.n) : 0u;
-    const size_t smem = persist_smem(a.K, a.Kp, persist_list_alloc(list_cap, a.K), a.dcode != nullptr);
+    const size_t smem = persist_smem(a.K, a.Kp, list_cap);
     // 2-point tiles up to 4 points per thread of the grid (survivor tiles are
     // latency-bound; measured cfg1 0.216 -> 0.212 ms, cfg2 0.591 -> 0.584 ms vs 4-point)
     const int ppt = a.n <= (uint64_t)ctx->num_sms * 2 * kSweepThreads * 4 ? 2 : 4;
@@ -918,6 +1403,7 @@ static bool launch_persistent(cqg_ctx *ctx, const SweepArgs &a, IterArgs ia, boo
     if (grid < 1) grid = 1;
     ia.use_cond = 0;
     ia.reset_qn = 1;
+    CQG_CUDA(cudaMemsetAsync(ia.dmom, 0, 3 * sizeof(Moments) * (size_t)a.K, ctx->stream));
     SweepArgs aa = a;
     int ff = first_full ? 1 : 0;
     uint32_t lc = list_cap;
@@ -925,6 +1411,57 @@ static bool launch_persistent(cqg_ctx *ctx, const SweepArgs &a, IterArgs ia, boo
     CQG_CUDA(launch_cooperative(ctx, kern, dim3((unsigned)grid), dim3(kSweepThreads), args, smem));
     launched(ctx);
     return true;
+}
+
+// key-row stride of the deferred NDC tables: a power of two >= max(K, 32)
+static int ndc_key_stride(int K) {
+    const int p = kpow_of(K);
+    return p < 32 ? 32 : p;
+}
+// prefix codes per row kept in shared memory by ndc_post_kernel
+static int ndc_post_prefix(int K, int KS) {
+    const int L = K <= 256 ? 64 : 32;
+    return L < KS ? L : KS;
+}
+
+// The NDC of the WALK iterations t0 .. st->iteration of one persistent launch
+// (the count of iterations is read on the device: nothing waits on the host).
+static void launch_ndc_post(cqg_ctx *ctx, const SweepArgs &a, const IterArgs &ia, uint32_t *keys, int t0) {
+    cudaStream_t s = ctx->stream;
+    const int K = a.K, KS = ndc_key_stride(K);
+    const size_t ksm = 24 * (size_t)K;
+    const unsigned gk = (unsigned)ctx->num_sms * 2;
+    switch (KS) {
+#define CQG_WALK_KEYS(V)                                                                        \
+    case V:                                                                                     \
+        if (ksm > 48 * 1024) CQG_CUDA(ensure_smem((const void *)walk_keys_kernel<V>, ksm));     \
+        walk_keys_kernel<V><<<gk, 1024, ksm, s>>>(ia.snap_cen, K, ia.st, t0, keys);            \
+        break;
+        CQG_WALK_KEYS(32)
+        CQG_WALK_KEYS(64)
+        CQG_WALK_KEYS(128)
+        CQG_WALK_KEYS(256)
+        CQG_WALK_KEYS(512)
+        CQG_WALK_KEYS(1024)
+#undef CQG_WALK_KEYS
+        default: fail(CQG_E_INVALID, "persistent Lloyd: K above 1024");
+    }
+    const int L = ndc_post_prefix(K, KS);
+    const size_t sm = 24 * (size_t)K + (size_t)K * (L + 2) * sizeof(uint16_t);
+    static thread_local size_t c_sm = 0;
+    static thread_local int c_dev = -1, c_bps = 1;
+    if (c_sm != sm || c_dev != ctx->device) {
+        CQG_CUDA(ensure_smem((const void *)ndc_post_kernel<4>, sm));
+        int bps = 0;
+        CQG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, ndc_post_kernel<4>, kNdcPostThreads, sm));
+        c_bps = bps < 1 ? 1 : bps;
+        c_sm = sm;
+        c_dev = ctx->device;
+    }
+    ndc_post_kernel<4><<<(unsigned)ctx->num_sms * c_bps, kNdcPostThreads, sm, s>>>(
+        a.colors, a.n, ia.snap_lab, ia.snap_cen, keys, K, KS, L, ia.st, t0, a.ndc);
+    CQG_CUDA(cudaGetLastError());
+    launched(ctx, 2);
 }
 
 int lloyd_finish(cqg_ctx *ctx, LloydOut &out, uint64_t n, int K) {
@@ -988,6 +1525,30 @@ LloydOut lloyd_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *count
     // (every block builds its own FP32 table: no fc_kernel launch)
     const bool persistent = use_graph && K <= 1024 &&
                             n <= (uint64_t)ctx->dev_sms * 2 * kSweepThreads * 4 * 2;
+    // persistent loop: the walk tables and the NDC leave the loop (deferred
+    // NDC over per-iteration snapshots, win iterations per launch)
+    double *rowmin = nullptr, *snap_cen = nullptr;
+    uint16_t *snap_lab = nullptr;
+    uint32_t *ndc_keys = nullptr;
+    Moments *dmom = nullptr;
+    double *rmpub = nullptr;
+    int win = 0;
+    if (persistent) {
+        const int KS = ndc_key_stride(K);
+        uint64_t w = (uint64_t)limit;
+        const uint64_t wl = (128ull << 20) / (2 * n + 2), wk = (64ull << 20) / (4ull * K * KS);
+        if (w > wl) w = wl;
+        if (w > wk) w = wk;
+        if (ctx->dbg_ndc_win > 0 && w > (uint64_t)ctx->dbg_ndc_win) w = (uint64_t)ctx->dbg_ndc_win;
+        win = w < 1 ? 1 : (int)w;
+        rowmin = static_cast<double *>(ctx->rowmin.ensure(sizeof(double) * (size_t)K));
+        snap_cen = static_cast<double *>(ctx->snap_cen.ensure(24 * (size_t)K * win));
+        snap_lab = static_cast<uint16_t *>(ctx->snap_lab.ensure(2 * n * (size_t)win + 16));
+        ndc_keys = static_cast<uint32_t *>(ctx->ndc_keys.ensure(4 * (size_t)K * KS * win));
+        dmom = static_cast<Moments *>(ctx->dmom.ensure(3 * sizeof(Moments) * (size_t)K));
+        rmpub = static_cast<double *>(ctx->rmpub.ensure(10 * sizeof(double) * (size_t)K));
+        dcode = nullptr; // no walk rows inside the loop
+    }
     CQG_CUDA(cudaMemsetAsync(mom, 0, sizeof(Moments) * (size_t)K, s));
     // one memset for the scalars: queue counter, ndc, flagged, iter_dev, status, swept, shift_inval
     CQG_CUDA(cudaMemsetAsync(qn, 0, 160, s));
@@ -1047,6 +1608,14 @@ LloydOut lloyd_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *count
     ia.shift = shift;
     ia.shift_inval = shift_inval;
     ia.dcode = dcode;
+    a.rowmin = rowmin;
+    ia.rowmin = rowmin;
+    ia.no_walk_rows = persistent ? 1 : 0;
+    ia.snap_cen = snap_cen;
+    ia.snap_lab = snap_lab;
+    ia.win = win;
+    ia.dmom = dmom;
+    ia.rmpub = rmpub;
 
     // The graph path needs no per-iteration host work: used unless history is
     // recorded (per-iteration copies) or kernel profiling is on (per-launch events).
@@ -1060,6 +1629,7 @@ LloydOut lloyd_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *count
         if (persistent) {
             const int pb = prof_begin(ctx);
             if (!launch_persistent(ctx, a, ia, first)) fail(CQG_E_CUDA, "persistent Lloyd kernel does not fit");
+            launch_ndc_post(ctx, a, ia, ndc_keys, first ? 2 : iter + 1);
             rec = prof_end(ctx, CQG_PROF_LLOYD, pb, 0.0);
         } else if (!first && use_graph) {
             cudaGraphExec_t ge = loop_graph(ctx, a, ia, qn);
@@ -1092,8 +1662,7 @@ LloydOut lloyd_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *count
                 out.labels = labels_d;
                 out.bnd = bnd;
                 out.shift = shift;
-                out.dsorted = dsorted;
-                out.dcode = dcode;
+                out.rowmin = rowmin; // the persistent loop built no walk table
                 out.mom = mom;
                 out.Kpow = Kpow;
             }
@@ -1131,8 +1700,12 @@ LloydOut lloyd_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *count
         out.labels = labels_d;
         out.bnd = bnd;
         out.shift = shift;
-        out.dsorted = dsorted;
-                out.dcode = dcode;
+        if (persistent) {
+            out.rowmin = rowmin;
+        } else {
+            out.dsorted = dsorted;
+            out.dcode = dcode;
+        }
         out.mom = mom;
         out.Kpow = Kpow;
     }

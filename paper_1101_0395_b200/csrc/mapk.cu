@@ -361,6 +361,7 @@ double map_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P, const uint32_t *c
         a.bnd = lloyd->bnd;                                  // read only in MODE_MAPW
         a.shift = lloyd->shift;
         a.dsorted = lloyd->dsorted;
+        a.rowmin = lloyd->rowmin;
         a.Kpow = lloyd->Kpow;
         launch_sweep(ctx, MODE_MAPW, a);
     } else {

@@ -62,6 +62,14 @@ struct SweepArgs {
     const float *shift;
     unsigned long long *swept;
     const uint16_t *dcode; // K x Kpow 16-bit monotone codes of dsorted (ndc_code_kernel), or null
+    // persistent Lloyd kernel (no walk table inside the loop): rowmin[k] =
+    // min_{j != k} D[k][j] for the stay test (else dsorted[k][1]); lab_snap
+    // receives every point's label as the filter reads it (deferred NDC)
+    const double *rowmin;
+    uint16_t *lab_snap;
+    // the caller filled the stay test's shared terms (s_aux: shift[K], 2s[K],
+    // max shift, second max, argmax bits) itself
+    int aux_ready;
 };
 
 // mapping result of distinct colour idx (colour c): the LUT the pixel pass
@@ -705,7 +713,7 @@ __device__ __forceinline__ bool prune_needs_sweep(const SweepArgs &a, uint64_t i
 }
 
 // Shared words the pruned WALK sweep needs besides the list: shift[K], 2s[K].
-__host__ __device__ constexpr int prune_aux_words(int K) { return 2 * K; }
+__host__ __device__ constexpr int prune_aux_words(int K) { return 2 * K + 4; }
 #ifndef CQG_FILTER_PPT
 #define CQG_FILTER_PPT 8
 #endif
@@ -728,15 +736,19 @@ __device__ __forceinline__ void sweep_range(const SweepArgs &a, uint64_t lo, uin
     __shared__ uint32_t s_m;
     const int Kp = a.Kp, K = a.K;
     const float ev = 0.5f * tau_abs;
-    const float smax1 = __ldg(a.shift + K), smax2 = __ldg(a.shift + K + 1);
-    const int sarg = __float_as_int(__ldg(a.shift + K + 2));
-    // per-centre terms of the stay test: shift and 2 s (nearest other centre, walk position 1)
-    for (int k = threadIdx.x; k < K; k += blockDim.x) {
-        s_aux[k] = __ldg(a.shift + k);
-        s_aux[K + k] = K > 1 ? __fsqrt_rd(__double2float_rd(
-                                   __dmul_rd(__ldg(a.dsorted + (size_t)k * a.Kpow + 1), 1.0 - 0x1.0p-40)))
-                             : __int_as_float(0x7f800000);
+    if (!a.aux_ready) {
+        // per-centre terms of the stay test: shift and 2 s (nearest other centre, walk position 1)
+        for (int k = threadIdx.x; k < K; k += blockDim.x) {
+            s_aux[k] = __ldg(a.shift + k);
+            const double nearest = a.rowmin ? a.rowmin[k] : __ldg(a.dsorted + (size_t)k * a.Kpow + 1);
+            s_aux[K + k] = K > 1 ? __fsqrt_rd(__double2float_rd(__dmul_rd(nearest, 1.0 - 0x1.0p-40)))
+                                 : __int_as_float(0x7f800000);
+        }
+        if (threadIdx.x < 3) s_aux[2 * K + threadIdx.x] = __ldg(a.shift + K + threadIdx.x);
+        __syncthreads();
     }
+    const float smax1 = s_aux[2 * K], smax2 = s_aux[2 * K + 1];
+    const int sarg = __float_as_int(s_aux[2 * K + 2]);
     constexpr uint32_t big = kSweepThreads * PPT;
     unsigned long long swept = 0;
     if (threadIdx.x == 0) s_m = 0;
@@ -756,6 +768,13 @@ __device__ __forceinline__ void sweep_range(const SweepArgs &a, uint64_t lo, uin
                 lab[f] = v ? a.labels[i] : 0u;
                 bd[f] = v ? a.bnd[i] : make_float2(0.f, 0.f);
                 col[f] = v ? __ldg(a.colors + i) : 0u;
+            }
+            if (a.lab_snap) {
+#pragma unroll
+                for (int f = 0; f < kFilterPPT; ++f) {
+                    const uint64_t i = i0 + threadIdx.x + (uint64_t)f * blockDim.x;
+                    if (i < ce) a.lab_snap[i] = (uint16_t)lab[f];
+                }
             }
 #pragma unroll
             for (int f = 0; f < kFilterPPT; ++f) {
@@ -916,6 +935,57 @@ __device__ __forceinline__ void replay_range(const SweepArgs &a, uint32_t gwarp,
                     accumulate_global(a.mom, best, cnt, r, g, b, +1);
                 }
             }
+        }
+    }
+}
+
+// WALK replay without the sorted walk table (persistent Lloyd kernel): the
+// walk of assign_point_sortmeans visits prev first, then every j with
+// D[prev][j] < cutoff in (D[prev][j], j) order, and keeps the first strict
+// minimum; so the winner is the lexicographic minimum of (d(x, c_j), walk
+// key) with walk key (-1) for prev and (D[prev][j], j) otherwise. Lanes split
+// the centres; D is recomputed as the reference's table holds it (dist2).
+__device__ __forceinline__ void replay_walk_tableless(const SweepArgs &a, uint32_t gwarp, uint32_t warps) {
+    const uint32_t nq = *a.qn;
+    const int lane = threadIdx.x & 31;
+    const double *cen = a.cen;
+    const int K = a.K;
+    for (uint32_t q = gwarp; q < nq; q += warps) {
+        const uint32_t idx = a.queue[q];
+        const uint32_t c = a.colors[idx], cnt = a.counts[idx];
+        const uint32_t r = (c >> 16) & 255u, g = (c >> 8) & 255u, b = c & 255u;
+        const double xr = (double)r, xg = (double)g, xb = (double)b;
+        const int prev = (int)a.labels[idx];
+        const double pr = cen[3 * prev], pg = cen[3 * prev + 1], pb = cen[3 * prev + 2];
+        const double pd = d2_exact(xr, xg, xb, pr, pg, pb);
+        const double cut = __dmul_rn(4.0, pd);
+        double bd = lane == 0 ? pd : 1.0e300, bD = -1.0;
+        int bj = lane == 0 ? prev : 0x7FFFFFFF;
+        for (int j = lane; j < K; j += 32) {
+            if (j == prev) continue;
+            const double D = d2_exact(pr, pg, pb, cen[3 * j], cen[3 * j + 1], cen[3 * j + 2]);
+            if (!(D < cut)) continue;
+            const double d = d2_exact(xr, xg, xb, cen[3 * j], cen[3 * j + 1], cen[3 * j + 2]);
+            if (d < bd || (d == bd && (D < bD || (D == bD && j < bj)))) {
+                bd = d;
+                bD = D;
+                bj = j;
+            }
+        }
+        for (int o = 16; o; o >>= 1) {
+            const double od = __shfl_xor_sync(0xffffffffu, bd, o);
+            const double oD = __shfl_xor_sync(0xffffffffu, bD, o);
+            const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+            if (od < bd || (od == bd && (oD < bD || (oD == bD && oj < bj)))) {
+                bd = od;
+                bD = oD;
+                bj = oj;
+            }
+        }
+        if (lane == 0 && bj != prev) {
+            a.labels[idx] = (uint32_t)bj;
+            accumulate_global(a.mom, bj, cnt, r, g, b, +1);
+            accumulate_global(a.mom, prev, cnt, r, g, b, -1);
         }
     }
 }

@@ -78,12 +78,18 @@ class NumpyShardEngine:
         mom = [g[5 * k: 5 * k + 5] for k in range(K)]
         if any(m[0] == 0 for m in mom):
             return 2, 0.0
-        tot = 0.0
+        terms = []
         for k, (nk, sr, sg, sb, q) in enumerate(mom):
             nd = float(nk)
             self.c[k] = [float(sr) / nd, float(sg) / nd, float(sb) / nd]
-            tot += float(nk * q - (sr * sr + sg * sg + sb * sb)) / nd
-        sse = tot / float(self.P)
+            terms.append(float(nk * q - (sr * sr + sg * sg + sb * sb)) / nd)
+        # the oracle's order: pairwise tree over the next power of two (cq_oracle.c tree_sum)
+        st = 1
+        while st < K:
+            for i in range(0, K - st, 2 * st):
+                terms[i] = terms[i] + terms[i + st]
+            st *= 2
+        sse = terms[0] / float(self.P)
         self.iter += 1
         self.sse.append(sse)
         it = self.iter

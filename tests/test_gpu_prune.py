@@ -178,3 +178,55 @@ def test_quantize_repair_after_deferred_check(ctx, oracle, dup):
     assert np.array_equal(r.mapping.indices, idx)
     assert np.array_equal(r.mapping.quantized.reshape(-1, 3), q)
     assert r.report.mse == mse_e
+
+
+@pytest.fixture(scope="module")
+def ctx_win3():
+    # the persistent loop's deferred-NDC window capped at 3 WALK iterations:
+    # every launch ends in the window-full state and the host relaunches
+    old = os.environ.get("CQG_DBG_NDC_WIN")
+    os.environ["CQG_DBG_NDC_WIN"] = "3"
+    try:
+        c = cabi.Context(0)
+    finally:
+        if old is None:
+            del os.environ["CQG_DBG_NDC_WIN"]
+        else:
+            os.environ["CQG_DBG_NDC_WIN"] = old
+    yield c
+    c.close()
+
+
+def test_deferred_ndc_window_relaunch(ctx_win3, oracle):
+    # cfg2 substrate, 20 iterations in launches of 3: NDC, labels, centres, SSE
+    # bit-exact; then the pipeline (deferred status check -> synchronous rerun)
+    cfg = CONFIGS["cfg2"]
+    img = cfg.image()
+    P = img.shape[0] * img.shape[1]
+    hist = quant.build_histogram(img, ctx=ctx_win3)
+    c, n = hist.packed, hist.counts
+    init = oracle.init_kmeanspp(c, n, P, cfg.k, cfg.seed)
+    dev = _run(ctx_win3, c, n, P, init)
+    ora = oracle.wsm(c, n, P, init, mode=UPDATE_EXACT)
+    assert ora.iterations > 7
+    assert_lloyd_equal(dev, ora, P)
+    qc = quant.QuantizeConfig(method=quant.parse_method("wsm-kpp"), k=cfg.k, seed=cfg.seed)
+    r = quant.run_quantize(img, qc, ctx=ctx_win3)
+    assert r.state.iterations == ora.iterations
+    assert r.state.ndc_total == ora.ndc_total
+    assert np.array_equal(r.palette, ora.centers)
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_deferred_ndc_window_with_repairs(ctx_win3, oracle, seed):
+    rng = np.random.default_rng(2000 + seed)
+    nu = int(rng.integers(60, 400))
+    keys = rng.choice(1 << 24, nu, replace=False).astype(np.uint32)
+    counts = rng.integers(1, 50, nu).astype(np.uint32)
+    P = int(counts.sum())
+    K = int(rng.integers(nu // 4, nu // 2 + 2))
+    pts = quant.unpack_colors(keys).astype(np.float64)
+    init = pts[rng.integers(0, 6, K)] + rng.normal(0, 0.5, (K, 3))
+    dev = _run(ctx_win3, keys, counts, P, init, max_iterations=40)
+    ora = oracle.wsm(keys, counts, P, init, max_it=40, mode=UPDATE_EXACT)
+    assert_lloyd_equal(dev, ora, P)

@@ -114,7 +114,7 @@ def run(name):
     for i, nm in enumerate(names):
         print(f"{nm:14s} {buf[i] / its:8.0f} cycles/iter  {100 * buf[i] / tot:5.1f}%")
     print(f"{'total':14s} {tot / its:8.0f} cycles/iter  (swept {st.swept_total / (st.iterations * len(hist.counts)):.3f})")
-    print(f"  iter_end: centres+status+fc {buf[6] / its:8.0f}  whole body {buf[7] / its:8.0f} cycles/iter")
+    print(f"  finalise (from the barrier): pass 1 {buf[6] / its:8.0f}  + SSE tree and status {buf[7] / its:8.0f} cycles/iter")
     if hasattr(L, "cqg_dbg_sweep_timing"):
         sb = (C.c_ulonglong * 8)()
         L.cqg_dbg_sweep_timing(sb, 0)
