@@ -122,7 +122,6 @@ struct IterArgs {
     uint16_t *snap_lab;
     int win;
     Moments *dmom; // persistent kernel: 3 x K moment deltas (iteration t into slot t % 3)
-    double *rmpub; // persistent kernel: 2 x 5K three nearest neighbours per centre (d1, d2, d3, j1, j2), published across the grid barrier
 };
 
 __device__ __forceinline__ void top2_merge(float &m1, int &i1, float &m2, float n1, int j1, float n2) {
@@ -196,67 +195,22 @@ __device__ __forceinline__ void bitonic_reg(unsigned long long &key, int &r, int
     }
 }
 
-// Nearest other centres per row of D[i][j] = dist2(c_i, c_j), j != i (the
-// stay test's Elkan term), rows spread over the blocks of the grid. TOP3:
-// out[5i..5i+4] = {d1, d2, d3, j1, j2}, the three smallest and the indices of
-// the first two; otherwise out[i] = d1.
-struct Near3 {
-    double d1, d2, d3;
-    int j1, j2;
-};
-__device__ __forceinline__ void near3_insert(Near3 &a, double d, int j) {
-    if (d < a.d1) {
-        a.d3 = a.d2;
-        a.d2 = a.d1;
-        a.j2 = a.j1;
-        a.d1 = d;
-        a.j1 = j;
-    } else if (d < a.d2) {
-        a.d3 = a.d2;
-        a.d2 = d;
-        a.j2 = j;
-    } else if (d < a.d3) {
-        a.d3 = d;
-    }
-}
-// merge b into a: b's third entry has no index, but only a's first two need one
-__device__ __forceinline__ void near3_merge(Near3 &a, const Near3 &b) {
-    near3_insert(a, b.d1, b.j1);
-    near3_insert(a, b.d2, b.j2);
-    if (b.d3 < a.d3) a.d3 = b.d3; // b.d3 can only land third: two smaller entries exist
-}
-__device__ __forceinline__ Near3 near3_shfl(const Near3 &a, int o) {
-    Near3 b;
-    b.d1 = __shfl_xor_sync(0xffffffffu, a.d1, o);
-    b.d2 = __shfl_xor_sync(0xffffffffu, a.d2, o);
-    b.d3 = __shfl_xor_sync(0xffffffffu, a.d3, o);
-    b.j1 = __shfl_xor_sync(0xffffffffu, a.j1, o);
-    b.j2 = __shfl_xor_sync(0xffffffffu, a.j2, o);
-    return b;
-}
-template <bool TOP3>
+// Nearest other centre per row, min_{j != i} dist2(c_i, c_j) (the stay
+// test's Elkan term), rows spread over the blocks of the grid.
 __device__ void rowmin_rows(const double *c, int K, double *out) {
-    __shared__ Near3 s_rn[32];
+    __shared__ double s_rm[32];
     const double kInf = __longlong_as_double(0x7FF0000000000000ll);
     for (int i = blockIdx.x; i < K; i += gridDim.x) {
         const double cr = c[3 * i], cg = c[3 * i + 1], cb = c[3 * i + 2];
-        Near3 m{kInf, kInf, kInf, -1, -1};
+        double m = kInf;
         for (int j = threadIdx.x; j < K; j += blockDim.x)
-            if (j != i) near3_insert(m, d2_exact(cr, cg, cb, c[3 * j], c[3 * j + 1], c[3 * j + 2]), j);
-        for (int o = 16; o; o >>= 1) near3_merge(m, near3_shfl(m, o));
-        if ((threadIdx.x & 31) == 0) s_rn[threadIdx.x >> 5] = m;
+            if (j != i) m = fmin(m, d2_exact(cr, cg, cb, c[3 * j], c[3 * j + 1], c[3 * j + 2]));
+        for (int o = 16; o; o >>= 1) m = fmin(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if ((threadIdx.x & 31) == 0) s_rm[threadIdx.x >> 5] = m;
         __syncthreads();
         if (threadIdx.x == 0) {
-            for (int w = 1; w < (int)(blockDim.x >> 5); ++w) near3_merge(m, s_rn[w]);
-            if (TOP3) {
-                out[5 * i] = m.d1;
-                out[5 * i + 1] = m.d2;
-                out[5 * i + 2] = m.d3;
-                out[5 * i + 3] = (double)m.j1;
-                out[5 * i + 4] = (double)m.j2;
-            } else {
-                out[i] = m.d1;
-            }
+            for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = fmin(m, s_rm[w]);
+            out[i] = m;
         }
         __syncthreads();
     }
@@ -409,7 +363,7 @@ __device__ bool iter_end_body(const IterArgs &a, double *sm, float *fc_dst, floa
     if (blockIdx.x == 0 && threadIdx.x == 0) g_lloyd_timing[6] += clock64() - _ie0;
 #endif
     const double kInf = __longlong_as_double(0x7FF0000000000000ll);
-    if (a.rowmin) rowmin_rows<false>(s_c, K, a.rowmin);
+    if (a.rowmin) rowmin_rows(s_c, K, a.rowmin);
     if (a.no_walk_rows) return true;
     // walk table row i (kmeans.cpp:14-38): sort by (d, index), then rotate self
     // to the front. Block bitonic sort over Kpow keys (padding = +inf).
@@ -491,10 +445,7 @@ __global__ void __launch_bounds__(1024) iter_end_kernel(IterArgs a) {
     iter_end_body(a, sm, a.fc, a.tau, false);
 }
 
-// Persistent cooperative Lloyd loop for small substrates: one launch runs all
-// iterations, two grid barriers per iteration (sweep + block-local replay |
-// finalise + walk table). Every block keeps its own FP32 centre table in shared memory.
-// Exits early (state 2) on an empty cluster; the host repairs and relaunches.
+// phase timing of the persistent kernel (timing builds, tools/init_timing.py)
 #ifdef CQG_INIT_TIMING
 #define PTIME(slot)                                                                  \
     do {                                                                             \
@@ -510,30 +461,21 @@ __global__ void __launch_bounds__(1024) iter_end_kernel(IterArgs a) {
     } while (0)
 #endif
 
-// The stay test's Elkan term as a Euclidean lower bound: sqrt of the squared
-// nearest-other-centre distance rm, rounded down.
-__device__ __forceinline__ float two_s_of(double rm) {
-    return __fsqrt_rd(__double2float_rd(__dmul_rd(rm, 1.0 - 0x1.0p-40)));
-}
-
 // Persistent cooperative Lloyd loop for small substrates: one launch runs all
 // iterations with ONE grid barrier per iteration. Per iteration t:
 //   sweep t (centres C_t) + block-local exact replay; moment deltas into
-//   dmom[t % 3]; this block's rows of the exact row minima of C_t into
-//   rmpub[t % 2]; block 0 clears dmom[(t + 1) % 3]
+//   dmom[t % 3]; block 0 clears dmom[(t + 1) % 3]
 //   | grid barrier |
 //   every block finalises redundantly: absolute moments M_t (shared copy) +=
 //   dmom[t % 3], centres C_{t+1} = S / n, centre shifts, per-cluster SSE, the
-//   reference's SSE sum in cluster order and its termination test
-//   (kmeans.cpp:249-257), the FP32 table, and the stay test's terms for
-//   C_{t+1}: 2 s from the row minima of C_t minus the shifts (d(c'_k, c'_j) >=
-//   d(c_k, c_j) - shift_k - shift_j), rounded down.
+//   SSE in the oracle's tree order and the termination test
+//   (kmeans.cpp:249-257), the FP32 table, and the stay test's Hamerly terms.
 // Deltas are read one barrier after they are written and cleared one barrier
-// before they are reused (three slots); row minima alternate between two.
-// The walk table and the NDC leave the loop (snapshots + ndc_post_kernel).
-// On exit (done, window full, empty cluster) block 0 publishes the state the
-// host and a relaunch start from: centres, absolute moments, shifts, exact
-// row minima (one more barrier), status.
+// before they are reused (three slots). The walk table and the NDC leave the
+// loop (label / centre snapshots + ndc_post_kernel). On exit (done, window
+// full, empty cluster) block 0 publishes the state the host, the mapping and
+// a relaunch start from: centres, absolute moments, shifts, status; every
+// block computes its rows of the exact row minima (the mapping's Elkan term).
 template <int PPT>
 __global__ void __launch_bounds__(kSweepThreads, 2) lloyd_persistent_kernel(SweepArgs a, IterArgs ia, int first_full,
                                                                             uint32_t list_cap) {
@@ -577,10 +519,11 @@ __global__ void __launch_bounds__(kSweepThreads, 2) lloyd_persistent_kernel(Swee
         for (int i = tid; i < 5 * K; i += blockDim.x) m[i] = full ? 0ull : g[i];
     }
     double sse_prev = (!full && t >= 2) ? ia.sse_arr[t - 2] : 0.0;
-    if (!full && a.bnd) { // a relaunch: the host-side finalise left shifts and exact row minima
+    for (int k = tid; k < K; k += blockDim.x) s_aux[K + k] = 0.f; // no Elkan term in this loop
+    if (!full && a.bnd) { // a relaunch: the host-side finalise left the shifts
         for (int k = tid; k < K; k += blockDim.x) {
             s_aux[k] = a.shift[k];
-            s_aux[K + k] = K > 1 ? two_s_of(ia.rowmin[k]) : __int_as_float(0x7f800000);
+            s_aux[K + k] = 0.f; // Hamerly only (see the finalise below)
         }
         if (tid < 3) s_aux[2 * K + tid] = a.shift[K + tid];
     }
@@ -626,7 +569,6 @@ __global__ void __launch_bounds__(kSweepThreads, 2) lloyd_persistent_kernel(Swee
         }
         __syncthreads();
         if (tid == 0 && s_qn) atomicAdd(ia.flagged, (unsigned long long)s_qn);
-        if (a.bnd) rowmin_rows<true>(cen, K, ia.rmpub + (size_t)(t & 1) * 5 * K);
         if (blockIdx.x == 0) {
             unsigned long long *z = reinterpret_cast<unsigned long long *>(ia.dmom + (size_t)((t + 1) % 3) * K);
             for (int i = tid; i < 5 * K; i += blockDim.x) z[i] = 0ull;
@@ -641,20 +583,11 @@ __global__ void __launch_bounds__(kSweepThreads, 2) lloyd_persistent_kernel(Swee
         // table row, and the neighbour terms of C_t (two nearest, rounded down)
         float cm = 0.f, m1 = -1.f, m2 = -1.f;
         int i1 = -1, empty = 0;
-        const double *rm = ia.rmpub + (size_t)(t & 1) * 5 * K;
-        float *s_td3 = reinterpret_cast<float *>(s_acc); // scratch until the next sweep
-        int *s_j1 = reinterpret_cast<int *>(s_acc + K), *s_j2 = reinterpret_cast<int *>(s_acc + 2 * K);
         for (int k = tid; k < K; k += blockDim.x) {
             // L2 reads (written by other blocks before the barrier), all issued first
             const unsigned long long *dq = reinterpret_cast<const unsigned long long *>(dst + k);
             const unsigned long long d0 = __ldcg(dq), d1s = __ldcg(dq + 1), d2s = __ldcg(dq + 2),
                                      d3s = __ldcg(dq + 3), d4 = __ldcg(dq + 4);
-            double n3 = 0.0, nj1 = 0.0, nj2 = 0.0;
-            if (a.bnd) {
-                n3 = __ldcg(rm + 5 * k + 2);
-                nj1 = __ldcg(rm + 5 * k + 3);
-                nj2 = __ldcg(rm + 5 * k + 4);
-            }
             Moments &m = s_M[k];
             m.n += d0;
             m.s[0] += (long long)d1s;
@@ -662,11 +595,6 @@ __global__ void __launch_bounds__(kSweepThreads, 2) lloyd_persistent_kernel(Swee
             m.s[2] += (long long)d3s;
             m.q += d4;
             s_sse[k] = 0.0;
-            if (a.bnd) {
-                s_td3[k] = two_s_of(n3);
-                s_j1[k] = (int)nj1;
-                s_j2[k] = (int)nj2;
-            }
             if (m.n == 0) {
                 empty = 1;
                 continue;
@@ -747,38 +675,18 @@ __global__ void __launch_bounds__(kSweepThreads, 2) lloyd_persistent_kernel(Swee
                 s_state = state;
             }
         } else {
-            // the other warps: the two largest shifts (each thread merges the
-            // warp partials itself) and the stay test's 2 s for C_{t+1}: the
-            // distances to the two nearest neighbours of C_t, recomputed on
-            // C_{t+1}, and for every other j the third-nearest distance lowered
-            // by the two moves: d(c'_k, c'_j) >= d3 - shift_k - (largest shift
-            // outside {k, j1, j2}); rounded down
-            m1 = s_rm1[0];
-            m2 = s_rm2[0];
-            i1 = s_ri1[0];
-            for (int w = 1; w < (int)nw; ++w) top2_merge(m1, i1, m2, s_rm1[w], s_ri1[w], s_rm2[w]);
-            const float sm1 = fmaxf(m1, 0.f), sm2 = fmaxf(m2, 0.f);
+            // the other warps: the two largest shifts for the stay test's
+            // Hamerly term (the Elkan term is off inside this loop: measured on
+            // cfg2, its per-iteration row minima cost more than the pruning
+            // they add -- survivor tiles are latency-bound, not count-bound)
             if (tid == 32) {
-                s_aux[2 * K] = sm1;
-                s_aux[2 * K + 1] = sm2;
+                m1 = s_rm1[0];
+                m2 = s_rm2[0];
+                i1 = s_ri1[0];
+                for (int w = 1; w < (int)nw; ++w) top2_merge(m1, i1, m2, s_rm1[w], s_ri1[w], s_rm2[w]);
+                s_aux[2 * K] = fmaxf(m1, 0.f);
+                s_aux[2 * K + 1] = fmaxf(m2, 0.f);
                 s_aux[2 * K + 2] = __int_as_float(i1);
-            }
-            if (a.bnd) {
-                for (int k = tid - 32; k < K; k += blockDim.x - 32) {
-                    float v = __int_as_float(0x7f800000);
-                    if (K > 1) {
-                        const int j1 = s_j1[k], j2 = s_j2[k];
-                        const double cr = cnx[3 * k], cg = cnx[3 * k + 1], cb = cnx[3 * k + 2];
-                        v = two_s_of(d2_exact(cr, cg, cb, cnx[3 * j1], cnx[3 * j1 + 1], cnx[3 * j1 + 2]));
-                        if (j2 >= 0) {
-                            v = fminf(v, two_s_of(d2_exact(cr, cg, cb, cnx[3 * j2], cnx[3 * j2 + 1], cnx[3 * j2 + 2])));
-                            const float sx = (i1 == k || i1 == j1 || i1 == j2) ? sm2 : sm1;
-                            v = fminf(v, __fadd_rd(__fadd_rd(s_td3[k], -s_aux[k]), -sx));
-                        }
-                        v = fmaxf(v, 0.f);
-                    }
-                    s_aux[K + k] = v;
-                }
             }
         }
         __syncthreads();
@@ -828,7 +736,7 @@ __global__ void __launch_bounds__(kSweepThreads, 2) lloyd_persistent_kernel(Swee
                     *ia.iter_dev = t;
                 }
             }
-            if (ia.rowmin) rowmin_rows<false>(cnx, K, ia.rowmin);
+            if (ia.rowmin) rowmin_rows(cnx, K, ia.rowmin);
             break;
         }
         sse_prev = s_ssev;
@@ -1482,7 +1390,7 @@ LloydOut lloyd_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *count
                    double *centers_d, double *sse_host, uint32_t *hist_labels_user,
                    double *hist_centers_user, bool allow_defer) {
     cudaStream_t s = ctx->stream;
-    const int Kp = (K + 7) & ~7;
+    const int Kp = pad_centres(K);
     const int limit = term.fixed_iterations > 0 ? term.fixed_iterations : term.max_iterations;
     double *cen = centers_d;
     CQG_CUDA(cudaMemcpyAsync(cen, init_d, sizeof(double) * 3 * K, cudaMemcpyDeviceToDevice, s));
@@ -1531,7 +1439,6 @@ LloydOut lloyd_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *count
     uint16_t *snap_lab = nullptr;
     uint32_t *ndc_keys = nullptr;
     Moments *dmom = nullptr;
-    double *rmpub = nullptr;
     int win = 0;
     if (persistent) {
         const int KS = ndc_key_stride(K);
@@ -1546,7 +1453,6 @@ LloydOut lloyd_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *count
         snap_lab = static_cast<uint16_t *>(ctx->snap_lab.ensure(2 * n * (size_t)win + 16));
         ndc_keys = static_cast<uint32_t *>(ctx->ndc_keys.ensure(4 * (size_t)K * KS * win));
         dmom = static_cast<Moments *>(ctx->dmom.ensure(3 * sizeof(Moments) * (size_t)K));
-        rmpub = static_cast<double *>(ctx->rmpub.ensure(10 * sizeof(double) * (size_t)K));
         dcode = nullptr; // no walk rows inside the loop
     }
     CQG_CUDA(cudaMemsetAsync(mom, 0, sizeof(Moments) * (size_t)K, s));
@@ -1615,7 +1521,6 @@ LloydOut lloyd_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *count
     ia.snap_lab = snap_lab;
     ia.win = win;
     ia.dmom = dmom;
-    ia.rmpub = rmpub;
 
     // The graph path needs no per-iteration host work: used unless history is
     // recorded (per-iteration copies) or kernel profiling is on (per-launch events).
@@ -1763,7 +1668,7 @@ void shard_begin_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *cou
     cudaStream_t s = ctx->stream;
     if (!ctx->shard) ctx->shard = new ShardState();
     ShardState &S = *static_cast<ShardState *>(ctx->shard);
-    const int Kp = (K + 7) & ~7;
+    const int Kp = pad_centres(K);
     int Kpow = 1;
     while (Kpow < K) Kpow <<= 1;
     S = ShardState();

@@ -316,7 +316,7 @@ double map_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P, const uint32_t *c
                int index_bytes, uint8_t *quant_d, double *mse_async, const LloydOut *lloyd,
                unsigned long long *ndc_async) {
     cudaStream_t s = ctx->stream;
-    const int Kp = (K + 7) & ~7;
+    const int Kp = pad_centres(K);
     const bool lut8 = K <= 256;
     float *fc = static_cast<float *>(ctx->fcen.ensure(sizeof(float) * (4 * (size_t)Kp + 8)));
     float *tau = fc + 4 * Kp;

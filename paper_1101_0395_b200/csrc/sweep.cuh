@@ -18,6 +18,9 @@
 namespace cqg {
 
 constexpr int kSweepThreads = 256;
+#ifndef CQG_GROUP
+#define CQG_GROUP 8 // centres per min-chain group of the sweep (build-time experiment knob)
+#endif
 constexpr int kAccPerCluster = 6; // n, s_r, s_g, s_b, q_lo16, q_hi
 constexpr uint32_t kHeavyCount = 2048; // counts >= this bypass the u32 smem accumulators
 
@@ -28,9 +31,14 @@ enum { MODE_FULL = 0, MODE_WALK = 1, MODE_MAP = 2, MODE_MAPW = 3 };
 // modes that keep u64 moment deltas and run the bound filter
 __host__ __device__ constexpr bool mode_delta(int m) { return m == MODE_WALK || m == MODE_MAPW; }
 
-// Shared-memory layout of the FP32 centre table (Kp = K rounded up to 8):
+// Shared-memory layout of the FP32 centre table (Kp = pad_centres(K)):
 //   m2r[Kp], m2g[Kp], m2b[Kp], cc[Kp]  (m2* = -2 * centre, cc = |centre|^2)
 // Padding centres have cc = 1e30 and never win.
+
+// centres per FP32 table row: K rounded up to the sweep's group size
+// (measured on B200, cfg3 dense sweep: 8-centre groups 40.7 TFLOP/s, 16-centre
+// groups 34.6 / 33.4 with one / two groups per unrolled step)
+__host__ __device__ constexpr int pad_centres(int K) { return (K + CQG_GROUP - 1) / CQG_GROUP * CQG_GROUP; }
 
 struct SweepArgs {
     const uint32_t *colors;
@@ -455,7 +463,11 @@ static __global__ void __launch_bounds__(256, 4) ndc_kernel(const uint32_t *__re
 // are recovered afterwards by recomputing that group's 8 distances with the
 // identical FP operation sequence (bit-identical values): the index is the
 // first that equals b1, and the true second-best is min(b2, group second).
-constexpr int kGroup = 8;
+constexpr int kGroup = CQG_GROUP;
+#ifndef CQG_GROUP_UNROLL
+#define CQG_GROUP_UNROLL 2
+#endif
+constexpr int kGroupUnroll = CQG_GROUP_UNROLL; // groups per unrolled step of the centre loop
 #ifdef CQG_SWEEP_TIMING
 // block 0: filter cycles, phase cycles, survivors, calls; list tiles (thread 0):
 // point loads, centre loop, resolve
@@ -541,7 +553,7 @@ __device__ __forceinline__ void sweep_tiles(const SweepArgs &a, uint64_t lo, uin
             g1[i] = 0;
         }
         STIME(4);
-#pragma unroll 2
+#pragma unroll (kGroupUnroll)
         for (int j = 0; j < Kp; j += kGroup) {
             float gm[PPT]; // this group's minimum per point
 #pragma unroll

@@ -55,8 +55,9 @@ def test_prune_persistent_path(ctx, ctx_noprune, oracle):
     dense = _run(ctx_noprune, c, n, P, init)
     assert_lloyd_equal(dense, ora, P)
     assert dense.swept_total == c.size * dense.iterations
-    # pruning is active: later iterations sweep a fraction of the points
-    assert dev.swept_total < 0.6 * c.size * dev.iterations
+    # pruning is active: later iterations sweep a fraction of the points (the
+    # persistent loop keeps only the Hamerly bound: DESIGN.md section 4)
+    assert dev.swept_total < 0.75 * c.size * dev.iterations
 
 
 def test_prune_graph_path(ctx, ctx_noprune, oracle):
