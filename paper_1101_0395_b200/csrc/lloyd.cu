@@ -230,23 +230,43 @@ __device__ double tree_sum_block(double *a, int K) {
     return a[0];
 }
 
-// The same tree by one warp (no block barrier): lane l first reduces its
-// aligned segment of L = N / 32 entries in place (the tree's lower levels),
-// then the upper levels run across lanes by shuffles. The sum is in lane 0.
-__device__ double tree_sum_warp(double *a, int K) {
-    const int lane = threadIdx.x & 31;
-    int N = 32;
+// The same tree with every thread of a block (blockDim a power of two, K <=
+// 4 blockDim): thread t sums its aligned segment of L = N / blockDim entries
+// (the tree's lowest levels) in registers, the next five levels run inside the
+// warp by shuffles, the last ones across the warp sums in warp 0. No shared
+// memory bank conflicts (a single lane walking a segment would hit one bank).
+// The sum is returned to thread 0; s_w: one double per warp.
+__device__ double tree_sum_threads(const double *a, int K, double *s_w) {
+    const int nt = blockDim.x, t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    int N = nt;
     while (N < K) N <<= 1;
-    const int L = N >> 5, base = lane * L;
-    for (int st = 1; st < L; st <<= 1)
-        for (int i = base; i + st < base + L; i += 2 * st)
-            if (i + st < K) a[i] = __dadd_rn(a[i], a[i + st]);
-    double v = base < K ? a[base] : 0.0;
-    for (int o = 1; o < 32; o <<= 1) {
-        const double w = __shfl_down_sync(0xffffffffu, v, o);
-        if ((lane & (2 * o - 1)) == 0) v = __dadd_rn(v, w);
+    const int L = N / nt, base = t * L; // L <= 4
+    double v0 = base < K ? a[base] : 0.0;
+    if (L >= 2) {
+        const double v1 = base + 1 < K ? a[base + 1] : 0.0;
+        double u = __dadd_rn(v0, v1);
+        if (L == 4) {
+            const double v2 = base + 2 < K ? a[base + 2] : 0.0, v3 = base + 3 < K ? a[base + 3] : 0.0;
+            u = __dadd_rn(u, __dadd_rn(v2, v3));
+        }
+        v0 = u;
     }
-    return v;
+    for (int o = 1; o < 32; o <<= 1) {
+        const double w = __shfl_down_sync(0xffffffffu, v0, o);
+        if ((lane & (2 * o - 1)) == 0) v0 = __dadd_rn(v0, w);
+    }
+    if (lane == 0) s_w[warp] = v0;
+    __syncthreads();
+    double r = 0.0;
+    if (warp == 0) {
+        const int nw = nt >> 5;
+        r = lane < nw ? s_w[lane] : 0.0;
+        for (int o = 1; o < nw; o <<= 1) {
+            const double w = __shfl_down_sync(0xffffffffu, r, o);
+            if ((lane & (2 * o - 1)) == 0) r = __dadd_rn(r, w);
+        }
+    }
+    return r;
 }
 
 __device__ bool iter_end_body(const IterArgs &a, double *sm, float *fc_dst, float *tau_dst, bool fc_every_block) {
@@ -495,7 +515,7 @@ __global__ void __launch_bounds__(kSweepThreads, 2) lloyd_persistent_kernel(Swee
     __shared__ float s_rmax[8], s_rm1[8], s_rm2[8];
     __shared__ int s_ri1[8], s_rempty[8];
     __shared__ int s_state;
-    __shared__ double s_ssev;
+    __shared__ double s_ssev, s_wsum[32];
     __shared__ uint32_t s_qn;
 
     const uint64_t chunk = (a.n + gridDim.x - 1) / gridDim.x;
@@ -581,19 +601,31 @@ __global__ void __launch_bounds__(kSweepThreads, 2) lloyd_persistent_kernel(Swee
         // ---- finalise iteration t (every block, identical results) ----
         // pass 1, per cluster: moments += deltas, centre, shift, SSE term, FP32
         // table row, and the neighbour terms of C_t (two nearest, rounded down)
+        {
+            // absolute moments += this iteration's deltas: coalesced L2 reads of
+            // the 5K words (other blocks' atomics), all issued before the adds
+            const unsigned long long *dq = reinterpret_cast<const unsigned long long *>(dst);
+            unsigned long long *mq = reinterpret_cast<unsigned long long *>(s_M);
+            const int nwd = 5 * K;
+            for (int e0 = tid; e0 < nwd; e0 += 8 * blockDim.x) {
+                unsigned long long v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int e = e0 + u * blockDim.x;
+                    v[u] = e < nwd ? __ldcg(dq + e) : 0ull;
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int e = e0 + u * blockDim.x;
+                    if (e < nwd) mq[e] += v[u];
+                }
+            }
+        }
+        __syncthreads();
         float cm = 0.f, m1 = -1.f, m2 = -1.f;
         int i1 = -1, empty = 0;
         for (int k = tid; k < K; k += blockDim.x) {
-            // L2 reads (written by other blocks before the barrier), all issued first
-            const unsigned long long *dq = reinterpret_cast<const unsigned long long *>(dst + k);
-            const unsigned long long d0 = __ldcg(dq), d1s = __ldcg(dq + 1), d2s = __ldcg(dq + 2),
-                                     d3s = __ldcg(dq + 3), d4 = __ldcg(dq + 4);
-            Moments &m = s_M[k];
-            m.n += d0;
-            m.s[0] += (long long)d1s;
-            m.s[1] += (long long)d2s;
-            m.s[2] += (long long)d3s;
-            m.q += d4;
+            const Moments &m = s_M[k];
             s_sse[k] = 0.0;
             if (m.n == 0) {
                 empty = 1;
@@ -639,14 +671,12 @@ __global__ void __launch_bounds__(kSweepThreads, 2) lloyd_persistent_kernel(Swee
 #ifdef CQG_INIT_TIMING
         if (blockIdx.x == 0 && tid == 0) g_lloyd_timing[6] += clock64() - _bprev;
 #endif
+        // the SSE in the oracle's tree order (all threads), then thread 0: the
+        // status; thread 32: the sweep's error bound and the largest shifts
+        const double tot = tree_sum_threads(s_sse, K, s_wsum);
         if (warp == 0) {
-            // the SSE in the oracle's tree order, the status and the sweep's error bound
-            const double tot = tree_sum_warp(s_sse, K);
             if (tid == 0) {
-                for (int w = 1; w < (int)nw; ++w) {
-                    cm = fmaxf(cm, s_rmax[w]);
-                    empty |= s_rempty[w];
-                }
+                for (int w = 1; w < (int)nw; ++w) empty |= s_rempty[w];
                 int state = 0;
                 if (empty) {
                     state = 2;
@@ -662,11 +692,6 @@ __global__ void __launch_bounds__(kSweepThreads, 2) lloyd_persistent_kernel(Swee
                     }
                     state = done ? 1 : (t + 1 - t0 >= ia.win ? 3 : 0);
                     s_ssev = sse;
-                    const double u = 0x1.0p-24, X = 255.0, C = (double)cm;
-                    const double E =
-                        u * 3.0 * C * C + u * 2.0 * X * 3.0 * C + 3.0 * u * (3.0 * C * C + 6.0 * X * C);
-                    s_tau[0] = (float)(2.0 * E * 1.0625 + 1.0e-3);
-                    s_tau[1] = 0x1.0p-20f;
                     if (blockIdx.x == 0) {
                         ia.sse_arr[t - 1] = sse;
                         if (t == 1) *ia.ndc += (unsigned long long)ia.n_points * (unsigned long long)K;
@@ -683,10 +708,18 @@ __global__ void __launch_bounds__(kSweepThreads, 2) lloyd_persistent_kernel(Swee
                 m1 = s_rm1[0];
                 m2 = s_rm2[0];
                 i1 = s_ri1[0];
-                for (int w = 1; w < (int)nw; ++w) top2_merge(m1, i1, m2, s_rm1[w], s_ri1[w], s_rm2[w]);
+                cm = s_rmax[0];
+                for (int w = 1; w < (int)nw; ++w) {
+                    top2_merge(m1, i1, m2, s_rm1[w], s_ri1[w], s_rm2[w]);
+                    cm = fmaxf(cm, s_rmax[w]);
+                }
                 s_aux[2 * K] = fmaxf(m1, 0.f);
                 s_aux[2 * K + 1] = fmaxf(m2, 0.f);
                 s_aux[2 * K + 2] = __int_as_float(i1);
+                const double u = 0x1.0p-24, X = 255.0, C = (double)cm;
+                const double E = u * 3.0 * C * C + u * 2.0 * X * 3.0 * C + 3.0 * u * (3.0 * C * C + 6.0 * X * C);
+                s_tau[0] = (float)(2.0 * E * 1.0625 + 1.0e-3);
+                s_tau[1] = 0x1.0p-20f;
             }
         }
         __syncthreads();
