@@ -509,7 +509,6 @@ __global__ void __launch_bounds__(kSweepThreads, 2) lloyd_persistent_kernel(Swee
     float *s_fc = reinterpret_cast<float *>(s_sse + K);       // 4 Kp
     float *s_tau = s_fc + 4 * Kp;                             // 2 (+2 pad)
     uint32_t *s_acc = reinterpret_cast<uint32_t *>(s_tau + 4); // 10 K u32 (= 5 K u64)
-    unsigned long long *s_acc64 = reinterpret_cast<unsigned long long *>(s_acc);
     uint32_t *s_list = s_acc + 10 * K;                        // prune list + carried tile
     float *s_aux = reinterpret_cast<float *>(s_list + list_cap + kSweepThreads * 4); // 2K + 4
     __shared__ float s_rmax[8], s_rm1[8], s_rm2[8];
@@ -526,6 +525,9 @@ __global__ void __launch_bounds__(kSweepThreads, 2) lloyd_persistent_kernel(Swee
     la.queue = a.queue + lo;
     la.qn = &s_qn;
     la.aux_ready = 1;
+    // one flush per sweep when the block owns at most 2048 points (no u32
+    // partial sum can overflow: SM-budgeted contexts give blocks more points)
+    la.flush_at_end = chunk <= 2048 ? 1 : 0;
 
     // entry state: centres C_t, moments M_{t-1} (zero before iteration 1)
     bool full = first_full != 0;
@@ -564,6 +566,7 @@ __global__ void __launch_bounds__(kSweepThreads, 2) lloyd_persistent_kernel(Swee
             __syncthreads();
             sweep_range<MODE_FULL, PPT>(wa, lo, hi, s_fc, s_acc, s_tau[0], s_tau[1]);
             __syncthreads();
+            if (la.flush_at_end) flush_acc(s_acc, dst, K);
             replay_range<MODE_FULL>(wa, warp, nw);
         } else {
             // the NDC of this iteration is counted after the loop (ndc_post_kernel)
@@ -574,7 +577,7 @@ __global__ void __launch_bounds__(kSweepThreads, 2) lloyd_persistent_kernel(Swee
             wa.lab_snap = ia.snap_lab + (size_t)slot * a.n;
             if (a.bnd == nullptr) // no filter pass: copy the labels here
                 for (uint64_t i = lo + tid; i < hi; i += blockDim.x) wa.lab_snap[i] = (uint16_t)a.labels[i];
-            for (int i = tid; i < K * 5; i += blockDim.x) s_acc64[i] = 0;
+            for (int i = tid; i < K * kAccPerCluster; i += blockDim.x) s_acc[i] = 0;
             __syncthreads();
             PTIME(0);
             BTIME(0);
@@ -582,7 +585,7 @@ __global__ void __launch_bounds__(kSweepThreads, 2) lloyd_persistent_kernel(Swee
             __syncthreads();
             PTIME(1);
             BTIME(1);
-            flush_acc64(s_acc64, dst, K);
+            if (la.flush_at_end) flush_acc(s_acc, dst, K);
             replay_walk_tableless(wa, warp, nw);
             PTIME(2);
             BTIME(2);

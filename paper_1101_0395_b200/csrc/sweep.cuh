@@ -78,6 +78,9 @@ struct SweepArgs {
     // the caller filled the stay test's shared terms (s_aux: shift[K], 2s[K],
     // max shift, second max, argmax bits) itself
     int aux_ready;
+    // the caller flushes the u32 shared accumulators once after the sweep
+    // (its whole range has at most 2048 points, so no partial sum can overflow)
+    int flush_at_end;
 };
 
 // mapping result of distinct colour idx (colour c): the LUT the pixel pass
@@ -133,19 +136,6 @@ __device__ __forceinline__ void accumulate(uint32_t *acc, Moments *mom, int k, u
         atomicAdd((unsigned long long *)&mom[k].s[2], (unsigned long long)(sc * (long long)b));
         atomicAdd(&mom[k].q, (unsigned long long)(sc * (long long)qq));
     }
-}
-
-// 64-bit shared accumulators laid out exactly like Moments (n, s[3], q): the
-// WALK-mode block total is flushed with one global add per field.
-__device__ __forceinline__ void accumulate64(unsigned long long *acc, int k, uint32_t cnt, uint32_t r,
-                                             uint32_t g, uint32_t b, int sign) {
-    const long long sc = (long long)sign * (long long)cnt;
-    unsigned long long *m = acc + 5 * k;
-    atomicAdd(m + 0, (unsigned long long)sc);
-    atomicAdd(m + 1, (unsigned long long)(sc * (long long)r));
-    atomicAdd(m + 2, (unsigned long long)(sc * (long long)g));
-    atomicAdd(m + 3, (unsigned long long)(sc * (long long)b));
-    atomicAdd(m + 4, (unsigned long long)(sc * (long long)(r * r + g * g + b * b)));
 }
 
 // global-atomic version (replay / repair paths)
@@ -505,7 +495,7 @@ constexpr int kSmemCentres = 1024; // FP64 centres staged in shared memory up to
 // Sweep points of this block against the FP32 centre table in shared memory
 // (s_fc: m2r | m2g | m2b | cc, Kp each): slots [lo, hi), point index = the
 // slot (LIST = false) or list[slot]. FULL/MAP flush the u32 shared
-// accumulators after every tile; WALK leaves its u64 deltas for the caller.
+// accumulators after every tile (WALK / MAPW: signed deltas, +new -old).
 template <int MODE, int PPT, bool LIST>
 __device__ __forceinline__ void sweep_tiles(const SweepArgs &a, uint64_t lo, uint64_t hi, const uint32_t *list,
                                             float *smem, uint32_t *s_acc, float tau_abs, float tau_rel) {
@@ -513,7 +503,6 @@ __device__ __forceinline__ void sweep_tiles(const SweepArgs &a, uint64_t lo, uin
     constexpr int PP = PPT / 2;
     const int K = a.K, Kp = a.Kp;
     float *s_m2r = smem, *s_m2g = smem + Kp, *s_m2b = smem + 2 * Kp, *s_cc = smem + 3 * Kp;
-    unsigned long long *s_acc64 = reinterpret_cast<unsigned long long *>(s_acc);
     // per-value error bound of the FP32 distances (tau_abs = 2E*1.0625 + 1e-3)
     const float ev = 0.5f * tau_abs;
     const uint64_t tile = (uint64_t)kSweepThreads * PPT;
@@ -669,8 +658,8 @@ __device__ __forceinline__ void sweep_tiles(const SweepArgs &a, uint64_t lo, uin
                 if (!flag && j1 != prev) {
                     const uint32_t cnt = kPre ? pcnt[kPre ? i : 0] : __ldg(a.counts + idx);
                     if (MODE == MODE_WALK) a.labels[idx] = (uint32_t)j1;
-                    accumulate64(s_acc64, j1, cnt, r, g, b, +1);
-                    accumulate64(s_acc64, prev, cnt, r, g, b, -1);
+                    accumulate(s_acc, a.mom, j1, cnt, r, g, b, +1);
+                    accumulate(s_acc, a.mom, prev, cnt, r, g, b, -1);
                 }
             } else if (valid && !flag) {
                 const uint32_t cnt = kPre ? pcnt[kPre ? i : 0] : __ldg(a.counts + idx);
@@ -682,7 +671,10 @@ __device__ __forceinline__ void sweep_tiles(const SweepArgs &a, uint64_t lo, uin
         }
         STIME(6);
         } // warp has points
-        if (!mode_delta(MODE)) {
+        // u32 shared partial sums, flushed every tile (the 64-bit shared
+        // atomics they replace compile to CAS loops: 29% of the cfg5 WALK
+        // sweep's stall samples)
+        if (!a.flush_at_end) {
             __syncthreads();
             flush_acc(s_acc, a.mom, K);
             __syncthreads();
@@ -848,14 +840,6 @@ __device__ __forceinline__ void sweep_range(const SweepArgs &a, uint64_t lo, uin
     if (threadIdx.x == 0 && a.swept && swept) atomicAdd(a.swept, swept);
 }
 
-// Flush the WALK-mode u64 block deltas (laid out as Moments) to the global moments.
-__device__ __forceinline__ void flush_acc64(const unsigned long long *s_acc64, Moments *mom, int K) {
-    for (int e = threadIdx.x; e < K * 5; e += blockDim.x) {
-        const unsigned long long v = s_acc64[e];
-        if (v) atomicAdd(reinterpret_cast<unsigned long long *>(mom) + e, v);
-    }
-}
-
 template <int MODE, int PPT>
 __global__ void __launch_bounds__(kSweepThreads, 2) sweep_kernel(SweepArgs a) {
     pdl_wait();
@@ -863,12 +847,8 @@ __global__ void __launch_bounds__(kSweepThreads, 2) sweep_kernel(SweepArgs a) {
     extern __shared__ __align__(16) float smem[];
     const int K = a.K, Kp = a.Kp;
     uint32_t *s_acc = reinterpret_cast<uint32_t *>(smem + 4 * Kp);
-    unsigned long long *s_acc64 = reinterpret_cast<unsigned long long *>(s_acc);
     for (int i = threadIdx.x; i < 4 * Kp; i += blockDim.x) smem[i] = a.fc[i];
-    if (mode_delta(MODE))
-        for (int i = threadIdx.x; i < K * 5; i += blockDim.x) s_acc64[i] = 0;
-    else
-        for (int i = threadIdx.x; i < K * kAccPerCluster; i += blockDim.x) s_acc[i] = 0;
+    for (int i = threadIdx.x; i < K * kAccPerCluster; i += blockDim.x) s_acc[i] = 0;
     __syncthreads();
     const uint64_t chunk = (a.n + gridDim.x - 1) / gridDim.x;
     const uint64_t lo = (uint64_t)blockIdx.x * chunk;
@@ -876,10 +856,6 @@ __global__ void __launch_bounds__(kSweepThreads, 2) sweep_kernel(SweepArgs a) {
     uint32_t *s_list = reinterpret_cast<uint32_t *>(s_acc) + sweep_acc_words(K);
     float *s_aux = reinterpret_cast<float *>(s_list + kPruneChunk + kSweepThreads * 8);
     sweep_range<MODE, PPT>(a, lo, hi, smem, s_acc, a.tau[0], a.tau[1], s_list, kPruneChunk, s_aux);
-    if (mode_delta(MODE)) {
-        __syncthreads();
-        flush_acc64(s_acc64, a.mom, K);
-    }
 }
 
 // ---------------------------------------------------------------------------
