@@ -212,6 +212,7 @@ cqg_ctx *cqg_create(int device) {
         CQG_CUDA(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
         CQG_CUDA(cudaEventCreateWithFlags(&ctx->aux_fork, cudaEventDisableTiming));
         CQG_CUDA(cudaEventCreateWithFlags(&ctx->aux_join, cudaEventDisableTiming));
+        CQG_CUDA(cudaEventCreateWithFlags(&ctx->lloyd_join, cudaEventDisableTiming));
         const char *ng = getenv("CQG_NO_GRAPH");
         ctx->use_graphs = !(ng && ng[0] == '1');
         const char *nc = getenv("CQG_NO_CLUSTER_INIT");
@@ -273,6 +274,7 @@ void cqg_destroy(cqg_ctx *ctx) {
         cudaStreamDestroy(ctx->aux);
         cudaEventDestroy(ctx->aux_fork);
         cudaEventDestroy(ctx->aux_join);
+        cudaEventDestroy(ctx->lloyd_join);
     }
     delete ctx;
 }
@@ -851,6 +853,8 @@ int cqg_quantize(cqg_ctx *ctx, const uint8_t *rgb, uint64_t P, const cqg_quantiz
             copy_out(ctx, labels, lab_d, 4 * ns);
             copy_out(ctx, indices, idx_d, P * (size_t)ib);
             copy_out(ctx, quantized, q_d, P * 3);
+            // the deferred Lloyd NDC ran on the side stream beside the mapping
+            if (o.pending) CQG_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->lloyd_join, 0));
             CQG_CUDA(cudaStreamSynchronize(ctx->stream)); // the pipeline's last synchronisation
         };
         map_and_copy();

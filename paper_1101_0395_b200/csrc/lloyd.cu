@@ -1568,10 +1568,29 @@ LloydOut lloyd_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *count
         int rec = -1;
         const int before = iter;
         if (persistent) {
+            // a launch rewrites the snapshots an earlier launch's NDC pass reads
+            CQG_CUDA(cudaStreamWaitEvent(s, ctx->lloyd_join, 0));
             const int pb = prof_begin(ctx);
             if (!launch_persistent(ctx, a, ia, first)) fail(CQG_E_CUDA, "persistent Lloyd kernel does not fit");
-            launch_ndc_post(ctx, a, ia, ndc_keys, first ? 2 : iter + 1);
             rec = prof_end(ctx, CQG_PROF_LLOYD, pb, 0.0);
+            // the deferred NDC on the side stream, beside what follows on this
+            // one (the mapping); its counter is read back from there
+            CQG_CUDA(cudaEventRecord(ctx->aux_fork, s));
+            CQG_CUDA(cudaStreamWaitEvent(ctx->aux, ctx->aux_fork, 0));
+            {
+                struct SideStream { // launches and profiling events below go to the side stream
+                    cqg_ctx *c;
+                    cudaStream_t main;
+                    ~SideStream() { c->stream = main; }
+                } side{ctx, s};
+                ctx->stream = ctx->aux;
+                const int pn = prof_begin(ctx);
+                launch_ndc_post(ctx, a, ia, ndc_keys, first ? 2 : iter + 1);
+                prof_end(ctx, CQG_PROF_NDC, pn, 0.0);
+                CQG_CUDA(cudaMemcpyAsync(hsc, reinterpret_cast<unsigned char *>(qn) + 32, 8, cudaMemcpyDeviceToHost,
+                                         ctx->aux));
+                CQG_CUDA(cudaEventRecord(ctx->lloyd_join, ctx->aux));
+            }
         } else if (!first && use_graph) {
             cudaGraphExec_t ge = loop_graph(ctx, a, ia, qn);
             const int pb = prof_begin(ctx);
@@ -1590,8 +1609,12 @@ LloydOut lloyd_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *count
             }
             launch_iter_end(ctx, ia);
         }
-        // one read-back per launch: counters, status (scalars bytes 32..136) and the SSE trace
-        CQG_CUDA(cudaMemcpyAsync(hsc, reinterpret_cast<unsigned char *>(qn) + 32, 104, cudaMemcpyDeviceToHost, s));
+        // one read-back per launch: counters, status (scalars bytes 32..136) and
+        // the SSE trace (the persistent path reads the NDC, bytes 32..40, on the side stream)
+        if (persistent)
+            CQG_CUDA(cudaMemcpyAsync(hsc + 8, reinterpret_cast<unsigned char *>(qn) + 40, 96, cudaMemcpyDeviceToHost, s));
+        else
+            CQG_CUDA(cudaMemcpyAsync(hsc, reinterpret_cast<unsigned char *>(qn) + 32, 104, cudaMemcpyDeviceToHost, s));
         if (sse_host) CQG_CUDA(cudaMemcpyAsync(sse_host, sse_d, sizeof(double) * (size_t)limit, cudaMemcpyDefault, s));
         if (persistent && first && allow_defer) {
             // the persistent kernel ends done (state 1) or on an empty cluster
@@ -1618,7 +1641,8 @@ LloydOut lloyd_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *count
             IterArgs ib = ia;
             ib.reset_qn = persistent ? 1 : 0;
             launch_iter_end(ctx, ib);
-            CQG_CUDA(cudaMemcpyAsync(hsc, reinterpret_cast<unsigned char *>(qn) + 32, 104, cudaMemcpyDeviceToHost, s));
+            // (the persistent path's NDC counter may still be growing on the side stream)
+            CQG_CUDA(cudaMemcpyAsync(hsc + 8, reinterpret_cast<unsigned char *>(qn) + 40, 96, cudaMemcpyDeviceToHost, s));
             if (sse_host) CQG_CUDA(cudaMemcpyAsync(sse_host, sse_d, sizeof(double) * (size_t)limit, cudaMemcpyDefault, s));
             CQG_CUDA(cudaStreamSynchronize(s));
             if (hst->state == 2) fail(CQG_E_RUNTIME, "repair left an empty cluster");
@@ -1630,6 +1654,13 @@ LloydOut lloyd_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *count
     if (hist) {
         if (hist_labels_user) copy_out(ctx, hist_labels_user, hl_d, sizeof(uint32_t) * n * (size_t)iter);
         if (hist_centers_user) copy_out(ctx, hist_centers_user, hc_d, 24 * (size_t)K * iter);
+        CQG_CUDA(cudaStreamSynchronize(s));
+    }
+    if (persistent) {
+        // the NDC counter after the side stream's last pass (and any repair's
+        // finalise on this stream; the repair also reuses the pinned buffer)
+        CQG_CUDA(cudaStreamWaitEvent(s, ctx->lloyd_join, 0));
+        CQG_CUDA(cudaMemcpyAsync(hsc, reinterpret_cast<unsigned char *>(qn) + 32, 8, cudaMemcpyDeviceToHost, s));
         CQG_CUDA(cudaStreamSynchronize(s));
     }
     const unsigned long long *hcnt = reinterpret_cast<const unsigned long long *>(hsc); // ndc, flagged
