@@ -153,22 +153,15 @@ __device__ __forceinline__ void accumulate_global(Moments *mom, int k, uint32_t 
 // Flush the block accumulators (interpreted as signed 32-bit partial sums;
 // at most 2048 light points per flush keeps every partial below 2^31).
 __device__ __forceinline__ void flush_acc(uint32_t *acc, Moments *mom, int K) {
+    // word f of cluster k goes to Moments field min(f, 4) (n, s_r, s_g, s_b, q);
+    // word 5 holds q's high part (x 65536). Branch-free addressing.
+    unsigned long long *m64 = reinterpret_cast<unsigned long long *>(mom);
     for (int e = threadIdx.x; e < K * kAccPerCluster; e += blockDim.x) {
         const int v = (int)acc[e];
         if (v != 0) {
             const int k = e / kAccPerCluster, f = e - k * kAccPerCluster;
-            const long long lv = (long long)v;
-            unsigned long long *dst;
-            long long add = lv;
-            switch (f) {
-                case 0: dst = &mom[k].n; break;
-                case 1: dst = (unsigned long long *)&mom[k].s[0]; break;
-                case 2: dst = (unsigned long long *)&mom[k].s[1]; break;
-                case 3: dst = (unsigned long long *)&mom[k].s[2]; break;
-                case 4: dst = &mom[k].q; break;
-                default: dst = &mom[k].q; add = lv * 65536; break;
-            }
-            atomicAdd(dst, (unsigned long long)add);
+            const long long lv = (long long)v * (f == 5 ? 65536 : 1);
+            atomicAdd(m64 + 5 * k + (f < 4 ? f : 4), (unsigned long long)lv);
             acc[e] = 0;
         }
     }
@@ -591,7 +584,16 @@ __device__ __forceinline__ void sweep_tiles(const SweepArgs &a, uint64_t lo, uin
             }
         }
         STIME(5);
-        // resolve
+        // resolve: larger tiles load every point's label and count here, all
+        // in flight together (small tiles issued them with the colours)
+        uint32_t rlab[kPre ? 1 : PPT], rcnt[kPre ? 1 : PPT];
+        if (!kPre) {
+#pragma unroll
+            for (int i = 0; i < PPT; ++i) {
+                rlab[kPre ? 0 : i] = mode_delta(MODE) ? a.labels[pidx[i]] : 0u;
+                rcnt[kPre ? 0 : i] = __ldg(a.counts + pidx[i]);
+            }
+        }
 #pragma unroll
         for (int i = 0; i < PPT; ++i) {
             const uint32_t idx = pidx[i];
@@ -653,16 +655,16 @@ __device__ __forceinline__ void sweep_tiles(const SweepArgs &a, uint64_t lo, uin
             }
             const uint32_t r = (col[i] >> 16) & 255u, g = (col[i] >> 8) & 255u, b = col[i] & 255u;
             if (mode_delta(MODE) && valid) {
-                const int prev = kPre ? (int)plab[kPre ? i : 0] : (int)a.labels[idx];
+                const int prev = kPre ? (int)plab[kPre ? i : 0] : (int)rlab[kPre ? 0 : i];
                 if (MODE == MODE_MAPW && !flag) map_store(a, col[i], idx, (uint32_t)j1);
                 if (!flag && j1 != prev) {
-                    const uint32_t cnt = kPre ? pcnt[kPre ? i : 0] : __ldg(a.counts + idx);
+                    const uint32_t cnt = kPre ? pcnt[kPre ? i : 0] : rcnt[kPre ? 0 : i];
                     if (MODE == MODE_WALK) a.labels[idx] = (uint32_t)j1;
                     accumulate(s_acc, a.mom, j1, cnt, r, g, b, +1);
                     accumulate(s_acc, a.mom, prev, cnt, r, g, b, -1);
                 }
             } else if (valid && !flag) {
-                const uint32_t cnt = kPre ? pcnt[kPre ? i : 0] : __ldg(a.counts + idx);
+                const uint32_t cnt = kPre ? pcnt[kPre ? i : 0] : rcnt[kPre ? 0 : i];
                 if (MODE == MODE_FULL) a.labels[idx] = (uint32_t)j1;
                 else map_store(a, col[i], idx, (uint32_t)j1);
                 accumulate(s_acc, a.mom, j1, cnt, r, g, b, +1);
