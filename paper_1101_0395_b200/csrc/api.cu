@@ -213,6 +213,8 @@ cqg_ctx *cqg_create(int device) {
         CQG_CUDA(cudaEventCreateWithFlags(&ctx->aux_fork, cudaEventDisableTiming));
         CQG_CUDA(cudaEventCreateWithFlags(&ctx->aux_join, cudaEventDisableTiming));
         CQG_CUDA(cudaEventCreateWithFlags(&ctx->lloyd_join, cudaEventDisableTiming));
+        CQG_CUDA(cudaEventCreateWithFlags(&ctx->lloyd_fork, cudaEventDisableTiming));
+        CQG_CUDA(cudaStreamCreateWithFlags(&ctx->aux2, cudaStreamNonBlocking));
         const char *ng = getenv("CQG_NO_GRAPH");
         ctx->use_graphs = !(ng && ng[0] == '1');
         const char *nc = getenv("CQG_NO_CLUSTER_INIT");
@@ -272,9 +274,14 @@ void cqg_destroy(cqg_ctx *ctx) {
     if (ctx->aux) {
         cudaStreamSynchronize(ctx->aux);
         cudaStreamDestroy(ctx->aux);
+        if (ctx->aux2) {
+            cudaStreamSynchronize(ctx->aux2);
+            cudaStreamDestroy(ctx->aux2);
+        }
         cudaEventDestroy(ctx->aux_fork);
         cudaEventDestroy(ctx->aux_join);
         cudaEventDestroy(ctx->lloyd_join);
+        cudaEventDestroy(ctx->lloyd_fork);
     }
     delete ctx;
 }

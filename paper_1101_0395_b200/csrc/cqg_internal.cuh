@@ -110,7 +110,8 @@ struct cqg_ctx {
     bool own_stream = false;
     cudaStream_t aux = nullptr;            // side stream for independent work (mapping NDC)
     cudaEvent_t aux_fork = nullptr, aux_join = nullptr;
-    cudaEvent_t lloyd_join = nullptr;      // the persistent Lloyd loop's NDC pass (side stream) is done
+    cudaStream_t aux2 = nullptr;           // second side stream: the persistent Lloyd loop's NDC pass
+    cudaEvent_t lloyd_fork = nullptr, lloyd_join = nullptr; // ... forked after the loop, done
     cudaEvent_t stage_ev[8] = {}; // cqg_quantize stage timing (created once per context)
     unsigned long long launches = 0;
 

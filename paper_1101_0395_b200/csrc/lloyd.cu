@@ -861,7 +861,13 @@ __global__ void __launch_bounds__(kNdcPostThreads) ndc_post_kernel(const uint32_
     const int rs = L + 2;
     const int nt = st->iteration - t0 + 1;
     if (nt <= 0) return;
-    const uint64_t nch = (n + kNdcPostChunk - 1) / kNdcPostChunk;
+    // chunks sized so that (table, chunk) items roughly fill the grid once:
+    // a multiple of one batch (Q x threads), at least kNdcPostChunk / 4
+    constexpr uint64_t batch = (uint64_t)Q * kNdcPostThreads;
+    uint64_t csz = ((uint64_t)nt * n + gridDim.x - 1) / gridDim.x;
+    csz = (csz + batch - 1) / batch * batch;
+    if (csz < kNdcPostChunk / 4) csz = kNdcPostChunk / 4;
+    const uint64_t nch = (n + csz - 1) / csz;
     const uint64_t items = (uint64_t)nt * nch;
     const uint64_t per = (items + gridDim.x - 1) / gridDim.x;
     const uint64_t i0 = (uint64_t)blockIdx.x * per, i1 = i0 + per < items ? i0 + per : items;
@@ -869,8 +875,8 @@ __global__ void __launch_bounds__(kNdcPostThreads) ndc_post_kernel(const uint32_
     int cur = -1;
     for (uint64_t it = i0; it < i1; ++it) {
         const int tab = (int)(it / nch);
-        const uint64_t p0 = (it - (uint64_t)tab * nch) * kNdcPostChunk;
-        const uint64_t p1 = p0 + kNdcPostChunk < n ? p0 + kNdcPostChunk : n;
+        const uint64_t p0 = (it - (uint64_t)tab * nch) * csz;
+        const uint64_t p1 = p0 + csz < n ? p0 + csz : n;
         const uint32_t *tkeys = keys + (size_t)tab * K * KS;
         if (tab != cur) {
             __syncthreads();
@@ -1575,21 +1581,21 @@ LloydOut lloyd_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *count
             rec = prof_end(ctx, CQG_PROF_LLOYD, pb, 0.0);
             // the deferred NDC on the side stream, beside what follows on this
             // one (the mapping); its counter is read back from there
-            CQG_CUDA(cudaEventRecord(ctx->aux_fork, s));
-            CQG_CUDA(cudaStreamWaitEvent(ctx->aux, ctx->aux_fork, 0));
+            CQG_CUDA(cudaEventRecord(ctx->lloyd_fork, s));
+            CQG_CUDA(cudaStreamWaitEvent(ctx->aux2, ctx->lloyd_fork, 0));
             {
                 struct SideStream { // launches and profiling events below go to the side stream
                     cqg_ctx *c;
                     cudaStream_t main;
                     ~SideStream() { c->stream = main; }
                 } side{ctx, s};
-                ctx->stream = ctx->aux;
+                ctx->stream = ctx->aux2;
                 const int pn = prof_begin(ctx);
                 launch_ndc_post(ctx, a, ia, ndc_keys, first ? 2 : iter + 1);
                 prof_end(ctx, CQG_PROF_NDC, pn, 0.0);
                 CQG_CUDA(cudaMemcpyAsync(hsc, reinterpret_cast<unsigned char *>(qn) + 32, 8, cudaMemcpyDeviceToHost,
-                                         ctx->aux));
-                CQG_CUDA(cudaEventRecord(ctx->lloyd_join, ctx->aux));
+                                         ctx->aux2));
+                CQG_CUDA(cudaEventRecord(ctx->lloyd_join, ctx->aux2));
             }
         } else if (!first && use_graph) {
             cudaGraphExec_t ge = loop_graph(ctx, a, ia, qn);
