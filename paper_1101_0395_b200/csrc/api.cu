@@ -214,6 +214,8 @@ cqg_ctx *cqg_create(int device) {
         CQG_CUDA(cudaEventCreateWithFlags(&ctx->aux_join, cudaEventDisableTiming));
         CQG_CUDA(cudaEventCreateWithFlags(&ctx->lloyd_join, cudaEventDisableTiming));
         CQG_CUDA(cudaEventCreateWithFlags(&ctx->lloyd_fork, cudaEventDisableTiming));
+        CQG_CUDA(cudaEventCreateWithFlags(&ctx->walk_fork, cudaEventDisableTiming));
+        CQG_CUDA(cudaEventCreateWithFlags(&ctx->walk_join, cudaEventDisableTiming));
         CQG_CUDA(cudaStreamCreateWithFlags(&ctx->aux2, cudaStreamNonBlocking));
         const char *ng = getenv("CQG_NO_GRAPH");
         ctx->use_graphs = !(ng && ng[0] == '1');
@@ -239,6 +241,8 @@ cqg_ctx *cqg_create(int device) {
         ctx->use_prune = !(np && np[0] == '1');
         const char *nn = getenv("CQG_NO_NDC_CODE");
         ctx->use_ndc_code = !(nn && nn[0] == '1');
+        const char *nf = getenv("CQG_NO_FILTER_LIST");
+        ctx->use_filter_list = !(nf && nf[0] == '1');
         const char *nw = getenv("CQG_DBG_NDC_WIN");
         if (nw) ctx->dbg_ndc_win = atoi(nw);
     });
@@ -261,7 +265,7 @@ void cqg_destroy(cqg_ctx *ctx) {
                       &ctx->status, &ctx->sizes, &ctx->red, &ctx->hist_labels, &ctx->hist_centers,
                       &ctx->sse, &ctx->lut, &ctx->idx_out, &ctx->q_out, &ctx->mom_map, &ctx->coarse, &ctx->mind2,
                       &ctx->initpart, &ctx->initsel, &ctx->unit_draws, &ctx->inittile, &ctx->mom_g, &ctx->partial, &ctx->shard_log,
-                      &ctx->bnd, &ctx->shift, &ctx->dcode, &ctx->rowmin, &ctx->snap_cen, &ctx->snap_lab, &ctx->ndc_keys, &ctx->dmom, &ctx->rmpub,
+                      &ctx->bnd, &ctx->shift, &ctx->dcode, &ctx->rowmin, &ctx->snap_cen, &ctx->snap_lab, &ctx->ndc_keys, &ctx->dmom, &ctx->survivors,
                       &ctx->sub_img, &ctx->raw_col, &ctx->raw_cnt,
                       &ctx->full_col, &ctx->full_cnt, &ctx->map_rows, &ctx->map_lab, &ctx->pcnt, &ctx->pent, &ctx->pseg};
     for (DevBuf *b : bufs) b->release();
@@ -282,6 +286,8 @@ void cqg_destroy(cqg_ctx *ctx) {
         cudaEventDestroy(ctx->aux_join);
         cudaEventDestroy(ctx->lloyd_join);
         cudaEventDestroy(ctx->lloyd_fork);
+        cudaEventDestroy(ctx->walk_fork);
+        cudaEventDestroy(ctx->walk_join);
     }
     delete ctx;
 }

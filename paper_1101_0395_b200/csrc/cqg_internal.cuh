@@ -112,6 +112,7 @@ struct cqg_ctx {
     cudaEvent_t aux_fork = nullptr, aux_join = nullptr;
     cudaStream_t aux2 = nullptr;           // second side stream: the persistent Lloyd loop's NDC pass
     cudaEvent_t lloyd_fork = nullptr, lloyd_join = nullptr; // ... forked after the loop, done
+    cudaEvent_t walk_fork = nullptr, walk_join = nullptr;   // large WALK iterations: NDC beside the stay-test pass
     cudaEvent_t stage_ev[8] = {}; // cqg_quantize stage timing (created once per context)
     unsigned long long launches = 0;
 
@@ -129,7 +130,8 @@ struct cqg_ctx {
     cqg::DevBuf labels, cen, fcen, dtab, dsorted, order, mom, queue, ndc, status, sizes, red;
     cqg::DevBuf hist_labels, hist_centers, sse;
     cqg::DevBuf bnd, shift, dcode;
-    cqg::DevBuf rowmin, snap_cen, snap_lab, ndc_keys, dmom, rmpub; // persistent Lloyd: stay-test row minima, deferred-NDC snapshots
+    cqg::DevBuf rowmin, snap_cen, snap_lab, ndc_keys, dmom;
+    cqg::DevBuf survivors; // WALK survivor list of filter_list_kernel (+ its counter) // persistent Lloyd: stay-test row minima, deferred-NDC snapshots
     cqg::DevBuf sub_img, raw_col, raw_cnt, full_col, full_cnt; // sampling modes     // distance-bound pruning: per-point (ub, lb), centre moves
     cqg::DevBuf mom_g, partial, shard_log; // sharded Lloyd: global moments, packed partials, state log
     void *shard = nullptr;      // cqg::ShardState (lloyd.cu)
@@ -155,6 +157,7 @@ struct cqg_ctx {
     uint64_t init_tile_min = 1ull << 20; // ... from this many points (CQG_INIT_TILE_MIN; below, the record layout is as fast)
     bool use_ndc_code = true; // shared-memory code table for the NDC count (CQG_NO_NDC_CODE=1: off)
     bool use_prune = true; // distance-bound pruning of the WALK sweep (CQG_NO_PRUNE=1: off)
+    bool use_filter_list = true; // large substrates: stay-test pass + survivor-list sweep (CQG_NO_FILTER_LIST=1: off)
     bool lloyd_prune_pending = false; // the deferred Lloyd run pruned (lloyd_finish)
     cudaGraphExec_t loop_exec = nullptr;
     cudaGraph_t loop_graph = nullptr;

@@ -1084,11 +1084,63 @@ static void launch_ppt(cqg_ctx *ctx, const SweepArgs &a, size_t smem, int bps) {
     else launch_pdl(sweep_kernel<MODE, PPT>, (unsigned)grid, kSweepThreads, smem, ctx->stream, a);
 }
 
+// Shared-memory attributes of the list sweep and its blocks per SM (cached
+// per device and size; called once before any graph capture).
+static int sweep_list_setup(cqg_ctx *ctx, int K, int Kp) {
+    const size_t lsm = (size_t)4 * Kp * sizeof(float) + (size_t)sweep_acc_words(K) * sizeof(uint32_t);
+    static thread_local size_t c_lsm = (size_t)-1;
+    static thread_local int c_dev = -1, c_bps = 1;
+    if (c_lsm != lsm || c_dev != ctx->device) {
+        CQG_CUDA(ensure_smem((const void *)sweep_list_kernel<8>, lsm));
+        int bps = 0;
+        CQG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, sweep_list_kernel<8>, kSweepThreads, lsm));
+        c_bps = bps < 1 ? 1 : bps;
+        c_lsm = lsm;
+        c_dev = ctx->device;
+    }
+    return c_bps;
+}
+
 template <int MODE>
 static void launch_sweep_mode(cqg_ctx *ctx, const SweepArgs &a) {
     const size_t smem = sweep_smem_bytes(a.K, a.Kp, MODE);
     const uint64_t n = a.n;
     const uint64_t sms = (uint64_t)ctx->num_sms;
+    if (MODE == MODE_WALK && a.surv) {
+        // the NDC, then one stay-test pass writing a survivor list, then the
+        // list sweep (buffers and kernel attributes set up before any graph
+        // capture: sweep_list_setup)
+        uint32_t *list = a.surv;
+        uint32_t *listn = list + n + 4;
+        // the NDC (reads the labels before the sweep changes them) runs on the
+        // second side stream beside the stay-test pass, joined before the sweep
+        const size_t cs = (size_t)a.K * 24 + (size_t)a.K * (a.Kpow + 2) * 2;
+        const int gc = pick_grid(ctx, n, 1024 * 4, 1);
+        CQG_CUDA(cudaEventRecord(ctx->walk_fork, ctx->stream));
+        CQG_CUDA(cudaStreamWaitEvent(ctx->aux2, ctx->walk_fork, 0));
+        ndc_code_kernel<4><<<gc, 1024, cs, ctx->aux2>>>(a.colors, a.labels, n, a.cen, a.dsorted, a.dcode, a.K,
+                                                       a.Kpow, a.ndc);
+        CQG_CUDA(cudaEventRecord(ctx->walk_join, ctx->aux2));
+        CQG_CUDA(cudaMemsetAsync(listn, 0, 4, ctx->stream));
+        const size_t fsm = filter_list_smem(a.K, a.Kp);
+        const int gf = pick_grid(ctx, n, kFilterThreads * kFilterQ, 8);
+        const int pb = prof_begin(ctx);
+        filter_list_kernel<<<(unsigned)gf, kFilterThreads, fsm, ctx->stream>>>(a, list, listn);
+        CQG_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->walk_join, 0));
+        const size_t lsm = (size_t)4 * a.Kp * sizeof(float) + (size_t)sweep_acc_words(a.K) * sizeof(uint32_t);
+        const int bps = sweep_list_setup(ctx, a.K, a.Kp);
+        sweep_list_kernel<8><<<(unsigned)(sms * bps), kSweepThreads, lsm, ctx->stream>>>(a, list, listn);
+        prof_end(ctx, CQG_PROF_SWEEP, pb, (double)n * (double)a.K);
+        const int rg = pick_grid(ctx, n * 32 / 256 + 1, 256, 2);
+        const int pr = prof_begin(ctx);
+        replay_kernel<MODE><<<rg, 256, 0, ctx->stream>>>(a);
+        prof_end(ctx, CQG_PROF_REPLAY, pr, 0.0);
+        CQG_CUDA(cudaGetLastError());
+        launched(ctx, 4);
+        std::memcpy(ctx->last_sweep, &a, sizeof(SweepArgs));
+        ctx->have_last_sweep = true;
+        return;
+    }
     if (MODE == MODE_WALK) {
         const size_t csm = a.K <= 2048 ? (size_t)a.K * 24 : 0;
         if (csm > 48 * 1024) { // ensure_smem caches per (device, kernel)
@@ -1558,6 +1610,12 @@ LloydOut lloyd_dev(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *count
     ia.dcode = dcode;
     a.rowmin = rowmin;
     ia.rowmin = rowmin;
+    if (!persistent && prune && dcode && K <= kNdcCodeMaxK && Kpow >= 8 && ctx->use_filter_list) {
+        a.surv = static_cast<uint32_t *>(ctx->survivors.ensure(4 * (n + 8)));
+        CQG_CUDA(ensure_smem((const void *)ndc_code_kernel<4>,
+                             kNdcCodeMaxK * 24 + kNdcCodeMaxK * (kNdcCodeMaxK + 2) * 2));
+        sweep_list_setup(ctx, K, Kp);
+    }
     ia.no_walk_rows = persistent ? 1 : 0;
     ia.snap_cen = snap_cen;
     ia.snap_lab = snap_lab;

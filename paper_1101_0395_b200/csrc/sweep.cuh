@@ -81,6 +81,9 @@ struct SweepArgs {
     // the caller flushes the u32 shared accumulators once after the sweep
     // (its whole range has at most 2048 points, so no partial sum can overflow)
     int flush_at_end;
+    // WALK with bounds on large substrates: survivor list (n entries + a
+    // counter at n + 4) for filter_list_kernel / sweep_list_kernel, or null
+    uint32_t *surv;
 };
 
 // mapping result of distinct colour idx (colour c): the LUT the pixel pass
@@ -840,6 +843,115 @@ __device__ __forceinline__ void sweep_range(const SweepArgs &a, uint64_t lo, uin
     }
 #endif
     if (threadIdx.x == 0 && a.swept && swept) atomicAdd(a.swept, swept);
+}
+
+// Large substrates, WALK iterations with bounds: one light pass runs the stay
+// test over every point (bounds of stayers rewritten) and appends the points
+// that may change label to a global survivor list; sweep_list_kernel then
+// sweeps only the list in full 8-point tiles, with no filter or list
+// bookkeeping in the 128-register sweep. (The NDC stays in its own kernel:
+// fused into this pass it made a 1-block-per-SM latency-bound kernel, 216 us
+// against 109 + ~70 us separately on cfg5.) List order is irrelevant: every
+// per-point result is deterministic and moments are integer sums.
+constexpr int kFilterThreads = 256;
+constexpr int kFilterQ = 8;
+__host__ __device__ constexpr size_t filter_list_smem(int K, int Kp) {
+    return (size_t)4 * Kp * 4 + (size_t)prune_aux_words(K) * 4;
+}
+static __global__ void __launch_bounds__(kFilterThreads) filter_list_kernel(SweepArgs a, uint32_t *list,
+                                                                          uint32_t *listn) {
+    extern __shared__ __align__(16) float s_ff[];
+    __shared__ uint32_t s_wcnt[64]; // per-warp survivor counts, then each warp's first list slot
+    const int K = a.K, Kp = a.Kp, Kpow = a.Kpow;
+    float *s_fc = s_ff;              // 4 Kp
+    float *s_aux = s_fc + 4 * Kp;    // 2K + 4
+    for (int i = threadIdx.x; i < 4 * Kp; i += blockDim.x) s_fc[i] = a.fc[i];
+    for (int k = threadIdx.x; k < K; k += blockDim.x) {
+        s_aux[k] = __ldg(a.shift + k);
+        s_aux[K + k] = K > 1 ? __fsqrt_rd(__double2float_rd(__dmul_rd(__ldg(a.dsorted + (size_t)k * Kpow + 1),
+                                                                        1.0 - 0x1.0p-40)))
+                             : __int_as_float(0x7f800000);
+    }
+    if (threadIdx.x < 3) s_aux[2 * K + threadIdx.x] = __ldg(a.shift + K + threadIdx.x);
+    __syncthreads();
+    const float ev = 0.5f * __ldg(a.tau);
+    const float smax1 = s_aux[2 * K], smax2 = s_aux[2 * K + 1];
+    const int sarg = __float_as_int(s_aux[2 * K + 2]);
+    constexpr int Q = kFilterQ;
+    const uint64_t n = a.n;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * Q;
+    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x * Q; base < n; base += stride) {
+        uint32_t col[Q], lab[Q];
+        float2 bd[Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const uint64_t i = base + threadIdx.x + (uint64_t)q * blockDim.x;
+            const uint64_t ic = i < n ? i : 0;
+            col[q] = __ldg(a.colors + ic);
+            lab[q] = a.labels[ic];
+            bd[q] = a.bnd[ic];
+        }
+        // stay test; the batch's survivors are appended with ONE global atomic
+        // per block (a per-warp atomic on the single counter serialised)
+        uint32_t need = 0;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const uint64_t i = base + threadIdx.x + (uint64_t)q * blockDim.x;
+            if (i < n && prune_needs_sweep(a, i, lab[q], bd[q], col[q], s_fc, s_aux, Kp, ev, smax1, smax2, sarg, true))
+                need |= 1u << q;
+        }
+        uint32_t wm[Q], wc = 0;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            wm[q] = __ballot_sync(0xffffffffu, (need >> q) & 1u);
+            wc += __popc(wm[q]);
+        }
+        if (lane == 0) s_wcnt[warp] = wc;
+        __syncthreads();
+        if (warp == 0) {
+            const uint32_t c = lane < (int)(blockDim.x >> 5) ? s_wcnt[lane] : 0u;
+            uint32_t incl = c;
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+            uint32_t b0 = 0;
+            if (lane == 0 && tot) b0 = atomicAdd(listn, tot);
+            b0 = __shfl_sync(0xffffffffu, b0, 0);
+            s_wcnt[32 + lane] = b0 + incl - c; // each warp's first slot
+        }
+        __syncthreads();
+        uint32_t slot = s_wcnt[32 + warp];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const uint64_t i = base + threadIdx.x + (uint64_t)q * blockDim.x;
+            if ((need >> q) & 1u) list[slot + __popc(wm[q] & lane_lt_mask())] = (uint32_t)i;
+            slot += __popc(wm[q]);
+        }
+        __syncthreads(); // s_wcnt is rewritten by the next batch
+    }
+}
+
+// The survivor list of filter_list_kernel, swept in full PPT-point tiles
+// (blocks stride over the tiles; the count is read on the device).
+template <int PPT>
+static __global__ void __launch_bounds__(kSweepThreads, 2) sweep_list_kernel(SweepArgs a, const uint32_t *list,
+                                                                             const uint32_t *listn) {
+    extern __shared__ __align__(16) float smem[];
+    const int K = a.K, Kp = a.Kp;
+    uint32_t *s_acc = reinterpret_cast<uint32_t *>(smem + 4 * Kp);
+    for (int i = threadIdx.x; i < 4 * Kp; i += blockDim.x) smem[i] = a.fc[i];
+    for (int i = threadIdx.x; i < K * kAccPerCluster; i += blockDim.x) s_acc[i] = 0;
+    __syncthreads();
+    const uint64_t m = *listn;
+    constexpr uint64_t tile = (uint64_t)kSweepThreads * PPT;
+    for (uint64_t lo = (uint64_t)blockIdx.x * tile; lo < m; lo += (uint64_t)gridDim.x * tile) {
+        const uint64_t hi = lo + tile < m ? lo + tile : m;
+        sweep_tiles<MODE_WALK, PPT, true>(a, lo, hi, list, smem, s_acc, __ldg(a.tau), __ldg(a.tau + 1));
+    }
+    if (threadIdx.x == 0 && a.swept && m && blockIdx.x == 0) atomicAdd(a.swept, m);
 }
 
 template <int MODE, int PPT>

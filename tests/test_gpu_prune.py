@@ -231,3 +231,28 @@ def test_deferred_ndc_window_with_repairs(ctx_win3, oracle, seed):
     dev = _run(ctx_win3, keys, counts, P, init, max_iterations=40)
     ora = oracle.wsm(keys, counts, P, init, max_it=40, mode=UPDATE_EXACT)
     assert_lloyd_equal(dev, ora, P)
+
+
+def test_prune_graph_path_in_sweep_filter(oracle):
+    # CQG_NO_FILTER_LIST=1: the stay test inside the sweep kernel (no separate
+    # survivor-list pass) on the graph path; bit-exact like the default
+    old = os.environ.get("CQG_NO_FILTER_LIST")
+    os.environ["CQG_NO_FILTER_LIST"] = "1"
+    try:
+        c0 = cabi.Context(0)
+    finally:
+        if old is None:
+            del os.environ["CQG_NO_FILTER_LIST"]
+        else:
+            os.environ["CQG_NO_FILTER_LIST"] = old
+    try:
+        img = synth_image(1400, 1400, 909, nblobs=40, sigma=30.0, noise=0.5)
+        P = img.shape[0] * img.shape[1]
+        hist = quant.build_histogram(img, ctx=c0)
+        c, n = hist.packed, hist.counts
+        init = oracle.init_maximin(c, n, P, 64, 909)
+        dev = _run(c0, c, n, P, init, max_iterations=12)
+        ora = oracle.wsm(c, n, P, init, max_it=12, mode=UPDATE_EXACT)
+        assert_lloyd_equal(dev, ora, P)
+    finally:
+        c0.close()
