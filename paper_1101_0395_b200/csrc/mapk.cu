@@ -404,9 +404,9 @@ double map_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P, const uint32_t *c
         if (crow) {
             // the rows as 16-bit codes in every block's shared memory (K <= 256)
             const size_t sm = (size_t)K * 24 + (size_t)K * (Kpow + 2) * 2;
-            CQG_CUDA(ensure_smem((const void *)map_ndc_kernel<true, 4, 1024>, sm));
-            const uint64_t g = (n + 4096 - 1) / 4096, gmax = (uint64_t)ctx->num_sms;
-            map_ndc_kernel<true, 4, 1024><<<(unsigned)(g < gmax ? g : gmax), 1024, sm, s>>>(
+            CQG_CUDA(ensure_smem((const void *)map_ndc_kernel<true, 4, 512>, sm));
+            const uint64_t g = (n + 2048 - 1) / 2048, gmax = (uint64_t)ctx->num_sms;
+            map_ndc_kernel<true, 4, 512><<<(unsigned)(g < gmax ? g : gmax), 512, sm, s>>>(
                 colors_d, n, a.maplab8, a.maplab32, pal_d, K, Kpow, rows, crow, ndc_d);
         } else {
             // FP64 rows through L1/L2
