@@ -535,17 +535,19 @@ def measure(args, cfg, env, steps, warmup, e2e_on=True, parity_on=True):
     sses = [np.zeros(128) for _ in range(nworkers)]
     pool = ThreadPoolExecutor(nworkers) if nworkers > 1 else None
 
-    def run_batch(srcs, idxs, qs, pals):
+    def run_batch(srcs, idxs, qs, pals, labs=None):
         # every worker stream starts after the timing stream's current point
-        # and the timing stream waits for all of them
+        # and the timing stream waits for all of them; labs: per-image buffers
+        # for ClusterState::memberships (the e2e run copies them back too)
+        lab = (lambda i: labs[i]) if labs is not None else (lambda i: None)
         if nworkers == 1:
-            return [ctx.quantize_raw(srcs[i], P_list[i], mkcfg(ks[i]), None, pals[i], None, sses[0],
+            return [ctx.quantize_raw(srcs[i], P_list[i], mkcfg(ks[i]), None, pals[i], lab(i), sses[0],
                                      idxs[i], qs[i]) for i in range(len(imgs))]
         for ws in wstreams:
             ws.wait_stream(stream)
 
         def work(w):
-            return [(i, ctxs[w].quantize_raw(srcs[i], P_list[i], mkcfg(ks[i]), None, pals[i], None,
+            return [(i, ctxs[w].quantize_raw(srcs[i], P_list[i], mkcfg(ks[i]), None, pals[i], lab(i),
                                              sses[w], idxs[i], qs[i]))
                     for i in range(w, len(imgs), nworkers)]
         res = dict(kv for part in pool.map(work, range(nworkers)) for kv in part)
@@ -727,14 +729,15 @@ def measure(args, cfg, env, steps, warmup, e2e_on=True, parity_on=True):
         h_idx = [torch.empty(P, dtype=torch.int32).pin_memory() for P in P_list]
         h_q = [torch.empty((P, 3), dtype=torch.uint8).pin_memory() for P in P_list]
         h_pal = [np.empty((k, 3)) for k in ks]
+        h_lab = [torch.empty(P, dtype=torch.int32).pin_memory() for P in P_list]  # N' <= P memberships
         for _ in range(max(1, warmup // 2)):
-            run_batch(h_imgs, h_idx, h_q, h_pal)
+            run_batch(h_imgs, h_idx, h_q, h_pal, h_lab)
         e_ms = []
         for s in range(steps):
             flush.fill_(s & 255)
             torch.cuda.synchronize()
             ev0.record(stream)
-            run_batch(h_imgs, h_idx, h_q, h_pal)
+            run_batch(h_imgs, h_idx, h_q, h_pal, h_lab)
             ev1.record(stream)
             torch.cuda.synchronize()
             e_ms.append(ev0.elapsed_time(ev1))
@@ -743,7 +746,9 @@ def measure(args, cfg, env, steps, warmup, e2e_on=True, parity_on=True):
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
         e_step = float(et.item()) / steps
         h2d = sum(3 * P for P in P_list)
-        d2h = sum(7 * P + 24 * k + 8 * 100 for P, k in zip(P_list, ks))
+        # indices (u32) + quantized RGB + palette + SSE trace + memberships (u32 per distinct colour)
+        nus = [st.n_unique for st in all_stats[-1]] if len(all_stats[-1]) == len(P_list) else [P for P in P_list]
+        d2h = sum(7 * P + 24 * k + 8 * 100 + 4 * nu for P, k, nu in zip(P_list, ks, nus))
         e2e = {"value": pixels_per_step_all / (e_step / 1e3) / 1e6, "unit": UNIT,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e_step,
                "index_layout": "uint32 per pixel (MappingResult::indices)"}
