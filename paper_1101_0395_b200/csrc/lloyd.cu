@@ -1084,6 +1084,14 @@ static void launch_ppt(cqg_ctx *ctx, const SweepArgs &a, size_t smem, int bps) {
     else launch_pdl(sweep_kernel<MODE, PPT>, (unsigned)grid, kSweepThreads, smem, ctx->stream, a);
 }
 
+#ifndef CQG_LIST_PPT
+#define CQG_LIST_PPT 4
+#endif
+constexpr int kListPPT = CQG_LIST_PPT; // points per thread of the survivor-list sweep (build-time knob)
+#ifndef CQG_DENSE_PPT
+#define CQG_DENSE_PPT 8
+#endif
+constexpr int kDensePPT = CQG_DENSE_PPT; // largest points per thread of the range sweeps (build-time knob)
 // Shared-memory attributes of the list sweep and its blocks per SM (cached
 // per device and size; called once before any graph capture).
 static int sweep_list_setup(cqg_ctx *ctx, int K, int Kp) {
@@ -1091,9 +1099,9 @@ static int sweep_list_setup(cqg_ctx *ctx, int K, int Kp) {
     static thread_local size_t c_lsm = (size_t)-1;
     static thread_local int c_dev = -1, c_bps = 1;
     if (c_lsm != lsm || c_dev != ctx->device) {
-        CQG_CUDA(ensure_smem((const void *)sweep_list_kernel<8>, lsm));
+        CQG_CUDA(ensure_smem((const void *)sweep_list_kernel<kListPPT>, lsm));
         int bps = 0;
-        CQG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, sweep_list_kernel<8>, kSweepThreads, lsm));
+        CQG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, sweep_list_kernel<kListPPT>, kSweepThreads, lsm));
         c_bps = bps < 1 ? 1 : bps;
         c_lsm = lsm;
         c_dev = ctx->device;
@@ -1129,7 +1137,7 @@ static void launch_sweep_mode(cqg_ctx *ctx, const SweepArgs &a) {
         CQG_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->walk_join, 0));
         const size_t lsm = (size_t)4 * a.Kp * sizeof(float) + (size_t)sweep_acc_words(a.K) * sizeof(uint32_t);
         const int bps = sweep_list_setup(ctx, a.K, a.Kp);
-        sweep_list_kernel<8><<<(unsigned)(sms * bps), kSweepThreads, lsm, ctx->stream>>>(a, list, listn);
+        sweep_list_kernel<kListPPT><<<(unsigned)(sms * bps), kSweepThreads, lsm, ctx->stream>>>(a, list, listn);
         prof_end(ctx, CQG_PROF_SWEEP, pb, (double)n * (double)a.K);
         const int rg = pick_grid(ctx, n * 32 / 256 + 1, 256, 2);
         const int pr = prof_begin(ctx);
@@ -1168,7 +1176,7 @@ static void launch_sweep_mode(cqg_ctx *ctx, const SweepArgs &a) {
     const int b2 = sweep_bps<MODE, 2>(ctx, smem), b4 = sweep_bps<MODE, 4>(ctx, smem), b8 = sweep_bps<MODE, 8>(ctx, smem);
     int ppt, bps;
     if (n <= sms * b2 * kSweepThreads * 2) ppt = 2, bps = b2;
-    else if (n <= sms * b4 * kSweepThreads * 4) ppt = 4, bps = b4;
+    else if (n <= sms * b4 * kSweepThreads * 4 || kDensePPT == 4) ppt = 4, bps = b4;
     else ppt = 8, bps = b8;
     uint64_t grid = sms * (uint64_t)bps;
     const uint64_t cap = (n + 63) / 64; // at least 64 points per block
@@ -1208,7 +1216,7 @@ void bench_sweep_dev(cqg_ctx *ctx, int reps, double *ms, double *units) {
               b8 = sweep_bps<MODE_WALK, 8>(ctx, smem);
     int ppt, bps;
     if (n <= sms * b2 * kSweepThreads * 2) ppt = 2, bps = b2;
-    else if (n <= sms * b4 * kSweepThreads * 4) ppt = 4, bps = b4;
+    else if (n <= sms * b4 * kSweepThreads * 4 || kDensePPT == 4) ppt = 4, bps = b4;
     else ppt = 8, bps = b8;
     uint64_t grid = sms * (uint64_t)bps;
     const uint64_t cap = (n + 63) / 64;
