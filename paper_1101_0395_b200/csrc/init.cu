@@ -815,6 +815,9 @@ __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long
 __device__ __forceinline__ void st_release_u64(unsigned long long *p, unsigned long long v) {
     asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 constexpr int kTileBitmapWords = 1 << 19; // 2^24 Morton slots
 
 __device__ __forceinline__ uint32_t tile_spread8(uint32_t x) {
@@ -1360,9 +1363,13 @@ __global__ void __launch_bounds__(kInitThreads, 3) init_kernel_tile(InitArgs a) 
 #endif
             if (threadIdx.x == 0) a.result[2] = v;
             __syncthreads();
-            // release every block through its own word (no single hot L2 line)
+            // release every block through its own word (no single hot L2 line):
+            // one gpu-scope fence per thread (cumulative over the pick, which
+            // the block barrier ordered before it), then relaxed stores -- a
+            // st.release per word would fence once per store
+            __threadfence();
             for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x)
-                st_release_u64(a.tflags + (size_t)b * kFlagStride, (unsigned long long)k);
+                st_relaxed_u64(a.tflags + (size_t)b * kFlagStride, (unsigned long long)k);
             __syncthreads(); // block 0's own threads read the pick below
             GTIME(2);
         } else {
