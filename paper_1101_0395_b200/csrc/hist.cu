@@ -128,29 +128,123 @@ __global__ void hist_emit_fused(const uint32_t *__restrict__ list, const uint32_
     }
 }
 
-// one thread per pixel, in pixel order: a set bit is a first occurrence whose
-// rank is the word prefix plus the set bits below it, so the stores of a warp
-// land on consecutive ranks (the colour comes from the image itself)
-__global__ void __launch_bounds__(kThreads) hist_emit(const uint8_t *__restrict__ rgb, uint64_t P,
+// The per-colour counts come from bucket_agg as a saturating u8 table (16 MiB:
+// it stays in L2 between the aggregation and the emit, where the 64 MiB u32
+// table was re-read from DRAM by one sector per gather); a count >= 255 is in
+// the sparse u32 side table.
+__device__ __forceinline__ uint32_t count_of(const uint8_t *__restrict__ cnt8, const uint32_t *__restrict__ cnt32,
+                                             uint32_t c) {
+    const uint32_t n = __ldg(cnt8 + c);
+    return n == 255u ? __ldg(cnt32 + c) : n;
+}
+
+// pixel order, 512 pixels per warp pass (16 per lane: 48 bytes and one bitmap
+// half-word). A set bit is a first occurrence whose rank is the word prefix
+// plus the set bits below it. Each lane drops its first occurrences (colour,
+// pixel offset) into the warp's shared-memory row at rank - warp base; the warp
+// then walks the row with all lanes busy: count gathers in flight together,
+// stores on consecutive ranks. The image loads do not depend on the preceding
+// kernels and are issued before the dependency wait.
+constexpr int kEmitWarps = kThreads / 32;
+__global__ void __launch_bounds__(kThreads) hist_emit16(const uint8_t *__restrict__ rgb, uint64_t groups,
+                                                       const uint32_t *__restrict__ bitmap,
+                                                       const uint32_t *__restrict__ wpref,
+                                                       const uint8_t *__restrict__ cnt8,
+                                                       const uint32_t *__restrict__ cnt32,
+                                                       uint32_t *__restrict__ colors, uint32_t *__restrict__ counts,
+                                                       uint32_t *__restrict__ first) {
+    __shared__ uint32_t s_col[kEmitWarps][512];
+    __shared__ uint16_t s_off[kEmitWarps][512];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x; // a multiple of 32: a warp's groups stay consecutive
+    uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    uint4 a = {}, b = {}, d = {};
+    if (g < groups) {
+        const uint4 *src = reinterpret_cast<const uint4 *>(rgb + g * 48);
+        a = ld_stream(src);
+        b = ld_stream(src + 1);
+        d = ld_stream(src + 2);
+    }
+    pdl_wait();
+    pdl_trigger();
+    for (uint64_t g0 = g - lane; g0 < groups; g0 += stride, g += stride) { // warp-uniform trip count
+        const bool v = g < groups;
+        const uint32_t word = v ? __ldg(bitmap + (g >> 1)) : 0u;
+        const uint32_t hi = (uint32_t)(g & 1);
+        const uint32_t bits = (word >> (16 * hi)) & 0xFFFFu;
+        const uint32_t rank = v ? __ldg(wpref + (g >> 1)) + (hi ? __popc(word & 0xFFFFu) : 0u) : 0u;
+        uint4 na = {}, nb = {}, nd = {};
+        if (g + stride < groups) {
+            const uint4 *src = reinterpret_cast<const uint4 *>(rgb + (g + stride) * 48);
+            na = ld_stream(src);
+            nb = ld_stream(src + 1);
+            nd = ld_stream(src + 2);
+        }
+        const uint32_t base = __shfl_sync(0xffffffffu, rank, 0);
+        // the warp's first occurrences: the last valid lane's rank + its bits
+        uint32_t endr = rank + __popc(bits);
+        endr = __reduce_max_sync(0xffffffffu, v ? endr : 0u);
+        const uint32_t total = endr > base ? endr - base : 0u;
+        if (bits) {
+            uint32_t col[16];
+            decode16(a, b, d, col);
+            uint32_t r = rank - base;
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                if ((bits >> j) & 1u) {
+                    s_col[warp][r] = col[j];
+                    s_off[warp][r] = (uint16_t)(lane * 16 + j);
+                    ++r;
+                }
+        }
+        __syncwarp();
+        for (uint32_t i0 = 0; i0 < total; i0 += 128) {
+            uint32_t c[4], n[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t i = i0 + u * 32 + lane;
+                c[u] = i < total ? s_col[warp][i] : 0u;
+                n[u] = i < total ? __ldg(cnt8 + c[u]) : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t i = i0 + u * 32 + lane;
+                if (i < total) {
+                    colors[base + i] = c[u];
+                    counts[base + i] = n[u] == 255u ? __ldg(cnt32 + c[u]) : n[u];
+                    if (first) first[base + i] = (uint32_t)(g0 * 16 + s_off[warp][i]);
+                }
+            }
+        }
+        __syncwarp();
+        a = na;
+        b = nb;
+        d = nd;
+    }
+}
+
+// one thread per pixel from p0 on: the tail of hist_emit16, or the whole image
+// when it is not 16-byte aligned
+__global__ void __launch_bounds__(kThreads) hist_emit(const uint8_t *__restrict__ rgb, uint64_t p0, uint64_t P,
                                                      const uint32_t *__restrict__ bitmap,
                                                      const uint32_t *__restrict__ wpref,
-                                                     const uint32_t *__restrict__ cnt,
+                                                     const uint8_t *__restrict__ cnt8,
+                                                     const uint32_t *__restrict__ cnt32,
                                                      uint32_t *__restrict__ colors, uint32_t *__restrict__ counts,
                                                      uint32_t *__restrict__ first) {
     pdl_wait();
     pdl_trigger();
-    for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < P;
+    for (uint64_t p = p0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < P;
          p += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t w = p >> 5;
         const uint32_t bits = __ldg(bitmap + w);
         const uint32_t b = (uint32_t)(p & 31);
         if (!((bits >> b) & 1u)) continue;
         const uint32_t rank = __ldg(wpref + w) + __popc(bits & ((1u << b) - 1u));
-        // image bytes streamed (evict-first), so the per-colour counts stay in L2
         const uint32_t c = ((uint32_t)__ldcs(rgb + 3 * p) << 16) | ((uint32_t)__ldcs(rgb + 3 * p + 1) << 8) |
                            __ldcs(rgb + 3 * p + 2);
         colors[rank] = c;
-        counts[rank] = __ldg(cnt + c);
+        counts[rank] = count_of(cnt8, cnt32, c);
         if (first) first[rank] = (uint32_t)p;
     }
 }
@@ -363,18 +457,19 @@ __global__ void __launch_bounds__(kPartThreads) part_scatter(const uint8_t *__re
 // one block per bucket (largest first): count and first pixel per colour in
 // shared memory. Each warp takes a contiguous slice of the bucket's entries;
 // a lane tracks the chunk segment its entry falls in (the segment starts are
-// in shared memory, entries only move forward), so the pixel index is
-// chunk * g + offset with no search and no idle lanes at segment ends.
+// in shared memory, entries only move forward). The minimum is kept on the key
+// (chunk << 18 | offset), which orders as the pixel index does (offset < chunk
+// size <= 2^18), and decoded to chunk * g + offset at the end.
 __global__ void __launch_bounds__(kAggThreads) bucket_agg(const uint32_t *__restrict__ ent,
                                                           const uint32_t *__restrict__ gcnt, int G, uint64_t chunk,
                                                           const uint32_t *__restrict__ bstart,
                                                           const uint32_t *__restrict__ bsize,
                                                           const uint32_t *__restrict__ border,
-                                                          uint32_t *__restrict__ cnt_out,
+                                                          uint8_t *__restrict__ cnt8, uint32_t *__restrict__ cnt32,
                                                           uint32_t *__restrict__ bitmap) {
     pdl_wait();
     pdl_trigger();
-    extern __shared__ uint32_t s_tab[]; // kSlots counts | kSlots minimum pixel indices | G + 1 segment starts
+    extern __shared__ __align__(16) uint32_t s_tab[]; // kSlots counts | kSlots minimum keys | G + 1 segment starts
     uint32_t *s_cnt = s_tab, *s_min = s_tab + kSlots, *s_seg = s_tab + 2 * kSlots;
     const uint32_t b = border[blockIdx.x];
     const uint32_t bs = bstart[b], bn = bsize[b];
@@ -386,11 +481,11 @@ __global__ void __launch_bounds__(kAggThreads) bucket_agg(const uint32_t *__rest
     if (threadIdx.x == 0) s_seg[G] = bn;
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    constexpr int kWarps = kAggThreads / 32, U = 4; // U entries per lane in flight
+    constexpr int kWarps = kAggThreads / 32, U = 8; // U entries per lane in flight
     const uint32_t per = (bn + kWarps - 1) / kWarps;
     const uint32_t w0 = per * warp < bn ? per * warp : bn, w1 = w0 + per < bn ? w0 + per : bn;
     // the segment of entry w0 + lane: first g with s_seg[g + 1] > e
-    int g = 0;
+    uint32_t g = 0;
     {
         int lo = 0, hi = G - 1;
         const uint32_t e = w0 + lane;
@@ -399,49 +494,71 @@ __global__ void __launch_bounds__(kAggThreads) bucket_agg(const uint32_t *__rest
             if (s_seg[mid] <= e) lo = mid;
             else hi = mid - 1;
         }
-        g = lo;
+        g = (uint32_t)lo;
     }
-    for (uint32_t e0 = w0; e0 < w1; e0 += 32 * U) { // warp-uniform trip count
-        uint32_t x[U];
+    for (uint32_t e0 = w0;; e0 += 32) { // warp-uniform control flow throughout
+        // full batches: no bounds tests. One vote per batch looks for a first
+        // row of a single colour (flat regions): that row takes the careful
+        // path below, which folds a one-colour row into one update.
+        for (; e0 < w1 && w1 - e0 >= 32 * U; e0 += 32 * U) {
+            uint32_t x[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const uint32_t e = e0 + u * 32 + lane;
-            x[u] = e < w1 ? __ldcs(ent + bs + e) : 0u;
-        }
+            for (int u = 0; u < U; ++u) x[u] = __ldcs(ent + bs + e0 + u * 32 + lane);
+            const uint32_t x0slot = x[0] & (kSlots - 1);
+            if (__all_sync(0xffffffffu, x0slot == __shfl_sync(0xffffffffu, x0slot, 0))) break;
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const uint32_t e = e0 + u * 32 + lane;
-            const bool v = e < w1;
-            if (!__any_sync(0xffffffffu, v)) break;
-            if (v)
-                while (s_seg[g + 1] <= e) ++g; // entries only move forward
-            const uint32_t slot = x[u] & (kSlots - 1);
-            const uint32_t p = (uint32_t)((uint64_t)g * chunk + (x[u] >> kSlotBits));
-            const uint32_t act = __ballot_sync(0xffffffffu, v);
-            const int lead = __ffs(act) - 1;
-            const uint32_t s_first = __shfl_sync(0xffffffffu, slot, lead);
-            if (__all_sync(0xffffffffu, !v || slot == s_first)) {
-                // one colour across the warp (flat images): one update per warp
-                const uint32_t pm = __reduce_min_sync(0xffffffffu, v ? p : 0xFFFFFFFFu);
-                if (lane == lead) {
-                    atomicAdd(&s_cnt[slot], (uint32_t)__popc(act));
-                    atomicMin(&s_min[slot], pm);
-                }
-            } else if (v) {
+            for (int u = 0; u < U; ++u) {
+                const uint32_t e = e0 + u * 32 + lane;
+                while (s_seg[g + 1] <= e) ++g;
+                const uint32_t slot = x[u] & (kSlots - 1);
+                const uint32_t key = (g << kChunkBits) | (x[u] >> kSlotBits);
                 atomicAdd(&s_cnt[slot], 1u);
-                if (p < s_min[slot]) atomicMin(&s_min[slot], p); // most later occurrences skip the atomic
+                if (key < s_min[slot]) atomicMin(&s_min[slot], key); // most later occurrences skip the atomic
             }
+        }
+        if (e0 >= w1) break;
+        const uint32_t e = e0 + lane;
+        const bool v = e < w1;
+        const uint32_t x = v ? __ldcs(ent + bs + e) : 0u;
+        if (v)
+            while (s_seg[g + 1] <= e) ++g;
+        const uint32_t slot = x & (kSlots - 1);
+        const uint32_t key = (g << kChunkBits) | (x >> kSlotBits);
+        const uint32_t act = __ballot_sync(0xffffffffu, v);
+        const int lead = __ffs(act) - 1;
+        const uint32_t s_first = __shfl_sync(0xffffffffu, slot, lead);
+        if (__all_sync(0xffffffffu, !v || slot == s_first)) {
+            // one colour across the warp: one update per warp
+            const uint32_t km = __reduce_min_sync(0xffffffffu, v ? key : 0xFFFFFFFFu);
+            if (lane == lead) {
+                atomicAdd(&s_cnt[slot], (uint32_t)__popc(act));
+                atomicMin(&s_min[slot], km);
+            }
+        } else if (v) {
+            atomicAdd(&s_cnt[slot], 1u);
+            if (key < s_min[slot]) atomicMin(&s_min[slot], key);
         }
     }
     __syncthreads();
-    uint32_t *dst = cnt_out + ((size_t)b << kSlotBits);
-    for (int i = threadIdx.x; i < kSlots; i += kAggThreads) {
-        const uint32_t c = s_cnt[i];
-        dst[i] = c; // stays in L2 for the emit's gathers
-        if (c) {
-            const uint32_t f = s_min[i];
-            atomicOr(&bitmap[f >> 5], 1u << (f & 31));
+    // four slots per thread: one packed u8x4 store; the u32 side table only
+    // where a count saturates
+    uint32_t *dst8 = reinterpret_cast<uint32_t *>(cnt8 + ((size_t)b << kSlotBits));
+    uint32_t *dst32 = cnt32 + ((size_t)b << kSlotBits);
+    for (int q = threadIdx.x; q < kSlots / 4; q += kAggThreads) {
+        const uint4 c4 = reinterpret_cast<const uint4 *>(s_cnt)[q];
+        const uint4 m4 = reinterpret_cast<const uint4 *>(s_min)[q];
+        const uint32_t c[4] = {c4.x, c4.y, c4.z, c4.w}, m[4] = {m4.x, m4.y, m4.z, m4.w};
+        uint32_t packed = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            packed |= (c[j] < 255u ? c[j] : 255u) << (8 * j);
+            if (c[j] >= 255u) dst32[4 * q + j] = c[j];
+            if (c[j]) {
+                const uint64_t f = (uint64_t)(m[j] >> kChunkBits) * chunk + (m[j] & ((1u << kChunkBits) - 1u));
+                atomicOr(&bitmap[f >> 5], 1u << (f & 31));
+            }
         }
+        dst8[q] = packed;
     }
 }
 
@@ -554,7 +671,7 @@ __global__ void pack_kernel(const uint8_t *__restrict__ rgb, uint64_t S, uint32_
 // large images: the bucketed partition (part_count .. bucket_agg) into the
 // first-occurrence bitmap and the per-colour counts
 static void histogram_partitioned(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P, uint32_t *bitmap,
-                                  uint32_t *&cnt_out) {
+                                  uint8_t *&cnt8, uint32_t *&cnt32) {
     cudaStream_t s = ctx->stream;
     // chunks of at most 2^18 pixels (an entry's offset field), a multiple of 16
     // pixels (48-byte vector loads), about 4 per SM
@@ -566,7 +683,9 @@ static void histogram_partitioned(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P
     uint32_t *gcnt = static_cast<uint32_t *>(ctx->pseg.ensure(sizeof(uint32_t) * ((size_t)kBuckets * G + 3 * kBuckets)));
     uint32_t *bsize = gcnt + (size_t)kBuckets * G, *bstart = bsize + kBuckets, *border = bstart + kBuckets;
     uint32_t *ent = static_cast<uint32_t *>(ctx->pent.ensure(sizeof(uint32_t) * P));
-    cnt_out = static_cast<uint32_t *>(ctx->pcnt.ensure(sizeof(uint32_t) << 24));
+    // per-colour counts: u32 side table (only saturated entries are written or read) | u8 table
+    cnt32 = static_cast<uint32_t *>(ctx->pcnt.ensure((sizeof(uint32_t) + sizeof(uint8_t)) << 24));
+    cnt8 = reinterpret_cast<uint8_t *>(cnt32 + (1u << 24));
     part_count<<<G, kPartThreads, 0, s>>>(rgb_d, P, chunk, vec, gcnt, G);
     launch_pdl(seg_scan, kBuckets, 256, 0, s, gcnt, G, bsize);
     launch_pdl(bucket_scan, 1, kBuckets, 0, s, bsize, bstart, border);
@@ -574,7 +693,7 @@ static void histogram_partitioned(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P
     launch_pdl(part_scatter, G, kPartThreads, kScatterSmem, s, rgb_d, P, chunk, vec, gcnt, G, bstart, ent);
     const size_t agg_smem = sizeof(uint32_t) * (2 * kSlots + (size_t)G + 1);
     CQG_CUDA(ensure_smem((const void *)bucket_agg, agg_smem));
-    launch_pdl(bucket_agg, kBuckets, kAggThreads, agg_smem, s, ent, gcnt, G, chunk, bstart, bsize, border, cnt_out, bitmap);
+    launch_pdl(bucket_agg, kBuckets, kAggThreads, agg_smem, s, ent, gcnt, G, chunk, bstart, bsize, border, cnt8, cnt32, bitmap);
     launched(ctx, 5);
 }
 
@@ -610,12 +729,13 @@ void histogram_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P, uint32_t *col
     // emit + reset per listed colour. Large images: the bucketed partition,
     // emit in pixel order.
     uint2 *tab = ctx->tab.as<uint2>();
-    uint32_t *cnt = nullptr;
+    uint8_t *cnt8 = nullptr;
+    uint32_t *cnt32 = nullptr;
     if (!large) {
         hist_count_fused<<<grid, kThreads, 0, s>>>(rgb_d, P, tab, list, n_dev, aligned);
         launch_pdl(hist_mark_fused, lgrid, kThreads, 0, s, list, n_dev, tab, bitmap);
     } else {
-        histogram_partitioned(ctx, rgb_d, P, bitmap, cnt);
+        histogram_partitioned(ctx, rgb_d, P, bitmap, cnt8, cnt32);
     }
     launch_pdl(scan_blocksum, nblk, kThreads, 0, s, bitmap, words, bsum);
     launch_pdl(scan_blocks, 1, 1024, 0, s, bsum, nblk, large ? n_dev : nullptr);
@@ -624,11 +744,20 @@ void histogram_dev(cqg_ctx *ctx, const uint8_t *rgb_d, uint64_t P, uint32_t *col
         launch_pdl(hist_emit_fused, lgrid, kThreads, 0, s, list, n_dev, tab, bitmap, wpref, colors_d, counts_d, first_d);
     } else {
         const unsigned egrid = (unsigned)ctx->num_sms * 8;
-        launch_pdl(hist_emit, egrid, kThreads, 0, s, rgb_d, P, bitmap, wpref, cnt, colors_d, counts_d, first_d);
+        const uint64_t groups = aligned ? P / 16 : 0;
+        if (groups)
+            launch_pdl(hist_emit16, egrid, kThreads, 0, s, rgb_d, groups, bitmap, wpref, (const uint8_t *)cnt8,
+                       (const uint32_t *)cnt32, colors_d, counts_d, first_d);
+        if (groups * 16 < P) {
+            unsigned tgrid = ceil_div(P - groups * 16, kThreads);
+            if (tgrid > egrid) tgrid = egrid;
+            launch_pdl(hist_emit, tgrid, kThreads, 0, s, rgb_d, groups * 16, P, bitmap, wpref, (const uint8_t *)cnt8,
+                       (const uint32_t *)cnt32, colors_d, counts_d, first_d);
+        }
     }
     prof_end(ctx, CQG_PROF_HIST, pb, 3.0 * (double)P); // + 8 N' added by the caller
     CQG_CUDA(cudaGetLastError());
-    launched(ctx, large ? 4 : 6);
+    launched(ctx, large ? 3 + (aligned && P >= 16) + ((aligned ? P / 16 * 16 : 0) < P) : 6);
 }
 
 void subsample_2to1_dev(cqg_ctx *ctx, const uint8_t *rgb_d, int w, int h, uint8_t *out_d) {
