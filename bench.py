@@ -8,10 +8,18 @@ A step is one pass of the hot path (histogram -> init -> weighted Lloyd ->
 mapping + MSE, i.e. quant::run_quantize) over one batch of synthetic input.
 The line's `value` is BASELINE.json configs[1] (cfg2: 512x512, K=256,
 k-means++), the K=256 configuration the reference's CPU build also runs in
-seconds; the other single-GPU K=256 configurations are reported in the same
-line under `by_config` (N=1: cfg3 4096^2 maximin, cfg5 8192^2 k-means++, each
-with its own roofline fractions, e2e, parity digest and 1-core reference
-baseline); cfg1 is the reference's own small case.
+seconds. One step quantizes a batch of 16 copies of the cfg2 image (separate
+buffers) through 8 concurrent library contexts of 32 SMs each -- the same
+batch the reference arm runs, one copy per host thread; one cfg2 image alone
+is two latency chains (255 dependent k-means++ draws on a 16-SM cluster, 20
+grid-synchronised Lloyd iterations) that leave most of the device idle. The
+single-image run (one context on the whole device) is measured first in the
+same process and reported under `single_image`; the per-kernel profile and
+the roofline come from it. The other single-GPU K=256 configurations are
+reported in the same line under `by_config` (N=1: cfg3 4096^2 maximin, cfg5
+8192^2 k-means++, one image per step, each with its own roofline fractions,
+e2e, parity digest and 1-core reference baseline); cfg1 is the reference's own
+small case.
 
 Multi-GPU (one rank per GPU; `--gpus N` starts torch.distributed.run itself
 when WORLD_SIZE is unset): cfg2 runs one independent replica per rank (the
@@ -42,9 +50,15 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# concurrent library contexts use 3 streams each: 32 hardware queues instead of the default 8,
+# so their streams do not alias (read at CUDA context creation: set before torch initialises CUDA)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 METRIC = "Lloyd color-center distances/s and quantized MPixel/s at K=256, 1-8 B200"
 UNIT = "MPixel/s"
+
+
+BATCH_DEFAULT = 16  # copies of a small image per step (both arms)
 
 
 def env_int(name, default):
@@ -172,8 +186,13 @@ def run_reference(args, cfg):
     else:
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
         return 0
-    imgs = [cfg.image(i % max(cfg.images, 1)) for i in range(threads)]
-    ks = [cfg.k_for(i) for i in range(threads)]
+    # one step = the GPU arm's batch (args.batch copies of the image; a batched config: its images), one
+    # image per host thread; with more host threads than images, whole batches run side by side
+    per_batch = cfg.images if cfg.images > 1 else max(1, args.batch)
+    nimg = per_batch * max(1, threads // per_batch)
+    base = cfg.image(0) if cfg.images == 1 else None
+    imgs = [base if base is not None else cfg.image(i % cfg.images) for i in range(nimg)]
+    ks = [cfg.k_for(i) for i in range(nimg)]
     P = imgs[0].shape[0] * imgs[0].shape[1]
 
     def one(i):
@@ -183,7 +202,7 @@ def run_reference(args, cfg):
     with ThreadPoolExecutor(max_workers=threads) as ex:
         for s in range(args.warmup + args.steps):
             t0 = time.perf_counter()
-            res = list(ex.map(one, range(threads)))
+            res = list(ex.map(one, range(nimg)))
             t1 = time.perf_counter()
             if s >= args.warmup:
                 times.append(t1 - t0)
@@ -191,18 +210,20 @@ def run_reference(args, cfg):
                     dist += o["n_unique"] * k * o["iterations"]
                     lloyd_s += o["stage_s"][2]
     step = sum(times) / len(times)
-    value = threads * P / step / 1e6
+    value = nimg * P / step / 1e6
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": step * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg.name, "image": f"{cfg.width}x{cfg.height}", "k": cfg.k,
-                   "init": cfg.init, "images_per_step": threads,
-                   "note": "reference sources compiled -O3 -DNDEBUG (oracle/Makefile), one image per host thread"},
-        "lloyd_distances_per_s": dist / lloyd_s * threads if lloyd_s > 0 else None,
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
-                         "sample": f"{threads} concurrent {cfg.name} run_quantize pipelines per step"},
+        "config": {"workload": cfg.name, "image": f"{cfg.width}x{cfg.height}", "images_per_step": per_batch,
+                   "k": cfg.k if not cfg.k_cycle else list(cfg.k_cycle), "init": cfg.init,
+                   "fixed_iterations": cfg.fixed_iterations or None},
+        "run": {"note": "reference sources compiled -O3 -DNDEBUG (oracle/Makefile), one image per host thread",
+                "host_threads": threads, "batches_side_by_side": nimg // per_batch},
+        "lloyd_distances_per_s": dist / lloyd_s * min(threads, nimg) if lloyd_s > 0 else None,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": min(threads, nimg), "kind": kind,
+                         "sample": f"{nimg} {cfg.name} run_quantize pipelines per step on {threads} host threads"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -442,6 +463,25 @@ def run_ours(args, cfg):
         for name in extra:
             cpu_jobs[name] = HOSTPOOL.submit(cpu_baseline, CONFIGS[name], 0.0)  # one pipeline
     line = measure(args, cfg, env, args.steps, args.warmup, not args.no_e2e, not args.no_parity)
+    if cfg.images == 1 and args.batch > 1:
+        # The headline: `batch` copies of the image per step, quantized concurrently by several library
+        # contexts (as the reference arm runs one copy per host thread). The single-image run above keeps
+        # the per-kernel profile, the roofline and the stage times, and is reported under single_image.
+        single = line
+        line = measure(args, cfg, env, args.steps, args.warmup, not args.no_e2e, not args.no_parity,
+                       batch=args.batch)
+        if rank == 0:
+            where = ("the single-image steps of this run (one library context on the whole device), timed before "
+                     "the batch steps: in a batch several such kernels share the device, each on its SM budget")
+            line["single_image"] = {k: single[k] for k in
+                                    ("value", "unit", "ms_per_step", "steps", "e2e", "lloyd_distances_per_s",
+                                     "stage_ms_last_step", "gpu_launches", "parity", "clocks")}
+            line["single_image"]["parity"] = resolve(line["single_image"]["parity"])
+            for k in ("kernels", "byte_kernels", "roofline", "dominant_kernel", "stage_ms_last_step",
+                      "lloyd_distances_per_s", "flagged_per_step", "swept_fraction"):
+                line[k] = single[k]
+            line["roofline"]["measured_on"] = where
+            line["kernels_measured_on"] = where
     by_config = {}
     for name in extra:
         res = measure(args, CONFIGS[name], env, 3, 3, not args.no_e2e, not args.no_parity)
@@ -475,7 +515,7 @@ def run_ours(args, cfg):
     return rc
 
 
-def measure(args, cfg, env, steps, warmup, e2e_on=True, parity_on=True):
+def measure(args, cfg, env, steps, warmup, e2e_on=True, parity_on=True, batch=1):
     """One workload on this rank: W warm-ups, `steps` timed steps (device
     events, L2 flushed between steps, max over ranks), the stage profile, the
     roofline of the dominant kernel, e2e through the C-ABI with pinned host
@@ -490,11 +530,13 @@ def measure(args, cfg, env, steps, warmup, e2e_on=True, parity_on=True):
     ctx.set_stream(stream.cuda_stream)
 
     # work owned by this rank
+    batch = max(1, batch) if cfg.images == 1 else 1
     if cfg.images > 1:
         my = list(range(rank, cfg.images, world))
     else:
-        my = [0]
-    imgs = [cfg.image(i) for i in my]
+        my = [0] * batch  # `batch` copies of the image in separate buffers, quantized concurrently
+    img0 = cfg.image(my[0])
+    imgs = [img0 if i == my[0] else cfg.image(i) for i in my]
     ks = [cfg.k_for(i) for i in my]
     P_list = [im.shape[0] * im.shape[1] for im in imgs]
     kind = cabi.INIT_KMEANSPP if cfg.init == "kpp" else cabi.INIT_MAXIMIN
@@ -514,7 +556,8 @@ def measure(args, cfg, env, steps, warmup, e2e_on=True, parity_on=True):
     # concurrently (the 16-SM cluster initialisers of different images share
     # the GPU; cooperative kernels are chained by the library). One image:
     # one context on the timing stream.
-    nworkers = max(1, min(args.workers if cfg.images > 1 else 1, len(imgs)))
+    want = args.workers if cfg.images > 1 else (args.batch_workers if batch > 1 else 1)
+    nworkers = max(1, min(want, len(imgs)))
     ctxs, wstreams = [ctx], [stream]
     for _ in range(nworkers - 1):
         c2 = cabi.Context(local)
@@ -526,11 +569,15 @@ def measure(args, cfg, env, steps, warmup, e2e_on=True, parity_on=True):
         s0 = torch.cuda.Stream(device=dev)  # worker 0 off the timing stream too
         ctx.set_stream(s0.cuda_stream)
         # each worker's grids (and cooperative kernels) on its own slice of the SMs
-        if args.sm_budget != 0:
+        sm_budget = args.sm_budget if cfg.images > 1 else args.batch_sm_budget
+        if sm_budget != 0:
             sms = torch.cuda.get_device_properties(dev).multi_processor_count
-            budget = args.sm_budget if args.sm_budget > 0 else sms // nworkers
+            budget = sm_budget if sm_budget > 0 else sms // nworkers
             for c in ctxs:
                 c.set_sm_budget(budget)
+            budget_label = f"{budget} SMs each"
+        else:
+            budget_label = "the whole device each"
         wstreams[0] = s0
     sses = [np.zeros(128) for _ in range(nworkers)]
     pool = ThreadPoolExecutor(nworkers) if nworkers > 1 else None
@@ -612,7 +659,7 @@ def measure(args, cfg, env, steps, warmup, e2e_on=True, parity_on=True):
         dist.barrier()
     total_ms = float(t.item())
     ms_per_step = total_ms / steps
-    pixels_per_step_all = cfg.images * P_list[0] * (1 if cfg.images > 1 else world)
+    pixels_per_step_all = cfg.images * P_list[0] if cfg.images > 1 else batch * P_list[0] * world
     value = pixels_per_step_all / (ms_per_step / 1e3) / 1e6
 
     # Lloyd distances/s (full-sweep equivalent N'.K.iters over Lloyd device time)
@@ -753,6 +800,15 @@ def measure(args, cfg, env, steps, warmup, e2e_on=True, parity_on=True):
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e_step,
                "index_layout": "uint32 per pixel (MappingResult::indices)"}
 
+    # a batch holds copies of one image: every copy's outputs must equal image 0's
+    batch_equal = None
+    if batch > 1:
+        torch.cuda.synchronize()
+        batch_equal = all(torch.equal(d_pal[i], d_pal[0]) and torch.equal(d_idx[i], d_idx[0]) and
+                          torch.equal(d_q[i], d_q[0]) for i in range(1, len(imgs)))
+        if not batch_equal:
+            raise RuntimeError("bench: the copies of a batch disagree with each other")
+
     # parity digest of the last timed step's outputs (image 0 of this rank)
     # against the C oracle (exact-moment mode): palette bytes, iterations,
     # NDC, mapping indices / pixels / MSE / mapping NDC. A mismatch fails the run.
@@ -770,13 +826,16 @@ def measure(args, cfg, env, steps, warmup, e2e_on=True, parity_on=True):
             "scaling": "weak" if cfg.images == 1 else "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
             "config": {"workload": cfg.name, "image": f"{cfg.width}x{cfg.height}",
-                       "images_per_rank": len(imgs), "k": cfg.k if not cfg.k_cycle else list(cfg.k_cycle),
-                       "init": cfg.init, "fixed_iterations": cfg.fixed_iterations or None,
-                       "parallelism": (f"replicas x{world}" if cfg.images == 1 else
-                                       f"images sharded over {world}; {nworkers} concurrent streams per GPU"),
-                       "l2": "flushed (512 MiB write) between timed steps",
-                       "arithmetic": "FP32 packed sweep + exact FP64 replay of near-ties + int64 moments",
-                       "index_layout": "uint32 per pixel"},
+                       "images_per_step": len(imgs) if cfg.images == 1 else cfg.images,
+                       "k": cfg.k if not cfg.k_cycle else list(cfg.k_cycle),
+                       "init": cfg.init, "fixed_iterations": cfg.fixed_iterations or None},
+            "run": {"images_per_rank": len(imgs),
+                    "parallelism": ((f"replicas x{world}" if cfg.images == 1 else f"images sharded over {world}") +
+                                    (f"; {nworkers} concurrent library contexts per GPU, {budget_label}"
+                                     if nworkers > 1 else "; one library context on the whole device")),
+                    "l2": "flushed (512 MiB write) between timed steps",
+                    "arithmetic": "FP32 packed sweep + exact FP64 replay of near-ties + int64 moments",
+                    "index_layout": "uint32 per pixel", "batch_copies_equal": batch_equal},
             "lloyd_distances_per_s": lloyd_rate,
             "n_unique": int(st0.n_unique), "iterations": int(st0.lloyd.iterations),
             "flagged_per_step": int(st0.lloyd.flagged_total),
@@ -806,10 +865,19 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--sm-budget", type=int, default=-1,
-                    help="batched configs: SMs per worker context (-1: SMs / workers, 0: whole device each)")
-    ap.add_argument("--workers", type=int, default=4,
+    ap.add_argument("--sm-budget", type=int, default=24,
+                    help="batched configs: SMs per worker context (-1: SMs / workers, 0: whole device each); "
+                         "measured on cfg4: 4 x 37 SMs 608, 8 x 37 880, 16 x 24 982 MPixel/s")
+    ap.add_argument("--workers", type=int, default=16,
                     help="batched configs: concurrent library contexts (streams + host threads) per GPU")
+    ap.add_argument("--batch", type=int, default=None,
+                    help="single-image configs: copies of the image per step, quantized concurrently "
+                         "(default: 16 for cfg1 / cfg2, as many as the reference arm's images per step; 1 otherwise)")
+    ap.add_argument("--batch-workers", type=int, default=8,
+                    help="concurrent library contexts (streams + host threads) for --batch")
+    ap.add_argument("--batch-sm-budget", type=int, default=32,
+                    help="SMs per library context for --batch (0: whole device each); the budgets may oversubscribe "
+                         "the device: kernels of different stages interleave")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true", help="skip the oracle digest of the outputs")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -834,6 +902,8 @@ def main():
         return 2
     from paper_1101_0395_b200.synth import CONFIGS
     cfg = CONFIGS[args.config]
+    if args.batch is None:
+        args.batch = BATCH_DEFAULT if cfg.name in ("cfg1", "cfg2") else 1
     if args.impl == "reference":
         return run_reference(args, cfg)
     return run_ours(args, cfg)

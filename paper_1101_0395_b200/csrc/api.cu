@@ -17,15 +17,49 @@
 namespace {
 thread_local std::string g_last_error;
 
+// Small results bound for pageable caller memory travel through the context's
+// pinned bounce buffer (copy_out) and are handed over here, at the end of the
+// call: a cudaMemcpyAsync into pageable memory is staged by the driver under a
+// device-wide lock and stalls the other contexts of a concurrent batch (cfg2,
+// 16 images through 8 contexts, palette into a pageable array: 6.2 -> 9.2 ms).
+struct PendingOut {
+    cqg_ctx *ctx;
+    void *dst;
+    const void *src;
+    size_t bytes;
+};
+thread_local std::vector<PendingOut> g_pending_out;
+
+void finish_pending_out(bool ok) {
+    if (g_pending_out.empty()) return;
+    std::vector<PendingOut> todo;
+    todo.swap(g_pending_out);
+    for (const auto &p : todo) p.ctx->bounce_used = 0;
+    if (!ok) return;
+    cudaStream_t last = nullptr;
+    bool have = false;
+    for (const auto &p : todo) {
+        if (!have || p.ctx->stream != last) {
+            if (cudaStreamSynchronize(p.ctx->stream) != cudaSuccess) cqg::fail(CQG_E_RUNTIME, "copy to host failed");
+            last = p.ctx->stream;
+            have = true;
+        }
+        std::memcpy(p.dst, p.src, p.bytes);
+    }
+}
+
 template <class F>
 int guarded(F &&f) {
     try {
         f();
+        finish_pending_out(true);
         return CQG_OK;
     } catch (const cqg::Error &e) {
+        finish_pending_out(false);
         g_last_error = e.msg;
         return e.code;
     } catch (const std::exception &e) {
+        finish_pending_out(false);
         g_last_error = e.what();
         return CQG_E_RUNTIME;
     }
@@ -155,8 +189,28 @@ const void *stage_in(cqg_ctx *ctx, const void *user, size_t bytes, DevBuf &buf) 
     return d;
 }
 
+static bool is_pageable_host(const void *p) {
+    cudaPointerAttributes attr{};
+    if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+        cudaGetLastError();
+        return true;
+    }
+    return attr.type == cudaMemoryTypeUnregistered;
+}
+
 void copy_out(cqg_ctx *ctx, void *user, const void *dev, size_t bytes) {
     if (!user || bytes == 0 || user == dev) return;
+    constexpr size_t kBounce = 1u << 20, kSmall = 256u << 10;
+    if (bytes <= kSmall && is_pageable_host(user)) {
+        char *b = static_cast<char *>(ctx->bounce.ensure(kBounce));
+        const size_t at = (ctx->bounce_used + 63) & ~(size_t)63;
+        if (at + bytes <= kBounce) {
+            CQG_CUDA(cudaMemcpyAsync(b + at, dev, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+            ctx->bounce_used = at + bytes;
+            g_pending_out.push_back({ctx, user, b + at, bytes});
+            return;
+        }
+    }
     CQG_CUDA(cudaMemcpyAsync(user, dev, bytes, cudaMemcpyDefault, ctx->stream));
 }
 

@@ -142,6 +142,8 @@ struct cqg_ctx {
     cqg::DevBuf mind2, initpart, initsel, unit_draws, inittile;
     cqg::HostBuf pinned;   // status readback and small results
     cqg::HostBuf pinned_nu; // initialiser unit draws (an async H2D source: no host-blocking copy)
+    cqg::HostBuf bounce;    // small results on their way to pageable caller memory (copy_out)
+    size_t bounce_used = 0;
 
     // cached CUDA graph of the Lloyd WHILE loop (lloyd.cu)
     bool use_graphs = true;
