@@ -519,11 +519,11 @@ __global__ void __launch_bounds__(kAggThreads) bucket_agg(const uint32_t *__rest
         if (e0 >= w1) break;
         const uint32_t e = e0 + lane;
         const bool v = e < w1;
-        const uint32_t x = v ? __ldcs(ent + bs + e) : 0u;
+        const uint32_t xe = v ? __ldcs(ent + bs + e) : 0u;
         if (v)
             while (s_seg[g + 1] <= e) ++g;
-        const uint32_t slot = x & (kSlots - 1);
-        const uint32_t key = (g << kChunkBits) | (x >> kSlotBits);
+        const uint32_t slot = xe & (kSlots - 1);
+        const uint32_t key = (g << kChunkBits) | (xe >> kSlotBits);
         const uint32_t act = __ballot_sync(0xffffffffu, v);
         const int lead = __ffs(act) - 1;
         const uint32_t s_first = __shfl_sync(0xffffffffu, slot, lead);
