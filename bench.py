@@ -440,6 +440,8 @@ def summarize(res, cpu):
         "pixel_map_hbm_frac": res["byte_kernels"]["pixel_map"]["frac"],
         "byte_kernels": res["byte_kernels"], "e2e": res["e2e"], "cpu_baseline": cpu,
         "parity": res["parity"], "gpu_launches": res["gpu_launches"], "clocks": res["clocks"],
+        "config": res["config"], "run": res["run"],
+        **({"single_image": res["single_image"]} if "single_image" in res else {}),
     }
 
 
@@ -455,21 +457,24 @@ def run_ours(args, cfg):
     if args.sharded or (world > 1 and cfg.images == 1 and cfg.name in ("cfg5", "cfg3", "cfg3k64")):
         return run_sharded_line(args, cfg, env)
     cpu_on = rank == 0 and world == 1 and not args.no_cpu_baseline
-    extra = [] if args.no_by_config or cfg.name not in ("cfg2",) else (["cfg3", "cfg5"] if world == 1 else ["cfg4"])
+    extra = [] if args.no_by_config or cfg.name not in ("cfg2",) else (
+        ["cfg1", "cfg3", "cfg4", "cfg5"] if world == 1 else ["cfg4"])
     # 1-core reference baselines run on host threads while the device measures
     cpu_jobs = {}
     if cpu_on:
         cpu_jobs[cfg.name] = HOSTPOOL.submit(cpu_baseline, cfg, args.cpu_seconds)
         for name in extra:
             cpu_jobs[name] = HOSTPOOL.submit(cpu_baseline, CONFIGS[name], 0.0)  # one pipeline
-    line = measure(args, cfg, env, args.steps, args.warmup, not args.no_e2e, not args.no_parity)
-    if cfg.images == 1 and args.batch > 1:
-        # The headline: `batch` copies of the image per step, quantized concurrently by several library
-        # contexts (as the reference arm runs one copy per host thread). The single-image run above keeps
-        # the per-kernel profile, the roofline and the stage times, and is reported under single_image.
+
+    def measure_cfg(c, steps, warmup, batch):
+        """A single-image config with batch > 1: the single-image run first (per-kernel profile, roofline,
+        stage times; reported under single_image), then `batch` copies of the image per step, quantized
+        concurrently by several library contexts (as the reference arm runs one copy per host thread)."""
+        line = measure(args, c, env, steps, warmup, not args.no_e2e, not args.no_parity)
+        if c.images > 1 or batch <= 1:
+            return line
         single = line
-        line = measure(args, cfg, env, args.steps, args.warmup, not args.no_e2e, not args.no_parity,
-                       batch=args.batch)
+        line = measure(args, c, env, steps, warmup, not args.no_e2e, not args.no_parity, batch=batch)
         if rank == 0:
             where = ("the single-image steps of this run (one library context on the whole device), timed before "
                      "the batch steps: in a batch several such kernels share the device, each on its SM budget")
@@ -482,9 +487,13 @@ def run_ours(args, cfg):
                 line[k] = single[k]
             line["roofline"]["measured_on"] = where
             line["kernels_measured_on"] = where
+        return line
+
+    line = measure_cfg(cfg, args.steps, args.warmup, args.batch)
     by_config = {}
     for name in extra:
-        res = measure(args, CONFIGS[name], env, 3, 3, not args.no_e2e, not args.no_parity)
+        small = name in ("cfg1", "cfg2")
+        res = measure_cfg(CONFIGS[name], 10 if small else 3, 3, BATCH_DEFAULT if small else 1)
         if rank == 0:
             by_config[name] = res
     if world > 1 and not args.no_by_config and cfg.name == "cfg2":
