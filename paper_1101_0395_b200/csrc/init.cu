@@ -901,6 +901,38 @@ __global__ void tile_place_kernel(const uint32_t *__restrict__ colors, const uin
     }
 }
 
+// The tile order is the Morton order of the distinct colours, so the tile-order
+// colour array is the bitmap read back: one thread per bitmap word writes its
+// set slots' colours at the word's prefix (sequential stores, no scatter).
+__device__ __forceinline__ uint32_t tile_compact8(uint32_t x) {
+    x &= 0x00249249u;
+    x = (x | (x >> 2)) & 0x000C30C3u;
+    x = (x | (x >> 4)) & 0x0000F00Fu;
+    x = (x | (x >> 8)) & 0x000000FFu;
+    return x;
+}
+__global__ void __launch_bounds__(256) tile_expand_kernel(const uint32_t *__restrict__ bits,
+                                                          const uint32_t *__restrict__ pref,
+                                                          const uint32_t *__restrict__ bsum,
+                                                          uint32_t *__restrict__ tcol) {
+    const uint32_t w = blockIdx.x * 256u + threadIdx.x;
+    uint32_t b = bits[w];
+    if (!b) return;
+    uint32_t pos = bsum[w >> 10] + pref[w];
+    while (b) {
+        const uint32_t m = (w << 5) | (uint32_t)(__ffs(b) - 1);
+        b &= b - 1;
+        tcol[pos++] = (tile_compact8(m >> 2) << 16) | (tile_compact8(m >> 1) << 8) | tile_compact8(m);
+    }
+}
+// the tile-order counts: gathered through the placed histogram indices (random
+// 4-byte reads cost about half of the scatter pass they replace)
+__global__ void tile_count_kernel(const uint32_t *__restrict__ counts, const uint32_t *__restrict__ tidx, uint64_t n,
+                                  uint32_t *__restrict__ tcnt) {
+    for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (uint64_t)gridDim.x * blockDim.x)
+        tcnt[p] = __ldg(counts + tidx[p]);
+}
+
 // setup 4: per tile the colour box (one warp per tile)
 __global__ void tile_box_kernel(const uint32_t *__restrict__ tcol, uint64_t n, uint64_t ntiles, uint2 *__restrict__ tbox,
                                 uint32_t *__restrict__ tmax) {
@@ -2497,10 +2529,10 @@ void run_init(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *counts_d, 
         tile_scan_blocks<<<kTileBitmapWords / 1024, 1024, 0, s>>>(tbits, tpref, tbsum);
         tile_scan_top<<<1, 1024, 0, s>>>(tbsum, kTileBitmapWords / 1024);
         const int g = tile_grid(ctx, n);
-        tile_place_kernel<<<g, 256, 0, s>>>(colors_d, counts_d, n, tbits, tpref, tbsum, tcol, 0, nullptr);
+        tile_expand_kernel<<<kTileBitmapWords / 256, 256, 0, s>>>(tbits, tpref, tbsum, tcol);
         tile_place_kernel<<<g, 256, 0, s>>>(colors_d, counts_d, n, tbits, tpref, tbsum, tidx, 1,
                                             kind == 1 ? hpos : nullptr);
-        if (kind == 1) tile_place_kernel<<<g, 256, 0, s>>>(colors_d, counts_d, n, tbits, tpref, tbsum, tcnt, 2, nullptr);
+        if (kind == 1) tile_count_kernel<<<g, 256, 0, s>>>(counts_d, tidx, n, tcnt);
         CQG_CUDA(cudaMemsetAsync(tmd, 0xFF, sizeof(uint32_t) * n, s));
         tile_box_kernel<<<tile_grid(ctx, ntiles * 32), 256, 0, s>>>(tcol, n, ntiles, tbox, tmax);
         launched(ctx, kind == 1 ? 6 : 5);
