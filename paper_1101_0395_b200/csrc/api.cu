@@ -325,6 +325,7 @@ void cqg_destroy(cqg_ctx *ctx) {
     for (DevBuf *b : bufs) b->release();
     ctx->pinned.release();
     ctx->pinned_nu.release();
+    ctx->bounce.release();
     for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
     for (cudaEvent_t e : ctx->stage_ev)
