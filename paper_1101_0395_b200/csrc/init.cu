@@ -902,8 +902,7 @@ __global__ void tile_place_kernel(const uint32_t *__restrict__ colors, const uin
 }
 
 // The tile order is the Morton order of the distinct colours, so the tile-order
-// colour array is the bitmap read back: one thread per bitmap word writes its
-// set slots' colours at the word's prefix (sequential stores, no scatter).
+// colour array is the bitmap read back (sequential stores, no scatter).
 __device__ __forceinline__ uint32_t tile_compact8(uint32_t x) {
     x &= 0x00249249u;
     x = (x | (x >> 2)) & 0x000C30C3u;
@@ -915,14 +914,24 @@ __global__ void __launch_bounds__(256) tile_expand_kernel(const uint32_t *__rest
                                                           const uint32_t *__restrict__ pref,
                                                           const uint32_t *__restrict__ bsum,
                                                           uint32_t *__restrict__ tcol) {
-    const uint32_t w = blockIdx.x * 256u + threadIdx.x;
-    uint32_t b = bits[w];
-    if (!b) return;
-    uint32_t pos = bsum[w >> 10] + pref[w];
-    while (b) {
-        const uint32_t m = (w << 5) | (uint32_t)(__ffs(b) - 1);
-        b &= b - 1;
-        tcol[pos++] = (tile_compact8(m >> 2) << 16) | (tile_compact8(m >> 1) << 8) | tile_compact8(m);
+    // a warp takes 32 words; word by word, lane l writes slot l's colour at
+    // the word's prefix + the set bits below it: one coalesced store per word
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t wbase = ((blockIdx.x * 256u + threadIdx.x) >> 5) << 5;
+    const uint32_t w = wbase + lane;
+    const uint32_t b = bits[w];
+    const uint32_t p0 = bsum[w >> 10] + pref[w];
+    if (!__any_sync(0xffffffffu, b != 0u)) return;
+    const uint32_t below = (1u << lane) - 1u;
+#pragma unroll 4
+    for (int j = 0; j < 32; ++j) {
+        const uint32_t bj = __shfl_sync(0xffffffffu, b, j);
+        const uint32_t pj = __shfl_sync(0xffffffffu, p0, j);
+        if ((bj >> lane) & 1u) {
+            const uint32_t m = ((wbase + (uint32_t)j) << 5) | lane;
+            tcol[pj + (uint32_t)__popc(bj & below)] =
+                (tile_compact8(m >> 2) << 16) | (tile_compact8(m >> 1) << 8) | tile_compact8(m);
+        }
     }
 }
 // the tile-order counts: gathered through the placed histogram indices (random
