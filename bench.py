@@ -262,6 +262,29 @@ def cpu_baseline(cfg, budget_s: float):
 # ---------------------------------------------------------------------------
 # our arm
 
+def cpp_dropin(cfg, batch, workers, sms):
+    """The same workload through the C++ drop-in (libquant_b200.so: quant::run_quantize with pageable
+    std::vector buffers and the full QuantizeResult; quant::run_bench over `batch` copies with the cells
+    shared out over worker threads): tools/cpp_e2e, wall clock."""
+    import tempfile
+    from paper_1101_0395_b200 import _build
+    if not os.path.exists(_build.CPP_E2E_BIN):
+        return {"unavailable": "tools/cpp_e2e not built"}
+    img = cfg.image(0)
+    h, w = img.shape[:2]
+    with tempfile.TemporaryDirectory() as td:
+        path = os.path.join(td, f"{cfg.name}.ppm")
+        with open(path, "wb") as f:
+            f.write(b"P6\n%d %d\n255\n" % (w, h))
+            f.write(np.ascontiguousarray(img, np.uint8).tobytes())
+        method = "wsm-kpp" if cfg.init == "kpp" else "wsm-mmx"
+        r = subprocess.run([_build.CPP_E2E_BIN, path, str(cfg.k), method, "20", str(batch), str(workers), str(sms)],
+                           capture_output=True, text=True, timeout=300)
+    if r.returncode != 0:
+        return {"error": (r.stdout + r.stderr)[-400:]}
+    return json.loads(r.stdout)
+
+
 def parity_digest(cfg, img, k, image_id, st, pal, didx, dq):
     """The bench step's outputs (host copies) against the C oracle
     (UPDATE_EXACT) on the same input."""
@@ -496,6 +519,10 @@ def run_ours(args, cfg):
         res = measure_cfg(CONFIGS[name], 10 if small else 3, 3, BATCH_DEFAULT if small else 1)
         if rank == 0:
             by_config[name] = res
+    cpp = None
+    if rank == 0 and world == 1 and cfg.images == 1 and not args.no_e2e:
+        # after the device measurements (its own process and contexts; the GPU is idle here)
+        cpp = cpp_dropin(cfg, max(args.batch, 1), args.batch_workers, args.batch_sm_budget)
     if world > 1 and not args.no_by_config and cfg.name == "cfg2":
         res = sharded_measure(args, CONFIGS["cfg5"], env, 3, 3)
         if rank == 0:
@@ -503,6 +530,8 @@ def run_ours(args, cfg):
     rc = 0
     if rank == 0:
         line["cpu_baseline"] = resolve(cpu_jobs.get(cfg.name))
+        if cpp is not None:
+            line["cpp_dropin"] = cpp
         line["parity"] = resolve(line["parity"])
         out = {}
         for name, res in by_config.items():

@@ -78,6 +78,8 @@ def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False) 
 HOST_LIB = os.path.join(PKG, "libquant_b200.so")
 CPP_TEST_SRC = os.path.join(ROOT, "tests", "cpp", "test_dropin.cpp")
 CPP_TEST_BIN = os.path.join(ROOT, "tests", "cpp", "test_dropin")
+CPP_E2E_SRC = os.path.join(ROOT, "tools", "cpp_e2e.cpp")
+CPP_E2E_BIN = os.path.join(ROOT, "tools", "cpp_e2e")
 
 
 HOST_SOURCES = ["context.cpp", "colour_rng.cpp", "image_io.cpp", "histogram_api.cpp", "cluster.cpp", "seeding.cpp",
@@ -107,6 +109,12 @@ def build_host(force: bool = False) -> str:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError("C++ test build failed:\n" + r.stdout + r.stderr)
+    if force or _newer([CPP_E2E_SRC, HOST_LIB, *hdrs], CPP_E2E_BIN):
+        cmd = [cxx, "-std=c++20", "-O2", *inc, CPP_E2E_SRC, "-o", CPP_E2E_BIN, "-L" + PKG, "-l:libquant_b200.so",
+               "-l:libcqg.so", "-Wl,-rpath," + PKG]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError("C++ e2e tool build failed:\n" + r.stdout + r.stderr)
     return HOST_LIB
 
 

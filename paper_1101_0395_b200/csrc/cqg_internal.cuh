@@ -142,8 +142,10 @@ struct cqg_ctx {
     cqg::DevBuf mind2, initpart, initsel, unit_draws, inittile;
     cqg::HostBuf pinned;   // status readback and small results
     cqg::HostBuf pinned_nu; // initialiser unit draws (an async H2D source: no host-blocking copy)
-    cqg::HostBuf bounce;    // small results on their way to pageable caller memory (copy_out)
-    size_t bounce_used = 0;
+    // pageable caller memory is reached through pinned staging buffers (copy_out / stage_in): one
+    // grow-only buffer per transfer of a call, in call order, so a repeated call reuses them
+    std::vector<cqg::HostBuf> stage_out, stage_in;
+    size_t stage_out_used = 0, stage_in_used = 0;
 
     // cached CUDA graph of the Lloyd WHILE loop (lloyd.cu)
     bool use_graphs = true;

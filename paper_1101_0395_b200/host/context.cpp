@@ -6,6 +6,7 @@
 namespace quant {
 namespace {
 thread_local int t_device = 0;
+thread_local int t_budget = 0;
 
 struct Contexts {
     std::map<int, cqg_ctx *> by_device;
@@ -18,7 +19,16 @@ thread_local Contexts t_contexts;
 
 void set_device(int device) { t_device = device; }
 
+void set_sm_budget(int sms) {
+    if (sms < 0) throw std::invalid_argument("set_sm_budget: negative SM count");
+    t_budget = sms;
+    auto it = t_contexts.by_device.find(t_device);
+    if (it != t_contexts.by_device.end()) detail::check(cqg_set_sm_budget(it->second, sms));
+}
+
 namespace detail {
+
+int current_device() { return t_device; }
 
 cqg_ctx *ctx() {
     auto it = t_contexts.by_device.find(t_device);
@@ -26,6 +36,7 @@ cqg_ctx *ctx() {
     cqg_ctx *c = cqg_create(t_device);
     if (!c) throw std::runtime_error(std::string("libcqg: ") + cqg_last_error());
     t_contexts.by_device[t_device] = c;
+    if (t_budget > 0) check(cqg_set_sm_budget(c, t_budget));
     return c;
 }
 

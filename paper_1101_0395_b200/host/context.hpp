@@ -15,6 +15,7 @@ namespace quant::detail {
 
 // one cqg context per (host thread, device), created on first use
 cqg_ctx *ctx();
+int current_device(); // the calling thread's set_device value
 
 // CQG_E_INVALID -> std::invalid_argument, everything else -> std::runtime_error,
 // with the library's (the reference's) message text

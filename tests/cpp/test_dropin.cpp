@@ -331,6 +331,17 @@ static void case_bench_sweep(const std::string &dir, const std::string &csv_out)
     };
     CHECK(slurp(c1) == slurp(c2));
     CHECK(slurp(c1).rfind("image,method,k,run,seed,sampling,", 0) == 0);
+    // the same sweep with its cells shared out over 4 worker threads (a device context of 32 SMs
+    // each): same rows, same CSV, same log
+    set_bench_workers(4, 32);
+    std::ostringstream log4;
+    const BenchResults a4 = run_bench(bc, &log4);
+    set_bench_workers(1);
+    const std::string c4 = tmp + "/w4.csv";
+    write_bench_csv(a4, c4);
+    CHECK(slurp(c1) == slurp(c4));
+    CHECK(log.str() == log4.str());
+    CHECK(a4.error_count == a.error_count);
     const RankSummary rs = rank_aggregate(a);
     CHECK(rs.methods == std::vector<std::string>({"wsm-kpp", "wsm-mmx"})); // error rows do not rank
     if (!csv_out.empty()) write_bench_csv(a, csv_out);
