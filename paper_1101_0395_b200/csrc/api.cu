@@ -286,18 +286,10 @@ cqg_ctx *cqg_create(int device) {
         ctx->use_graphs = !(ng && ng[0] == '1');
         const char *nc = getenv("CQG_NO_CLUSTER_INIT");
         ctx->use_cluster_init = !(nc && nc[0] == '1');
-        const char *nm = getenv("CQG_NO_MBAR_INIT");
-        ctx->use_mbar_init = !(nm && nm[0] == '1');
-        const char *cp = getenv("CQG_CLUSTER_MAX_PPT");
-        if (cp && atoi(cp) > 0) ctx->cluster_max_ppt = atoi(cp);
-        const char *ng2 = getenv("CQG_NO_INIT_REG");
-        ctx->use_init_reg = !(ng2 && ng2[0] == '1');
         const char *cn = getenv("CQG_CLUSTER_NT");
         if (cn) ctx->cluster_nt = atoi(cn);
         const char *fs = getenv("CQG_DBG_INIT_FORCE_SEQ");
         if (fs) ctx->dbg_init_force_seq = atoi(fs);
-        const char *nr = getenv("CQG_NO_INIT_REC");
-        ctx->use_init_rec = !(nr && nr[0] == '1');
         const char *nt = getenv("CQG_NO_INIT_TILE");
         ctx->use_init_tile = !(nt && nt[0] == '1');
         const char *tm = getenv("CQG_INIT_TILE_MIN");

@@ -150,13 +150,9 @@ struct cqg_ctx {
     // cached CUDA graph of the Lloyd WHILE loop (lloyd.cu)
     bool use_graphs = true;
     bool use_cluster_init = true;
-    bool use_mbar_init = true; // cluster init signals through mbarrier transactions (CQG_NO_MBAR_INIT=1: barriers)
-    int cluster_max_ppt = 12; // cluster initialiser up to 16 x 1024 x ppt colours (CQG_CLUSTER_MAX_PPT); 16 measured slower on cfg4
     int dbg_init_force_seq = 0; // tests only: CQG_DBG_INIT_FORCE_SEQ=1|2 drives the register cluster kernel's sequential paths
     int dbg_ndc_win = 0; // tests only: CQG_DBG_NDC_WIN=n caps the persistent loop's deferred-NDC window (relaunches)
     int cluster_nt = 0; // cluster init CTA size: 0 fewest padded slots, else forced (CQG_CLUSTER_NT=512..1024)
-    bool use_init_reg = true; // cluster init keeps points in registers (CQG_NO_INIT_REG=1: shared-memory kernel)
-    bool use_init_rec = true; // {colour, md} record layout for large-N init (CQG_NO_INIT_REC=1: off)
     bool use_init_tile = true; // colour-space tiles with box pruning for large-N init (CQG_NO_INIT_TILE=1: off)
     uint64_t init_tile_min = 1ull << 20; // ... from this many points (CQG_INIT_TILE_MIN; below, the record layout is as fast)
     bool use_ndc_code = true; // shared-memory code table for the NDC count (CQG_NO_NDC_CODE=1: off)

@@ -242,17 +242,6 @@ __device__ int warp_locate(const typename M::T *arr, int cnt, bool from_total, d
     return found;
 }
 
-template <class M>
-__device__ typename M::T block_sum(typename M::T v, typename M::T *s_w) {
-    typedef typename M::T T;
-    for (int o = 16; o; o >>= 1) v += M::shfl(v, (threadIdx.x & 31) ^ o);
-    if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = v;
-    __syncthreads();
-    T t = 0;
-    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += s_w[i];
-    __syncthreads();
-    return t;
-}
 
 template <class M>
 __device__ typename M::T block_excl(typename M::T v, typename M::T *s_w, typename M::T *total) {
@@ -467,102 +456,6 @@ __device__ uint64_t locate_draw(const InitArgs &a, cg::grid_group &grid, int par
         idx = a.result[par];
     }
     return idx;
-}
-
-template <class M>
-__global__ void __launch_bounds__(kInitThreads) init_kernel(InitArgs a) {
-    cg::grid_group grid = cg::this_grid();
-    __shared__ typename M::T s_w[kInitThreads / 32];
-    __shared__ unsigned long long s_m[kInitThreads / 32];
-    const uint64_t lo = (uint64_t)blockIdx.x * a.chunk;
-    const uint64_t hi = lo + a.chunk < a.n ? lo + a.chunk : a.n;
-    int par = 0;
-
-    // ---- first centre ---------------------------------------------------
-    uint64_t first;
-    if (a.kind == 1 || a.weighted_first) {
-        update_masses<M>(a, par, 1, 0, 0, nullptr, nullptr, lo, hi, s_w);
-        grid.sync();
-        first = locate_draw<M>(a, grid, par, a.nu[0], 1, nullptr, s_w);
-        par ^= 1;
-    } else {
-        first = a.first_index;
-    }
-    uint32_t clast = __ldg(a.colors + first);
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        a.cen[0] = (double)((clast >> 16) & 255u);
-        a.cen[1] = (double)((clast >> 8) & 255u);
-        a.cen[2] = (double)(clast & 255u);
-    }
-
-    for (int k = 1; k < a.K; ++k) {
-        // round k reads md[(k-1)&1] (absent for k == 1) and writes md[k&1]
-        const uint32_t *md_in = a.md + (size_t)((k - 1) & 1) * a.n;
-        uint32_t *md_out = a.md + (size_t)(k & 1) * a.n;
-        uint64_t pick;
-        if (a.kind == 0) {
-            unsigned long long best = 0;
-            for (uint64_t i0 = lo + threadIdx.x; i0 < hi; i0 += 8ull * blockDim.x) {
-                uint32_t col[8], mi[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const uint64_t i = i0 + (uint64_t)u * blockDim.x;
-                    col[u] = i < hi ? __ldg(a.colors + i) : 0u;
-                    mi[u] = (i < hi && k > 1) ? md_in[i] : 0xFFFFFFFFu;
-                }
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const uint64_t i = i0 + (uint64_t)u * blockDim.x;
-                    if (i < hi) {
-                        const uint32_t m = min(mi[u], d2_int(col[u], clast));
-                        md_out[i] = m;
-                        const unsigned long long key = ((unsigned long long)m << 32) | (uint32_t)~(uint32_t)i;
-                        best = key > best ? key : best;
-                    }
-                }
-            }
-            for (int o = 16; o; o >>= 1) {
-                const unsigned long long t = __shfl_xor_sync(0xffffffffu, best, o);
-                best = t > best ? t : best;
-            }
-            if ((threadIdx.x & 31) == 0) s_m[threadIdx.x >> 5] = best;
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                unsigned long long b = 0;
-                for (int i = 0; i < kInitThreads / 32; ++i) b = s_m[i] > b ? s_m[i] : b;
-                a.mparts[(size_t)par * gridDim.x + blockIdx.x] = b;
-            }
-            grid.sync();
-            unsigned long long b = 0;
-            if (threadIdx.x < 32) {
-                for (unsigned i = threadIdx.x; i < gridDim.x; i += 32) {
-                    const unsigned long long t = a.mparts[(size_t)par * gridDim.x + i];
-                    b = t > b ? t : b;
-                }
-                for (int o = 16; o; o >>= 1) {
-                    const unsigned long long t = __shfl_xor_sync(0xffffffffu, b, o);
-                    b = t > b ? t : b;
-                }
-            }
-            __syncthreads(); // everyone has read s_m before it is overwritten
-            if (threadIdx.x == 0) s_m[0] = b;
-            __syncthreads();
-            b = s_m[0];
-            pick = (uint64_t)(uint32_t)~(uint32_t)(b & 0xFFFFFFFFull);
-        } else {
-            update_masses<M>(a, par, 0, k == 1, clast, md_in, md_out, lo, hi, s_w);
-            grid.sync();
-            pick = locate_draw<M>(a, grid, par, a.nu[k], 0, md_out, s_w);
-        }
-        par ^= 1;
-        clast = __ldg(a.colors + pick);
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
-            a.cen[3 * k] = (double)((clast >> 16) & 255u);
-            a.cen[3 * k + 1] = (double)((clast >> 8) & 255u);
-            a.cen[3 * k + 2] = (double)(clast & 255u);
-        }
-        __syncthreads();
-    }
 }
 
 // ---------------------------------------------------------------------------
@@ -811,9 +704,6 @@ __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long
     unsigned long long v;
     asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
-}
-__device__ __forceinline__ void st_release_u64(unsigned long long *p, unsigned long long v) {
-    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ void st_relaxed_u64(unsigned long long *p, unsigned long long v) {
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -1443,9 +1333,6 @@ __global__ void __launch_bounds__(kInitThreads, 3) init_kernel_tile(InitArgs a) 
 #ifndef CQG_EXP_SKIP_UPDATE
 #define CQG_EXP_SKIP_UPDATE 0
 #endif
-#ifndef CQG_EXP_SKIP_BARRIER2
-#define CQG_EXP_SKIP_BARRIER2 0
-#endif
 #ifndef CQG_CLUSTER_THREADS
 #define CQG_CLUSTER_THREADS 1024
 #endif
@@ -1520,15 +1407,6 @@ __device__ __forceinline__ void st_async_T(uint32_t raddr, u128 v, uint32_t rbar
     st_async_v4(raddr, (uint32_t)v, (uint32_t)(v >> 32), (uint32_t)(v >> 64), (uint32_t)(v >> 96), rbar);
 }
 
-// Split cluster barrier: only a warp that wrote data other CTAs (or other
-// warps) will read after the barrier pays the release fence; the rest arrive
-// relaxed. Every warp waits with acquire semantics.
-__device__ __forceinline__ void cluster_barrier(bool release) {
-    if (release) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
-    else asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
-    asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
-}
-
 // Phase timing of the cluster initialiser (tools/init_timing.py builds with
 // -DCQG_INIT_TIMING): clock64 deltas of CTA 0 / thread 0, summed over rounds.
 #ifdef CQG_INIT_TIMING
@@ -1569,425 +1447,6 @@ __device__ uint64_t cluster_sequential_draw(const InitArgs &a, cg::cluster_group
     return a.n - 1;
 }
 
-// inclusive warp scan of up to 32 values; returns the first lane whose
-// inclusive prefix exceeds U (or 32) and the exclusive prefix at that lane
-template <class M>
-__device__ __forceinline__ int lane_locate(typename M::T v, typename M::T U, typename M::T *before,
-                                           typename M::T *total) {
-    typedef typename M::T T;
-    const int lane = threadIdx.x & 31;
-    const T incl = warp_incl<M>(v);
-    *total = M::shfl(incl, 31);
-    const unsigned m = __ballot_sync(0xffffffffu, incl > U);
-    if (!m) {
-        *before = *total;
-        return 32;
-    }
-    const int l = __ffs(m) - 1;
-    *before = M::shfl(incl - v, l);
-    return l;
-}
-
-template <class M>
-__global__ void __launch_bounds__(kClusterThreads, 1) init_cluster_kernel(InitArgs a, int ppt, int mbar) {
-    typedef typename M::T T;
-    cg::cluster_group cl = cg::this_cluster();
-    const int C = (int)cl.num_blocks(), crank = (int)cl.block_rank();
-    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    const uint64_t chunk = (uint64_t)kClusterThreads * ppt;
-    const uint64_t lo = (uint64_t)crank * chunk;
-    const uint64_t hi = lo + chunk < a.n ? lo + chunk : a.n;
-    const int mine = hi > lo ? (int)(hi - lo) : 0;
-    extern __shared__ __align__(16) unsigned char sm_raw[];
-    T *s_wsum = reinterpret_cast<T *>(sm_raw);                 // 2 x 32 warp totals
-    T *s_wpre = s_wsum + 2 * 32;                               // 2 x 32 exclusive warp prefixes
-    // every rank's CTA sum, pushed here by its owner before the cluster barrier
-    T *s_allc = s_wpre + 2 * 32;                               // 2 x kMaxClusterCtas
-    unsigned long long *s_key = reinterpret_cast<unsigned long long *>(s_allc + 2 * kMaxClusterCtas); // 2
-    __shared__ unsigned long long s_wkey[32];
-    __shared__ uint32_t s_wcol[32];
-    uint32_t *s_col = reinterpret_cast<uint32_t *>(s_key + 2);
-    uint32_t *s_cnt = s_col + chunk;
-    uint32_t *s_md = s_cnt + chunk;                            // chunk, updated in place
-    __shared__ unsigned long long s_pick;
-    __shared__ int s_amb, s_found;
-    for (int i = t; i < (int)chunk; i += kClusterThreads) { // padding: colour 0, count 0 (mass 0)
-        s_col[i] = i < mine ? __ldg(a.colors + lo + i) : 0u;
-        s_cnt[i] = i < mine ? __ldg(a.counts + lo + i) : 0u;
-    }
-    __syncthreads();
-    // ppt is a multiple of 4: each thread's run is 16-byte aligned (128-bit shared loads)
-    const int p0 = t * ppt, p1 = min(p0 + ppt, mine);
-    __shared__ uint32_t s_pickcol;
-    // mbar: CTA sums and the pick travel by st.async into per-parity slots, each
-    // signalling the receiver's mbarrier (s_bar[par]: sums, s_bar[2 + par]: pick)
-    __shared__ uint64_t s_bar[4];
-    __shared__ __align__(16) uint32_t s_pk4[2][4]; // pick lo, pick hi, colour, ambiguous
-    __shared__ __align__(16) uint32_t s_mk[2][kMaxClusterCtas][4]; // maximin: every CTA's best key + colour
-    __shared__ int s_nf;
-    int use_s[2] = {0, 0}, use_p[2] = {0, 0}; // phases consumed per barrier (uniform per CTA)
-    if (mbar) {
-        if (t == 0) {
-            for (int i = 0; i < 4; ++i) mbar_init(&s_bar[i], 1);
-            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        }
-        cl.sync(); // every CTA's barriers exist before the first remote signal
-    }
-
-    auto colour_of = [&](uint64_t gi) -> uint32_t {
-        return *cl.map_shared_rank(s_col + (gi % chunk), (unsigned)(gi / chunk));
-    };
-
-    // Thread sums -> warp totals (s_wsum) -> exclusive warp prefixes (s_wpre,
-    // warp 0) and the CTA sum pushed into every rank.
-    __shared__ T s_U, s_cpre;
-    __shared__ int s_tw;
-    auto publish = [&](int par, T ts) {
-        if (t == 0) {
-            s_found = 0; // before this round's first barrier: no owner has written yet
-            if (mbar) { // this round's incoming bytes: C CTA sums, one 16-byte pick
-                mbar_arrive_expect(&s_bar[par], (uint32_t)(C * sizeof(T)));
-                mbar_arrive_expect(&s_bar[2 + par], 16u);
-            }
-        }
-        T w = ts;
-        for (int o = 16; o; o >>= 1) w += M::shfl(w, lane ^ o);
-        if (lane == 0) s_wsum[par * 32 + warp] = w;
-        __syncthreads();
-        if (warp == 0) {
-            const T wv = s_wsum[par * 32 + lane];
-            const T wincl = warp_incl<M>(wv);
-            s_wpre[par * 32 + lane] = wincl - wv;
-            const T c = M::shfl(wincl, 31);
-            if (lane < C) {
-                if (mbar)
-                    st_async_T(mapa_rank(smem_addr(s_allc + par * kMaxClusterCtas + crank), lane), c,
-                               mapa_rank(smem_addr(&s_bar[par]), lane));
-                else
-                    *cl.map_shared_rank(s_allc + par * kMaxClusterCtas + crank, lane) = c;
-            }
-        }
-        if (mbar) __syncthreads(); // s_wpre (warp 0) for every warp; the cluster barrier did this before
-    };
-
-    // after publish: every CTA sum has arrived
-    auto wait_sums = [&](int par) {
-        if (mbar) {
-            mbar_wait(&s_bar[par], (uint32_t)(use_s[par] & 1));
-            ++use_s[par];
-        } else {
-            cluster_barrier(warp == 0); // warp 0 pushed the CTA sum and wrote s_wpre
-        }
-    };
-
-    // One weighted draw over this round's masses (md = nullptr: weights only),
-    // after the cluster barrier that published every CTA sum. Warp 0 finds the
-    // target U, this CTA's offset and the warp whose range holds U (if any);
-    // only that warp scans its lanes' sums and searches the owning thread's
-    // <= 32 points in local shared memory, then writes (index, colour,
-    // ambiguity) into every rank; a second cluster barrier publishes them.
-    auto draw = [&](int par, double nu, const uint32_t *mdb, T ts, uint32_t &pick_col) -> uint64_t {
-        if (warp == 0) {
-            const T cv = lane < C ? s_allc[par * kMaxClusterCtas + lane] : (T)0;
-            const T cincl = warp_incl<M>(cv);
-            const T total = M::shfl(cincl, 31);
-            const T U = M::target(nu, total);
-            const T cpre = M::shfl(cincl - cv, crank);
-            const T wlo = cpre + s_wpre[par * 32 + lane];
-            const T whi = wlo + s_wsum[par * 32 + lane];
-            const unsigned m = __ballot_sync(0xffffffffu, !(U < wlo) && U < whi && s_wsum[par * 32 + lane] != (T)0);
-            if (lane == 0) {
-                s_U = U;
-                s_cpre = cpre;
-                s_tw = m ? __ffs(m) - 1 : -1;
-                s_nf = U < total ? 0 : 1; // no owner anywhere: identical in every CTA
-            }
-        }
-        __syncthreads();
-        const T U = s_U;
-        if (warp == s_tw) {
-            const T incl = warp_incl<M>(ts);
-            const T lo_t = s_cpre + s_wpre[par * 32 + warp] + incl - ts;
-            const unsigned hm = __ballot_sync(0xffffffffu, ts != (T)0 && !(U < lo_t) && U < lo_t + ts);
-            const int tl = __ffs(hm) - 1; // the owning lane (exactly one)
-            const T base = M::shfl(lo_t, tl);
-            // the owner's points, one per lane, from local shared memory
-            const int q0 = (warp * 32 + tl) * ppt;
-            const int q = q0 + lane;
-            T m = 0;
-            uint32_t col = 0;
-            if (lane < ppt) {
-                m = M::mass_c(a, s_cnt[q], mdb ? mdb[q] : kWeightsOnly);
-                col = s_col[q];
-            }
-            const T mincl = warp_incl<M>(m);
-            const unsigned pm = __ballot_sync(0xffffffffu, lane < ppt && U < base + mincl);
-            const int pl = __ffs(pm) - 1;
-            const T E = base + M::shfl(mincl, pl);
-            const T prevE = E - M::shfl(m, pl);
-            const uint32_t pcol = __shfl_sync(0xffffffffu, col, pl);
-            const uint64_t gi = lo + (uint64_t)(q0 + pl);
-            bool amb = false;
-            if (!M::exact) {
-                T total = 0;
-                for (int r = 0; r < C; ++r) total += s_allc[par * kMaxClusterCtas + r];
-                const T B2 = M::bound(a.n, total);
-                // the reference returns n-1 when no earlier prefix exceeds u
-                amb = gi == a.n - 1 ? !(U > prevE + B2) : (!(E > U + B2) || (gi > 0 && !(U > prevE + B2)));
-            }
-            if (lane < C) { // one rank per lane
-                if (mbar) {
-                    st_async_v4(mapa_rank(smem_addr(s_pk4[par]), lane), (uint32_t)gi, (uint32_t)(gi >> 32), pcol,
-                                amb ? 1u : 0u, mapa_rank(smem_addr(&s_bar[2 + par]), lane));
-                } else {
-                    *cl.map_shared_rank(&s_pick, lane) = gi;
-                    *cl.map_shared_rank(&s_pickcol, lane) = pcol;
-                    *cl.map_shared_rank(&s_amb, lane) = amb ? 1 : 0;
-                    *cl.map_shared_rank(&s_found, lane) = 1;
-                }
-            }
-            if (!mbar && !CQG_EXP_SKIP_BARRIER2) cluster_barrier(true);
-        } else {
-            if (!mbar && !CQG_EXP_SKIP_BARRIER2) cluster_barrier(false);
-        }
-        if (CQG_EXP_SKIP_BARRIER2) __syncthreads();
-        if (mbar) {
-            // no owner: complete this CTA's expected pick bytes itself (the phase must end)
-            if (s_nf && t == 0) mbar_complete_local(&s_bar[2 + par], 16u);
-            mbar_wait(&s_bar[2 + par], (uint32_t)(use_p[par] & 1));
-            ++use_p[par];
-            // the common case: every thread reads the pushed pick itself (the wait
-            // acquired it), no further block barrier
-            if (!s_nf && !s_pk4[par][3]) {
-                pick_col = s_pk4[par][2];
-                return ((unsigned long long)s_pk4[par][1] << 32) | s_pk4[par][0];
-            }
-            if (t == 0 && !s_nf) {
-                s_pick = ((unsigned long long)s_pk4[par][1] << 32) | s_pk4[par][0];
-                s_pickcol = s_pk4[par][2];
-                s_amb = (int)s_pk4[par][3];
-                s_found = 1;
-            }
-            __syncthreads();
-        }
-        if (!s_found) { // the target lies beyond every prefix: the reference returns n-1
-            cl.sync(); // uniform; other CTAs' min distances stay untouched while read below
-            __syncthreads();
-            if (t == 0) {
-                const uint64_t last = a.n - 1;
-                bool amb = false;
-                if (!M::exact && a.n > 1) {
-                    T total = 0;
-                    for (int r = 0; r < C; ++r) total += s_allc[par * kMaxClusterCtas + r];
-                    const uint32_t r = (uint32_t)(last / chunk), li = (uint32_t)(last % chunk);
-                    const uint32_t cnt = *cl.map_shared_rank(s_cnt + li, r);
-                    const uint32_t md = mdb ? *cl.map_shared_rank(mdb + li, r) : kWeightsOnly;
-                    amb = !(U > total - M::mass_c(a, cnt, md) + M::bound(a.n, total));
-                }
-                s_pick = last;
-                s_pickcol = colour_of(last);
-                s_amb = amb ? 1 : 0;
-            }
-            __syncthreads();
-            cl.sync(); // nobody updates before every CTA has read
-        }
-        if (s_amb) { // identical in every CTA: uniform extra barrier
-            __syncthreads();
-            if (crank == 0 && t == 0) {
-                s_pick = cluster_sequential_draw<M>(a, cl, s_cnt, mdb, chunk, nu, mdb == nullptr);
-                atomicAdd(a.fallbacks, 1ull);
-            }
-            cl.sync();
-            const unsigned long long v = *cl.map_shared_rank(&s_pick, 0);
-            __syncthreads();
-            if (t == 0) {
-                s_pick = v;
-                s_pickcol = colour_of(v);
-            }
-            __syncthreads();
-        }
-        pick_col = s_pickcol;
-        return s_pick;
-    };
-
-    int par = 0;
-    uint64_t first;
-    if (a.kind == 1 || a.weighted_first) {
-        T ts = 0;
-        for (int i = p0; i < p1; ++i) ts += M::mass_c(a, s_cnt[i], kWeightsOnly);
-        publish(par, ts);
-        wait_sums(par);
-        uint32_t fcol = 0;
-        first = draw(par, a.nu[0], nullptr, ts, fcol);
-        __syncthreads(); // s_pickcol is written by thread 0 below
-        if (t == 0) s_pickcol = fcol;
-        __syncthreads();
-        par ^= 1;
-    } else {
-        first = a.first_index;
-        if (t == 0) s_pickcol = colour_of(first);
-        __syncthreads();
-    }
-    uint32_t clast = s_pickcol;
-    if (crank == 0 && t == 0) {
-        a.cen[0] = (double)((clast >> 16) & 255u);
-        a.cen[1] = (double)((clast >> 8) & 255u);
-        a.cen[2] = (double)(clast & 255u);
-    }
-#ifdef CQG_INIT_TIMING
-    unsigned long long _tprev = clock64();
-#endif
-    T ts_run = 0; // this thread's mass sum, kept across rounds (exact deltas)
-    for (int k = 1; k < a.K; ++k) {
-        uint64_t pick;
-        uint32_t kcol = 0;
-        const uint32_t bb = __dp4a(clast, clast, 0u);
-        if (a.kind == 0) {
-            unsigned long long best = 0;
-            uint32_t bcol = 0;
-            for (int i = p0; i < p1; ++i) {
-                const uint32_t d = d2_int_bb(s_col[i], clast, bb);
-                const uint32_t m = k == 1 ? d : min(s_md[i], d);
-                s_md[i] = m;
-                const unsigned long long key = ((unsigned long long)m << 32) | (uint32_t)~(uint32_t)(lo + i);
-                if (key > best) {
-                    best = key;
-                    bcol = s_col[i];
-                }
-            }
-            if (mbar) {
-                // (key, colour) maxima -> pushed into every CTA; every thread takes the max
-                if (t == 0) mbar_arrive_expect(&s_bar[par], (uint32_t)(C * 16));
-                for (int o = 16; o; o >>= 1) {
-                    const unsigned long long x = __shfl_xor_sync(0xffffffffu, best, o);
-                    const uint32_t xc = __shfl_xor_sync(0xffffffffu, bcol, o);
-                    if (x > best) {
-                        best = x;
-                        bcol = xc;
-                    }
-                }
-                if (lane == 0) {
-                    s_wkey[warp] = best;
-                    s_wcol[warp] = bcol;
-                }
-                __syncthreads();
-                if (warp == 0) {
-                    unsigned long long b = s_wkey[lane];
-                    uint32_t bc = s_wcol[lane];
-                    for (int o = 16; o; o >>= 1) {
-                        const unsigned long long x = __shfl_xor_sync(0xffffffffu, b, o);
-                        const uint32_t xc = __shfl_xor_sync(0xffffffffu, bc, o);
-                        if (x > b) {
-                            b = x;
-                            bc = xc;
-                        }
-                    }
-                    if (lane < C)
-                        st_async_v4(mapa_rank(smem_addr(s_mk[par][crank]), lane), (uint32_t)b, (uint32_t)(b >> 32), bc,
-                                    0u, mapa_rank(smem_addr(&s_bar[par]), lane));
-                }
-                mbar_wait(&s_bar[par], (uint32_t)(use_s[par] & 1));
-                ++use_s[par];
-                unsigned long long b = 0;
-                uint32_t bc = 0;
-                for (int r = 0; r < C; ++r) {
-                    const unsigned long long x = ((unsigned long long)s_mk[par][r][1] << 32) | s_mk[par][r][0];
-                    if (x > b) {
-                        b = x;
-                        bc = s_mk[par][r][2];
-                    }
-                }
-                pick = (uint64_t)(uint32_t)~(uint32_t)(b & 0xFFFFFFFFull);
-                kcol = bc;
-            } else {
-            for (int o = 16; o; o >>= 1) {
-                const unsigned long long x = __shfl_xor_sync(0xffffffffu, best, o);
-                best = x > best ? x : best;
-            }
-            if (lane == 0) s_wkey[warp] = best;
-            __syncthreads();
-            if (warp == 0) {
-                unsigned long long b = s_wkey[lane];
-                for (int o = 16; o; o >>= 1) {
-                    const unsigned long long x = __shfl_xor_sync(0xffffffffu, b, o);
-                    b = x > b ? x : b;
-                }
-                if (lane == 0) s_key[par] = b;
-            }
-            cl.sync();
-            if (warp == 0) {
-                unsigned long long b = lane < C ? *cl.map_shared_rank(s_key + par, lane) : 0ull;
-                for (int o = 16; o; o >>= 1) {
-                    const unsigned long long x = __shfl_xor_sync(0xffffffffu, b, o);
-                    b = x > b ? x : b;
-                }
-                if (lane == 0) s_pick = (uint64_t)(uint32_t)~(uint32_t)(b & 0xFFFFFFFFull);
-            }
-            __syncthreads();
-            pick = s_pick;
-            kcol = colour_of(pick);
-            }
-        } else {
-            const double nu_k = __ldg(a.nu + k); // off the locate's critical path
-            // whole 4-point runs (padding has count 0: mass 0). md is updated in
-            // place: after the previous round's second barrier nobody reads it.
-            if (k == 1) {
-                for (int i = p0; i < p0 + ppt; i += 4) {
-                    const uint4 c4 = *reinterpret_cast<const uint4 *>(s_col + i);
-                    const uint4 n4 = *reinterpret_cast<const uint4 *>(s_cnt + i);
-                    uint4 m4;
-                    m4.x = d2_int_bb(c4.x, clast, bb);
-                    m4.y = d2_int_bb(c4.y, clast, bb);
-                    m4.z = d2_int_bb(c4.z, clast, bb);
-                    m4.w = d2_int_bb(c4.w, clast, bb);
-                    *reinterpret_cast<uint4 *>(s_md + i) = m4;
-                    ts_run += M::mass_c(a, n4.x, m4.x) + M::mass_c(a, n4.y, m4.y) + M::mass_c(a, n4.z, m4.z) +
-                              M::mass_c(a, n4.w, m4.w);
-                }
-            } else if (CQG_EXP_SKIP_UPDATE) {
-                // timing experiment only (tools/init_timing.py --skip-update)
-            } else {
-                // only points closer to the new centre change: their mass
-                // difference is subtracted from the running sum (exact)
-                T delta = 0;
-                for (int i = p0; i < p0 + ppt; i += 4) {
-                    const uint4 c4 = *reinterpret_cast<const uint4 *>(s_col + i);
-                    uint4 m4 = *reinterpret_cast<const uint4 *>(s_md + i);
-                    const uint32_t dx = d2_int_bb(c4.x, clast, bb), dy = d2_int_bb(c4.y, clast, bb),
-                                   dz = d2_int_bb(c4.z, clast, bb), dw = d2_int_bb(c4.w, clast, bb);
-                    if ((dx < m4.x) | (dy < m4.y) | (dz < m4.z) | (dw < m4.w)) {
-                        const uint4 n4 = *reinterpret_cast<const uint4 *>(s_cnt + i);
-                        if (dx < m4.x) { delta += M::mass_c(a, n4.x, m4.x) - M::mass_c(a, n4.x, dx); m4.x = dx; }
-                        if (dy < m4.y) { delta += M::mass_c(a, n4.y, m4.y) - M::mass_c(a, n4.y, dy); m4.y = dy; }
-                        if (dz < m4.z) { delta += M::mass_c(a, n4.z, m4.z) - M::mass_c(a, n4.z, dz); m4.z = dz; }
-                        if (dw < m4.w) { delta += M::mass_c(a, n4.w, m4.w) - M::mass_c(a, n4.w, dw); m4.w = dw; }
-                        *reinterpret_cast<uint4 *>(s_md + i) = m4;
-                    }
-                }
-                ts_run -= delta;
-            }
-            ITIME(0);
-            publish(par, ts_run);
-            ITIME(1);
-            wait_sums(par);
-            ITIME(2);
-            pick = draw(par, nu_k, s_md, ts_run, kcol);
-            ITIME(3);
-        }
-        par ^= 1;
-        clast = kcol;
-        if (crank == 0 && t == 0) {
-            a.cen[3 * k] = (double)((clast >> 16) & 255u);
-            a.cen[3 * k + 1] = (double)((clast >> 8) & 255u);
-            a.cen[3 * k + 2] = (double)(clast & 255u);
-        }
-        // with mbarrier signalling the rounds are ordered by the next round's
-        // signals (slots are per parity); the barrier path reuses s_pick
-        if (!mbar) __syncthreads();
-        ITIME(4);
-    }
-    cl.sync(); // no CTA may exit while others still read its shared memory
-}
 
 // Register-resident variant (the default): thread t keeps its PPT colours and
 // min distances in registers, so a round's update reads no shared memory
@@ -2301,12 +1760,6 @@ __global__ void __launch_bounds__(NT, 1) init_cluster_reg_kernel(InitArgs a) {
     cl.sync(); // no CTA may exit while others still read its shared memory
 }
 
-template <class M>
-static size_t cluster_smem(int ppt) {
-    return sizeof(typename M::T) * (2 * 32 + 2 * 32 + 2 * kMaxClusterCtas) + 16 +
-           (size_t)kClusterThreads * ppt * 3 * sizeof(uint32_t); // colour, count, md
-}
-
 // launch one 16-CTA cluster of `kern`; false when it cannot be resident
 template <class... KArgs, class... Args>
 static bool launch_cluster(cqg_ctx *ctx, const InitArgs &a, int nt, void (*kern)(KArgs...), size_t smem,
@@ -2352,7 +1805,7 @@ static bool launch_cluster_init(cqg_ctx *ctx, InitArgs a) {
     // ppt is capped per size by the register budget (65536 / threads).
     // Measured: cfg2 k-means++ 1024x12 0.648 ms -> 896x12 0.596 ms; cfg1
     // maximin 1024x12 0.104 -> 512x20 0.085 ms. CQG_CLUSTER_NT forces a size.
-    if (ctx->use_init_reg && ctx->use_mbar_init && ctx->cluster_nt != kClusterThreads) {
+    if (ctx->cluster_nt != kClusterThreads) {
         static const int kNt[5] = {512, 640, 768, 896, 1024}, kCap[5] = {24, 20, 16, 12, 12};
         int bi = -1, bp = 0;
         uint64_t bslots = ~0ull;
@@ -2375,25 +1828,23 @@ static bool launch_cluster_init(cqg_ctx *ctx, InitArgs a) {
 #undef CQG_REG_CASE
         }
     }
+    // kClusterThreads threads per CTA: up to 12 points per thread (the register budget at 1024 threads;
+    // up to 24 in a CQG_CLUSTER_THREADS < 1024 experiment build)
     const int ppt = ((int)((per + kClusterThreads - 1) / kClusterThreads) + 3) & ~3; // 128-bit runs
-    if (ppt < 1 || ppt > ctx->cluster_max_ppt) return false;
-    const bool reg = ctx->use_init_reg && ctx->use_mbar_init && (ppt <= 12 || (kClusterThreads < 1024 && ppt <= 24));
-    const size_t smem = reg ? (size_t)kClusterThreads * ppt * 3 * sizeof(uint32_t) : cluster_smem<M>(ppt);
+    if (ppt < 1 || !(ppt <= 12 || (kClusterThreads < 1024 && ppt <= 24))) return false;
+    const size_t smem = (size_t)kClusterThreads * ppt * 3 * sizeof(uint32_t);
     if (smem > 227 * 1024) return false;
     constexpr int NT = kClusterThreads;
-    if (reg) {
-        switch (ppt) {
-        case 4: return launch_cluster(ctx, a, NT, init_cluster_reg_kernel<M, 4, NT>, smem, a);
-        case 8: return launch_cluster(ctx, a, NT, init_cluster_reg_kernel<M, 8, NT>, smem, a);
+    switch (ppt) {
+    case 4: return launch_cluster(ctx, a, NT, init_cluster_reg_kernel<M, 4, NT>, smem, a);
+    case 8: return launch_cluster(ctx, a, NT, init_cluster_reg_kernel<M, 8, NT>, smem, a);
 #if CQG_CLUSTER_THREADS < 1024
-        case 16: return launch_cluster(ctx, a, NT, init_cluster_reg_kernel<M, 16, NT>, smem, a);
-        case 20: return launch_cluster(ctx, a, NT, init_cluster_reg_kernel<M, 20, NT>, smem, a);
-        case 24: return launch_cluster(ctx, a, NT, init_cluster_reg_kernel<M, 24, NT>, smem, a);
+    case 16: return launch_cluster(ctx, a, NT, init_cluster_reg_kernel<M, 16, NT>, smem, a);
+    case 20: return launch_cluster(ctx, a, NT, init_cluster_reg_kernel<M, 20, NT>, smem, a);
+    case 24: return launch_cluster(ctx, a, NT, init_cluster_reg_kernel<M, 24, NT>, smem, a);
 #endif
-        default: return launch_cluster(ctx, a, NT, init_cluster_reg_kernel<M, 12, NT>, smem, a);
-        }
+    default: return launch_cluster(ctx, a, NT, init_cluster_reg_kernel<M, 12, NT>, smem, a);
     }
-    return launch_cluster(ctx, a, NT, init_cluster_kernel<M>, smem, a, ppt, ctx->use_mbar_init ? 1 : 0);
 }
 
 static int tile_grid(const cqg_ctx *ctx, uint64_t threads) {
@@ -2446,10 +1897,9 @@ void run_init(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *counts_d, 
         c.force_seq = ctx->dbg_init_force_seq;
         if (exact ? launch_cluster_init<ExactMass>(ctx, c) : launch_cluster_init<FixedMass>(ctx, c)) return;
     }
-    const bool rec = ctx->use_init_rec;
     // colour-space tiles: every colour on its own Morton slot (a duplicate
     // colour -- raw-pixel substrates -- keeps the record layout)
-    bool tile = rec && ctx->use_init_tile && n >= ctx->init_tile_min && n <= (1ull << 24);
+    bool tile = ctx->use_init_tile && n >= ctx->init_tile_min && n <= (1ull << 24);
     const uint64_t ntiles = (n + kTile - 1) / kTile;
     uint32_t *tbits = nullptr, *tpref = nullptr, *tbsum = nullptr;
     if (tile) {
@@ -2472,16 +1922,15 @@ void run_init(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *counts_d, 
         CQG_CUDA(cudaStreamSynchronize(s));
         tile = *dup_h == 0;
     }
-    const void *kern = tile  ? (exact ? (const void *)init_kernel_tile<ExactMass> : (const void *)init_kernel_tile<FixedMass>)
-                       : rec ? (exact ? (const void *)init_kernel_rec<ExactMass> : (const void *)init_kernel_rec<FixedMass>)
-                             : (exact ? (const void *)init_kernel<ExactMass> : (const void *)init_kernel<FixedMass>);
+    const void *kern = tile ? (exact ? (const void *)init_kernel_tile<ExactMass> : (const void *)init_kernel_tile<FixedMass>)
+                            : (exact ? (const void *)init_kernel_rec<ExactMass> : (const void *)init_kernel_rec<FixedMass>);
     int occ = 0;
     CQG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kInitThreads, 0));
     if (occ < 1) occ = 1;
     // k-means++ record rounds are load-latency bound: 3 blocks per SM (maximin
     // measured faster with 2: one barrier per round, fewer arrivals)
     // (tile rounds: 2 per SM -- fewer arrivals per hand-off; cfg3 2.34 -> 1.97 ms, cfg5 6.33 -> 6.12 ms vs 3)
-    const int per_want = tile ? 2 : (rec && kind == 1 ? 3 : 2);
+    const int per_want = tile ? 2 : (kind == 1 ? 3 : 2);
     const int per_sm = occ > per_want ? per_want : occ;
     uint64_t grid = (uint64_t)ctx->num_sms * (uint64_t)per_sm;
     if (grid > (uint64_t)kLocateMax) grid = kLocateMax; // warp_locate scans <= kLocateMax block sums
@@ -2517,7 +1966,7 @@ void run_init(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *counts_d, 
     a.chunk = chunk;
     a.nu = nu_d;
     a.md = md;
-    a.mds = rec ? 2 : 1;
+    a.mds = 2; // {colour, md} records
     a.parts = parts;
     a.segs = segs;
     a.mparts = mparts;

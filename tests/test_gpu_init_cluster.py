@@ -2,10 +2,8 @@
 bit-exact against the oracle: the register-resident kernel (default: the CTA
 shape with the fewest padded slots; CQG_CLUSTER_NT forces 512..1024 threads)
 at each points-per-thread instantiation and both mass arithmetics (P a
-power of two: exact integers; otherwise 2^-88 fixed point), the
-shared-memory kernel (CQG_NO_INIT_REG=1), its cluster-barrier signalling
-(CQG_NO_MBAR_INIT=1), and the register kernel's rare sequential paths forced
-on every draw (CQG_DBG_INIT_FORCE_SEQ=1: ambiguous decision; =2: target beyond
+power of two: exact integers; otherwise 2^-88 fixed point), and the register
+kernel's rare sequential paths forced on every draw (CQG_DBG_INIT_FORCE_SEQ=1: ambiguous decision; =2: target beyond
 every prefix) -- the reference replay must give the same centres.
 """
 import os
@@ -35,8 +33,6 @@ def _ctx(**env):
 @pytest.fixture(scope="module")
 def ctxs():
     cs = {"reg": _ctx(),
-          "smem": _ctx(CQG_NO_INIT_REG="1"),
-          "barrier": _ctx(CQG_NO_MBAR_INIT="1"),
           "nt1024": _ctx(CQG_CLUSTER_NT="1024"),
           "nt896": _ctx(CQG_CLUSTER_NT="896"),
           "nt768": _ctx(CQG_CLUSTER_NT="768"),
@@ -73,7 +69,7 @@ CASES = [(256, 256, 0.3, 64, 3, 4), (300, 200, 0.02, 64, 9, 4),
          (512, 512, 0.02, 256, 5, 12), (384, 384, 0.6, 200, 11, 12)]
 
 
-@pytest.mark.parametrize("variant", ["reg", "smem", "barrier", "nt1024", "nt896", "nt768", "nt640", "nt512"])
+@pytest.mark.parametrize("variant", ["reg", "nt1024", "nt896", "nt768", "nt640", "nt512"])
 @pytest.mark.parametrize("w,h,noise,K,seed,ppt", CASES)
 def test_init_cluster_variants(ctxs, oracle, variant, w, h, noise, K, seed, ppt):
     img = synth_image(w, h, 5, nblobs=10, sigma=15.0, noise=noise)
@@ -100,7 +96,7 @@ def test_init_cluster_shapes_near_unique(ctxs, oracle, variant, w, h):
 def test_init_cluster_tiny_and_duplicates(ctxs, oracle):
     # fewer colours than CTAs x threads: most threads and whole CTAs own padding only
     rng = np.random.default_rng(1)
-    for ctx in (ctxs["reg"], ctxs["smem"]):
+    for ctx in (ctxs["reg"], ctxs["nt1024"]):
         img = rng.integers(0, 3, size=(17, 13, 3), dtype=np.uint8) * 100
         n = quant.build_histogram(img, ctx=ctx).packed.size
         _check(ctx, oracle, img, min(n, 5), 2)

@@ -1,7 +1,7 @@
 """Initialisers on the cooperative (large substrate) kernels: bit-exact
-against the oracle for the three grid layouts -- colour-space tiles with box
-pruning (default), {colour, md} records in histogram order
-(CQG_NO_INIT_TILE=1) and the ping-pong layout (CQG_NO_INIT_REC=1) -- and for
+against the oracle for the two grid layouts -- colour-space tiles with box
+pruning (default) and {colour, md} records in histogram order
+(CQG_NO_INIT_TILE=1) -- and for
 both mass arithmetics (P a power of two: exact integers; otherwise 2^-88
 fixed point with the sequential FP64 fallback). Small inputs reach the same
 kernels with the cluster initialiser switched off (CQG_NO_CLUSTER_INIT=1).
@@ -35,8 +35,7 @@ def _ctx(**env):
 @pytest.fixture(scope="module")
 def ctxs():
     cs = {"tile": _ctx(CQG_NO_CLUSTER_INIT="1", CQG_INIT_TILE_MIN="0"),
-          "rec": _ctx(CQG_NO_CLUSTER_INIT="1", CQG_NO_INIT_TILE="1"),
-          "pingpong": _ctx(CQG_NO_CLUSTER_INIT="1", CQG_NO_INIT_REC="1")}
+          "rec": _ctx(CQG_NO_CLUSTER_INIT="1", CQG_NO_INIT_TILE="1")}
     yield cs
     for c in cs.values():
         c.close()
@@ -55,14 +54,14 @@ def _check(ctx, oracle, img, K, seed):
     return c.size
 
 
-@pytest.mark.parametrize("layout", ["tile", "rec", "pingpong"])
+@pytest.mark.parametrize("layout", ["tile", "rec"])
 @pytest.mark.parametrize("w,h,K,seed", [(40, 40, 8, 3), (300, 200, 64, 9), (512, 512, 33, 5)])
 def test_init_cooperative_small(ctxs, oracle, layout, w, h, K, seed):
     img = synth_image(w, h, seed, nblobs=10, sigma=15.0, noise=0.02)
     _check(ctxs[layout], oracle, img, K, seed)
 
 
-@pytest.mark.parametrize("layout", ["tile", "rec", "pingpong"])
+@pytest.mark.parametrize("layout", ["tile", "rec"])
 @pytest.mark.parametrize("w,h", [(1024, 1024), (1100, 900)])  # P = 2^20 (exact) / not a power of two
 def test_init_cooperative_large(ctxs, ctx, oracle, layout, w, h):
     img = synth_image(w, h, 4242, nblobs=30, sigma=25.0, noise=0.7)

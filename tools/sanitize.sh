@@ -4,7 +4,7 @@
 #   tools/sanitize.sh [tool ...]   (default: memcheck racecheck synccheck initcheck)
 mkdir -p gpurun_out/sanitize
 tools=${*:-memcheck racecheck synccheck initcheck}
-variants="default CQG_NO_PRUNE=1 CQG_NO_GRAPH=1 CQG_NO_NDC_CODE=1 CQG_NO_CLUSTER_INIT=1 CQG_NO_INIT_REG=1 CQG_NO_MBAR_INIT=1 CQG_NO_INIT_REC=1 CQG_INIT_TILE_MIN=1000"
+variants="default CQG_NO_PRUNE=1 CQG_NO_GRAPH=1 CQG_NO_NDC_CODE=1 CQG_NO_CLUSTER_INIT=1 CQG_INIT_TILE_MIN=1000"
 for tool in $tools; do
   for v in $variants; do
     env_set=""; [ "$v" != "default" ] && env_set="$v"

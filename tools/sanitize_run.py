@@ -3,7 +3,7 @@
 
   histogram     small fused path (P < 2^22) and the bucketed large path (2^22 pixels)
   initialisers  k-means++ and maximin (cluster kernel by default; CQG_NO_CLUSTER_INIT,
-                CQG_NO_INIT_REG, CQG_NO_MBAR_INIT, CQG_INIT_TILE_MIN select the others)
+                CQG_INIT_TILE_MIN / CQG_NO_INIT_TILE select the others)
   Lloyd         persistent kernel (default) / graph or host loop (CQG_NO_GRAPH) /
                 unpruned (CQG_NO_PRUNE) / without the code table (CQG_NO_NDC_CODE), repair
   mapping       MAPW / MAP sweeps, replay, MSE, mapping NDC, pixel kernel
