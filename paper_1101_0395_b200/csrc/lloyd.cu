@@ -1122,12 +1122,17 @@ static void launch_sweep_mode(cqg_ctx *ctx, const SweepArgs &a) {
         uint32_t *listn = list + n + 4;
         // the NDC (reads the labels before the sweep changes them) runs on the
         // second side stream beside the stay-test pass, joined before the sweep
-        const size_t cs = (size_t)a.K * 24 + (size_t)a.K * (a.Kpow + 2) * 2;
-        const int gc = pick_grid(ctx, n, 1024 * 4, 1);
         CQG_CUDA(cudaEventRecord(ctx->walk_fork, ctx->stream));
         CQG_CUDA(cudaStreamWaitEvent(ctx->aux2, ctx->walk_fork, 0));
-        ndc_code_kernel<4><<<gc, 1024, cs, ctx->aux2>>>(a.colors, a.labels, n, a.cen, a.dsorted, a.dcode, a.K,
-                                                       a.Kpow, a.ndc);
+        {
+            // prefix codes in shared memory, 2 blocks of 512 threads per SM: half of each SM's threads
+            // stay free for the stay-test pass running beside it (measured: 1 / 2 / 3 / 4 blocks per SM
+            // -> cfg5 Lloyd 11.52 / 10.44 / 10.52 / 10.59 ms; whole rows in one 1024-thread block 10.57)
+            const size_t cs = (size_t)a.K * 24 + (size_t)a.K * (kNdcPrefix + 2) * 2;
+            const int gc = pick_grid(ctx, n, 512 * 4, 2);
+            ndc_pre_kernel<4><<<gc, 512, cs, ctx->aux2>>>(a.colors, a.labels, n, a.cen, a.dsorted, a.dcode, a.K,
+                                                         a.Kpow, a.ndc);
+        }
         CQG_CUDA(cudaEventRecord(ctx->walk_join, ctx->aux2));
         CQG_CUDA(cudaMemsetAsync(listn, 0, 4, ctx->stream));
         const size_t fsm = filter_list_smem(a.K, a.Kp);

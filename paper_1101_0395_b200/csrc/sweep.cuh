@@ -424,6 +424,35 @@ __device__ __forceinline__ unsigned long long ndc_range_pre(const uint32_t *__re
     return local;
 }
 
+// NDC of a large substrate's WALK iteration with only the first kNdcPrefix walk
+// positions of every row in shared memory (34 KB at K = 256 against 132 KB for
+// whole rows): 4 blocks of 512 threads per SM instead of one of 1024, and a
+// lifting of 6 steps instead of 8. A walk visits ~4 centres on average, so
+// the FP64 row in L2 is searched for very few points.
+template <int Q>
+static __global__ void __launch_bounds__(512, 4) ndc_pre_kernel(const uint32_t *__restrict__ colors,
+                                                                 const uint32_t *__restrict__ labels, uint64_t n,
+                                                                 const double *__restrict__ cen,
+                                                                 const double *__restrict__ dsorted,
+                                                                 const uint16_t *__restrict__ dcode, int K, int Kpow,
+                                                                 unsigned long long *ndc) {
+    extern __shared__ __align__(16) double s_cenp[];
+    constexpr int rs = kNdcPrefix + 2;
+    uint16_t *s_pre = reinterpret_cast<uint16_t *>(s_cenp + 3 * K);
+    const int L = Kpow < kNdcPrefix ? Kpow : kNdcPrefix;
+    for (int i = threadIdx.x; i < 3 * K; i += blockDim.x) s_cenp[i] = cen[i];
+    for (int e = threadIdx.x; e < K * L; e += blockDim.x) {
+        const int r = e / L, p = e - r * L;
+        s_pre[r * rs + p] = __ldg(dcode + (size_t)r * Kpow + p);
+    }
+    __syncthreads();
+    unsigned long long local =
+        ndc_range_pre<Q>(colors, labels, 0, n, (uint64_t)blockIdx.x * blockDim.x * Q,
+                         (uint64_t)gridDim.x * blockDim.x * Q, s_cenp, dsorted, Kpow, s_pre);
+    for (int o = 16; o; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+    if ((threadIdx.x & 31) == 0 && local) atomicAdd(ndc, local);
+}
+
 template <int Q>
 static __global__ void __launch_bounds__(256, 4) ndc_kernel(const uint32_t *__restrict__ colors,
                                                   const uint32_t *__restrict__ labels, uint64_t n,
