@@ -1274,6 +1274,7 @@ __global__ void __launch_bounds__(kInitThreads, 3) init_kernel_tile(InitArgs a) 
     // block 0 alone waits for all arrivals, locates the draw and publishes it;
     // the others poll the published round number with back-off (a spinning grid
     // barrier would load the memory system under block 0's locate).
+    __shared__ unsigned long long s_rel;
     unsigned long long *arrive = a.result + 6;
     unsigned long long *flag = a.tflags + (size_t)blockIdx.x * kFlagStride; // this block's release word
     const unsigned long long G = gridDim.x;
@@ -1310,26 +1311,27 @@ __global__ void __launch_bounds__(kInitThreads, 3) init_kernel_tile(InitArgs a) 
 #ifdef CQG_INIT_TIMING
             if (threadIdx.x == 0 && k < 1024) g_tile_rounds[k][1] += clock64() - _l0;
 #endif
-            if (threadIdx.x == 0) a.result[2] = v;
+            // The release word carries the picked colour (round << 32 | colour): a released block
+            // needs nothing else, so it reads neither the pick nor the colour array. Every block has
+            // its own word (no single hot L2 line); the words are relaxed stores (the data travels
+            // in the word itself; the md / segment updates of the round were ordered by the arrivals).
+            if (threadIdx.x == 0) s_rel = ((unsigned long long)k << 32) | __ldg(a.colors + v);
             __syncthreads();
-            // release every block through its own word (no single hot L2 line):
-            // one gpu-scope fence per thread (cumulative over the pick, which
-            // the block barrier ordered before it), then relaxed stores -- a
-            // st.release per word would fence once per store
-            __threadfence();
+            const unsigned long long rel = s_rel;
             for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x)
-                st_relaxed_u64(a.tflags + (size_t)b * kFlagStride, (unsigned long long)k);
-            __syncthreads(); // block 0's own threads read the pick below
+                st_relaxed_u64(a.tflags + (size_t)b * kFlagStride, rel);
             GTIME(2);
         } else {
-            if (threadIdx.x == 0)
-                while (ld_acquire_u64(flag) < (unsigned long long)k) __nanosleep(64);
+            if (threadIdx.x == 0) {
+                unsigned long long w;
+                while (((w = ld_acquire_u64(flag)) >> 32) < (unsigned long long)k) __nanosleep(64);
+                s_rel = w;
+            }
             __syncthreads();
             GTIME(3);
         }
-        const uint64_t pick = *reinterpret_cast<volatile unsigned long long *>(a.result + 2);
-        __syncthreads(); // every thread has the pick before block 0 can overwrite it next round
-        clast = __ldg(a.colors + pick);
+        clast = (uint32_t)s_rel;
+        __syncthreads(); // every thread has the colour before thread 0 rewrites s_rel next round
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             a.cen[3 * k] = (double)((clast >> 16) & 255u);
             a.cen[3 * k + 1] = (double)((clast >> 8) & 255u);
