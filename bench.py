@@ -391,8 +391,24 @@ def sharded_measure(args, cfg, env, steps, warmup):
     h_idx = torch.empty(max(Pr, 1), dtype=torch.int32).pin_memory()
     h_q = torch.empty((max(Pr, 1), 3), dtype=torch.uint8).pin_memory()
     e_ms = timed(lambda: step(h_img, h_idx, h_q), steps)
+    # roofline of this rank's Lloyd kernel: the dense sweep over its colour shard, back-to-back launches
+    # on the final state (cqg_bench_sweep, CUDA events), against the FP32 peak of one GPU
+    roofline = None
+    try:
+        iso_ms, iso_units = ctx.bench_sweep(20)
+        peaks, peak_kind = measured_peaks()
+        sms = torch.cuda.get_device_properties(local).multi_processor_count
+        fp32_peak = sms * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+        ach = 8.0 * iso_units / (iso_ms / 1e3) / 1e12
+        roofline = {"bound": "fp32", "kernel": "sweep_kernel<WALK> on rank 0's colour shard (dense launch)",
+                    "achieved": ach, "peak": fp32_peak, "unit": "TFLOP/s", "frac": ach / fp32_peak,
+                    "traffic": None, "avg_launch_ms": iso_ms, "units_per_launch": iso_units,
+                    "peak_source": f"{sms} SMs x 128 FP32 lanes x 2 x sm_max_mhz ({peak_kind} MEASURED_PEAKS.json)"}
+    except Exception as e:  # the shard engine kept no sweep state
+        roofline = {"unavailable": str(e)[:200]}
     ctx.close()
     return {
+        "roofline": roofline,
         "workload": cfg.name, "value": P / (ms / 1e3) / 1e6, "unit": UNIT, "n_gpus": world, "steps": steps,
         "ms_per_step": ms, "scaling": "strong",
         "parallelism": (f"unique colours sharded over {world} ranks (int64 moment allreduce per iteration); "
@@ -412,20 +428,37 @@ def run_sharded_line(args, cfg, env):
     if env["world"] == 1:
         backend = "gloo" if env["share"] else "nccl"
         kw = {} if env["share"] else {"device_id": torch.device("cuda", env["local"])}
-        dist.init_process_group(backend, rank=0, world_size=1, init_method="tcp://127.0.0.1:29533", **kw)
+        with stdout_to_stderr():
+            dist.init_process_group(backend, rank=0, world_size=1, init_method="tcp://127.0.0.1:29533", **kw)
+            dist.barrier()
     res = sharded_measure(args, cfg, env, args.steps, args.warmup)
     if env["rank"] == 0:
         line = {"metric": METRIC, "higher_is_better": True, "warmup": args.warmup, "vs_baseline": None,
                 "dtype": "f32", "data": "synthetic",
                 "config": {"workload": cfg.name, "image": f"{cfg.width}x{cfg.height}", "k": cfg.k, "init": cfg.init,
                            "parallelism": res.pop("parallelism"), "l2": "flushed (512 MiB write) between timed steps"},
-                "roofline": None, "cpu_baseline": None, **res}
+                "cpu_baseline": None, **res}
         print(json.dumps(line))
     dist.destroy_process_group()
     return 0
 
 
 HOSTPOOL = ThreadPoolExecutor(4)  # parity digests and 1-core CPU baselines, overlapped with device work
+
+
+class stdout_to_stderr:
+    """Rank 0's stdout carries the JSON line only: NCCL prints its "NCCL version ..." banner on stdout when
+    the first communicator is created, so file descriptor 1 points at stderr while that happens."""
+
+    def __enter__(self):
+        sys.stdout.flush()
+        self.saved = os.dup(1)
+        os.dup2(2, 1)
+
+    def __exit__(self, *exc):
+        sys.stdout.flush()
+        os.dup2(self.saved, 1)
+        os.close(self.saved)
 
 
 def setup_env(args):
@@ -441,10 +474,12 @@ def setup_env(args):
         local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        if share:
-            dist.init_process_group("gloo")
-        else:
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        with stdout_to_stderr():
+            if share:
+                dist.init_process_group("gloo")
+            else:
+                dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+                dist.barrier()  # the communicator exists (and has said so) before anything is printed
     return {"world": world, "rank": rank, "local": local, "share": share,
             "dev": torch.device("cuda", local), "stream": torch.cuda.current_stream()}
 
