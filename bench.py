@@ -581,7 +581,7 @@ def run_ours(args, cfg):
         line["parity"] = resolve(line["parity"])
         out = {}
         for name, res in by_config.items():
-            if "roofline" in res:
+            if "byte_kernels" in res:  # a measure() line (the sharded result is reported as it is)
                 res["parity"] = resolve(res["parity"])
                 out[name] = summarize(res, resolve(cpu_jobs.get(name)))
             else:
