@@ -61,6 +61,13 @@ UNIT = "MPixel/s"
 BATCH_DEFAULT = 16  # copies of a small image per step (both arms)
 
 
+def config_dict(cfg, images_per_step):
+    """The workload both arms print as `config` (the same dictionary on the GPU and the reference arm)."""
+    return {"workload": cfg.name, "image": f"{cfg.width}x{cfg.height}", "images_per_step": int(images_per_step),
+            "k": cfg.k if not cfg.k_cycle else list(cfg.k_cycle), "init": cfg.init,
+            "fixed_iterations": cfg.fixed_iterations or None}
+
+
 def env_int(name, default):
     try:
         return int(os.environ.get(name, default))
@@ -216,9 +223,7 @@ def run_reference(args, cfg):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": step * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg.name, "image": f"{cfg.width}x{cfg.height}", "images_per_step": per_batch,
-                   "k": cfg.k if not cfg.k_cycle else list(cfg.k_cycle), "init": cfg.init,
-                   "fixed_iterations": cfg.fixed_iterations or None},
+        "config": config_dict(cfg, per_batch),
         "run": {"note": "reference sources compiled -O3 -DNDEBUG (oracle/Makefile), one image per host thread",
                 "host_threads": threads, "batches_side_by_side": nimg // per_batch},
         "lloyd_distances_per_s": dist / lloyd_s * min(threads, nimg) if lloyd_s > 0 else None,
@@ -909,10 +914,7 @@ def measure(args, cfg, env, steps, warmup, e2e_on=True, parity_on=True, batch=1)
             "warmup": warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak" if cfg.images == 1 else "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
-            "config": {"workload": cfg.name, "image": f"{cfg.width}x{cfg.height}",
-                       "images_per_step": len(imgs) if cfg.images == 1 else cfg.images,
-                       "k": cfg.k if not cfg.k_cycle else list(cfg.k_cycle),
-                       "init": cfg.init, "fixed_iterations": cfg.fixed_iterations or None},
+            "config": config_dict(cfg, len(imgs) if cfg.images == 1 else cfg.images),
             "run": {"images_per_rank": len(imgs),
                     "parallelism": ((f"replicas x{world}" if cfg.images == 1 else f"images sharded over {world}") +
                                     (f"; {nworkers} concurrent library contexts per GPU, {budget_label}"
