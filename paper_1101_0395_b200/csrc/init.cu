@@ -474,6 +474,8 @@ constexpr int kRecBatch = 16; // records in flight per lane (32 doubles the regi
 __device__ unsigned long long g_coop_timing[8]; // [5] tiles updated, [6] points changed, [7] slowest block's update
 __device__ unsigned long long g_tile_round_max;
 __device__ unsigned long long g_tile_rounds[1024][2]; // per round: slowest block update, block 0 locate
+__device__ unsigned long long g_warp_hist[16][2];    // per warp-round of update_tiles by reached tiles: cycles, count
+__device__ int g_warp_hist_on;                       // set by block 0 from round 32 on (steady state)
 __device__ unsigned long long g_loc_phase[4];
 #define GTIME(slot)                                                                  \
     do {                                                                             \
@@ -905,6 +907,10 @@ __device__ unsigned long long update_tiles(const InitArgs &a, bool full, uint32_
     const uint64_t W = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     const uint32_t bb = __dp4a(clast, clast, 0u);
     unsigned long long best = 0;
+#ifdef CQG_INIT_TIMING
+    const unsigned long long _w0 = clock64();
+    int _wn = 0;
+#endif
     for (uint64_t j0 = 0; gw + j0 * W < a.ntiles; j0 += 32) {
         const uint64_t t = gw + (j0 + lane) * W;
         // branch-free metadata loads (clamped tile index, masked result)
@@ -916,6 +922,9 @@ __device__ unsigned long long update_tiles(const InitArgs &a, bool full, uint32_
         const bool need = tin && (full || box_d2(bx, clast) < tm);
         if (tin && !need) best = max(best, tk);
         unsigned m = __ballot_sync(0xffffffffu, need);
+#ifdef CQG_INIT_TIMING
+        _wn += __popc(m);
+#endif
         while (m) {
             const int l = __ffs(m) - 1;
             m &= m - 1;
@@ -978,6 +987,13 @@ __device__ unsigned long long update_tiles(const InitArgs &a, bool full, uint32_
             best = max(best, kb);
         }
     }
+#ifdef CQG_INIT_TIMING
+    if (!full && lane == 0 && *(volatile int *)&g_warp_hist_on) {
+        const int b_ = _wn < 15 ? _wn : 15;
+        atomicAdd(&g_warp_hist[b_][0], clock64() - _w0);
+        atomicAdd(&g_warp_hist[b_][1], 1ull);
+    }
+#endif
     for (int o = 16; o; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
     return best;
 }
@@ -1237,6 +1253,9 @@ __global__ void __launch_bounds__(kInitThreads, 3) init_kernel_tile(InitArgs a) 
         __shared__ unsigned long long s_pickm;
         const unsigned G32 = gridDim.x;
         for (int k = 1; k < a.K; ++k) {
+#ifdef CQG_INIT_TIMING
+            if (blockIdx.x == 0 && threadIdx.x == 0) g_warp_hist_on = k >= 32;
+#endif
             const unsigned long long wb = update_tiles<M>(a, k == 1, clast);
             if ((threadIdx.x & 31) == 0) s_m[threadIdx.x >> 5] = wb;
             __syncthreads();
@@ -1281,6 +1300,9 @@ __global__ void __launch_bounds__(kInitThreads, 3) init_kernel_tile(InitArgs a) 
     for (int k = 1; k < a.K; ++k) {
         GTIME(4);
         if (k == 1) tile_first_sums<M>(a, clast);
+#ifdef CQG_INIT_TIMING
+        if (blockIdx.x == 0 && threadIdx.x == 0) g_warp_hist_on = k >= 32;
+#endif
 #ifdef CQG_INIT_TIMING
         const unsigned long long _u0 = clock64();
 #endif
@@ -2057,6 +2079,17 @@ extern "C" int cqg_dbg_init_timing(unsigned long long *out, int reset) {
     if (reset) {
         unsigned long long z[8] = {};
         cudaMemcpyToSymbol(cqg::g_init_timing, z, sizeof(z));
+    }
+    return 0;
+}
+#endif
+
+#ifdef CQG_INIT_TIMING
+extern "C" int cqg_dbg_warp_hist(unsigned long long *out, int reset) {
+    if (cudaMemcpyFromSymbol(out, cqg::g_warp_hist, sizeof(cqg::g_warp_hist)) != cudaSuccess) return 1;
+    if (reset) {
+        unsigned long long z[32] = {};
+        cudaMemcpyToSymbol(cqg::g_warp_hist, z, sizeof(z));
     }
     return 0;
 }
