@@ -898,7 +898,7 @@ __device__ __forceinline__ void atomic_sub_mass(u128 *p, u128 v) {
 // lane). k-means++: changed points subtract their exact mass drop from their
 // histogram segment and part sums. Maximin: returns the warp's largest
 // (md, ~index) over all its tiles.
-template <class M>
+template <class M, bool PAIR>
 __device__ unsigned long long update_tiles(const InitArgs &a, bool full, uint32_t clast) {
     typedef typename M::T T;
     T *segs = reinterpret_cast<T *>(a.segs);
@@ -925,33 +925,35 @@ __device__ unsigned long long update_tiles(const InitArgs &a, bool full, uint32_
 #ifdef CQG_INIT_TIMING
         _wn += __popc(m);
 #endif
-        while (m) {
-            const int l = __ffs(m) - 1;
-            m &= m - 1;
-            const uint64_t tt = gw + (j0 + l) * W;
+        // the reached tiles of this warp; k-means++ (PAIR) takes them two at a time, both tiles' loads in
+        // flight before either is updated: a tile costs a DRAM round trip and a round waits for the warp
+        // with the most tiles (cfg5 init stage 5.23 -> 5.06 ms). Maximin tiles are cheap and its kernel
+        // keeps the smaller register budget (pairing them measured slower: cfg3 1.59 -> 1.73 ms).
+        constexpr int TP = kTile / 32;
+        auto load_tile = [&](uint64_t tt, uint2 *r, uint32_t *cn, uint32_t *hx) {
             // every load of the tile issued at once (clamped indices: the
             // last tile's padding lanes re-read point n-1 and are masked)
-            uint2 r[kTile / 32];
-            uint32_t cn[kTile / 32], hx[kTile / 32];
 #pragma unroll
-            for (int u = 0; u < kTile / 32; ++u) {
+            for (int u = 0; u < TP; ++u) {
                 const uint64_t p = tt * kTile + u * 32 + lane;
                 const uint64_t pc = p < a.n ? p : a.n - 1;
                 r[u] = make_uint2(__ldg(a.tcol + pc), a.tmd[pc]);
                 cn[u] = (a.kind == 1 && !full) ? __ldg(a.tcnt + pc) : 0u;
                 hx[u] = (a.kind == 0 || !full) ? __ldg(a.tidx + pc) : 0u;
             }
+        };
+        auto update_tile = [&](uint64_t tt, uint2 *r, const uint32_t *cn, const uint32_t *hx) {
             uint32_t mx = 0;
             unsigned long long kb = 0;
-            uint32_t dn[kTile / 32], chg = 0;
+            uint32_t dn[TP], chg = 0;
 #pragma unroll
-            for (int u = 0; u < kTile / 32; ++u) {
+            for (int u = 0; u < TP; ++u) {
                 const uint64_t p = tt * kTile + u * 32 + lane;
                 dn[u] = d2_int_bb(r[u].x, clast, bb);
                 if (p < a.n && dn[u] < r[u].y) chg |= 1u << u; // first round: md = 0xFFFFFFFF
             }
 #pragma unroll
-            for (int u = 0; u < kTile / 32; ++u) {
+            for (int u = 0; u < TP; ++u) {
                 const uint64_t p = tt * kTile + u * 32 + lane;
                 if ((chg >> u) & 1u) {
                     a.tmd[p] = dn[u];
@@ -985,6 +987,80 @@ __device__ unsigned long long update_tiles(const InitArgs &a, bool full, uint32_
             }
 #endif
             best = max(best, kb);
+        };
+        while (m) {
+            const int l0 = __ffs(m) - 1;
+            m &= m - 1;
+            if constexpr (!PAIR) {
+                const uint64_t tt = gw + (j0 + l0) * W;
+                // every load of the tile issued at once (clamped indices: the
+                // last tile's padding lanes re-read point n-1 and are masked)
+                uint2 r[kTile / 32];
+                uint32_t cn[kTile / 32], hx[kTile / 32];
+    #pragma unroll
+                for (int u = 0; u < kTile / 32; ++u) {
+                    const uint64_t p = tt * kTile + u * 32 + lane;
+                    const uint64_t pc = p < a.n ? p : a.n - 1;
+                    r[u] = make_uint2(__ldg(a.tcol + pc), a.tmd[pc]);
+                    cn[u] = (a.kind == 1 && !full) ? __ldg(a.tcnt + pc) : 0u;
+                    hx[u] = (a.kind == 0 || !full) ? __ldg(a.tidx + pc) : 0u;
+                }
+                uint32_t mx = 0;
+                unsigned long long kb = 0;
+                uint32_t dn[kTile / 32], chg = 0;
+    #pragma unroll
+                for (int u = 0; u < kTile / 32; ++u) {
+                    const uint64_t p = tt * kTile + u * 32 + lane;
+                    dn[u] = d2_int_bb(r[u].x, clast, bb);
+                    if (p < a.n && dn[u] < r[u].y) chg |= 1u << u; // first round: md = 0xFFFFFFFF
+                }
+    #pragma unroll
+                for (int u = 0; u < kTile / 32; ++u) {
+                    const uint64_t p = tt * kTile + u * 32 + lane;
+                    if ((chg >> u) & 1u) {
+                        a.tmd[p] = dn[u];
+                        if (a.kind == 1 && !full) {
+                            const T dm = M::mass_c(a, cn[u], r[u].y) - M::mass_c(a, cn[u], dn[u]);
+                            if (dm != (T)0) atomic_sub_mass(segs + hx[u] / kSeg, dm);
+                        }
+                        r[u].y = dn[u];
+                    }
+                    if (p < a.n) {
+                        mx = max(mx, r[u].y);
+                        if (a.kind == 0) kb = max(kb, ((unsigned long long)r[u].y << 32) | (uint32_t)~hx[u]);
+                    }
+                }
+                for (int o = 16; o; o >>= 1) {
+                    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                    kb = max(kb, __shfl_xor_sync(0xffffffffu, kb, o));
+                }
+                if (lane == 0) {
+                    a.tmax[tt] = mx;
+                    if (a.kind == 0) a.tkey[tt] = kb;
+                }
+    #ifdef CQG_INIT_TIMING
+                {
+                    unsigned nc = __popc(chg);
+                    for (int o = 16; o; o >>= 1) nc += __shfl_xor_sync(0xffffffffu, nc, o);
+                    if (lane == 0) {
+                        atomicAdd(&g_coop_timing[5], 1ull);
+                        atomicAdd(&g_coop_timing[6], (unsigned long long)nc);
+                    }
+                }
+    #endif
+                best = max(best, kb);
+            } else {
+                const bool two = m != 0;
+                const int l1 = two ? __ffs(m) - 1 : l0;
+                if (two) m &= m - 1;
+                const uint64_t t0 = gw + (j0 + l0) * W, t1 = gw + (j0 + l1) * W;
+                uint2 r0[TP], r1[TP];
+                uint32_t cn0[TP], hx0[TP], cn1[TP], hx1[TP];
+                load_tile(t0, r0, cn0, hx0);
+                if (two) load_tile(t1, r1, cn1, hx1);
+                update_tile(t0, r0, cn0, hx0);
+                if (two) update_tile(t1, r1, cn1, hx1);
+            }
         }
     }
 #ifdef CQG_INIT_TIMING
@@ -1219,8 +1295,8 @@ __device__ uint64_t locate_one_block(const InitArgs &a, double nu, const uint32_
     return idx;
 }
 
-template <class M>
-__global__ void __launch_bounds__(kInitThreads, 3) init_kernel_tile(InitArgs a) {
+template <class M, int KIND>
+__global__ void __launch_bounds__(kInitThreads, KIND == 1 ? 2 : 3) init_kernel_tile(InitArgs a) {
     cg::grid_group grid = cg::this_grid();
     __shared__ typename M::T s_w[kInitThreads / 32];
     __shared__ unsigned long long s_m[kInitThreads / 32];
@@ -1245,7 +1321,7 @@ __global__ void __launch_bounds__(kInitThreads, 3) init_kernel_tile(InitArgs a) 
         a.cen[1] = (double)((clast >> 8) & 255u);
         a.cen[2] = (double)(clast & 255u);
     }
-    if (a.kind == 0) {
+    if (KIND == 0 && a.kind == 0) { // (the KIND 0 kernel keeps both loops: compiled alone, the maximin loop ran 3% slower)
         // Maximin has no draw to locate: one grid barrier per round, and every block reduces the
         // block maxima itself (ping-ponged by round parity, read past L1), instead of the arrival
         // counter -> block 0 -> release flags hand-off the k-means++ rounds need (cfg3 init stage
@@ -1256,7 +1332,7 @@ __global__ void __launch_bounds__(kInitThreads, 3) init_kernel_tile(InitArgs a) 
 #ifdef CQG_INIT_TIMING
             if (blockIdx.x == 0 && threadIdx.x == 0) g_warp_hist_on = k >= 32;
 #endif
-            const unsigned long long wb = update_tiles<M>(a, k == 1, clast);
+            const unsigned long long wb = update_tiles<M, false>(a, k == 1, clast);
             if ((threadIdx.x & 31) == 0) s_m[threadIdx.x >> 5] = wb;
             __syncthreads();
             unsigned long long *mp = a.mparts + (size_t)(k & 1) * G32;
@@ -1306,7 +1382,7 @@ __global__ void __launch_bounds__(kInitThreads, 3) init_kernel_tile(InitArgs a) 
 #ifdef CQG_INIT_TIMING
         const unsigned long long _u0 = clock64();
 #endif
-        update_tiles<M>(a, k == 1, clast);
+        update_tiles<M, KIND == 1>(a, k == 1, clast);
         __syncthreads();
 #ifdef CQG_INIT_TIMING
         if (threadIdx.x == 0) atomicMax(&g_tile_round_max, clock64() - _u0);
@@ -1964,7 +2040,8 @@ void run_init(cqg_ctx *ctx, const uint32_t *colors_d, const uint32_t *counts_d, 
         CQG_CUDA(cudaStreamSynchronize(s));
         tile = *dup_h == 0;
     }
-    const void *kern = tile ? (exact ? (const void *)init_kernel_tile<ExactMass> : (const void *)init_kernel_tile<FixedMass>)
+    const void *kern = tile ? (kind == 1 ? (exact ? (const void *)init_kernel_tile<ExactMass, 1> : (const void *)init_kernel_tile<FixedMass, 1>)
+                                         : (exact ? (const void *)init_kernel_tile<ExactMass, 0> : (const void *)init_kernel_tile<FixedMass, 0>))
                             : (exact ? (const void *)init_kernel_rec<ExactMass> : (const void *)init_kernel_rec<FixedMass>);
     int occ = 0;
     CQG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kInitThreads, 0));
